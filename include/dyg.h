@@ -1,0 +1,241 @@
+/*
+ * dyg.h -- C-ABI of the B200-native dyGRASS batched update path.
+ *
+ * The reference (/root/reference/proj) has no C API or FFI; its seams are two
+ * C++ interfaces:
+ *   (1) run_batch(const DynamicGraph&, span<const WalkQuery>, const WalkConfig&)
+ *       -- proj/src/walk.hpp:86-92, a pure function of the graph snapshot;
+ *   (2) SparsifierState -- proj/src/sparsifier.hpp:71-112: ctor(G, H, options),
+ *       graph(), sparsifier(), update_counter(), apply_insertion(),
+ *       apply_deletion(), last_event_steps(), replay_batch(stream, b),
+ *       replay(stream).
+ * Each entry point below names the reference interface it replaces. Plain
+ * pointers and sizes only; no exceptions cross the boundary. Return codes are
+ * the reference's ErrorKind values (proj/src/error.hpp:8-9: "values match ...
+ * the C API status codes"): 0 ok, 1 Usage, 2 Data, 3 Numeric, plus 4 for a
+ * CUDA/device failure. dyg_last_error() holds the message (thread-local).
+ *
+ * Ownership: the caller owns every host buffer passed in or out; a session
+ * owns its device memory. One session = one writer thread (sparsifier.hpp:
+ * 67-70). All calls are stream-ordered on the session's CUDA stream and
+ * synchronous on return unless stated otherwise.
+ *
+ * Struct layouts are part of the ABI (tests share numpy dtypes with them).
+ */
+#ifndef DYG_H
+#define DYG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define DYG_OK 0
+#define DYG_ERR_USAGE 1   /* ErrorKind::Usage   (error.hpp:9) */
+#define DYG_ERR_DATA 2    /* ErrorKind::Data    */
+#define DYG_ERR_NUMERIC 3 /* ErrorKind::Numeric */
+#define DYG_ERR_DEVICE 4  /* CUDA error or missing device (no reference analogue) */
+
+/* Graph rows in reference row order: row u is DynamicGraph::neighbors(u)
+ * (graph.hpp:37-38), flattened. row_ptr has n+1 entries; ids/w have
+ * row_ptr[n] = 2|E| entries. Every edge appears in both endpoint rows with
+ * bit-identical weights. */
+typedef struct dyg_csr {
+  uint32_t n;
+  uint32_t pad;
+  const uint64_t* row_ptr;
+  const uint32_t* ids;
+  const double* w;
+} dyg_csr;
+
+/* WalkConfig (walk.hpp:13-18). */
+typedef struct dyg_walk_config {
+  double distortion_threshold; /* K; 0 = no-filter baseline (sparsifier.hpp:32-33) */
+  uint32_t step_cap;           /* T */
+  uint32_t walker_count;       /* s */
+  uint64_t global_seed;
+} dyg_walk_config;
+
+/* SparsifierOptions (sparsifier.hpp:25-34). */
+typedef struct dyg_options {
+  dyg_walk_config walk;
+  int32_t batched;           /* deferred (batched) replay; 0 = immediate */
+  int32_t freeze_sparsifier; /* drift baseline */
+} dyg_options;
+
+/* EdgeEvent (stream.hpp:11-18). kind: 0 insertion, 1 deletion. */
+typedef struct dyg_event {
+  uint32_t kind;
+  uint32_t u;
+  uint32_t v;
+  uint32_t batch_index;
+  double weight; /* insertions only */
+} dyg_event;
+
+/* WalkQuery (walk.hpp:71-78). kind: 0 Reach, 1 MinPath. */
+typedef struct dyg_walk_query {
+  uint32_t kind;
+  uint32_t p;
+  uint32_t q;
+  uint32_t pad;
+  double w_pq; /* Reach only */
+  uint64_t update_id;
+} dyg_walk_query;
+
+/* WalkResult (walk.hpp:80-84) flattened: Reach -> reached, best_estimate;
+ * MinPath -> reached (= path found), path_len, resistance and the loop-erased
+ * vertices in path_buf[i*(T+1) ...]. */
+typedef struct dyg_walk_result {
+  uint32_t reached;
+  uint32_t path_len;
+  double best_estimate;
+  uint64_t steps_used;
+  double resistance;
+} dyg_walk_result;
+
+/* BatchReport (sparsifier.hpp:44-59). wall_ms is device time of the batch
+ * (CUDA events) plus host staging. */
+typedef struct dyg_batch_report {
+  uint32_t batch_index;
+  uint32_t pad;
+  uint64_t insertions_seen;
+  uint64_t insertions_kept;
+  uint64_t insertions_pruned;
+  uint64_t deletions_seen;
+  uint64_t deletions_in_sparsifier;
+  uint64_t paths_recovered;
+  uint64_t edges_recovered;
+  uint64_t fallback_activations;
+  uint64_t walker_steps;
+  uint64_t max_event_steps;
+  double wall_ms;
+  double density_graph;
+  double density_sparsifier;
+} dyg_batch_report;
+
+/* Per-session counters (no reference analogue; SURVEY.md 5 "metrics"). */
+typedef struct dyg_stats {
+  uint64_t batches;
+  uint64_t kernel_launches;     /* kernels this library launched */
+  uint64_t reach_queries;
+  uint64_t minpath_queries;
+  uint64_t reach_steps;         /* walker steps on H (== sum of steps_used) */
+  uint64_t minpath_steps;       /* walker steps on shadow G */
+  uint64_t reach_row_bytes;     /* sum over steps of 32*ceil((8+12*deg)/32) */
+  uint64_t minpath_row_bytes;
+  double reach_ms;              /* device time of the reach-walk kernel(s) */
+  double minpath_ms;            /* device time of the min-path walk + winner kernels */
+  double commit_ms;             /* device time of the commit engine */
+  double total_ms;              /* device time of whole batches */
+  uint64_t commit_rounds;       /* dependency rounds used by the commit engine */
+  uint64_t pool_used;           /* overflow-pool entries in use (G + H) */
+  uint64_t pool_capacity;
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+} dyg_stats;
+
+typedef struct dyg_session dyg_session;
+
+/* Thread-local message for the last non-zero return on this thread. */
+const char* dyg_last_error(void);
+/* Library build string (arch, flags). */
+const char* dyg_version(void);
+/* Number of visible CUDA devices (0 when none). */
+int dyg_device_count(void);
+
+/* SparsifierState::SparsifierState(G, H, options) (sparsifier.cpp:183-203):
+ * validates shapes and H subset of G, uploads both graphs to `device` as
+ * device-resident dynamic rows. */
+int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* options,
+                       int device, dyg_session** out);
+void dyg_session_destroy(dyg_session* s);
+
+/* SparsifierState::replay_batch(stream, b) (sparsifier.cpp:541-548): the
+ * stream is `events[0..n_events)` with `batch_count` (UpdateStream,
+ * stream.hpp:20-23); events of batch b are found by scanning, as the
+ * reference does (sparsifier.cpp:401-404). Deferred or immediate mode per
+ * options.batched. */
+int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
+                     uint32_t batch_count, uint32_t batch_index, dyg_batch_report* out);
+
+/* The same for a batch already extracted by the caller: `events` are the
+ * batch's events in stream order and `positions` their stream indices (used
+ * in error messages; NULL means 0..n-1). */
+int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* positions,
+                      size_t n, uint32_t batch_index, dyg_batch_report* out);
+
+/* Device-resident stream: upload once, then replay batches with no per-batch
+ * host->device traffic (used for the kernel-level benchmark). */
+int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
+                      uint32_t batch_count);
+int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* out);
+
+/* SparsifierState::apply_insertion / apply_deletion (sparsifier.cpp:243-317).
+ * decision: 0 Kept, 1 Pruned (InsertionDecision). kind: 0 GraphOnly,
+ * 1 PathRecovered, 2 LocalFallback (DeletionOutcome::Kind). */
+int dyg_apply_insertion(dyg_session* s, uint32_t u, uint32_t v, double w, int* decision);
+int dyg_apply_deletion(dyg_session* s, uint32_t u, uint32_t v, int* kind,
+                       uint32_t* edges_added);
+/* SparsifierState::last_event_steps (sparsifier.hpp:92-93). */
+uint64_t dyg_last_event_steps(const dyg_session* s);
+/* SparsifierState::update_counter (sparsifier.hpp:79). */
+uint64_t dyg_update_counter(const dyg_session* s);
+
+/* graph() / sparsifier() accessors (sparsifier.hpp:76-77). which: 0 = G,
+ * 1 = H. Counters, then a row-order export: row_ptr[n+1], ids/w sized by
+ * *entries (= 2|E|). */
+int dyg_graph_info(const dyg_session* s, int which, uint32_t* n, uint64_t* edges,
+                   double* density);
+int dyg_export_rows(dyg_session* s, int which, uint64_t* row_ptr, uint32_t* ids, double* w,
+                    uint64_t capacity);
+
+/* Device-side snapshot of (G, H, update_counter) and its restore: resume /
+ * parity bisection (SURVEY.md 5 checkpoint row) and benchmark resets. */
+int dyg_session_snapshot(dyg_session* s);
+int dyg_session_restore(dyg_session* s);
+
+int dyg_session_stats(const dyg_session* s, dyg_stats* out);
+int dyg_session_reset_stats(dyg_session* s);
+
+/* Stateless twin of run_batch (walk.hpp:86-92): uploads g, runs the queries
+ * on `device`, returns results in query order. path_buf (nullable) receives
+ * MinPath vertices at [i*(T+1)]. */
+int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_queries,
+                  const dyg_walk_config* cfg, dyg_walk_result* out, uint32_t* path_buf,
+                  int device);
+
+/* ---- multi-GPU split of replay_batch -------------------
+ * Every rank holds a replica of (G, H). For batch b every rank calls
+ * dyg_shard_walk(rank, world), which runs the walk phase for the contiguous
+ * query range [floor(nq*rank/world), floor(nq*(rank+1)/world)) and writes a
+ * fixed-size record per query slot into `records` (device pointer,
+ * dyg_shard_record_bytes() bytes per slot, `slots` slots = ceil(nq/world) on
+ * every rank, unused slots zeroed). The caller all-gathers the records
+ * (NCCL over NVLink) into `gathered` (world*slots slots, rank-major) and
+ * calls dyg_shard_commit, which applies the identical deterministic commit on
+ * every replica. dyg_shard_begin returns the query counts so the caller can
+ * size buffers. The session stream may be replaced by the caller's
+ * (dyg_set_stream) so the collective is stream-ordered with the kernels. */
+int dyg_set_stream(dyg_session* s, void* cuda_stream);
+int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* positions,
+                    size_t n, uint32_t batch_index, uint64_t* n_reach, uint64_t* n_minpath);
+size_t dyg_shard_record_bytes(const dyg_session* s, int minpath);
+int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
+                   void* minpath_records);
+int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
+                     const void* minpath_gathered, dyg_batch_report* out);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYG_H */

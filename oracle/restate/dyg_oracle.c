@@ -307,9 +307,12 @@ void* orc_make_random_connected(uint32_t n, uint32_t extra, uint64_t seed, doubl
   rng_t rng = {hash_mix(seed + 0x57A77ull)};
 #define WEIGHT() (w_min + rng_next_double(&rng) * (w_max - w_min))
   const uint32_t core = with_pendant ? n - 1 : n;
+  /* generators.hpp:46 passes rng.next_below(v) and weight() as arguments of
+   * one call; GCC evaluates them right to left, so the weight is drawn first. */
   for (uint32_t v = 1; v < core; ++v) {
+    const double w = WEIGHT();
     uint32_t to = (uint32_t)rng_next_below(&rng, v);
-    g_insert(g, v, to, WEIGHT());
+    g_insert(g, v, to, w);
   }
   uint32_t added = 0, attempts = 0;
   while (added < extra && attempts < 100 * extra + 100) {
@@ -321,8 +324,9 @@ void* orc_make_random_connected(uint32_t n, uint32_t extra, uint64_t seed, doubl
     ++added;
   }
   if (with_pendant) {
+    const double w = WEIGHT(); /* same right-to-left order (generators.hpp:58) */
     uint32_t to = (uint32_t)rng_next_below(&rng, core);
-    g_insert(g, n - 1, to, WEIGHT());
+    g_insert(g, n - 1, to, w);
   }
 #undef WEIGHT
   return g;

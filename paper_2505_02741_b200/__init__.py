@@ -1,0 +1,31 @@
+"""B200-native dyGRASS batched incremental / decremental sparsifier update.
+
+The device path (libdyg.so: hand-written sm_100a CUDA behind the C-ABI in
+include/dyg.h) is the product; this package is the host-side mirror of the
+reference's interface (see api.py). There is no CPU fallback.
+"""
+from .api import (  # noqa: F401
+    BatchReport,
+    DeletionOutcome,
+    DynamicGraph,
+    Error,
+    ErrorKind,
+    InsertionDecision,
+    SparsifierOptions,
+    SparsifierState,
+    StreamGenOptions,
+    UpdateReport,
+    UpdateStream,
+    WalkConfig,
+    build_initial_sparsifier,
+    device_count,
+    generate_update_stream,
+    load_matrix_market,
+    load_update_stream,
+    make_grid4,
+    make_mesh,
+    make_random_connected,
+    run_batch,
+    save_matrix_market,
+    save_update_stream,
+)

@@ -1,0 +1,529 @@
+// batch.cu -- validation, walk shadow, query build and the commit engine of
+// one deferred batch. See batch.cuh for the kernel map and the dependency
+// round scheme.
+#include <cooperative_groups.h>
+
+#include <cub/cub.cuh>
+
+#include "batch.cuh"
+#include "graph_store.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dyg {
+
+namespace {
+
+__device__ __forceinline__ bool batch_aborted(const BatchCtl* ctl) {
+  return *reinterpret_cast<const volatile unsigned long long*>(&ctl->val_err) != ~0ull;
+}
+
+// sparsifier.cpp:321-337 validate_event_shape; the lowest failing event
+// wins (the reference validates in stream order before walking).
+__global__ void k_validate(const DevEvent* __restrict__ ev, uint32_t nb, uint32_t n,
+                           BatchCtl* ctl) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  const DevEvent e = ev[k];
+  uint32_t code = 0;
+  if (e.u >= n || e.v >= n) {
+    code = kErrRange;
+  } else if (e.u == e.v) {
+    code = kErrSelfLoop;
+  } else if (e.kind == 0 && (!(e.weight > 0.0) || !isfinite(e.weight))) {
+    code = kErrWeight;
+  }
+  if (code) atomicMin(&ctl->val_err, (static_cast<unsigned long long>(k) << 8) | code);
+}
+
+// The round engine. Op provides for_rows(k, f) (every row event k reads or
+// writes, possibly with repeats) and apply(k) -> error code.
+template <class Op>
+__global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
+  const uint32_t nth = static_cast<uint32_t>(grid.size());
+  volatile BatchCtl* ctl = b.ctl;
+  if (ctl->val_err != ~0ull) return;  // uniform: nothing below ran yet
+  unsigned long long round = *b.round_ctr;
+  uint32_t r = 0;
+  for (;; ++r) {
+    ++round;
+    const uint32_t lim = op.limit();
+    if (tid == 0) ctl->remaining[(r + 1) % 3] = 0;
+    for (uint32_t k = tid; k < nev; k += nth) {
+      if (k >= lim || b.state[k] != 0) continue;
+      const unsigned long long key = (round << 32) | (0xFFFFFFFFull - k);
+      op.for_rows(k, [&](uint32_t row) { atomicMax(b.locks + row, key); });
+    }
+    grid.sync();
+    for (uint32_t k = tid; k < nev; k += nth) {
+      if (k >= lim || b.state[k] != 0) continue;
+      const unsigned long long key = (round << 32) | (0xFFFFFFFFull - k);
+      bool ready = true;
+      op.for_rows(k, [&](uint32_t row) {
+        if (ready && *reinterpret_cast<volatile unsigned long long*>(b.locks + row) != key)
+          ready = false;
+      });
+      if (ready) {
+        const uint32_t e = op.apply(k);
+        b.state[k] = e ? 2 : 1;
+        if (e) atomicMin(&b.ctl->commit_err, (static_cast<unsigned long long>(k) << 8) | e);
+      } else {
+        atomicAdd(&b.ctl->remaining[r % 3], 1u);
+      }
+    }
+    grid.sync();
+    if (ctl->remaining[r % 3] == 0) break;
+  }
+  if (tid == 0) {
+    *b.round_ctr = round;
+    ctl->rounds = ctl->rounds + r + 1;
+  }
+}
+
+// Walk shadow (sparsifier.cpp:416-423): apply the batch's deletions to the
+// copy of G in event order, skipping absent edges. first_absent records the
+// lowest deletion that found no edge: in a deletion-only batch that is
+// exactly the first event whose graph_.delete_edge throws (:491).
+struct ShadowOp {
+  DevGraph<kCapG> S;
+  const DevEvent* ev;
+  BatchCtl* ctl;
+  __device__ uint32_t limit() const { return 0xFFFFFFFFu; }
+  template <class F>
+  __device__ void for_rows(uint32_t k, F&& f) const {
+    const DevEvent& e = ev[k];
+    if (e.kind == 1) {
+      f(e.u);
+      f(e.v);
+    }
+  }
+  __device__ uint32_t apply(uint32_t k) const {
+    const DevEvent e = ev[k];
+    if (e.kind != 1) return 0;
+    if (has_edge(S, e.u, e.v)) {
+      delete_edge(S, e.u, e.v);
+    } else {
+      atomicMin(&ctl->first_absent, k);
+    }
+    return 0;
+  }
+};
+
+// sparsifier.cpp:207-216 set_edge_weight.
+__device__ __forceinline__ bool set_edge_weight(const DevGraph<kCapH>& h, uint32_t u, uint32_t v,
+                                                double target) {
+  const double current = edge_weight(h, u, v);
+  if (target > current) {
+    return insert_edge(h, u, v, __dsub_rn(target, current)) >= 0;
+  } else if (target < current) {
+    delete_edge(h, u, v);
+    return insert_edge(h, u, v, target) >= 0;
+  }
+  return true;
+}
+
+// Max-weight G neighbour of x (tie -> lowest id) ignoring `skip`
+// (sparsifier.cpp:270-276); kNoVertex when none.
+__device__ __forceinline__ uint32_t best_neighbor(const DevGraph<kCapG>& g, uint32_t x,
+                                                  uint32_t skip, double* wout) {
+  const uint32_t d = g.slab[x].deg;
+  const uint32_t* ids = row_ids(g, x);
+  const double* ws = row_ws(g, x);
+  uint32_t best = kNoVertex;
+  double bw = 0.0;
+  for (uint32_t i = 0; i < d; ++i) {
+    const uint32_t id = ids[i];
+    if (id == skip) continue;
+    const double w = ws[i];
+    if (best == kNoVertex || w > bw || (w == bw && id < best)) {
+      best = id;
+      bw = w;
+    }
+  }
+  if (wout) *wout = bw;
+  return best;
+}
+
+// The sequential commit of sparsifier.cpp:466-533, one event per apply().
+struct CommitOp {
+  DevGraph<kCapG> G;
+  DevGraph<kCapH> H;
+  const DevEvent* ev;
+  const uint32_t* slot;
+  ReachOut rout;
+  MinOut mout;
+  uint32_t* dec;
+  BatchCtl* ctl;
+  WalkOpts o;
+
+  // Events at or past the first failing one never commit (the reference
+  // stops there, :525-529). In a deletion-only batch the shadow pass already
+  // found the first failing deletion exactly (first_absent).
+  __device__ uint32_t limit() const {
+    const volatile BatchCtl* c = ctl;
+    const unsigned long long cerr = c->commit_err >> 8;
+    unsigned long long l = c->limit;
+    if (c->use_absent_limit && c->first_absent < l) l = c->first_absent;
+    return static_cast<uint32_t>(cerr < l ? cerr : l);
+  }
+
+  __device__ const uint32_t* path_of(uint32_t s) const {
+    return mout.paths + static_cast<uint64_t>(s) * (o.T + 1ull);
+  }
+
+  template <class F>
+  __device__ void for_rows(uint32_t k, F&& f) const {
+    const DevEvent& e = ev[k];
+    f(e.u);
+    f(e.v);
+    if (e.kind != 1 || o.freeze) return;
+    const uint32_t s = slot[k];
+    if (s != kNoSlot && mout.has_path[s]) {
+      const uint32_t* p = path_of(s);
+      const uint32_t len = mout.path_len[s];
+      for (uint32_t i = 0; i < len; ++i) f(p[i]);
+    } else {
+      // Local fallback may add the max-weight live-G edge of either end.
+      const uint32_t bu = best_neighbor(G, e.u, e.v, nullptr);
+      if (bu != kNoVertex) f(bu);
+      const uint32_t bv = best_neighbor(G, e.v, e.u, nullptr);
+      if (bv != kNoVertex) f(bv);
+    }
+  }
+
+  __device__ void account(unsigned long long steps) const {
+    atomicAdd(&ctl->report[kWalkerSteps], steps);
+    atomicMax(&ctl->report[kMaxEventSteps], steps);
+  }
+
+  __device__ uint32_t apply(uint32_t k) const {
+    const DevEvent e = ev[k];
+    const uint32_t u = e.u, v = e.v;
+    const uint32_t s = slot[k];
+    unsigned long long steps = 0;
+    if (e.kind == 0) {
+      // :473-488
+      atomicAdd(&ctl->report[kInsSeen], 1ull);
+      if (insert_edge(G, u, v, e.weight) < 0) return kErrPool;
+      bool have = false, reached = false;
+      if (s != kNoSlot) {
+        have = true;
+        reached = rout.reached[s] != 0;
+        steps = rout.steps[s];
+      }
+      // commit_insertion (:220-241)
+      bool kept;
+      if (o.freeze) {
+        kept = false;
+      } else {
+        const double total = edge_weight(G, u, v);
+        kept = !(o.K != 0.0 && have && reached);
+        if (has_edge(H, u, v)) {
+          if (!set_edge_weight(H, u, v, total)) return kErrPool;
+        } else if (kept) {
+          if (insert_edge(H, u, v, total) < 0) return kErrPool;
+        }
+      }
+      atomicAdd(&ctl->report[kept ? kInsKept : kInsPruned], 1ull);
+      dec[k] = kept ? 0u : 1u;
+      account(steps);
+      return 0;
+    }
+    // Deletion (:489-523)
+    atomicAdd(&ctl->report[kDelSeen], 1ull);
+    if (!delete_edge(G, u, v)) return kErrAbsent;
+    uint32_t outcome = 0, added = 0;
+    if (has_edge(H, u, v)) {
+      atomicAdd(&ctl->report[kDelInH], 1ull);
+      delete_edge(H, u, v);
+      if (!o.freeze) {
+        bool path = false;
+        if (s != kNoSlot) {
+          steps = mout.steps[s];
+          path = mout.has_path[s] != 0;
+        }
+        if (path) {
+          const uint32_t* p = path_of(s);
+          const uint32_t len = mout.path_len[s];
+          for (uint32_t i = 0; i + 1 < len; ++i) {
+            const uint32_t a = p[i], bb = p[i + 1];
+            if (!has_edge(H, a, bb)) {
+              if (insert_edge(H, a, bb, edge_weight(G, a, bb)) < 0) return kErrPool;
+              ++added;
+            }
+          }
+          atomicAdd(&ctl->report[kPaths], 1ull);
+          outcome = 1;
+        } else {
+          // run_local_fallback (:264-280): u then v.
+          const uint32_t ends[2] = {u, v};
+          for (int j = 0; j < 2; ++j) {
+            const uint32_t x = ends[j];
+            if (H.slab[x].deg != 0 || G.slab[x].deg == 0) continue;
+            double bw = 0.0;
+            const uint32_t b = best_neighbor(G, x, kNoVertex, &bw);
+            if (insert_edge(H, x, b, bw) < 0) return kErrPool;
+            ++added;
+          }
+          atomicAdd(&ctl->report[kFallbacks], 1ull);
+          outcome = 2;
+        }
+        atomicAdd(&ctl->report[kEdgesRec], static_cast<unsigned long long>(added));
+      } else {
+        atomicAdd(&ctl->report[kFallbacks], 1ull);
+        outcome = 2;
+      }
+    }
+    dec[k] = outcome | (added << 8);
+    account(steps);
+    return 0;
+  }
+};
+
+// Query build (sparsifier.cpp:429-457) on batch-start H / G and the shadow.
+__global__ void k_flags(DevGraph<kCapH> H, DevGraph<kCapG> G, DevGraph<kCapG> S,
+                        const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb || batch_aborted(b.ctl)) return;
+  const DevEvent e = ev[k];
+  unsigned long long flag = 0;
+  if (e.kind == 0) {
+    if (o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) flag = 1ull;
+  } else if (!o.freeze && has_edge(H, e.u, e.v) && S.slab[e.u].deg > 0 && S.slab[e.v].deg > 0) {
+    flag = 1ull << 32;
+  }
+  b.scan_in[k] = flag;
+  b.state[k] = 0;
+  b.dec[k] = 0;
+}
+
+__global__ void k_scatter(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, uint32_t nb,
+                          uint64_t counter, BatchDev b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb || batch_aborted(b.ctl)) return;
+  const unsigned long long f = b.scan_in[k];
+  const unsigned long long x = b.scan_out[k];
+  const uint32_t ri = static_cast<uint32_t>(x & 0xFFFFFFFFull);
+  const uint32_t mi = static_cast<uint32_t>(x >> 32);
+  const DevEvent e = ev[k];
+  const uint64_t uid = counter + k;  // update_id = update_counter_ + k (:431)
+  uint32_t s = kNoSlot;
+  if (f & 0xFFFFFFFFull) {
+    ReachQuery q;
+    q.p = e.u;
+    q.q = e.v;
+    q.w_pq = __dadd_rn(edge_weight(G, e.u, e.v), e.weight);  // :441
+    q.update_id = uid;
+    b.rq[ri] = q;
+    s = ri;
+  } else if (f >> 32) {
+    MinQuery q;
+    q.p = e.u;
+    q.q = e.v;
+    q.update_id = uid;
+    b.mq[mi] = q;
+    s = mi;
+  }
+  b.slot[k] = s;
+  if (k == nb - 1) {
+    b.ctl->nq_reach = ri + static_cast<uint32_t>(f & 0xFFFFFFFFull);
+    b.ctl->nq_min = mi + static_cast<uint32_t>(f >> 32);
+  }
+}
+
+__global__ void k_finish(const unsigned long long* g_cnt, const unsigned long long* h_cnt,
+                         const unsigned long long* s_top, BatchCtl* ctl) {
+  ctl->g_pool_top = g_cnt[0];
+  ctl->g_edges = g_cnt[1];
+  ctl->h_pool_top = h_cnt[0];
+  ctl->h_edges = h_cnt[1];
+  ctl->s_pool_top = s_top ? *s_top : 0ull;
+}
+
+unsigned grid_for(uint64_t n, unsigned bs = 256) {
+  return static_cast<unsigned>((n + bs - 1) / bs);
+}
+
+__global__ void k_pack_reach(ReachOut r, uint32_t lo, uint32_t n, uint32_t slots,
+                             ReachRecord* rec) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= slots) return;
+  ReachRecord x{0, 0, 0ull};
+  if (i < n) {
+    x.reached = r.reached[lo + i];
+    x.steps = r.steps[lo + i];
+  }
+  rec[i] = x;
+}
+
+__global__ void k_pack_min(MinOut m, uint32_t lo, uint32_t n, uint32_t slots, uint32_t T,
+                           uint8_t* rec, size_t rec_bytes) {
+  const uint32_t i = blockIdx.x;
+  if (i >= slots) return;
+  uint8_t* base = rec + static_cast<size_t>(i) * rec_bytes;
+  MinRecordHead* h = reinterpret_cast<MinRecordHead*>(base);
+  uint32_t* path = reinterpret_cast<uint32_t*>(base + sizeof(MinRecordHead));
+  const bool have = i < n;
+  const uint32_t len = have ? m.path_len[lo + i] : 0;
+  if (threadIdx.x == 0) {
+    h->has_path = have ? m.has_path[lo + i] : 0;
+    h->path_len = len;
+    h->steps = have ? m.steps[lo + i] : 0ull;
+    h->resistance = have ? m.resistance[lo + i] : 0.0;
+  }
+  const uint32_t* src = m.paths + static_cast<uint64_t>(lo + i) * (T + 1ull);
+  for (uint32_t j = threadIdx.x; j < T + 1; j += blockDim.x) path[j] = (j < len) ? src[j] : 0u;
+}
+
+// Query q of a world-way split lives on rank r = owner with
+// lo_r = floor(nq*r/world) (contiguous ranges).
+__device__ __forceinline__ void locate(uint32_t q, uint32_t nq, int world, uint32_t* rank,
+                                       uint32_t* idx) {
+  uint32_t r = static_cast<uint32_t>((static_cast<unsigned long long>(q) * world) / (nq ? nq : 1));
+  while (r + 1 < static_cast<uint32_t>(world) &&
+         (static_cast<unsigned long long>(nq) * (r + 1)) / world <= q)
+    ++r;
+  while (r > 0 && (static_cast<unsigned long long>(nq) * r) / world > q) --r;
+  *rank = r;
+  *idx = q - static_cast<uint32_t>((static_cast<unsigned long long>(nq) * r) / world);
+}
+
+__global__ void k_unpack_reach(ReachOut r, uint32_t nq, int world, uint32_t slots,
+                               const ReachRecord* rec) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  uint32_t rank, idx;
+  locate(q, nq, world, &rank, &idx);
+  const ReachRecord x = rec[static_cast<size_t>(rank) * slots + idx];
+  r.reached[q] = x.reached;
+  r.steps[q] = x.steps;
+}
+
+__global__ void k_unpack_min(MinOut m, uint32_t nq, int world, uint32_t slots, uint32_t T,
+                             const uint8_t* rec, size_t rec_bytes) {
+  const uint32_t q = blockIdx.x;
+  if (q >= nq) return;
+  uint32_t rank, idx;
+  locate(q, nq, world, &rank, &idx);
+  const uint8_t* base = rec + (static_cast<size_t>(rank) * slots + idx) * rec_bytes;
+  const MinRecordHead* h = reinterpret_cast<const MinRecordHead*>(base);
+  const uint32_t* path = reinterpret_cast<const uint32_t*>(base + sizeof(MinRecordHead));
+  if (threadIdx.x == 0) {
+    m.has_path[q] = h->has_path;
+    m.path_len[q] = h->path_len;
+    m.steps[q] = h->steps;
+    m.resistance[q] = h->resistance;
+  }
+  uint32_t* dst = m.paths + static_cast<uint64_t>(q) * (T + 1ull);
+  for (uint32_t j = threadIdx.x; j < h->path_len; j += blockDim.x) dst[j] = path[j];
+}
+
+template <class Op>
+int launch_rounds(const Op& op, uint32_t nev, const BatchDev& b, int coop_blocks,
+                  cudaStream_t st) {
+  if (nev == 0) return 0;
+  Op op_copy = op;
+  BatchDev b_copy = b;
+  void* args[] = {&op_copy, &nev, &b_copy};
+  const int need = static_cast<int>(grid_for(nev));
+  const int blocks = need < coop_blocks ? need : coop_blocks;
+  cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&k_rounds<Op>), dim3(blocks),
+                                         dim3(256), args, 0, st),
+             "cooperative round launch");
+  return 1;
+}
+
+}  // namespace
+
+int coop_grid_blocks(int device) {
+  int sms = 0, per_sm_a = 0, per_sm_b = 0;
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, k_rounds<CommitOp>, 256, 0),
+             "occupancy");
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_rounds<ShadowOp>, 256, 0),
+             "occupancy");
+  const int per_sm = per_sm_a < per_sm_b ? per_sm_a : per_sm_b;
+  return sms * (per_sm > 0 ? per_sm : 1);
+}
+
+size_t scan_temp_bytes(uint32_t nb_cap) {
+  size_t temp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<unsigned long long*>(nullptr),
+                                static_cast<unsigned long long*>(nullptr), nb_cap);
+  return temp;
+}
+
+int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, cudaStream_t st) {
+  if (nb == 0) return 0;
+  k_validate<<<grid_for(nb), 256, 0, st>>>(b.events, nb, n, b.ctl);
+  return 1;
+}
+
+int launch_shadow(const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb, int coop_blocks,
+                  cudaStream_t st) {
+  ShadowOp op{S, b.events, b.ctl};
+  cuda_check(cudaMemsetAsync(b.state, 0, nb, st), "memset state");
+  return launch_rounds(op, nb, b, coop_blocks, st);
+}
+
+int launch_queries(const DevGraph<kCapH>& H, const DevGraph<kCapG>& G,
+                   const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb, uint64_t counter,
+                   const WalkOpts& o, cudaStream_t st) {
+  if (nb == 0) return 0;
+  k_flags<<<grid_for(nb), 256, 0, st>>>(H, G, S, b.events, nb, o, b);
+  size_t temp = b.cub_temp_bytes;
+  cuda_check(cub::DeviceScan::ExclusiveSum(b.cub_temp, temp, b.scan_in, b.scan_out, nb, st),
+             "query scan");
+  k_scatter<<<grid_for(nb), 256, 0, st>>>(G, b.events, nb, counter, b);
+  return 3;
+}
+
+int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
+                  uint32_t nb, const WalkOpts& o, int coop_blocks, cudaStream_t st) {
+  CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.dec, b.ctl, o};
+  return launch_rounds(op, nb, b, coop_blocks, st);
+}
+
+int launch_pack(const BatchDev& b, uint32_t lo_r, uint32_t n_r, uint32_t lo_m, uint32_t n_m,
+                uint32_t slots_r, uint32_t slots_m, uint32_t T, void* rrec, void* mrec,
+                cudaStream_t st) {
+  int l = 0;
+  if (slots_r) {
+    k_pack_reach<<<grid_for(slots_r), 256, 0, st>>>(b.rout, lo_r, n_r, slots_r,
+                                                     static_cast<ReachRecord*>(rrec));
+    ++l;
+  }
+  if (slots_m) {
+    k_pack_min<<<slots_m, 128, 0, st>>>(b.mout, lo_m, n_m, slots_m, T, static_cast<uint8_t*>(mrec),
+                                        min_record_bytes(T));
+    ++l;
+  }
+  return l;
+}
+
+int launch_unpack(const BatchDev& b, uint32_t nq_r, uint32_t nq_m, int world, uint32_t slots_r,
+                  uint32_t slots_m, uint32_t T, const void* rrec, const void* mrec,
+                  cudaStream_t st) {
+  int l = 0;
+  if (nq_r) {
+    k_unpack_reach<<<grid_for(nq_r), 256, 0, st>>>(b.rout, nq_r, world, slots_r,
+                                                   static_cast<const ReachRecord*>(rrec));
+    ++l;
+  }
+  if (nq_m) {
+    k_unpack_min<<<nq_m, 128, 0, st>>>(b.mout, nq_m, world, slots_m, T,
+                                       static_cast<const uint8_t*>(mrec), min_record_bytes(T));
+    ++l;
+  }
+  return l;
+}
+
+int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H,
+                  const unsigned long long* s_pool_top, const BatchDev& b, cudaStream_t st) {
+  k_finish<<<1, 1, 0, st>>>(G.pool_top, H.pool_top, s_pool_top, b.ctl);
+  return 1;
+}
+
+}  // namespace dyg

@@ -1,0 +1,136 @@
+// batch.cuh -- device side of replay_batch_deferred
+// (proj/src/sparsifier.cpp:395-539), minus the walks (walk.cuh).
+//
+// Kernel map (SURVEY.md 2 kernel table):
+//   k_validate        validate_event_shape (sparsifier.cpp:321-337)
+//   ShadowOp rounds   shadow G = batch-start G minus the batch's deletions in
+//                     event order (sparsifier.cpp:416-423)          [K5]
+//   k_flags/k_scatter query build (sparsifier.cpp:429-457)           [K4]
+//   CommitOp rounds   the sequential commit (sparsifier.cpp:466-533)
+//                     incl. commit_insertion / set_edge_weight
+//                     (:207-241) and run_local_fallback (:264-280)  [K6-K8]
+//   k_finish          BatchReport counters (sparsifier.hpp:44-59)    [K9]
+//
+// The commit engine ("dependency rounds"): every round, each pending event
+// reserves all rows it will read or write (atomicMax of a round-stamped key
+// that prefers the lowest event index); an event that won all its rows
+// applies, with exactly the reference's per-event operations. Events that
+// touch disjoint rows commute, and an event only applies after every
+// earlier event sharing a row, so the final rows equal the sequential
+// event-order commit bit for bit. One cooperative launch runs all rounds.
+#pragma once
+
+#include "walk.cuh"
+
+namespace dyg {
+
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+
+struct DevEvent {   // dyg_event / EdgeEvent (stream.hpp:11-18)
+  uint32_t kind;    // 0 insertion, 1 deletion
+  uint32_t u, v;
+  uint32_t batch_index;
+  double weight;
+};
+
+// Report counters in BatchReport order (sparsifier.hpp:46-55).
+enum ReportField {
+  kInsSeen = 0, kInsKept, kInsPruned, kDelSeen, kDelInH, kPaths, kEdgesRec, kFallbacks,
+  kWalkerSteps, kMaxEventSteps, kReportFields
+};
+
+// Validation error codes (packed as (k << 8) | code into err keys).
+enum EventError : uint32_t {
+  kErrRange = 1,       // "vertex id out of range"
+  kErrSelfLoop = 2,    // "self-loop"
+  kErrWeight = 3,      // "non-positive weight"
+  kErrAbsent = 4,      // delete_edge: "edge (u, v) does not exist"
+  kErrPool = 5,        // overflow pool exhausted (device)
+};
+
+struct BatchCtl {
+  unsigned long long val_err;     // min (k << 8 | code) from validation
+  unsigned long long commit_err;  // min (k << 8 | code) from the commit
+  unsigned int first_absent;      // min k whose deletion found no shadow edge
+  unsigned int limit;             // commit only events k < limit
+  unsigned int use_absent_limit;  // deletion-only batch: also k < first_absent
+  unsigned int nq_reach;
+  unsigned int nq_min;
+  unsigned int remaining[3];
+  unsigned int rounds;
+  unsigned long long report[kReportFields];
+  WalkCounters reach;
+  WalkCounters minpath;
+  unsigned long long g_edges, h_edges, g_pool_top, h_pool_top, s_pool_top;
+};
+
+struct WalkOpts {
+  double K;
+  uint32_t T;
+  uint32_t s;
+  uint64_t seed;
+  int filtering;   // K != 0 && !freeze (sparsifier.cpp:409-410)
+  int freeze;
+};
+
+// Device buffers of one batch (sized by the session; grown on demand).
+struct BatchDev {
+  DevEvent* events;
+  uint8_t* state;
+  uint32_t* slot;
+  unsigned long long* scan_in;
+  unsigned long long* scan_out;
+  ReachQuery* rq;
+  MinQuery* mq;
+  ReachOut rout;
+  MinOut mout;
+  MinScratch mscratch;
+  uint32_t* dec;           // per-event outcome (kind | edges_added << 8)
+  unsigned long long* locks;  // per-vertex row reservations
+  unsigned long long* round_ctr;
+  BatchCtl* ctl;
+  void* cub_temp;
+  size_t cub_temp_bytes;
+};
+
+// Host launchers (batch.cu); each returns kernels launched.
+int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, cudaStream_t st);
+int launch_shadow(const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb, int coop_blocks,
+                  cudaStream_t st);
+int launch_queries(const DevGraph<kCapH>& H, const DevGraph<kCapG>& G,
+                   const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb,
+                   uint64_t counter, const WalkOpts& o, cudaStream_t st);
+int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
+                  uint32_t nb, const WalkOpts& o, int coop_blocks, cudaStream_t st);
+int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H,
+                  const unsigned long long* s_pool_top, const BatchDev& b, cudaStream_t st);
+size_t scan_temp_bytes(uint32_t nb_cap);
+
+// Multi-GPU exchange records. Reach: 16 B per query.
+// MinPath: 24 B header + (T+1) u32 vertices, padded to 8 B.
+struct ReachRecord {
+  uint32_t reached;
+  uint32_t pad;
+  unsigned long long steps;
+};
+struct MinRecordHead {
+  uint32_t has_path;
+  uint32_t path_len;
+  unsigned long long steps;
+  double resistance;
+};
+inline size_t min_record_bytes(uint32_t T) {
+  return (sizeof(MinRecordHead) + 4ull * (T + 1ull) + 7ull) & ~7ull;
+}
+// Pack this rank's queries [lo, hi) into `slots` records (rest zeroed).
+int launch_pack(const BatchDev& b, uint32_t lo_r, uint32_t n_r, uint32_t lo_m, uint32_t n_m,
+                uint32_t slots_r, uint32_t slots_m, uint32_t T, void* rrec, void* mrec,
+                cudaStream_t st);
+// Scatter rank-major gathered records back to query order.
+int launch_unpack(const BatchDev& b, uint32_t nq_r, uint32_t nq_m, int world, uint32_t slots_r,
+                  uint32_t slots_m, uint32_t T, const void* rrec, const void* mrec,
+                  cudaStream_t st);
+// Co-resident blocks for the cooperative round kernels.
+int coop_grid_blocks(int device);
+
+}  // namespace dyg

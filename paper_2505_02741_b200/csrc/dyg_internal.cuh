@@ -1,0 +1,192 @@
+// dyg_internal.cuh -- device data layout and shared device helpers.
+//
+// Device-resident dynamic rows (reference
+// DynamicGraph = vector<vector<Neighbor>>, proj/src/graph.hpp:65).
+//
+// Every vertex owns one fixed-size, size-aligned SLAB:
+//     { u32 deg; u32 ext; u32 id[C]; f64 w[C]; }
+// H uses C = 4 (64 B, one half line), G uses C = 10 (128 B, one line).
+// A row with deg <= C lives inline, so a walker step needs ONE dependent
+// fetch (header + ids + weights in the same line) instead of the two a
+// row_ptr CSR needs. A row that outgrows its slab moves to the overflow pool
+// (SoA arrays pool_id / pool_w, block of cap[u] entries at index ext); the
+// slab then only carries deg and ext. Per-row order is exactly the
+// reference's: append = push_back (graph.cpp:80-81), delete = move the last
+// entry into the hole (graph.cpp:97-108), coalesce in place (graph.cpp:74-79).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dyg {
+
+constexpr uint32_t kNoVertex = 0xFFFFFFFFu;  // walk.cpp:12
+constexpr uint32_t kInline = 0xFFFFFFFFu;    // slab.ext for inline rows
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr int kCapH = 4;   // inline entries per H slab (64 B)
+constexpr int kCapG = 10;  // inline entries per G slab (128 B)
+
+// rng.hpp:37-41
+__host__ __device__ __forceinline__ uint64_t hash_mix(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+// rng.hpp:45-50
+__host__ __device__ __forceinline__ uint64_t walker_seed(uint64_t global_seed, uint64_t update_id,
+                                                         uint64_t walker) {
+  uint64_t h = hash_mix(global_seed + 0x9E3779B97F4A7C15ull);
+  h = hash_mix(h ^ (update_id + 0xBF58476D1CE4E5B9ull));
+  return hash_mix(h ^ (walker + 0x94D049BB133111EBull));
+}
+// The k-th (1-based) SplitMix64 draw of a stream seeded `seed` is
+// hash_mix(seed + k*gamma) (rng.hpp:7-13); next_double = (x >> 11) * 2^-53
+// (rng.hpp:24). Counter form: a lane computes step t's draw (k = t + 1)
+// without carrying generator state.
+__device__ __forceinline__ double draw_u01(uint64_t seed, uint32_t k) {
+  const uint64_t x = hash_mix(seed + static_cast<uint64_t>(k) * kGamma);
+  return __dmul_rn(static_cast<double>(x >> 11), 0x1.0p-53);
+}
+
+template <int C>
+struct alignas(C <= 4 ? 64 : 128) Slab {
+  uint32_t deg;
+  uint32_t ext;
+  uint32_t id[C];
+  double w[C];
+};
+static_assert(sizeof(Slab<kCapH>) == 64, "H slab must be 64 B");
+static_assert(sizeof(Slab<kCapG>) == 128, "G slab must be 128 B");
+
+// POD view of one device graph, passed by value to kernels.
+template <int C>
+struct DevGraph {
+  Slab<C>* slab;
+  uint32_t* cap;                  // overflow block capacity (0 = inline)
+  uint32_t* pool_id;
+  double* pool_w;
+  unsigned long long* pool_top;   // entries handed out (device counter)
+  unsigned long long pool_cap;
+  unsigned long long* edges;      // |E| (device counter)
+  uint32_t n;
+};
+
+// ---------------------------------------------------------------- rows
+template <int C>
+__device__ __forceinline__ uint32_t* row_ids(const DevGraph<C>& g, uint32_t u) {
+  Slab<C>& s = g.slab[u];
+  return s.ext == kInline ? s.id : g.pool_id + s.ext;
+}
+template <int C>
+__device__ __forceinline__ double* row_ws(const DevGraph<C>& g, uint32_t u) {
+  Slab<C>& s = g.slab[u];
+  return s.ext == kInline ? s.w : g.pool_w + s.ext;
+}
+// graph.cpp:34-46 find: index of the first entry of row u with id v, or -1.
+template <int C>
+__device__ __forceinline__ int row_find(const DevGraph<C>& g, uint32_t u, uint32_t v) {
+  const uint32_t d = g.slab[u].deg;
+  const uint32_t* ids = row_ids(g, u);
+  for (uint32_t i = 0; i < d; ++i)
+    if (ids[i] == v) return static_cast<int>(i);
+  return -1;
+}
+// graph.cpp:48-53 has_edge (scan the smaller row; symmetric result).
+template <int C>
+__device__ __forceinline__ bool has_edge(const DevGraph<C>& g, uint32_t u, uint32_t v) {
+  if (g.slab[u].deg > g.slab[v].deg) { const uint32_t t = u; u = v; v = t; }
+  return row_find(g, u, v) >= 0;
+}
+// graph.cpp:55-62 edge_weight (0.0 when absent).
+template <int C>
+__device__ __forceinline__ double edge_weight(const DevGraph<C>& g, uint32_t u, uint32_t v) {
+  if (g.slab[u].deg > g.slab[v].deg) { const uint32_t t = u; u = v; v = t; }
+  const int i = row_find(g, u, v);
+  return i < 0 ? 0.0 : row_ws(g, u)[i];
+}
+// push_back with slab -> pool relocation. Returns false when the pool is
+// exhausted (the host keeps enough headroom that this never happens).
+template <int C>
+__device__ __forceinline__ bool row_push(const DevGraph<C>& g, uint32_t u, uint32_t id,
+                                         double w) {
+  Slab<C>& s = g.slab[u];
+  const uint32_t d = s.deg;
+  if (s.ext == kInline) {
+    if (d < C) {
+      s.id[d] = id;
+      s.w[d] = w;
+      s.deg = d + 1;
+      return true;
+    }
+    const uint32_t nc = 2 * C < 8 ? 8 : 2 * C;
+    const unsigned long long b = atomicAdd(g.pool_top, static_cast<unsigned long long>(nc));
+    if (b + nc > g.pool_cap) return false;
+    for (uint32_t i = 0; i < d; ++i) {
+      g.pool_id[b + i] = s.id[i];
+      g.pool_w[b + i] = s.w[i];
+    }
+    s.ext = static_cast<uint32_t>(b);
+    g.cap[u] = nc;
+  } else if (d == g.cap[u]) {
+    const uint32_t nc = 2 * g.cap[u];
+    const unsigned long long b = atomicAdd(g.pool_top, static_cast<unsigned long long>(nc));
+    if (b + nc > g.pool_cap) return false;
+    for (uint32_t i = 0; i < d; ++i) {
+      g.pool_id[b + i] = g.pool_id[s.ext + i];
+      g.pool_w[b + i] = g.pool_w[s.ext + i];
+    }
+    s.ext = static_cast<uint32_t>(b);
+    g.cap[u] = nc;
+  }
+  g.pool_id[s.ext + d] = id;
+  g.pool_w[s.ext + d] = w;
+  s.deg = d + 1;
+  return true;
+}
+// graph.cpp:97-105 remove_from: the last entry moves into the hole.
+template <int C>
+__device__ __forceinline__ void row_remove_at(const DevGraph<C>& g, uint32_t u, uint32_t i) {
+  Slab<C>& s = g.slab[u];
+  const uint32_t last = s.deg - 1;
+  uint32_t* ids = row_ids(g, u);
+  double* ws = row_ws(g, u);
+  ids[i] = ids[last];
+  ws[i] = ws[last];
+  s.deg = last;
+}
+
+// graph.cpp:64-85 insert_edge on validated input. Returns 0 New,
+// 1 Coalesced, -1 pool exhausted.
+template <int C>
+__device__ __forceinline__ int insert_edge(const DevGraph<C>& g, uint32_t u, uint32_t v,
+                                           double w) {
+  const int i = row_find(g, u, v);
+  if (i >= 0) {
+    double* wu = row_ws(g, u);
+    wu[i] = __dadd_rn(wu[i], w);
+    row_ws(g, v)[row_find(g, v, u)] = wu[i];
+    return 1;
+  }
+  if (!row_push(g, u, v, w)) return -1;
+  if (!row_push(g, v, u, w)) return -1;
+  atomicAdd(g.edges, 1ull);
+  return 0;
+}
+// graph.cpp:87-112 delete_edge. Returns false when absent (Data error).
+template <int C>
+__device__ __forceinline__ bool delete_edge(const DevGraph<C>& g, uint32_t u, uint32_t v) {
+  const int i = row_find(g, u, v);
+  if (i < 0) return false;
+  row_remove_at(g, u, static_cast<uint32_t>(i));
+  row_remove_at(g, v, static_cast<uint32_t>(row_find(g, v, u)));
+  atomicAdd(g.edges, static_cast<unsigned long long>(-1ll));
+  return true;
+}
+
+// Algorithmic bytes of one walker step at a row of degree d:
+// the header plus d (u32 id, f64 w) pairs, rounded up to 32 B sectors.
+__device__ __forceinline__ uint32_t step_bytes(uint32_t d) {
+  return 32u * ((8u + 12u * d + 31u) / 32u);
+}
+
+}  // namespace dyg

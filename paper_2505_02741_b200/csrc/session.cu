@@ -1,0 +1,1141 @@
+// session.cu -- the C-ABI (include/dyg.h): device session lifecycle, the
+// per-batch pipeline of replay_batch_deferred (sparsifier.cpp:395-539),
+// immediate mode as 1-event batches, the stateless
+// run_batch twin, exports and snapshots.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/dyg.h"
+#include "batch.cuh"
+#include "graph_store.cuh"
+
+using namespace dyg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ApiError {
+  int code;
+  std::string message;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw ApiError{code, msg}; }
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return DYG_OK;
+  } catch (const ApiError& e) {
+    g_last_error = e.message;
+    return e.code;
+  } catch (const DeviceError& e) {
+    g_last_error = e.message;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return DYG_ERR_DEVICE;
+  }
+}
+
+void check(cudaError_t e, const char* what) { cuda_check(e, what); }
+
+template <typename T>
+void dev_alloc(T** p, size_t count, const char* what) {
+  check(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * std::max<size_t>(count, 1)), what);
+}
+template <typename T>
+void dev_free(T*& p) {
+  cudaFree(p);
+  p = nullptr;
+}
+
+double density_of(uint64_t edges, uint32_t n) {
+  return static_cast<double>(edges) / static_cast<double>(n) - 1.0;  // graph.cpp:114-116
+}
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  void init() {
+    check(cudaEventCreate(&a), "event");
+    check(cudaEventCreate(&b), "event");
+  }
+  void destroy() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    a = b = nullptr;
+  }
+  float ms() const {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    return t;
+  }
+};
+
+}  // namespace
+
+struct dyg_session {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  dyg_options opt{};
+  uint32_t n = 0;
+  int coop_blocks = 0;
+
+  GraphStore<kCapG> G, S, G_snap;
+  GraphStore<kCapH> H, H_snap;
+  uint64_t counter = 0, counter_snap = 0;
+  uint64_t g_edges = 0, h_edges = 0, g_top = 0, h_top = 0;
+  uint64_t g_edges_snap = 0, h_edges_snap = 0, g_top_snap = 0, h_top_snap = 0;
+  bool have_snap = false;
+  uint64_t last_event_steps = 0;
+
+  // Batch buffers.
+  BatchDev b{};
+  uint32_t nb_cap = 0, nd_cap = 0;
+  unsigned long long* d_locks = nullptr;
+  unsigned long long* d_round = nullptr;
+  DevEvent* d_events = nullptr;
+  DevEvent* h_events_pinned = nullptr;
+  BatchCtl* h_ctl = nullptr;
+
+  // Device-resident stream.
+  DevEvent* d_stream = nullptr;
+  std::vector<dyg_event> stream_events;      // sorted by batch (stable)
+  std::vector<uint64_t> stream_positions;    // original stream index
+  std::vector<uint64_t> batch_off, batch_cnt, batch_ins, batch_del;
+  uint32_t stream_batches = 0;
+  bool have_stream = false;
+
+  // Last-batch outputs (immediate mode / apply_*).
+  uint32_t last_dec = 0;
+  uint32_t* d_counts = nullptr;   // shard query counts (device)
+  uint32_t* h_counts = nullptr;   // pinned: [0..1] shard counts, [2] decision
+  // Multi-GPU split state (dyg_shard_*).
+  bool shard_active = false;
+  std::vector<DevEvent> shard_host;
+  std::vector<uint64_t> shard_pos;
+  uint32_t shard_nb = 0, shard_ins = 0, shard_del = 0, shard_batch = 0;
+  uint32_t shard_nq_r = 0, shard_nq_m = 0;
+  std::chrono::steady_clock::time_point shard_wall0;
+  int shard_launches = 0;
+
+  dyg_stats stats{};
+  Timer t_total, t_reach, t_min, t_commit;
+  bool debug_sync = false;
+};
+
+namespace {
+
+void maybe_sync(dyg_session* s, const char* what) {
+  if (s->debug_sync) check(cudaStreamSynchronize(s->stream), what);
+  else check(cudaGetLastError(), what);
+}
+
+void free_batch(dyg_session* s) {
+  BatchDev& b = s->b;
+  dev_free(b.state);
+  dev_free(b.slot);
+  dev_free(b.scan_in);
+  dev_free(b.scan_out);
+  dev_free(b.rq);
+  dev_free(b.mq);
+  dev_free(b.rout.reached);
+  dev_free(b.rout.steps);
+  dev_free(b.rout.best_bits);
+  dev_free(b.mout.has_path);
+  dev_free(b.mout.path_len);
+  dev_free(b.mout.steps);
+  dev_free(b.mout.resistance);
+  dev_free(b.mout.paths);
+  dev_free(b.mscratch.acc);
+  dev_free(b.mscratch.term);
+  dev_free(b.mscratch.steps);
+  dev_free(b.mscratch.paths);
+  dev_free(b.mscratch.rvals);
+  dev_free(b.dec);
+  cudaFree(b.cub_temp);
+  b.cub_temp = nullptr;
+  dev_free(s->d_events);
+  if (s->h_events_pinned) cudaFreeHost(s->h_events_pinned);
+  s->h_events_pinned = nullptr;
+  s->nb_cap = s->nd_cap = 0;
+}
+
+// Sizes the batch buffers for nb events of which nd are deletions.
+void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
+  BatchDev& b = s->b;
+  const uint64_t T1 = static_cast<uint64_t>(s->opt.walk.step_cap) + 1;
+  const uint64_t sw = s->opt.walk.walker_count;
+  if (nb > s->nb_cap) {
+    const uint32_t cap = std::max<uint32_t>(nb, 1024);
+    const uint32_t keep_nd = s->nd_cap;
+    free_batch(s);
+    dev_alloc(&b.state, cap, "batch state");
+    dev_alloc(&b.slot, cap, "batch slots");
+    dev_alloc(&b.scan_in, cap, "batch scan");
+    dev_alloc(&b.scan_out, cap, "batch scan");
+    dev_alloc(&b.rq, cap, "reach queries");
+    dev_alloc(&b.mq, cap, "minpath queries");
+    dev_alloc(&b.rout.reached, cap, "reach out");
+    dev_alloc(&b.rout.steps, cap, "reach out");
+    dev_alloc(&b.rout.best_bits, cap, "reach out");
+    dev_alloc(&b.dec, cap, "decisions");
+    dev_alloc(&s->d_events, cap, "batch events");
+    check(cudaMallocHost(reinterpret_cast<void**>(&s->h_events_pinned), sizeof(DevEvent) * cap),
+          "pinned events");
+    b.cub_temp_bytes = scan_temp_bytes(cap);
+    check(cudaMalloc(&b.cub_temp, std::max<size_t>(b.cub_temp_bytes, 16)), "scan temp");
+    s->nb_cap = cap;
+    s->nd_cap = 0;
+    (void)keep_nd;
+  }
+  if (nd > s->nd_cap || b.mout.has_path == nullptr) {
+    const uint32_t cap = std::max<uint32_t>(nd, 256);
+    dev_free(b.mout.has_path);
+    dev_free(b.mout.path_len);
+    dev_free(b.mout.steps);
+    dev_free(b.mout.resistance);
+    dev_free(b.mout.paths);
+    dev_free(b.mscratch.acc);
+    dev_free(b.mscratch.term);
+    dev_free(b.mscratch.steps);
+    dev_free(b.mscratch.paths);
+    dev_free(b.mscratch.rvals);
+    dev_alloc(&b.mout.has_path, cap, "minpath out");
+    dev_alloc(&b.mout.path_len, cap, "minpath out");
+    dev_alloc(&b.mout.steps, cap, "minpath out");
+    dev_alloc(&b.mout.resistance, cap, "minpath out");
+    dev_alloc(&b.mout.paths, cap * T1, "minpath paths");
+    dev_alloc(&b.mscratch.acc, cap * sw, "minpath scratch");
+    dev_alloc(&b.mscratch.term, cap * sw, "minpath scratch");
+    dev_alloc(&b.mscratch.steps, cap * sw, "minpath scratch");
+    dev_alloc(&b.mscratch.paths, cap * sw * T1, "minpath traces");
+    dev_alloc(&b.mscratch.rvals, cap * T1, "minpath scratch");
+    s->nd_cap = cap;
+  }
+}
+
+WalkOpts walk_opts(const dyg_session* s) {
+  WalkOpts o;
+  o.K = s->opt.walk.distortion_threshold;
+  o.T = s->opt.walk.step_cap;
+  o.s = s->opt.walk.walker_count;
+  o.seed = s->opt.walk.global_seed;
+  o.freeze = s->opt.freeze_sparsifier != 0;
+  o.filtering = (o.K != 0.0 && !o.freeze) ? 1 : 0;  // sparsifier.cpp:409-410
+  return o;
+}
+
+std::string event_error_message(uint32_t code, uint64_t pos, const DevEvent& e) {
+  char buf[256];
+  switch (code) {
+    case kErrRange:
+      std::snprintf(buf, sizeof buf, "event %llu: vertex id out of range",
+                    static_cast<unsigned long long>(pos));
+      break;
+    case kErrSelfLoop:
+      std::snprintf(buf, sizeof buf, "event %llu: self-loop", static_cast<unsigned long long>(pos));
+      break;
+    case kErrWeight:
+      std::snprintf(buf, sizeof buf, "event %llu: non-positive weight",
+                    static_cast<unsigned long long>(pos));
+      break;
+    case kErrAbsent:
+      std::snprintf(buf, sizeof buf, "event %llu: edge (%u, %u) does not exist",
+                    static_cast<unsigned long long>(pos), e.u, e.v);
+      break;
+    default:
+      std::snprintf(buf, sizeof buf, "event %llu: overflow pool exhausted",
+                    static_cast<unsigned long long>(pos));
+  }
+  return buf;
+}
+
+// One deferred batch in three phases, so the multi-GPU split
+// (dyg_shard_*) can run the walk phase on a query range and exchange
+// results before the replicated commit.
+struct Pending {
+  const DevEvent* dev = nullptr;
+  const DevEvent* host = nullptr;
+  const uint64_t* pos = nullptr;
+  uint32_t nb = 0, n_ins = 0, n_del = 0, batch = 0;
+  bool imm_msgs = false;
+  std::chrono::steady_clock::time_point wall0;
+  int launches = 0;
+};
+
+[[noreturn]] void fail_validation(dyg_session* s, const Pending& p, unsigned long long val_err) {
+  const uint32_t k = static_cast<uint32_t>(val_err >> 8);
+  const uint64_t pos = p.pos ? p.pos[k] : k;
+  std::string msg = event_error_message(static_cast<uint32_t>(val_err & 0xFF), pos, p.host[k]);
+  if (p.imm_msgs) {
+    char pre[64];
+    std::snprintf(pre, sizeof pre, "event %llu: ", static_cast<unsigned long long>(pos));
+    msg = pre + msg;  // sparsifier.cpp:479+503-507 rewraps validate's message
+  }
+  (void)s;
+  fail(DYG_ERR_DATA, msg);
+}
+
+// validate (:405-407), walk shadow (:416-423), query build (:429-457).
+void phase_prepare(dyg_session* s, Pending& p) {
+  const WalkOpts o = walk_opts(s);
+  const uint64_t T1 = static_cast<uint64_t>(o.T) + 1;
+  ensure_batch(s, p.nb, p.n_del);
+  // Pool headroom: appends this batch can make (sparsifier.cpp:474,483,
+  // 503-519), with a 4x factor for slab->pool relocations.
+  const uint64_t g_app = 2ull * p.n_ins;
+  const uint64_t h_app = 2ull * p.n_ins + p.n_del * (2 * T1 + 4);
+  s->G.ensure_pool(s->g_top, 4 * g_app + (1u << 16), s->stream);
+  s->H.ensure_pool(s->h_top, 4 * h_app + (1u << 16), s->stream);
+  BatchDev& b = s->b;
+  b.events = const_cast<DevEvent*>(p.dev);
+  b.locks = s->d_locks;
+  b.round_ctr = s->d_round;
+  BatchCtl& c = *s->h_ctl;
+  std::memset(&c, 0, sizeof c);
+  c.val_err = ~0ull;
+  c.commit_err = ~0ull;
+  c.first_absent = 0xFFFFFFFFu;
+  c.limit = p.nb;
+  c.use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
+  check(cudaMemcpyAsync(b.ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->stream), "ctl upload");
+  s->stats.h2d_bytes += sizeof c;
+  check(cudaEventRecord(s->t_total.a, s->stream), "event");
+  p.launches += launch_validate(b, p.nb, s->n, s->stream);
+  maybe_sync(s, "validate");
+  if (p.n_del > 0) {
+    s->S.copy_from(s->G, s->stream);
+    ++p.launches;
+    p.launches += launch_shadow(s->S.view(), b, p.nb, s->coop_blocks, s->stream);
+    maybe_sync(s, "shadow");
+  }
+  p.launches += launch_queries(s->H.view(), s->G.view(), p.n_del > 0 ? s->S.view() : s->G.view(),
+                               b, p.nb, s->counter, o, s->stream);
+  maybe_sync(s, "queries");
+}
+
+// Walks over query ranges. Full range (single GPU): counts stay on the
+// device (no host sync). Shard range: counts written from the host.
+void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n_r, uint32_t lo_m,
+                uint32_t n_m) {
+  const WalkOpts o = walk_opts(s);
+  BatchDev& b = s->b;
+  WalkParams P{o.K, o.T, o.s, o.seed};
+  const uint32_t* cnt_r = &b.ctl->nq_reach;
+  const uint32_t* cnt_m = &b.ctl->nq_min;
+  uint32_t max_r = p.n_ins, max_m = p.n_del;
+  if (!full) {
+    s->h_counts[0] = n_r;
+    s->h_counts[1] = n_m;
+    check(cudaMemcpyAsync(s->d_counts, s->h_counts, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                          s->stream), "shard counts");
+    cnt_r = s->d_counts;
+    cnt_m = s->d_counts + 1;
+    max_r = n_r;
+    max_m = n_m;
+  }
+  check(cudaEventRecord(s->t_reach.a, s->stream), "event");
+  if (p.n_ins > 0 && o.filtering && max_r > 0) {
+    ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
+    p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
+                               s->stream);
+    maybe_sync(s, "reach walks");
+  }
+  check(cudaEventRecord(s->t_reach.b, s->stream), "event");
+  check(cudaEventRecord(s->t_min.a, s->stream), "event");
+  if (p.n_del > 0 && !o.freeze && max_m > 0) {
+    WalkParams Pd = P;
+    Pd.K = std::numeric_limits<double>::infinity();  // sparsifier.cpp:458-459
+    const uint64_t T1 = static_cast<uint64_t>(o.T) + 1;
+    MinOut mo{b.mout.has_path + lo_m, b.mout.path_len + lo_m, b.mout.steps + lo_m,
+              b.mout.resistance + lo_m, b.mout.paths + lo_m * T1};
+    p.launches += launch_minpath(s->S.view(), b.mq + lo_m, cnt_m, max_m, Pd, b.mscratch, mo,
+                                 &b.ctl->minpath, s->stream);
+    maybe_sync(s, "minpath walks");
+  }
+  check(cudaEventRecord(s->t_min.b, s->stream), "event");
+}
+
+// Commit (:466-533), report (:535-537), error mapping.
+void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
+  const WalkOpts o = walk_opts(s);
+  BatchDev& b = s->b;
+  BatchCtl& c = *s->h_ctl;
+  check(cudaEventRecord(s->t_commit.a, s->stream), "event");
+  p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, o, s->coop_blocks, s->stream);
+  maybe_sync(s, "commit");
+  check(cudaEventRecord(s->t_commit.b, s->stream), "event");
+  p.launches += launch_finish(s->G.view(), s->H.view(),
+                              p.n_del > 0 ? s->S.pool_top_ptr() : nullptr, b, s->stream);
+  check(cudaEventRecord(s->t_total.b, s->stream), "event");
+  check(cudaMemcpyAsync(&c, b.ctl, sizeof c, cudaMemcpyDeviceToHost, s->stream), "ctl download");
+  if (p.nb == 1)
+    check(cudaMemcpyAsync(&s->h_counts[2], b.dec, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                          s->stream), "decision download");
+  check(cudaStreamSynchronize(s->stream), "batch");
+  s->stats.d2h_bytes += sizeof c;
+  s->stats.kernel_launches += p.launches;
+  s->stats.batches += 1;
+  if (c.val_err != ~0ull) fail_validation(s, p, c.val_err);
+  // Commit-side state is now final for events < limit.
+  s->g_edges = c.g_edges;
+  s->h_edges = c.h_edges;
+  s->g_top = c.g_pool_top;
+  s->h_top = c.h_pool_top;
+  uint64_t fail_k = ~0ull;
+  uint32_t fail_code = 0;
+  if (c.commit_err != ~0ull) {
+    fail_k = c.commit_err >> 8;
+    fail_code = static_cast<uint32_t>(c.commit_err & 0xFF);
+  }
+  if (c.use_absent_limit && c.first_absent != 0xFFFFFFFFu && c.first_absent < fail_k) {
+    fail_k = c.first_absent;
+    fail_code = kErrAbsent;
+  }
+  s->stats.reach_steps += c.reach.steps;
+  s->stats.reach_row_bytes += c.reach.row_bytes;
+  s->stats.minpath_steps += c.minpath.steps;
+  s->stats.minpath_row_bytes += c.minpath.row_bytes;
+  s->stats.reach_queries += c.nq_reach;
+  s->stats.minpath_queries += c.nq_min;
+  s->stats.commit_rounds += c.rounds;
+  s->stats.reach_ms += s->t_reach.ms();
+  s->stats.minpath_ms += s->t_min.ms();
+  s->stats.commit_ms += s->t_commit.ms();
+  s->stats.total_ms += s->t_total.ms();
+  if (fail_k != ~0ull) {
+    s->counter += fail_k + 1;  // ++update_counter_ precedes the throw (:469)
+    const uint64_t pos = p.pos ? p.pos[fail_k] : fail_k;
+    fail(fail_code == kErrPool ? DYG_ERR_DEVICE : DYG_ERR_DATA,
+         event_error_message(fail_code, pos, p.host[fail_k]));
+  }
+  s->counter += p.nb;
+  s->last_dec = p.nb == 1 ? s->h_counts[2] : 0;
+  dyg_batch_report rep{};
+  rep.batch_index = p.batch;
+  rep.insertions_seen = c.report[kInsSeen];
+  rep.insertions_kept = c.report[kInsKept];
+  rep.insertions_pruned = c.report[kInsPruned];
+  rep.deletions_seen = c.report[kDelSeen];
+  rep.deletions_in_sparsifier = c.report[kDelInH];
+  rep.paths_recovered = c.report[kPaths];
+  rep.edges_recovered = c.report[kEdgesRec];
+  rep.fallback_activations = c.report[kFallbacks];
+  rep.walker_steps = c.report[kWalkerSteps];
+  rep.max_event_steps = c.report[kMaxEventSteps];
+  rep.density_graph = density_of(s->g_edges, s->n);
+  rep.density_sparsifier = density_of(s->h_edges, s->n);
+  rep.wall_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - p.wall0).count();
+  *out = rep;
+}
+
+void empty_report(dyg_session* s, uint32_t batch_index, dyg_batch_report* out) {
+  dyg_batch_report rep{};
+  rep.batch_index = batch_index;
+  rep.density_graph = density_of(s->g_edges, s->n);
+  rep.density_sparsifier = density_of(s->h_edges, s->n);
+  *out = rep;
+}
+
+void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* host_events,
+                  const uint64_t* positions, uint32_t nb, uint32_t n_ins, uint32_t n_del,
+                  uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs) {
+  if (nb == 0) {
+    empty_report(s, batch_index, out);
+    return;
+  }
+  Pending p;
+  p.wall0 = std::chrono::steady_clock::now();
+  p.dev = dev_events;
+  p.host = host_events;
+  p.pos = positions;
+  p.nb = nb;
+  p.n_ins = n_ins;
+  p.n_del = n_del;
+  p.batch = batch_index;
+  p.imm_msgs = immediate_msgs;
+  phase_prepare(s, p);
+  phase_walk(s, p, true, 0, 0, 0, 0);
+  phase_commit(s, p, out);
+}
+
+// Host events -> pinned staging -> device, then the deferred pipeline.
+void run_host_batch(dyg_session* s, const dyg_event* ev, const uint64_t* positions, size_t nb,
+                    uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs) {
+  uint32_t n_ins = 0, n_del = 0;
+  for (size_t i = 0; i < nb; ++i) (ev[i].kind == 0 ? n_ins : n_del)++;
+  ensure_batch(s, static_cast<uint32_t>(nb), n_del);
+  static_assert(sizeof(DevEvent) == sizeof(dyg_event), "event layout");
+  std::memcpy(s->h_events_pinned, ev, sizeof(DevEvent) * nb);
+  if (nb) {
+    check(cudaMemcpyAsync(s->d_events, s->h_events_pinned, sizeof(DevEvent) * nb,
+                          cudaMemcpyHostToDevice, s->stream), "events upload");
+    s->stats.h2d_bytes += sizeof(DevEvent) * nb;
+  }
+  run_deferred(s, s->d_events, reinterpret_cast<const DevEvent*>(ev), positions,
+               static_cast<uint32_t>(nb), n_ins, n_del, batch_index, out, immediate_msgs);
+}
+
+void accumulate(dyg_batch_report& acc, const dyg_batch_report& r) {
+  acc.insertions_seen += r.insertions_seen;
+  acc.insertions_kept += r.insertions_kept;
+  acc.insertions_pruned += r.insertions_pruned;
+  acc.deletions_seen += r.deletions_seen;
+  acc.deletions_in_sparsifier += r.deletions_in_sparsifier;
+  acc.paths_recovered += r.paths_recovered;
+  acc.edges_recovered += r.edges_recovered;
+  acc.fallback_activations += r.fallback_activations;
+  acc.walker_steps += r.walker_steps;
+  acc.max_event_steps = std::max(acc.max_event_steps, r.max_event_steps);
+}
+
+// replay_batch_immediate (sparsifier.cpp:347-393) as 1-event deferred
+// batches (identical decisions).
+void run_immediate(dyg_session* s, const dyg_event* ev, const uint64_t* positions, size_t nb,
+                   uint32_t batch_index, dyg_batch_report* out) {
+  const auto wall0 = std::chrono::steady_clock::now();
+  dyg_batch_report acc{};
+  acc.batch_index = batch_index;
+  for (size_t i = 0; i < nb; ++i) {
+    dyg_batch_report r{};
+    const uint64_t pos = positions ? positions[i] : i;
+    run_host_batch(s, ev + i, &pos, 1, batch_index, &r, true);
+    accumulate(acc, r);
+  }
+  acc.density_graph = density_of(s->g_edges, s->n);
+  acc.density_sparsifier = density_of(s->h_edges, s->n);
+  acc.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+  *out = acc;
+}
+
+void check_csr(const dyg_csr* c, const char* what) {
+  if (c == nullptr || c->row_ptr == nullptr) fail(DYG_ERR_USAGE, std::string(what) + " is null");
+  if (c->n == 0) fail(DYG_ERR_USAGE, "graph must have at least one vertex");  // graph.cpp:9-13
+  const uint64_t nnz = c->row_ptr[c->n];
+  if (nnz && (c->ids == nullptr || c->w == nullptr))
+    fail(DYG_ERR_USAGE, std::string(what) + " has null row arrays");
+}
+
+bool csr_has_edge(const dyg_csr* c, uint32_t u, uint32_t v) {
+  for (uint64_t i = c->row_ptr[u]; i < c->row_ptr[u + 1]; ++i)
+    if (c->ids[i] == v) return true;
+  return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dyg_last_error(void) { return g_last_error.c_str(); }
+
+const char* dyg_version(void) {
+  return "dyg-b200 0.1 (sm_100a; slabs H64B/G128B; fmad=false)";
+}
+
+int dyg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* options,
+                       int device, dyg_session** out) {
+  return guarded([&] {
+    if (out == nullptr || options == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    *out = nullptr;
+    check_csr(g, "graph");
+    check_csr(h, "sparsifier");
+    // sparsifier.cpp:183-203
+    if (g->n != h->n) fail(DYG_ERR_USAGE, "graph and sparsifier must share a vertex set");
+    const dyg_walk_config& w = options->walk;
+    if (w.distortion_threshold < 0.0 || w.step_cap == 0 || w.walker_count == 0)
+      fail(DYG_ERR_USAGE, "invalid walk configuration");
+    for (uint32_t u = 0; u < h->n; ++u) {
+      for (uint64_t i = h->row_ptr[u]; i < h->row_ptr[u + 1]; ++i) {
+        const uint32_t v = h->ids[i];
+        if (u < v && !csr_has_edge(g, u, v)) {
+          char buf[160];
+          std::snprintf(buf, sizeof buf, "sparsifier edge (%u, %u) missing from the graph", u, v);
+          fail(DYG_ERR_DATA, buf);
+        }
+      }
+    }
+    if (dyg_device_count() == 0) fail(DYG_ERR_DEVICE, "no CUDA device visible");
+    auto* s = new dyg_session();
+    try {
+      s->device = device;
+      check(cudaSetDevice(device), "set device");
+      check(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
+      s->opt = *options;
+      s->n = g->n;
+      s->debug_sync = std::getenv("DYG_DEBUG_SYNC") != nullptr;
+      s->G.upload(g->n, g->row_ptr, g->ids, g->w, s->stream);
+      s->H.upload(h->n, h->row_ptr, h->ids, h->w, s->stream);
+      s->g_edges = g->row_ptr[g->n] / 2;
+      s->h_edges = h->row_ptr[h->n] / 2;
+      s->g_top = 0;
+      s->h_top = 0;
+      // pool_top after build: read once (setup).
+      unsigned long long tops[2];
+      check(cudaMemcpy(&tops[0], s->G.pool_top_ptr(), 8, cudaMemcpyDeviceToHost), "top");
+      check(cudaMemcpy(&tops[1], s->H.pool_top_ptr(), 8, cudaMemcpyDeviceToHost), "top");
+      s->g_top = tops[0];
+      s->h_top = tops[1];
+      dev_alloc(&s->d_locks, s->n, "row locks");
+      check(cudaMemset(s->d_locks, 0, sizeof(unsigned long long) * s->n), "locks");
+      dev_alloc(&s->d_round, 1, "round counter");
+      check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
+      dev_alloc(&s->b.ctl, 1, "batch ctl");
+      dev_alloc(&s->d_counts, 2, "shard counts");
+      check(cudaMallocHost(reinterpret_cast<void**>(&s->h_counts), 4 * sizeof(uint32_t)),
+            "pinned counts");
+      check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctl), sizeof(BatchCtl)), "pinned ctl");
+      s->coop_blocks = coop_grid_blocks(device);
+      s->t_total.init();
+      s->t_reach.init();
+      s->t_min.init();
+      s->t_commit.init();
+      ensure_batch(s, 1024, 256);
+    } catch (...) {
+      dyg_session_destroy(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void dyg_session_destroy(dyg_session* s) {
+  if (s == nullptr) return;
+  cudaSetDevice(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  free_batch(s);
+  dev_free(s->b.mout.has_path);
+  dev_free(s->b.mout.path_len);
+  dev_free(s->b.mout.steps);
+  dev_free(s->b.mout.resistance);
+  dev_free(s->b.mout.paths);
+  dev_free(s->b.mscratch.acc);
+  dev_free(s->b.mscratch.term);
+  dev_free(s->b.mscratch.steps);
+  dev_free(s->b.mscratch.paths);
+  dev_free(s->b.mscratch.rvals);
+  dev_free(s->b.ctl);
+  dev_free(s->d_locks);
+  dev_free(s->d_round);
+  dev_free(s->d_stream);
+  if (s->h_ctl) cudaFreeHost(s->h_ctl);
+  if (s->h_counts) cudaFreeHost(s->h_counts);
+  dev_free(s->d_counts);
+  s->t_total.destroy();
+  s->t_reach.destroy();
+  s->t_min.destroy();
+  s->t_commit.destroy();
+  s->G.release();
+  s->S.release();
+  s->G_snap.release();
+  s->H.release();
+  s->H_snap.release();
+  if (s->stream && s->own_stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* positions,
+                      size_t n, uint32_t batch_index, dyg_batch_report* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr || (n && events == nullptr))
+      fail(DYG_ERR_USAGE, "null argument");
+    check(cudaSetDevice(s->device), "set device");
+    if (n > 0xFFFFFFF0ull) fail(DYG_ERR_USAGE, "batch too large");
+    if (s->opt.batched) {
+      run_host_batch(s, events, positions, n, batch_index, out, false);
+    } else {
+      run_immediate(s, events, positions, n, batch_index, out);
+    }
+  });
+}
+
+int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
+                     uint32_t batch_count, uint32_t batch_index, dyg_batch_report* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr || (n_events && events == nullptr))
+      fail(DYG_ERR_USAGE, "null argument");
+    // sparsifier.cpp:541-548
+    if (batch_index >= batch_count && batch_count > 0) fail(DYG_ERR_USAGE, "batch index out of range");
+    std::vector<dyg_event> sel;
+    std::vector<uint64_t> pos;
+    for (size_t i = 0; i < n_events; ++i) {
+      if (events[i].batch_index == batch_index) {
+        sel.push_back(events[i]);
+        pos.push_back(i);
+      }
+    }
+    check(cudaSetDevice(s->device), "set device");
+    if (s->opt.batched) {
+      run_host_batch(s, sel.data(), pos.data(), sel.size(), batch_index, out, false);
+    } else {
+      run_immediate(s, sel.data(), pos.data(), sel.size(), batch_index, out);
+    }
+  });
+}
+
+int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
+                      uint32_t batch_count) {
+  return guarded([&] {
+    if (s == nullptr || (n_events && events == nullptr)) fail(DYG_ERR_USAGE, "null argument");
+    check(cudaSetDevice(s->device), "set device");
+    uint32_t nbatches = batch_count;
+    for (size_t i = 0; i < n_events; ++i) nbatches = std::max(nbatches, events[i].batch_index + 1);
+    s->batch_cnt.assign(nbatches, 0);
+    s->batch_ins.assign(nbatches, 0);
+    s->batch_del.assign(nbatches, 0);
+    for (size_t i = 0; i < n_events; ++i) {
+      s->batch_cnt[events[i].batch_index]++;
+      (events[i].kind == 0 ? s->batch_ins : s->batch_del)[events[i].batch_index]++;
+    }
+    s->batch_off.assign(nbatches + 1, 0);
+    for (uint32_t b = 0; b < nbatches; ++b) s->batch_off[b + 1] = s->batch_off[b] + s->batch_cnt[b];
+    s->stream_events.resize(n_events);
+    s->stream_positions.resize(n_events);
+    std::vector<uint64_t> fill(s->batch_off.begin(), s->batch_off.end() - 1);
+    for (size_t i = 0; i < n_events; ++i) {
+      const uint64_t at = fill[events[i].batch_index]++;
+      s->stream_events[at] = events[i];
+      s->stream_positions[at] = i;
+    }
+    dev_free(s->d_stream);
+    dev_alloc(&s->d_stream, n_events, "stream");
+    if (n_events)
+      check(cudaMemcpy(s->d_stream, s->stream_events.data(), sizeof(DevEvent) * n_events,
+                       cudaMemcpyHostToDevice), "stream upload");
+    s->stream_batches = batch_count;
+    s->have_stream = true;
+  });
+}
+
+int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    if (!s->have_stream) fail(DYG_ERR_USAGE, "no stream uploaded");
+    if (batch_index >= s->stream_batches && s->stream_batches > 0)
+      fail(DYG_ERR_USAGE, "batch index out of range");
+    check(cudaSetDevice(s->device), "set device");
+    if (batch_index >= s->batch_cnt.size()) {
+      run_deferred(s, nullptr, nullptr, nullptr, 0, 0, 0, batch_index, out, false);
+      return;
+    }
+    const uint64_t off = s->batch_off[batch_index];
+    const uint32_t nb = static_cast<uint32_t>(s->batch_cnt[batch_index]);
+    if (!s->opt.batched) {
+      run_immediate(s, s->stream_events.data() + off, s->stream_positions.data() + off, nb,
+                    batch_index, out);
+      return;
+    }
+    run_deferred(s, s->d_stream + off,
+                 reinterpret_cast<const DevEvent*>(s->stream_events.data() + off),
+                 s->stream_positions.data() + off, nb,
+                 static_cast<uint32_t>(s->batch_ins[batch_index]),
+                 static_cast<uint32_t>(s->batch_del[batch_index]), batch_index, out, false);
+  });
+}
+
+int dyg_apply_insertion(dyg_session* s, uint32_t u, uint32_t v, double w, int* decision) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    check(cudaSetDevice(s->device), "set device");
+    // apply_insertion validates through insert_edge (graph.cpp:64-73).
+    if (u >= s->n || v >= s->n) {
+      char buf[128];
+      std::snprintf(buf, sizeof buf, "vertex id %u out of range (n = %u)", u >= s->n ? u : v, s->n);
+      fail(DYG_ERR_USAGE, buf);
+    }
+    if (u == v) fail(DYG_ERR_USAGE, "self-loops are not allowed");
+    if (!(w > 0.0) || !std::isfinite(w)) fail(DYG_ERR_USAGE, "edge weight must be a positive finite number");
+    dyg_event e{0, u, v, 0, w};
+    dyg_batch_report r{};
+    const uint64_t pos = 0;
+    run_host_batch(s, &e, &pos, 1, 0, &r, false);
+    s->last_event_steps = r.walker_steps;
+    if (decision) *decision = static_cast<int>(s->last_dec & 0xFF);
+  });
+}
+
+int dyg_apply_deletion(dyg_session* s, uint32_t u, uint32_t v, int* kind, uint32_t* edges_added) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    check(cudaSetDevice(s->device), "set device");
+    if (u >= s->n || v >= s->n) {
+      char buf[128];
+      std::snprintf(buf, sizeof buf, "vertex id %u out of range (n = %u)", u >= s->n ? u : v, s->n);
+      fail(DYG_ERR_USAGE, buf);
+    }
+    dyg_event e{1, u, v, 0, 0.0};
+    dyg_batch_report r{};
+    const uint64_t pos = 0;
+    try {
+      run_host_batch(s, &e, &pos, 1, 0, &r, false);
+    } catch (const ApiError& err) {
+      // delete_edge's own message without the replay prefix (graph.cpp:90-95).
+      if (err.code == DYG_ERR_DATA) {
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "edge (%u, %u) does not exist", u, v);
+        fail(DYG_ERR_DATA, buf);
+      }
+      throw;
+    }
+    s->last_event_steps = r.walker_steps;
+    if (kind) *kind = static_cast<int>(s->last_dec & 0xFF);
+    if (edges_added) *edges_added = s->last_dec >> 8;
+  });
+}
+
+uint64_t dyg_last_event_steps(const dyg_session* s) { return s ? s->last_event_steps : 0; }
+uint64_t dyg_update_counter(const dyg_session* s) { return s ? s->counter : 0; }
+
+int dyg_graph_info(const dyg_session* s, int which, uint32_t* n, uint64_t* edges, double* density) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    const uint64_t e = which == 0 ? s->g_edges : s->h_edges;
+    if (n) *n = s->n;
+    if (edges) *edges = e;
+    if (density) *density = density_of(e, s->n);
+  });
+}
+
+int dyg_export_rows(dyg_session* s, int which, uint64_t* row_ptr, uint32_t* ids, double* w,
+                    uint64_t capacity) {
+  return guarded([&] {
+    if (s == nullptr || row_ptr == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    check(cudaSetDevice(s->device), "set device");
+    const uint64_t nnz = which == 0 ? s->G.export_rows(row_ptr, ids, w, capacity, s->stream)
+                                    : s->H.export_rows(row_ptr, ids, w, capacity, s->stream);
+    if (nnz > capacity) fail(DYG_ERR_USAGE, "export buffers too small");
+  });
+}
+
+int dyg_session_snapshot(dyg_session* s) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    check(cudaSetDevice(s->device), "set device");
+    s->G_snap.copy_from(s->G, s->stream);
+    s->H_snap.copy_from(s->H, s->stream);
+    check(cudaStreamSynchronize(s->stream), "snapshot");
+    s->counter_snap = s->counter;
+    s->g_edges_snap = s->g_edges;
+    s->h_edges_snap = s->h_edges;
+    s->g_top_snap = s->g_top;
+    s->h_top_snap = s->h_top;
+    s->have_snap = true;
+  });
+}
+
+int dyg_session_restore(dyg_session* s) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    if (!s->have_snap) fail(DYG_ERR_USAGE, "no snapshot taken");
+    check(cudaSetDevice(s->device), "set device");
+    s->G.copy_from(s->G_snap, s->stream);
+    s->H.copy_from(s->H_snap, s->stream);
+    s->stats.kernel_launches += 2;
+    s->counter = s->counter_snap;
+    s->g_edges = s->g_edges_snap;
+    s->h_edges = s->h_edges_snap;
+    s->g_top = s->g_top_snap;
+    s->h_top = s->h_top_snap;
+    if (s->debug_sync) check(cudaStreamSynchronize(s->stream), "restore");
+  });
+}
+
+int dyg_session_stats(const dyg_session* s, dyg_stats* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    *out = s->stats;
+    out->pool_used = s->g_top + s->h_top;
+    out->pool_capacity = s->G.pool_capacity() + s->H.pool_capacity();
+  });
+}
+
+int dyg_session_reset_stats(dyg_session* s) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    s->stats = dyg_stats{};
+  });
+}
+
+int dyg_set_stream(dyg_session* s, void* cuda_stream) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    check(cudaStreamSynchronize(s->stream), "set stream");
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    s->stream = static_cast<cudaStream_t>(cuda_stream);
+    s->own_stream = false;
+  });
+}
+
+// ---- multi-GPU split ---------------------------------------
+int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* positions, size_t n,
+                    uint32_t batch_index, uint64_t* n_reach, uint64_t* n_minpath) {
+  return guarded([&] {
+    if (s == nullptr || (n && events == nullptr)) fail(DYG_ERR_USAGE, "null argument");
+    if (!s->opt.batched) fail(DYG_ERR_USAGE, "the multi-GPU split needs batched (deferred) mode");
+    check(cudaSetDevice(s->device), "set device");
+    s->shard_active = false;
+    s->shard_host.assign(reinterpret_cast<const DevEvent*>(events),
+                         reinterpret_cast<const DevEvent*>(events) + n);
+    s->shard_pos.resize(n);
+    for (size_t i = 0; i < n; ++i) s->shard_pos[i] = positions ? positions[i] : i;
+    uint32_t n_ins = 0, n_del = 0;
+    for (size_t i = 0; i < n; ++i) (events[i].kind == 0 ? n_ins : n_del)++;
+    s->shard_nb = static_cast<uint32_t>(n);
+    s->shard_ins = n_ins;
+    s->shard_del = n_del;
+    s->shard_batch = batch_index;
+    s->shard_wall0 = std::chrono::steady_clock::now();
+    s->shard_nq_r = s->shard_nq_m = 0;
+    if (n > 0) {
+      ensure_batch(s, static_cast<uint32_t>(n), n_del);
+      std::memcpy(s->h_events_pinned, events, sizeof(DevEvent) * n);
+      check(cudaMemcpyAsync(s->d_events, s->h_events_pinned, sizeof(DevEvent) * n,
+                            cudaMemcpyHostToDevice, s->stream), "events upload");
+      s->stats.h2d_bytes += sizeof(DevEvent) * n;
+      Pending p;
+      p.dev = s->d_events;
+      p.host = s->shard_host.data();
+      p.pos = s->shard_pos.data();
+      p.nb = s->shard_nb;
+      p.n_ins = n_ins;
+      p.n_del = n_del;
+      p.batch = batch_index;
+      phase_prepare(s, p);
+      BatchCtl& c = *s->h_ctl;
+      check(cudaMemcpyAsync(&c, s->b.ctl, sizeof c, cudaMemcpyDeviceToHost, s->stream), "ctl");
+      check(cudaStreamSynchronize(s->stream), "shard prepare");
+      s->shard_launches = p.launches;
+      if (c.val_err != ~0ull) fail_validation(s, p, c.val_err);
+      s->shard_nq_r = c.nq_reach;
+      s->shard_nq_m = c.nq_min;
+    }
+    s->shard_active = true;
+    if (n_reach) *n_reach = s->shard_nq_r;
+    if (n_minpath) *n_minpath = s->shard_nq_m;
+  });
+}
+
+size_t dyg_shard_record_bytes(const dyg_session* s, int minpath) {
+  if (s == nullptr) return 0;
+  return minpath ? min_record_bytes(s->opt.walk.step_cap) : sizeof(ReachRecord);
+}
+
+int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
+                   void* minpath_records) {
+  return guarded([&] {
+    if (s == nullptr || !s->shard_active) fail(DYG_ERR_USAGE, "no shard batch in progress");
+    if (world < 1 || rank < 0 || rank >= world) fail(DYG_ERR_USAGE, "invalid rank / world");
+    check(cudaSetDevice(s->device), "set device");
+    if (s->shard_nb == 0) return;
+    auto range = [&](uint32_t nq, uint32_t* lo, uint32_t* cnt, uint32_t* slots) {
+      const uint64_t a = static_cast<uint64_t>(nq) * rank / world;
+      const uint64_t b = static_cast<uint64_t>(nq) * (rank + 1) / world;
+      *lo = static_cast<uint32_t>(a);
+      *cnt = static_cast<uint32_t>(b - a);
+      *slots = static_cast<uint32_t>((static_cast<uint64_t>(nq) + world - 1) / world);
+    };
+    uint32_t lo_r, n_r, sl_r, lo_m, n_m, sl_m;
+    range(s->shard_nq_r, &lo_r, &n_r, &sl_r);
+    range(s->shard_nq_m, &lo_m, &n_m, &sl_m);
+    if ((sl_r && reach_records == nullptr) || (sl_m && minpath_records == nullptr))
+      fail(DYG_ERR_USAGE, "null record buffer");
+    Pending p;
+    p.nb = s->shard_nb;
+    p.n_ins = s->shard_ins;
+    p.n_del = s->shard_del;
+    phase_walk(s, p, false, lo_r, n_r, lo_m, n_m);
+    p.launches += launch_pack(s->b, lo_r, n_r, lo_m, n_m, sl_r, sl_m, s->opt.walk.step_cap,
+                              reach_records, minpath_records, s->stream);
+    check(cudaStreamSynchronize(s->stream), "shard walk");
+    s->shard_launches += p.launches;
+  });
+}
+
+int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
+                     const void* minpath_gathered, dyg_batch_report* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr || !s->shard_active)
+      fail(DYG_ERR_USAGE, "no shard batch in progress");
+    if (world < 1) fail(DYG_ERR_USAGE, "invalid world");
+    check(cudaSetDevice(s->device), "set device");
+    s->shard_active = false;
+    if (s->shard_nb == 0) {
+      empty_report(s, s->shard_batch, out);
+      return;
+    }
+    const uint32_t sl_r = static_cast<uint32_t>((s->shard_nq_r + world - 1ull) / world);
+    const uint32_t sl_m = static_cast<uint32_t>((s->shard_nq_m + world - 1ull) / world);
+    Pending p;
+    p.dev = s->d_events;
+    p.host = s->shard_host.data();
+    p.pos = s->shard_pos.data();
+    p.nb = s->shard_nb;
+    p.n_ins = s->shard_ins;
+    p.n_del = s->shard_del;
+    p.batch = s->shard_batch;
+    p.wall0 = s->shard_wall0;
+    p.launches = s->shard_launches;
+    p.launches += launch_unpack(s->b, s->shard_nq_r, s->shard_nq_m, world, sl_r, sl_m,
+                                s->opt.walk.step_cap, reach_gathered, minpath_gathered, s->stream);
+    phase_commit(s, p, out);
+  });
+}
+
+// ---- stateless run_batch twin (walk.hpp:86-92) ----------------------------
+int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_queries,
+                  const dyg_walk_config* cfg, dyg_walk_result* out, uint32_t* path_buf,
+                  int device) {
+  return guarded([&] {
+    if (cfg == nullptr || (n_queries && (queries == nullptr || out == nullptr)))
+      fail(DYG_ERR_USAGE, "null argument");
+    check_csr(g, "graph");
+    // single_walk's usage checks (walk.cpp:43-48), first failing query.
+    for (size_t i = 0; i < n_queries; ++i) {
+      const dyg_walk_query& q = queries[i];
+      if (q.p == q.q) fail(DYG_ERR_USAGE, "walk endpoints must differ");
+      if (q.p >= g->n) {
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "vertex id %u out of range (n = %u)", q.p, g->n);
+        fail(DYG_ERR_USAGE, buf);
+      }
+      if (g->row_ptr[q.p + 1] == g->row_ptr[q.p]) fail(DYG_ERR_USAGE, "walk started at an isolated vertex");
+    }
+    if (n_queries == 0) return;
+    if (dyg_device_count() == 0) fail(DYG_ERR_DEVICE, "no CUDA device visible");
+    check(cudaSetDevice(device), "set device");
+    cudaStream_t st;
+    check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    std::vector<ReachQuery> rq;
+    std::vector<MinQuery> mq;
+    std::vector<size_t> ri, mi;
+    for (size_t i = 0; i < n_queries; ++i) {
+      const dyg_walk_query& q = queries[i];
+      if (q.kind == 0) {
+        rq.push_back(ReachQuery{q.p, q.q, q.w_pq, q.update_id});
+        ri.push_back(i);
+      } else {
+        mq.push_back(MinQuery{q.p, q.q, q.update_id});
+        mi.push_back(i);
+      }
+    }
+    const WalkParams P{cfg->distortion_threshold, cfg->step_cap, cfg->walker_count,
+                       cfg->global_seed};
+    const uint64_t T1 = static_cast<uint64_t>(cfg->step_cap) + 1;
+    WalkCounters* ctr = nullptr;
+    uint32_t* d_n = nullptr;
+    dev_alloc(&ctr, 2, "counters");
+    dev_alloc(&d_n, 2, "counts");
+    const uint32_t counts[2] = {static_cast<uint32_t>(rq.size()), static_cast<uint32_t>(mq.size())};
+    check(cudaMemcpy(d_n, counts, sizeof counts, cudaMemcpyHostToDevice), "counts");
+    check(cudaMemset(ctr, 0, 2 * sizeof(WalkCounters)), "counters");
+    if (!rq.empty()) {
+      GraphStore<kCapH> gh;
+      gh.upload(g->n, g->row_ptr, g->ids, g->w, st);
+      ReachQuery* d_q = nullptr;
+      ReachOut ro{};
+      dev_alloc(&d_q, rq.size(), "queries");
+      dev_alloc(&ro.reached, rq.size(), "out");
+      dev_alloc(&ro.steps, rq.size(), "out");
+      dev_alloc(&ro.best_bits, rq.size(), "out");
+      check(cudaMemcpy(d_q, rq.data(), sizeof(ReachQuery) * rq.size(), cudaMemcpyHostToDevice), "q");
+      launch_reach(gh.view(), d_q, d_n, counts[0], P, ro, ctr, st);
+      check(cudaGetLastError(), "reach launch");
+      check(cudaStreamSynchronize(st), "reach");
+      std::vector<uint32_t> reached(rq.size());
+      std::vector<unsigned long long> steps(rq.size()), best(rq.size());
+      check(cudaMemcpy(reached.data(), ro.reached, 4 * rq.size(), cudaMemcpyDeviceToHost), "out");
+      check(cudaMemcpy(steps.data(), ro.steps, 8 * rq.size(), cudaMemcpyDeviceToHost), "out");
+      check(cudaMemcpy(best.data(), ro.best_bits, 8 * rq.size(), cudaMemcpyDeviceToHost), "out");
+      for (size_t j = 0; j < rq.size(); ++j) {
+        dyg_walk_result& r = out[ri[j]];
+        r = dyg_walk_result{};
+        r.reached = reached[j];
+        r.steps_used = steps[j];
+        if (reached[j]) std::memcpy(&r.best_estimate, &best[j], 8);
+      }
+      cudaFree(d_q);
+      cudaFree(ro.reached);
+      cudaFree(ro.steps);
+      cudaFree(ro.best_bits);
+    }
+    if (!mq.empty()) {
+      GraphStore<kCapG> gg;
+      gg.upload(g->n, g->row_ptr, g->ids, g->w, st);
+      const size_t nm = mq.size();
+      const uint64_t sw = cfg->walker_count;
+      MinQuery* d_q = nullptr;
+      MinOut mo{};
+      MinScratch sc{};
+      dev_alloc(&d_q, nm, "queries");
+      dev_alloc(&mo.has_path, nm, "out");
+      dev_alloc(&mo.path_len, nm, "out");
+      dev_alloc(&mo.steps, nm, "out");
+      dev_alloc(&mo.resistance, nm, "out");
+      dev_alloc(&mo.paths, nm * T1, "out");
+      dev_alloc(&sc.acc, nm * sw, "scratch");
+      dev_alloc(&sc.term, nm * sw, "scratch");
+      dev_alloc(&sc.steps, nm * sw, "scratch");
+      dev_alloc(&sc.paths, nm * sw * T1, "scratch");
+      dev_alloc(&sc.rvals, nm * T1, "scratch");
+      check(cudaMemcpy(d_q, mq.data(), sizeof(MinQuery) * nm, cudaMemcpyHostToDevice), "q");
+      launch_minpath(gg.view(), d_q, d_n + 1, counts[1], P, sc, mo, ctr + 1, st);
+      check(cudaGetLastError(), "minpath launch");
+      check(cudaStreamSynchronize(st), "minpath");
+      std::vector<uint32_t> has(nm), len(nm), paths(nm * T1);
+      std::vector<unsigned long long> steps(nm);
+      std::vector<double> res(nm);
+      check(cudaMemcpy(has.data(), mo.has_path, 4 * nm, cudaMemcpyDeviceToHost), "out");
+      check(cudaMemcpy(len.data(), mo.path_len, 4 * nm, cudaMemcpyDeviceToHost), "out");
+      check(cudaMemcpy(steps.data(), mo.steps, 8 * nm, cudaMemcpyDeviceToHost), "out");
+      check(cudaMemcpy(res.data(), mo.resistance, 8 * nm, cudaMemcpyDeviceToHost), "out");
+      check(cudaMemcpy(paths.data(), mo.paths, 4 * nm * T1, cudaMemcpyDeviceToHost), "out");
+      for (size_t j = 0; j < nm; ++j) {
+        dyg_walk_result& r = out[mi[j]];
+        r = dyg_walk_result{};
+        r.reached = has[j];
+        r.steps_used = steps[j];
+        if (has[j]) {
+          r.path_len = len[j];
+          r.resistance = res[j];
+          if (path_buf)
+            std::memcpy(path_buf + mi[j] * T1, paths.data() + j * T1, 4ull * len[j]);
+        }
+      }
+      cudaFree(d_q);
+      cudaFree(mo.has_path);
+      cudaFree(mo.path_len);
+      cudaFree(mo.steps);
+      cudaFree(mo.resistance);
+      cudaFree(mo.paths);
+      cudaFree(sc.acc);
+      cudaFree(sc.term);
+      cudaFree(sc.steps);
+      cudaFree(sc.paths);
+      cudaFree(sc.rvals);
+    }
+    cudaFree(ctr);
+    cudaFree(d_n);
+    cudaStreamDestroy(st);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// walk.cuh -- localized non-backtracking random walks on device rows.
+//
+// Bit-exact restatement of the reference walk engine
+// (proj/src/walk.cpp:17-145) as SIMT lanes: one lane per walker, the s
+// walkers of a query on s consecutive lanes. The RNG is the reference's own
+// SplitMix64 stream in counter form, so a lane
+// needs no generator state; fp64 sums run sequentially in row order with
+// explicit _rn intrinsics (no FMA contraction).
+#pragma once
+
+#include "dyg_internal.cuh"
+
+namespace dyg {
+
+enum Terminal : uint32_t { kReached = 0, kBudget = 1, kStepCap = 2, kDeadEnd = 3 };  // walk.hpp:20
+
+struct WalkParams {
+  double K;        // distortion threshold (budget)
+  uint32_t T;      // step cap
+  uint32_t s;      // walkers per query
+  uint64_t seed;   // global seed
+};
+
+struct ReachQuery {   // WalkQuery Reach (walk.hpp:71-78)
+  uint32_t p, q;
+  double w_pq;
+  uint64_t update_id;
+};
+struct MinQuery {     // WalkQuery MinPath
+  uint32_t p, q;
+  uint64_t update_id;
+};
+
+// Per-query outputs of the reach walk (ReachVerdict, walk.hpp:29-33).
+struct ReachOut {
+  uint32_t* reached;
+  unsigned long long* steps;
+  unsigned long long* best_bits;  // f64 bits of best_estimate
+};
+// Per-query outputs of the min-path walk (RecoveredPath, walk.hpp:35-39).
+struct MinOut {
+  uint32_t* has_path;
+  uint32_t* path_len;
+  unsigned long long* steps;
+  double* resistance;
+  uint32_t* paths;     // [q*(T+1)] loop-erased vertices
+};
+// Per-walker scratch of the min-path walk.
+struct MinScratch {
+  double* acc;
+  uint32_t* term;
+  uint32_t* steps;
+  uint32_t* paths;     // [(q*s+i)*(T+1)] raw traces
+  double* rvals;       // [q*(T+1)] per-edge 1/w for the resistance sum
+};
+
+// Walk-phase counters (device), for the roofline accounting.
+struct WalkCounters {
+  unsigned long long steps;
+  unsigned long long row_bytes;
+};
+
+// Host launchers (walk.cu). nq_dev: device count of queries (nq_max bounds
+// the launch). stream: session stream. Each returns the number of kernels
+// launched.
+template <int C>
+int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
+                 uint32_t nq_max, const WalkParams& P, ReachOut out,
+                 WalkCounters* ctr, cudaStream_t st);
+template <int C>
+int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_dev,
+                   uint32_t nq_max, const WalkParams& P, MinScratch scratch, MinOut out,
+                   WalkCounters* ctr, cudaStream_t st);
+
+}  // namespace dyg
