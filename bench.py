@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark: dyGRASS batched incremental + decremental update on B200.
+
+Workload (BASELINE.json metric, configs[4]): the
+delaunay_n22-shaped mesh make_mesh(2048, 2048, seed 1) -- 4.19M vertices,
+12.57M edges -- with the initial sparsifier at 10% off-tree density and the
+generated 10 insertion + 10 deletion batch stream (1,048,576 insertions,
+125,747 deletions; K=100, T=100, s=16, walk seed 42). Synthetic data from the
+reference's own deterministic generators (no network datasets).
+
+A step = restore (G0, H0, counter 0) from the device snapshot + replay of all
+20 batches through the reference-shaped API. value = edge updates per second
+over the timed steps (device timeline, CUDA events on the session stream);
+e2e = the same through the C-ABI with host event buffers (H2D of every
+batch's events and D2H of every batch report inside the timed region).
+
+--impl reference times the reference CPU implementation (oracle/_ref: the
+unmodified /root/reference sources) on the host's cores, one batch per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (rows, cols, generator, insert_fraction, delete_fraction, locality)
+    "C1": (100, 100, "mesh", 0.25, 0.0, 3),
+    "C2": (100, 110, "mesh", 0.25, 0.01, 3),
+    "C3": (512, 512, "mesh", 0.25, 0.01, 3),
+    "C4": (1225, 1225, "grid4", 0.25, 0.0, 0),
+    "C5": (2048, 2048, "mesh", 0.25, 0.01, 0),
+}
+WORKLOAD_NAMES = {
+    "C1": "grid 100x100", "C2": "fe_4elt-shaped mesh 100x110",
+    "C3": "delaunay_n18-shaped mesh 512x512", "C4": "G3_circuit-shaped grid 1225x1225",
+    "C5": "delaunay_n22-shaped mesh 2048x2048",
+}
+K_BUDGET, T_CAP, WALKERS, WALK_SEED = 100.0, 100, 16, 42
+METRIC = "edge updates/sec (T_update per batch) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "edge_updates/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def make_inputs_product(cfg):
+    import paper_2505_02741_b200 as D
+    rows, cols, kind, ins, dele, loc = CONFIGS[cfg]
+    gen = D.make_mesh if kind == "mesh" else D.make_grid4
+    g = gen(rows, cols, 1)
+    h = D.build_initial_sparsifier(g, 0.10, 1)
+    s = D.generate_update_stream(g, D.StreamGenOptions(ins, dele, 10, 7, loc))
+    return g, h, s
+
+
+def make_inputs_oracle(orc, cfg):
+    rows, cols, kind, ins, dele, loc = CONFIGS[cfg]
+    g = orc.make_mesh(rows, cols, 1) if kind == "mesh" else orc.make_grid4(rows, cols, 1)
+    h = orc.build_initial_sparsifier(g, 0.10, 1)
+    s = orc.generate_stream(g, ins, dele, 10, 7, loc)
+    return g, h, s
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def load_peak():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu --set full capture."""
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline(cfg: str):
+    """The reference CPU implementation on this host, bounded sample: the
+    first insertion batch and the first deletion batch of the stream, each
+    replayed (deferred mode) from the initial state, all host threads."""
+    from oracle import oracle as O
+    kind = "reference" if O.available("reference") else "port"
+    orc = O.load("reference" if kind == "reference" else "restate")
+    cores = os.cpu_count() or 1
+    os.environ["DYSPARSE_THREADS"] = str(cores)
+    t0 = time.perf_counter()
+    g, h, s = make_inputs_oracle(orc, cfg)
+    setup = time.perf_counter() - t0
+    ev = s.events()
+    nb = s.batch_count
+    ins_b = 0
+    del_b = nb // 2 if nb > 10 else None
+    events, wall = 0, 0.0
+    for b in [ins_b] + ([del_b] if del_b is not None else []):
+        st = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED)
+        sel = ev[ev["batch_index"] == b].copy()
+        sel["batch_index"] = 0
+        t = time.perf_counter()
+        st.replay_batch(orc.stream(sel, 1), 0)
+        wall += time.perf_counter() - t
+        events += len(sel)
+    return {"value": events / wall, "unit": UNIT,
+            "cores": cores if kind == "reference" else 1, "kind": kind,
+            "sample": (f"{cfg}: insertion batch 0 + deletion batch {del_b} replayed from the "
+                       f"initial state ({events} events, {wall:.2f} s, setup {setup:.1f} s "
+                       "excluded), SparsifierState::replay_batch batched mode")}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    kind = "reference" if O.available("reference") else "port"
+    orc = O.load("reference" if kind == "reference" else "restate")
+    cores = os.cpu_count() or 1
+    os.environ["DYSPARSE_THREADS"] = str(cores)
+    g, h, s = make_inputs_oracle(orc, args.config)
+    nb = s.batch_count
+    st = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED)
+    b = 0
+
+    def step():
+        nonlocal st, b
+        if b == nb:
+            st, b = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED), 0
+        r = st.replay_batch(s, b)
+        b += 1
+        return int(r["insertions_seen"] + r["deletions_seen"])
+
+    for _ in range(args.warmup):
+        step()
+    events, t0 = 0, time.perf_counter()
+    for _ in range(args.steps):
+        events += step()
+    el = time.perf_counter() - t0
+    v = events / el
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators)",
+        "config": {"workload": WORKLOAD_NAMES[args.config], "config": args.config,
+                   "step": "one deferred batch of the stream, in order",
+                   "K": K_BUDGET, "T": T_CAP, "s": WALKERS},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores if kind == "reference" else 1,
+                         "kind": kind,
+                         "sample": f"{args.steps} consecutive batches of {args.config}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2505_02741_b200 as D
+    from paper_2505_02741_b200.parallel import ShardedReplay
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    t0 = time.perf_counter()
+    g, h, stream = make_inputs_product(args.config)
+    log(f"[rank {rank}] inputs {time.perf_counter() - t0:.1f}s")
+    opts = D.SparsifierOptions(D.WalkConfig(K_BUDGET, T_CAP, WALKERS, WALK_SEED), True, False)
+    st = D.SparsifierState(g, h, opts, device=dev)
+    torch_stream = torch.cuda.current_stream()
+    st.set_stream(torch_stream.cuda_stream)
+    st.snapshot()
+    nb = stream.batch_count
+    batches = [stream.batch(b) for b in range(nb)]
+    n_events = int(sum(len(e) for e, _ in batches))
+    sharded = ShardedReplay(st, rank, world) if world > 1 else None
+    if world == 1:
+        st.upload_stream(stream)
+
+    def step_device():
+        st.restore()
+        for b in range(nb):
+            if sharded is None:
+                st.replay_uploaded(b)
+            else:
+                sharded.replay_events(batches[b][0], batches[b][1], b)
+
+    def step_e2e():
+        st.restore()
+        for b in range(nb):
+            if sharded is None:
+                st.replay_events(batches[b][0], batches[b][1], b)
+            else:
+                sharded.replay_events(batches[b][0], batches[b][1], b)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    st.reset_stats()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(torch_stream)
+        for _ in range(args.steps):
+            step_device()
+        ev1.record(torch_stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    stats = st.stats()
+    # Check the final state of the last timed step against the first run.
+    rep_events = n_events
+
+    # End-to-end through the C-ABI with host buffers.
+    st.reset_stats()
+    for _ in range(min(args.warmup, 1)):
+        step_e2e()
+    torch.cuda.synchronize()
+    st.reset_stats()
+    barrier()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        step_e2e()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t) / args.steps)
+    estats = st.stats()
+
+    if rank != 0:
+        return
+    peak, peak_src = load_peak()
+    kern = {
+        "k_reach (K1, reach walks on H)": (stats["reach_ms"], stats["reach_row_bytes"]),
+        "k_minpath+finish (K2+K3, recovery walks on shadow G)":
+            (stats["minpath_ms"], stats["minpath_row_bytes"]),
+        "k_rounds<CommitOp> (K6-K8 commit)": (stats["commit_ms"], None),
+    }
+    dom = max(kern, key=lambda k: kern[k][0])
+    walk_key = max(list(kern)[:2], key=lambda k: kern[k][0])
+    wms, wbytes = kern[walk_key]
+    achieved = wbytes / (wms * 1e-3) / 1e9 if wms > 0 else 0.0
+    launches = stats["batches"]  # one reach or min-path launch per batch phase
+    out = {
+        "metric": METRIC,
+        "value": rep_events / (ms * 1e-3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference generators: make_mesh, build_initial_sparsifier, "
+                "generate_update_stream; bit-identical inputs)",
+        "config": {
+            "workload": WORKLOAD_NAMES[args.config], "config": args.config,
+            "vertices": g.vertex_count(), "edges": g.edge_count(),
+            "sparsifier_edges": h.edge_count(), "batches": nb, "events_per_step": rep_events,
+            "step": "restore(G0,H0) + replay of all batches (10 incremental + 10 decremental)",
+            "K": K_BUDGET, "T": T_CAP, "s": WALKERS, "walk_seed": WALK_SEED,
+            "parallelism": f"replicated G/H, walks sharded x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (G slabs 537 MB + H slabs 268 MB > 126 MB)",
+        },
+        "e2e": {
+            "value": rep_events / (e2e_ms * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": int(estats["h2d_bytes"] // args.steps),
+            "d2h_bytes_per_step": int(estats["d2h_bytes"] // args.steps),
+        },
+        "gpu_launches": int(stats["kernel_launches"]),
+        "roofline": {
+            "kernel": walk_key, "bound": "hbm", "achieved": achieved, "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s",
+            "frac": achieved / peak if peak else None,
+            "traffic": load_traffic(walk_key.split(" ")[0]),
+            "algorithmic_bytes_per_launch": wbytes / max(1, stats["batches"] // 2),
+            "avg_launch_ms": wms / max(1, stats["batches"] // 2),
+            "dominant_phase": dom,
+        },
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
+        "device_ms_per_step": stats["total_ms"] / args.steps,
+        "walker_steps_per_step": (stats["reach_steps"] + stats["minpath_steps"]) / args.steps,
+        "commit_rounds_per_step": stats["commit_rounds"] / args.steps,
+        "clocks": clocks.summary(),
+    }
+    del launches
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(args.config)
+        except Exception as exc:  # reported, never silently replaced
+            out["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    print(json.dumps(out), flush=True)
+    st.close()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=sorted(CONFIGS), default="C5")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

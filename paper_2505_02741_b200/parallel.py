@@ -1,0 +1,95 @@
+"""Multi-GPU replay: one process per GPU.
+
+Every rank holds a full replica of G and H (SparsifierState on its own
+device). For each batch:
+
+  1. every rank builds the same query lists on its replica
+     (dyg_shard_begin: validate, walk shadow, query build);
+  2. rank r walks the contiguous query range
+     [floor(nq*r/P), floor(nq*(r+1)/P)) and packs one fixed-size record per
+     query slot (dyg_shard_walk; reach: 16 B {reached, steps}; min-path:
+     24 B header + (T+1) path vertices);
+  3. the records are all-gathered over NCCL (NVLink) -- the batch's single
+     real exchange step;
+  4. every rank applies the identical deterministic commit
+     (dyg_shard_commit), so the replicas stay bit-identical.
+
+torch.distributed is plumbing only (process group, the all-gather); the walk
+and commit run in libdyg.so. The exchange helpers take any
+torch.distributed backend, so the protocol is covered on CPU with gloo.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_range(nq: int, rank: int, world: int) -> tuple[int, int]:
+    """Query range of `rank` (same formula as dyg_shard_walk)."""
+    return nq * rank // world, nq * (rank + 1) // world
+
+
+def slots_per_rank(nq: int, world: int) -> int:
+    return (nq + world - 1) // world
+
+
+def owner_of(q: int, nq: int, world: int) -> tuple[int, int]:
+    """(rank, index within the rank's slots) of query q."""
+    r = min(world - 1, q * world // max(nq, 1))
+    while r + 1 < world and nq * (r + 1) // world <= q:
+        r += 1
+    while r > 0 and nq * r // world > q:
+        r -= 1
+    return r, q - nq * r // world
+
+
+def allgather_records(local, world: int, group=None):
+    """Rank-major all-gather of equal-size record buffers (uint8 tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+    if local.numel():
+        dist.all_gather_into_tensor(out, local, group=group)
+    return out
+
+
+def unpack_records(gathered: np.ndarray, nq: int, world: int, rec_bytes: int) -> np.ndarray:
+    """Host mirror of k_unpack_*: rank-major slots -> query order (tests)."""
+    slots = slots_per_rank(nq, world)
+    g = gathered.reshape(world * slots, rec_bytes) if nq else gathered.reshape(0, rec_bytes)
+    out = np.zeros((nq, rec_bytes), np.uint8)
+    for q in range(nq):
+        r, i = owner_of(q, nq, world)
+        out[q] = g[r * slots + i]
+    return out
+
+
+class ShardedReplay:
+    """Drives a SparsifierState replica on this rank's GPU through the
+    sharded protocol. `state` must live on torch.cuda.current_device()."""
+
+    def __init__(self, state, rank: int, world: int, group=None):
+        import torch
+
+        self.state, self.rank, self.world, self.group = state, rank, world, group
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        # Kernels and the collective share one stream (stream-ordered).
+        state.set_stream(torch.cuda.current_stream().cuda_stream)
+        self.rbytes = state.shard_record_bytes(False)
+        self.mbytes = state.shard_record_bytes(True)
+        self.bytes_exchanged = 0
+
+    def replay_events(self, events, positions, batch_index: int):
+        import torch
+
+        nr, nm = self.state.shard_begin(events, positions, batch_index)
+        sr, sm = slots_per_rank(nr, self.world), slots_per_rank(nm, self.world)
+        rloc = torch.empty(sr * self.rbytes, dtype=torch.uint8, device=self.device)
+        mloc = torch.empty(sm * self.mbytes, dtype=torch.uint8, device=self.device)
+        self.state.shard_walk(self.rank, self.world, rloc.data_ptr() if sr else 0,
+                              mloc.data_ptr() if sm else 0)
+        rall = allgather_records(rloc, self.world, self.group)
+        mall = allgather_records(mloc, self.world, self.group)
+        self.bytes_exchanged += rall.numel() + mall.numel()
+        return self.state.shard_commit(self.world, rall.data_ptr() if sr else 0,
+                                       mall.data_ptr() if sm else 0)
