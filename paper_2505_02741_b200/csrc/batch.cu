@@ -128,15 +128,14 @@ __device__ __forceinline__ bool set_edge_weight(const DevGraph<kCapH>& h, uint32
 // (sparsifier.cpp:270-276); kNoVertex when none.
 __device__ __forceinline__ uint32_t best_neighbor(const DevGraph<kCapG>& g, uint32_t x,
                                                   uint32_t skip, double* wout) {
-  const uint32_t d = g.slab[x].deg;
-  const uint32_t* ids = row_ids(g, x);
-  const double* ws = row_ws(g, x);
+  const RowRef<kCapG> r = row(g, x);
+  const uint32_t d = r.deg();
   uint32_t best = kNoVertex;
   double bw = 0.0;
   for (uint32_t i = 0; i < d; ++i) {
-    const uint32_t id = ids[i];
+    const uint32_t id = r.id(i);
     if (id == skip) continue;
-    const double w = ws[i];
+    const double w = r.w(i);
     if (best == kNoVertex || w > bw || (w == bw && id < best)) {
       best = id;
       bw = w;

@@ -3,16 +3,21 @@
 // Device-resident dynamic rows (reference
 // DynamicGraph = vector<vector<Neighbor>>, proj/src/graph.hpp:65).
 //
-// Every vertex owns one fixed-size, size-aligned SLAB:
-//     { u32 deg; u32 ext; u32 id[C]; f64 w[C]; }
-// H uses C = 4 (64 B, one half line), G uses C = 10 (128 B, one line).
-// A row with deg <= C lives inline, so a walker step needs ONE dependent
-// fetch (header + ids + weights in the same line) instead of the two a
-// row_ptr CSR needs. A row that outgrows its slab moves to the overflow pool
-// (SoA arrays pool_id / pool_w, block of cap[u] entries at index ext); the
-// slab then only carries deg and ext. Per-row order is exactly the
-// reference's: append = push_back (graph.cpp:80-81), delete = move the last
-// entry into the hole (graph.cpp:97-108), coalesce in place (graph.cpp:74-79).
+// Every vertex owns one fixed-size SLAB holding the row header and, while
+// the row fits, the entries themselves:
+//   G (C = 10, 128 B, one line):  { u32 deg; u32 ext; u32 id[10]; f64 w[10]; }
+//   H (C = 7, 96 B, split):       bytes 0..63 = { deg, ext, id[0..3], w[0..3],
+//                                 id[4..5] }, bytes 64..95 = { id[6], pad,
+//                                 w[4..6] } -- the first 64 B are a complete
+//                                 4-entry row (95% of H rows), the tail is
+//                                 fetched only when deg > 4.
+// A walker step therefore needs ONE dependent fetch (header + ids + weights
+// in the same line) instead of the two a row_ptr CSR needs. A row that
+// outgrows its slab moves to the overflow pool (SoA arrays pool_id /
+// pool_w, block of cap[u] entries at index ext); the slab then only carries
+// deg and ext. Per-row order is exactly the reference's: append =
+// push_back (graph.cpp:80-81), delete = move the last entry into the hole
+// (graph.cpp:97-108), coalesce in place (graph.cpp:74-79).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,7 +28,7 @@ namespace dyg {
 constexpr uint32_t kNoVertex = 0xFFFFFFFFu;  // walk.cpp:12
 constexpr uint32_t kInline = 0xFFFFFFFFu;    // slab.ext for inline rows
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
-constexpr int kCapH = 4;   // inline entries per H slab (64 B)
+constexpr int kCapH = 7;   // inline entries per H slab (96 B, split 64 + 32)
 constexpr int kCapG = 10;  // inline entries per G slab (128 B)
 
 // rng.hpp:37-41
@@ -49,13 +54,31 @@ __device__ __forceinline__ double draw_u01(uint64_t seed, uint32_t k) {
 }
 
 template <int C>
-struct alignas(C <= 4 ? 64 : 128) Slab {
+struct Slab;
+
+template <>
+struct alignas(128) Slab<kCapG> {
   uint32_t deg;
   uint32_t ext;
-  uint32_t id[C];
-  double w[C];
+  uint32_t id[kCapG];
+  double w[kCapG];
+  __host__ __device__ uint32_t& idr(uint32_t i) { return id[i]; }
+  __host__ __device__ double& wr(uint32_t i) { return w[i]; }
 };
-static_assert(sizeof(Slab<kCapH>) == 64, "H slab must be 64 B");
+
+template <>
+struct alignas(32) Slab<kCapH> {
+  uint32_t deg;
+  uint32_t ext;
+  uint32_t id_lo[4];
+  double w_lo[4];
+  uint32_t id_hi[3];
+  uint32_t pad;
+  double w_hi[3];
+  __host__ __device__ uint32_t& idr(uint32_t i) { return i < 4 ? id_lo[i] : id_hi[i - 4]; }
+  __host__ __device__ double& wr(uint32_t i) { return i < 4 ? w_lo[i] : w_hi[i - 4]; }
+};
+static_assert(sizeof(Slab<kCapH>) == 96, "H slab must be 96 B");
 static_assert(sizeof(Slab<kCapG>) == 128, "G slab must be 128 B");
 
 // POD view of one device graph, passed by value to kernels.
@@ -72,23 +95,42 @@ struct DevGraph {
 };
 
 // ---------------------------------------------------------------- rows
+// Index-based view of row u (inline slab or overflow block).
 template <int C>
-__device__ __forceinline__ uint32_t* row_ids(const DevGraph<C>& g, uint32_t u) {
-  Slab<C>& s = g.slab[u];
-  return s.ext == kInline ? s.id : g.pool_id + s.ext;
-}
+struct RowRef {
+  Slab<C>* s;
+  uint32_t* pid;  // nullptr when inline
+  double* pw;
+  __device__ __forceinline__ uint32_t deg() const { return s->deg; }
+  __device__ __forceinline__ uint32_t id(uint32_t i) const { return pid ? pid[i] : s->idr(i); }
+  __device__ __forceinline__ double w(uint32_t i) const { return pid ? pw[i] : s->wr(i); }
+  __device__ __forceinline__ void set_w(uint32_t i, double x) const {
+    if (pid) pw[i] = x;
+    else s->wr(i) = x;
+  }
+  __device__ __forceinline__ void set(uint32_t i, uint32_t id, double x) const {
+    if (pid) {
+      pid[i] = id;
+      pw[i] = x;
+    } else {
+      s->idr(i) = id;
+      s->wr(i) = x;
+    }
+  }
+};
 template <int C>
-__device__ __forceinline__ double* row_ws(const DevGraph<C>& g, uint32_t u) {
-  Slab<C>& s = g.slab[u];
-  return s.ext == kInline ? s.w : g.pool_w + s.ext;
+__device__ __forceinline__ RowRef<C> row(const DevGraph<C>& g, uint32_t u) {
+  Slab<C>* s = g.slab + u;
+  if (s->ext == kInline) return RowRef<C>{s, nullptr, nullptr};
+  return RowRef<C>{s, g.pool_id + s->ext, g.pool_w + s->ext};
 }
 // graph.cpp:34-46 find: index of the first entry of row u with id v, or -1.
 template <int C>
 __device__ __forceinline__ int row_find(const DevGraph<C>& g, uint32_t u, uint32_t v) {
-  const uint32_t d = g.slab[u].deg;
-  const uint32_t* ids = row_ids(g, u);
+  const RowRef<C> r = row(g, u);
+  const uint32_t d = r.deg();
   for (uint32_t i = 0; i < d; ++i)
-    if (ids[i] == v) return static_cast<int>(i);
+    if (r.id(i) == v) return static_cast<int>(i);
   return -1;
 }
 // graph.cpp:48-53 has_edge (scan the smaller row; symmetric result).
@@ -102,7 +144,7 @@ template <int C>
 __device__ __forceinline__ double edge_weight(const DevGraph<C>& g, uint32_t u, uint32_t v) {
   if (g.slab[u].deg > g.slab[v].deg) { const uint32_t t = u; u = v; v = t; }
   const int i = row_find(g, u, v);
-  return i < 0 ? 0.0 : row_ws(g, u)[i];
+  return i < 0 ? 0.0 : row(g, u).w(static_cast<uint32_t>(i));
 }
 // push_back with slab -> pool relocation. Returns false when the pool is
 // exhausted (the host keeps enough headroom that this never happens).
@@ -113,8 +155,8 @@ __device__ __forceinline__ bool row_push(const DevGraph<C>& g, uint32_t u, uint3
   const uint32_t d = s.deg;
   if (s.ext == kInline) {
     if (d < C) {
-      s.id[d] = id;
-      s.w[d] = w;
+      s.idr(d) = id;
+      s.wr(d) = w;
       s.deg = d + 1;
       return true;
     }
@@ -122,8 +164,8 @@ __device__ __forceinline__ bool row_push(const DevGraph<C>& g, uint32_t u, uint3
     const unsigned long long b = atomicAdd(g.pool_top, static_cast<unsigned long long>(nc));
     if (b + nc > g.pool_cap) return false;
     for (uint32_t i = 0; i < d; ++i) {
-      g.pool_id[b + i] = s.id[i];
-      g.pool_w[b + i] = s.w[i];
+      g.pool_id[b + i] = s.idr(i);
+      g.pool_w[b + i] = s.wr(i);
     }
     s.ext = static_cast<uint32_t>(b);
     g.cap[u] = nc;
@@ -146,13 +188,10 @@ __device__ __forceinline__ bool row_push(const DevGraph<C>& g, uint32_t u, uint3
 // graph.cpp:97-105 remove_from: the last entry moves into the hole.
 template <int C>
 __device__ __forceinline__ void row_remove_at(const DevGraph<C>& g, uint32_t u, uint32_t i) {
-  Slab<C>& s = g.slab[u];
-  const uint32_t last = s.deg - 1;
-  uint32_t* ids = row_ids(g, u);
-  double* ws = row_ws(g, u);
-  ids[i] = ids[last];
-  ws[i] = ws[last];
-  s.deg = last;
+  const RowRef<C> r = row(g, u);
+  const uint32_t last = r.deg() - 1;
+  r.set(i, r.id(last), r.w(last));
+  r.s->deg = last;
 }
 
 // graph.cpp:64-85 insert_edge on validated input. Returns 0 New,
@@ -162,9 +201,10 @@ __device__ __forceinline__ int insert_edge(const DevGraph<C>& g, uint32_t u, uin
                                            double w) {
   const int i = row_find(g, u, v);
   if (i >= 0) {
-    double* wu = row_ws(g, u);
-    wu[i] = __dadd_rn(wu[i], w);
-    row_ws(g, v)[row_find(g, v, u)] = wu[i];
+    const RowRef<C> ru = row(g, u);
+    const double nw = __dadd_rn(ru.w(static_cast<uint32_t>(i)), w);
+    ru.set_w(static_cast<uint32_t>(i), nw);
+    row(g, v).set_w(static_cast<uint32_t>(row_find(g, v, u)), nw);
     return 1;
   }
   if (!row_push(g, u, v, w)) return -1;

@@ -39,8 +39,8 @@ __global__ void k_build(DevGraph<C> g, const uint64_t* __restrict__ rp,
     s.ext = kInline;
     g.cap[u] = 0;
     for (uint32_t i = 0; i < d; ++i) {
-      s.id[i] = ids[b + i];
-      s.w[i] = w[b + i];
+      s.idr(i) = ids[b + i];
+      s.wr(i) = w[b + i];
     }
     return;
   }
@@ -65,13 +65,12 @@ __global__ void k_gather(DevGraph<C> g, const uint64_t* __restrict__ rp, uint32_
                          double* w) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= g.n) return;
-  const uint32_t d = g.slab[u].deg;
-  const uint32_t* ri = row_ids(g, u);
-  const double* rw = row_ws(g, u);
+  const RowRef<C> r = row(g, u);
+  const uint32_t d = r.deg();
   const uint64_t b = rp[u];
   for (uint32_t i = 0; i < d; ++i) {
-    ids[b + i] = ri[i];
-    w[b + i] = rw[i];
+    ids[b + i] = r.id(i);
+    w[b + i] = r.w(i);
   }
 }
 

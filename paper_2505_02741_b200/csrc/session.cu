@@ -103,6 +103,7 @@ struct dyg_session {
   uint32_t nb_cap = 0, nd_cap = 0;
   unsigned long long* d_locks = nullptr;
   unsigned long long* d_round = nullptr;
+  unsigned int* d_work = nullptr;  // walk work counter
   DevEvent* d_events = nullptr;
   DevEvent* h_events_pinned = nullptr;
   BatchCtl* h_ctl = nullptr;
@@ -348,7 +349,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
     p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
-                               s->stream);
+                               s->d_work, s->stream);
     maybe_sync(s, "reach walks");
   }
   check(cudaEventRecord(s->t_reach.b, s->stream), "event");
@@ -360,7 +361,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     MinOut mo{b.mout.has_path + lo_m, b.mout.path_len + lo_m, b.mout.steps + lo_m,
               b.mout.resistance + lo_m, b.mout.paths + lo_m * T1};
     p.launches += launch_minpath(s->S.view(), b.mq + lo_m, cnt_m, max_m, Pd, b.mscratch, mo,
-                                 &b.ctl->minpath, s->stream);
+                                 &b.ctl->minpath, s->d_work, s->stream);
     maybe_sync(s, "minpath walks");
   }
   check(cudaEventRecord(s->t_min.b, s->stream), "event");
@@ -598,6 +599,7 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       dev_alloc(&s->d_locks, s->n, "row locks");
       check(cudaMemset(s->d_locks, 0, sizeof(unsigned long long) * s->n), "locks");
       dev_alloc(&s->d_round, 1, "round counter");
+      dev_alloc(&s->d_work, 1, "walk work counter");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
       dev_alloc(&s->b.ctl, 1, "batch ctl");
       dev_alloc(&s->d_counts, 2, "shard counts");
@@ -636,6 +638,7 @@ void dyg_session_destroy(dyg_session* s) {
   dev_free(s->b.ctl);
   dev_free(s->d_locks);
   dev_free(s->d_round);
+  dev_free(s->d_work);
   dev_free(s->d_stream);
   if (s->h_ctl) cudaFreeHost(s->h_ctl);
   if (s->h_counts) cudaFreeHost(s->h_counts);
@@ -1042,6 +1045,8 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
     const uint64_t T1 = static_cast<uint64_t>(cfg->step_cap) + 1;
     WalkCounters* ctr = nullptr;
     uint32_t* d_n = nullptr;
+    unsigned int* d_work = nullptr;
+    dev_alloc(&d_work, 1, "work counter");
     dev_alloc(&ctr, 2, "counters");
     dev_alloc(&d_n, 2, "counts");
     const uint32_t counts[2] = {static_cast<uint32_t>(rq.size()), static_cast<uint32_t>(mq.size())};
@@ -1057,7 +1062,7 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
       dev_alloc(&ro.steps, rq.size(), "out");
       dev_alloc(&ro.best_bits, rq.size(), "out");
       check(cudaMemcpy(d_q, rq.data(), sizeof(ReachQuery) * rq.size(), cudaMemcpyHostToDevice), "q");
-      launch_reach(gh.view(), d_q, d_n, counts[0], P, ro, ctr, st);
+      launch_reach(gh.view(), d_q, d_n, counts[0], P, ro, ctr, d_work, st);
       check(cudaGetLastError(), "reach launch");
       check(cudaStreamSynchronize(st), "reach");
       std::vector<uint32_t> reached(rq.size());
@@ -1097,7 +1102,7 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
       dev_alloc(&sc.paths, nm * sw * T1, "scratch");
       dev_alloc(&sc.rvals, nm * T1, "scratch");
       check(cudaMemcpy(d_q, mq.data(), sizeof(MinQuery) * nm, cudaMemcpyHostToDevice), "q");
-      launch_minpath(gg.view(), d_q, d_n + 1, counts[1], P, sc, mo, ctr + 1, st);
+      launch_minpath(gg.view(), d_q, d_n + 1, counts[1], P, sc, mo, ctr + 1, d_work, st);
       check(cudaGetLastError(), "minpath launch");
       check(cudaStreamSynchronize(st), "minpath");
       std::vector<uint32_t> has(nm), len(nm), paths(nm * T1);
@@ -1134,6 +1139,7 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
     }
     cudaFree(ctr);
     cudaFree(d_n);
+    cudaFree(d_work);
     cudaStreamDestroy(st);
   });
 }

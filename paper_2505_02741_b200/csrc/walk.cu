@@ -9,6 +9,7 @@
 //                       walk.cpp:131-133), loop_erase (walk.cpp:100-117),
 //                       resistance recompute (walk.cpp:140-143)
 #include <math.h>
+#include <stdlib.h>
 
 #include "walk.cuh"
 
@@ -18,40 +19,103 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
-// One sample_neighbor call (walk.cpp:17-37) at `cur`. Loads the whole slab
-// with 16-byte vector loads (one line), sums candidate weights in row order
-// (pass 1), draws target = u01 * total with draw k, and selects the first
-// candidate whose running sum exceeds target (pass 2), falling back to the
-// last candidate. Returns false on a dead end (no draw consumed).
+
+inline unsigned blocks_for(uint64_t threads, unsigned per_block) {
+  return static_cast<unsigned>((threads + per_block - 1) / per_block);
+}
+
+// Cooperative slab gather. A per-lane 16-byte vector load of 32 scattered
+// slabs touches 32 different lines per warp instruction, and the L1TEX data
+// pipe processes one line per wavefront (ncu: ~42-58% busy, long-scoreboard
+// stalls dominate). Here each load instruction covers WHOLE slabs instead --
+// 8 lanes x 16 B per 128 B G slab (4 slabs per instruction), 4 lanes x 16 B
+// per 64 B H head (8 per instruction) -- so every slab costs one wavefront.
+// The slabs are staged in shared memory (row stride padded to 9 / 5 x 16 B,
+// conflict-free) and each lane reads its own back. Lanes pass kNoVertex when
+// they need no row this iteration.
 template <int C>
-__device__ __forceinline__ bool walk_step(const DevGraph<C>& g, uint32_t cur, uint32_t prev,
-                                          uint64_t wseed, uint32_t k, uint32_t& next,
-                                          double& ew, uint32_t& deg) {
+struct Gather {
+  static constexpr int kChunks = C == kCapH ? 4 : 8;   // 16 B chunks fetched
+  static constexpr int kLanesPerRow = kChunks;
+  static constexpr int kRowsPerRound = 32 / kLanesPerRow;
+  static constexpr int kRounds = 32 / kRowsPerRound;
+  static constexpr int kStride = kChunks + 1;          // uint4 per staged row
+  static constexpr int kWarpWords = 32 * kStride;      // uint4 per warp
+};
+
+// 16-byte global->shared async copy (LDGSTS); src_bytes = 0 zero-fills
+// without reading (lanes with no row this round).
+__device__ __forceinline__ void cp_async16(uint4* dst, const void* src, uint32_t src_bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+
+template <int C>
+__device__ __forceinline__ const uint4* gather_rows(const DevGraph<C>& g, uint32_t my_row,
+                                                   uint4* stage) {
+  using Gt = Gather<C>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t sub = lane / Gt::kLanesPerRow;
+  const uint32_t chunk = lane % Gt::kLanesPerRow;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < Gt::kRounds; ++j) {
+    const uint32_t r = j * Gt::kRowsPerRound + sub;
+    const uint32_t u = __shfl_sync(kFull, my_row, r);
+    const bool live = u != kNoVertex;
+    const uint4* src = reinterpret_cast<const uint4*>(g.slab + (live ? u : 0)) + chunk;
+    cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncwarp();
+  return stage + lane * Gt::kStride;
+}
+
+// One sample_neighbor call (walk.cpp:17-37) at `cur` on the gathered slab
+// head, given this step's uniform draw u01. The reference's pass 1 sums
+// candidate weights in row order and its pass 2 re-accumulates the same
+// running sums until target < cumulative; both passes produce the identical
+// sequence of partial sums, so they are computed ONCE (prefix[i]) and pass 2
+// becomes independent compares -- bit-identical, with half the dependent
+// fp64 adds. Rounding fallback = the last candidate. Returns false on a
+// dead end. H rows with more than 4 entries fetch the slab tail here.
+template <int C>
+__device__ __forceinline__ bool walk_step(const DevGraph<C>& g, const uint4* head, uint32_t cur,
+                                          uint32_t prev, double u01, uint32_t& next, double& ew,
+                                          uint32_t& deg) {
   constexpr int NV = static_cast<int>(sizeof(Slab<C>) / 16);
+  constexpr int NH = Gather<C>::kChunks;
   union {
     uint4 v[NV];
     Slab<C> s;
   } r;
-  const uint4* src = reinterpret_cast<const uint4*>(g.slab + cur);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) r.v[i] = __ldg(src + i);
+  for (int i = 0; i < NH; ++i) r.v[i] = head[i];  // shared-memory reads (LDS.128)
   deg = r.s.deg;
   if (r.s.ext == kInline) {
+    if (NH < NV && deg > 4) {
+      const uint4* src = reinterpret_cast<const uint4*>(g.slab + cur);
+#pragma unroll
+      for (int i = NH; i < NV; ++i) r.v[i] = __ldg(src + i);
+    }
+    double prefix[C];
     double total = 0.0;
 #pragma unroll
-    for (int i = 0; i < C; ++i)
-      if (i < static_cast<int>(deg) && r.s.id[i] != prev) total = __dadd_rn(total, r.s.w[i]);
+    for (int i = 0; i < C; ++i) {
+      if (i < static_cast<int>(deg) && r.s.idr(i) != prev) total = __dadd_rn(total, r.s.wr(i));
+      prefix[i] = total;
+    }
     if (total <= 0.0) return false;
-    const double target = __dmul_rn(draw_u01(wseed, k), total);
-    double cum = 0.0;
+    const double target = __dmul_rn(u01, total);
     bool found = false;
 #pragma unroll
     for (int i = 0; i < C; ++i) {
-      if (!found && i < static_cast<int>(deg) && r.s.id[i] != prev) {
-        cum = __dadd_rn(cum, r.s.w[i]);
-        next = r.s.id[i];
-        ew = r.s.w[i];
-        if (target < cum) found = true;
+      if (!found && i < static_cast<int>(deg) && r.s.idr(i) != prev) {
+        next = r.s.idr(i);
+        ew = r.s.wr(i);
+        found = target < prefix[i];
       }
     }
     return true;
@@ -62,7 +126,7 @@ __device__ __forceinline__ bool walk_step(const DevGraph<C>& g, uint32_t cur, ui
   for (uint32_t i = 0; i < deg; ++i)
     if (__ldg(ids + i) != prev) total = __dadd_rn(total, __ldg(ws + i));
   if (total <= 0.0) return false;
-  const double target = __dmul_rn(draw_u01(wseed, k), total);
+  const double target = __dmul_rn(u01, total);
   double cum = 0.0;
   for (uint32_t i = 0; i < deg; ++i) {
     const uint32_t id = __ldg(ids + i);
@@ -74,6 +138,12 @@ __device__ __forceinline__ bool walk_step(const DevGraph<C>& g, uint32_t cur, ui
     if (target < cum) break;
   }
   return true;
+}
+
+// Uniform draw from the SplitMix64 counter (rng.hpp:7-24): `ctr` already
+// advanced by gamma for this draw.
+__device__ __forceinline__ double u01_of(uint64_t ctr) {
+  return __dmul_rn(static_cast<double>(hash_mix(ctr) >> 11), 0x1.0p-53);
 }
 
 __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long long steps,
@@ -89,135 +159,164 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long lo
   }
 }
 
-// K1: lane = (query, walker); the s walkers of a query sit on s consecutive
-// lanes. single_walk's check order (walk.cpp:54-78): cap at the loop top,
-// then after each traversed edge budget before target.
-template <int C>
-__global__ void __launch_bounds__(256) k_reach(DevGraph<C> g, const ReachQuery* __restrict__ qs,
-                                               const uint32_t* __restrict__ nq_dev, WalkParams P,
-                                               ReachOut out, WalkCounters* ctr) {
-  const uint32_t nq = *nq_dev;
-  const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint32_t qi = static_cast<uint32_t>(gt / P.s);
-  const uint32_t wi = static_cast<uint32_t>(gt % P.s);
-  const bool valid = qi < nq;
-  if (__all_sync(kFull, !valid)) return;
+// K1/K2 as persistent lane-refill kernels. Walk lengths are long-tailed
+// (most insertion walkers dead-end within a few steps, a few run to T), so a
+// static lane<->walker mapping leaves most lanes idle (ncu: 6.4 of 32 lanes
+// active). Here a lane that finishes its walker takes the next work item
+// (query = w / s, walker = w % s) from a global counter with one
+// warp-aggregated atomic, so warps stay full until the queue drains.
+// Per-walker semantics are single_walk's (walk.cpp:41-80): cap at the loop
+// top, then after each traversed edge budget before target.
+//
+// Reach results (nbrw_reach, walk.cpp:82-98) are order-free reductions --
+// reached = OR, steps = SUM, best = MIN -- so they are accumulated with
+// atomics into outputs pre-set by k_reach_init. Min-path walkers keep their
+// raw trace and (acc, terminal, steps) for K3.
+template <int C, bool kMinPath, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks)
+    k_walk(DevGraph<C> g, const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
+           const uint32_t* __restrict__ nq_dev, WalkParams P, ReachOut rout, MinScratch S,
+           WalkCounters* ctr, unsigned int* __restrict__ work) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t total_work = *nq_dev * P.s;
+  __shared__ uint4 stage_all[8 * Gather<C>::kWarpWords];
+  uint4* stage = stage_all + (threadIdx.x >> 5) * Gather<C>::kWarpWords;
+  // Warp-uniform chunk of 32 work items [chunk_base, chunk_base + 32); lane
+  // i holds item chunk_base + i's query, prefetched when the chunk is taken.
+  uint32_t chunk_base = 0, chunk_pos = 32, chunk_end = 32;
+  bool drained = false;
+  uint32_t pf_p = 0, pf_q = 0;
+  double pf_w = 1.0;
+  unsigned long long pf_uid = 0;
 
-  uint32_t steps = 0;
-  double acc = 0.0;
-  bool reached = false;
-  unsigned long long bytes = 0;
-  if (valid) {
-    const ReachQuery Q = qs[qi];
-    const uint64_t wseed = walker_seed(P.seed, Q.update_id, wi);
-    uint32_t cur = Q.p, prev = kNoVertex;
-    while (steps < P.T) {
-      uint32_t next = kNoVertex, deg = 0;
-      double ew = 0.0;
-      const bool ok = walk_step(g, cur, prev, wseed, steps + 1, next, ew, deg);
-      bytes += step_bytes(deg);
-      if (!ok) break;
-      acc = __dadd_rn(acc, __drcp_rn(ew));
-      ++steps;
-      prev = cur;
-      cur = next;
-      if (__dmul_rn(Q.w_pq, acc) > P.K) break;
-      if (cur == Q.q) {
-        reached = true;
-        break;
+  bool has = false;
+  uint32_t qi = 0, cur = 0, prev = kNoVertex, target_v = 0, steps = 0, w_idx = 0;
+  uint64_t rng = 0;
+  double acc = 0.0, w_pq = 1.0;
+  uint32_t* trace = nullptr;
+  unsigned long long my_steps = 0, my_bytes = 0;
+  for (;;) {
+    unsigned need = __ballot_sync(kFull, !has);
+    while (need && !drained) {
+      if (chunk_pos == chunk_end) {
+        unsigned int base = 0;
+        if (lane == 0) base = atomicAdd(work, 32u);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= total_work) {
+          drained = true;
+          break;
+        }
+        chunk_base = base;
+        chunk_pos = 0;
+        chunk_end = min(32u, total_work - base);
+        const uint32_t w = base + lane;
+        if (w < total_work) {
+          const uint32_t q = w / P.s;
+          if (kMinPath) {
+            const MinQuery Q = mq[q];
+            pf_p = Q.p;
+            pf_q = Q.q;
+            pf_uid = Q.update_id;
+          } else {
+            const ReachQuery Q = rq[q];
+            pf_p = Q.p;
+            pf_q = Q.q;
+            pf_w = Q.w_pq;
+            pf_uid = Q.update_id;
+          }
+        }
+      }
+      const uint32_t rank = __popc(need & ((1u << lane) - 1u));
+      const uint32_t take = min(static_cast<uint32_t>(__popc(need)), chunk_end - chunk_pos);
+      const uint32_t from = (chunk_pos + rank) & 31u;
+      const uint32_t p = __shfl_sync(kFull, pf_p, from);
+      const uint32_t q = __shfl_sync(kFull, pf_q, from);
+      const double wq = __shfl_sync(kFull, pf_w, from);
+      const unsigned long long uid = __shfl_sync(kFull, pf_uid, from);
+      const bool mine = ((need >> lane) & 1u) && rank < take;
+      if (mine) {
+        w_idx = chunk_base + chunk_pos + rank;
+        qi = w_idx / P.s;
+        const uint32_t wi = w_idx - qi * P.s;
+        cur = p;
+        target_v = q;
+        w_pq = kMinPath ? 1.0 : wq;
+        rng = walker_seed(P.seed, uid, wi);
+        prev = kNoVertex;
+        steps = 0;
+        acc = 0.0;
+        has = true;
+        if (kMinPath) {
+          trace = S.paths + static_cast<uint64_t>(w_idx) * (P.T + 1ull);
+          trace[0] = cur;
+        }
+      }
+      chunk_pos += take;
+      need = __ballot_sync(kFull, !has);
+    }
+    if (!__any_sync(kFull, has)) break;
+    const uint4* head = gather_rows(g, (has && steps < P.T) ? cur : kNoVertex, stage);
+    if (has) {
+      uint32_t term = 0xFFFFFFFFu;
+      if (steps >= P.T) {
+        term = kStepCap;
+      } else {
+        rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
+        const double u = u01_of(rng);
+        uint32_t next = kNoVertex, deg = 0;
+        double ew = 0.0;
+        const bool ok = walk_step(g, head, cur, prev, u, next, ew, deg);
+        my_bytes += step_bytes(deg);
+        if (!ok) {
+          term = kDeadEnd;
+        } else {
+          acc = __dadd_rn(acc, __drcp_rn(ew));
+          ++steps;
+          prev = cur;
+          cur = next;
+          if (kMinPath) trace[steps] = cur;
+          if (__dmul_rn(w_pq, acc) > P.K) {
+            term = kBudget;
+          } else if (cur == target_v) {
+            term = kReached;
+          }
+        }
+      }
+      if (term != 0xFFFFFFFFu) {
+        my_steps += steps;
+        if (kMinPath) {
+          S.acc[w_idx] = acc;
+          S.term[w_idx] = term;
+          S.steps[w_idx] = steps;
+        } else {
+          atomicAdd(&rout.steps[qi], static_cast<unsigned long long>(steps));
+          if (term == kReached) {
+            atomicOr(&rout.reached[qi], 1u);
+            atomicMin(&rout.best_bits[qi],
+                      static_cast<unsigned long long>(__double_as_longlong(acc)));
+          }
+        }
+        has = false;
       }
     }
   }
-  add_counters(ctr, steps, bytes);
-
-  // nbrw_reach (walk.cpp:82-98): reached = any; best = min; steps = sum.
-  // All three reductions are order-free, so a tree reduction is exact.
-  if (P.s <= 32 && (P.s & (P.s - 1)) == 0) {
-    unsigned long long st = steps;
-    uint32_t r = reached ? 1u : 0u;
-    double best = reached ? acc : INFINITY;
-    for (uint32_t off = 1; off < P.s; off <<= 1) {
-      st += __shfl_xor_sync(kFull, st, off);
-      r |= __shfl_xor_sync(kFull, r, off);
-      best = fmin(best, __shfl_xor_sync(kFull, best, off));
-    }
-    if (valid && wi == 0) {
-      out.reached[qi] = r;
-      out.steps[qi] = st;
-      out.best_bits[qi] = r ? static_cast<unsigned long long>(__double_as_longlong(best)) : 0ull;
-    }
-  } else if (valid) {
-    // Outputs pre-set to {0, 0, +inf bits}; positive doubles order as u64.
-    atomicAdd(&out.steps[qi], static_cast<unsigned long long>(steps));
-    if (reached) {
-      atomicOr(&out.reached[qi], 1u);
-      atomicMin(&out.best_bits[qi], static_cast<unsigned long long>(__double_as_longlong(acc)));
-    }
-  }
+  add_counters(ctr, my_steps, my_bytes);
 }
 
-__global__ void k_reach_init(ReachOut out, uint32_t n) {
+__global__ void k_reach_init(ReachOut out, uint32_t n, unsigned int* work) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *work = 0;
   if (i >= n) return;
   out.reached[i] = 0;
   out.steps[i] = 0;
   out.best_bits[i] = 0x7FF0000000000000ull;
 }
 
-// K2: min-path walkers (w_pq = 1, budget from P.K = +inf for deletions),
-// raw trace of each walker kept for K3.
-template <int C>
-__global__ void __launch_bounds__(256) k_minpath(DevGraph<C> g, const MinQuery* __restrict__ qs,
-                                                 const uint32_t* __restrict__ nq_dev,
-                                                 WalkParams P, MinScratch S, WalkCounters* ctr) {
-  const uint32_t nq = *nq_dev;
-  const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint32_t qi = static_cast<uint32_t>(gt / P.s);
-  const uint32_t wi = static_cast<uint32_t>(gt % P.s);
-  const bool valid = qi < nq;
-  if (__all_sync(kFull, !valid)) return;
-  uint32_t steps = 0;
-  unsigned long long bytes = 0;
-  if (valid) {
-    const MinQuery Q = qs[qi];
-    const uint64_t wseed = walker_seed(P.seed, Q.update_id, wi);
-    uint32_t* trace = S.paths + gt * (P.T + 1ull);
-    uint32_t cur = Q.p, prev = kNoVertex;
-    uint32_t term = kStepCap;
-    double acc = 0.0;
-    trace[0] = cur;
-    while (true) {
-      if (steps >= P.T) {
-        term = kStepCap;
-        break;
-      }
-      uint32_t next = kNoVertex, deg = 0;
-      double ew = 0.0;
-      const bool ok = walk_step(g, cur, prev, wseed, steps + 1, next, ew, deg);
-      bytes += step_bytes(deg);
-      if (!ok) {
-        term = kDeadEnd;
-        break;
-      }
-      acc = __dadd_rn(acc, __drcp_rn(ew));
-      ++steps;
-      prev = cur;
-      cur = next;
-      trace[steps] = cur;
-      if (__dmul_rn(1.0, acc) > P.K) {
-        term = kBudget;
-        break;
-      }
-      if (cur == Q.q) {
-        term = kReached;
-        break;
-      }
-    }
-    S.acc[gt] = acc;
-    S.term[gt] = term;
-    S.steps[gt] = steps;
-  }
-  add_counters(ctr, steps, bytes);
+// Reach outputs of queries that found no walker keep +inf in best_bits;
+// the reference leaves best_estimate = 0 when not reached (walk.hpp:31).
+__global__ void k_reach_fix(ReachOut out, const uint32_t* __restrict__ nq_dev) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < *nq_dev && !out.reached[i]) out.best_bits[i] = 0ull;
 }
 
 // K3: one warp per min-path query.
@@ -296,51 +395,72 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
   }
 }
 
-inline unsigned blocks_for(uint64_t threads, unsigned per_block) {
-  return static_cast<unsigned>((threads + per_block - 1) / per_block);
+}  // namespace
+
+template <typename K>
+unsigned persistent_blocks(K kernel, uint64_t work) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+  const unsigned b = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
+  const unsigned need = blocks_for(work, 256);
+  return need < b ? need : b;
 }
 
-}  // namespace
+// Reach occupancy variant (registers vs resident warps); DYG_REACH_BLOCKS
+// selects 3 (default, no spills) or 4 blocks/SM.
+int reach_variant() {
+  static int v = [] {
+    const char* e = std::getenv("DYG_REACH_BLOCKS");
+    return (e && std::atoi(e) == 4) ? 4 : 3;
+  }();
+  return v;
+}
 
 template <int C>
 int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
                  uint32_t nq_max, const WalkParams& P, ReachOut out, WalkCounters* ctr,
-                 cudaStream_t st) {
+                 unsigned int* work, cudaStream_t st) {
   if (nq_max == 0) return 0;
-  int launches = 0;
-  const bool seg = P.s <= 32 && (P.s & (P.s - 1)) == 0;
-  if (!seg) {
-    k_reach_init<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_max);
-    ++launches;
-  }
+  k_reach_init<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_max, work);
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
-  k_reach<C><<<blocks_for(threads, 256), 256, 0, st>>>(g, q, nq_dev, P, out, ctr);
-  return launches + 1;
+  if (reach_variant() == 4) {
+    auto k = k_walk<C, false, 4>;
+    k<<<persistent_blocks(k, threads), 256, 0, st>>>(g, q, nullptr, nq_dev, P, out,
+                                                    MinScratch{}, ctr, work);
+  } else {
+    auto k = k_walk<C, false, 3>;
+    k<<<persistent_blocks(k, threads), 256, 0, st>>>(g, q, nullptr, nq_dev, P, out,
+                                                    MinScratch{}, ctr, work);
+  }
+  k_reach_fix<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_dev);
+  return 3;
 }
+
+__global__ void k_zero(unsigned int* work) { *work = 0; }
 
 template <int C>
 int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_dev,
                    uint32_t nq_max, const WalkParams& P, MinScratch scratch, MinOut out,
-                   WalkCounters* ctr, cudaStream_t st) {
+                   WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
   if (nq_max == 0) return 0;
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
-  k_minpath<C><<<blocks_for(threads, 256), 256, 0, st>>>(g, q, nq_dev, P, scratch, ctr);
+  k_zero<<<1, 1, 0, st>>>(work);
+  auto k = k_walk<C, true, 2>;
+  k<<<persistent_blocks(k, threads), 256, 0, st>>>(g, nullptr, q, nq_dev, P, ReachOut{},
+                                                  scratch, ctr, work);
   k_minpath_finish<C><<<blocks_for(static_cast<uint64_t>(nq_max) * 32, 256), 256, 0, st>>>(
       g, nq_dev, P, scratch, out);
-  return 2;
+  return 3;
 }
 
 template int launch_reach<kCapH>(const DevGraph<kCapH>&, const ReachQuery*, const uint32_t*,
                                  uint32_t, const WalkParams&, ReachOut, WalkCounters*,
-                                 cudaStream_t);
-template int launch_reach<kCapG>(const DevGraph<kCapG>&, const ReachQuery*, const uint32_t*,
-                                 uint32_t, const WalkParams&, ReachOut, WalkCounters*,
-                                 cudaStream_t);
+                                 unsigned int*, cudaStream_t);
 template int launch_minpath<kCapG>(const DevGraph<kCapG>&, const MinQuery*, const uint32_t*,
                                    uint32_t, const WalkParams&, MinScratch, MinOut,
-                                   WalkCounters*, cudaStream_t);
-template int launch_minpath<kCapH>(const DevGraph<kCapH>&, const MinQuery*, const uint32_t*,
-                                   uint32_t, const WalkParams&, MinScratch, MinOut,
-                                   WalkCounters*, cudaStream_t);
+                                   WalkCounters*, unsigned int*, cudaStream_t);
+
 
 }  // namespace dyg

@@ -61,15 +61,15 @@ struct WalkCounters {
 };
 
 // Host launchers (walk.cu). nq_dev: device count of queries (nq_max bounds
-// the launch). stream: session stream. Each returns the number of kernels
-// launched.
+// the launch); work: a device u32 work counter (reset by the launcher).
+// stream: session stream. Each returns the number of kernels launched.
 template <int C>
 int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
                  uint32_t nq_max, const WalkParams& P, ReachOut out,
-                 WalkCounters* ctr, cudaStream_t st);
+                 WalkCounters* ctr, unsigned int* work, cudaStream_t st);
 template <int C>
 int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_dev,
                    uint32_t nq_max, const WalkParams& P, MinScratch scratch, MinOut out,
-                   WalkCounters* ctr, cudaStream_t st);
+                   WalkCounters* ctr, unsigned int* work, cudaStream_t st);
 
 }  // namespace dyg
