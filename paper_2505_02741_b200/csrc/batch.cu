@@ -36,8 +36,46 @@ __global__ void k_validate(const DevEvent* __restrict__ ev, uint32_t nb, uint32_
   if (code) atomicMin(&ctl->val_err, (static_cast<unsigned long long>(k) << 8) | code);
 }
 
+// Per-thread accumulators of one round-engine launch: report counters and
+// |E| deltas are summed locally and flushed once per warp at the end
+// (one atomic per warp instead of several same-address atomics per event).
+struct Acc {
+  unsigned long long r[kReportFields];
+  long long dg, dh;
+};
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, off);
+  return x;
+}
+__device__ __forceinline__ unsigned long long warp_max(unsigned long long x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, x, off);
+    x = o > x ? o : x;
+  }
+  return x;
+}
+__device__ __forceinline__ void flush_acc(const Acc& a, BatchCtl* ctl, unsigned long long* g_edges,
+                                          unsigned long long* h_edges) {
+  const bool lead = (threadIdx.x & 31) == 0;
+#pragma unroll
+  for (int f = 0; f < kReportFields; ++f) {
+    const unsigned long long v = f == kMaxEventSteps ? warp_max(a.r[f]) : warp_sum(a.r[f]);
+    if (lead && v) {
+      if (f == kMaxEventSteps) atomicMax(&ctl->report[f], v);
+      else atomicAdd(&ctl->report[f], v);
+    }
+  }
+  const unsigned long long dg = warp_sum(static_cast<unsigned long long>(a.dg));
+  const unsigned long long dh = warp_sum(static_cast<unsigned long long>(a.dh));
+  if (lead && dg && g_edges) atomicAdd(g_edges, dg);
+  if (lead && dh && h_edges) atomicAdd(h_edges, dh);
+}
+
 // The round engine. Op provides for_rows(k, f) (every row event k reads or
-// writes, possibly with repeats) and apply(k) -> error code.
+// writes, possibly with repeats) and apply(k, acc) -> error code.
 template <class Op>
 __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b) {
   cg::grid_group grid = cg::this_grid();
@@ -45,6 +83,7 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
   const uint32_t nth = static_cast<uint32_t>(grid.size());
   volatile BatchCtl* ctl = b.ctl;
   if (ctl->val_err != ~0ull) return;  // uniform: nothing below ran yet
+  Acc acc{};
   unsigned long long round = *b.round_ctr;
   uint32_t r = 0;
   for (;; ++r) {
@@ -66,7 +105,7 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
           ready = false;
       });
       if (ready) {
-        const uint32_t e = op.apply(k);
+        const uint32_t e = op.apply(k, acc);
         b.state[k] = e ? 2 : 1;
         if (e) atomicMin(&b.ctl->commit_err, (static_cast<unsigned long long>(k) << 8) | e);
       } else {
@@ -76,6 +115,7 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
     grid.sync();
     if (ctl->remaining[r % 3] == 0) break;
   }
+  op.flush(acc);
   if (tid == 0) {
     *b.round_ctr = round;
     ctl->rounds = ctl->rounds + r + 1;
@@ -99,11 +139,12 @@ struct ShadowOp {
       f(e.v);
     }
   }
-  __device__ uint32_t apply(uint32_t k) const {
+  __device__ void flush(const Acc& a) const { flush_acc(a, ctl, nullptr, nullptr); }
+  __device__ uint32_t apply(uint32_t k, Acc& acc) const {
     const DevEvent e = ev[k];
     if (e.kind != 1) return 0;
     if (has_edge(S, e.u, e.v)) {
-      delete_edge(S, e.u, e.v);
+      delete_edge(S, e.u, e.v, acc.dg);
     } else {
       atomicMin(&ctl->first_absent, k);
     }
@@ -113,13 +154,13 @@ struct ShadowOp {
 
 // sparsifier.cpp:207-216 set_edge_weight.
 __device__ __forceinline__ bool set_edge_weight(const DevGraph<kCapH>& h, uint32_t u, uint32_t v,
-                                                double target) {
+                                                double target, long long& dh) {
   const double current = edge_weight(h, u, v);
   if (target > current) {
-    return insert_edge(h, u, v, __dsub_rn(target, current)) >= 0;
+    return insert_edge(h, u, v, __dsub_rn(target, current), dh) >= 0;
   } else if (target < current) {
-    delete_edge(h, u, v);
-    return insert_edge(h, u, v, target) >= 0;
+    delete_edge(h, u, v, dh);
+    return insert_edge(h, u, v, target, dh) >= 0;
   }
   return true;
 }
@@ -192,20 +233,22 @@ struct CommitOp {
     }
   }
 
-  __device__ void account(unsigned long long steps) const {
-    atomicAdd(&ctl->report[kWalkerSteps], steps);
-    atomicMax(&ctl->report[kMaxEventSteps], steps);
+  __device__ void flush(const Acc& a) const { flush_acc(a, ctl, G.edges, H.edges); }
+
+  __device__ static void account(Acc& acc, unsigned long long steps) {
+    acc.r[kWalkerSteps] += steps;
+    if (steps > acc.r[kMaxEventSteps]) acc.r[kMaxEventSteps] = steps;
   }
 
-  __device__ uint32_t apply(uint32_t k) const {
+  __device__ uint32_t apply(uint32_t k, Acc& acc) const {
     const DevEvent e = ev[k];
     const uint32_t u = e.u, v = e.v;
     const uint32_t s = slot[k];
     unsigned long long steps = 0;
     if (e.kind == 0) {
       // :473-488
-      atomicAdd(&ctl->report[kInsSeen], 1ull);
-      if (insert_edge(G, u, v, e.weight) < 0) return kErrPool;
+      acc.r[kInsSeen] += 1;
+      if (insert_edge(G, u, v, e.weight, acc.dg) < 0) return kErrPool;
       bool have = false, reached = false;
       if (s != kNoSlot) {
         have = true;
@@ -220,23 +263,23 @@ struct CommitOp {
         const double total = edge_weight(G, u, v);
         kept = !(o.K != 0.0 && have && reached);
         if (has_edge(H, u, v)) {
-          if (!set_edge_weight(H, u, v, total)) return kErrPool;
+          if (!set_edge_weight(H, u, v, total, acc.dh)) return kErrPool;
         } else if (kept) {
-          if (insert_edge(H, u, v, total) < 0) return kErrPool;
+          if (insert_edge(H, u, v, total, acc.dh) < 0) return kErrPool;
         }
       }
-      atomicAdd(&ctl->report[kept ? kInsKept : kInsPruned], 1ull);
+      acc.r[kept ? kInsKept : kInsPruned] += 1;
       dec[k] = kept ? 0u : 1u;
-      account(steps);
+      account(acc, steps);
       return 0;
     }
     // Deletion (:489-523)
-    atomicAdd(&ctl->report[kDelSeen], 1ull);
-    if (!delete_edge(G, u, v)) return kErrAbsent;
+    acc.r[kDelSeen] += 1;
+    if (!delete_edge(G, u, v, acc.dg)) return kErrAbsent;
     uint32_t outcome = 0, added = 0;
     if (has_edge(H, u, v)) {
-      atomicAdd(&ctl->report[kDelInH], 1ull);
-      delete_edge(H, u, v);
+      acc.r[kDelInH] += 1;
+      delete_edge(H, u, v, acc.dh);
       if (!o.freeze) {
         bool path = false;
         if (s != kNoSlot) {
@@ -249,11 +292,11 @@ struct CommitOp {
           for (uint32_t i = 0; i + 1 < len; ++i) {
             const uint32_t a = p[i], bb = p[i + 1];
             if (!has_edge(H, a, bb)) {
-              if (insert_edge(H, a, bb, edge_weight(G, a, bb)) < 0) return kErrPool;
+              if (insert_edge(H, a, bb, edge_weight(G, a, bb), acc.dh) < 0) return kErrPool;
               ++added;
             }
           }
-          atomicAdd(&ctl->report[kPaths], 1ull);
+          acc.r[kPaths] += 1;
           outcome = 1;
         } else {
           // run_local_fallback (:264-280): u then v.
@@ -263,43 +306,59 @@ struct CommitOp {
             if (H.slab[x].deg != 0 || G.slab[x].deg == 0) continue;
             double bw = 0.0;
             const uint32_t b = best_neighbor(G, x, kNoVertex, &bw);
-            if (insert_edge(H, x, b, bw) < 0) return kErrPool;
+            if (insert_edge(H, x, b, bw, acc.dh) < 0) return kErrPool;
             ++added;
           }
-          atomicAdd(&ctl->report[kFallbacks], 1ull);
+          acc.r[kFallbacks] += 1;
           outcome = 2;
         }
-        atomicAdd(&ctl->report[kEdgesRec], static_cast<unsigned long long>(added));
+        acc.r[kEdgesRec] += added;
       } else {
-        atomicAdd(&ctl->report[kFallbacks], 1ull);
+        acc.r[kFallbacks] += 1;
         outcome = 2;
       }
     }
     dec[k] = outcome | (added << 8);
-    account(steps);
+    account(acc, steps);
     return 0;
   }
 };
 
-// Query build (sparsifier.cpp:429-457) on batch-start H / G and the shadow.
-__global__ void k_flags(DevGraph<kCapH> H, DevGraph<kCapG> G, DevGraph<kCapG> S,
-                        const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
+// Query build (sparsifier.cpp:429-457), phase 1 on batch-start H and G:
+// insertion flags and w_pq = G.w(u,v) + w (:441). Runs before the walk
+// shadow is applied to G.
+__global__ void k_flags_ins(DevGraph<kCapH> H, DevGraph<kCapG> G,
+                            const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o,
+                            BatchDev b) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nb || batch_aborted(b.ctl)) return;
   const DevEvent e = ev[k];
   unsigned long long flag = 0;
-  if (e.kind == 0) {
-    if (o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) flag = 1ull;
-  } else if (!o.freeze && has_edge(H, e.u, e.v) && S.slab[e.u].deg > 0 && S.slab[e.v].deg > 0) {
-    flag = 1ull << 32;
+  if (e.kind == 0 && o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) {
+    flag = 1ull;
+    b.wpq[k] = __dadd_rn(edge_weight(G, e.u, e.v), e.weight);
   }
   b.scan_in[k] = flag;
   b.state[k] = 0;
   b.dec[k] = 0;
 }
 
-__global__ void k_scatter(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, uint32_t nb,
-                          uint64_t counter, BatchDev b) {
+// Phase 2, deletions: batch-start H (:447) and shadow degrees (:448). With
+// deletions in the batch G currently IS the shadow (see k_save_rows).
+__global__ void k_flags_del(DevGraph<kCapH> H, DevGraph<kCapG> S,
+                            const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o,
+                            BatchDev b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb || batch_aborted(b.ctl)) return;
+  const DevEvent e = ev[k];
+  if (e.kind == 1 && !o.freeze && has_edge(H, e.u, e.v) && S.slab[e.u].deg > 0 &&
+      S.slab[e.v].deg > 0)
+    b.scan_in[k] = 1ull << 32;
+  b.state[k] = 0;
+}
+
+__global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t counter,
+                          BatchDev b) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nb || batch_aborted(b.ctl)) return;
   const unsigned long long f = b.scan_in[k];
@@ -313,7 +372,7 @@ __global__ void k_scatter(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, ui
     ReachQuery q;
     q.p = e.u;
     q.q = e.v;
-    q.w_pq = __dadd_rn(edge_weight(G, e.u, e.v), e.weight);  // :441
+    q.w_pq = b.wpq[k];
     q.update_id = uid;
     b.rq[ri] = q;
     s = ri;
@@ -332,13 +391,55 @@ __global__ void k_scatter(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, ui
   }
 }
 
+// Walk shadow without copying G (sparsifier.cpp:416-423 deep-copies it):
+// every row a batch deletion will touch is saved once (first claimer of a
+// per-vertex stamp), the deletions are then applied to G in place, the
+// recovery walks run on G, and k_restore_rows puts the saved rows back
+// before the event-order commit. Deletions never relocate a row, so a row's
+// overflow block index and capacity are unchanged by the shadow pass.
+__global__ void k_save_rows(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, uint32_t nb,
+                            uint32_t stamp, BatchDev b) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * nb || batch_aborted(b.ctl)) return;
+  const DevEvent e = ev[t >> 1];
+  if (e.kind != 1) return;
+  const uint32_t row = (t & 1) ? e.v : e.u;
+  if (atomicExch(b.mark + row, stamp) == stamp) return;
+  const uint32_t idx = atomicAdd(&b.ctl->n_saved, 1u);
+  b.saved_rows[idx] = row;
+  const Slab<kCapG> sl = G.slab[row];
+  b.side_slab[idx] = sl;
+  if (sl.ext != kInline) {
+    const unsigned long long off = atomicAdd(b.side_top, static_cast<unsigned long long>(sl.deg));
+    b.side_off[idx] = off;
+    for (uint32_t i = 0; i < sl.deg; ++i) {
+      b.side_id[off + i] = G.pool_id[sl.ext + i];
+      b.side_w[off + i] = G.pool_w[sl.ext + i];
+    }
+  }
+}
+
+__global__ void k_restore_rows(DevGraph<kCapG> G, BatchDev b) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= b.ctl->n_saved) return;
+  const uint32_t row = b.saved_rows[idx];
+  const Slab<kCapG> sl = b.side_slab[idx];
+  G.slab[row] = sl;
+  if (sl.ext != kInline) {
+    const unsigned long long off = b.side_off[idx];
+    for (uint32_t i = 0; i < sl.deg; ++i) {
+      G.pool_id[sl.ext + i] = b.side_id[off + i];
+      G.pool_w[sl.ext + i] = b.side_w[off + i];
+    }
+  }
+}
+
 __global__ void k_finish(const unsigned long long* g_cnt, const unsigned long long* h_cnt,
-                         const unsigned long long* s_top, BatchCtl* ctl) {
+                         BatchCtl* ctl) {
   ctl->g_pool_top = g_cnt[0];
   ctl->g_edges = g_cnt[1];
   ctl->h_pool_top = h_cnt[0];
   ctl->h_edges = h_cnt[1];
-  ctl->s_pool_top = s_top ? *s_top : 0ull;
 }
 
 unsigned grid_for(uint64_t n, unsigned bs = 256) {
@@ -460,23 +561,34 @@ int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, cudaStream_t st)
   return 1;
 }
 
-int launch_shadow(const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb, int coop_blocks,
-                  cudaStream_t st) {
-  ShadowOp op{S, b.events, b.ctl};
-  cuda_check(cudaMemsetAsync(b.state, 0, nb, st), "memset state");
-  return launch_rounds(op, nb, b, coop_blocks, st);
-}
-
-int launch_queries(const DevGraph<kCapH>& H, const DevGraph<kCapG>& G,
-                   const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb, uint64_t counter,
-                   const WalkOpts& o, cudaStream_t st) {
+int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b,
+                   uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
+                   const WalkOpts& o, int coop_blocks, cudaStream_t st) {
   if (nb == 0) return 0;
-  k_flags<<<grid_for(nb), 256, 0, st>>>(H, G, S, b.events, nb, o, b);
+  int l = 0;
+  k_flags_ins<<<grid_for(nb), 256, 0, st>>>(H, G, b.events, nb, o, b);
+  ++l;
+  if (n_del > 0) {
+    k_save_rows<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, stamp, b);
+    ++l;
+    // The shadow pass must not move G's |E| counter: give it a scratch one.
+    DevGraph<kCapG> Gs = G;
+    Gs.edges = b.scratch_edges;
+    ShadowOp op{Gs, b.events, b.ctl};
+    l += launch_rounds(op, nb, b, coop_blocks, st);
+    k_flags_del<<<grid_for(nb), 256, 0, st>>>(H, G, b.events, nb, o, b);
+    ++l;
+  }
   size_t temp = b.cub_temp_bytes;
   cuda_check(cub::DeviceScan::ExclusiveSum(b.cub_temp, temp, b.scan_in, b.scan_out, nb, st),
              "query scan");
-  k_scatter<<<grid_for(nb), 256, 0, st>>>(G, b.events, nb, counter, b);
-  return 3;
+  k_scatter<<<grid_for(nb), 256, 0, st>>>(b.events, nb, counter, b);
+  return l + 2;
+}
+
+int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st) {
+  k_restore_rows<<<grid_for(2ull * nb), 256, 0, st>>>(G, b);
+  return 1;
 }
 
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
@@ -519,9 +631,9 @@ int launch_unpack(const BatchDev& b, uint32_t nq_r, uint32_t nq_m, int world, ui
   return l;
 }
 
-int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H,
-                  const unsigned long long* s_pool_top, const BatchDev& b, cudaStream_t st) {
-  k_finish<<<1, 1, 0, st>>>(G.pool_top, H.pool_top, s_pool_top, b.ctl);
+int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
+                  cudaStream_t st) {
+  k_finish<<<1, 1, 0, st>>>(G.pool_top, H.pool_top, b.ctl);
   return 1;
 }
 

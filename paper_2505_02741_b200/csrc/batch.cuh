@@ -61,7 +61,10 @@ struct BatchCtl {
   unsigned long long report[kReportFields];
   WalkCounters reach;
   WalkCounters minpath;
-  unsigned long long g_edges, h_edges, g_pool_top, h_pool_top, s_pool_top;
+  unsigned long long g_edges, h_edges, g_pool_top, h_pool_top;
+  unsigned int n_saved;  // rows saved for the in-place walk shadow
+  unsigned long long side_top;       // side-pool entries used by saved rows
+  unsigned long long scratch_edges;  // |E| sink of the shadow pass
 };
 
 struct WalkOpts {
@@ -86,6 +89,16 @@ struct BatchDev {
   MinOut mout;
   MinScratch mscratch;
   uint32_t* dec;           // per-event outcome (kind | edges_added << 8)
+  double* wpq;             // per-event insertion w_pq (batch-start G)
+  // In-place walk shadow (k_save_rows / k_restore_rows).
+  uint32_t* mark;          // per-vertex batch stamp
+  uint32_t* saved_rows;
+  Slab<kCapG>* side_slab;
+  unsigned long long* side_off;
+  uint32_t* side_id;
+  double* side_w;
+  unsigned long long* side_top;       // = &ctl->side_top
+  unsigned long long* scratch_edges;  // = &ctl->scratch_edges
   unsigned long long* locks;  // per-vertex row reservations
   unsigned long long* round_ctr;
   BatchCtl* ctl;
@@ -95,15 +108,16 @@ struct BatchDev {
 
 // Host launchers (batch.cu); each returns kernels launched.
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, cudaStream_t st);
-int launch_shadow(const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb, int coop_blocks,
-                  cudaStream_t st);
-int launch_queries(const DevGraph<kCapH>& H, const DevGraph<kCapG>& G,
-                   const DevGraph<kCapG>& S, const BatchDev& b, uint32_t nb,
-                   uint64_t counter, const WalkOpts& o, cudaStream_t st);
+// Query build; with deletions in the batch it also saves the touched G
+// rows and applies the walk shadow to G in place (undo: launch_restore).
+int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b,
+                   uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
+                   const WalkOpts& o, int coop_blocks, cudaStream_t st);
+int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st);
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, const WalkOpts& o, int coop_blocks, cudaStream_t st);
-int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H,
-                  const unsigned long long* s_pool_top, const BatchDev& b, cudaStream_t st);
+int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
+                  cudaStream_t st);
 size_t scan_temp_bytes(uint32_t nb_cap);
 
 // Multi-GPU exchange records. Reach: 16 B per query.

@@ -195,10 +195,11 @@ __device__ __forceinline__ void row_remove_at(const DevGraph<C>& g, uint32_t u, 
 }
 
 // graph.cpp:64-85 insert_edge on validated input. Returns 0 New,
-// 1 Coalesced, -1 pool exhausted.
+// 1 Coalesced, -1 pool exhausted. |E| changes are accumulated into
+// `dedges` by the caller (flushed once per warp, not one atomic per edge).
 template <int C>
 __device__ __forceinline__ int insert_edge(const DevGraph<C>& g, uint32_t u, uint32_t v,
-                                           double w) {
+                                           double w, long long& dedges) {
   const int i = row_find(g, u, v);
   if (i >= 0) {
     const RowRef<C> ru = row(g, u);
@@ -209,17 +210,18 @@ __device__ __forceinline__ int insert_edge(const DevGraph<C>& g, uint32_t u, uin
   }
   if (!row_push(g, u, v, w)) return -1;
   if (!row_push(g, v, u, w)) return -1;
-  atomicAdd(g.edges, 1ull);
+  ++dedges;
   return 0;
 }
 // graph.cpp:87-112 delete_edge. Returns false when absent (Data error).
 template <int C>
-__device__ __forceinline__ bool delete_edge(const DevGraph<C>& g, uint32_t u, uint32_t v) {
+__device__ __forceinline__ bool delete_edge(const DevGraph<C>& g, uint32_t u, uint32_t v,
+                                            long long& dedges) {
   const int i = row_find(g, u, v);
   if (i < 0) return false;
   row_remove_at(g, u, static_cast<uint32_t>(i));
   row_remove_at(g, v, static_cast<uint32_t>(row_find(g, v, u)));
-  atomicAdd(g.edges, static_cast<unsigned long long>(-1ll));
+  --dedges;
   return true;
 }
 

@@ -90,7 +90,7 @@ struct dyg_session {
   uint32_t n = 0;
   int coop_blocks = 0;
 
-  GraphStore<kCapG> G, S, G_snap;
+  GraphStore<kCapG> G, G_snap;
   GraphStore<kCapH> H, H_snap;
   uint64_t counter = 0, counter_snap = 0;
   uint64_t g_edges = 0, h_edges = 0, g_top = 0, h_top = 0;
@@ -104,6 +104,8 @@ struct dyg_session {
   unsigned long long* d_locks = nullptr;
   unsigned long long* d_round = nullptr;
   unsigned int* d_work = nullptr;  // walk work counter
+  uint64_t side_cap = 0;           // side-pool entries allocated
+  uint32_t stamp = 0;              // batch stamp for the row-save marks
   DevEvent* d_events = nullptr;
   DevEvent* h_events_pinned = nullptr;
   BatchCtl* h_ctl = nullptr;
@@ -163,6 +165,10 @@ void free_batch(dyg_session* s) {
   dev_free(b.mscratch.paths);
   dev_free(b.mscratch.rvals);
   dev_free(b.dec);
+  dev_free(b.wpq);
+  dev_free(b.saved_rows);
+  dev_free(b.side_slab);
+  dev_free(b.side_off);
   cudaFree(b.cub_temp);
   b.cub_temp = nullptr;
   dev_free(s->d_events);
@@ -190,6 +196,10 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.rout.steps, cap, "reach out");
     dev_alloc(&b.rout.best_bits, cap, "reach out");
     dev_alloc(&b.dec, cap, "decisions");
+    dev_alloc(&b.wpq, cap, "w_pq");
+    dev_alloc(&b.saved_rows, 2ull * cap, "saved rows");
+    dev_alloc(&b.side_slab, 2ull * cap, "saved slabs");
+    dev_alloc(&b.side_off, 2ull * cap, "saved offsets");
     dev_alloc(&s->d_events, cap, "batch events");
     check(cudaMallocHost(reinterpret_cast<void**>(&s->h_events_pinned), sizeof(DevEvent) * cap),
           "pinned events");
@@ -223,6 +233,18 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.mscratch.rvals, cap * T1, "minpath scratch");
     s->nd_cap = cap;
   }
+}
+
+// Side pool for saved overflow rows: bounded by G's pool (each row is saved
+// at most once per batch).
+void ensure_side_pool(dyg_session* s) {
+  const uint64_t need = s->G.pool_capacity();
+  if (s->side_cap >= need && s->b.side_id != nullptr) return;
+  dev_free(s->b.side_id);
+  dev_free(s->b.side_w);
+  dev_alloc(&s->b.side_id, need, "side pool");
+  dev_alloc(&s->b.side_w, need, "side pool");
+  s->side_cap = need;
 }
 
 WalkOpts walk_opts(const dyg_session* s) {
@@ -309,20 +331,21 @@ void phase_prepare(dyg_session* s, Pending& p) {
   c.first_absent = 0xFFFFFFFFu;
   c.limit = p.nb;
   c.use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
+  b.side_top = &b.ctl->side_top;
+  b.scratch_edges = &b.ctl->scratch_edges;
+  if (p.n_del > 0) ensure_side_pool(s);
   check(cudaMemcpyAsync(b.ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->stream), "ctl upload");
   s->stats.h2d_bytes += sizeof c;
   check(cudaEventRecord(s->t_total.a, s->stream), "event");
   p.launches += launch_validate(b, p.nb, s->n, s->stream);
   maybe_sync(s, "validate");
-  if (p.n_del > 0) {
-    s->S.copy_from(s->G, s->stream);
-    ++p.launches;
-    p.launches += launch_shadow(s->S.view(), b, p.nb, s->coop_blocks, s->stream);
-    maybe_sync(s, "shadow");
+  if (p.n_del > 0 && ++s->stamp == 0) {  // stamps restart: clear the marks
+    check(cudaMemsetAsync(b.mark, 0, sizeof(uint32_t) * s->n, s->stream), "marks");
+    s->stamp = 1;
   }
-  p.launches += launch_queries(s->H.view(), s->G.view(), p.n_del > 0 ? s->S.view() : s->G.view(),
-                               b, p.nb, s->counter, o, s->stream);
-  maybe_sync(s, "queries");
+  p.launches += launch_queries(s->H.view(), s->G.view(), b, p.nb, p.n_del, s->counter,
+                               s->stamp, o, s->coop_blocks, s->stream);
+  maybe_sync(s, "queries + walk shadow");
 }
 
 // Walks over query ranges. Full range (single GPU): counts stay on the
@@ -360,7 +383,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     const uint64_t T1 = static_cast<uint64_t>(o.T) + 1;
     MinOut mo{b.mout.has_path + lo_m, b.mout.path_len + lo_m, b.mout.steps + lo_m,
               b.mout.resistance + lo_m, b.mout.paths + lo_m * T1};
-    p.launches += launch_minpath(s->S.view(), b.mq + lo_m, cnt_m, max_m, Pd, b.mscratch, mo,
+    p.launches += launch_minpath(s->G.view(), b.mq + lo_m, cnt_m, max_m, Pd, b.mscratch, mo,
                                  &b.ctl->minpath, s->d_work, s->stream);
     maybe_sync(s, "minpath walks");
   }
@@ -373,11 +396,11 @@ void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
   BatchDev& b = s->b;
   BatchCtl& c = *s->h_ctl;
   check(cudaEventRecord(s->t_commit.a, s->stream), "event");
+  if (p.n_del > 0) p.launches += launch_restore(s->G.view(), b, p.nb, s->stream);
   p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, o, s->coop_blocks, s->stream);
   maybe_sync(s, "commit");
   check(cudaEventRecord(s->t_commit.b, s->stream), "event");
-  p.launches += launch_finish(s->G.view(), s->H.view(),
-                              p.n_del > 0 ? s->S.pool_top_ptr() : nullptr, b, s->stream);
+  p.launches += launch_finish(s->G.view(), s->H.view(), b, s->stream);
   check(cudaEventRecord(s->t_total.b, s->stream), "event");
   check(cudaMemcpyAsync(&c, b.ctl, sizeof c, cudaMemcpyDeviceToHost, s->stream), "ctl download");
   if (p.nb == 1)
@@ -600,6 +623,8 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       check(cudaMemset(s->d_locks, 0, sizeof(unsigned long long) * s->n), "locks");
       dev_alloc(&s->d_round, 1, "round counter");
       dev_alloc(&s->d_work, 1, "walk work counter");
+      dev_alloc(&s->b.mark, s->n, "row marks");
+      check(cudaMemset(s->b.mark, 0, sizeof(uint32_t) * s->n), "row marks");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
       dev_alloc(&s->b.ctl, 1, "batch ctl");
       dev_alloc(&s->d_counts, 2, "shard counts");
@@ -639,6 +664,9 @@ void dyg_session_destroy(dyg_session* s) {
   dev_free(s->d_locks);
   dev_free(s->d_round);
   dev_free(s->d_work);
+  dev_free(s->b.mark);
+  dev_free(s->b.side_id);
+  dev_free(s->b.side_w);
   dev_free(s->d_stream);
   if (s->h_ctl) cudaFreeHost(s->h_ctl);
   if (s->h_counts) cudaFreeHost(s->h_counts);
@@ -648,7 +676,6 @@ void dyg_session_destroy(dyg_session* s) {
   s->t_min.destroy();
   s->t_commit.destroy();
   s->G.release();
-  s->S.release();
   s->G_snap.release();
   s->H.release();
   s->H_snap.release();
