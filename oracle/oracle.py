@@ -108,6 +108,7 @@ class Oracle:
         vp, u32, u64, dbl, i32, sz = C.c_void_p, C.c_uint32, C.c_uint64, C.c_double, C.c_int, C.c_size_t
         sig = {
             "orc_last_error": (C.c_char_p, []),
+            "orc_last_error_kind": (i32, []),
             "orc_impl_name": (C.c_char_p, []),
             "orc_graph_new": (vp, [u32]),
             "orc_graph_clone": (vp, [vp]),
@@ -156,7 +157,7 @@ class Oracle:
 
     def _checkp(self, p):
         if not p:
-            raise OracleError(0, self.lib.orc_last_error().decode())
+            raise OracleError(self.lib.orc_last_error_kind(), self.lib.orc_last_error().decode())
         return p
 
     # -- graphs -----------------------------------------------------------

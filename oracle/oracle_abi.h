@@ -88,6 +88,7 @@ typedef struct orc_report {
 
 /* Status codes: 0 ok, else ErrorKind (error.hpp:9): 1 Usage, 2 Data, 3 Numeric. */
 const char* orc_last_error(void);
+int orc_last_error_kind(void);
 const char* orc_impl_name(void);
 
 /* ---- graph (graph.hpp:23-68) ---- */

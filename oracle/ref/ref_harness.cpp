@@ -27,13 +27,16 @@ using namespace dysparse;
 namespace {
 
 thread_local std::string g_error;
+thread_local int g_kind = 0;
 
 int fail(const Error& e) {
   g_error = e.what();
-  return static_cast<int>(e.kind());
+  g_kind = static_cast<int>(e.kind());
+  return g_kind;
 }
 int fail_other(const std::exception& e) {
   g_error = e.what();
+  g_kind = 2;
   return 2;
 }
 
@@ -73,6 +76,7 @@ struct State {
 extern "C" {
 
 const char* orc_last_error(void) { return g_error.c_str(); }
+int orc_last_error_kind(void) { return g_kind; }
 const char* orc_impl_name(void) { return "reference"; }
 
 void* orc_graph_new(uint32_t n) {

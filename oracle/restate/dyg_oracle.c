@@ -41,6 +41,7 @@ static int set_err(int kind, const char* fmt, ...) {
   return kind;
 }
 const char* orc_last_error(void) { return g_err; }
+int orc_last_error_kind(void) { return g_err_kind; }
 const char* orc_impl_name(void) { return "restate"; }
 
 /* ------------------------------------------------------------------- rng */
