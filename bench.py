@@ -368,6 +368,8 @@ def run_ours(args):
         "device_ms_per_step": stats["total_ms"] / args.steps,
         "walker_steps_per_step": (stats["reach_steps"] + stats["minpath_steps"]) / args.steps,
         "commit_rounds_per_step": stats["commit_rounds"] / args.steps,
+        "commit_ms_per_step_deletion_batches": stats["commit_ms_deletion"] / args.steps,
+        "commit_rounds_per_step_deletion_batches": stats["commit_rounds_deletion"] / args.steps,
         "clocks": clocks.summary(),
     }
     del launches

@@ -138,6 +138,8 @@ typedef struct dyg_stats {
   uint64_t pool_capacity;
   uint64_t h2d_bytes;
   uint64_t d2h_bytes;
+  double commit_ms_deletion;    /* commit_ms share of batches containing deletions */
+  uint64_t commit_rounds_deletion;
 } dyg_stats;
 
 typedef struct dyg_session dyg_session;

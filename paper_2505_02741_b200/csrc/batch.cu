@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
       if (k >= lim || b.state[k] != 0) continue;
       const unsigned long long key = (round << 32) | (0xFFFFFFFFull - k);
       op.for_rows(k, [&](uint32_t row) { atomicMax(b.locks + row, key); });
+      op.prefetch(k);
     }
     grid.sync();
     for (uint32_t k = tid; k < nev; k += nth) {
@@ -122,6 +123,62 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
   }
 }
 
+// Warp-per-event variant for batches with deletions: the lanes of a warp
+// reserve an event's rows (path vertices) in parallel and apply it together
+// (path recovery is parallel over path edges, CommitOp::apply_warp). Same
+// round protocol as k_rounds.
+template <class Op>
+__global__ void __launch_bounds__(256) k_rounds_warp(Op op, uint32_t nev, BatchDev b) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
+  const uint32_t lane = tid & 31;
+  const uint32_t wid = tid >> 5;
+  const uint32_t nw = static_cast<uint32_t>(grid.size()) >> 5;
+  volatile BatchCtl* ctl = b.ctl;
+  if (ctl->val_err != ~0ull) return;
+  Acc acc{};
+  unsigned long long round = *b.round_ctr;
+  uint32_t r = 0;
+  for (;; ++r) {
+    ++round;
+    const uint32_t lim = op.limit();
+    if (tid == 0) ctl->remaining[(r + 1) % 3] = 0;
+    for (uint32_t k = wid; k < nev; k += nw) {
+      if (k >= lim || b.state[k] != 0) continue;
+      const unsigned long long key = (round << 32) | (0xFFFFFFFFull - k);
+      op.for_rows_warp(k, lane, [&](uint32_t row) { atomicMax(b.locks + row, key); });
+    }
+    grid.sync();
+    for (uint32_t k = wid; k < nev; k += nw) {
+      if (k >= lim || b.state[k] != 0) continue;
+      const unsigned long long key = (round << 32) | (0xFFFFFFFFull - k);
+      bool ready = true;
+      op.for_rows_warp(k, lane, [&](uint32_t row) {
+        if (ready && *reinterpret_cast<volatile unsigned long long*>(b.locks + row) != key)
+          ready = false;
+      });
+      ready = __all_sync(0xFFFFFFFFu, ready);
+      if (ready) {
+        const uint32_t e = op.apply_warp(k, lane, acc);
+        if (lane == 0) {
+          b.state[k] = e ? 2 : 1;
+          if (e) atomicMin(&b.ctl->commit_err, (static_cast<unsigned long long>(k) << 8) | e);
+        }
+      } else if (lane == 0) {
+        atomicAdd(&b.ctl->remaining[r % 3], 1u);
+      }
+      __syncwarp();
+    }
+    grid.sync();
+    if (ctl->remaining[r % 3] == 0) break;
+  }
+  op.flush(acc);
+  if (tid == 0) {
+    *b.round_ctr = round;
+    ctl->rounds = ctl->rounds + r + 1;
+  }
+}
+
 // Walk shadow (sparsifier.cpp:416-423): apply the batch's deletions to the
 // copy of G in event order, skipping absent edges. first_absent records the
 // lowest deletion that found no edge: in a deletion-only batch that is
@@ -131,6 +188,7 @@ struct ShadowOp {
   const DevEvent* ev;
   BatchCtl* ctl;
   __device__ uint32_t limit() const { return 0xFFFFFFFFu; }
+  __device__ void prefetch(uint32_t) const {}
   template <class F>
   __device__ void for_rows(uint32_t k, F&& f) const {
     const DevEvent& e = ev[k];
@@ -194,6 +252,7 @@ struct CommitOp {
   const uint32_t* slot;
   ReachOut rout;
   MinOut mout;
+  MinScratch mscratch;
   uint32_t* dec;
   BatchCtl* ctl;
   WalkOpts o;
@@ -231,6 +290,145 @@ struct CommitOp {
       const uint32_t bv = best_neighbor(G, e.v, e.u, nullptr);
       if (bv != kNoVertex) f(bv);
     }
+  }
+
+  // Lane-parallel row list: index 0 -> u, 1 -> v, then the recovery path
+  // vertices or the two fallback candidates.
+  template <class F>
+  __device__ void for_rows_warp(uint32_t k, uint32_t lane, F&& f) const {
+    const DevEvent& e = ev[k];
+    uint32_t n = 2;
+    const uint32_t* p = nullptr;
+    bool fallback = false;
+    if (e.kind == 1 && !o.freeze) {
+      const uint32_t s = slot[k];
+      if (s != kNoSlot && mout.has_path[s]) {
+        p = path_of(s);
+        n = 2 + mout.path_len[s];
+      } else {
+        fallback = true;
+        n = 4;
+      }
+    }
+    for (uint32_t i = lane; i < n; i += 32) {
+      uint32_t row;
+      if (i == 0) row = e.u;
+      else if (i == 1) row = e.v;
+      else if (!fallback) row = p[i - 2];
+      else row = i == 2 ? best_neighbor(G, e.u, e.v, nullptr) : best_neighbor(G, e.v, e.u, nullptr);
+      if (row != kNoVertex) f(row);
+    }
+  }
+
+  // Pull an insertion's four slabs toward L2 one grid barrier before the
+  // apply phase needs them.
+  __device__ void prefetch(uint32_t k) const {
+    const DevEvent& e = ev[k];
+    if (e.kind != 0) return;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(G.slab + e.u));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(G.slab + e.v));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(H.slab + e.u));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(H.slab + e.v));
+  }
+
+  // Warp-cooperative apply. Insertions run on lane 0. A deletion's path
+  // recovery (sparsifier.cpp:503-514) runs over path edges in parallel: the
+  // loop-erased path has distinct vertices, hence distinct edges, so each
+  // edge's live-H membership and live-G weight are independent of the other
+  // path edges' insertions; the appends then go row by row -- row p[j]
+  // receives p[j-1] (from edge j-1) before p[j+1] (from edge j), exactly
+  // the sequential order.
+  __device__ uint32_t apply_warp(uint32_t k, uint32_t lane, Acc& acc) const {
+    constexpr unsigned kAll = 0xFFFFFFFFu;
+    const DevEvent e = ev[k];
+    if (e.kind == 0) {
+      uint32_t err = 0;
+      if (lane == 0) err = apply(k, acc);
+      return __shfl_sync(kAll, err, 0);
+    }
+    const uint32_t u = e.u, v = e.v;
+    const uint32_t s = slot[k];
+    // Lane 0: G delete, H membership, H delete (:490-494).
+    uint32_t stage = 0;  // 0 error/graph-only/freeze done, 1 path recovery, 2 fallback
+    uint32_t err = 0;
+    unsigned long long steps = 0;
+    if (lane == 0) {
+      acc.r[kDelSeen] += 1;
+      if (!delete_edge(G, u, v, acc.dg)) {
+        err = kErrAbsent;
+      } else if (has_edge(H, u, v)) {
+        acc.r[kDelInH] += 1;
+        delete_edge(H, u, v, acc.dh);
+        if (!o.freeze) {
+          bool path = false;
+          if (s != kNoSlot) {
+            steps = mout.steps[s];
+            path = mout.has_path[s] != 0;
+          }
+          stage = path ? 1u : 2u;
+        } else {
+          acc.r[kFallbacks] += 1;
+          dec[k] = 2u;
+        }
+      } else {
+        dec[k] = 0u;
+      }
+    }
+    __syncwarp();  // lane 0's row updates visible to the other lanes
+    err = __shfl_sync(kAll, err, 0);
+    if (err) return err;
+    stage = __shfl_sync(kAll, stage, 0);
+    uint32_t added = 0;
+    if (stage == 1) {
+      const uint32_t* p = path_of(s);
+      const uint32_t len = mout.path_len[s];
+      double* need_w = mscratch.rvals + static_cast<uint64_t>(s) * (o.T + 1ull);
+      // Phase 1: per edge i, w if H lacks (p[i], p[i+1]) else -1.
+      for (uint32_t i = lane; i + 1 < len; i += 32) {
+        const uint32_t a = p[i], bb = p[i + 1];
+        need_w[i] = has_edge(H, a, bb) ? -1.0 : edge_weight(G, a, bb);
+      }
+      __syncwarp();
+      // Phase 2: row p[j] appends p[j-1] then p[j+1] where needed.
+      uint32_t my_added = 0, fail = 0;
+      for (uint32_t j = lane; j < len; j += 32) {
+        const uint32_t x = p[j];
+        if (j >= 1 && need_w[j - 1] > 0.0) {
+          if (!row_push(H, x, p[j - 1], need_w[j - 1])) fail = 1;
+        }
+        if (j + 1 < len && need_w[j] > 0.0) {
+          if (!row_push(H, x, p[j + 1], need_w[j])) fail = 1;
+          ++my_added;
+        }
+      }
+      added = static_cast<uint32_t>(warp_sum(my_added));
+      if (__any_sync(kAll, fail)) return kErrPool;
+      if (lane == 0) {
+        acc.dh += added;
+        acc.r[kPaths] += 1;
+        acc.r[kEdgesRec] += added;
+        dec[k] = 1u | (added << 8);
+      }
+    } else if (stage == 2 && lane == 0) {
+      // run_local_fallback (:264-280): u then v.
+      const uint32_t ends[2] = {u, v};
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t x = ends[j];
+        if (H.slab[x].deg != 0 || G.slab[x].deg == 0) continue;
+        double bw = 0.0;
+        const uint32_t b = best_neighbor(G, x, kNoVertex, &bw);
+        if (insert_edge(H, x, b, bw, acc.dh) < 0) {
+          err = kErrPool;
+          break;
+        }
+        ++added;
+      }
+      acc.r[kFallbacks] += 1;
+      acc.r[kEdgesRec] += added;
+      dec[k] = 2u | (added << 8);
+    }
+    if (lane == 0) account(acc, steps);
+    return __shfl_sync(kAll, err, 0);
   }
 
   __device__ void flush(const Acc& a) const { flush_acc(a, ctl, G.edges, H.edges); }
@@ -358,7 +556,7 @@ __global__ void k_flags_del(DevGraph<kCapH> H, DevGraph<kCapG> S,
 }
 
 __global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t counter,
-                          BatchDev b) {
+                          uint64_t seed, BatchDev b) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nb || batch_aborted(b.ctl)) return;
   const unsigned long long f = b.scan_in[k];
@@ -373,14 +571,14 @@ __global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t
     q.p = e.u;
     q.q = e.v;
     q.w_pq = b.wpq[k];
-    q.update_id = uid;
+    q.qseed = query_seed(seed, uid);
     b.rq[ri] = q;
     s = ri;
   } else if (f >> 32) {
     MinQuery q;
     q.p = e.u;
     q.q = e.v;
-    q.update_id = uid;
+    q.qseed = query_seed(seed, uid);
     b.mq[mi] = q;
     s = mi;
   }
@@ -520,32 +718,50 @@ __global__ void k_unpack_min(MinOut m, uint32_t nq, int world, uint32_t slots, u
   for (uint32_t j = threadIdx.x; j < h->path_len; j += blockDim.x) dst[j] = path[j];
 }
 
-template <class Op>
-int launch_rounds(const Op& op, uint32_t nev, const BatchDev& b, int coop_blocks,
-                  cudaStream_t st) {
+// Co-resident grid for a cooperative kernel (cached per kernel).
+template <typename K>
+int coop_blocks_for(K kernel) {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    cached = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return cached;
+}
+
+template <bool kWarp, class Op>
+int launch_rounds(const Op& op, uint32_t nev, const BatchDev& b, cudaStream_t st) {
   if (nev == 0) return 0;
   Op op_copy = op;
   BatchDev b_copy = b;
   void* args[] = {&op_copy, &nev, &b_copy};
-  const int need = static_cast<int>(grid_for(nev));
-  const int blocks = need < coop_blocks ? need : coop_blocks;
-  cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&k_rounds<Op>), dim3(blocks),
-                                         dim3(256), args, 0, st),
-             "cooperative round launch");
+  if constexpr (kWarp) {
+    auto kern = k_rounds_warp<Op>;
+    const int need = static_cast<int>(grid_for(static_cast<uint64_t>(nev) * 32));
+    const int cap = coop_blocks_for(kern);
+    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern),
+                                           dim3(need < cap ? need : cap), dim3(256), args, 0, st),
+               "cooperative round launch");
+  } else {
+    auto kern = k_rounds<Op>;
+    const int need = static_cast<int>(grid_for(nev));
+    const int cap = coop_blocks_for(kern);
+    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern),
+                                           dim3(need < cap ? need : cap), dim3(256), args, 0, st),
+               "cooperative round launch");
+  }
   return 1;
 }
 
 }  // namespace
 
 int coop_grid_blocks(int device) {
-  int sms = 0, per_sm_a = 0, per_sm_b = 0;
+  int sms = 0;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, k_rounds<CommitOp>, 256, 0),
-             "occupancy");
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_rounds<ShadowOp>, 256, 0),
-             "occupancy");
-  const int per_sm = per_sm_a < per_sm_b ? per_sm_a : per_sm_b;
-  return sms * (per_sm > 0 ? per_sm : 1);
+  return sms;
 }
 
 size_t scan_temp_bytes(uint32_t nb_cap) {
@@ -575,14 +791,14 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
     DevGraph<kCapG> Gs = G;
     Gs.edges = b.scratch_edges;
     ShadowOp op{Gs, b.events, b.ctl};
-    l += launch_rounds(op, nb, b, coop_blocks, st);
+    l += launch_rounds<false>(op, nb, b, st);
     k_flags_del<<<grid_for(nb), 256, 0, st>>>(H, G, b.events, nb, o, b);
     ++l;
   }
   size_t temp = b.cub_temp_bytes;
   cuda_check(cub::DeviceScan::ExclusiveSum(b.cub_temp, temp, b.scan_in, b.scan_out, nb, st),
              "query scan");
-  k_scatter<<<grid_for(nb), 256, 0, st>>>(b.events, nb, counter, b);
+  k_scatter<<<grid_for(nb), 256, 0, st>>>(b.events, nb, counter, o.seed, b);
   return l + 2;
 }
 
@@ -592,9 +808,9 @@ int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cud
 }
 
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  uint32_t nb, const WalkOpts& o, int coop_blocks, cudaStream_t st) {
-  CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.dec, b.ctl, o};
-  return launch_rounds(op, nb, b, coop_blocks, st);
+                  uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st) {
+  CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.mscratch, b.dec, b.ctl, o};
+  return n_del > 0 ? launch_rounds<true>(op, nb, b, st) : launch_rounds<false>(op, nb, b, st);
 }
 
 int launch_pack(const BatchDev& b, uint32_t lo_r, uint32_t n_r, uint32_t lo_m, uint32_t n_m,

@@ -114,8 +114,9 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
                    uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
                    const WalkOpts& o, int coop_blocks, cudaStream_t st);
 int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st);
+// n_del > 0 selects the warp-per-event round engine (parallel path recovery).
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  uint32_t nb, const WalkOpts& o, int coop_blocks, cudaStream_t st);
+                  uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st);
 int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   cudaStream_t st);
 size_t scan_temp_bytes(uint32_t nb_cap);

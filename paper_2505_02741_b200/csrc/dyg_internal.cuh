@@ -44,6 +44,15 @@ __host__ __device__ __forceinline__ uint64_t walker_seed(uint64_t global_seed, u
   h = hash_mix(h ^ (update_id + 0xBF58476D1CE4E5B9ull));
   return hash_mix(h ^ (walker + 0x94D049BB133111EBull));
 }
+// walker_seed split at its query-level part: the first two mixes depend only
+// on (global_seed, update_id) and are computed once per query.
+__host__ __device__ __forceinline__ uint64_t query_seed(uint64_t global_seed, uint64_t update_id) {
+  const uint64_t h = hash_mix(global_seed + 0x9E3779B97F4A7C15ull);
+  return hash_mix(h ^ (update_id + 0xBF58476D1CE4E5B9ull));
+}
+__host__ __device__ __forceinline__ uint64_t walker_seed_from(uint64_t qseed, uint64_t walker) {
+  return hash_mix(qseed ^ (walker + 0x94D049BB133111EBull));
+}
 // The k-th (1-based) SplitMix64 draw of a stream seeded `seed` is
 // hash_mix(seed + k*gamma) (rng.hpp:7-13); next_double = (x >> 11) * 2^-53
 // (rng.hpp:24). Counter form: a lane computes step t's draw (k = t + 1)

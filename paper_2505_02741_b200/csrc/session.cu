@@ -354,7 +354,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                 uint32_t n_m) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
-  WalkParams P{o.K, o.T, o.s, o.seed};
+  const WalkParams P = make_walk_params(o.K, o.T, o.s, o.seed);
   const uint32_t* cnt_r = &b.ctl->nq_reach;
   const uint32_t* cnt_m = &b.ctl->nq_min;
   uint32_t max_r = p.n_ins, max_m = p.n_del;
@@ -397,7 +397,7 @@ void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
   BatchCtl& c = *s->h_ctl;
   check(cudaEventRecord(s->t_commit.a, s->stream), "event");
   if (p.n_del > 0) p.launches += launch_restore(s->G.view(), b, p.nb, s->stream);
-  p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, o, s->coop_blocks, s->stream);
+  p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
   maybe_sync(s, "commit");
   check(cudaEventRecord(s->t_commit.b, s->stream), "event");
   p.launches += launch_finish(s->G.view(), s->H.view(), b, s->stream);
@@ -433,6 +433,10 @@ void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
   s->stats.reach_queries += c.nq_reach;
   s->stats.minpath_queries += c.nq_min;
   s->stats.commit_rounds += c.rounds;
+  if (p.n_del > 0) {
+    s->stats.commit_ms_deletion += s->t_commit.ms();
+    s->stats.commit_rounds_deletion += c.rounds;
+  }
   s->stats.reach_ms += s->t_reach.ms();
   s->stats.minpath_ms += s->t_min.ms();
   s->stats.commit_ms += s->t_commit.ms();
@@ -1060,15 +1064,15 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
     for (size_t i = 0; i < n_queries; ++i) {
       const dyg_walk_query& q = queries[i];
       if (q.kind == 0) {
-        rq.push_back(ReachQuery{q.p, q.q, q.w_pq, q.update_id});
+        rq.push_back(ReachQuery{q.p, q.q, q.w_pq, query_seed(cfg->global_seed, q.update_id)});
         ri.push_back(i);
       } else {
-        mq.push_back(MinQuery{q.p, q.q, q.update_id});
+        mq.push_back(MinQuery{q.p, q.q, query_seed(cfg->global_seed, q.update_id)});
         mi.push_back(i);
       }
     }
-    const WalkParams P{cfg->distortion_threshold, cfg->step_cap, cfg->walker_count,
-                       cfg->global_seed};
+    const WalkParams P = make_walk_params(cfg->distortion_threshold, cfg->step_cap,
+                                          cfg->walker_count, cfg->global_seed);
     const uint64_t T1 = static_cast<uint64_t>(cfg->step_cap) + 1;
     WalkCounters* ctr = nullptr;
     uint32_t* d_n = nullptr;

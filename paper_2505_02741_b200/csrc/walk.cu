@@ -181,13 +181,17 @@ __global__ void __launch_bounds__(256, kMinBlocks)
   const uint32_t total_work = *nq_dev * P.s;
   __shared__ uint4 stage_all[8 * Gather<C>::kWarpWords];
   uint4* stage = stage_all + (threadIdx.x >> 5) * Gather<C>::kWarpWords;
-  // Warp-uniform chunk of 32 work items [chunk_base, chunk_base + 32); lane
-  // i holds item chunk_base + i's query, prefetched when the chunk is taken.
+  // Warp-uniform chunk of 32 work items [chunk_base, chunk_base + 32): item
+  // chunk_base + i's query endpoints, w_pq and walker seed are prefetched by
+  // lane i into shared memory when the chunk is taken.
+  __shared__ uint2 chunk_pq_all[8 * 32];
+  __shared__ double chunk_w_all[8 * 32];
+  __shared__ unsigned long long chunk_seed_all[8 * 32];
+  uint2* chunk_pq = chunk_pq_all + (threadIdx.x >> 5) * 32;
+  double* chunk_w = chunk_w_all + (threadIdx.x >> 5) * 32;
+  unsigned long long* chunk_seed = chunk_seed_all + (threadIdx.x >> 5) * 32;
   uint32_t chunk_base = 0, chunk_pos = 32, chunk_end = 32;
   bool drained = false;
-  uint32_t pf_p = 0, pf_q = 0;
-  double pf_w = 1.0;
-  unsigned long long pf_uid = 0;
 
   bool has = false;
   uint32_t qi = 0, cur = 0, prev = kNoVertex, target_v = 0, steps = 0, w_idx = 0;
@@ -206,42 +210,42 @@ __global__ void __launch_bounds__(256, kMinBlocks)
           drained = true;
           break;
         }
+        __syncwarp();  // every lane has read the previous chunk
         chunk_base = base;
         chunk_pos = 0;
         chunk_end = min(32u, total_work - base);
         const uint32_t w = base + lane;
         if (w < total_work) {
-          const uint32_t q = w / P.s;
+          const uint32_t q = P.s_shift != kNoShift ? (w >> P.s_shift) : w / P.s;
+          const uint32_t wi = w - q * P.s;
+          uint64_t qseed;
           if (kMinPath) {
             const MinQuery Q = mq[q];
-            pf_p = Q.p;
-            pf_q = Q.q;
-            pf_uid = Q.update_id;
+            chunk_pq[lane] = make_uint2(Q.p, Q.q);
+            chunk_w[lane] = 1.0;
+            qseed = Q.qseed;
           } else {
             const ReachQuery Q = rq[q];
-            pf_p = Q.p;
-            pf_q = Q.q;
-            pf_w = Q.w_pq;
-            pf_uid = Q.update_id;
+            chunk_pq[lane] = make_uint2(Q.p, Q.q);
+            chunk_w[lane] = Q.w_pq;
+            qseed = Q.qseed;
           }
+          chunk_seed[lane] = walker_seed_from(qseed, wi);
         }
+        __syncwarp();
       }
       const uint32_t rank = __popc(need & ((1u << lane) - 1u));
       const uint32_t take = min(static_cast<uint32_t>(__popc(need)), chunk_end - chunk_pos);
-      const uint32_t from = (chunk_pos + rank) & 31u;
-      const uint32_t p = __shfl_sync(kFull, pf_p, from);
-      const uint32_t q = __shfl_sync(kFull, pf_q, from);
-      const double wq = __shfl_sync(kFull, pf_w, from);
-      const unsigned long long uid = __shfl_sync(kFull, pf_uid, from);
       const bool mine = ((need >> lane) & 1u) && rank < take;
       if (mine) {
-        w_idx = chunk_base + chunk_pos + rank;
-        qi = w_idx / P.s;
-        const uint32_t wi = w_idx - qi * P.s;
-        cur = p;
-        target_v = q;
-        w_pq = kMinPath ? 1.0 : wq;
-        rng = walker_seed(P.seed, uid, wi);
+        const uint32_t item = chunk_pos + rank;
+        w_idx = chunk_base + item;
+        qi = P.s_shift != kNoShift ? (w_idx >> P.s_shift) : w_idx / P.s;
+        const uint2 pq = chunk_pq[item];
+        cur = pq.x;
+        target_v = pq.y;
+        w_pq = chunk_w[item];
+        rng = chunk_seed[item];
         prev = kNoVertex;
         steps = 0;
         acc = 0.0;

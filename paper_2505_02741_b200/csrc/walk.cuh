@@ -14,21 +14,33 @@ namespace dyg {
 
 enum Terminal : uint32_t { kReached = 0, kBudget = 1, kStepCap = 2, kDeadEnd = 3 };  // walk.hpp:20
 
+constexpr uint32_t kNoShift = 0xFFFFFFFFu;
+
 struct WalkParams {
-  double K;        // distortion threshold (budget)
-  uint32_t T;      // step cap
-  uint32_t s;      // walkers per query
-  uint64_t seed;   // global seed
+  double K;          // distortion threshold (budget)
+  uint32_t T;        // step cap
+  uint32_t s;        // walkers per query
+  uint64_t seed;     // global seed
+  uint32_t s_shift;  // log2(s) when s is a power of two, else kNoShift
 };
+
+inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t seed) {
+  uint32_t sh = kNoShift;
+  if (s && (s & (s - 1)) == 0) {
+    sh = 0;
+    while ((1u << sh) != s) ++sh;
+  }
+  return WalkParams{K, T, s, seed, sh};
+}
 
 struct ReachQuery {   // WalkQuery Reach (walk.hpp:71-78)
   uint32_t p, q;
   double w_pq;
-  uint64_t update_id;
+  uint64_t qseed;   // query_seed(global_seed, update_id)
 };
 struct MinQuery {     // WalkQuery MinPath
   uint32_t p, q;
-  uint64_t update_id;
+  uint64_t qseed;
 };
 
 // Per-query outputs of the reach walk (ReachVerdict, walk.hpp:29-33).
