@@ -253,11 +253,11 @@ def run_ours(args):
 
     def step_device():
         st.restore()
+        if sharded is None:
+            st.replay_uploaded_range(0, nb)  # device-resident replay(stream)
+            return
         for b in range(nb):
-            if sharded is None:
-                st.replay_uploaded(b)
-            else:
-                sharded.replay_events(batches[b][0], batches[b][1], b)
+            sharded.replay_events(batches[b][0], batches[b][1], b)
 
     def step_e2e():
         st.restore()

@@ -177,6 +177,13 @@ int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* p
 int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
                       uint32_t batch_count);
 int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* out);
+/* SparsifierState::replay over batches [first, first + count) of the
+ * uploaded stream (sparsifier.cpp:550-559): all batches are enqueued back to
+ * back with one host synchronisation; out[i] is batch first + i. On an error
+ * the batches before the failing one are committed and reported, the
+ * failing one returns the reference's error, and later ones do not run. */
+int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
+                              dyg_batch_report* out);
 
 /* SparsifierState::apply_insertion / apply_deletion (sparsifier.cpp:243-317).
  * decision: 0 Kept, 1 Pruned (InsertionDecision). kind: 0 GraphOnly,

@@ -386,6 +386,13 @@ class SparsifierState:
         _check(_lib.lib().dyg_replay_uploaded(self._s, batch_index, ptr(rep)))
         return BatchReport.from_record(rep[0])
 
+    def replay_uploaded_range(self, first: int, count: int) -> list:
+        """Batches [first, first+count) of the uploaded stream, enqueued back to
+        back with one host sync (the device-side replay())."""
+        rep = np.zeros(max(count, 1), REPORT_DTYPE)
+        _check(_lib.lib().dyg_replay_uploaded_range(self._s, first, count, ptr(rep)))
+        return [BatchReport.from_record(rep[i]) for i in range(count)]
+
     def snapshot(self) -> None:
         _check(_lib.lib().dyg_session_snapshot(self._s))
 

@@ -21,9 +21,13 @@ __device__ __forceinline__ bool batch_aborted(const BatchCtl* ctl) {
 // sparsifier.cpp:321-337 validate_event_shape; the lowest failing event
 // wins (the reference validates in stream order before walking).
 __global__ void k_validate(const DevEvent* __restrict__ ev, uint32_t nb, uint32_t n,
-                           BatchCtl* ctl) {
+                           BatchCtl* ctl, const unsigned int* __restrict__ abort_flag) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nb) return;
+  if (*abort_flag) {  // an earlier batch of this range failed: do nothing
+    if (k == 0) atomicMin(&ctl->val_err, static_cast<unsigned long long>(kErrAborted));
+    return;
+  }
   const DevEvent e = ev[k];
   uint32_t code = 0;
   if (e.u >= n || e.v >= n) {
@@ -633,7 +637,10 @@ __global__ void k_restore_rows(DevGraph<kCapG> G, BatchDev b) {
 }
 
 __global__ void k_finish(const unsigned long long* g_cnt, const unsigned long long* h_cnt,
-                         BatchCtl* ctl) {
+                         BatchCtl* ctl, unsigned int* abort_flag) {
+  if (ctl->val_err != ~0ull || ctl->commit_err != ~0ull ||
+      (ctl->use_absent_limit && ctl->first_absent != 0xFFFFFFFFu))
+    *abort_flag = 1;
   ctl->g_pool_top = g_cnt[0];
   ctl->g_edges = g_cnt[1];
   ctl->h_pool_top = h_cnt[0];
@@ -771,9 +778,10 @@ size_t scan_temp_bytes(uint32_t nb_cap) {
   return temp;
 }
 
-int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, cudaStream_t st) {
+int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
+                    cudaStream_t st) {
   if (nb == 0) return 0;
-  k_validate<<<grid_for(nb), 256, 0, st>>>(b.events, nb, n, b.ctl);
+  k_validate<<<grid_for(nb), 256, 0, st>>>(b.events, nb, n, b.ctl, abort_flag);
   return 1;
 }
 
@@ -848,8 +856,8 @@ int launch_unpack(const BatchDev& b, uint32_t nq_r, uint32_t nq_m, int world, ui
 }
 
 int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  cudaStream_t st) {
-  k_finish<<<1, 1, 0, st>>>(G.pool_top, H.pool_top, b.ctl);
+                  unsigned int* abort_flag, cudaStream_t st) {
+  k_finish<<<1, 1, 0, st>>>(G.pool_top, H.pool_top, b.ctl, abort_flag);
   return 1;
 }
 

@@ -46,6 +46,7 @@ enum EventError : uint32_t {
   kErrWeight = 3,      // "non-positive weight"
   kErrAbsent = 4,      // delete_edge: "edge (u, v) does not exist"
   kErrPool = 5,        // overflow pool exhausted (device)
+  kErrAborted = 6,     // an earlier batch of the same enqueued range failed
 };
 
 struct BatchCtl {
@@ -107,7 +108,8 @@ struct BatchDev {
 };
 
 // Host launchers (batch.cu); each returns kernels launched.
-int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, cudaStream_t st);
+int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
+                    cudaStream_t st);
 // Query build; with deletions in the batch it also saves the touched G
 // rows and applies the walk shadow to G in place (undo: launch_restore).
 int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b,
@@ -118,7 +120,7 @@ int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cud
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st);
 int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  cudaStream_t st);
+                  unsigned int* abort_flag, cudaStream_t st);
 size_t scan_temp_bytes(uint32_t nb_cap);
 
 // Multi-GPU exchange records. Reach: 16 B per query.

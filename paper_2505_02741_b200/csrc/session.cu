@@ -32,6 +32,10 @@ struct ApiError {
 template <typename F>
 int guarded(F&& f) {
   try {
+    // Launch checks read cudaGetLastError(): start every entry point from a
+    // clean slate so a non-sticky error left by an earlier unchecked call
+    // (e.g. a free during teardown) is not misattributed.
+    cudaGetLastError();
     f();
     return DYG_OK;
   } catch (const ApiError& e) {
@@ -75,7 +79,10 @@ struct Timer {
   }
   float ms() const {
     float t = 0.f;
-    cudaEventElapsedTime(&t, a, b);
+    if (cudaEventElapsedTime(&t, a, b) != cudaSuccess) {
+      cudaGetLastError();
+      return 0.f;
+    }
     return t;
   }
 };
@@ -130,9 +137,15 @@ struct dyg_session {
   uint32_t shard_nq_r = 0, shard_nq_m = 0;
   std::chrono::steady_clock::time_point shard_wall0;
   int shard_launches = 0;
+  uint64_t shard_counter = 0;
 
   dyg_stats stats{};
-  Timer t_total, t_reach, t_min, t_commit;
+  Timer timers[4];                 // per-batch path: total, reach, minpath, commit
+  std::vector<Timer> range_timers; // batch-range path, 4 per batch
+  BatchCtl* d_ctls = nullptr;      // batch-range control blocks
+  BatchCtl* h_ctls = nullptr;
+  uint32_t ctl_cap = 0;
+  unsigned int* d_abort = nullptr; // set by a failing batch; later batches no-op
   bool debug_sync = false;
 };
 
@@ -283,9 +296,10 @@ std::string event_error_message(uint32_t code, uint64_t pos, const DevEvent& e) 
   return buf;
 }
 
-// One deferred batch in three phases, so the multi-GPU split
-// (dyg_shard_*) can run the walk phase on a query range and exchange
-// results before the replicated commit.
+// One deferred batch in phases, so the multi-GPU split (dyg_shard_*) can
+// run the walk phase on a query range and exchange results before the
+// replicated commit, and so a device-resident stream can enqueue many
+// batches back to back with a single host sync (dyg_replay_uploaded_range).
 struct Pending {
   const DevEvent* dev = nullptr;
   const DevEvent* host = nullptr;
@@ -294,7 +308,20 @@ struct Pending {
   bool imm_msgs = false;
   std::chrono::steady_clock::time_point wall0;
   int launches = 0;
+  BatchCtl* dctl = nullptr;   // device control block of this batch
+  BatchCtl* hctl = nullptr;   // pinned host copy
+  uint32_t* hdec = nullptr;   // pinned: decision of a 1-event batch
+  Timer* tm = nullptr;        // [0] total, [1] reach, [2] minpath, [3] commit
+  uint64_t counter_base = 0;  // update_counter at batch start
 };
+
+void bind_pending(dyg_session* s, Pending& p) {
+  p.dctl = s->b.ctl;
+  p.hctl = s->h_ctl;
+  p.hdec = &s->h_counts[2];
+  p.tm = s->timers;
+  p.counter_base = s->counter;
+}
 
 [[noreturn]] void fail_validation(dyg_session* s, const Pending& p, unsigned long long val_err) {
   const uint32_t k = static_cast<uint32_t>(val_err >> 8);
@@ -309,22 +336,27 @@ struct Pending {
   fail(DYG_ERR_DATA, msg);
 }
 
+// Pool headroom for appends of n_ins insertions and n_del deletions
+// (sparsifier.cpp:474,483,503-519), with a 4x factor for relocations.
+void ensure_pools(dyg_session* s, uint64_t n_ins, uint64_t n_del) {
+  const uint64_t T1 = static_cast<uint64_t>(s->opt.walk.step_cap) + 1;
+  const uint64_t g_app = 2ull * n_ins;
+  const uint64_t h_app = 2ull * n_ins + n_del * (2 * T1 + 4);
+  s->G.ensure_pool(s->g_top, 4 * g_app + (1u << 16), s->stream);
+  s->H.ensure_pool(s->h_top, 4 * h_app + (1u << 16), s->stream);
+}
+
 // validate (:405-407), walk shadow (:416-423), query build (:429-457).
 void phase_prepare(dyg_session* s, Pending& p) {
   const WalkOpts o = walk_opts(s);
-  const uint64_t T1 = static_cast<uint64_t>(o.T) + 1;
   ensure_batch(s, p.nb, p.n_del);
-  // Pool headroom: appends this batch can make (sparsifier.cpp:474,483,
-  // 503-519), with a 4x factor for slab->pool relocations.
-  const uint64_t g_app = 2ull * p.n_ins;
-  const uint64_t h_app = 2ull * p.n_ins + p.n_del * (2 * T1 + 4);
-  s->G.ensure_pool(s->g_top, 4 * g_app + (1u << 16), s->stream);
-  s->H.ensure_pool(s->h_top, 4 * h_app + (1u << 16), s->stream);
+  ensure_pools(s, p.n_ins, p.n_del);
   BatchDev& b = s->b;
+  b.ctl = p.dctl;
   b.events = const_cast<DevEvent*>(p.dev);
   b.locks = s->d_locks;
   b.round_ctr = s->d_round;
-  BatchCtl& c = *s->h_ctl;
+  BatchCtl& c = *p.hctl;
   std::memset(&c, 0, sizeof c);
   c.val_err = ~0ull;
   c.commit_err = ~0ull;
@@ -336,14 +368,14 @@ void phase_prepare(dyg_session* s, Pending& p) {
   if (p.n_del > 0) ensure_side_pool(s);
   check(cudaMemcpyAsync(b.ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->stream), "ctl upload");
   s->stats.h2d_bytes += sizeof c;
-  check(cudaEventRecord(s->t_total.a, s->stream), "event");
-  p.launches += launch_validate(b, p.nb, s->n, s->stream);
+  check(cudaEventRecord(p.tm[0].a, s->stream), "event");
+  p.launches += launch_validate(b, p.nb, s->n, s->d_abort, s->stream);
   maybe_sync(s, "validate");
   if (p.n_del > 0 && ++s->stamp == 0) {  // stamps restart: clear the marks
     check(cudaMemsetAsync(b.mark, 0, sizeof(uint32_t) * s->n, s->stream), "marks");
     s->stamp = 1;
   }
-  p.launches += launch_queries(s->H.view(), s->G.view(), b, p.nb, p.n_del, s->counter,
+  p.launches += launch_queries(s->H.view(), s->G.view(), b, p.nb, p.n_del, p.counter_base,
                                s->stamp, o, s->coop_blocks, s->stream);
   maybe_sync(s, "queries + walk shadow");
 }
@@ -354,6 +386,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                 uint32_t n_m) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
+  b.ctl = p.dctl;
   const WalkParams P = make_walk_params(o.K, o.T, o.s, o.seed);
   const uint32_t* cnt_r = &b.ctl->nq_reach;
   const uint32_t* cnt_m = &b.ctl->nq_min;
@@ -368,15 +401,15 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     max_r = n_r;
     max_m = n_m;
   }
-  check(cudaEventRecord(s->t_reach.a, s->stream), "event");
+  check(cudaEventRecord(p.tm[1].a, s->stream), "event");
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
     p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
                                s->d_work, s->stream);
     maybe_sync(s, "reach walks");
   }
-  check(cudaEventRecord(s->t_reach.b, s->stream), "event");
-  check(cudaEventRecord(s->t_min.a, s->stream), "event");
+  check(cudaEventRecord(p.tm[1].b, s->stream), "event");
+  check(cudaEventRecord(p.tm[2].a, s->stream), "event");
   if (p.n_del > 0 && !o.freeze && max_m > 0) {
     WalkParams Pd = P;
     Pd.K = std::numeric_limits<double>::infinity();  // sparsifier.cpp:458-459
@@ -387,26 +420,33 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                                  &b.ctl->minpath, s->d_work, s->stream);
     maybe_sync(s, "minpath walks");
   }
-  check(cudaEventRecord(s->t_min.b, s->stream), "event");
+  check(cudaEventRecord(p.tm[2].b, s->stream), "event");
 }
 
-// Commit (:466-533), report (:535-537), error mapping.
-void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
+// Commit (:466-533) enqueue: restore the shadowed rows, run the commit
+// engine, snapshot the counters and copy the control block back (async).
+void commit_enqueue(dyg_session* s, Pending& p) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
-  BatchCtl& c = *s->h_ctl;
-  check(cudaEventRecord(s->t_commit.a, s->stream), "event");
+  b.ctl = p.dctl;
+  check(cudaEventRecord(p.tm[3].a, s->stream), "event");
   if (p.n_del > 0) p.launches += launch_restore(s->G.view(), b, p.nb, s->stream);
   p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
   maybe_sync(s, "commit");
-  check(cudaEventRecord(s->t_commit.b, s->stream), "event");
-  p.launches += launch_finish(s->G.view(), s->H.view(), b, s->stream);
-  check(cudaEventRecord(s->t_total.b, s->stream), "event");
-  check(cudaMemcpyAsync(&c, b.ctl, sizeof c, cudaMemcpyDeviceToHost, s->stream), "ctl download");
+  check(cudaEventRecord(p.tm[3].b, s->stream), "event");
+  p.launches += launch_finish(s->G.view(), s->H.view(), b, s->d_abort, s->stream);
+  check(cudaEventRecord(p.tm[0].b, s->stream), "event");
+  check(cudaMemcpyAsync(p.hctl, b.ctl, sizeof(BatchCtl), cudaMemcpyDeviceToHost, s->stream),
+        "ctl download");
   if (p.nb == 1)
-    check(cudaMemcpyAsync(&s->h_counts[2], b.dec, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                          s->stream), "decision download");
-  check(cudaStreamSynchronize(s->stream), "batch");
+    check(cudaMemcpyAsync(p.hdec, b.dec, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream),
+          "decision download");
+}
+
+// After the stream has synchronised: error mapping (:525-529), counters and
+// the BatchReport (:535-537).
+void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
+  const BatchCtl& c = *p.hctl;
   s->stats.d2h_bytes += sizeof c;
   s->stats.kernel_launches += p.launches;
   s->stats.batches += 1;
@@ -434,21 +474,21 @@ void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
   s->stats.minpath_queries += c.nq_min;
   s->stats.commit_rounds += c.rounds;
   if (p.n_del > 0) {
-    s->stats.commit_ms_deletion += s->t_commit.ms();
+    s->stats.commit_ms_deletion += p.tm[3].ms();
     s->stats.commit_rounds_deletion += c.rounds;
   }
-  s->stats.reach_ms += s->t_reach.ms();
-  s->stats.minpath_ms += s->t_min.ms();
-  s->stats.commit_ms += s->t_commit.ms();
-  s->stats.total_ms += s->t_total.ms();
+  s->stats.reach_ms += p.tm[1].ms();
+  s->stats.minpath_ms += p.tm[2].ms();
+  s->stats.commit_ms += p.tm[3].ms();
+  s->stats.total_ms += p.tm[0].ms();
   if (fail_k != ~0ull) {
-    s->counter += fail_k + 1;  // ++update_counter_ precedes the throw (:469)
+    s->counter = p.counter_base + fail_k + 1;  // ++update_counter_ precedes the throw (:469)
     const uint64_t pos = p.pos ? p.pos[fail_k] : fail_k;
     fail(fail_code == kErrPool ? DYG_ERR_DEVICE : DYG_ERR_DATA,
          event_error_message(fail_code, pos, p.host[fail_k]));
   }
-  s->counter += p.nb;
-  s->last_dec = p.nb == 1 ? s->h_counts[2] : 0;
+  s->counter = p.counter_base + p.nb;
+  s->last_dec = p.nb == 1 ? *p.hdec : 0;
   dyg_batch_report rep{};
   rep.batch_index = p.batch;
   rep.insertions_seen = c.report[kInsSeen];
@@ -468,12 +508,22 @@ void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
   *out = rep;
 }
 
+void phase_commit(dyg_session* s, Pending& p, dyg_batch_report* out) {
+  commit_enqueue(s, p);
+  check(cudaStreamSynchronize(s->stream), "batch");
+  commit_finalize(s, p, out);
+}
+
 void empty_report(dyg_session* s, uint32_t batch_index, dyg_batch_report* out) {
   dyg_batch_report rep{};
   rep.batch_index = batch_index;
   rep.density_graph = density_of(s->g_edges, s->n);
   rep.density_sparsifier = density_of(s->h_edges, s->n);
   *out = rep;
+}
+
+void reset_abort(dyg_session* s) {
+  check(cudaMemsetAsync(s->d_abort, 0, sizeof(unsigned int), s->stream), "abort flag");
 }
 
 void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* host_events,
@@ -484,6 +534,7 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
     return;
   }
   Pending p;
+  bind_pending(s, p);
   p.wall0 = std::chrono::steady_clock::now();
   p.dev = dev_events;
   p.host = host_events;
@@ -493,6 +544,7 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
   p.n_del = n_del;
   p.batch = batch_index;
   p.imm_msgs = immediate_msgs;
+  reset_abort(s);
   phase_prepare(s, p);
   phase_walk(s, p, true, 0, 0, 0, 0);
   phase_commit(s, p, out);
@@ -513,6 +565,76 @@ void run_host_batch(dyg_session* s, const dyg_event* ev, const uint64_t* positio
   }
   run_deferred(s, s->d_events, reinterpret_cast<const DevEvent*>(ev), positions,
                static_cast<uint32_t>(nb), n_ins, n_del, batch_index, out, immediate_msgs);
+}
+
+// Device-resident stream, batches [first, first + count) enqueued back to
+// back; one host sync at the end (the device-side replay(stream),
+// sparsifier.cpp:550-559). Buffers and pool headroom are sized for the whole
+// range up front; a failing batch raises the device abort flag so the later
+// batches of the range do nothing, and the error is reported for it.
+void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batch_report* out) {
+  if (count == 0) return;
+  uint64_t sum_ins = 0, sum_del = 0;
+  uint32_t max_nb = 0, max_nd = 0;
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t b = first + i;
+    if (b >= s->batch_cnt.size()) continue;
+    sum_ins += s->batch_ins[b];
+    sum_del += s->batch_del[b];
+    max_nb = std::max<uint32_t>(max_nb, static_cast<uint32_t>(s->batch_cnt[b]));
+    max_nd = std::max<uint32_t>(max_nd, static_cast<uint32_t>(s->batch_del[b]));
+  }
+  ensure_batch(s, std::max<uint32_t>(max_nb, 1), max_nd);
+  ensure_pools(s, sum_ins, sum_del);
+  if (sum_del > 0) ensure_side_pool(s);
+  if (s->ctl_cap < count) {
+    dev_free(s->d_ctls);
+    if (s->h_ctls) cudaFreeHost(s->h_ctls);
+    s->h_ctls = nullptr;
+    dev_alloc(&s->d_ctls, count, "batch control blocks");
+    check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctls), sizeof(BatchCtl) * count),
+          "pinned control blocks");
+    s->ctl_cap = count;
+  }
+  while (s->range_timers.size() < 4ull * count) {
+    s->range_timers.emplace_back();
+    s->range_timers.back().init();
+  }
+  std::vector<Pending> ps(count);
+  uint64_t counter = s->counter;
+  const auto wall0 = std::chrono::steady_clock::now();
+  reset_abort(s);
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t b = first + i;
+    Pending& p = ps[i];
+    p.batch = b;
+    p.wall0 = wall0;
+    p.dctl = s->d_ctls + i;
+    p.hctl = s->h_ctls + i;
+    p.hdec = &s->h_counts[2];
+    p.tm = s->range_timers.data() + 4ull * i;
+    p.counter_base = counter;
+    if (b >= s->batch_cnt.size() || s->batch_cnt[b] == 0) continue;
+    const uint64_t off = s->batch_off[b];
+    p.dev = s->d_stream + off;
+    p.host = reinterpret_cast<const DevEvent*>(s->stream_events.data() + off);
+    p.pos = s->stream_positions.data() + off;
+    p.nb = static_cast<uint32_t>(s->batch_cnt[b]);
+    p.n_ins = static_cast<uint32_t>(s->batch_ins[b]);
+    p.n_del = static_cast<uint32_t>(s->batch_del[b]);
+    phase_prepare(s, p);
+    phase_walk(s, p, true, 0, 0, 0, 0);
+    commit_enqueue(s, p);
+    counter += p.nb;
+  }
+  check(cudaStreamSynchronize(s->stream), "batch range");
+  for (uint32_t i = 0; i < count; ++i) {
+    if (ps[i].nb == 0) {
+      empty_report(s, ps[i].batch, &out[i]);
+      continue;
+    }
+    commit_finalize(s, ps[i], &out[i]);  // throws at the first failing batch
+  }
 }
 
 void accumulate(dyg_batch_report& acc, const dyg_batch_report& r) {
@@ -636,10 +758,9 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
             "pinned counts");
       check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctl), sizeof(BatchCtl)), "pinned ctl");
       s->coop_blocks = coop_grid_blocks(device);
-      s->t_total.init();
-      s->t_reach.init();
-      s->t_min.init();
-      s->t_commit.init();
+      for (Timer& t : s->timers) t.init();
+      dev_alloc(&s->d_abort, 1, "abort flag");
+      check(cudaMemset(s->d_abort, 0, sizeof(unsigned int)), "abort flag");
       ensure_batch(s, 1024, 256);
     } catch (...) {
       dyg_session_destroy(s);
@@ -675,10 +796,11 @@ void dyg_session_destroy(dyg_session* s) {
   if (s->h_ctl) cudaFreeHost(s->h_ctl);
   if (s->h_counts) cudaFreeHost(s->h_counts);
   dev_free(s->d_counts);
-  s->t_total.destroy();
-  s->t_reach.destroy();
-  s->t_min.destroy();
-  s->t_commit.destroy();
+  for (Timer& t : s->timers) t.destroy();
+  for (Timer& t : s->range_timers) t.destroy();
+  dev_free(s->d_ctls);
+  if (s->h_ctls) cudaFreeHost(s->h_ctls);
+  dev_free(s->d_abort);
   s->G.release();
   s->G_snap.release();
   s->H.release();
@@ -783,6 +905,19 @@ int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* 
                  s->stream_positions.data() + off, nb,
                  static_cast<uint32_t>(s->batch_ins[batch_index]),
                  static_cast<uint32_t>(s->batch_del[batch_index]), batch_index, out, false);
+  });
+}
+
+int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
+                              dyg_batch_report* out) {
+  return guarded([&] {
+    if (s == nullptr || (count && out == nullptr)) fail(DYG_ERR_USAGE, "null argument");
+    if (!s->have_stream) fail(DYG_ERR_USAGE, "no stream uploaded");
+    if (count && static_cast<uint64_t>(first) + count > s->stream_batches && s->stream_batches > 0)
+      fail(DYG_ERR_USAGE, "batch index out of range");
+    if (!s->opt.batched) fail(DYG_ERR_USAGE, "batch ranges need batched (deferred) mode");
+    check(cudaSetDevice(s->device), "set device");
+    run_uploaded_range(s, first, count, out);
   });
 }
 
@@ -938,6 +1073,7 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
     s->shard_del = n_del;
     s->shard_batch = batch_index;
     s->shard_wall0 = std::chrono::steady_clock::now();
+    s->shard_counter = s->counter;
     s->shard_nq_r = s->shard_nq_m = 0;
     if (n > 0) {
       ensure_batch(s, static_cast<uint32_t>(n), n_del);
@@ -946,6 +1082,8 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
                             cudaMemcpyHostToDevice, s->stream), "events upload");
       s->stats.h2d_bytes += sizeof(DevEvent) * n;
       Pending p;
+      bind_pending(s, p);
+      reset_abort(s);
       p.dev = s->d_events;
       p.host = s->shard_host.data();
       p.pos = s->shard_pos.data();
@@ -993,6 +1131,7 @@ int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
     if ((sl_r && reach_records == nullptr) || (sl_m && minpath_records == nullptr))
       fail(DYG_ERR_USAGE, "null record buffer");
     Pending p;
+    bind_pending(s, p);
     p.nb = s->shard_nb;
     p.n_ins = s->shard_ins;
     p.n_del = s->shard_del;
@@ -1019,6 +1158,8 @@ int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
     const uint32_t sl_r = static_cast<uint32_t>((s->shard_nq_r + world - 1ull) / world);
     const uint32_t sl_m = static_cast<uint32_t>((s->shard_nq_m + world - 1ull) / world);
     Pending p;
+    bind_pending(s, p);
+    p.counter_base = s->shard_counter;
     p.dev = s->d_events;
     p.host = s->shard_host.data();
     p.pos = s->shard_pos.data();

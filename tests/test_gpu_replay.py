@@ -250,3 +250,47 @@ def test_session_ctor_checks(dyg):
         dyg.SparsifierState(g, dyg.DynamicGraph(16),
                             dyg.SparsifierOptions(dyg.WalkConfig(10.0, 0, 16, 0), True, False))
     assert e.value.kind == dyg.ErrorKind.Usage
+
+
+def test_uploaded_range_equals_per_batch(oracle, dyg):
+    c, g, h, s = cfg_inputs(oracle, "C2")
+    opts = dyg.SparsifierOptions(dyg.WalkConfig(c.K, c.T, c.s, c.walk_seed), True, False)
+    a = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
+    b = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
+    stream = dyg.UpdateStream(s.events(), s.batch_count)
+    ra = [a.replay_batch(stream, k) for k in range(s.batch_count)]
+    b.upload_stream(stream)
+    rb = b.replay_uploaded_range(0, 7) + b.replay_uploaded_range(7, s.batch_count - 7)
+    for x, y in zip(ra, rb):
+        for f in O.REPORT_EXACT:
+            assert getattr(x, f) == getattr(y, f)
+    assert same_rows(a.rows(0), b.rows(0)) and same_rows(a.rows(1), b.rows(1))
+    assert a.update_counter == b.update_counter
+
+
+def test_uploaded_range_stops_at_failing_batch(oracle, dyg):
+    g = oracle.make_mesh(9, 9, 3)
+    h = oracle.build_initial_sparsifier(g, 0.1, 3)
+    rp, ids, _ = g.export()
+    edges = [(u, int(ids[i])) for u in range(len(rp) - 1) for i in range(rp[u], rp[u + 1])
+             if u < ids[i]]
+    ev = [(0, 0, 40, 0, 1.0), (0, 1, 50, 0, 1.0),            # batch 0: insertions
+          (1, edges[0][0], edges[0][1], 1, 0.0),             # batch 1: deletions,
+          (1, edges[0][0], edges[0][1], 1, 0.0),             #   the second fails
+          (0, 2, 60, 2, 1.0)]                                # batch 2: never runs
+    ev = np.array(ev, dtype=O.EVENT_DTYPE)
+    ost = oracle.state(g, h, K=10.0, T=30, s=8, seed=3)
+    ostream = oracle.stream(ev, 3)
+    r0 = ost.replay_batch(ostream, 0)
+    with pytest.raises(O.OracleError) as oe:
+        ost.replay_batch(ostream, 1)
+    st = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h),
+                             dyg.SparsifierOptions(dyg.WalkConfig(10.0, 30, 8, 3), True, False))
+    st.upload_stream(dyg.UpdateStream(ev, 3))
+    with pytest.raises(dyg.Error) as de:
+        st.replay_uploaded_range(0, 3)
+    assert str(de.value) == oe.value.message
+    assert st.update_counter == ost.update_counter
+    assert same_rows(ost.graph().export(), st.rows(0))
+    assert same_rows(ost.sparsifier().export(), st.rows(1))
+    assert r0["insertions_seen"] == 2
