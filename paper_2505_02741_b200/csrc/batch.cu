@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
   const uint32_t nth = static_cast<uint32_t>(grid.size());
   volatile BatchCtl* ctl = b.ctl;
   if (ctl->val_err != ~0ull) return;  // uniform: nothing below ran yet
+  if (ctl->fast && !ctl->not_simple) return;  // the insertion fast path committed it
   Acc acc{};
   unsigned long long round = *b.round_ctr;
   uint32_t r = 0;
@@ -536,9 +537,14 @@ __global__ void k_flags_ins(DevGraph<kCapH> H, DevGraph<kCapG> G,
   if (k >= nb || batch_aborted(b.ctl)) return;
   const DevEvent e = ev[k];
   unsigned long long flag = 0;
-  if (e.kind == 0 && o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) {
-    flag = 1ull;
-    b.wpq[k] = __dadd_rn(edge_weight(G, e.u, e.v), e.weight);
+  if (e.kind == 0) {
+    const double gw = edge_weight(G, e.u, e.v);
+    // Insertion fast path precondition: the key is new to G (no coalescing).
+    if (gw != 0.0) b.ctl->not_simple = 1;
+    if (o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) {
+      flag = 1ull;
+      b.wpq[k] = __dadd_rn(gw, e.weight);
+    }
   }
   b.scan_in[k] = flag;
   b.state[k] = 0;
@@ -636,8 +642,134 @@ __global__ void k_restore_rows(DevGraph<kCapG> G, BatchDev b) {
   }
 }
 
-__global__ void k_finish(const unsigned long long* g_cnt, const unsigned long long* h_cnt,
-                         BatchCtl* ctl, unsigned int* abort_flag) {
+// ---------------------------------------------------------------------------
+// Insertion fast path. In an insertion-only batch where every key is new to
+// G (k_flags_ins) and no key repeats within the batch (k_fp_check), event k's
+// whole commit (:473-488 with :220-241) is: push_back(u: v, w) and
+// push_back(v: u, w) into G, and -- when kept -- the same two appends into H
+// with weight G.w(u,v) = w. H lacks the key because H is a subgraph of G.
+// Rows only receive appends, in event order. Each append record r = 2k +
+// side (row u or v of event k) is counted per row and pushed onto the row's
+// lock-free list (k_fp_link); rows with one record (the vast majority) write
+// it directly, a row with several has one owner that applies them in
+// increasing r, i.e. event order (k_fp_write). Any violated precondition
+// sets not_simple BEFORE anything is written (k_fp_check) and the round
+// engine (k_rounds) commits the batch instead. The per-row counters and
+// list heads are left zeroed / empty for the next batch.
+__device__ __forceinline__ void fp_link(uint32_t* cnt, uint32_t* head, uint32_t* next,
+                                        uint32_t row, uint32_t r) {
+  atomicAdd(cnt + row, 1u);
+  next[r] = atomicExch(head + row, r);
+}
+
+__global__ void k_fp_link(const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
+  unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
+  if (live) {
+    const DevEvent e = ev[k];
+    const uint32_t s = b.slot[k];
+    bool have = false, reached = false;
+    if (s != kNoSlot) {
+      have = true;
+      reached = b.rout.reached[s] != 0;
+      steps = b.rout.steps[s];
+    }
+    const bool kept = !o.freeze && !(o.K != 0.0 && have && reached);
+    fp_link(b.fp_cnt[0], b.fp_head[0], b.fp_next[0], e.u, 2 * k);
+    fp_link(b.fp_cnt[0], b.fp_head[0], b.fp_next[0], e.v, 2 * k + 1);
+    if (kept) {
+      fp_link(b.fp_cnt[1], b.fp_head[1], b.fp_next[1], e.u, 2 * k);
+      fp_link(b.fp_cnt[1], b.fp_head[1], b.fp_next[1], e.v, 2 * k + 1);
+    }
+    b.fp_kept[k] = kept ? 1 : 0;
+    b.dec[k] = kept ? 0u : 1u;
+    (kept ? kept_n : pruned_n) = 1;
+  }
+  kept_n = warp_sum(kept_n);
+  pruned_n = warp_sum(pruned_n);
+  const unsigned long long steps_sum = warp_sum(steps);
+  const unsigned long long steps_max = warp_max(steps);
+  if ((threadIdx.x & 31) == 0 && (kept_n | pruned_n)) {
+    atomicAdd(&b.ctl->fp_report[kInsSeen], kept_n + pruned_n);
+    atomicAdd(&b.ctl->fp_report[kInsKept], kept_n);
+    atomicAdd(&b.ctl->fp_report[kInsPruned], pruned_n);
+    atomicAdd(&b.ctl->fp_report[kWalkerSteps], steps_sum);
+    atomicMax(&b.ctl->fp_report[kMaxEventSteps], steps_max);
+  }
+}
+
+__device__ __forceinline__ uint32_t rec_row(const DevEvent* ev, uint32_t rec) {
+  const DevEvent& e = ev[rec >> 1];
+  return (rec & 1) ? e.v : e.u;
+}
+__device__ __forceinline__ uint32_t other_end(const DevEvent* ev, uint32_t rec) {
+  const DevEvent& e = ev[rec >> 1];
+  return (rec & 1) ? e.u : e.v;
+}
+
+// A key repeated inside the batch shows up as a repeated neighbour on a
+// G row with several records; its list owner (the head) checks.
+__global__ void k_fp_check(const DevEvent* __restrict__ ev, uint32_t n, BatchDev b) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || batch_aborted(b.ctl) || b.ctl->not_simple) return;
+  const uint32_t row = rec_row(ev, r);
+  if (b.fp_cnt[0][row] < 2 || b.fp_head[0][row] != r) return;
+  for (uint32_t x = r; x != kNoSlot; x = b.fp_next[0][x])
+    for (uint32_t y = b.fp_next[0][x]; y != kNoSlot; y = b.fp_next[0][y])
+      if (other_end(ev, x) == other_end(ev, y)) b.ctl->not_simple = 1;
+}
+
+// Record r's row: a sole record appends directly; the list owner of a row
+// with several records appends them in increasing r (= event order) by
+// repeated minimum selection over the short list. Both reset the row's
+// counter and list head for the next batch, also when the batch fell back.
+template <int C>
+__device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* ev, uint32_t* cnt,
+                                         uint32_t* head, const uint32_t* next, uint32_t r,
+                                         bool write) {
+  const uint32_t row = rec_row(ev, r);
+  const uint32_t c = cnt[row];
+  if (c == 0 || (c > 1 && head[row] != r)) return true;
+  bool ok = true;
+  if (write) {
+    if (c == 1) {
+      ok = row_push(g, row, other_end(ev, r), ev[r >> 1].weight);
+    } else {
+      uint32_t last = 0;
+      for (uint32_t i = 0; i < c && ok; ++i) {
+        uint32_t best = kNoSlot;
+        for (uint32_t x = r; x != kNoSlot; x = next[x])
+          if ((i == 0 || x > last) && x < best) best = x;
+        ok = row_push(g, row, other_end(ev, best), ev[best >> 1].weight);
+        last = best;
+      }
+    }
+  }
+  cnt[row] = 0;
+  head[row] = kNoSlot;
+  return ok;
+}
+
+__global__ void k_fp_write(DevGraph<kCapG> G, DevGraph<kCapH> H, const DevEvent* __restrict__ ev,
+                           uint32_t n, BatchDev b) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || batch_aborted(b.ctl)) return;
+  const bool write = !b.ctl->not_simple;
+  if (!fp_apply(G, ev, b.fp_cnt[0], b.fp_head[0], b.fp_next[0], r, write))
+    atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
+  if (b.fp_kept[r >> 1] &&
+      !fp_apply(H, ev, b.fp_cnt[1], b.fp_head[1], b.fp_next[1], r, write))
+    atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
+}
+
+__global__ void k_finish(unsigned long long* g_cnt, unsigned long long* h_cnt, BatchCtl* ctl,
+                         unsigned int* abort_flag) {
+  if (ctl->fast && !ctl->not_simple && ctl->val_err == ~0ull) {
+    for (int f = 0; f < kReportFields; ++f) ctl->report[f] = ctl->fp_report[f];
+    g_cnt[1] += ctl->fp_report[kInsSeen];
+    h_cnt[1] += ctl->fp_report[kInsKept];
+  }
   if (ctl->val_err != ~0ull || ctl->commit_err != ~0ull ||
       (ctl->use_absent_limit && ctl->first_absent != 0xFFFFFFFFu))
     *abort_flag = 1;
@@ -819,6 +951,16 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st) {
   CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.mscratch, b.dec, b.ctl, o};
   return n_del > 0 ? launch_rounds<true>(op, nb, b, st) : launch_rounds<false>(op, nb, b, st);
+}
+
+int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
+                           uint32_t nb, const WalkOpts& o, cudaStream_t st) {
+  if (nb == 0) return 0;
+  const uint32_t n = 2 * nb;
+  k_fp_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, o, b);
+  k_fp_check<<<grid_for(n), 256, 0, st>>>(b.events, n, b);
+  k_fp_write<<<grid_for(n), 256, 0, st>>>(G, H, b.events, n, b);
+  return 3;
 }
 
 int launch_pack(const BatchDev& b, uint32_t lo_r, uint32_t n_r, uint32_t lo_m, uint32_t n_m,

@@ -66,6 +66,9 @@ struct BatchCtl {
   unsigned int n_saved;  // rows saved for the in-place walk shadow
   unsigned long long side_top;       // side-pool entries used by saved rows
   unsigned long long scratch_edges;  // |E| sink of the shadow pass
+  unsigned int fast;                 // insertion fast path attempted
+  unsigned int not_simple;           // fast-path precondition violated
+  unsigned long long fp_report[kReportFields];
 };
 
 struct WalkOpts {
@@ -105,6 +108,12 @@ struct BatchDev {
   BatchCtl* ctl;
   void* cub_temp;
   size_t cub_temp_bytes;
+  // Insertion fast path ([0] = G, [1] = H): per-vertex append counts and
+  // list heads (zero / kNoSlot between batches), per-record list links.
+  uint32_t* fp_cnt[2];
+  uint32_t* fp_head[2];
+  uint32_t* fp_next[2];
+  uint8_t* fp_kept;
 };
 
 // Host launchers (batch.cu); each returns kernels launched.
@@ -116,6 +125,10 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
                    uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
                    const WalkOpts& o, int coop_blocks, cudaStream_t st);
 int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st);
+// Insertion-only batches: sort-based append commit (ctl.fast must be set);
+// k_rounds then only runs if a precondition failed on the device.
+int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
+                           uint32_t nb, const WalkOpts& o, cudaStream_t st);
 // n_del > 0 selects the warp-per-event round engine (parallel path recovery).
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st);

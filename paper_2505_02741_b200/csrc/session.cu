@@ -147,6 +147,7 @@ struct dyg_session {
   uint32_t ctl_cap = 0;
   unsigned int* d_abort = nullptr; // set by a failing batch; later batches no-op
   bool debug_sync = false;
+  bool no_fastpath = false;        // DYG_NO_FASTPATH: force the round engine
 };
 
 namespace {
@@ -182,6 +183,8 @@ void free_batch(dyg_session* s) {
   dev_free(b.saved_rows);
   dev_free(b.side_slab);
   dev_free(b.side_off);
+  for (int i = 0; i < 2; ++i) dev_free(b.fp_next[i]);
+  dev_free(b.fp_kept);
   cudaFree(b.cub_temp);
   b.cub_temp = nullptr;
   dev_free(s->d_events);
@@ -218,6 +221,8 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
           "pinned events");
     b.cub_temp_bytes = scan_temp_bytes(cap);
     check(cudaMalloc(&b.cub_temp, std::max<size_t>(b.cub_temp_bytes, 16)), "scan temp");
+    for (int i = 0; i < 2; ++i) dev_alloc(&b.fp_next[i], 2ull * cap, "append links");
+    dev_alloc(&b.fp_kept, cap, "append kept flags");
     s->nb_cap = cap;
     s->nd_cap = 0;
     (void)keep_nd;
@@ -363,6 +368,7 @@ void phase_prepare(dyg_session* s, Pending& p) {
   c.first_absent = 0xFFFFFFFFu;
   c.limit = p.nb;
   c.use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
+  c.fast = (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath) ? 1u : 0u;
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
   if (p.n_del > 0) ensure_side_pool(s);
@@ -431,6 +437,8 @@ void commit_enqueue(dyg_session* s, Pending& p) {
   b.ctl = p.dctl;
   check(cudaEventRecord(p.tm[3].a, s->stream), "event");
   if (p.n_del > 0) p.launches += launch_restore(s->G.view(), b, p.nb, s->stream);
+  if (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath)
+    p.launches += launch_insert_fastpath(s->G.view(), s->H.view(), b, p.nb, o, s->stream);
   p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
   maybe_sync(s, "commit");
   check(cudaEventRecord(p.tm[3].b, s->stream), "event");
@@ -733,6 +741,7 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->opt = *options;
       s->n = g->n;
       s->debug_sync = std::getenv("DYG_DEBUG_SYNC") != nullptr;
+      s->no_fastpath = std::getenv("DYG_NO_FASTPATH") != nullptr;
       s->G.upload(g->n, g->row_ptr, g->ids, g->w, s->stream);
       s->H.upload(h->n, h->row_ptr, h->ids, h->w, s->stream);
       s->g_edges = g->row_ptr[g->n] / 2;
@@ -750,6 +759,12 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       dev_alloc(&s->d_round, 1, "round counter");
       dev_alloc(&s->d_work, 1, "walk work counter");
       dev_alloc(&s->b.mark, s->n, "row marks");
+      for (int i = 0; i < 2; ++i) {
+        dev_alloc(&s->b.fp_cnt[i], s->n, "append counts");
+        dev_alloc(&s->b.fp_head[i], s->n, "append heads");
+        check(cudaMemset(s->b.fp_cnt[i], 0, sizeof(uint32_t) * s->n), "append counts");
+        check(cudaMemset(s->b.fp_head[i], 0xFF, sizeof(uint32_t) * s->n), "append heads");
+      }
       check(cudaMemset(s->b.mark, 0, sizeof(uint32_t) * s->n), "row marks");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
       dev_alloc(&s->b.ctl, 1, "batch ctl");
@@ -790,6 +805,10 @@ void dyg_session_destroy(dyg_session* s) {
   dev_free(s->d_round);
   dev_free(s->d_work);
   dev_free(s->b.mark);
+  for (int i = 0; i < 2; ++i) {
+    dev_free(s->b.fp_cnt[i]);
+    dev_free(s->b.fp_head[i]);
+  }
   dev_free(s->b.side_id);
   dev_free(s->b.side_w);
   dev_free(s->d_stream);

@@ -294,3 +294,21 @@ def test_uploaded_range_stops_at_failing_batch(oracle, dyg):
     assert same_rows(ost.graph().export(), st.rows(0))
     assert same_rows(ost.sparsifier().export(), st.rows(1))
     assert r0["insertions_seen"] == 2
+
+
+@pytest.mark.parametrize("dup", [False, True])
+def test_insertion_fast_path_matches_round_engine(oracle, dyg, monkeypatch, dup):
+    # Insertion-only batches of new keys take the sort-based append path;
+    # a repeated key in the batch (coalescing inside the batch) must fall
+    # back to the dependency rounds. Both must equal the reference.
+    g = oracle.make_mesh(20, 20, 5)
+    h = oracle.build_initial_sparsifier(g, 0.1, 5)
+    st = oracle.generate_stream(g, 0.3, 0.0, 3, 9, 2)
+    ev = st.events()
+    if dup:  # repeat an earlier key (reversed endpoints) later in batch 0
+        e0 = ev[0].copy()
+        e0["u"], e0["v"] = ev[0]["v"], ev[0]["u"]
+        ev = np.concatenate([ev[:5], [e0], ev[5:]]).astype(O.EVENT_DTYPE)
+    compare_replay(dyg, oracle, g, h, ev, st.batch_count, K=100.0, T=100, s=16, seed=9)
+    monkeypatch.setenv("DYG_NO_FASTPATH", "1")
+    compare_replay(dyg, oracle, g, h, ev, st.batch_count, K=100.0, T=100, s=16, seed=9)
