@@ -100,24 +100,39 @@ __device__ __forceinline__ bool walk_step(const DevGraph<C>& g, const uint4* hea
 #pragma unroll
       for (int i = NH; i < NV; ++i) r.v[i] = __ldg(src + i);
     }
+    uint32_t cand = 0;  // bit i: entry i is a candidate (exists, is not `prev`)
     double prefix[C];
     double total = 0.0;
 #pragma unroll
     for (int i = 0; i < C; ++i) {
-      if (i < static_cast<int>(deg) && r.s.idr(i) != prev) total = __dadd_rn(total, r.s.wr(i));
+      if (i < static_cast<int>(deg) && r.s.idr(i) != prev) {
+        total = __dadd_rn(total, r.s.wr(i));
+        cand |= 1u << i;
+      }
       prefix[i] = total;
     }
     if (total <= 0.0) return false;
     const double target = __dmul_rn(u01, total);
-    bool found = false;
+    // The reference picks the first candidate whose running sum exceeds
+    // target: that is the lowest set bit of `hit` (whatever the rounding of
+    // the sums); none -> the rounding fallback, the last candidate.
+    uint32_t hit = 0;
 #pragma unroll
-    for (int i = 0; i < C; ++i) {
-      if (!found && i < static_cast<int>(deg) && r.s.idr(i) != prev) {
-        next = r.s.idr(i);
-        ew = r.s.wr(i);
-        found = target < prefix[i];
+    for (int i = 0; i < C; ++i)
+      if (target < prefix[i]) hit |= 1u << i;
+    hit &= cand;
+    const int sel = hit ? __ffs(hit) - 1 : 31 - __clz(cand);
+    uint32_t id_sel = r.s.idr(0);
+    double w_sel = r.s.wr(0);
+#pragma unroll
+    for (int i = 1; i < C; ++i) {
+      if (sel == i) {
+        id_sel = r.s.idr(i);
+        w_sel = r.s.wr(i);
       }
     }
+    next = id_sel;
+    ew = w_sel;
     return true;
   }
   const uint32_t* ids = g.pool_id + r.s.ext;
