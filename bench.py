@@ -370,6 +370,8 @@ def run_ours(args):
         "commit_rounds_per_step": stats["commit_rounds"] / args.steps,
         "commit_ms_per_step_deletion_batches": stats["commit_ms_deletion"] / args.steps,
         "commit_rounds_per_step_deletion_batches": stats["commit_rounds_deletion"] / args.steps,
+        "walk_tail_ms_per_step": {"reach": stats["reach_tail_ms"] / args.steps,
+                                  "minpath": stats["minpath_tail_ms"] / args.steps},
         "clocks": clocks.summary(),
     }
     del launches

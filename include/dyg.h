@@ -139,6 +139,8 @@ typedef struct dyg_stats {
   uint64_t h2d_bytes;
   uint64_t d2h_bytes;
   double commit_ms_deletion;    /* commit_ms share of batches containing deletions */
+  double reach_tail_ms;         /* reach walks after the work queue drained (device clock) */
+  double minpath_tail_ms;
   uint64_t commit_rounds_deletion;
 } dyg_stats;
 

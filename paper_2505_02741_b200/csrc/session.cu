@@ -368,6 +368,7 @@ void phase_prepare(dyg_session* s, Pending& p) {
   c.first_absent = 0xFFFFFFFFu;
   c.limit = p.nb;
   c.use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
+  c.reach.t_start = c.reach.t_drain = c.minpath.t_start = c.minpath.t_drain = ~0ull;
   c.fast = (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath) ? 1u : 0u;
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
@@ -476,6 +477,11 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   }
   s->stats.reach_steps += c.reach.steps;
   s->stats.reach_row_bytes += c.reach.row_bytes;
+  auto tail_ms = [](const WalkCounters& w) {
+    return (w.t_end > w.t_drain && w.t_drain != ~0ull) ? (w.t_end - w.t_drain) * 1e-6 : 0.0;
+  };
+  s->stats.reach_tail_ms += tail_ms(c.reach);
+  s->stats.minpath_tail_ms += tail_ms(c.minpath);
   s->stats.minpath_steps += c.minpath.steps;
   s->stats.minpath_row_bytes += c.minpath.row_bytes;
   s->stats.reach_queries += c.nq_reach;

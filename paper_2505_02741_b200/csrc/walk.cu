@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(256, kMinBlocks)
            WalkCounters* ctr, unsigned int* __restrict__ work) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t total_work = *nq_dev * P.s;
+  const unsigned long long t0 = global_ns();
   __shared__ uint4 stage_all[8 * Gather<C>::kWarpWords];
   uint4* stage = stage_all + (threadIdx.x >> 5) * Gather<C>::kWarpWords;
   // Warp-uniform chunk of 32 work items [chunk_base, chunk_base + 32): item
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(256, kMinBlocks)
         base = __shfl_sync(kFull, base, 0);
         if (base >= total_work) {
           drained = true;
+          if (lane == 0) atomicMin(&ctr->t_drain, global_ns());
           break;
         }
         __syncwarp();  // every lane has read the previous chunk
@@ -320,6 +322,10 @@ __global__ void __launch_bounds__(256, kMinBlocks)
     }
   }
   add_counters(ctr, my_steps, my_bytes);
+  if (lane == 0) {
+    atomicMin(&ctr->t_start, t0);
+    atomicMax(&ctr->t_end, global_ns());
+  }
 }
 
 __global__ void k_reach_init(ReachOut out, uint32_t n, unsigned int* work) {

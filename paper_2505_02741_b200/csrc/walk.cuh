@@ -70,7 +70,18 @@ struct MinScratch {
 struct WalkCounters {
   unsigned long long steps;
   unsigned long long row_bytes;
+  // %globaltimer (ns): first warp start, first warp to find the work queue
+  // drained, last warp exit -- the post-drain tail is drain..end.
+  unsigned long long t_start;   // min
+  unsigned long long t_drain;   // min
+  unsigned long long t_end;     // max
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Host launchers (walk.cu). nq_dev: device count of queries (nq_max bounds
 // the launch); work: a device u32 work counter (reset by the launcher).
