@@ -370,6 +370,9 @@ def run_ours(args):
         "commit_rounds_per_step": stats["commit_rounds"] / args.steps,
         "commit_ms_per_step_deletion_batches": stats["commit_ms_deletion"] / args.steps,
         "commit_rounds_per_step_deletion_batches": stats["commit_rounds_deletion"] / args.steps,
+        "flow_commit_phase_ms_per_step": {
+            k: stats[f"flow_ms_{k}"] / args.steps
+            for k in ("promote", "emit", "rank", "apply", "reset")},
         "walk_tail_ms_per_step": {"reach": stats["reach_tail_ms"] / args.steps,
                                   "minpath": stats["minpath_tail_ms"] / args.steps},
         "clocks": clocks.summary(),

@@ -142,6 +142,13 @@ typedef struct dyg_stats {
   double reach_tail_ms;         /* reach walks after the work queue drained (device clock) */
   double minpath_tail_ms;
   uint64_t commit_rounds_deletion;
+  /* Dataflow deletion commit (k_del_flow) phase times, device clock:
+     fallback promotion, record emission, ranks, apply, reset. */
+  double flow_ms_promote;
+  double flow_ms_emit;
+  double flow_ms_rank;
+  double flow_ms_apply;
+  double flow_ms_reset;
 } dyg_stats;
 
 typedef struct dyg_session dyg_session;

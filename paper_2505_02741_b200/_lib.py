@@ -44,7 +44,8 @@ STATS_FIELDS = (
     ("minpath_ms", "f8"), ("commit_ms", "f8"), ("total_ms", "f8"), ("commit_rounds", "u8"),
     ("pool_used", "u8"), ("pool_capacity", "u8"), ("h2d_bytes", "u8"), ("d2h_bytes", "u8"),
     ("commit_ms_deletion", "f8"), ("reach_tail_ms", "f8"), ("minpath_tail_ms", "f8"),
-    ("commit_rounds_deletion", "u8"),
+    ("commit_rounds_deletion", "u8"), ("flow_ms_promote", "f8"), ("flow_ms_emit", "f8"),
+    ("flow_ms_rank", "f8"), ("flow_ms_apply", "f8"), ("flow_ms_reset", "f8"),
 )
 STATS_DTYPE = np.dtype([(n, "<" + t) for n, t in STATS_FIELDS])
 

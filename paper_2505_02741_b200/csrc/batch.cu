@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(256) k_rounds_warp(Op op, uint32_t nev, BatchD
   const uint32_t nw = static_cast<uint32_t>(grid.size()) >> 5;
   volatile BatchCtl* ctl = b.ctl;
   if (ctl->val_err != ~0ull) return;
+  if (ctl->flow_done) return;  // k_del_flow committed the batch
   Acc acc{};
   unsigned long long round = *b.round_ctr;
   uint32_t r = 0;
@@ -325,6 +326,44 @@ struct CommitOp {
     }
   }
 
+  // Row superset of deletion event k for k_del_flow, known before any event
+  // of the batch commits: u, v, plus the recovery path when one was found,
+  // or -- when the event may run the local fallback (`fb`) -- every
+  // batch-start G neighbour of u and v (the fallback edge is a live-G edge of
+  // u or v, and a deletion-only batch only removes G edges). Calls f(i, row)
+  // for i = lane, lane + 32, ... < the returned (warp-uniform) count.
+  __device__ bool has_path_of(uint32_t k) const {
+    const uint32_t s = slot[k];
+    return s != kNoSlot && mout.has_path[s] != 0;
+  }
+  template <class F>
+  __device__ uint32_t flow_rows(uint32_t k, uint32_t lane, bool fb, F&& f) const {
+    const DevEvent& e = ev[k];
+    const uint32_t* p = nullptr;
+    uint32_t n = 2, du = 0, dv = 0;
+    if (!o.freeze) {
+      if (has_path_of(k)) {
+        const uint32_t s = slot[k];
+        p = path_of(s);
+        n += mout.path_len[s];
+      } else if (fb) {
+        du = G.slab[e.u].deg;
+        dv = G.slab[e.v].deg;
+        n += du + dv;
+      }
+    }
+    for (uint32_t i = lane; i < n; i += 32) {
+      uint32_t r;
+      if (i == 0) r = e.u;
+      else if (i == 1) r = e.v;
+      else if (p) r = p[i - 2];
+      else if (i - 2 < du) r = row(G, e.u).id(i - 2);
+      else r = row(G, e.v).id(i - 2 - du);
+      f(i, r);
+    }
+    return n;
+  }
+
   // Pull an insertion's four slabs toward L2 one grid barrier before the
   // apply phase needs them.
   __device__ void prefetch(uint32_t k) const {
@@ -353,33 +392,51 @@ struct CommitOp {
     }
     const uint32_t u = e.u, v = e.v;
     const uint32_t s = slot[k];
-    // Lane 0: G delete, H membership, H delete (:490-494).
+    // G delete, H membership, H delete (:490-494), on four lanes: the four
+    // rows (G u, G v, H u, H v) are distinct, so each lane scans and edits
+    // its own row -- one dependent round of row fetches instead of the
+    // sequential has_edge / delete_edge chain. has_edge scans the smaller
+    // row; either row answers the same (rows are symmetric). H is edited only
+    // once the G deletion is known to succeed (:491 throws first).
+    int found = -1;
+    if (lane < 4) {
+      const uint32_t a = (lane & 1) ? v : u, bb = (lane & 1) ? u : v;
+      found = lane < 2 ? row_find(G, a, bb) : row_find(H, a, bb);
+      if (lane < 2 && found >= 0) row_remove_at(G, a, static_cast<uint32_t>(found));
+    }
+    const bool in_g = __shfl_sync(kAll, found, 0) >= 0;
+    const bool in_h = __shfl_sync(kAll, found, 2) >= 0;
+    if (in_g && in_h && (lane == 2 || lane == 3))
+      row_remove_at(H, lane == 2 ? u : v, static_cast<uint32_t>(found));
     uint32_t stage = 0;  // 0 error/graph-only/freeze done, 1 path recovery, 2 fallback
     uint32_t err = 0;
     unsigned long long steps = 0;
     if (lane == 0) {
       acc.r[kDelSeen] += 1;
-      if (!delete_edge(G, u, v, acc.dg)) {
+      if (!in_g) {
         err = kErrAbsent;
-      } else if (has_edge(H, u, v)) {
-        acc.r[kDelInH] += 1;
-        delete_edge(H, u, v, acc.dh);
-        if (!o.freeze) {
-          bool path = false;
-          if (s != kNoSlot) {
-            steps = mout.steps[s];
-            path = mout.has_path[s] != 0;
-          }
-          stage = path ? 1u : 2u;
-        } else {
-          acc.r[kFallbacks] += 1;
-          dec[k] = 2u;
-        }
       } else {
-        dec[k] = 0u;
+        --acc.dg;
+        if (in_h) {
+          acc.r[kDelInH] += 1;
+          --acc.dh;
+          if (!o.freeze) {
+            bool path = false;
+            if (s != kNoSlot) {
+              steps = mout.steps[s];
+              path = mout.has_path[s] != 0;
+            }
+            stage = path ? 1u : 2u;
+          } else {
+            acc.r[kFallbacks] += 1;
+            dec[k] = 2u;
+          }
+        } else {
+          dec[k] = 0u;
+        }
       }
     }
-    __syncwarp();  // lane 0's row updates visible to the other lanes
+    __syncwarp();  // the row updates above visible to the other lanes
     err = __shfl_sync(kAll, err, 0);
     if (err) return err;
     stage = __shfl_sync(kAll, stage, 0);
@@ -526,6 +583,218 @@ struct CommitOp {
     return 0;
   }
 };
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Dataflow commit of a deletion-only batch (the sequential :489-523 loop),
+// replacing the dependency rounds: every event lists the superset of rows it
+// can touch (CommitOp::flow_rows); per row, the events touching it are
+// ordered by event index, and event k may apply once, on each of its rows,
+// every earlier event touching that row has applied. Record (row x, event k)
+// carries rank = #records of earlier events on x; a row's done counter
+// counts applied records, so "done[x] >= rank" is exactly that condition.
+// Each warp applies its events in increasing order, so the lowest unapplied
+// event is always some warp's current event and has no unapplied
+// predecessor: progress is guaranteed, and the result equals the event-order commit bit for bit
+// (disjoint events commute). No grid barrier per round: the critical path is
+// the longest chain of row-sharing events, not rounds x barriers.
+// Phases: emit records + per-row lists | ranks | apply (spin on done) |
+// reset the per-row heads and counters. A record-buffer overflow skips the
+// apply phase and leaves the batch to the round engine (flow_done = 0).
+__global__ void __launch_bounds__(256) k_del_flow(CommitOp op, uint32_t nev, BatchDev b) {
+  constexpr unsigned kAll = 0xFFFFFFFFu;
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
+  const uint32_t nth = static_cast<uint32_t>(grid.size());
+  const uint32_t lane = tid & 31;
+  const uint32_t wid = tid >> 5;
+  const uint32_t nw = nth >> 5;
+  volatile BatchCtl* ctl = b.ctl;
+  if (ctl->val_err != ~0ull) return;  // uniform
+  const uint32_t lim = min(nev, op.limit());
+  uint32_t* head = b.fp_head[0];
+  uint32_t* done = b.fp_cnt[0];
+  uint32_t* mark = b.fp_cnt[1];
+  if (tid == 0) ctl->fl_t[0] = global_ns();
+  // Phase 0: which events may run the local fallback. An event whose edge
+  // is in batch-start H without a recovered path may. An event whose edge is
+  // NOT in batch-start H may only if an earlier fallback inserted its edge
+  // into H: recovery paths never do (they run on the shadow G, which lacks
+  // every edge this batch deletes), and a fallback edge is incident to that
+  // event's u or v. So: mark the endpoints of fallback-capable events and
+  // promote the events touching a marked vertex, to a fixpoint (order-free,
+  // hence a superset). Most deletions then list only {u, v}.
+  if (!op.o.freeze) {
+    for (uint32_t k = tid; k < lim; k += nth) {
+      const DevEvent& e = op.ev[k];
+      const bool fb = op.slot[k] != kNoSlot && !op.has_path_of(k);
+      b.fl_promo[k] = fb ? 1 : 0;
+      if (fb) {
+        mark[e.u] = 1;
+        mark[e.v] = 1;
+      }
+    }
+    for (uint32_t it = 0;; ++it) {
+      grid.sync();
+      if (tid == 0) ctl->fl_changed[(it + 1) & 1] = 0;
+      for (uint32_t k = tid; k < lim; k += nth) {
+        if (b.fl_promo[k] || op.slot[k] != kNoSlot) continue;
+        const DevEvent& e = op.ev[k];
+        if (*reinterpret_cast<volatile uint32_t*>(mark + e.u) ||
+            *reinterpret_cast<volatile uint32_t*>(mark + e.v)) {
+          b.fl_promo[k] = 1;
+          mark[e.u] = 1;
+          mark[e.v] = 1;
+          ctl->fl_changed[it & 1] = 1;
+        }
+      }
+      grid.sync();
+      if (!ctl->fl_changed[it & 1]) break;
+    }
+  }
+  if (tid == 0) ctl->fl_t[1] = global_ns();
+  // Phase 1: records and per-row lists. Record ranges are allocated per
+  // block (a block-wide scan, one atomic per block and pass): one global
+  // counter bumped per event serialises ~12k same-address atomics.
+  {
+    __shared__ uint32_t wcnt[8];
+    __shared__ uint32_t bbase;
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint32_t passes = (lim + nw - 1) / nw;
+    for (uint32_t pass = 0; pass < passes; ++pass) {
+      const uint32_t k = pass * nw + wid;
+      const bool fb = k < lim && !op.o.freeze && b.fl_promo[k];
+      const uint32_t n = k < lim ? op.flow_rows(k, lane, fb, [](uint32_t, uint32_t) {}) : 0;
+      if (lane == 0) wcnt[wib] = n;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+          const uint32_t c = wcnt[w];
+          wcnt[w] = t;
+          t += c;
+        }
+        bbase = t ? atomicAdd(&b.ctl->fl_top, t) : 0;
+      }
+      __syncthreads();
+      const uint32_t base = bbase + wcnt[wib];
+      __syncthreads();  // wcnt / bbase are rewritten next pass
+      if (k >= lim) continue;
+      if (base + static_cast<uint64_t>(n) > b.fl_cap) {
+        if (lane == 0) {
+          b.fl_cnt[k] = 0;
+          b.ctl->fl_overflow = 1;
+        }
+        continue;
+      }
+      if (lane == 0) {
+        b.fl_base[k] = base;
+        b.fl_cnt[k] = n;
+      }
+      op.flow_rows(k, lane, fb, [&](uint32_t i, uint32_t r) {
+        b.fl_row[base + i] = r;
+        b.fl_ev[base + i] = k;
+        b.fl_next[base + i] = atomicExch(head + r, base + i);
+      });
+    }
+  }
+  grid.sync();
+  if (tid == 0) ctl->fl_t[2] = global_ns();
+  const bool overflow = ctl->fl_overflow != 0;
+  if (!overflow) {
+    // Phase 2: ranks.
+    const uint32_t total = ctl->fl_top;
+    for (uint32_t p = tid; p < total; p += nth) {
+      const uint32_t x = b.fl_row[p], k = b.fl_ev[p];
+      uint32_t r = 0;
+      for (uint32_t q = head[x]; q != kNoSlot; q = b.fl_next[q]) r += b.fl_ev[q] < k;
+      b.fl_rank[p] = r;
+    }
+    grid.sync();
+    if (tid == 0) ctl->fl_t[3] = global_ns();
+    // Phase 3: apply in dataflow order. Chain depth (the critical path, in
+    // events) is tracked per row for the report's round counter.
+    Acc acc{};
+    uint32_t max_depth = 0;
+    // Each warp owns events k = wid + j*nw (j = 0, 1, ...) and keeps a
+    // window of its 8 lowest unapplied ones, applying whichever is ready
+    // (non-blocking readiness polls), so an event stuck behind a long chain
+    // does not hold up the warp's independent later events. The lowest
+    // unapplied event overall is always inside its owner's window and ready:
+    // no deadlock, and no shared work counter to contend on.
+    const uint32_t count = wid < lim ? (lim - wid + nw - 1) / nw : 0;
+    constexpr uint32_t kWin = 8;
+    uint32_t jlo = 0;
+    uint32_t mask = count >= kWin ? 0xFFu : ((1u << count) - 1u);
+    while (mask) {
+      bool progressed = false;
+      for (uint32_t i = 0; i < kWin; ++i) {
+        if (!((mask >> i) & 1u)) continue;
+        const uint32_t k = wid + (jlo + i) * nw;
+        const uint32_t base = b.fl_base[k], n = b.fl_cnt[k];
+        bool ready = true;
+        for (uint32_t t = lane; t < n && ready; t += 32)
+          ready = ld_acquire(done + b.fl_row[base + t]) >= b.fl_rank[base + t];
+        if (!__all_sync(kAll, ready)) continue;
+        __threadfence();
+        uint32_t depth = 0;
+        for (uint32_t t = lane; t < n; t += 32) depth = max(depth, b.fl_depth[b.fl_row[base + t]]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) depth = max(depth, __shfl_xor_sync(kAll, depth, off));
+        ++depth;
+        max_depth = max(max_depth, depth);
+        uint32_t e = 0;
+        if ((ctl->commit_err >> 8) > k) e = op.apply_warp(k, lane, acc);
+        if (lane == 0) {
+          b.state[k] = e ? 2 : 1;
+          if (e) atomicMin(&b.ctl->commit_err, (static_cast<unsigned long long>(k) << 8) | e);
+        }
+        for (uint32_t t = lane; t < n; t += 32) b.fl_depth[b.fl_row[base + t]] = depth;
+        __threadfence();
+        __syncwarp();
+        for (uint32_t t = lane; t < n; t += 32) atomicAdd(done + b.fl_row[base + t], 1u);
+        mask &= ~(1u << i);
+        progressed = true;
+      }
+      // Slide the window past applied events at its bottom.
+      while (!(mask & 1u) && jlo < count) {
+        mask >>= 1;
+        ++jlo;
+        if (jlo + kWin - 1 < count) mask |= 1u << (kWin - 1);
+      }
+      if (!progressed) __nanosleep(64);
+    }
+    op.flush(acc);
+    if (lane == 0 && max_depth) atomicMax(&b.ctl->fl_depth, max_depth);
+  }
+  grid.sync();
+  if (tid == 0) ctl->fl_t[4] = global_ns();
+  // Phase 4: reset the per-row state for the next batch.
+  for (uint32_t k = wid; k < lim; k += nw) {
+    const uint32_t base = b.fl_base[k], n = b.fl_cnt[k];
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t x = b.fl_row[base + i];
+      head[x] = kNoSlot;
+      done[x] = 0;
+      b.fl_depth[x] = 0;
+    }
+    if (lane == 0 && b.fl_promo[k]) {
+      const DevEvent& e = op.ev[k];
+      mark[e.u] = 0;
+      mark[e.v] = 0;
+    }
+  }
+  grid.sync();
+  if (tid == 0) ctl->fl_t[5] = global_ns();
+  if (tid == 0 && !overflow) {
+    ctl->flow_done = 1;
+    ctl->rounds = ctl->rounds + ctl->fl_depth;
+  }
+}
 
 // Query build (sparsifier.cpp:429-457), phase 1 on batch-start H and G:
 // insertion flags and w_pq = G.w(u,v) + w (:441). Runs before the walk
@@ -910,6 +1179,32 @@ size_t scan_temp_bytes(uint32_t nb_cap) {
   return temp;
 }
 
+// Batch control block initialisation on the device (a kernel instead of a
+// host->device copy: a copy-engine transfer in the stream costs several
+// microseconds of latency per batch).
+__global__ void k_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, uint32_t fast) {
+  constexpr uint32_t kWords = sizeof(BatchCtl) / sizeof(uint32_t);
+  uint32_t* w = reinterpret_cast<uint32_t*>(ctl);
+  for (uint32_t i = threadIdx.x; i < kWords; i += blockDim.x) w[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->val_err = ~0ull;
+    ctl->commit_err = ~0ull;
+    ctl->first_absent = 0xFFFFFFFFu;
+    ctl->limit = limit;
+    ctl->use_absent_limit = use_absent_limit;
+    ctl->reach.t_start = ctl->reach.t_drain = ctl->minpath.t_start = ctl->minpath.t_drain = ~0ull;
+    ctl->fast = fast;
+  }
+}
+
+int launch_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, uint32_t fast,
+                    cudaStream_t st) {
+  static_assert(sizeof(BatchCtl) % sizeof(uint32_t) == 0, "BatchCtl words");
+  k_ctl_init<<<1, 128, 0, st>>>(ctl, limit, use_absent_limit, fast);
+  return 1;
+}
+
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st) {
   if (nb == 0) return 0;
@@ -947,10 +1242,34 @@ int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cud
   return 1;
 }
 
+// DYG_COMMIT_ROUNDS=1 forces the dependency-round engine for deletion-only
+// batches (A/B and testing knob).
+bool flow_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYG_COMMIT_ROUNDS");
+    return !(e && std::atoi(e) == 1);
+  }();
+  return on;
+}
+
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st) {
   CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.mscratch, b.dec, b.ctl, o};
-  return n_del > 0 ? launch_rounds<true>(op, nb, b, st) : launch_rounds<false>(op, nb, b, st);
+  if (n_del == 0) return launch_rounds<false>(op, nb, b, st);
+  int l = 0;
+  if (n_del == nb && flow_enabled()) {
+    CommitOp op_copy = op;
+    BatchDev b_copy = b;
+    uint32_t nev = nb;
+    void* args[] = {&op_copy, &nev, &b_copy};
+    const int need = static_cast<int>(grid_for(static_cast<uint64_t>(nb) * 32));
+    const int cap = coop_blocks_for(k_del_flow);
+    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_del_flow),
+                                           dim3(need < cap ? need : cap), dim3(256), args, 0, st),
+               "cooperative flow launch");
+    ++l;
+  }
+  return l + launch_rounds<true>(op, nb, b, st);
 }
 
 int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,

@@ -69,6 +69,14 @@ struct BatchCtl {
   unsigned int fast;                 // insertion fast path attempted
   unsigned int not_simple;           // fast-path precondition violated
   unsigned long long fp_report[kReportFields];
+  // Dataflow commit of deletion-only batches (k_del_flow).
+  unsigned int fl_top;       // row records handed out
+  unsigned int fl_next_ev;   // next event to take (in event order)
+  unsigned int fl_overflow;  // record buffer too small: the round engine commits
+  unsigned int flow_done;    // k_del_flow committed the batch
+  unsigned int fl_changed[2];  // fallback-promotion fixpoint
+  unsigned int fl_depth;     // longest chain of row-sharing events
+  unsigned long long fl_t[6];  // %globaltimer at the phase boundaries
 };
 
 struct WalkOpts {
@@ -114,9 +122,23 @@ struct BatchDev {
   uint32_t* fp_head[2];
   uint32_t* fp_next[2];
   uint8_t* fp_kept;
+  // Dataflow commit (k_del_flow): one record per (event, row) of the event's
+  // row superset; per-event record ranges. Per-vertex list heads and done
+  // counters reuse fp_head[0] / fp_cnt[0] (kNoSlot / 0 between batches).
+  uint32_t* fl_row;
+  uint32_t* fl_ev;
+  uint32_t* fl_next;
+  uint32_t* fl_rank;
+  uint32_t* fl_base;
+  uint32_t* fl_cnt;
+  uint8_t* fl_promo;   // per event: may run the local fallback
+  uint32_t* fl_depth;  // per vertex, 0 between batches
+  uint64_t fl_cap;
 };
 
 // Host launchers (batch.cu); each returns kernels launched.
+int launch_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, uint32_t fast,
+                    cudaStream_t st);
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st);
 // Query build; with deletions in the batch it also saves the touched G

@@ -178,6 +178,10 @@ void free_batch(dyg_session* s) {
   dev_free(b.mscratch.steps);
   dev_free(b.mscratch.paths);
   dev_free(b.mscratch.rvals);
+  dev_free(b.fl_row);
+  dev_free(b.fl_ev);
+  dev_free(b.fl_next);
+  dev_free(b.fl_rank);
   dev_free(b.dec);
   dev_free(b.wpq);
   dev_free(b.saved_rows);
@@ -185,6 +189,9 @@ void free_batch(dyg_session* s) {
   dev_free(b.side_off);
   for (int i = 0; i < 2; ++i) dev_free(b.fp_next[i]);
   dev_free(b.fp_kept);
+  dev_free(b.fl_base);
+  dev_free(b.fl_cnt);
+  dev_free(b.fl_promo);
   cudaFree(b.cub_temp);
   b.cub_temp = nullptr;
   dev_free(s->d_events);
@@ -223,6 +230,9 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     check(cudaMalloc(&b.cub_temp, std::max<size_t>(b.cub_temp_bytes, 16)), "scan temp");
     for (int i = 0; i < 2; ++i) dev_alloc(&b.fp_next[i], 2ull * cap, "append links");
     dev_alloc(&b.fp_kept, cap, "append kept flags");
+    dev_alloc(&b.fl_base, cap, "flow record ranges");
+    dev_alloc(&b.fl_cnt, cap, "flow record ranges");
+    dev_alloc(&b.fl_promo, cap, "flow fallback flags");
     s->nb_cap = cap;
     s->nd_cap = 0;
     (void)keep_nd;
@@ -249,6 +259,17 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.mscratch.steps, cap * sw, "minpath scratch");
     dev_alloc(&b.mscratch.paths, cap * sw * T1, "minpath traces");
     dev_alloc(&b.mscratch.rvals, cap * T1, "minpath scratch");
+    // Flow records: u, v and a path of <= T+1 vertices or two G rows per
+    // deletion; overflow falls back to the round engine.
+    dev_free(b.fl_row);
+    dev_free(b.fl_ev);
+    dev_free(b.fl_next);
+    dev_free(b.fl_rank);
+    b.fl_cap = static_cast<uint64_t>(cap) * 48 + 65536;
+    dev_alloc(&b.fl_row, b.fl_cap, "flow records");
+    dev_alloc(&b.fl_ev, b.fl_cap, "flow records");
+    dev_alloc(&b.fl_next, b.fl_cap, "flow records");
+    dev_alloc(&b.fl_rank, b.fl_cap, "flow records");
     s->nd_cap = cap;
   }
 }
@@ -361,20 +382,12 @@ void phase_prepare(dyg_session* s, Pending& p) {
   b.events = const_cast<DevEvent*>(p.dev);
   b.locks = s->d_locks;
   b.round_ctr = s->d_round;
-  BatchCtl& c = *p.hctl;
-  std::memset(&c, 0, sizeof c);
-  c.val_err = ~0ull;
-  c.commit_err = ~0ull;
-  c.first_absent = 0xFFFFFFFFu;
-  c.limit = p.nb;
-  c.use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
-  c.reach.t_start = c.reach.t_drain = c.minpath.t_start = c.minpath.t_drain = ~0ull;
-  c.fast = (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath) ? 1u : 0u;
+  const uint32_t use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
+  const uint32_t fast = (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath) ? 1u : 0u;
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
   if (p.n_del > 0) ensure_side_pool(s);
-  check(cudaMemcpyAsync(b.ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->stream), "ctl upload");
-  s->stats.h2d_bytes += sizeof c;
+  p.launches += launch_ctl_init(b.ctl, p.nb, use_absent_limit, fast, s->stream);
   check(cudaEventRecord(p.tm[0].a, s->stream), "event");
   p.launches += launch_validate(b, p.nb, s->n, s->d_abort, s->stream);
   maybe_sync(s, "validate");
@@ -432,7 +445,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
 
 // Commit (:466-533) enqueue: restore the shadowed rows, run the commit
 // engine, snapshot the counters and copy the control block back (async).
-void commit_enqueue(dyg_session* s, Pending& p) {
+void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
@@ -445,8 +458,9 @@ void commit_enqueue(dyg_session* s, Pending& p) {
   check(cudaEventRecord(p.tm[3].b, s->stream), "event");
   p.launches += launch_finish(s->G.view(), s->H.view(), b, s->d_abort, s->stream);
   check(cudaEventRecord(p.tm[0].b, s->stream), "event");
-  check(cudaMemcpyAsync(p.hctl, b.ctl, sizeof(BatchCtl), cudaMemcpyDeviceToHost, s->stream),
-        "ctl download");
+  if (download)
+    check(cudaMemcpyAsync(p.hctl, b.ctl, sizeof(BatchCtl), cudaMemcpyDeviceToHost, s->stream),
+          "ctl download");
   if (p.nb == 1)
     check(cudaMemcpyAsync(p.hdec, b.dec, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream),
           "decision download");
@@ -487,6 +501,13 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   s->stats.reach_queries += c.nq_reach;
   s->stats.minpath_queries += c.nq_min;
   s->stats.commit_rounds += c.rounds;
+  if (c.flow_done && c.fl_t[5] > c.fl_t[0]) {
+    s->stats.flow_ms_promote += (c.fl_t[1] - c.fl_t[0]) * 1e-6;
+    s->stats.flow_ms_emit += (c.fl_t[2] - c.fl_t[1]) * 1e-6;
+    s->stats.flow_ms_rank += (c.fl_t[3] - c.fl_t[2]) * 1e-6;
+    s->stats.flow_ms_apply += (c.fl_t[4] - c.fl_t[3]) * 1e-6;
+    s->stats.flow_ms_reset += (c.fl_t[5] - c.fl_t[4]) * 1e-6;
+  }
   if (p.n_del > 0) {
     s->stats.commit_ms_deletion += p.tm[3].ms();
     s->stats.commit_rounds_deletion += c.rounds;
@@ -638,9 +659,12 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
     p.n_del = static_cast<uint32_t>(s->batch_del[b]);
     phase_prepare(s, p);
     phase_walk(s, p, true, 0, 0, 0, 0);
-    commit_enqueue(s, p);
+    commit_enqueue(s, p, false);
     counter += p.nb;
   }
+  // All control blocks in one transfer (one copy-engine round trip per range).
+  check(cudaMemcpyAsync(s->h_ctls, s->d_ctls, sizeof(BatchCtl) * count, cudaMemcpyDeviceToHost,
+                        s->stream), "ctl download");
   check(cudaStreamSynchronize(s->stream), "batch range");
   for (uint32_t i = 0; i < count; ++i) {
     if (ps[i].nb == 0) {
@@ -772,6 +796,8 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
         check(cudaMemset(s->b.fp_head[i], 0xFF, sizeof(uint32_t) * s->n), "append heads");
       }
       check(cudaMemset(s->b.mark, 0, sizeof(uint32_t) * s->n), "row marks");
+      dev_alloc(&s->b.fl_depth, s->n, "flow depths");
+      check(cudaMemset(s->b.fl_depth, 0, sizeof(uint32_t) * s->n), "flow depths");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
       dev_alloc(&s->b.ctl, 1, "batch ctl");
       dev_alloc(&s->d_counts, 2, "shard counts");
@@ -815,6 +841,7 @@ void dyg_session_destroy(dyg_session* s) {
     dev_free(s->b.fp_cnt[i]);
     dev_free(s->b.fp_head[i]);
   }
+  dev_free(s->b.fl_depth);
   dev_free(s->b.side_id);
   dev_free(s->b.side_w);
   dev_free(s->d_stream);

@@ -52,27 +52,6 @@ __device__ __forceinline__ void cp_async16(uint4* dst, const void* src, uint32_t
                : "memory");
 }
 
-template <int C>
-__device__ __forceinline__ const uint4* gather_rows(const DevGraph<C>& g, uint32_t my_row,
-                                                   uint4* stage) {
-  using Gt = Gather<C>;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t sub = lane / Gt::kLanesPerRow;
-  const uint32_t chunk = lane % Gt::kLanesPerRow;
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < Gt::kRounds; ++j) {
-    const uint32_t r = j * Gt::kRowsPerRound + sub;
-    const uint32_t u = __shfl_sync(kFull, my_row, r);
-    const bool live = u != kNoVertex;
-    const uint4* src = reinterpret_cast<const uint4*>(g.slab + (live ? u : 0)) + chunk;
-    cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
-  }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncwarp();
-  return stage + lane * Gt::kStride;
-}
-
 // One sample_neighbor call (walk.cpp:17-37) at `cur` on the gathered slab
 // head, given this step's uniform draw u01. The reference's pass 1 sums
 // candidate weights in row order and its pass 2 re-accumulates the same
@@ -174,49 +153,100 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long lo
   }
 }
 
-// K1/K2 as persistent lane-refill kernels. Walk lengths are long-tailed
-// (most insertion walkers dead-end within a few steps, a few run to T), so a
-// static lane<->walker mapping leaves most lanes idle (ncu: 6.4 of 32 lanes
-// active). Here a lane that finishes its walker takes the next work item
-// (query = w / s, walker = w % s) from a global counter with one
-// warp-aggregated atomic, so warps stay full until the queue drains.
+// K1/K2 as persistent, software-pipelined lane-refill kernels.
+//
+// Refill: walk lengths are long-tailed (most insertion walkers dead-end
+// within a few steps, a few run to T), so a static lane<->walker mapping
+// leaves most lanes idle (ncu: 6.4 of 32 lanes active). A lane that finishes
+// a walker takes the next work item (query = w / s, walker = w % s) from a
+// warp-local chunk of 32 items whose queries are prefetched with one
+// coalesced load (one global atomic per 32 walkers).
+//
+// Pipelining: every lane carries NS walker SLOTS. Each slot has its own
+// staging buffer and cp.async group; while slot k's sample runs, the row
+// fetches of the other slots are in flight (wait_group NS-1 retires exactly
+// the oldest group). ncu on the single-slot kernel: 50 % of warp stalls were
+// the dependent row fetch and the schedulers idled half the cycles with the
+// issue slots only 47 % busy -- the fetch of one walker now overlaps the
+// arithmetic of another.
+//
 // Per-walker semantics are single_walk's (walk.cpp:41-80): cap at the loop
-// top, then after each traversed edge budget before target.
+// top, then after each traversed edge budget before target. A walker whose
+// step count reaches T after a non-terminal step ends as StepCap at once
+// (exactly what the next loop-top check would decide, without a row fetch).
 //
 // Reach results (nbrw_reach, walk.cpp:82-98) are order-free reductions --
 // reached = OR, steps = SUM, best = MIN -- so they are accumulated with
 // atomics into outputs pre-set by k_reach_init. Min-path walkers keep their
 // raw trace and (acc, terminal, steps) for K3.
-template <int C, bool kMinPath, int kMinBlocks>
-__global__ void __launch_bounds__(256, kMinBlocks)
+struct Slot {
+  uint32_t cur, prev, tgt, steps, widx;
+  bool has;
+  uint64_t rng;
+  double acc, wpq;
+};
+
+struct ChunkSmem {  // per warp: the current 32-item chunk
+  uint2 pq[32];
+  double w[32];
+  unsigned long long seed[32];
+};
+
+template <int C, int NS, int kWarps>
+struct WalkLayout {
+  static constexpr size_t kStageBytes = sizeof(uint4) * Gather<C>::kWarpWords;  // one slot
+  static constexpr size_t kWarpBytes = NS * kStageBytes + sizeof(ChunkSmem);
+  static constexpr size_t kBytes = kWarps * kWarpBytes;
+};
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Issue (without waiting) the cooperative gather of the 32 rows `my_row`
+// of one slot into `stage`, as one cp.async group.
+template <int C>
+__device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row, uint4* stage) {
+  using Gt = Gather<C>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t sub = lane / Gt::kLanesPerRow;
+  const uint32_t chunk = lane % Gt::kLanesPerRow;
+  if (__any_sync(kFull, my_row != kNoVertex)) {
+#pragma unroll
+    for (int j = 0; j < Gt::kRounds; ++j) {
+      const uint32_t r = j * Gt::kRowsPerRound + sub;
+      const uint32_t u = __shfl_sync(kFull, my_row, r);
+      const bool live = u != kNoVertex;
+      const uint4* src = reinterpret_cast<const uint4*>(g.slab + (live ? u : 0)) + chunk;
+      cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
+    }
+  }
+  cp_async_commit();
+}
+
+template <int C, bool kMinPath, int NS, int kWarps, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_walk(DevGraph<C> g, const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
            const uint32_t* __restrict__ nq_dev, WalkParams P, ReachOut rout, MinScratch S,
            WalkCounters* ctr, unsigned int* __restrict__ work) {
+  using L = WalkLayout<C, NS, kWarps>;
+  extern __shared__ __align__(16) unsigned char walk_smem[];
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  unsigned char* wbase = walk_smem + warp * L::kWarpBytes;
+  uint4* stage0 = reinterpret_cast<uint4*>(wbase);
+  ChunkSmem& cs = *reinterpret_cast<ChunkSmem*>(wbase + NS * L::kStageBytes);
   const uint32_t total_work = *nq_dev * P.s;
   const unsigned long long t0 = global_ns();
-  __shared__ uint4 stage_all[8 * Gather<C>::kWarpWords];
-  uint4* stage = stage_all + (threadIdx.x >> 5) * Gather<C>::kWarpWords;
-  // Warp-uniform chunk of 32 work items [chunk_base, chunk_base + 32): item
-  // chunk_base + i's query endpoints, w_pq and walker seed are prefetched by
-  // lane i into shared memory when the chunk is taken.
-  __shared__ uint2 chunk_pq_all[8 * 32];
-  __shared__ double chunk_w_all[8 * 32];
-  __shared__ unsigned long long chunk_seed_all[8 * 32];
-  uint2* chunk_pq = chunk_pq_all + (threadIdx.x >> 5) * 32;
-  double* chunk_w = chunk_w_all + (threadIdx.x >> 5) * 32;
-  unsigned long long* chunk_seed = chunk_seed_all + (threadIdx.x >> 5) * 32;
   uint32_t chunk_base = 0, chunk_pos = 32, chunk_end = 32;
   bool drained = false;
-
-  bool has = false;
-  uint32_t qi = 0, cur = 0, prev = kNoVertex, target_v = 0, steps = 0, w_idx = 0;
-  uint64_t rng = 0;
-  double acc = 0.0, w_pq = 1.0;
-  uint32_t* trace = nullptr;
   unsigned long long my_steps = 0, my_bytes = 0;
-  for (;;) {
-    unsigned need = __ballot_sync(kFull, !has);
+
+  // Give every lane of the warp whose slot is empty the next work item.
+  auto refill = [&](Slot& w) {
+    unsigned need = __ballot_sync(kFull, !w.has);
     while (need && !drained) {
       if (chunk_pos == chunk_end) {
         unsigned int base = 0;
@@ -231,96 +261,120 @@ __global__ void __launch_bounds__(256, kMinBlocks)
         chunk_base = base;
         chunk_pos = 0;
         chunk_end = min(32u, total_work - base);
-        const uint32_t w = base + lane;
-        if (w < total_work) {
-          const uint32_t q = P.s_shift != kNoShift ? (w >> P.s_shift) : w / P.s;
-          const uint32_t wi = w - q * P.s;
+        const uint32_t wi_all = base + lane;
+        if (wi_all < total_work) {
+          const uint32_t q = P.s_shift != kNoShift ? (wi_all >> P.s_shift) : wi_all / P.s;
+          const uint32_t wi = wi_all - q * P.s;
           uint64_t qseed;
           if (kMinPath) {
             const MinQuery Q = mq[q];
-            chunk_pq[lane] = make_uint2(Q.p, Q.q);
-            chunk_w[lane] = 1.0;
+            cs.pq[lane] = make_uint2(Q.p, Q.q);
+            cs.w[lane] = 1.0;
             qseed = Q.qseed;
           } else {
             const ReachQuery Q = rq[q];
-            chunk_pq[lane] = make_uint2(Q.p, Q.q);
-            chunk_w[lane] = Q.w_pq;
+            cs.pq[lane] = make_uint2(Q.p, Q.q);
+            cs.w[lane] = Q.w_pq;
             qseed = Q.qseed;
           }
-          chunk_seed[lane] = walker_seed_from(qseed, wi);
+          cs.seed[lane] = walker_seed_from(qseed, wi);
         }
         __syncwarp();
       }
       const uint32_t rank = __popc(need & ((1u << lane) - 1u));
       const uint32_t take = min(static_cast<uint32_t>(__popc(need)), chunk_end - chunk_pos);
-      const bool mine = ((need >> lane) & 1u) && rank < take;
-      if (mine) {
+      if (((need >> lane) & 1u) && rank < take) {
         const uint32_t item = chunk_pos + rank;
-        w_idx = chunk_base + item;
-        qi = P.s_shift != kNoShift ? (w_idx >> P.s_shift) : w_idx / P.s;
-        const uint2 pq = chunk_pq[item];
-        cur = pq.x;
-        target_v = pq.y;
-        w_pq = chunk_w[item];
-        rng = chunk_seed[item];
-        prev = kNoVertex;
-        steps = 0;
-        acc = 0.0;
-        has = true;
-        if (kMinPath) {
-          trace = S.paths + static_cast<uint64_t>(w_idx) * (P.T + 1ull);
-          trace[0] = cur;
-        }
+        w.widx = chunk_base + item;
+        const uint2 pq = cs.pq[item];
+        w.cur = pq.x;
+        w.tgt = pq.y;
+        w.wpq = cs.w[item];
+        w.rng = cs.seed[item];
+        w.prev = kNoVertex;
+        w.steps = 0;
+        w.acc = 0.0;
+        w.has = true;
+        if (kMinPath) S.paths[static_cast<uint64_t>(w.widx) * (P.T + 1ull)] = w.cur;
       }
       chunk_pos += take;
-      need = __ballot_sync(kFull, !has);
+      need = __ballot_sync(kFull, !w.has);
     }
-    if (!__any_sync(kFull, has)) break;
-    const uint4* head = gather_rows(g, (has && steps < P.T) ? cur : kNoVertex, stage);
-    if (has) {
-      uint32_t term = 0xFFFFFFFFu;
-      if (steps >= P.T) {
-        term = kStepCap;
-      } else {
-        rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
-        const double u = u01_of(rng);
-        uint32_t next = kNoVertex, deg = 0;
-        double ew = 0.0;
-        const bool ok = walk_step(g, head, cur, prev, u, next, ew, deg);
-        my_bytes += step_bytes(deg);
-        if (!ok) {
-          term = kDeadEnd;
-        } else {
-          acc = __dadd_rn(acc, __drcp_rn(ew));
-          ++steps;
-          prev = cur;
-          cur = next;
-          if (kMinPath) trace[steps] = cur;
-          if (__dmul_rn(w_pq, acc) > P.K) {
-            term = kBudget;
-          } else if (cur == target_v) {
-            term = kReached;
-          }
-        }
-      }
-      if (term != 0xFFFFFFFFu) {
-        my_steps += steps;
-        if (kMinPath) {
-          S.acc[w_idx] = acc;
-          S.term[w_idx] = term;
-          S.steps[w_idx] = steps;
-        } else {
-          atomicAdd(&rout.steps[qi], static_cast<unsigned long long>(steps));
-          if (term == kReached) {
-            atomicOr(&rout.reached[qi], 1u);
-            atomicMin(&rout.best_bits[qi],
-                      static_cast<unsigned long long>(__double_as_longlong(acc)));
-          }
-        }
-        has = false;
-      }
-    }
+  };
+  auto row_of = [&](const Slot& w) { return (w.has && w.steps < P.T) ? w.cur : kNoVertex; };
+
+  Slot sl[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    sl[k].has = false;
+    refill(sl[k]);
+    issue_rows(g, row_of(sl[k]), stage0 + k * Gather<C>::kWarpWords);
   }
+  for (;;) {
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      Slot& w = sl[k];
+      uint4* stage = stage0 + k * Gather<C>::kWarpWords;
+      // This step's uniform draw (draw k = steps + 1) does not depend on the row.
+      const double u = u01_of(w.rng + kGamma);
+      cp_async_wait<NS - 1>();  // slot k's group is the oldest outstanding
+      __syncwarp();
+      if (w.has) {
+        uint32_t term = 0xFFFFFFFFu;
+        if (w.steps >= P.T) {
+          term = kStepCap;
+        } else {
+          w.rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
+          uint32_t next = kNoVertex, deg = 0;
+          double ew = 0.0;
+          const bool ok =
+              walk_step(g, stage + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
+          my_bytes += step_bytes(deg);
+          if (!ok) {
+            term = kDeadEnd;
+          } else {
+            w.acc = __dadd_rn(w.acc, __drcp_rn(ew));
+            ++w.steps;
+            w.prev = w.cur;
+            w.cur = next;
+            if (kMinPath) S.paths[static_cast<uint64_t>(w.widx) * (P.T + 1ull) + w.steps] = next;
+            if (__dmul_rn(w.wpq, w.acc) > P.K) {
+              term = kBudget;
+            } else if (next == w.tgt) {
+              term = kReached;
+            } else if (w.steps >= P.T) {
+              term = kStepCap;
+            }
+          }
+        }
+        if (term != 0xFFFFFFFFu) {
+          my_steps += w.steps;
+          if (kMinPath) {
+            S.acc[w.widx] = w.acc;
+            S.term[w.widx] = term;
+            S.steps[w.widx] = w.steps;
+          } else {
+            const uint32_t qi =
+                P.s_shift != kNoShift ? (w.widx >> P.s_shift) : w.widx / P.s;
+            atomicAdd(&rout.steps[qi], static_cast<unsigned long long>(w.steps));
+            if (term == kReached) {
+              atomicOr(&rout.reached[qi], 1u);
+              atomicMin(&rout.best_bits[qi],
+                        static_cast<unsigned long long>(__double_as_longlong(w.acc)));
+            }
+          }
+          w.has = false;
+        }
+      }
+      __syncwarp();  // every lane has read its staged row before the slot is refilled
+      refill(w);
+      issue_rows(g, row_of(w), stage);
+      any |= w.has;
+    }
+    if (!__any_sync(kFull, any)) break;
+  }
+  cp_async_wait<0>();
   add_counters(ctr, my_steps, my_bytes);
   if (lane == 0) {
     atomicMin(&ctr->t_start, t0);
@@ -423,24 +477,38 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
 }  // namespace
 
 template <typename K>
-unsigned persistent_blocks(K kernel, uint64_t work) {
+unsigned persistent_blocks(K kernel, uint64_t work, int threads, size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
   const unsigned b = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
-  const unsigned need = blocks_for(work, 256);
+  const unsigned need = blocks_for(work, static_cast<unsigned>(threads));
   return need < b ? need : b;
 }
 
-// Reach occupancy variant (registers vs resident warps); DYG_REACH_BLOCKS
-// selects 3 (default, no spills) or 4 blocks/SM.
-int reach_variant() {
-  static int v = [] {
-    const char* e = std::getenv("DYG_REACH_BLOCKS");
-    return (e && std::atoi(e) == 4) ? 4 : 3;
+// One walk-kernel configuration: slots per lane, warps per block, minimum
+// resident blocks (register budget).
+template <int C, bool kMinPath, int NS, int kWarps, int kMinBlocks>
+void launch_walk(const DevGraph<C>& g, const ReachQuery* rq, const MinQuery* mq,
+                 const uint32_t* nq_dev, uint64_t threads, const WalkParams& P, ReachOut ro,
+                 MinScratch S, WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
+  auto k = k_walk<C, kMinPath, NS, kWarps, kMinBlocks>;
+  constexpr size_t smem = WalkLayout<C, NS, kWarps>::kBytes;
+  static bool attr = [&] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    return true;
   }();
-  return v;
+  (void)attr;
+  k<<<persistent_blocks(k, threads, kWarps * 32, smem), kWarps * 32, smem, st>>>(
+      g, rq, mq, nq_dev, P, ro, S, ctr, work);
+}
+
+// Walk-kernel variant (tuning knob, default = the measured best):
+// DYG_WALK_REACH / DYG_WALK_MIN = index into the tables below.
+int walk_variant(const char* env, int dflt) {
+  const char* e = std::getenv(env);
+  return e ? std::atoi(e) : dflt;
 }
 
 template <int C>
@@ -448,16 +516,15 @@ int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_d
                  uint32_t nq_max, const WalkParams& P, ReachOut out, WalkCounters* ctr,
                  unsigned int* work, cudaStream_t st) {
   if (nq_max == 0) return 0;
+  static const int v = walk_variant("DYG_WALK_REACH", 0);
   k_reach_init<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_max, work);
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
-  if (reach_variant() == 4) {
-    auto k = k_walk<C, false, 4>;
-    k<<<persistent_blocks(k, threads), 256, 0, st>>>(g, q, nullptr, nq_dev, P, out,
-                                                    MinScratch{}, ctr, work);
-  } else {
-    auto k = k_walk<C, false, 3>;
-    k<<<persistent_blocks(k, threads), 256, 0, st>>>(g, q, nullptr, nq_dev, P, out,
-                                                    MinScratch{}, ctr, work);
+  switch (v) {
+    case 0: launch_walk<C, false, 1, 8, 3>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
+    case 2: launch_walk<C, false, 2, 8, 3>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
+    case 3: launch_walk<C, false, 2, 4, 5>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
+    case 4: launch_walk<C, false, 3, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
+    default: launch_walk<C, false, 2, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
   }
   k_reach_fix<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_dev);
   return 3;
@@ -470,11 +537,14 @@ int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_d
                    uint32_t nq_max, const WalkParams& P, MinScratch scratch, MinOut out,
                    WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
   if (nq_max == 0) return 0;
+  static const int v = walk_variant("DYG_WALK_MIN", 0);
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
   k_zero<<<1, 1, 0, st>>>(work);
-  auto k = k_walk<C, true, 2>;
-  k<<<persistent_blocks(k, threads), 256, 0, st>>>(g, nullptr, q, nq_dev, P, ReachOut{},
-                                                  scratch, ctr, work);
+  switch (v) {
+    case 0: launch_walk<C, true, 1, 8, 2>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
+    case 2: launch_walk<C, true, 2, 4, 4>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
+    default: launch_walk<C, true, 2, 8, 2>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
+  }
   k_minpath_finish<C><<<blocks_for(static_cast<uint64_t>(nq_max) * 32, 256), 256, 0, st>>>(
       g, nq_dev, P, scratch, out);
   return 3;
