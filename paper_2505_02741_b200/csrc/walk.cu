@@ -79,15 +79,22 @@ __device__ __forceinline__ bool walk_step(const DevGraph<C>& g, const uint4* hea
 #pragma unroll
       for (int i = NH; i < NV; ++i) r.v[i] = __ldg(src + i);
     }
+    // Candidate weights pre-masked (non-candidates contribute +0.0, an exact
+    // no-op: weights are positive finite, graph.cpp:71), so the dependent
+    // chain is DADD after DADD with no select in between.
     uint32_t cand = 0;  // bit i: entry i is a candidate (exists, is not `prev`)
+    double wm[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const bool c = i < static_cast<int>(deg) && r.s.idr(i) != prev;
+      wm[i] = c ? r.s.wr(i) : 0.0;
+      cand |= static_cast<uint32_t>(c) << i;
+    }
     double prefix[C];
     double total = 0.0;
 #pragma unroll
     for (int i = 0; i < C; ++i) {
-      if (i < static_cast<int>(deg) && r.s.idr(i) != prev) {
-        total = __dadd_rn(total, r.s.wr(i));
-        cand |= 1u << i;
-      }
+      total = __dadd_rn(total, wm[i]);
       prefix[i] = total;
     }
     if (total <= 0.0) return false;
@@ -190,6 +197,7 @@ struct ChunkSmem {  // per warp: the current 32-item chunk
   uint2 pq[32];
   double w[32];
   unsigned long long seed[32];
+  double u[32];  // this step's draw, stored before the fetch wait (see k_walk)
 };
 
 template <int C, int NS, int kWarps>
@@ -316,36 +324,53 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     for (int k = 0; k < NS; ++k) {
       Slot& w = sl[k];
       uint4* stage = stage0 + k * Gather<C>::kWarpWords;
-      // This step's uniform draw (draw k = steps + 1) does not depend on the row.
+      // This step's uniform draw (draw k = steps + 1) does not depend on the
+      // row: computed while the fetch is in flight. The shared store pins it
+      // before the wait (ptxas otherwise sinks the hash below the DEPBAR, onto
+      // the dependent chain).
       const double u = u01_of(w.rng + kGamma);
+      *reinterpret_cast<volatile double*>(&cs.u[lane]) = u;
       cp_async_wait<NS - 1>();  // slot k's group is the oldest outstanding
       __syncwarp();
+      // Once the queue is drained no refill follows, so the next row can be
+      // requested right after sampling, before the reciprocal / budget
+      // arithmetic: in the tail every walker is a chain of dependent steps
+      // and this takes that arithmetic off the chain. A walker the budget
+      // then ends wastes its fetch (the memory system is idle by then).
+      const bool early = drained && P.early;
+      uint32_t term = 0xFFFFFFFFu;
+      uint32_t next = kNoVertex;
+      double ew = 0.0;
       if (w.has) {
-        uint32_t term = 0xFFFFFFFFu;
         if (w.steps >= P.T) {
           term = kStepCap;
         } else {
           w.rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
-          uint32_t next = kNoVertex, deg = 0;
-          double ew = 0.0;
+          uint32_t deg = 0;
           const bool ok =
               walk_step(g, stage + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
           my_bytes += step_bytes(deg);
-          if (!ok) {
-            term = kDeadEnd;
-          } else {
-            w.acc = __dadd_rn(w.acc, __drcp_rn(ew));
-            ++w.steps;
-            w.prev = w.cur;
-            w.cur = next;
-            if (kMinPath) S.paths[static_cast<uint64_t>(w.widx) * (P.T + 1ull) + w.steps] = next;
-            if (__dmul_rn(w.wpq, w.acc) > P.K) {
-              term = kBudget;
-            } else if (next == w.tgt) {
-              term = kReached;
-            } else if (w.steps >= P.T) {
-              term = kStepCap;
-            }
+          if (!ok) term = kDeadEnd;
+        }
+      }
+      if (early) {
+        __syncwarp();  // every lane has read its staged row
+        const bool cont = w.has && term == 0xFFFFFFFFu && next != w.tgt && w.steps + 1 < P.T;
+        issue_rows(g, cont ? next : kNoVertex, stage);
+      }
+      if (w.has) {
+        if (term == 0xFFFFFFFFu) {
+          w.acc = __dadd_rn(w.acc, __drcp_rn(ew));
+          ++w.steps;
+          w.prev = w.cur;
+          w.cur = next;
+          if (kMinPath) S.paths[static_cast<uint64_t>(w.widx) * (P.T + 1ull) + w.steps] = next;
+          if (__dmul_rn(w.wpq, w.acc) > P.K) {
+            term = kBudget;
+          } else if (next == w.tgt) {
+            term = kReached;
+          } else if (w.steps >= P.T) {
+            term = kStepCap;
           }
         }
         if (term != 0xFFFFFFFFu) {
@@ -367,9 +392,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
           w.has = false;
         }
       }
-      __syncwarp();  // every lane has read its staged row before the slot is refilled
-      refill(w);
-      issue_rows(g, row_of(w), stage);
+      if (!early) {
+        __syncwarp();  // every lane has read its staged row before the slot is refilled
+        refill(w);
+        issue_rows(g, row_of(w), stage);
+      }
       any |= w.has;
     }
     if (!__any_sync(kFull, any)) break;

@@ -8,6 +8,8 @@
 // explicit _rn intrinsics (no FMA contraction).
 #pragma once
 
+#include <cstdlib>
+
 #include "dyg_internal.cuh"
 
 namespace dyg {
@@ -22,6 +24,7 @@ struct WalkParams {
   uint32_t s;        // walkers per query
   uint64_t seed;     // global seed
   uint32_t s_shift;  // log2(s) when s is a power of two, else kNoShift
+  uint32_t early;    // tail mode: request the next row right after sampling
 };
 
 inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t seed) {
@@ -30,7 +33,11 @@ inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t se
     sh = 0;
     while ((1u << sh) != s) ++sh;
   }
-  return WalkParams{K, T, s, seed, sh};
+  static const uint32_t early = [] {
+    const char* e = std::getenv("DYG_WALK_EARLY");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 1u;
+  }();
+  return WalkParams{K, T, s, seed, sh, early};
 }
 
 struct ReachQuery {   // WalkQuery Reach (walk.hpp:71-78)

@@ -3,7 +3,7 @@
 # Usage: gpurun -- bash tools/ab.sh TAG "ENV=.. ENV2=.." "ENV=.." ...   ("-" = defaults)
 TAG=$1; shift
 mkdir -p gpurun_out
-if [ -z "$SKIP_TESTS" ]; then
+if [[ "$TAG" != nt* ]]; then
   timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu_$TAG.log
 fi
 i=0
