@@ -159,6 +159,12 @@ const char* dyg_last_error(void);
 const char* dyg_version(void);
 /* Number of visible CUDA devices (0 when none). */
 int dyg_device_count(void);
+/* Page-locked host memory for event buffers (NULL on failure / no device).
+   dyg_replay_events and dyg_shard_begin DMA straight from such buffers;
+   other host buffers are staged through the session's pinned copy first.
+   No reference counterpart: a B200 host-side addition. */
+void* dyg_host_alloc(size_t bytes);
+void dyg_host_free(void* p);
 
 /* SparsifierState::SparsifierState(G, H, options) (sparsifier.cpp:183-203):
  * validates shapes and H subset of G, uploads both graphs to `device` as
@@ -238,8 +244,10 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
  * (NCCL over NVLink) into `gathered` (world*slots slots, rank-major) and
  * calls dyg_shard_commit, which applies the identical deterministic commit on
  * every replica. dyg_shard_begin returns the query counts so the caller can
- * size buffers. The session stream may be replaced by the caller's
- * (dyg_set_stream) so the collective is stream-ordered with the kernels. */
+ * size buffers. The event and position buffers passed to dyg_shard_begin
+ * must stay valid until dyg_shard_commit returns (error messages read them).
+ * The session stream may be replaced by the caller's (dyg_set_stream) so
+ * the collective is stream-ordered with the kernels. */
 int dyg_set_stream(dyg_session* s, void* cuda_stream);
 int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* positions,
                     size_t n, uint32_t batch_index, uint64_t* n_reach, uint64_t* n_minpath);

@@ -84,6 +84,8 @@ def lib() -> C.CDLL:
         "dyg_last_error": (C.c_char_p, []),
         "dyg_version": (C.c_char_p, []),
         "dyg_device_count": (i32, []),
+        "dyg_host_alloc": (vp, [sz]),
+        "dyg_host_free": (None, [vp]),
         "dyg_session_create": (i32, [C.POINTER(Csr), C.POINTER(Csr), C.POINTER(Options), i32, pvp]),
         "dyg_session_destroy": (None, [vp]),
         "dyg_replay_batch": (i32, [vp, vp, sz, u32, u32, vp]),
@@ -141,6 +143,38 @@ def lib() -> C.CDLL:
         fn.argtypes = args
     _LIB = L
     return L
+
+
+class _PinnedBlock:
+    """Owner of one dyg_host_alloc block (freed when the last view dies)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = ptr, nbytes
+
+    def __del__(self):
+        if self.ptr and _LIB is not None:
+            _LIB.dyg_host_free(self.ptr)
+            self.ptr = 0
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """Uninitialised array in page-locked memory (the C-ABI DMAs event
+    batches straight from it); a plain numpy array when no device is
+    usable."""
+    dtype = np.dtype(dtype)
+    nbytes = n * dtype.itemsize
+    if nbytes == 0:
+        return np.zeros(n, dtype)
+    try:
+        ptr = lib().dyg_host_alloc(nbytes)
+    except (ImportError, OSError):
+        ptr = None
+    if not ptr:
+        return np.zeros(n, dtype)
+    owner = _PinnedBlock(ptr, nbytes)
+    buf = (C.c_uint8 * nbytes).from_address(ptr)
+    buf._dyg_owner = owner  # numpy views keep buf (their base), buf keeps the block
+    return np.frombuffer(buf, dtype=dtype, count=n)
 
 
 # Every symbol include/*.h declares (checked by tests/test_abi.py).

@@ -228,25 +228,33 @@ class UpdateStream:
     """stream.hpp:20-23: events (numpy EVENT_DTYPE records) + batch_count."""
 
     def __init__(self, events=None, batch_count: int = 0):
-        self.events = (np.zeros(0, EVENT_DTYPE) if events is None
-                       else np.ascontiguousarray(events, EVENT_DTYPE))
+        # Events live in page-locked host memory, so replaying a batch DMAs
+        # it straight to the device (no staging copy on the host).
+        src = np.zeros(0, EVENT_DTYPE) if events is None else np.asarray(events)
+        self.events = _lib.pinned_empty(len(src), EVENT_DTYPE)
+        if len(src):
+            self.events[:] = np.ascontiguousarray(src, EVENT_DTYPE)
         self.batch_count = int(batch_count)
 
     @classmethod
     def _from_handle(cls, h) -> "UpdateStream":
         L = _lib.lib()
         n = L.dygh_stream_size(h)
-        ev = np.zeros(n, EVENT_DTYPE)
+        s = cls(None, L.dygh_stream_batches(h))
+        s.events = _lib.pinned_empty(n, EVENT_DTYPE)
         if n:
             src = L.dygh_stream_events(h)
-            C.memmove(ev.ctypes.data, src, n * EVENT_DTYPE.itemsize)
-        s = cls(ev, L.dygh_stream_batches(h))
+            C.memmove(s.events.ctypes.data, src, n * EVENT_DTYPE.itemsize)
         L.dygh_stream_free(h)
         return s
 
     def batch(self, b: int):
-        """(events, positions) of batch b, in stream order."""
+        """(events, positions) of batch b, in stream order. A batch stored
+        contiguously (the usual case) is returned as a view of the stream's
+        page-locked buffer."""
         pos = np.nonzero(self.events["batch_index"] == b)[0].astype(np.uint64)
+        if len(pos) and int(pos[-1]) - int(pos[0]) + 1 == len(pos):
+            return self.events[int(pos[0]):int(pos[-1]) + 1], pos
         return np.ascontiguousarray(self.events[pos]), pos
 
 
@@ -411,6 +419,7 @@ class SparsifierState:
     def shard_begin(self, events, positions, batch_index):
         ev = np.ascontiguousarray(events, EVENT_DTYPE)
         pos = np.ascontiguousarray(positions, np.uint64)
+        self._shard_keep = (ev, pos)  # the library reads them until shard_commit
         nr, nm = C.c_uint64(), C.c_uint64()
         _check(_lib.lib().dyg_shard_begin(self._s, ptr(ev), ptr(pos), len(ev), batch_index,
                                           C.byref(nr), C.byref(nm)))

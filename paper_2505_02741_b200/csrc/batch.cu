@@ -918,19 +918,14 @@ __global__ void k_restore_rows(DevGraph<kCapG> G, BatchDev b) {
 // push_back(v: u, w) into G, and -- when kept -- the same two appends into H
 // with weight G.w(u,v) = w. H lacks the key because H is a subgraph of G.
 // Rows only receive appends, in event order. Each append record r = 2k +
-// side (row u or v of event k) is counted per row and pushed onto the row's
-// lock-free list (k_fp_link); rows with one record (the vast majority) write
-// it directly, a row with several has one owner that applies them in
-// increasing r, i.e. event order (k_fp_write). Any violated precondition
-// sets not_simple BEFORE anything is written (k_fp_check) and the round
-// engine (k_rounds) commits the batch instead. The per-row counters and
-// list heads are left zeroed / empty for the next batch.
-__device__ __forceinline__ void fp_link(uint32_t* cnt, uint32_t* head, uint32_t* next,
-                                        uint32_t row, uint32_t r) {
-  atomicAdd(cnt + row, 1u);
-  next[r] = atomicExch(head + row, r);
-}
-
+// side (row u or v of event k) is pushed onto its row's lock-free list
+// (k_fp_link, one atomic exchange per record). The list head owns the row:
+// a sole record (the vast majority) appends directly, a head with followers
+// applies the row's records in increasing r, i.e. event order (k_fp_write,
+// one thread per record and graph). Any violated precondition sets
+// not_simple BEFORE anything is written (k_fp_check) and the round engine
+// (k_rounds) commits the batch instead. The list heads are left empty for
+// the next batch.
 __global__ void k_fp_link(const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
@@ -945,11 +940,15 @@ __global__ void k_fp_link(const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts
       steps = b.rout.steps[s];
     }
     const bool kept = !o.freeze && !(o.K != 0.0 && have && reached);
-    fp_link(b.fp_cnt[0], b.fp_head[0], b.fp_next[0], e.u, 2 * k);
-    fp_link(b.fp_cnt[0], b.fp_head[0], b.fp_next[0], e.v, 2 * k + 1);
+    const uint32_t gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
+    const uint32_t gv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
+    b.fp_next[0][2 * k] = gu;
+    b.fp_next[0][2 * k + 1] = gv;
     if (kept) {
-      fp_link(b.fp_cnt[1], b.fp_head[1], b.fp_next[1], e.u, 2 * k);
-      fp_link(b.fp_cnt[1], b.fp_head[1], b.fp_next[1], e.v, 2 * k + 1);
+      const uint32_t hu = atomicExch(b.fp_head[1] + e.u, 2 * k);
+      const uint32_t hv = atomicExch(b.fp_head[1] + e.v, 2 * k + 1);
+      b.fp_next[1][2 * k] = hu;
+      b.fp_next[1][2 * k + 1] = hv;
     }
     b.fp_kept[k] = kept ? 1 : 0;
     b.dec[k] = kept ? 0u : 1u;
@@ -978,58 +977,66 @@ __device__ __forceinline__ uint32_t other_end(const DevEvent* ev, uint32_t rec) 
 }
 
 // A key repeated inside the batch shows up as a repeated neighbour on a
-// G row with several records; its list owner (the head) checks.
+// G row with several records; its list head checks.
 __global__ void k_fp_check(const DevEvent* __restrict__ ev, uint32_t n, BatchDev b) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n || batch_aborted(b.ctl) || b.ctl->not_simple) return;
   const uint32_t row = rec_row(ev, r);
-  if (b.fp_cnt[0][row] < 2 || b.fp_head[0][row] != r) return;
-  for (uint32_t x = r; x != kNoSlot; x = b.fp_next[0][x])
-    for (uint32_t y = b.fp_next[0][x]; y != kNoSlot; y = b.fp_next[0][y])
+  const uint32_t* next = b.fp_next[0];
+  if (b.fp_head[0][row] != r || next[r] == kNoSlot) return;
+  for (uint32_t x = r; x != kNoSlot; x = next[x])
+    for (uint32_t y = next[x]; y != kNoSlot; y = next[y])
       if (other_end(ev, x) == other_end(ev, y)) b.ctl->not_simple = 1;
 }
 
-// Record r's row: a sole record appends directly; the list owner of a row
-// with several records appends them in increasing r (= event order) by
-// repeated minimum selection over the short list. Both reset the row's
-// counter and list head for the next batch, also when the batch fell back.
+// Record r's row on one graph: the list head appends the row's records --
+// itself alone, or all of them in increasing r by repeated minimum selection
+// over the short list -- and empties the list head.
 template <int C>
-__device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* ev, uint32_t* cnt,
-                                         uint32_t* head, const uint32_t* next, uint32_t r,
-                                         bool write) {
+__device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* ev, uint32_t* head,
+                                         const uint32_t* next, uint32_t r, bool write) {
   const uint32_t row = rec_row(ev, r);
-  const uint32_t c = cnt[row];
-  if (c == 0 || (c > 1 && head[row] != r)) return true;
+  // The row's slab is needed by the head's append: request it alongside the
+  // list lookups.
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(g.slab + row));
+  const uint32_t h = head[row];
+  const uint32_t nx = next[r];
+  if (h != r) return true;
   bool ok = true;
   if (write) {
-    if (c == 1) {
+    if (nx == kNoSlot) {
       ok = row_push(g, row, other_end(ev, r), ev[r >> 1].weight);
     } else {
       uint32_t last = 0;
-      for (uint32_t i = 0; i < c && ok; ++i) {
+      for (bool first = true; ok; first = false) {
         uint32_t best = kNoSlot;
         for (uint32_t x = r; x != kNoSlot; x = next[x])
-          if ((i == 0 || x > last) && x < best) best = x;
+          if ((first || x > last) && x < best) best = x;
+        if (best == kNoSlot) break;
         ok = row_push(g, row, other_end(ev, best), ev[best >> 1].weight);
         last = best;
       }
     }
   }
-  cnt[row] = 0;
   head[row] = kNoSlot;
   return ok;
 }
 
+// One thread per (record, graph): t = 2 r + (0: G, 1: H).
 __global__ void k_fp_write(DevGraph<kCapG> G, DevGraph<kCapH> H, const DevEvent* __restrict__ ev,
                            uint32_t n, BatchDev b) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = t >> 1;
   if (r >= n || batch_aborted(b.ctl)) return;
   const bool write = !b.ctl->not_simple;
-  if (!fp_apply(G, ev, b.fp_cnt[0], b.fp_head[0], b.fp_next[0], r, write))
-    atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
-  if (b.fp_kept[r >> 1] &&
-      !fp_apply(H, ev, b.fp_cnt[1], b.fp_head[1], b.fp_next[1], r, write))
-    atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
+  bool ok;
+  if ((t & 1) == 0) {
+    ok = fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write);
+  } else {
+    if (!b.fp_kept[r >> 1]) return;
+    ok = fp_apply(H, ev, b.fp_head[1], b.fp_next[1], r, write);
+  }
+  if (!ok) atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
 }
 
 __global__ void k_finish(unsigned long long* g_cnt, unsigned long long* h_cnt, BatchCtl* ctl,
@@ -1205,6 +1212,25 @@ int launch_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, ui
   return 1;
 }
 
+// Insertion (kind 0) / other event counts of a batch: out[0], out[1].
+__global__ void k_count_kinds(const DevEvent* __restrict__ ev, uint32_t nb, uint32_t* out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ins = k < nb && ev[k].kind == 0;
+  const bool oth = k < nb && ev[k].kind != 0;
+  const uint32_t ci = __popc(__ballot_sync(0xFFFFFFFFu, ins));
+  const uint32_t co = __popc(__ballot_sync(0xFFFFFFFFu, oth));
+  if ((threadIdx.x & 31) == 0) {
+    if (ci) atomicAdd(out, ci);
+    if (co) atomicAdd(out + 1, co);
+  }
+}
+
+int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStream_t st) {
+  cuda_check(cudaMemsetAsync(out, 0, 2 * sizeof(uint32_t), st), "kind counts");
+  k_count_kinds<<<grid_for(nb), 256, 0, st>>>(ev, nb, out);
+  return 1;
+}
+
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st) {
   if (nb == 0) return 0;
@@ -1255,7 +1281,11 @@ bool flow_enabled() {
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st) {
   CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.mscratch, b.dec, b.ctl, o};
-  if (n_del == 0) return launch_rounds<false>(op, nb, b, st);
+  static const int skip = [] {  // MEASUREMENT ONLY: skip the fallback launch
+    const char* e = std::getenv("DYG_SKIP_FALLBACK");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (n_del == 0) return skip ? 0 : launch_rounds<false>(op, nb, b, st);
   int l = 0;
   if (n_del == nb && flow_enabled()) {
     CommitOp op_copy = op;
@@ -1268,6 +1298,7 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
                                            dim3(need < cap ? need : cap), dim3(256), args, 0, st),
                "cooperative flow launch");
     ++l;
+    if (skip) return l;
   }
   return l + launch_rounds<true>(op, nb, b, st);
 }
@@ -1278,7 +1309,7 @@ int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, c
   const uint32_t n = 2 * nb;
   k_fp_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, o, b);
   k_fp_check<<<grid_for(n), 256, 0, st>>>(b.events, n, b);
-  k_fp_write<<<grid_for(n), 256, 0, st>>>(G, H, b.events, n, b);
+  k_fp_write<<<grid_for(2ull * n), 256, 0, st>>>(G, H, b.events, n, b);
   return 3;
 }
 

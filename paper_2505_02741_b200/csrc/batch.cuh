@@ -139,6 +139,7 @@ struct BatchDev {
 // Host launchers (batch.cu); each returns kernels launched.
 int launch_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, uint32_t fast,
                     cudaStream_t st);
+int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStream_t st);
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st);
 // Query build; with deletions in the batch it also saves the touched G

@@ -127,12 +127,12 @@ struct dyg_session {
 
   // Last-batch outputs (immediate mode / apply_*).
   uint32_t last_dec = 0;
-  uint32_t* d_counts = nullptr;   // shard query counts (device)
-  uint32_t* h_counts = nullptr;   // pinned: [0..1] shard counts, [2] decision
+  uint32_t* d_counts = nullptr;   // [0..1] shard query counts, [2..3] batch kind counts
+  uint32_t* h_counts = nullptr;   // pinned: [0..1] shard counts, [2] decision, [4..5] kinds
   // Multi-GPU split state (dyg_shard_*).
   bool shard_active = false;
-  std::vector<DevEvent> shard_host;
-  std::vector<uint64_t> shard_pos;
+  const DevEvent* shard_host = nullptr;  // caller's buffers, valid until dyg_shard_commit
+  const uint64_t* shard_pos = nullptr;
   uint32_t shard_nb = 0, shard_ins = 0, shard_del = 0, shard_batch = 0;
   uint32_t shard_nq_r = 0, shard_nq_m = 0;
   std::chrono::steady_clock::time_point shard_wall0;
@@ -585,19 +585,52 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
   phase_commit(s, p, out);
 }
 
-// Host events -> pinned staging -> device, then the deferred pipeline.
+// True when p is page-locked host memory the DMA engines can read directly.
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host events -> device (straight from page-locked buffers, else through the
+// session's pinned staging copy), then the deferred pipeline.
+void upload_events(dyg_session* s, const dyg_event* ev, size_t nb) {
+  static_assert(sizeof(DevEvent) == sizeof(dyg_event), "event layout");
+  if (nb == 0) return;
+  const void* src = ev;
+  if (!host_pinned(ev)) {
+    std::memcpy(s->h_events_pinned, ev, sizeof(DevEvent) * nb);
+    src = s->h_events_pinned;
+  }
+  check(cudaMemcpyAsync(s->d_events, src, sizeof(DevEvent) * nb, cudaMemcpyHostToDevice,
+                        s->stream), "events upload");
+  s->stats.h2d_bytes += sizeof(DevEvent) * nb;
+}
+
+// Insertion / deletion counts of the uploaded batch, counted on the device:
+// one short round trip instead of a host pass over every event (at C5 that
+// host pass read 2.5 MB per batch and cost more than the upload itself).
+void count_kinds(dyg_session* s, uint32_t nb, uint32_t& n_ins, uint32_t& n_del) {
+  n_ins = n_del = 0;
+  if (nb == 0) return;
+  s->stats.kernel_launches += launch_count_kinds(s->d_events, nb, s->d_counts + 2, s->stream);
+  check(cudaMemcpyAsync(s->h_counts + 4, s->d_counts + 2, 2 * sizeof(uint32_t),
+                        cudaMemcpyDeviceToHost, s->stream), "kind counts");
+  check(cudaStreamSynchronize(s->stream), "kind counts");
+  n_ins = s->h_counts[4];
+  n_del = s->h_counts[5];
+}
+
 void run_host_batch(dyg_session* s, const dyg_event* ev, const uint64_t* positions, size_t nb,
                     uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs) {
+  ensure_batch(s, static_cast<uint32_t>(nb), 0);
+  upload_events(s, ev, nb);
   uint32_t n_ins = 0, n_del = 0;
-  for (size_t i = 0; i < nb; ++i) (ev[i].kind == 0 ? n_ins : n_del)++;
+  count_kinds(s, static_cast<uint32_t>(nb), n_ins, n_del);
   ensure_batch(s, static_cast<uint32_t>(nb), n_del);
-  static_assert(sizeof(DevEvent) == sizeof(dyg_event), "event layout");
-  std::memcpy(s->h_events_pinned, ev, sizeof(DevEvent) * nb);
-  if (nb) {
-    check(cudaMemcpyAsync(s->d_events, s->h_events_pinned, sizeof(DevEvent) * nb,
-                          cudaMemcpyHostToDevice, s->stream), "events upload");
-    s->stats.h2d_bytes += sizeof(DevEvent) * nb;
-  }
   run_deferred(s, s->d_events, reinterpret_cast<const DevEvent*>(ev), positions,
                static_cast<uint32_t>(nb), n_ins, n_del, batch_index, out, immediate_msgs);
 }
@@ -727,6 +760,19 @@ extern "C" {
 
 const char* dyg_last_error(void) { return g_last_error.c_str(); }
 
+void* dyg_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0 || cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dyg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 const char* dyg_version(void) {
   return "dyg-b200 0.1 (sm_100a; slabs H64B/G128B; fmad=false)";
 }
@@ -800,8 +846,8 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       check(cudaMemset(s->b.fl_depth, 0, sizeof(uint32_t) * s->n), "flow depths");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
       dev_alloc(&s->b.ctl, 1, "batch ctl");
-      dev_alloc(&s->d_counts, 2, "shard counts");
-      check(cudaMallocHost(reinterpret_cast<void**>(&s->h_counts), 4 * sizeof(uint32_t)),
+      dev_alloc(&s->d_counts, 4, "shard / kind counts");
+      check(cudaMallocHost(reinterpret_cast<void**>(&s->h_counts), 8 * sizeof(uint32_t)),
             "pinned counts");
       check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctl), sizeof(BatchCtl)), "pinned ctl");
       s->coop_blocks = coop_grid_blocks(device);
@@ -1114,12 +1160,14 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
     if (!s->opt.batched) fail(DYG_ERR_USAGE, "the multi-GPU split needs batched (deferred) mode");
     check(cudaSetDevice(s->device), "set device");
     s->shard_active = false;
-    s->shard_host.assign(reinterpret_cast<const DevEvent*>(events),
-                         reinterpret_cast<const DevEvent*>(events) + n);
-    s->shard_pos.resize(n);
-    for (size_t i = 0; i < n; ++i) s->shard_pos[i] = positions ? positions[i] : i;
+    s->shard_host = reinterpret_cast<const DevEvent*>(events);
+    s->shard_pos = positions;
     uint32_t n_ins = 0, n_del = 0;
-    for (size_t i = 0; i < n; ++i) (events[i].kind == 0 ? n_ins : n_del)++;
+    if (n > 0) {
+      ensure_batch(s, static_cast<uint32_t>(n), 0);
+      upload_events(s, events, n);
+      count_kinds(s, static_cast<uint32_t>(n), n_ins, n_del);
+    }
     s->shard_nb = static_cast<uint32_t>(n);
     s->shard_ins = n_ins;
     s->shard_del = n_del;
@@ -1129,16 +1177,12 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
     s->shard_nq_r = s->shard_nq_m = 0;
     if (n > 0) {
       ensure_batch(s, static_cast<uint32_t>(n), n_del);
-      std::memcpy(s->h_events_pinned, events, sizeof(DevEvent) * n);
-      check(cudaMemcpyAsync(s->d_events, s->h_events_pinned, sizeof(DevEvent) * n,
-                            cudaMemcpyHostToDevice, s->stream), "events upload");
-      s->stats.h2d_bytes += sizeof(DevEvent) * n;
       Pending p;
       bind_pending(s, p);
       reset_abort(s);
       p.dev = s->d_events;
-      p.host = s->shard_host.data();
-      p.pos = s->shard_pos.data();
+      p.host = s->shard_host;
+      p.pos = s->shard_pos;
       p.nb = s->shard_nb;
       p.n_ins = n_ins;
       p.n_del = n_del;
@@ -1213,8 +1257,8 @@ int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
     bind_pending(s, p);
     p.counter_base = s->shard_counter;
     p.dev = s->d_events;
-    p.host = s->shard_host.data();
-    p.pos = s->shard_pos.data();
+    p.host = s->shard_host;
+    p.pos = s->shard_pos;
     p.nb = s->shard_nb;
     p.n_ins = s->shard_ins;
     p.n_del = s->shard_del;
