@@ -896,6 +896,68 @@ __global__ void k_save_rows(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, 
   }
 }
 
+// Walk shadow by per-row event lists (replaces a dependency-round pass):
+// the shadow only applies the batch's deletions to G in event order
+// (:416-423), and a deletion edits rows u and v alone, so each row can
+// replay its own deletions in increasing event order independently. Every
+// deletion record r = 2k + side goes onto its row's list (k_sh_link); the
+// list head owns the row (k_sh_apply): it saves the row once for
+// k_restore_rows, then removes the row's entries in event order. A record
+// that finds its edge already gone is an absent deletion; first_absent =
+// the lowest such event, exactly the first event whose graph_.delete_edge
+// would throw in a deletion-only batch (:491).
+__global__ void k_sh_link(const DevEvent* __restrict__ ev, uint32_t nb, BatchDev b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb || batch_aborted(b.ctl)) return;
+  const DevEvent e = ev[k];
+  if (e.kind != 1) return;
+  const uint32_t hu = atomicExch(b.fp_head[0] + e.u, 2 * k);
+  const uint32_t hv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
+  b.fp_next[0][2 * k] = hu;
+  b.fp_next[0][2 * k + 1] = hv;
+}
+
+__global__ void k_sh_apply(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, uint32_t nb,
+                           BatchDev b) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 2 * nb || batch_aborted(b.ctl)) return;
+  const DevEvent& e = ev[r >> 1];
+  if (e.kind != 1) return;
+  const uint32_t row = (r & 1) ? e.v : e.u;
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(G.slab + row));
+  uint32_t* head = b.fp_head[0];
+  const uint32_t* next = b.fp_next[0];
+  if (head[row] != r) return;
+  // Save the row (the owner is its only writer in this pass).
+  const uint32_t idx = atomicAdd(&b.ctl->n_saved, 1u);
+  b.saved_rows[idx] = row;
+  const Slab<kCapG> sl = G.slab[row];
+  b.side_slab[idx] = sl;
+  if (sl.ext != kInline) {
+    const unsigned long long off = atomicAdd(b.side_top, static_cast<unsigned long long>(sl.deg));
+    b.side_off[idx] = off;
+    for (uint32_t i = 0; i < sl.deg; ++i) {
+      b.side_id[off + i] = G.pool_id[sl.ext + i];
+      b.side_w[off + i] = G.pool_w[sl.ext + i];
+    }
+  }
+  // The row's deletions in increasing event order.
+  uint32_t last = 0;
+  for (bool first = true;; first = false) {
+    uint32_t best = kNoSlot;
+    for (uint32_t x = r; x != kNoSlot; x = next[x])
+      if ((first || x > last) && x < best) best = x;
+    if (best == kNoSlot) break;
+    const DevEvent& eb = ev[best >> 1];
+    const uint32_t other = (best & 1) ? eb.u : eb.v;
+    const int i = row_find(G, row, other);
+    if (i < 0) atomicMin(&b.ctl->first_absent, best >> 1);
+    else row_remove_at(G, row, static_cast<uint32_t>(i));
+    last = best;
+  }
+  head[row] = kNoSlot;
+}
+
 __global__ void k_restore_rows(DevGraph<kCapG> G, BatchDev b) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= b.ctl->n_saved) return;
@@ -1238,6 +1300,15 @@ int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned i
   return 1;
 }
 
+// DYG_SHADOW_ROUNDS=1 selects the dependency-round shadow pass (A/B knob).
+bool shadow_lists_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYG_SHADOW_ROUNDS");
+    return !(e && std::atoi(e) == 1);
+  }();
+  return on;
+}
+
 int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b,
                    uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
                    const WalkOpts& o, int coop_blocks, cudaStream_t st) {
@@ -1246,13 +1317,19 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   k_flags_ins<<<grid_for(nb), 256, 0, st>>>(H, G, b.events, nb, o, b);
   ++l;
   if (n_del > 0) {
-    k_save_rows<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, stamp, b);
-    ++l;
-    // The shadow pass must not move G's |E| counter: give it a scratch one.
-    DevGraph<kCapG> Gs = G;
-    Gs.edges = b.scratch_edges;
-    ShadowOp op{Gs, b.events, b.ctl};
-    l += launch_rounds<false>(op, nb, b, st);
+    if (shadow_lists_enabled()) {
+      k_sh_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, b);
+      k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, b);
+      l += 2;
+    } else {
+      k_save_rows<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, stamp, b);
+      ++l;
+      // The shadow pass must not move G's |E| counter: give it a scratch one.
+      DevGraph<kCapG> Gs = G;
+      Gs.edges = b.scratch_edges;
+      ShadowOp op{Gs, b.events, b.ctl};
+      l += launch_rounds<false>(op, nb, b, st);
+    }
     k_flags_del<<<grid_for(nb), 256, 0, st>>>(H, G, b.events, nb, o, b);
     ++l;
   }
