@@ -605,7 +605,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 // Phases: emit records + per-row lists | ranks | apply (spin on done) |
 // reset the per-row heads and counters. A record-buffer overflow skips the
 // apply phase and leaves the batch to the round engine (flow_done = 0).
-__global__ void __launch_bounds__(256) k_del_flow(CommitOp op, uint32_t nev, BatchDev b) {
+__global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, BatchDev b) {
   constexpr unsigned kAll = 0xFFFFFFFFu;
   cg::grid_group grid = cg::this_grid();
   const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
@@ -716,10 +716,8 @@ __global__ void __launch_bounds__(256) k_del_flow(CommitOp op, uint32_t nev, Bat
     }
     grid.sync();
     if (tid == 0) ctl->fl_t[3] = global_ns();
-    // Phase 3: apply in dataflow order. Chain depth (the critical path, in
-    // events) is tracked per row for the report's round counter.
+    // Phase 3: apply in dataflow order.
     Acc acc{};
-    uint32_t max_depth = 0;
     // Each warp owns events k = wid + j*nw (j = 0, 1, ...) and keeps a
     // window of its 8 lowest unapplied ones, applying whichever is ready
     // (non-blocking readiness polls), so an event stuck behind a long chain
@@ -741,19 +739,12 @@ __global__ void __launch_bounds__(256) k_del_flow(CommitOp op, uint32_t nev, Bat
           ready = ld_acquire(done + b.fl_row[base + t]) >= b.fl_rank[base + t];
         if (!__all_sync(kAll, ready)) continue;
         __threadfence();
-        uint32_t depth = 0;
-        for (uint32_t t = lane; t < n; t += 32) depth = max(depth, b.fl_depth[b.fl_row[base + t]]);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) depth = max(depth, __shfl_xor_sync(kAll, depth, off));
-        ++depth;
-        max_depth = max(max_depth, depth);
         uint32_t e = 0;
         if ((ctl->commit_err >> 8) > k) e = op.apply_warp(k, lane, acc);
         if (lane == 0) {
           b.state[k] = e ? 2 : 1;
           if (e) atomicMin(&b.ctl->commit_err, (static_cast<unsigned long long>(k) << 8) | e);
         }
-        for (uint32_t t = lane; t < n; t += 32) b.fl_depth[b.fl_row[base + t]] = depth;
         __threadfence();
         __syncwarp();
         for (uint32_t t = lane; t < n; t += 32) atomicAdd(done + b.fl_row[base + t], 1u);
@@ -769,7 +760,6 @@ __global__ void __launch_bounds__(256) k_del_flow(CommitOp op, uint32_t nev, Bat
       if (!progressed) __nanosleep(64);
     }
     op.flush(acc);
-    if (lane == 0 && max_depth) atomicMax(&b.ctl->fl_depth, max_depth);
   }
   grid.sync();
   if (tid == 0) ctl->fl_t[4] = global_ns();
@@ -780,7 +770,6 @@ __global__ void __launch_bounds__(256) k_del_flow(CommitOp op, uint32_t nev, Bat
       const uint32_t x = b.fl_row[base + i];
       head[x] = kNoSlot;
       done[x] = 0;
-      b.fl_depth[x] = 0;
     }
     if (lane == 0 && b.fl_promo[k]) {
       const DevEvent& e = op.ev[k];
@@ -792,7 +781,7 @@ __global__ void __launch_bounds__(256) k_del_flow(CommitOp op, uint32_t nev, Bat
   if (tid == 0) ctl->fl_t[5] = global_ns();
   if (tid == 0 && !overflow) {
     ctl->flow_done = 1;
-    ctl->rounds = ctl->rounds + ctl->fl_depth;
+    ctl->rounds = ctl->rounds + 1;
   }
 }
 
