@@ -260,12 +260,15 @@ def run_ours(args):
             sharded.replay_events(batches[b][0], batches[b][1], b)
 
     def step_e2e():
+        # The reference-facing replay(stream) from the host stream (page-locked
+        # UpdateStream): every batch's events cross PCIe inside the step, the
+        # reports come back; the library pipelines the uploads with the work.
         st.restore()
+        if sharded is None:
+            st.replay(stream)
+            return
         for b in range(nb):
-            if sharded is None:
-                st.replay_events(batches[b][0], batches[b][1], b)
-            else:
-                sharded.replay_events(batches[b][0], batches[b][1], b)
+            sharded.replay_events(batches[b][0], batches[b][1], b)
 
     def barrier():
         if world > 1:
@@ -355,6 +358,7 @@ def run_ours(args):
             "d2h_bytes_per_step": int(estats["d2h_bytes"] // args.steps),
         },
         "gpu_launches": int(stats["kernel_launches"]),
+        "graph_launches": int(stats["graph_launches"]),
         "roofline": {
             "kernel": walk_key, "bound": "hbm", "achieved": achieved, "peak": peak,
             "peak_source": peak_src, "unit": "GB/s",

@@ -149,6 +149,7 @@ typedef struct dyg_stats {
   double flow_ms_rank;
   double flow_ms_apply;
   double flow_ms_reset;
+  uint64_t graph_launches;      /* CUDA-graph replays (one per batch or per range) */
 } dyg_stats;
 
 typedef struct dyg_session dyg_session;
@@ -186,6 +187,18 @@ int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
  * in error messages; NULL means 0..n-1). */
 int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* positions,
                       size_t n, uint32_t batch_index, dyg_batch_report* out);
+
+/* SparsifierState::replay(stream) (sparsifier.cpp:550-559) from a host
+ * stream: out[b] for every batch b < batch_count. Events grouped by batch
+ * (batch b = events[batch_offsets[b] .. batch_offsets[b+1]); batch_offsets
+ * NULL = found by one pass over batch_index) replay with the upload of later
+ * batches overlapping the work on earlier ones; ungrouped streams replay
+ * batch by batch. On an error the batches before the failing one are
+ * committed and reported, the failing one returns the reference's error and
+ * later ones do not run. */
+int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
+                      const uint64_t* batch_offsets, uint32_t batch_count,
+                      dyg_batch_report* out);
 
 /* Device-resident stream: upload once, then replay batches with no per-batch
  * host->device traffic (used for the kernel-level benchmark). */

@@ -46,6 +46,7 @@ STATS_FIELDS = (
     ("commit_ms_deletion", "f8"), ("reach_tail_ms", "f8"), ("minpath_tail_ms", "f8"),
     ("commit_rounds_deletion", "u8"), ("flow_ms_promote", "f8"), ("flow_ms_emit", "f8"),
     ("flow_ms_rank", "f8"), ("flow_ms_apply", "f8"), ("flow_ms_reset", "f8"),
+    ("graph_launches", "u8"),
 )
 STATS_DTYPE = np.dtype([(n, "<" + t) for n, t in STATS_FIELDS])
 
@@ -91,6 +92,7 @@ def lib() -> C.CDLL:
         "dyg_replay_batch": (i32, [vp, vp, sz, u32, u32, vp]),
         "dyg_replay_events": (i32, [vp, vp, vp, sz, u32, vp]),
         "dyg_stream_upload": (i32, [vp, vp, sz, u32]),
+        "dyg_replay_stream": (i32, [vp, vp, sz, vp, u32, vp]),
         "dyg_replay_uploaded": (i32, [vp, u32, vp]),
         "dyg_replay_uploaded_range": (i32, [vp, u32, u32, vp]),
         "dyg_apply_insertion": (i32, [vp, u32, u32, dbl, C.POINTER(C.c_int)]),

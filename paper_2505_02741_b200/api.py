@@ -248,6 +248,18 @@ class UpdateStream:
         L.dygh_stream_free(h)
         return s
 
+    def batch_offsets(self):
+        """Batch b = events[off[b]:off[b+1]] when the events are grouped by
+        batch (the generator's and loader's order), else None. Cached."""
+        key = (self.events.ctypes.data, len(self.events), self.batch_count)
+        if getattr(self, "_off_key", None) != key:
+            bi = self.events["batch_index"]
+            off = None
+            if len(bi) == 0 or (bool(np.all(bi[1:] >= bi[:-1])) and int(bi[-1]) < self.batch_count):
+                off = np.searchsorted(bi, np.arange(self.batch_count + 1)).astype(np.uint64)
+            self._off, self._off_key = off, key
+        return self._off
+
     def batch(self, b: int):
         """(events, positions) of batch b, in stream order. A batch stored
         contiguously (the usual case) is returned as a view of the stream's
@@ -370,10 +382,17 @@ class SparsifierState:
         return BatchReport.from_record(rep[0])
 
     def replay(self, stream: UpdateStream) -> UpdateReport:
+        """sparsifier.cpp:550-559. One library call: the host stream's upload
+        is pipelined with the batches (dyg_replay_stream)."""
         out = UpdateReport()
-        for b in range(stream.batch_count):
-            ev, pos = stream.batch(b)
-            out.batches.append(self.replay_events(ev, pos, b))
+        n = stream.batch_count
+        if n:
+            off = stream.batch_offsets()
+            rep = np.zeros(n, REPORT_DTYPE)
+            _check(_lib.lib().dyg_replay_stream(
+                self._s, ptr(stream.events), len(stream.events),
+                ptr(off) if off is not None else None, n, ptr(rep)))
+            out.batches = [BatchReport.from_record(r) for r in rep]
         out.final_density_graph = self.info(0)[2]
         out.final_density_sparsifier = self.info(1)[2]
         return out

@@ -823,10 +823,11 @@ __global__ void k_flags_del(DevGraph<kCapH> H, DevGraph<kCapG> S,
   b.state[k] = 0;
 }
 
-__global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t counter,
-                          uint64_t seed, BatchDev b) {
+__global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t seed,
+                          BatchDev b) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nb || batch_aborted(b.ctl)) return;
+  const uint64_t counter = b.ctl->counter_base;
   const unsigned long long f = b.scan_in[k];
   const unsigned long long x = b.scan_out[k];
   const uint32_t ri = static_cast<uint32_t>(x & 0xFFFFFFFFull);
@@ -1240,8 +1241,9 @@ size_t scan_temp_bytes(uint32_t nb_cap) {
 // Batch control block initialisation on the device (a kernel instead of a
 // host->device copy: a copy-engine transfer in the stream costs several
 // microseconds of latency per batch).
-__global__ void k_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, uint32_t fast) {
+__global__ void k_ctl_init(CtlInitArgs a) {
   constexpr uint32_t kWords = sizeof(BatchCtl) / sizeof(uint32_t);
+  BatchCtl* ctl = a.ctl;
   uint32_t* w = reinterpret_cast<uint32_t*>(ctl);
   for (uint32_t i = threadIdx.x; i < kWords; i += blockDim.x) w[i] = 0;
   __syncthreads();
@@ -1249,18 +1251,44 @@ __global__ void k_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_li
     ctl->val_err = ~0ull;
     ctl->commit_err = ~0ull;
     ctl->first_absent = 0xFFFFFFFFu;
-    ctl->limit = limit;
-    ctl->use_absent_limit = use_absent_limit;
+    ctl->limit = a.limit;
+    ctl->use_absent_limit = a.use_absent_limit;
     ctl->reach.t_start = ctl->reach.t_drain = ctl->minpath.t_start = ctl->minpath.t_drain = ~0ull;
-    ctl->fast = fast;
+    ctl->fast = a.fast;
+    ctl->counter_base = a.counter_base;
   }
 }
 
-int launch_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, uint32_t fast,
-                    cudaStream_t st) {
+int launch_ctl_init(const CtlInitArgs& a, cudaStream_t st) {
   static_assert(sizeof(BatchCtl) % sizeof(uint32_t) == 0, "BatchCtl words");
-  k_ctl_init<<<1, 128, 0, st>>>(ctl, limit, use_absent_limit, fast);
+  k_ctl_init<<<1, 128, 0, st>>>(a);
   return 1;
+}
+
+bool ctl_init_node_args(cudaGraphNode_t n, CtlInitArgs* out) {
+  cudaGraphNodeType t;
+  if (cudaGraphNodeGetType(n, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
+  cudaKernelNodeParams kp{};
+  if (cudaGraphKernelNodeGetParams(n, &kp) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (kp.func != reinterpret_cast<void*>(k_ctl_init)) return false;
+  *out = *static_cast<const CtlInitArgs*>(kp.kernelParams[0]);
+  return true;
+}
+
+cudaError_t ctl_init_node_update(cudaGraphExec_t ex, cudaGraphNode_t n, const CtlInitArgs& a) {
+  CtlInitArgs copy = a;
+  void* args[] = {&copy};
+  cudaKernelNodeParams kp{};
+  kp.func = reinterpret_cast<void*>(k_ctl_init);
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(128);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  return cudaGraphExecKernelNodeSetParams(ex, n, &kp);
 }
 
 // Insertion (kind 0) / other event counts of a batch: out[0], out[1].
@@ -1325,7 +1353,8 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   size_t temp = b.cub_temp_bytes;
   cuda_check(cub::DeviceScan::ExclusiveSum(b.cub_temp, temp, b.scan_in, b.scan_out, nb, st),
              "query scan");
-  k_scatter<<<grid_for(nb), 256, 0, st>>>(b.events, nb, counter, o.seed, b);
+  (void)counter;  // read on the device from the control block (graph replay)
+  k_scatter<<<grid_for(nb), 256, 0, st>>>(b.events, nb, o.seed, b);
   return l + 2;
 }
 

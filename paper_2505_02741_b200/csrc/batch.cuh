@@ -77,6 +77,17 @@ struct BatchCtl {
   unsigned int fl_changed[2];  // fallback-promotion fixpoint
   unsigned int fl_depth;     // longest chain of row-sharing events
   unsigned long long fl_t[6];  // %globaltimer at the phase boundaries
+  unsigned long long counter_base;  // update_counter_ at batch start (:431)
+};
+
+// Arguments of the batch control-block initialisation kernel: the only
+// per-batch values a captured batch graph has to be re-pointed with.
+struct CtlInitArgs {
+  BatchCtl* ctl;
+  uint32_t limit;
+  uint32_t use_absent_limit;
+  uint32_t fast;
+  unsigned long long counter_base;
 };
 
 struct WalkOpts {
@@ -137,8 +148,11 @@ struct BatchDev {
 };
 
 // Host launchers (batch.cu); each returns kernels launched.
-int launch_ctl_init(BatchCtl* ctl, uint32_t limit, uint32_t use_absent_limit, uint32_t fast,
-                    cudaStream_t st);
+int launch_ctl_init(const CtlInitArgs& a, cudaStream_t st);
+// Graph support: is `n` a k_ctl_init kernel node (then *out = its args)?
+bool ctl_init_node_args(cudaGraphNode_t n, CtlInitArgs* out);
+cudaError_t ctl_init_node_update(cudaGraphExec_t ex, cudaGraphNode_t n, const CtlInitArgs& a);
+bool shadow_lists_enabled();
 int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStream_t st);
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st);

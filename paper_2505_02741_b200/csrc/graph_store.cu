@@ -223,11 +223,14 @@ void GraphStore<C>::ensure_pool(uint64_t top, uint64_t free_entries, cudaStream_
   double* nw = nullptr;
   cuda_check(cudaMalloc(&nid, sizeof(uint32_t) * cap), "grow pool");
   cuda_check(cudaMalloc(&nw, sizeof(double) * cap), "grow pool");
-  if (top) {
-    cuda_check(cudaMemcpyAsync(nid, v_.pool_id, sizeof(uint32_t) * top, cudaMemcpyDeviceToDevice, st),
-               "grow pool");
-    cuda_check(cudaMemcpyAsync(nw, v_.pool_w, sizeof(double) * top, cudaMemcpyDeviceToDevice, st),
-               "grow pool");
+  // Copy the whole old capacity, not just `top`: batches already enqueued on
+  // `st` may append past the host's last known top before this copy runs.
+  (void)top;
+  if (v_.pool_cap) {
+    cuda_check(cudaMemcpyAsync(nid, v_.pool_id, sizeof(uint32_t) * v_.pool_cap,
+                               cudaMemcpyDeviceToDevice, st), "grow pool");
+    cuda_check(cudaMemcpyAsync(nw, v_.pool_w, sizeof(double) * v_.pool_cap,
+                               cudaMemcpyDeviceToDevice, st), "grow pool");
   }
   cuda_check(cudaStreamSynchronize(st), "grow pool");
   cudaFree(v_.pool_id);

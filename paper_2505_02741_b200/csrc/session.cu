@@ -87,6 +87,27 @@ struct Timer {
   }
 };
 
+// One instantiated CUDA graph of an enqueue sequence. Its only per-launch
+// input is the update counter, carried by the k_ctl_init nodes.
+struct CapturedGraph {
+  uint64_t key = 0;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;        // kept: node handles refer to it
+  std::vector<cudaGraphNode_t> ctl_nodes;
+  std::vector<CtlInitArgs> ctl_args;  // as captured
+  uint64_t cap_base = 0;              // update counter at capture
+  uint64_t base = 0;                  // update counter the nodes currently hold
+  int launches = 0;
+  std::vector<int> per_batch;  // range graphs: kernels per batch
+  uint64_t last_use = 0;
+};
+
+uint64_t fnv(uint64_t h, const void* p, size_t n) {
+  const unsigned char* c = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+  return h;
+}
+
 }  // namespace
 
 struct dyg_session {
@@ -147,10 +168,28 @@ struct dyg_session {
   uint32_t ctl_cap = 0;
   unsigned int* d_abort = nullptr; // set by a failing batch; later batches no-op
   bool debug_sync = false;
+  // Captured device sequences (one batch, or a whole uploaded range), keyed
+  // by a fingerprint of everything baked into their kernel arguments.
+  std::vector<CapturedGraph> graphs;
+  bool graphs_on = true;   // DYG_GRAPHS=0 disables; a failed capture disables
+  bool capturing = false;
+  uint64_t graph_clock = 0;
+  uint64_t stream_gen = 0;  // bumped by every dyg_stream_upload
+  // dyg_replay_stream: host stream replayed with its upload pipelined.
+  cudaStream_t copy_stream = nullptr;
+  DevEvent* d_replay = nullptr;
+  uint64_t replay_cap = 0;
+  uint32_t* d_kinds = nullptr;
+  uint32_t* h_kinds = nullptr;
+  uint64_t kinds_cap = 0;
+  std::vector<cudaEvent_t> ready;
   bool no_fastpath = false;        // DYG_NO_FASTPATH: force the round engine
 };
 
 namespace {
+
+// Timing events: inside a stream capture they must be external record nodes.
+void record(dyg_session* s, cudaEvent_t e);
 
 void maybe_sync(dyg_session* s, const char* what) {
   if (s->debug_sync) check(cudaStreamSynchronize(s->stream), what);
@@ -330,6 +369,7 @@ struct Pending {
   const DevEvent* dev = nullptr;
   const DevEvent* host = nullptr;
   const uint64_t* pos = nullptr;
+  uint64_t pos_base = 0;      // stream position of event 0 when pos is null
   uint32_t nb = 0, n_ins = 0, n_del = 0, batch = 0;
   bool imm_msgs = false;
   std::chrono::steady_clock::time_point wall0;
@@ -351,7 +391,7 @@ void bind_pending(dyg_session* s, Pending& p) {
 
 [[noreturn]] void fail_validation(dyg_session* s, const Pending& p, unsigned long long val_err) {
   const uint32_t k = static_cast<uint32_t>(val_err >> 8);
-  const uint64_t pos = p.pos ? p.pos[k] : k;
+  const uint64_t pos = p.pos ? p.pos[k] : p.pos_base + k;
   std::string msg = event_error_message(static_cast<uint32_t>(val_err & 0xFF), pos, p.host[k]);
   if (p.imm_msgs) {
     char pre[64];
@@ -387,8 +427,9 @@ void phase_prepare(dyg_session* s, Pending& p) {
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
   if (p.n_del > 0) ensure_side_pool(s);
-  p.launches += launch_ctl_init(b.ctl, p.nb, use_absent_limit, fast, s->stream);
-  check(cudaEventRecord(p.tm[0].a, s->stream), "event");
+  p.launches += launch_ctl_init(CtlInitArgs{b.ctl, p.nb, use_absent_limit, fast, p.counter_base},
+                                s->stream);
+  record(s, p.tm[0].a);
   p.launches += launch_validate(b, p.nb, s->n, s->d_abort, s->stream);
   maybe_sync(s, "validate");
   if (p.n_del > 0 && ++s->stamp == 0) {  // stamps restart: clear the marks
@@ -421,15 +462,15 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     max_r = n_r;
     max_m = n_m;
   }
-  check(cudaEventRecord(p.tm[1].a, s->stream), "event");
+  record(s, p.tm[1].a);
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
     p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
                                s->d_work, s->stream);
     maybe_sync(s, "reach walks");
   }
-  check(cudaEventRecord(p.tm[1].b, s->stream), "event");
-  check(cudaEventRecord(p.tm[2].a, s->stream), "event");
+  record(s, p.tm[1].b);
+  record(s, p.tm[2].a);
   if (p.n_del > 0 && !o.freeze && max_m > 0) {
     WalkParams Pd = P;
     Pd.K = std::numeric_limits<double>::infinity();  // sparsifier.cpp:458-459
@@ -440,7 +481,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                                  &b.ctl->minpath, s->d_work, s->stream);
     maybe_sync(s, "minpath walks");
   }
-  check(cudaEventRecord(p.tm[2].b, s->stream), "event");
+  record(s, p.tm[2].b);
 }
 
 // Commit (:466-533) enqueue: restore the shadowed rows, run the commit
@@ -449,15 +490,15 @@ void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
-  check(cudaEventRecord(p.tm[3].a, s->stream), "event");
+  record(s, p.tm[3].a);
   if (p.n_del > 0) p.launches += launch_restore(s->G.view(), b, p.nb, s->stream);
   if (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath)
     p.launches += launch_insert_fastpath(s->G.view(), s->H.view(), b, p.nb, o, s->stream);
   p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
   maybe_sync(s, "commit");
-  check(cudaEventRecord(p.tm[3].b, s->stream), "event");
+  record(s, p.tm[3].b);
   p.launches += launch_finish(s->G.view(), s->H.view(), b, s->d_abort, s->stream);
-  check(cudaEventRecord(p.tm[0].b, s->stream), "event");
+  record(s, p.tm[0].b);
   if (download)
     check(cudaMemcpyAsync(p.hctl, b.ctl, sizeof(BatchCtl), cudaMemcpyDeviceToHost, s->stream),
           "ctl download");
@@ -518,7 +559,7 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   s->stats.total_ms += p.tm[0].ms();
   if (fail_k != ~0ull) {
     s->counter = p.counter_base + fail_k + 1;  // ++update_counter_ precedes the throw (:469)
-    const uint64_t pos = p.pos ? p.pos[fail_k] : fail_k;
+    const uint64_t pos = p.pos ? p.pos[fail_k] : p.pos_base + fail_k;
     fail(fail_code == kErrPool ? DYG_ERR_DEVICE : DYG_ERR_DATA,
          event_error_message(fail_code, pos, p.host[fail_k]));
   }
@@ -561,6 +602,141 @@ void reset_abort(dyg_session* s) {
   check(cudaMemsetAsync(s->d_abort, 0, sizeof(unsigned int), s->stream), "abort flag");
 }
 
+void record(dyg_session* s, cudaEvent_t e) {
+  if (s->capturing)
+    check(cudaEventRecordWithFlags(e, s->stream, cudaEventRecordExternal), "event");
+  else
+    check(cudaEventRecord(e, s->stream), "event");
+}
+
+// ------------------------------------------------------------ CUDA graphs
+// A batch is ~15 short kernels; launched one by one, the host launch cost
+// and the inter-kernel gaps are a visible share of a batch (tens of us on
+// ~0.4 ms). The enqueue sequence of a batch -- or of a whole uploaded range
+// -- is captured once into a CUDA graph and replayed with one launch. Every
+// kernel argument except the update counter is a pure function of the batch
+// shape and of the session's buffer pointers, so the graph is keyed by a
+// fingerprint of exactly those; the counter lives in the k_ctl_init nodes
+// and is re-pointed per launch when it differs.
+bool graphs_usable(const dyg_session* s) { return s->graphs_on && !s->debug_sync; }
+
+uint64_t session_fingerprint(dyg_session* s, uint64_t tag) {
+  uint64_t h = fnv(1469598103934665603ull, &tag, sizeof tag);
+  const auto add_graph = [&](auto v) {
+    const void* ptrs[] = {v.slab, v.cap, v.pool_id, v.pool_w, v.pool_top, v.edges};
+    h = fnv(h, ptrs, sizeof ptrs);
+    h = fnv(h, &v.pool_cap, sizeof v.pool_cap);
+    h = fnv(h, &v.n, sizeof v.n);
+  };
+  add_graph(s->G.view());
+  add_graph(s->H.view());
+  BatchDev b = s->b;  // all buffer pointers and capacities; per-batch fields blanked
+  b.ctl = nullptr;
+  b.events = nullptr;
+  b.side_top = nullptr;
+  b.scratch_edges = nullptr;
+  h = fnv(h, &b, sizeof b);
+  const WalkOpts o = walk_opts(s);
+  h = fnv(h, &o, sizeof o);
+  const void* fixed[] = {s->d_work, s->d_abort, s->d_counts, s->timers, s->h_ctl};
+  h = fnv(h, fixed, sizeof fixed);
+  const uint32_t flags = (s->no_fastpath ? 1u : 0u) | (shadow_lists_enabled() ? 2u : 0u);
+  h = fnv(h, &flags, sizeof flags);
+  if (!shadow_lists_enabled()) h = fnv(h, &s->stamp, sizeof s->stamp);
+  return h;
+}
+
+void destroy_graph(CapturedGraph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.graph) cudaGraphDestroy(g.graph);
+  g.exec = nullptr;
+  g.graph = nullptr;
+}
+
+CapturedGraph* find_graph(dyg_session* s, uint64_t key) {
+  for (CapturedGraph& g : s->graphs)
+    if (g.key == key) return &g;
+  return nullptr;
+}
+
+// Capture `enqueue` (returns the kernels it launched) into a graph. Returns
+// nullptr -- and turns graphs off for the session -- when capture is not
+// possible; the caller then enqueues eagerly.
+template <class F>
+CapturedGraph* capture_graph(dyg_session* s, uint64_t key, uint64_t counter, F&& enqueue) {
+  cudaGetLastError();
+  if (cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    s->graphs_on = false;
+    return nullptr;
+  }
+  s->capturing = true;
+  int launches = 0;
+  try {
+    launches = enqueue();
+  } catch (...) {
+    s->capturing = false;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(s->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    throw;
+  }
+  s->capturing = false;
+  CapturedGraph cg;
+  cudaError_t e1 = cudaStreamEndCapture(s->stream, &cg.graph);
+  cudaError_t e2 = (e1 == cudaSuccess && cg.graph) ? cudaGraphInstantiate(&cg.exec, cg.graph, 0)
+                                                   : cudaErrorUnknown;
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    if (std::getenv("DYG_GRAPH_DEBUG"))
+      std::fprintf(stderr, "dyg: graph capture failed (%s / %s); launching eagerly\n",
+                   cudaGetErrorString(e1), cudaGetErrorString(e2));
+    cudaGetLastError();
+    destroy_graph(cg);
+    s->graphs_on = false;
+    return nullptr;
+  }
+  size_t n = 0;
+  check(cudaGraphGetNodes(cg.graph, nullptr, &n), "graph nodes");
+  std::vector<cudaGraphNode_t> nodes(n);
+  check(cudaGraphGetNodes(cg.graph, nodes.data(), &n), "graph nodes");
+  for (cudaGraphNode_t node : nodes) {
+    CtlInitArgs a{};
+    if (ctl_init_node_args(node, &a)) {
+      cg.ctl_nodes.push_back(node);
+      cg.ctl_args.push_back(a);
+    }
+  }
+  cg.key = key;
+  cg.base = counter;
+  cg.cap_base = counter;
+  cg.launches = launches;
+  constexpr size_t kMaxGraphs = 8;
+  if (s->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+    size_t lru = 0;
+    for (size_t i = 1; i < s->graphs.size(); ++i)
+      if (s->graphs[i].last_use < s->graphs[lru].last_use) lru = i;
+    destroy_graph(s->graphs[lru]);
+    s->graphs.erase(s->graphs.begin() + lru);
+  }
+  s->graphs.push_back(std::move(cg));
+  return &s->graphs.back();
+}
+
+void launch_graph(dyg_session* s, CapturedGraph& g, uint64_t counter) {
+  if (counter != g.base) {
+    for (size_t i = 0; i < g.ctl_nodes.size(); ++i) {
+      CtlInitArgs a = g.ctl_args[i];
+      a.counter_base = a.counter_base - g.cap_base + counter;
+      check(ctl_init_node_update(g.exec, g.ctl_nodes[i], a), "graph counter update");
+    }
+    g.base = counter;
+  }
+  g.last_use = ++s->graph_clock;
+  check(cudaGraphLaunch(g.exec, s->stream), "graph launch");
+  s->stats.graph_launches += 1;
+}
+
 void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* host_events,
                   const uint64_t* positions, uint32_t nb, uint32_t n_ins, uint32_t n_del,
                   uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs) {
@@ -580,6 +756,34 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
   p.batch = batch_index;
   p.imm_msgs = immediate_msgs;
   reset_abort(s);
+  if (graphs_usable(s)) {
+    // Size every buffer first: nothing may allocate inside a capture.
+    ensure_batch(s, nb, n_del);
+    ensure_pools(s, n_ins, n_del);
+    if (n_del > 0) ensure_side_pool(s);
+    uint64_t key = session_fingerprint(s, 1);
+    const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
+                              reinterpret_cast<uint64_t>(p.hctl), reinterpret_cast<uint64_t>(p.hdec),
+                              reinterpret_cast<uint64_t>(p.tm), nb, n_ins, n_del};
+    key = fnv(key, shape, sizeof shape);
+    CapturedGraph* g = find_graph(s, key);
+    if (g == nullptr) {
+      g = capture_graph(s, key, p.counter_base, [&] {
+        Pending q = p;
+        phase_prepare(s, q);
+        phase_walk(s, q, true, 0, 0, 0, 0);
+        commit_enqueue(s, q);
+        return q.launches;
+      });
+    }
+    if (g != nullptr) {
+      launch_graph(s, *g, p.counter_base);
+      p.launches = g->launches;
+      check(cudaStreamSynchronize(s->stream), "batch");
+      commit_finalize(s, p, out);
+      return;
+    }
+  }
   phase_prepare(s, p);
   phase_walk(s, p, true, 0, 0, 0, 0);
   phase_commit(s, p, out);
@@ -669,35 +873,68 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
     s->range_timers.back().init();
   }
   std::vector<Pending> ps(count);
-  uint64_t counter = s->counter;
+  const uint64_t counter0 = s->counter;
   const auto wall0 = std::chrono::steady_clock::now();
   reset_abort(s);
-  for (uint32_t i = 0; i < count; ++i) {
-    const uint32_t b = first + i;
-    Pending& p = ps[i];
-    p.batch = b;
-    p.wall0 = wall0;
-    p.dctl = s->d_ctls + i;
-    p.hctl = s->h_ctls + i;
-    p.hdec = &s->h_counts[2];
-    p.tm = s->range_timers.data() + 4ull * i;
-    p.counter_base = counter;
-    if (b >= s->batch_cnt.size() || s->batch_cnt[b] == 0) continue;
-    const uint64_t off = s->batch_off[b];
-    p.dev = s->d_stream + off;
-    p.host = reinterpret_cast<const DevEvent*>(s->stream_events.data() + off);
-    p.pos = s->stream_positions.data() + off;
-    p.nb = static_cast<uint32_t>(s->batch_cnt[b]);
-    p.n_ins = static_cast<uint32_t>(s->batch_ins[b]);
-    p.n_del = static_cast<uint32_t>(s->batch_del[b]);
-    phase_prepare(s, p);
-    phase_walk(s, p, true, 0, 0, 0, 0);
-    commit_enqueue(s, p, false);
-    counter += p.nb;
+  // Host-side description of every batch (also what commit_finalize reads).
+  {
+    uint64_t counter = counter0;
+    for (uint32_t i = 0; i < count; ++i) {
+      const uint32_t b = first + i;
+      Pending& p = ps[i];
+      p.batch = b;
+      p.wall0 = wall0;
+      p.dctl = s->d_ctls + i;
+      p.hctl = s->h_ctls + i;
+      p.hdec = &s->h_counts[2];
+      p.tm = s->range_timers.data() + 4ull * i;
+      p.counter_base = counter;
+      if (b >= s->batch_cnt.size() || s->batch_cnt[b] == 0) continue;
+      const uint64_t off = s->batch_off[b];
+      p.dev = s->d_stream + off;
+      p.host = reinterpret_cast<const DevEvent*>(s->stream_events.data() + off);
+      p.pos = s->stream_positions.data() + off;
+      p.nb = static_cast<uint32_t>(s->batch_cnt[b]);
+      p.n_ins = static_cast<uint32_t>(s->batch_ins[b]);
+      p.n_del = static_cast<uint32_t>(s->batch_del[b]);
+      counter += p.nb;
+    }
   }
-  // All control blocks in one transfer (one copy-engine round trip per range).
-  check(cudaMemcpyAsync(s->h_ctls, s->d_ctls, sizeof(BatchCtl) * count, cudaMemcpyDeviceToHost,
-                        s->stream), "ctl download");
+  auto enqueue = [&] {
+    int launches = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+      Pending p = ps[i];
+      if (p.nb == 0) continue;
+      phase_prepare(s, p);
+      phase_walk(s, p, true, 0, 0, 0, 0);
+      commit_enqueue(s, p, false);
+      ps[i].launches = p.launches;
+      launches += p.launches;
+    }
+    // All control blocks in one transfer (one copy-engine round trip per range).
+    check(cudaMemcpyAsync(s->h_ctls, s->d_ctls, sizeof(BatchCtl) * count, cudaMemcpyDeviceToHost,
+                          s->stream), "ctl download");
+    return launches;
+  };
+  CapturedGraph* g = nullptr;
+  if (graphs_usable(s)) {
+    uint64_t key = session_fingerprint(s, 2);
+    const uint64_t shape[] = {first, count, s->stream_gen, reinterpret_cast<uint64_t>(s->d_stream),
+                              reinterpret_cast<uint64_t>(s->d_ctls),
+                              reinterpret_cast<uint64_t>(s->h_ctls),
+                              reinterpret_cast<uint64_t>(s->range_timers.data())};
+    key = fnv(key, shape, sizeof shape);
+    g = find_graph(s, key);
+    if (g == nullptr) g = capture_graph(s, key, counter0, enqueue);
+    else
+      for (uint32_t i = 0; i < count; ++i) ps[i].launches = g->per_batch[i];
+    if (g != nullptr) {
+      if (g->per_batch.empty())
+        for (uint32_t i = 0; i < count; ++i) g->per_batch.push_back(ps[i].launches);
+      launch_graph(s, *g, counter0);
+    }
+  }
+  if (g == nullptr) enqueue();
   check(cudaStreamSynchronize(s->stream), "batch range");
   for (uint32_t i = 0; i < count; ++i) {
     if (ps[i].nb == 0) {
@@ -705,6 +942,123 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
       continue;
     }
     commit_finalize(s, ps[i], &out[i]);  // throws at the first failing batch
+  }
+}
+
+// SparsifierState::replay(stream) (sparsifier.cpp:550-559) from a host
+// stream whose events are grouped by batch (batch b = [off[b], off[b+1])).
+// Uploads run on a copy stream, batch by batch, each followed by a device
+// count of its insertions / deletions; batch b's kernels wait only for batch
+// b's upload, so the PCIe transfer of later batches overlaps the walks and
+// commits of earlier ones, and the host enqueues batch b + 1 while batch b
+// runs. One synchronisation at the end; reports as in the uploaded-range
+// replay (a failing batch stops the ones after it).
+void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_t* off,
+                uint32_t nbatches, dyg_batch_report* out) {
+  if (nbatches == 0) return;
+  uint64_t max_nb = 1;
+  for (uint32_t b = 0; b < nbatches; ++b) max_nb = std::max<uint64_t>(max_nb, off[b + 1] - off[b]);
+  if (max_nb > 0xFFFFFFF0ull) fail(DYG_ERR_USAGE, "batch too large");
+  ensure_batch(s, static_cast<uint32_t>(max_nb), 0);
+  if (s->copy_stream == nullptr)
+    check(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking), "copy stream");
+  if (s->replay_cap < n) {
+    dev_free(s->d_replay);
+    dev_alloc(&s->d_replay, std::max<uint64_t>(n, 1), "replay events");
+    s->replay_cap = n;
+  }
+  if (s->kinds_cap < nbatches) {
+    dev_free(s->d_kinds);
+    if (s->h_kinds) cudaFreeHost(s->h_kinds);
+    s->h_kinds = nullptr;
+    dev_alloc(&s->d_kinds, 2ull * nbatches, "kind counts");
+    check(cudaMallocHost(reinterpret_cast<void**>(&s->h_kinds), 2 * sizeof(uint32_t) * nbatches),
+          "pinned kind counts");
+    s->kinds_cap = nbatches;
+  }
+  if (s->ctl_cap < nbatches) {
+    dev_free(s->d_ctls);
+    if (s->h_ctls) cudaFreeHost(s->h_ctls);
+    s->h_ctls = nullptr;
+    dev_alloc(&s->d_ctls, nbatches, "batch control blocks");
+    check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctls), sizeof(BatchCtl) * nbatches),
+          "pinned control blocks");
+    s->ctl_cap = nbatches;
+  }
+  while (s->range_timers.size() < 4ull * nbatches) {
+    s->range_timers.emplace_back();
+    s->range_timers.back().init();
+  }
+  while (s->ready.size() < nbatches) {
+    cudaEvent_t e;
+    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    s->ready.push_back(e);
+  }
+  // 1. Uploads and kind counts, all batches, on the copy stream.
+  const bool pinned = host_pinned(events);
+  for (uint32_t b = 0; b < nbatches; ++b) {
+    const uint64_t nb = off[b + 1] - off[b];
+    if (nb) {
+      check(cudaMemcpyAsync(s->d_replay + off[b], events + off[b], sizeof(DevEvent) * nb,
+                            pinned ? cudaMemcpyHostToDevice : cudaMemcpyDefault, s->copy_stream),
+            "events upload");
+      s->stats.h2d_bytes += sizeof(DevEvent) * nb;
+      s->stats.kernel_launches += launch_count_kinds(s->d_replay + off[b], static_cast<uint32_t>(nb),
+                                                     s->d_kinds + 2ull * b, s->copy_stream);
+      check(cudaMemcpyAsync(s->h_kinds + 2ull * b, s->d_kinds + 2ull * b, 2 * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s->copy_stream), "kind counts");
+    }
+    check(cudaEventRecord(s->ready[b], s->copy_stream), "upload event");
+  }
+  // 2. Batches in order on the session stream.
+  std::vector<Pending> ps(nbatches);
+  const auto wall0 = std::chrono::steady_clock::now();
+  reset_abort(s);
+  uint64_t counter = s->counter, sum_ins = 0, sum_del = 0;
+  for (uint32_t b = 0; b < nbatches; ++b) {
+    Pending& p = ps[b];
+    p.batch = b;
+    p.wall0 = wall0;
+    p.dctl = s->d_ctls + b;
+    p.hctl = s->h_ctls + b;
+    p.hdec = &s->h_counts[2];
+    p.tm = s->range_timers.data() + 4ull * b;
+    p.counter_base = counter;
+    p.nb = static_cast<uint32_t>(off[b + 1] - off[b]);
+    if (p.nb == 0) continue;
+    p.dev = s->d_replay + off[b];
+    p.host = reinterpret_cast<const DevEvent*>(events + off[b]);
+    p.pos = nullptr;
+    p.pos_base = off[b];
+    check(cudaEventSynchronize(s->ready[b]), "upload");
+    p.n_ins = s->h_kinds[2ull * b];
+    p.n_del = s->h_kinds[2ull * b + 1];
+    sum_ins += p.n_ins;
+    sum_del += p.n_del;
+    // Pool growth copies on the session stream behind the enqueued batches;
+    // the deletion buffers and the side pool are freed and reallocated, so
+    // let the enqueued batches drain first when they have to grow.
+    ensure_pools(s, sum_ins, sum_del);
+    if (p.n_del > s->nd_cap ||
+        (p.n_del > 0 && (s->b.side_id == nullptr || s->side_cap < s->G.pool_capacity())))
+      check(cudaStreamSynchronize(s->stream), "buffer growth");
+    ensure_batch(s, p.nb, p.n_del);
+    if (p.n_del > 0) ensure_side_pool(s);
+    check(cudaStreamWaitEvent(s->stream, s->ready[b], 0), "upload wait");
+    phase_prepare(s, p);
+    phase_walk(s, p, true, 0, 0, 0, 0);
+    commit_enqueue(s, p, false);
+    counter += p.nb;
+  }
+  check(cudaMemcpyAsync(s->h_ctls, s->d_ctls, sizeof(BatchCtl) * nbatches, cudaMemcpyDeviceToHost,
+                        s->stream), "ctl download");
+  check(cudaStreamSynchronize(s->stream), "stream replay");
+  for (uint32_t b = 0; b < nbatches; ++b) {
+    if (ps[b].nb == 0) {
+      empty_report(s, b, &out[b]);
+      continue;
+    }
+    commit_finalize(s, ps[b], &out[b]);  // throws at the first failing batch
   }
 }
 
@@ -818,6 +1172,10 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->n = g->n;
       s->debug_sync = std::getenv("DYG_DEBUG_SYNC") != nullptr;
       s->no_fastpath = std::getenv("DYG_NO_FASTPATH") != nullptr;
+      {
+        const char* e = std::getenv("DYG_GRAPHS");
+        s->graphs_on = !(e && std::atoi(e) == 0);
+      }
       s->G.upload(g->n, g->row_ptr, g->ids, g->w, s->stream);
       s->H.upload(h->n, h->row_ptr, h->ids, h->w, s->stream);
       s->g_edges = g->row_ptr[g->n] / 2;
@@ -867,6 +1225,17 @@ void dyg_session_destroy(dyg_session* s) {
   if (s == nullptr) return;
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (CapturedGraph& g : s->graphs) destroy_graph(g);
+  s->graphs.clear();
+  if (s->copy_stream) cudaStreamSynchronize(s->copy_stream);
+  for (cudaEvent_t e : s->ready) cudaEventDestroy(e);
+  s->ready.clear();
+  dev_free(s->d_replay);
+  dev_free(s->d_kinds);
+  if (s->h_kinds) cudaFreeHost(s->h_kinds);
+  s->h_kinds = nullptr;
+  if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
+  s->copy_stream = nullptr;
   free_batch(s);
   dev_free(s->b.mout.has_path);
   dev_free(s->b.mout.path_len);
@@ -953,6 +1322,7 @@ int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
     check(cudaSetDevice(s->device), "set device");
     uint32_t nbatches = batch_count;
     for (size_t i = 0; i < n_events; ++i) nbatches = std::max(nbatches, events[i].batch_index + 1);
+    ++s->stream_gen;
     s->batch_cnt.assign(nbatches, 0);
     s->batch_ins.assign(nbatches, 0);
     s->batch_del.assign(nbatches, 0);
@@ -1016,6 +1386,52 @@ int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
     if (!s->opt.batched) fail(DYG_ERR_USAGE, "batch ranges need batched (deferred) mode");
     check(cudaSetDevice(s->device), "set device");
     run_uploaded_range(s, first, count, out);
+  });
+}
+
+int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
+                      const uint64_t* batch_offsets, uint32_t batch_count,
+                      dyg_batch_report* out) {
+  return guarded([&] {
+    if (s == nullptr || (batch_count && out == nullptr) || (n_events && events == nullptr))
+      fail(DYG_ERR_USAGE, "null argument");
+    check(cudaSetDevice(s->device), "set device");
+    // Batch ranges: given, or found by one pass when the events are grouped.
+    std::vector<uint64_t> off;
+    const uint64_t* o = batch_offsets;
+    bool grouped = true;
+    if (o == nullptr) {
+      off.assign(batch_count + 1ull, 0);
+      uint32_t prev = 0;
+      for (size_t i = 0; i < n_events && grouped; ++i) {
+        const uint32_t bi = events[i].batch_index;
+        if (bi < prev || bi >= batch_count) grouped = false;
+        else ++off[bi + 1ull];
+        prev = bi;
+      }
+      for (uint32_t b = 0; b < batch_count; ++b) off[b + 1ull] += off[b];
+      o = off.data();
+    } else if (o[batch_count] != n_events || o[0] != 0) {
+      fail(DYG_ERR_USAGE, "batch offsets do not cover the events");
+    }
+    if (grouped && s->opt.batched) {
+      run_stream(s, events, n_events, o, batch_count, out);
+      return;
+    }
+    // Ungrouped events or immediate mode: the per-batch reference path.
+    for (uint32_t b = 0; b < batch_count; ++b) {
+      std::vector<dyg_event> ev;
+      std::vector<uint64_t> pos;
+      for (size_t i = 0; i < n_events; ++i)
+        if (events[i].batch_index == b) {
+          ev.push_back(events[i]);
+          pos.push_back(i);
+        }
+      if (s->opt.batched)
+        run_host_batch(s, ev.data(), pos.data(), ev.size(), b, &out[b], false);
+      else
+        run_immediate(s, ev.data(), pos.data(), ev.size(), b, &out[b]);
+    }
   });
 }
 

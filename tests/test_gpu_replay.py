@@ -312,3 +312,65 @@ def test_insertion_fast_path_matches_round_engine(oracle, dyg, monkeypatch, dup)
     compare_replay(dyg, oracle, g, h, ev, st.batch_count, K=100.0, T=100, s=16, seed=9)
     monkeypatch.setenv("DYG_NO_FASTPATH", "1")
     compare_replay(dyg, oracle, g, h, ev, st.batch_count, K=100.0, T=100, s=16, seed=9)
+
+
+def _replay_all_reference(oracle, g, h, ev, nb, K, T, s, seed):
+    ost = oracle.state(g, h, K=K, T=T, s=s, seed=seed)
+    ostream = oracle.stream(ev, nb)
+    return ost, [ost.replay_batch(ostream, b) for b in range(nb)]
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_replay_stream_pipelined_equals_reference(oracle, dyg, shuffle):
+    # replay(stream) in one call (dyg_replay_stream: uploads pipelined with the
+    # batches) must equal the reference's replay batch by batch; a stream whose
+    # events are not grouped by batch takes the per-batch path.
+    c, g, h, s = cfg_inputs(oracle, "C2")
+    ev = s.events()
+    if shuffle:
+        ev = ev[np.random.default_rng(3).permutation(len(ev))]
+        ev = ev[np.argsort(ev["batch_index"], kind="stable")][::-1].copy()
+    ost, refs = _replay_all_reference(oracle, g, h, ev, s.batch_count, 100.0, 100, 16, 42)
+    st = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h),
+                             dyg.SparsifierOptions(dyg.WalkConfig(100.0, 100, 16, 42), True, False))
+    stream = dyg.UpdateStream(ev, s.batch_count)
+    assert (stream.batch_offsets() is None) == shuffle
+    rep = st.replay(stream)
+    assert len(rep.batches) == s.batch_count
+    for r1, r2 in zip(refs, rep.batches):
+        for f in O.REPORT_EXACT:
+            assert r1[f] == getattr(r2, f), (f, r1[f], getattr(r2, f))
+    assert st.update_counter == ost.update_counter
+    assert same_rows(ost.graph().export(), st.rows(0))
+    assert same_rows(ost.sparsifier().export(), st.rows(1))
+
+
+def test_replay_stream_stops_at_failing_batch(oracle, dyg):
+    g = oracle.make_mesh(9, 9, 3)
+    h = oracle.build_initial_sparsifier(g, 0.1, 3)
+    rp, ids, _ = g.export()
+    edges = [(u, int(ids[i])) for u in range(len(rp) - 1) for i in range(rp[u], rp[u + 1])
+             if u < ids[i]]
+    ev = [(0, 0, 40, 0, 1.0), (0, 1, 50, 0, 1.0),
+          (1, edges[0][0], edges[0][1], 1, 0.0),
+          (1, edges[0][0], edges[0][1], 1, 0.0),             # fails
+          (0, 2, 60, 2, 1.0)]                                # never runs
+    ev = np.array(ev, dtype=O.EVENT_DTYPE)
+    ost = oracle.state(g, h, K=10.0, T=30, s=8, seed=3)
+    ostream = oracle.stream(ev, 3)
+    ost.replay_batch(ostream, 0)
+    with pytest.raises(O.OracleError) as oe:
+        ost.replay_batch(ostream, 1)
+    st = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h),
+                             dyg.SparsifierOptions(dyg.WalkConfig(10.0, 30, 8, 3), True, False))
+    with pytest.raises(dyg.Error) as de:
+        st.replay(dyg.UpdateStream(ev, 3))
+    assert str(de.value) == oe.value.message
+    assert st.update_counter == ost.update_counter
+    assert same_rows(ost.graph().export(), st.rows(0))
+    assert same_rows(ost.sparsifier().export(), st.rows(1))
+    # The session stays usable: the next replay continues from this state.
+    st2 = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h),
+                              dyg.SparsifierOptions(dyg.WalkConfig(10.0, 30, 8, 3), True, False))
+    st2.replay(dyg.UpdateStream(ev[:2], 1))
+    assert st2.update_counter == 2

@@ -27,9 +27,36 @@ for rep in range(3):
         walls.append(1e3 * (time.perf_counter() - t))
         devs.append(st.stats()["total_ms"] - before)
     tot = 1e3 * (time.perf_counter() - t_all)
+    print("graph launches", st.stats()["graph_launches"], "kernels", st.stats()["kernel_launches"])
     print(f"rep {rep}: total {tot:.2f} ms, sum wall {sum(walls):.2f}, sum device {sum(devs):.2f}")
-for b in range(len(walls)):
+for b in range(0):
     print(f"  batch {b:2d}: n={len(batches[b][0]):6d} wall {walls[b]:.3f} ms device {devs[b]:.3f} ms gap {walls[b]-devs[b]:.3f}")
 # host-side pieces
 ev = batches[0][0]
 t = time.perf_counter(); k = int((ev["kind"] == 1).sum()); print("numpy count ms", 1e3 * (time.perf_counter() - t))
+# H2D bandwidth of a pinned 2.5 MB buffer and the bare call overhead
+import torch
+src = torch.empty(2_516_592, dtype=torch.uint8).pin_memory()
+dst = torch.empty_like(src, device="cuda")
+for _ in range(3):
+    dst.copy_(src, non_blocking=True)
+torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(20):
+    dst.copy_(src, non_blocking=True)
+torch.cuda.synchronize()
+dt = (time.perf_counter() - t) / 20
+print(f"H2D 2.5 MB pinned: {dt*1e6:.1f} us ({2.5166/dt/1e3:.1f} GB/s)")
+empty = np.zeros(0, D.api.EVENT_DTYPE)
+t = time.perf_counter()
+for _ in range(200):
+    st.replay_events(empty, None, 0)
+print(f"empty replay_events call: {(time.perf_counter()-t)/200*1e6:.1f} us")
+one = batches[10][0][:1]
+t = time.perf_counter()
+for _ in range(50):
+    try:
+        st.replay_events(one, None, 10)
+    except Exception:
+        pass
+print(f"1-event deletion batch call: {(time.perf_counter()-t)/50*1e6:.1f} us")
