@@ -5,6 +5,9 @@
 
 #include <cub/cub.cuh>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "batch.cuh"
 #include "graph_store.cuh"
 
@@ -1185,18 +1188,23 @@ __global__ void k_unpack_min(MinOut m, uint32_t nq, int world, uint32_t slots, u
   for (uint32_t j = threadIdx.x; j < h->path_len; j += blockDim.x) dst[j] = path[j];
 }
 
-// Co-resident grid for a cooperative kernel (cached per kernel).
+// Co-resident grid for a cooperative kernel, cached per kernel (not per
+// kernel type: several cooperative kernels share a signature).
 template <typename K>
 int coop_blocks_for(K kernel) {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
-    cached = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  return cached;
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const void* key = reinterpret_cast<const void*>(kernel);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+  const int blocks = sms * (per_sm > 0 ? per_sm : 1);
+  cache.emplace(key, blocks);
+  return blocks;
 }
 
 template <bool kWarp, class Op>
