@@ -79,20 +79,37 @@ def make_inputs_oracle(orc, cfg):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    polled every 5 ms from a thread (the timed region is tens of ms), else
+    nvidia-smi at its 100 ms minimum."""
 
-    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason* bits
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "sw_power_cap": 0x4,
+    }
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.stop = index, [], None, threading.Event()
+        self.nvml = None
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -100,13 +117,30 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = self.reasons_fn(self.h)
+                self.rows.append((float(mhz), float(self.max_mhz), int(rs)))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+            if len(parts) == 3:
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -116,15 +150,25 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        reasons = sorted({n for _, _, bits in self.rows for n, b in self.REASONS.items()
+                          if bits & b})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
+
+
+# Random-gather ceiling measured on this pool (tools/gather_peak.cu ->
+# profiles/gather_peak_r1.txt): best rows/s for (row bytes, table MB).
+GATHER_CEILING = {(64, 281): 69.6e9, (64, 563): 50.9e9, (128, 281): 43.6e9, (128, 563): 40.2e9}
+
+
+def gather_ceiling(row_bytes: int, table_mb: float) -> float:
+    """Rows/s ceiling, log-linear in table size between the measured points."""
+    import math
+    lo, hi = GATHER_CEILING[(row_bytes, 281)], GATHER_CEILING[(row_bytes, 563)]
+    t = min(max((math.log(table_mb) - math.log(281)) / (math.log(563) - math.log(281)), 0.0), 1.0)
+    return lo + t * (hi - lo)
 
 
 def load_peak():
@@ -220,6 +264,24 @@ def run_reference_arm(args):
                          "sample": f"{args.steps} consecutive batches of {args.config}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def gather_block(stats, n):
+    """K1 / K2 step rates against the measured random-gather ceiling (the DRAM
+    side is access-bound: ~40 G rows/s at any row size once the table is far
+    beyond L2, so the copy peak above is not reachable by a gather)."""
+    out = {}
+    for key, ms, steps, row, table in (
+            ("k_reach", stats["reach_ms"], stats["reach_steps"], 64, 96 * n / 2**20),
+            ("k_minpath", stats["minpath_ms"], stats["minpath_steps"], 128, 128 * n / 2**20)):
+        if ms <= 0:
+            continue
+        rate = steps / (ms * 1e-3)
+        ceil = gather_ceiling(row, table)
+        out[key] = {"steps_per_s": rate, "row_bytes": row, "table_mb": round(table, 1),
+                    "ceiling_rows_per_s": ceil, "frac": rate / ceil}
+    out["source"] = "profiles/gather_peak_r1.txt (tools/gather_peak.cu, measured on this pool)"
+    return out
 
 
 def run_ours(args):
@@ -368,6 +430,7 @@ def run_ours(args):
             "avg_launch_ms": wms / max(1, stats["batches"] // 2),
             "dominant_phase": dom,
         },
+        "gather_roofline": gather_block(stats, g.vertex_count()),
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
         "device_ms_per_step": stats["total_ms"] / args.steps,
         "walker_steps_per_step": (stats["reach_steps"] + stats["minpath_steps"]) / args.steps,

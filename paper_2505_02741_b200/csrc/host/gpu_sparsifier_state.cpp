@@ -88,24 +88,16 @@ BatchReport GpuSparsifierState::replay_batch(const UpdateStream& stream,
   return r;
 }
 
-// sparsifier.cpp:550-559; the stream is grouped by batch once.
+// sparsifier.cpp:550-559, one library call: dyg_replay_stream pipelines the
+// upload of later batches with the work on earlier ones (events grouped by
+// batch; an ungrouped stream replays batch by batch inside the library).
 UpdateReport GpuSparsifierState::replay(const UpdateStream& stream) {
   const std::vector<dyg_event> ev = flatten(stream);
-  std::vector<std::vector<dyg_event>> per(stream.batch_count);
-  std::vector<std::vector<std::uint64_t>> pos(stream.batch_count);
-  for (std::size_t i = 0; i < ev.size(); ++i) {
-    if (ev[i].batch_index < stream.batch_count) {
-      per[ev[i].batch_index].push_back(ev[i]);
-      pos[ev[i].batch_index].push_back(i);
-    }
-  }
   UpdateReport report;
-  report.batches.reserve(stream.batch_count);
-  for (std::uint32_t b = 0; b < stream.batch_count; ++b) {
-    BatchReport r{};
-    raise(dyg_replay_events(session_, per[b].data(), pos[b].data(), per[b].size(), b, &r));
-    report.batches.push_back(r);
-  }
+  report.batches.resize(stream.batch_count);
+  if (stream.batch_count)
+    raise(dyg_replay_stream(session_, ev.data(), ev.size(), nullptr, stream.batch_count,
+                            report.batches.data()));
   double dg = 0.0, dh = 0.0;
   raise(dyg_graph_info(session_, 0, nullptr, nullptr, &dg));
   raise(dyg_graph_info(session_, 1, nullptr, nullptr, &dh));
