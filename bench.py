@@ -359,6 +359,14 @@ def run_ours(args):
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     stats = st.stats()
+    # Diagnostic: the snapshot restore each step begins with (not update work).
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(torch_stream)
+    for _ in range(3):
+        st.restore()
+    r1.record(torch_stream)
+    torch.cuda.synchronize()
+    restore_ms = r0.elapsed_time(r1) / 3
     # Check the final state of the last timed step against the first run.
     rep_events = n_events
 
@@ -433,6 +441,7 @@ def run_ours(args):
         "gather_roofline": gather_block(stats, g.vertex_count()),
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in kern.items()},
         "device_ms_per_step": stats["total_ms"] / args.steps,
+        "restore_ms_per_step": restore_ms,
         "walker_steps_per_step": (stats["reach_steps"] + stats["minpath_steps"]) / args.steps,
         "commit_rounds_per_step": stats["commit_rounds"] / args.steps,
         "commit_ms_per_step_deletion_batches": stats["commit_ms_deletion"] / args.steps,

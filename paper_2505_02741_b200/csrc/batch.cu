@@ -81,16 +81,192 @@ __device__ __forceinline__ void flush_acc(const Acc& a, BatchCtl* ctl, unsigned 
   if (lead && dh && h_edges) atomicAdd(h_edges, dh);
 }
 
+// Insertion fast path. In an insertion-only batch where every key is new to
+// G (k_flags_ins) and no key repeats within the batch (k_fp_check), event k's
+// whole commit (:473-488 with :220-241) is: push_back(u: v, w) and
+// push_back(v: u, w) into G, and -- when kept -- the same two appends into H
+// with weight G.w(u,v) = w. H lacks the key because H is a subgraph of G.
+// Rows only receive appends, in event order. Each append record r = 2k +
+// side (row u or v of event k) is pushed onto its row's lock-free list
+// (k_fp_link, one atomic exchange per record). The list head owns the row:
+// a sole record (the vast majority) appends directly, a head with followers
+// applies the row's records in increasing r, i.e. event order (k_fp_write,
+// one thread per record and graph). Any violated precondition sets
+// not_simple BEFORE anything is written (k_fp_check) and the round engine
+// (k_rounds) commits the batch instead. The list heads are left empty for
+// the next batch.
+__global__ void k_fp_link(const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
+  unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
+  if (live) {
+    const DevEvent e = ev[k];
+    const uint32_t s = b.slot[k];
+    bool have = false, reached = false;
+    if (s != kNoSlot) {
+      have = true;
+      reached = b.rout.reached[s] != 0;
+      steps = b.rout.steps[s];
+    }
+    const bool kept = !o.freeze && !(o.K != 0.0 && have && reached);
+    const uint32_t gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
+    const uint32_t gv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
+    b.fp_next[0][2 * k] = gu;
+    b.fp_next[0][2 * k + 1] = gv;
+    if (kept) {
+      const uint32_t hu = atomicExch(b.fp_head[1] + e.u, 2 * k);
+      const uint32_t hv = atomicExch(b.fp_head[1] + e.v, 2 * k + 1);
+      b.fp_next[1][2 * k] = hu;
+      b.fp_next[1][2 * k + 1] = hv;
+    }
+    b.fp_kept[k] = kept ? 1 : 0;
+    b.dec[k] = kept ? 0u : 1u;
+    (kept ? kept_n : pruned_n) = 1;
+  }
+  kept_n = warp_sum(kept_n);
+  pruned_n = warp_sum(pruned_n);
+  const unsigned long long steps_sum = warp_sum(steps);
+  const unsigned long long steps_max = warp_max(steps);
+  if ((threadIdx.x & 31) == 0 && (kept_n | pruned_n)) {
+    atomicAdd(&b.ctl->fp_report[kInsSeen], kept_n + pruned_n);
+    atomicAdd(&b.ctl->fp_report[kInsKept], kept_n);
+    atomicAdd(&b.ctl->fp_report[kInsPruned], pruned_n);
+    atomicAdd(&b.ctl->fp_report[kWalkerSteps], steps_sum);
+    atomicMax(&b.ctl->fp_report[kMaxEventSteps], steps_max);
+  }
+}
+
+__device__ __forceinline__ uint32_t rec_row(const DevEvent* ev, uint32_t rec) {
+  const DevEvent& e = ev[rec >> 1];
+  return (rec & 1) ? e.v : e.u;
+}
+__device__ __forceinline__ uint32_t other_end(const DevEvent* ev, uint32_t rec) {
+  const DevEvent& e = ev[rec >> 1];
+  return (rec & 1) ? e.u : e.v;
+}
+
+// A key repeated inside the batch shows up as a repeated neighbour on a
+// G row with several records; its list head checks.
+__global__ void k_fp_check(const DevEvent* __restrict__ ev, uint32_t n, BatchDev b) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || batch_aborted(b.ctl) || b.ctl->not_simple) return;
+  const uint32_t row = rec_row(ev, r);
+  const uint32_t* next = b.fp_next[0];
+  if (b.fp_head[0][row] != r || next[r] == kNoSlot) return;
+  for (uint32_t x = r; x != kNoSlot; x = next[x])
+    for (uint32_t y = next[x]; y != kNoSlot; y = next[y])
+      if (other_end(ev, x) == other_end(ev, y)) b.ctl->not_simple = 1;
+}
+
+// Record r's row on one graph: the list head appends the row's records --
+// itself alone, or all of them in increasing r by repeated minimum selection
+// over the short list -- and empties the list head.
+template <int C>
+__device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* ev, uint32_t* head,
+                                         const uint32_t* next, uint32_t r, bool write) {
+  const uint32_t row = rec_row(ev, r);
+  // The row's slab is needed by the head's append: request it alongside the
+  // list lookups.
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(g.slab + row));
+  const uint32_t h = head[row];
+  const uint32_t nx = next[r];
+  if (h != r) return true;
+  bool ok = true;
+  if (write) {
+    if (nx == kNoSlot) {
+      ok = row_push(g, row, other_end(ev, r), ev[r >> 1].weight);
+    } else {
+      uint32_t last = 0;
+      for (bool first = true; ok; first = false) {
+        uint32_t best = kNoSlot;
+        for (uint32_t x = r; x != kNoSlot; x = next[x])
+          if ((first || x > last) && x < best) best = x;
+        if (best == kNoSlot) break;
+        ok = row_push(g, row, other_end(ev, best), ev[best >> 1].weight);
+        last = best;
+      }
+    }
+  }
+  head[row] = kNoSlot;
+  return ok;
+}
+
+// Batch epilogue: fast-path report, |E| and pool tops for the host, and the
+// device abort flag that stops the later batches of a range after an error.
+__device__ void batch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H,
+                             const BatchDev& b) {
+  BatchCtl* ctl = b.ctl;
+  if (ctl->fast && !ctl->not_simple && ctl->val_err == ~0ull) {
+    for (int f = 0; f < kReportFields; ++f) ctl->report[f] = ctl->fp_report[f];
+    G.edges[0] += ctl->fp_report[kInsSeen];
+    H.edges[0] += ctl->fp_report[kInsKept];
+  }
+  if (ctl->val_err != ~0ull || ctl->commit_err != ~0ull ||
+      (ctl->use_absent_limit && ctl->first_absent != 0xFFFFFFFFu))
+    *b.abort_flag = 1;
+  ctl->g_pool_top = *G.pool_top;
+  ctl->g_edges = *G.edges;
+  ctl->h_pool_top = *H.pool_top;
+  ctl->h_edges = *H.edges;
+}
+
+// Undo the in-place walk shadow (rows saved by k_sh_apply / k_save_rows).
+__device__ void restore_rows(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t tid,
+                             uint32_t nth) {
+  const uint32_t n = b.ctl->n_saved;
+  for (uint32_t idx = tid; idx < n; idx += nth) {
+    const uint32_t row = b.saved_rows[idx];
+    const Slab<kCapG> sl = b.side_slab[idx];
+    G.slab[row] = sl;
+    if (sl.ext != kInline) {
+      const unsigned long long off = b.side_off[idx];
+      for (uint32_t i = 0; i < sl.deg; ++i) {
+        G.pool_id[sl.ext + i] = b.side_id[off + i];
+        G.pool_w[sl.ext + i] = b.side_w[off + i];
+      }
+    }
+  }
+}
+
+// One thread per (record, graph): t = 2 r + (0: G, 1: H).
+__global__ void k_fp_write(DevGraph<kCapG> G, DevGraph<kCapH> H, const DevEvent* __restrict__ ev,
+                           uint32_t n, BatchDev b) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t r = t >> 1;
+  if (r >= n || batch_aborted(b.ctl)) return;
+  const bool write = !b.ctl->not_simple;
+  bool ok;
+  if ((t & 1) == 0) {
+    ok = fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write);
+  } else {
+    if (!b.fp_kept[r >> 1]) return;
+    ok = fp_apply(H, ev, b.fp_head[1], b.fp_next[1], r, write);
+  }
+  if (!ok) atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
+}
+
 // The round engine. Op provides for_rows(k, f) (every row event k reads or
-// writes, possibly with repeats) and apply(k, acc) -> error code.
+// writes, possibly with repeats) and apply(k, acc) -> error code. For the
+// commit (Op::kCommit) the launch also runs the batch epilogue; a batch the
+// insertion fast path committed goes straight to it.
 template <class Op>
 __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b) {
   cg::grid_group grid = cg::this_grid();
   const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
   const uint32_t nth = static_cast<uint32_t>(grid.size());
   volatile BatchCtl* ctl = b.ctl;
-  if (ctl->val_err != ~0ull) return;  // uniform: nothing below ran yet
-  if (ctl->fast && !ctl->not_simple) return;  // the insertion fast path committed it
+  if (ctl->val_err != ~0ull) {  // uniform: nothing below ran yet
+    if constexpr (Op::kCommit) {
+      if (tid == 0) batch_finish(op.G, op.H, b);
+    }
+    return;
+  }
+  if constexpr (Op::kCommit) {
+    if (ctl->fast && !ctl->not_simple) {  // k_fp_write committed the batch
+      if (tid == 0) batch_finish(op.G, op.H, b);
+      return;
+    }
+  }
   Acc acc{};
   unsigned long long round = *b.round_ctr;
   uint32_t r = 0;
@@ -129,22 +305,25 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
     *b.round_ctr = round;
     ctl->rounds = ctl->rounds + r + 1;
   }
+  if constexpr (Op::kCommit) {
+    grid.sync();
+    if (tid == 0) batch_finish(op.G, op.H, b);
+  }
 }
 
-// Warp-per-event variant for batches with deletions: the lanes of a warp
+// Warp-per-event rounds for batches with deletions: the lanes of a warp
 // reserve an event's rows (path vertices) in parallel and apply it together
 // (path recovery is parallel over path edges, CommitOp::apply_warp). Same
-// round protocol as k_rounds.
+// round protocol as k_rounds. Shared by k_rounds_warp (mixed batches) and
+// k_del_flow (its fallback when the record buffer overflows).
 template <class Op>
-__global__ void __launch_bounds__(256) k_rounds_warp(Op op, uint32_t nev, BatchDev b) {
-  cg::grid_group grid = cg::this_grid();
+__device__ void rounds_warp_loop(const Op& op, uint32_t nev, const BatchDev& b,
+                                 cg::grid_group& grid) {
   const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
   const uint32_t lane = tid & 31;
   const uint32_t wid = tid >> 5;
   const uint32_t nw = static_cast<uint32_t>(grid.size()) >> 5;
   volatile BatchCtl* ctl = b.ctl;
-  if (ctl->val_err != ~0ull) return;
-  if (ctl->flow_done) return;  // k_del_flow committed the batch
   Acc acc{};
   unsigned long long round = *b.round_ctr;
   uint32_t r = 0;
@@ -188,11 +367,28 @@ __global__ void __launch_bounds__(256) k_rounds_warp(Op op, uint32_t nev, BatchD
   }
 }
 
+// Commit of a batch with deletions by rounds: undo the walk shadow, the
+// rounds, the epilogue -- one cooperative launch.
+template <class Op>
+__global__ void __launch_bounds__(256) k_rounds_warp(Op op, uint32_t nev, BatchDev b) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
+  volatile BatchCtl* ctl = b.ctl;
+  if (ctl->val_err == ~0ull) {
+    restore_rows(op.G, b, tid, static_cast<uint32_t>(grid.size()));
+    grid.sync();
+    rounds_warp_loop(op, nev, b, grid);
+    grid.sync();
+  }
+  if (tid == 0) batch_finish(op.G, op.H, b);
+}
+
 // Walk shadow (sparsifier.cpp:416-423): apply the batch's deletions to the
 // copy of G in event order, skipping absent edges. first_absent records the
 // lowest deletion that found no edge: in a deletion-only batch that is
 // exactly the first event whose graph_.delete_edge throws (:491).
 struct ShadowOp {
+  static constexpr bool kCommit = false;
   DevGraph<kCapG> S;
   const DevEvent* ev;
   BatchCtl* ctl;
@@ -255,6 +451,7 @@ __device__ __forceinline__ uint32_t best_neighbor(const DevGraph<kCapG>& g, uint
 
 // The sequential commit of sparsifier.cpp:466-533, one event per apply().
 struct CommitOp {
+  static constexpr bool kCommit = true;
   DevGraph<kCapG> G;
   DevGraph<kCapH> H;
   const DevEvent* ev;
@@ -617,7 +814,13 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   const uint32_t wid = tid >> 5;
   const uint32_t nw = nth >> 5;
   volatile BatchCtl* ctl = b.ctl;
-  if (ctl->val_err != ~0ull) return;  // uniform
+  if (ctl->val_err != ~0ull) {  // uniform
+    if (tid == 0) batch_finish(op.G, op.H, b);
+    return;
+  }
+  // Undo the in-place walk shadow before anything reads G.
+  restore_rows(op.G, b, tid, nth);
+  grid.sync();
   const uint32_t lim = min(nev, op.limit());
   uint32_t* head = b.fp_head[0];
   uint32_t* done = b.fp_cnt[0];
@@ -782,9 +985,16 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   }
   grid.sync();
   if (tid == 0) ctl->fl_t[5] = global_ns();
-  if (tid == 0 && !overflow) {
-    ctl->flow_done = 1;
-    ctl->rounds = ctl->rounds + 1;
+  if (overflow) {  // record buffer too small: the dependency rounds commit the batch
+    rounds_warp_loop(op, nev, b, grid);
+    grid.sync();
+  }
+  if (tid == 0) {
+    if (!overflow) {
+      ctl->flow_done = 1;
+      ctl->rounds = ctl->rounds + 1;
+    }
+    batch_finish(op.G, op.H, b);
   }
 }
 
@@ -837,6 +1047,7 @@ __global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t
   const uint32_t mi = static_cast<uint32_t>(x >> 32);
   const DevEvent e = ev[k];
   const uint64_t uid = counter + k;  // update_id = update_counter_ + k (:431)
+  if (k == 0) *b.work = 0;           // the walk's work counter
   uint32_t s = kNoSlot;
   if (f & 0xFFFFFFFFull) {
     ReachQuery q;
@@ -845,6 +1056,11 @@ __global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t
     q.w_pq = b.wpq[k];
     q.qseed = query_seed(seed, uid);
     b.rq[ri] = q;
+    // The reach walk's order-free reductions start from here (reached = OR,
+    // steps = SUM, best = MIN).
+    b.rout.reached[ri] = 0;
+    b.rout.steps[ri] = 0;
+    b.rout.best_bits[ri] = 0x7FF0000000000000ull;
     s = ri;
   } else if (f >> 32) {
     MinQuery q;
@@ -951,165 +1167,8 @@ __global__ void k_sh_apply(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, u
   head[row] = kNoSlot;
 }
 
-__global__ void k_restore_rows(DevGraph<kCapG> G, BatchDev b) {
-  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= b.ctl->n_saved) return;
-  const uint32_t row = b.saved_rows[idx];
-  const Slab<kCapG> sl = b.side_slab[idx];
-  G.slab[row] = sl;
-  if (sl.ext != kInline) {
-    const unsigned long long off = b.side_off[idx];
-    for (uint32_t i = 0; i < sl.deg; ++i) {
-      G.pool_id[sl.ext + i] = b.side_id[off + i];
-      G.pool_w[sl.ext + i] = b.side_w[off + i];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
-// Insertion fast path. In an insertion-only batch where every key is new to
-// G (k_flags_ins) and no key repeats within the batch (k_fp_check), event k's
-// whole commit (:473-488 with :220-241) is: push_back(u: v, w) and
-// push_back(v: u, w) into G, and -- when kept -- the same two appends into H
-// with weight G.w(u,v) = w. H lacks the key because H is a subgraph of G.
-// Rows only receive appends, in event order. Each append record r = 2k +
-// side (row u or v of event k) is pushed onto its row's lock-free list
-// (k_fp_link, one atomic exchange per record). The list head owns the row:
-// a sole record (the vast majority) appends directly, a head with followers
-// applies the row's records in increasing r, i.e. event order (k_fp_write,
-// one thread per record and graph). Any violated precondition sets
-// not_simple BEFORE anything is written (k_fp_check) and the round engine
-// (k_rounds) commits the batch instead. The list heads are left empty for
-// the next batch.
-__global__ void k_fp_link(const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
-  unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
-  if (live) {
-    const DevEvent e = ev[k];
-    const uint32_t s = b.slot[k];
-    bool have = false, reached = false;
-    if (s != kNoSlot) {
-      have = true;
-      reached = b.rout.reached[s] != 0;
-      steps = b.rout.steps[s];
-    }
-    const bool kept = !o.freeze && !(o.K != 0.0 && have && reached);
-    const uint32_t gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
-    const uint32_t gv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
-    b.fp_next[0][2 * k] = gu;
-    b.fp_next[0][2 * k + 1] = gv;
-    if (kept) {
-      const uint32_t hu = atomicExch(b.fp_head[1] + e.u, 2 * k);
-      const uint32_t hv = atomicExch(b.fp_head[1] + e.v, 2 * k + 1);
-      b.fp_next[1][2 * k] = hu;
-      b.fp_next[1][2 * k + 1] = hv;
-    }
-    b.fp_kept[k] = kept ? 1 : 0;
-    b.dec[k] = kept ? 0u : 1u;
-    (kept ? kept_n : pruned_n) = 1;
-  }
-  kept_n = warp_sum(kept_n);
-  pruned_n = warp_sum(pruned_n);
-  const unsigned long long steps_sum = warp_sum(steps);
-  const unsigned long long steps_max = warp_max(steps);
-  if ((threadIdx.x & 31) == 0 && (kept_n | pruned_n)) {
-    atomicAdd(&b.ctl->fp_report[kInsSeen], kept_n + pruned_n);
-    atomicAdd(&b.ctl->fp_report[kInsKept], kept_n);
-    atomicAdd(&b.ctl->fp_report[kInsPruned], pruned_n);
-    atomicAdd(&b.ctl->fp_report[kWalkerSteps], steps_sum);
-    atomicMax(&b.ctl->fp_report[kMaxEventSteps], steps_max);
-  }
-}
-
-__device__ __forceinline__ uint32_t rec_row(const DevEvent* ev, uint32_t rec) {
-  const DevEvent& e = ev[rec >> 1];
-  return (rec & 1) ? e.v : e.u;
-}
-__device__ __forceinline__ uint32_t other_end(const DevEvent* ev, uint32_t rec) {
-  const DevEvent& e = ev[rec >> 1];
-  return (rec & 1) ? e.u : e.v;
-}
-
-// A key repeated inside the batch shows up as a repeated neighbour on a
-// G row with several records; its list head checks.
-__global__ void k_fp_check(const DevEvent* __restrict__ ev, uint32_t n, BatchDev b) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n || batch_aborted(b.ctl) || b.ctl->not_simple) return;
-  const uint32_t row = rec_row(ev, r);
-  const uint32_t* next = b.fp_next[0];
-  if (b.fp_head[0][row] != r || next[r] == kNoSlot) return;
-  for (uint32_t x = r; x != kNoSlot; x = next[x])
-    for (uint32_t y = next[x]; y != kNoSlot; y = next[y])
-      if (other_end(ev, x) == other_end(ev, y)) b.ctl->not_simple = 1;
-}
-
-// Record r's row on one graph: the list head appends the row's records --
-// itself alone, or all of them in increasing r by repeated minimum selection
-// over the short list -- and empties the list head.
-template <int C>
-__device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* ev, uint32_t* head,
-                                         const uint32_t* next, uint32_t r, bool write) {
-  const uint32_t row = rec_row(ev, r);
-  // The row's slab is needed by the head's append: request it alongside the
-  // list lookups.
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(g.slab + row));
-  const uint32_t h = head[row];
-  const uint32_t nx = next[r];
-  if (h != r) return true;
-  bool ok = true;
-  if (write) {
-    if (nx == kNoSlot) {
-      ok = row_push(g, row, other_end(ev, r), ev[r >> 1].weight);
-    } else {
-      uint32_t last = 0;
-      for (bool first = true; ok; first = false) {
-        uint32_t best = kNoSlot;
-        for (uint32_t x = r; x != kNoSlot; x = next[x])
-          if ((first || x > last) && x < best) best = x;
-        if (best == kNoSlot) break;
-        ok = row_push(g, row, other_end(ev, best), ev[best >> 1].weight);
-        last = best;
-      }
-    }
-  }
-  head[row] = kNoSlot;
-  return ok;
-}
-
-// One thread per (record, graph): t = 2 r + (0: G, 1: H).
-__global__ void k_fp_write(DevGraph<kCapG> G, DevGraph<kCapH> H, const DevEvent* __restrict__ ev,
-                           uint32_t n, BatchDev b) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t r = t >> 1;
-  if (r >= n || batch_aborted(b.ctl)) return;
-  const bool write = !b.ctl->not_simple;
-  bool ok;
-  if ((t & 1) == 0) {
-    ok = fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write);
-  } else {
-    if (!b.fp_kept[r >> 1]) return;
-    ok = fp_apply(H, ev, b.fp_head[1], b.fp_next[1], r, write);
-  }
-  if (!ok) atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
-}
-
-__global__ void k_finish(unsigned long long* g_cnt, unsigned long long* h_cnt, BatchCtl* ctl,
-                         unsigned int* abort_flag) {
-  if (ctl->fast && !ctl->not_simple && ctl->val_err == ~0ull) {
-    for (int f = 0; f < kReportFields; ++f) ctl->report[f] = ctl->fp_report[f];
-    g_cnt[1] += ctl->fp_report[kInsSeen];
-    h_cnt[1] += ctl->fp_report[kInsKept];
-  }
-  if (ctl->val_err != ~0ull || ctl->commit_err != ~0ull ||
-      (ctl->use_absent_limit && ctl->first_absent != 0xFFFFFFFFu))
-    *abort_flag = 1;
-  ctl->g_pool_top = g_cnt[0];
-  ctl->g_edges = g_cnt[1];
-  ctl->h_pool_top = h_cnt[0];
-  ctl->h_edges = h_cnt[1];
-}
-
 unsigned grid_for(uint64_t n, unsigned bs = 256) {
   return static_cast<unsigned>((n + bs - 1) / bs);
 }
@@ -1366,11 +1425,6 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   return l + 2;
 }
 
-int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st) {
-  k_restore_rows<<<grid_for(2ull * nb), 256, 0, st>>>(G, b);
-  return 1;
-}
-
 // DYG_COMMIT_ROUNDS=1 forces the dependency-round engine for deletion-only
 // batches (A/B and testing knob).
 bool flow_enabled() {
@@ -1384,12 +1438,7 @@ bool flow_enabled() {
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st) {
   CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.mscratch, b.dec, b.ctl, o};
-  static const int skip = [] {  // MEASUREMENT ONLY: skip the fallback launch
-    const char* e = std::getenv("DYG_SKIP_FALLBACK");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (n_del == 0) return skip ? 0 : launch_rounds<false>(op, nb, b, st);
-  int l = 0;
+  if (n_del == 0) return launch_rounds<false>(op, nb, b, st);
   if (n_del == nb && flow_enabled()) {
     CommitOp op_copy = op;
     BatchDev b_copy = b;
@@ -1400,10 +1449,9 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
     cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_del_flow),
                                            dim3(need < cap ? need : cap), dim3(256), args, 0, st),
                "cooperative flow launch");
-    ++l;
-    if (skip) return l;
+    return 1;
   }
-  return l + launch_rounds<true>(op, nb, b, st);
+  return launch_rounds<true>(op, nb, b, st);
 }
 
 int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
@@ -1450,10 +1498,6 @@ int launch_unpack(const BatchDev& b, uint32_t nq_r, uint32_t nq_m, int world, ui
   return l;
 }
 
-int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  unsigned int* abort_flag, cudaStream_t st) {
-  k_finish<<<1, 1, 0, st>>>(G.pool_top, H.pool_top, b.ctl, abort_flag);
-  return 1;
-}
+
 
 }  // namespace dyg

@@ -9,7 +9,8 @@
 //   CommitOp rounds   the sequential commit (sparsifier.cpp:466-533)
 //                     incl. commit_insertion / set_edge_weight
 //                     (:207-241) and run_local_fallback (:264-280)  [K6-K8]
-//   k_finish          BatchReport counters (sparsifier.hpp:44-59)    [K9]
+//   batch_finish      BatchReport counters (sparsifier.hpp:44-59), run at
+//                     the end of the commit launch                   [K9]
 //
 // The commit engine ("dependency rounds"): every round, each pending event
 // reserves all rows it will read or write (atomicMax of a round-stamped key
@@ -113,7 +114,7 @@ struct BatchDev {
   MinScratch mscratch;
   uint32_t* dec;           // per-event outcome (kind | edges_added << 8)
   double* wpq;             // per-event insertion w_pq (batch-start G)
-  // In-place walk shadow (k_save_rows / k_restore_rows).
+  // In-place walk shadow (k_sh_apply / k_save_rows save, the commit restores).
   uint32_t* mark;          // per-vertex batch stamp
   uint32_t* saved_rows;
   Slab<kCapG>* side_slab;
@@ -125,6 +126,8 @@ struct BatchDev {
   unsigned long long* locks;  // per-vertex row reservations
   unsigned long long* round_ctr;
   BatchCtl* ctl;
+  unsigned int* abort_flag;  // session device abort flag (stops later batches)
+  unsigned int* work;        // walk work counter (reset by k_scatter)
   void* cub_temp;
   size_t cub_temp_bytes;
   // Insertion fast path ([0] = G, [1] = H): per-vertex append counts and
@@ -157,20 +160,20 @@ int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStrea
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st);
 // Query build; with deletions in the batch it also saves the touched G
-// rows and applies the walk shadow to G in place (undo: launch_restore).
+// rows and applies the walk shadow to G in place (undone at the start of
+// the commit launch).
 int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b,
                    uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
                    const WalkOpts& o, int coop_blocks, cudaStream_t st);
-int launch_restore(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st);
 // Insertion-only batches: sort-based append commit (ctl.fast must be set);
 // k_rounds then only runs if a precondition failed on the device.
 int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                            uint32_t nb, const WalkOpts& o, cudaStream_t st);
-// n_del > 0 selects the warp-per-event round engine (parallel path recovery).
+// The whole commit in one cooperative launch, epilogue included: insertion
+// batches k_rounds (fast-path appends, or rounds), deletion-only batches
+// k_del_flow (shadow undo + dataflow commit), mixed batches k_rounds_warp.
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st);
-int launch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  unsigned int* abort_flag, cudaStream_t st);
 size_t scan_temp_bytes(uint32_t nb_cap);
 
 // Multi-GPU exchange records. Reach: 16 B per query.

@@ -422,6 +422,8 @@ void phase_prepare(dyg_session* s, Pending& p) {
   b.events = const_cast<DevEvent*>(p.dev);
   b.locks = s->d_locks;
   b.round_ctr = s->d_round;
+  b.abort_flag = s->d_abort;
+  b.work = s->d_work;
   const uint32_t use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
   const uint32_t fast = (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath) ? 1u : 0u;
   b.side_top = &b.ctl->side_top;
@@ -466,7 +468,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
     p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
-                               s->d_work, s->stream);
+                               s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
   record(s, p.tm[1].b);
@@ -477,27 +479,28 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     const uint64_t T1 = static_cast<uint64_t>(o.T) + 1;
     MinOut mo{b.mout.has_path + lo_m, b.mout.path_len + lo_m, b.mout.steps + lo_m,
               b.mout.resistance + lo_m, b.mout.paths + lo_m * T1};
+    // k_scatter reset the work counter; a mixed batch's reach walk used it,
+    // and a shard range walk may follow another range's walk.
+    const bool reset = !full || (p.n_ins > 0 && o.filtering);
     p.launches += launch_minpath(s->G.view(), b.mq + lo_m, cnt_m, max_m, Pd, b.mscratch, mo,
-                                 &b.ctl->minpath, s->d_work, s->stream);
+                                 &b.ctl->minpath, s->d_work, s->stream, reset);
     maybe_sync(s, "minpath walks");
   }
   record(s, p.tm[2].b);
 }
 
-// Commit (:466-533) enqueue: restore the shadowed rows, run the commit
-// engine, snapshot the counters and copy the control block back (async).
+// Commit (:466-533) enqueue: the commit launch (shadow undo, commit engine,
+// epilogue) and the async copy of the control block back.
 void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
   record(s, p.tm[3].a);
-  if (p.n_del > 0) p.launches += launch_restore(s->G.view(), b, p.nb, s->stream);
   if (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath)
     p.launches += launch_insert_fastpath(s->G.view(), s->H.view(), b, p.nb, o, s->stream);
   p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
   maybe_sync(s, "commit");
   record(s, p.tm[3].b);
-  p.launches += launch_finish(s->G.view(), s->H.view(), b, s->d_abort, s->stream);
   record(s, p.tm[0].b);
   if (download)
     check(cudaMemcpyAsync(p.hctl, b.ctl, sizeof(BatchCtl), cudaMemcpyDeviceToHost, s->stream),

@@ -541,10 +541,14 @@ int walk_variant(const char* env, int dflt) {
 template <int C>
 int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
                  uint32_t nq_max, const WalkParams& P, ReachOut out, WalkCounters* ctr,
-                 unsigned int* work, cudaStream_t st) {
+                 unsigned int* work, cudaStream_t st, bool standalone) {
   if (nq_max == 0) return 0;
+  int l = 1;
   static const int v = walk_variant("DYG_WALK_REACH", 0);
-  k_reach_init<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_max, work);
+  if (standalone) {
+    k_reach_init<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_max, work);
+    ++l;
+  }
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
   switch (v) {
     case 0: launch_walk<C, false, 1, 8, 3>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
@@ -553,8 +557,11 @@ int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_d
     case 4: launch_walk<C, false, 3, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
     default: launch_walk<C, false, 2, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
   }
-  k_reach_fix<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_dev);
-  return 3;
+  if (standalone) {
+    k_reach_fix<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_dev);
+    ++l;
+  }
+  return l;
 }
 
 __global__ void k_zero(unsigned int* work) { *work = 0; }
@@ -562,11 +569,15 @@ __global__ void k_zero(unsigned int* work) { *work = 0; }
 template <int C>
 int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_dev,
                    uint32_t nq_max, const WalkParams& P, MinScratch scratch, MinOut out,
-                   WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
+                   WalkCounters* ctr, unsigned int* work, cudaStream_t st, bool reset_work) {
   if (nq_max == 0) return 0;
+  int l = 2;
   static const int v = walk_variant("DYG_WALK_MIN", 0);
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
-  k_zero<<<1, 1, 0, st>>>(work);
+  if (reset_work) {
+    k_zero<<<1, 1, 0, st>>>(work);
+    ++l;
+  }
   switch (v) {
     case 0: launch_walk<C, true, 1, 8, 2>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
     case 2: launch_walk<C, true, 2, 4, 4>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
@@ -574,15 +585,15 @@ int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_d
   }
   k_minpath_finish<C><<<blocks_for(static_cast<uint64_t>(nq_max) * 32, 256), 256, 0, st>>>(
       g, nq_dev, P, scratch, out);
-  return 3;
+  return l;
 }
 
 template int launch_reach<kCapH>(const DevGraph<kCapH>&, const ReachQuery*, const uint32_t*,
                                  uint32_t, const WalkParams&, ReachOut, WalkCounters*,
-                                 unsigned int*, cudaStream_t);
+                                 unsigned int*, cudaStream_t, bool);
 template int launch_minpath<kCapG>(const DevGraph<kCapG>&, const MinQuery*, const uint32_t*,
                                    uint32_t, const WalkParams&, MinScratch, MinOut,
-                                   WalkCounters*, unsigned int*, cudaStream_t);
+                                   WalkCounters*, unsigned int*, cudaStream_t, bool);
 
 
 }  // namespace dyg

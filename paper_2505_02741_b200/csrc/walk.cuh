@@ -91,15 +91,19 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 // Host launchers (walk.cu). nq_dev: device count of queries (nq_max bounds
-// the launch); work: a device u32 work counter (reset by the launcher).
+// the launch); work: a device u32 work counter. Standalone (run_batch) the
+// launchers reset it and initialise / finalise the reach outputs; inside a
+// session batch k_scatter does both and best_estimate is not needed.
 // stream: session stream. Each returns the number of kernels launched.
 template <int C>
 int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
                  uint32_t nq_max, const WalkParams& P, ReachOut out,
-                 WalkCounters* ctr, unsigned int* work, cudaStream_t st);
+                 WalkCounters* ctr, unsigned int* work, cudaStream_t st,
+                 bool standalone = true);
 template <int C>
 int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_dev,
                    uint32_t nq_max, const WalkParams& P, MinScratch scratch, MinOut out,
-                   WalkCounters* ctr, unsigned int* work, cudaStream_t st);
+                   WalkCounters* ctr, unsigned int* work, cudaStream_t st,
+                   bool reset_work = true);
 
 }  // namespace dyg

@@ -16,7 +16,7 @@ import json,sys
 try:
     d=json.load(open(sys.argv[2]))
     p=d["phases_ms_per_step"]; r=d["roofline"]
-    print(f"[{sys.argv[1] or 'default'}] ms/step={d['ms_per_step']:.3f} dev={d['device_ms_per_step']:.3f} value={d['value']/1e6:.1f}M e2e={d['e2e']['value']/1e6:.1f}M frac={r['frac']:.3f} " + " ".join(f"{k.split()[0]}={v:.3f}" for k,v in p.items()) + f" delcommit={d['commit_ms_per_step_deletion_batches']:.3f} rounds={d['commit_rounds_per_step']} tail={d['walk_tail_ms_per_step']}")
+    print(f"[{sys.argv[1] or 'default'}] ms/step={d['ms_per_step']:.3f} dev={d['device_ms_per_step']:.3f} restore={d.get('restore_ms_per_step',0):.3f} value={d['value']/1e6:.1f}M e2e={d['e2e']['value']/1e6:.1f}M frac={r['frac']:.3f} " + " ".join(f"{k.split()[0]}={v:.3f}" for k,v in p.items()) + f" delcommit={d['commit_ms_per_step_deletion_batches']:.3f} rounds={d['commit_rounds_per_step']} tail={d['walk_tail_ms_per_step']}")
 except Exception as e:
     print("run", sys.argv[1], "failed", e)
 PY
