@@ -436,6 +436,9 @@ def run_ours(args):
             "traffic": load_traffic(walk_key.split(" ")[0]),
             "algorithmic_bytes_per_launch": wbytes / max(1, stats["batches"] // 2),
             "avg_launch_ms": wms / max(1, stats["batches"] // 2),
+            "duration_source": "kernel-written %globaltimer stamps (first warp start to last "
+                               "warp exit), summed over the timed steps; the step itself is "
+                               "CUDA-event timed",
             "dominant_phase": dom,
         },
         "gather_roofline": gather_block(stats, g.vertex_count()),

@@ -51,6 +51,11 @@ struct Acc {
   long long dg, dh;
 };
 
+// Commit start stamp (first block of the first commit kernel wins).
+__device__ __forceinline__ void stamp_commit_start(BatchCtl* ctl) {
+  if (threadIdx.x == 0) atomicMin(&ctl->t_commit0, global_ns());
+}
+
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, off);
@@ -97,6 +102,7 @@ __device__ __forceinline__ void flush_acc(const Acc& a, BatchCtl* ctl, unsigned 
 // the next batch.
 __global__ void k_fp_link(const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  stamp_commit_start(b.ctl);
   const bool live = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
   unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
   if (live) {
@@ -208,7 +214,9 @@ __device__ void batch_finish(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H,
   ctl->g_edges = *G.edges;
   ctl->h_pool_top = *H.pool_top;
   ctl->h_edges = *H.edges;
+  ctl->t_batch1 = global_ns();
 }
+
 
 // Undo the in-place walk shadow (rows saved by k_sh_apply / k_save_rows).
 __device__ void restore_rows(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t tid,
@@ -255,6 +263,7 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
   const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
   const uint32_t nth = static_cast<uint32_t>(grid.size());
   volatile BatchCtl* ctl = b.ctl;
+  if constexpr (Op::kCommit) stamp_commit_start(b.ctl);
   if (ctl->val_err != ~0ull) {  // uniform: nothing below ran yet
     if constexpr (Op::kCommit) {
       if (tid == 0) batch_finish(op.G, op.H, b);
@@ -374,6 +383,7 @@ __global__ void __launch_bounds__(256) k_rounds_warp(Op op, uint32_t nev, BatchD
   cg::grid_group grid = cg::this_grid();
   const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
   volatile BatchCtl* ctl = b.ctl;
+  stamp_commit_start(b.ctl);
   if (ctl->val_err == ~0ull) {
     restore_rows(op.G, b, tid, static_cast<uint32_t>(grid.size()));
     grid.sync();
@@ -814,6 +824,7 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   const uint32_t wid = tid >> 5;
   const uint32_t nw = nth >> 5;
   volatile BatchCtl* ctl = b.ctl;
+  stamp_commit_start(b.ctl);
   if (ctl->val_err != ~0ull) {  // uniform
     if (tid == 0) batch_finish(op.G, op.H, b);
     return;
@@ -1323,6 +1334,8 @@ __global__ void k_ctl_init(CtlInitArgs a) {
     ctl->reach.t_start = ctl->reach.t_drain = ctl->minpath.t_start = ctl->minpath.t_drain = ~0ull;
     ctl->fast = a.fast;
     ctl->counter_base = a.counter_base;
+    ctl->t_commit0 = ~0ull;
+    ctl->t_batch0 = global_ns();
   }
 }
 

@@ -79,6 +79,11 @@ struct BatchCtl {
   unsigned int fl_depth;     // longest chain of row-sharing events
   unsigned long long fl_t[6];  // %globaltimer at the phase boundaries
   unsigned long long counter_base;  // update_counter_ at batch start (:431)
+  // %globaltimer stamps (ns) for the phase times in dyg_stats.
+  unsigned long long t_batch0;   // k_ctl_init
+  unsigned long long t_commit0;  // first commit kernel (min over blocks)
+  unsigned long long t_mp_end;   // k_minpath_finish end (max over blocks)
+  unsigned long long t_batch1;   // batch epilogue
 };
 
 // Arguments of the batch control-block initialisation kernel: the only

@@ -62,30 +62,15 @@ void dev_free(T*& p) {
   p = nullptr;
 }
 
+// Milliseconds between two %globaltimer stamps (0 when a phase did not run).
+double span_ms(unsigned long long a, unsigned long long b) {
+  return (a != ~0ull && a != 0 && b > a) ? (b - a) * 1e-6 : 0.0;
+}
+
 double density_of(uint64_t edges, uint32_t n) {
   return static_cast<double>(edges) / static_cast<double>(n) - 1.0;  // graph.cpp:114-116
 }
 
-struct Timer {
-  cudaEvent_t a = nullptr, b = nullptr;
-  void init() {
-    check(cudaEventCreate(&a), "event");
-    check(cudaEventCreate(&b), "event");
-  }
-  void destroy() {
-    if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
-    a = b = nullptr;
-  }
-  float ms() const {
-    float t = 0.f;
-    if (cudaEventElapsedTime(&t, a, b) != cudaSuccess) {
-      cudaGetLastError();
-      return 0.f;
-    }
-    return t;
-  }
-};
 
 // One instantiated CUDA graph of an enqueue sequence. Its only per-launch
 // input is the update counter, carried by the k_ctl_init nodes.
@@ -161,8 +146,6 @@ struct dyg_session {
   uint64_t shard_counter = 0;
 
   dyg_stats stats{};
-  Timer timers[4];                 // per-batch path: total, reach, minpath, commit
-  std::vector<Timer> range_timers; // batch-range path, 4 per batch
   BatchCtl* d_ctls = nullptr;      // batch-range control blocks
   BatchCtl* h_ctls = nullptr;
   uint32_t ctl_cap = 0;
@@ -188,8 +171,6 @@ struct dyg_session {
 
 namespace {
 
-// Timing events: inside a stream capture they must be external record nodes.
-void record(dyg_session* s, cudaEvent_t e);
 
 void maybe_sync(dyg_session* s, const char* what) {
   if (s->debug_sync) check(cudaStreamSynchronize(s->stream), what);
@@ -377,7 +358,6 @@ struct Pending {
   BatchCtl* dctl = nullptr;   // device control block of this batch
   BatchCtl* hctl = nullptr;   // pinned host copy
   uint32_t* hdec = nullptr;   // pinned: decision of a 1-event batch
-  Timer* tm = nullptr;        // [0] total, [1] reach, [2] minpath, [3] commit
   uint64_t counter_base = 0;  // update_counter at batch start
 };
 
@@ -385,7 +365,6 @@ void bind_pending(dyg_session* s, Pending& p) {
   p.dctl = s->b.ctl;
   p.hctl = s->h_ctl;
   p.hdec = &s->h_counts[2];
-  p.tm = s->timers;
   p.counter_base = s->counter;
 }
 
@@ -431,7 +410,6 @@ void phase_prepare(dyg_session* s, Pending& p) {
   if (p.n_del > 0) ensure_side_pool(s);
   p.launches += launch_ctl_init(CtlInitArgs{b.ctl, p.nb, use_absent_limit, fast, p.counter_base},
                                 s->stream);
-  record(s, p.tm[0].a);
   p.launches += launch_validate(b, p.nb, s->n, s->d_abort, s->stream);
   maybe_sync(s, "validate");
   if (p.n_del > 0 && ++s->stamp == 0) {  // stamps restart: clear the marks
@@ -464,21 +442,18 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     max_r = n_r;
     max_m = n_m;
   }
-  record(s, p.tm[1].a);
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
     p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
                                s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
-  record(s, p.tm[1].b);
-  record(s, p.tm[2].a);
   if (p.n_del > 0 && !o.freeze && max_m > 0) {
     WalkParams Pd = P;
     Pd.K = std::numeric_limits<double>::infinity();  // sparsifier.cpp:458-459
     const uint64_t T1 = static_cast<uint64_t>(o.T) + 1;
     MinOut mo{b.mout.has_path + lo_m, b.mout.path_len + lo_m, b.mout.steps + lo_m,
-              b.mout.resistance + lo_m, b.mout.paths + lo_m * T1};
+              b.mout.resistance + lo_m, b.mout.paths + lo_m * T1, &b.ctl->t_mp_end};
     // k_scatter reset the work counter; a mixed batch's reach walk used it,
     // and a shard range walk may follow another range's walk.
     const bool reset = !full || (p.n_ins > 0 && o.filtering);
@@ -486,7 +461,6 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                                  &b.ctl->minpath, s->d_work, s->stream, reset);
     maybe_sync(s, "minpath walks");
   }
-  record(s, p.tm[2].b);
 }
 
 // Commit (:466-533) enqueue: the commit launch (shadow undo, commit engine,
@@ -495,13 +469,10 @@ void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
-  record(s, p.tm[3].a);
   if (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath)
     p.launches += launch_insert_fastpath(s->G.view(), s->H.view(), b, p.nb, o, s->stream);
   p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
   maybe_sync(s, "commit");
-  record(s, p.tm[3].b);
-  record(s, p.tm[0].b);
   if (download)
     check(cudaMemcpyAsync(p.hctl, b.ctl, sizeof(BatchCtl), cudaMemcpyDeviceToHost, s->stream),
           "ctl download");
@@ -553,13 +524,16 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
     s->stats.flow_ms_reset += (c.fl_t[5] - c.fl_t[4]) * 1e-6;
   }
   if (p.n_del > 0) {
-    s->stats.commit_ms_deletion += p.tm[3].ms();
+    s->stats.commit_ms_deletion += span_ms(c.t_commit0, c.t_batch1);
     s->stats.commit_rounds_deletion += c.rounds;
   }
-  s->stats.reach_ms += p.tm[1].ms();
-  s->stats.minpath_ms += p.tm[2].ms();
-  s->stats.commit_ms += p.tm[3].ms();
-  s->stats.total_ms += p.tm[0].ms();
+  // Phase times from %globaltimer stamps the kernels write into the control
+  // block (CUDA events between the phases cost ~4 us each in the stream:
+  // 8 per batch were 0.67 ms of a 10 ms C5 step).
+  s->stats.reach_ms += span_ms(c.reach.t_start, c.reach.t_end);
+  s->stats.minpath_ms += span_ms(c.minpath.t_start, c.t_mp_end);
+  s->stats.commit_ms += span_ms(c.t_commit0, c.t_batch1);
+  s->stats.total_ms += span_ms(c.t_batch0, c.t_batch1);
   if (fail_k != ~0ull) {
     s->counter = p.counter_base + fail_k + 1;  // ++update_counter_ precedes the throw (:469)
     const uint64_t pos = p.pos ? p.pos[fail_k] : p.pos_base + fail_k;
@@ -605,12 +579,6 @@ void reset_abort(dyg_session* s) {
   check(cudaMemsetAsync(s->d_abort, 0, sizeof(unsigned int), s->stream), "abort flag");
 }
 
-void record(dyg_session* s, cudaEvent_t e) {
-  if (s->capturing)
-    check(cudaEventRecordWithFlags(e, s->stream, cudaEventRecordExternal), "event");
-  else
-    check(cudaEventRecord(e, s->stream), "event");
-}
 
 // ------------------------------------------------------------ CUDA graphs
 // A batch is ~15 short kernels; launched one by one, the host launch cost
@@ -641,7 +609,7 @@ uint64_t session_fingerprint(dyg_session* s, uint64_t tag) {
   h = fnv(h, &b, sizeof b);
   const WalkOpts o = walk_opts(s);
   h = fnv(h, &o, sizeof o);
-  const void* fixed[] = {s->d_work, s->d_abort, s->d_counts, s->timers, s->h_ctl};
+  const void* fixed[] = {s->d_work, s->d_abort, s->d_counts, s->h_ctl};
   h = fnv(h, fixed, sizeof fixed);
   const uint32_t flags = (s->no_fastpath ? 1u : 0u) | (shadow_lists_enabled() ? 2u : 0u);
   h = fnv(h, &flags, sizeof flags);
@@ -767,7 +735,7 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
     uint64_t key = session_fingerprint(s, 1);
     const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
                               reinterpret_cast<uint64_t>(p.hctl), reinterpret_cast<uint64_t>(p.hdec),
-                              reinterpret_cast<uint64_t>(p.tm), nb, n_ins, n_del};
+                              nb, n_ins, n_del};
     key = fnv(key, shape, sizeof shape);
     CapturedGraph* g = find_graph(s, key);
     if (g == nullptr) {
@@ -871,10 +839,6 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
           "pinned control blocks");
     s->ctl_cap = count;
   }
-  while (s->range_timers.size() < 4ull * count) {
-    s->range_timers.emplace_back();
-    s->range_timers.back().init();
-  }
   std::vector<Pending> ps(count);
   const uint64_t counter0 = s->counter;
   const auto wall0 = std::chrono::steady_clock::now();
@@ -890,7 +854,6 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
       p.dctl = s->d_ctls + i;
       p.hctl = s->h_ctls + i;
       p.hdec = &s->h_counts[2];
-      p.tm = s->range_timers.data() + 4ull * i;
       p.counter_base = counter;
       if (b >= s->batch_cnt.size() || s->batch_cnt[b] == 0) continue;
       const uint64_t off = s->batch_off[b];
@@ -924,8 +887,7 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
     uint64_t key = session_fingerprint(s, 2);
     const uint64_t shape[] = {first, count, s->stream_gen, reinterpret_cast<uint64_t>(s->d_stream),
                               reinterpret_cast<uint64_t>(s->d_ctls),
-                              reinterpret_cast<uint64_t>(s->h_ctls),
-                              reinterpret_cast<uint64_t>(s->range_timers.data())};
+                              reinterpret_cast<uint64_t>(s->h_ctls)};
     key = fnv(key, shape, sizeof shape);
     g = find_graph(s, key);
     if (g == nullptr) g = capture_graph(s, key, counter0, enqueue);
@@ -988,10 +950,6 @@ void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_
           "pinned control blocks");
     s->ctl_cap = nbatches;
   }
-  while (s->range_timers.size() < 4ull * nbatches) {
-    s->range_timers.emplace_back();
-    s->range_timers.back().init();
-  }
   while (s->ready.size() < nbatches) {
     cudaEvent_t e;
     check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -1025,7 +983,6 @@ void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_
     p.dctl = s->d_ctls + b;
     p.hctl = s->h_ctls + b;
     p.hdec = &s->h_counts[2];
-    p.tm = s->range_timers.data() + 4ull * b;
     p.counter_base = counter;
     p.nb = static_cast<uint32_t>(off[b + 1] - off[b]);
     if (p.nb == 0) continue;
@@ -1212,7 +1169,6 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
             "pinned counts");
       check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctl), sizeof(BatchCtl)), "pinned ctl");
       s->coop_blocks = coop_grid_blocks(device);
-      for (Timer& t : s->timers) t.init();
       dev_alloc(&s->d_abort, 1, "abort flag");
       check(cudaMemset(s->d_abort, 0, sizeof(unsigned int)), "abort flag");
       ensure_batch(s, 1024, 256);
@@ -1266,8 +1222,6 @@ void dyg_session_destroy(dyg_session* s) {
   if (s->h_ctl) cudaFreeHost(s->h_ctl);
   if (s->h_counts) cudaFreeHost(s->h_counts);
   dev_free(s->d_counts);
-  for (Timer& t : s->timers) t.destroy();
-  for (Timer& t : s->range_timers) t.destroy();
   dev_free(s->d_ctls);
   if (s->h_ctls) cudaFreeHost(s->h_ctls);
   dev_free(s->d_abort);

@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
   const uint32_t nq = *nq_dev;
   const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  if (out.t_end && lane == 0) atomicMax(out.t_end, global_ns());
   if (qi >= nq) return;
   const uint64_t base = static_cast<uint64_t>(qi) * P.s;
   unsigned long long st = 0;

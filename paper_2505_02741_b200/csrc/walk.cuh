@@ -63,6 +63,7 @@ struct MinOut {
   unsigned long long* steps;
   double* resistance;
   uint32_t* paths;     // [q*(T+1)] loop-erased vertices
+  unsigned long long* t_end;  // optional: %globaltimer at K3 end (max)
 };
 // Per-walker scratch of the min-path walk.
 struct MinScratch {
