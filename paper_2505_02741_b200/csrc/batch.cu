@@ -1047,6 +1047,194 @@ __global__ void k_flags_del(DevGraph<kCapH> H, DevGraph<kCapG> S,
   b.state[k] = 0;
 }
 
+// ------------------------------------------------- single-pass batch prepare
+// Validation + query flags + the query scan + the query scatter in ONE
+// launch (decoupled look-back scan over 256-event tiles) for insertion-only
+// and deletion-only batches: the separate k_validate / k_flags_* / cub scan
+// (2 kernels) / k_scatter chain costs five launches and their gaps per batch.
+// Same results as that chain: a thread checks its own event's shape before
+// touching the graph, and an invalid batch's queries are never committed
+// (the commit reads val_err), exactly like the aborted chain.
+
+// Shape check of one event (sparsifier.cpp:321-337); 0 when valid.
+__device__ __forceinline__ uint32_t event_code(const DevEvent& e, uint32_t n) {
+  if (e.u >= n || e.v >= n) return kErrRange;
+  if (e.u == e.v) return kErrSelfLoop;
+  if (e.kind == 0 && (!(e.weight > 0.0) || !isfinite(e.weight))) return kErrWeight;
+  return 0;
+}
+
+// Writes the queries of event k given its scan offsets (ri, mi).
+__device__ __forceinline__ void scatter_event(const DevEvent& e, uint32_t k, unsigned long long f,
+                                              uint32_t ri, uint32_t mi, uint64_t seed,
+                                              const BatchDev& b) {
+  const uint64_t uid = b.ctl->counter_base + k;  // update_id = update_counter_ + k (:431)
+  uint32_t s = kNoSlot;
+  if (f & 0xFFFFFFFFull) {
+    ReachQuery q;
+    q.p = e.u;
+    q.q = e.v;
+    q.w_pq = b.wpq[k];
+    q.qseed = query_seed(seed, uid);
+    b.rq[ri] = q;
+    b.rout.reached[ri] = 0;  // the reach walk's OR / SUM / MIN start here
+    b.rout.steps[ri] = 0;
+    b.rout.best_bits[ri] = 0x7FF0000000000000ull;
+    s = ri;
+  } else if (f >> 32) {
+    MinQuery q;
+    q.p = e.u;
+    q.q = e.v;
+    q.qseed = query_seed(seed, uid);
+    b.mq[mi] = q;
+    s = mi;
+  }
+  b.slot[k] = s;
+}
+
+// Exclusive prefix of this tile's aggregate over all earlier tiles, by one
+// warp (decoupled look-back, 32 predecessors per step). Per tile:
+// {aggregate, inclusive prefix, epoch << 2 | state} -- separate words for the
+// two values, so a reader that saw state 1 never reads a value the owner
+// rewrote afterwards.
+__device__ unsigned long long tile_lookback(const BatchDev& b, uint32_t tile,
+                                            unsigned long long agg, uint32_t lane) {
+  constexpr unsigned kAll = 0xFFFFFFFFu;
+  const unsigned long long ep = b.ctl->epoch << 2;
+  volatile unsigned long long* ts = b.tile_state;
+  if (lane == 0) {
+    ts[3ull * tile] = agg;
+    if (tile == 0) ts[3ull * tile + 1] = agg;
+    __threadfence();
+    ts[3ull * tile + 2] = ep | (tile == 0 ? 2ull : 1ull);
+  }
+  if (tile == 0) return 0ull;
+  unsigned long long prefix = 0;
+  int64_t base = static_cast<int64_t>(tile) - 1;
+  for (;;) {
+    const int64_t t = base - static_cast<int64_t>(lane);
+    unsigned long long st = ep | 2ull, v = 0;  // before tile 0: an empty inclusive
+    if (t >= 0) {
+      while (((st = ts[3ull * t + 2]) & ~3ull) != ep || (st & 3ull) == 0) __nanosleep(20);
+      __threadfence();
+      v = (st & 3ull) == 2ull ? ts[3ull * t + 1] : ts[3ull * t];
+    }
+    const unsigned inc = __ballot_sync(kAll, (st & 3ull) == 2ull);
+    const uint32_t stop = inc ? static_cast<uint32_t>(__ffs(inc) - 1) : 31u;
+    unsigned long long part = lane <= stop ? v : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(kAll, part, off);
+    prefix += part;
+    if (inc) break;
+    base -= 32;
+  }
+  if (lane == 0) {
+    ts[3ull * tile + 1] = prefix + agg;
+    __threadfence();
+    ts[3ull * tile + 2] = ep | 2ull;
+  }
+  return prefix;
+}
+
+// kDel = false: insertion-only batch (validate + insertion flags).
+// kDel = true: deletion-only batch after the shadow (deletion flags).
+template <bool kDel>
+__global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG> G,
+                                              const DevEvent* __restrict__ ev, uint32_t nb,
+                                              uint32_t n, WalkOpts o, BatchDev b) {
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_warp[8];
+  __shared__ unsigned long long s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&b.ctl->tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t k = tile * 256 + threadIdx.x;
+  const bool aborted = kDel ? batch_aborted(b.ctl) : (*b.abort_flag != 0);
+  unsigned long long f = 0;
+  DevEvent e{};
+  if (k < nb && !aborted) {
+    e = ev[k];
+    if constexpr (!kDel) {
+      const uint32_t code = event_code(e, n);
+      if (code) {
+        atomicMin(&b.ctl->val_err, (static_cast<unsigned long long>(k) << 8) | code);
+      } else if (e.kind == 0) {
+        const double gw = edge_weight(G, e.u, e.v);
+        if (gw != 0.0) b.ctl->not_simple = 1;  // fast-path precondition: new key
+        if (o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) {
+          f = 1ull;
+          b.wpq[k] = __dadd_rn(gw, e.weight);
+        }
+      }
+      b.dec[k] = 0;
+    } else {
+      if (e.kind == 1 && !o.freeze && has_edge(H, e.u, e.v) && G.slab[e.u].deg > 0 &&
+          G.slab[e.v].deg > 0)
+        f = 1ull << 32;
+    }
+    b.state[k] = 0;
+  }
+  if (!kDel && k == 0 && *b.abort_flag)
+    atomicMin(&b.ctl->val_err, static_cast<unsigned long long>(kErrAborted));
+  if (k == 0) *b.work = 0;  // the walk's work counter
+  // Block exclusive scan of f (reach count in the low half, min-path high).
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long x = f;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+    if (lane >= static_cast<uint32_t>(off)) x += y;
+  }
+  if (lane == 31) s_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long run = 0;  // warp totals -> exclusive warp offsets
+    if (lane == 0) {
+      for (int w = 0; w < 8; ++w) {
+        const unsigned long long t = s_warp[w];
+        s_warp[w] = run;
+        run += t;
+      }
+    }
+    run = __shfl_sync(0xFFFFFFFFu, run, 0);
+    const unsigned long long pre = tile_lookback(b, tile, run, lane);
+    if (lane == 0) s_prefix = pre;
+  }
+  __syncthreads();
+  const unsigned long long excl = s_prefix + s_warp[wid] + x - f;
+  if (k < nb && !aborted) {
+    scatter_event(e, k, f, static_cast<uint32_t>(excl & 0xFFFFFFFFull),
+                  static_cast<uint32_t>(excl >> 32), o.seed, b);
+    if (k == nb - 1) {
+      b.ctl->nq_reach = static_cast<uint32_t>((excl + f) & 0xFFFFFFFFull);
+      b.ctl->nq_min = static_cast<uint32_t>((excl + f) >> 32);
+    }
+  }
+}
+
+// Deletion-only batch, first launch: validation + the shadow's row lists.
+__global__ void k_val_link(const DevEvent* __restrict__ ev, uint32_t nb, uint32_t n,
+                           BatchDev b) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  if (*b.abort_flag) {  // an earlier batch of this range failed: do nothing
+    if (k == 0) atomicMin(&b.ctl->val_err, static_cast<unsigned long long>(kErrAborted));
+    return;
+  }
+  const DevEvent e = ev[k];
+  const uint32_t code = event_code(e, n);
+  if (code) {
+    atomicMin(&b.ctl->val_err, (static_cast<unsigned long long>(k) << 8) | code);
+    return;
+  }
+  b.dec[k] = 0;
+  if (e.kind != 1) return;
+  const uint32_t hu = atomicExch(b.fp_head[0] + e.u, 2 * k);
+  const uint32_t hv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
+  b.fp_next[0][2 * k] = hu;
+  b.fp_next[0][2 * k + 1] = hv;
+}
+
 __global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t seed,
                           BatchDev b) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1138,14 +1326,18 @@ __global__ void k_sh_link(const DevEvent* __restrict__ ev, uint32_t nb, BatchDev
 }
 
 __global__ void k_sh_apply(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, uint32_t nb,
-                           BatchDev b) {
+                           uint32_t n, BatchDev b) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= 2 * nb || batch_aborted(b.ctl)) return;
+  if (r >= 2 * nb) return;
   const DevEvent& e = ev[r >> 1];
-  if (e.kind != 1) return;
+  if (e.kind != 1 || e.u >= n || e.v >= n || e.u == e.v) return;  // never linked
   const uint32_t row = (r & 1) ? e.v : e.u;
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(G.slab + row));
   uint32_t* head = b.fp_head[0];
+  if (batch_aborted(b.ctl)) {  // linked before validation finished: just clear
+    if (head[row] == r) head[row] = kNoSlot;
+    return;
+  }
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(G.slab + row));
   const uint32_t* next = b.fp_next[0];
   if (head[row] != r) return;
   // Save the row (the owner is its only writer in this pass).
@@ -1336,6 +1528,7 @@ __global__ void k_ctl_init(CtlInitArgs a) {
     ctl->counter_base = a.counter_base;
     ctl->t_commit0 = ~0ull;
     ctl->t_batch0 = global_ns();
+    ctl->epoch = atomicAdd(a.epoch_ctr, 1ull) + 1ull;
   }
 }
 
@@ -1406,6 +1599,34 @@ bool shadow_lists_enabled() {
   return on;
 }
 
+// DYG_SINGLE_PASS=0 selects the multi-kernel prepare chain (A/B knob).
+bool single_pass_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYG_SINGLE_PASS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+int launch_prepare(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b, uint32_t nb,
+                   uint32_t n_del, uint32_t n, uint32_t stamp, const WalkOpts& o,
+                   cudaStream_t st) {
+  if (nb == 0) return 0;
+  const unsigned tiles = grid_for(nb);
+  if (single_pass_enabled() && n_del == 0) {
+    k_prep<false><<<tiles, 256, 0, st>>>(H, G, b.events, nb, n, o, b);
+    return 1;
+  }
+  if (single_pass_enabled() && n_del == nb && shadow_lists_enabled()) {
+    k_val_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, n, b);
+    k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, n, b);
+    k_prep<true><<<tiles, 256, 0, st>>>(H, G, b.events, nb, n, o, b);
+    return 3;
+  }
+  const int l = launch_validate(b, nb, n, b.abort_flag, st);
+  return l + launch_queries(H, G, b, nb, n_del, 0, stamp, o, 0, st);
+}
+
 int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b,
                    uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
                    const WalkOpts& o, int coop_blocks, cudaStream_t st) {
@@ -1416,7 +1637,7 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   if (n_del > 0) {
     if (shadow_lists_enabled()) {
       k_sh_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, b);
-      k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, b);
+      k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, G.n, b);
       l += 2;
     } else {
       k_save_rows<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, stamp, b);

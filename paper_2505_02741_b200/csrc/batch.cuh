@@ -84,12 +84,16 @@ struct BatchCtl {
   unsigned long long t_commit0;  // first commit kernel (min over blocks)
   unsigned long long t_mp_end;   // k_minpath_finish end (max over blocks)
   unsigned long long t_batch1;   // batch epilogue
+  unsigned long long epoch;      // unique per batch (single-pass scan tile states)
+  unsigned int tile_ctr;         // single-pass scan: next tile
+  unsigned int pad_tile;
 };
 
 // Arguments of the batch control-block initialisation kernel: the only
 // per-batch values a captured batch graph has to be re-pointed with.
 struct CtlInitArgs {
   BatchCtl* ctl;
+  unsigned long long* epoch_ctr;  // session counter: one epoch per batch
   uint32_t limit;
   uint32_t use_absent_limit;
   uint32_t fast;
@@ -133,6 +137,9 @@ struct BatchDev {
   BatchCtl* ctl;
   unsigned int* abort_flag;  // session device abort flag (stops later batches)
   unsigned int* work;        // walk work counter (reset by k_scatter)
+  // Single-pass (decoupled look-back) query scan: per 256-event tile,
+  // {aggregate, inclusive, epoch << 2 | state}; state 1 = aggregate, 2 = inclusive.
+  unsigned long long* tile_state;
   void* cub_temp;
   size_t cub_temp_bytes;
   // Insertion fast path ([0] = G, [1] = H): per-vertex append counts and
@@ -164,6 +171,11 @@ bool shadow_lists_enabled();
 int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStream_t st);
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st);
+// Validation + walk shadow + query build: single-pass kernels for
+// insertion-only / deletion-only batches, else the chain below.
+int launch_prepare(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b, uint32_t nb,
+                   uint32_t n_del, uint32_t n, uint32_t stamp, const WalkOpts& o,
+                   cudaStream_t st);
 // Query build; with deletions in the batch it also saves the touched G
 // rows and applies the walk shadow to G in place (undone at the start of
 // the commit launch).

@@ -157,6 +157,7 @@ struct dyg_session {
   bool graphs_on = true;   // DYG_GRAPHS=0 disables; a failed capture disables
   bool capturing = false;
   uint64_t graph_clock = 0;
+  unsigned long long* d_epoch = nullptr;  // batch epochs (single-pass scan tile states)
   uint64_t stream_gen = 0;  // bumped by every dyg_stream_upload
   // dyg_replay_stream: host stream replayed with its upload pipelined.
   cudaStream_t copy_stream = nullptr;
@@ -212,6 +213,7 @@ void free_batch(dyg_session* s) {
   dev_free(b.fl_base);
   dev_free(b.fl_cnt);
   dev_free(b.fl_promo);
+  dev_free(b.tile_state);
   cudaFree(b.cub_temp);
   b.cub_temp = nullptr;
   dev_free(s->d_events);
@@ -253,6 +255,9 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.fl_base, cap, "flow record ranges");
     dev_alloc(&b.fl_cnt, cap, "flow record ranges");
     dev_alloc(&b.fl_promo, cap, "flow fallback flags");
+    dev_alloc(&b.tile_state, 3ull * (cap / 256 + 2), "scan tile states");
+    check(cudaMemset(b.tile_state, 0, sizeof(unsigned long long) * 3ull * (cap / 256 + 2)),
+          "scan tile states");
     s->nb_cap = cap;
     s->nd_cap = 0;
     (void)keep_nd;
@@ -408,17 +413,15 @@ void phase_prepare(dyg_session* s, Pending& p) {
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
   if (p.n_del > 0) ensure_side_pool(s);
-  p.launches += launch_ctl_init(CtlInitArgs{b.ctl, p.nb, use_absent_limit, fast, p.counter_base},
-                                s->stream);
-  p.launches += launch_validate(b, p.nb, s->n, s->d_abort, s->stream);
-  maybe_sync(s, "validate");
-  if (p.n_del > 0 && ++s->stamp == 0) {  // stamps restart: clear the marks
+  p.launches += launch_ctl_init(
+      CtlInitArgs{b.ctl, s->d_epoch, p.nb, use_absent_limit, fast, p.counter_base}, s->stream);
+  if (p.n_del > 0 && !shadow_lists_enabled() && ++s->stamp == 0) {  // stamps restart
     check(cudaMemsetAsync(b.mark, 0, sizeof(uint32_t) * s->n, s->stream), "marks");
     s->stamp = 1;
   }
-  p.launches += launch_queries(s->H.view(), s->G.view(), b, p.nb, p.n_del, p.counter_base,
-                               s->stamp, o, s->coop_blocks, s->stream);
-  maybe_sync(s, "queries + walk shadow");
+  p.launches += launch_prepare(s->H.view(), s->G.view(), b, p.nb, p.n_del, s->n, s->stamp, o,
+                               s->stream);
+  maybe_sync(s, "validate + queries + walk shadow");
 }
 
 // Walks over query ranges. Full range (single GPU): counts stay on the
@@ -1169,6 +1172,8 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
             "pinned counts");
       check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctl), sizeof(BatchCtl)), "pinned ctl");
       s->coop_blocks = coop_grid_blocks(device);
+      dev_alloc(&s->d_epoch, 1, "batch epoch");
+      check(cudaMemset(s->d_epoch, 0, sizeof(unsigned long long)), "batch epoch");
       dev_alloc(&s->d_abort, 1, "abort flag");
       check(cudaMemset(s->d_abort, 0, sizeof(unsigned int)), "abort flag");
       ensure_batch(s, 1024, 256);
@@ -1225,6 +1230,7 @@ void dyg_session_destroy(dyg_session* s) {
   dev_free(s->d_ctls);
   if (s->h_ctls) cudaFreeHost(s->h_ctls);
   dev_free(s->d_abort);
+  dev_free(s->d_epoch);
   s->G.release();
   s->G_snap.release();
   s->H.release();
