@@ -87,61 +87,22 @@ __device__ __forceinline__ void flush_acc(const Acc& a, BatchCtl* ctl, unsigned 
 }
 
 // Insertion fast path. In an insertion-only batch where every key is new to
-// G (k_flags_ins) and no key repeats within the batch (k_fp_check), event k's
-// whole commit (:473-488 with :220-241) is: push_back(u: v, w) and
+// G (checked in k_prep) and no key repeats within the batch (k_fp_check),
+// event k's whole commit (:473-488 with :220-241) is: push_back(u: v, w) and
 // push_back(v: u, w) into G, and -- when kept -- the same two appends into H
 // with weight G.w(u,v) = w. H lacks the key because H is a subgraph of G.
 // Rows only receive appends, in event order. Each append record r = 2k +
-// side (row u or v of event k) is pushed onto its row's lock-free list
-// (k_fp_link, one atomic exchange per record). The list head owns the row:
-// a sole record (the vast majority) appends directly, a head with followers
-// applies the row's records in increasing r, i.e. event order (k_fp_write,
-// one thread per record and graph). Any violated precondition sets
-// not_simple BEFORE anything is written (k_fp_check) and the round engine
-// (k_rounds) commits the batch instead. The list heads are left empty for
-// the next batch.
-__global__ void k_fp_link(const DevEvent* __restrict__ ev, uint32_t nb, WalkOpts o, BatchDev b) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  stamp_commit_start(b.ctl);
-  const bool live = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
-  unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
-  if (live) {
-    const DevEvent e = ev[k];
-    const uint32_t s = b.slot[k];
-    bool have = false, reached = false;
-    if (s != kNoSlot) {
-      have = true;
-      reached = b.rout.reached[s] != 0;
-      steps = b.rout.steps[s];
-    }
-    const bool kept = !o.freeze && !(o.K != 0.0 && have && reached);
-    const uint32_t gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
-    const uint32_t gv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
-    b.fp_next[0][2 * k] = gu;
-    b.fp_next[0][2 * k + 1] = gv;
-    if (kept) {
-      const uint32_t hu = atomicExch(b.fp_head[1] + e.u, 2 * k);
-      const uint32_t hv = atomicExch(b.fp_head[1] + e.v, 2 * k + 1);
-      b.fp_next[1][2 * k] = hu;
-      b.fp_next[1][2 * k + 1] = hv;
-    }
-    b.fp_kept[k] = kept ? 1 : 0;
-    b.dec[k] = kept ? 0u : 1u;
-    (kept ? kept_n : pruned_n) = 1;
-  }
-  kept_n = warp_sum(kept_n);
-  pruned_n = warp_sum(pruned_n);
-  const unsigned long long steps_sum = warp_sum(steps);
-  const unsigned long long steps_max = warp_max(steps);
-  if ((threadIdx.x & 31) == 0 && (kept_n | pruned_n)) {
-    atomicAdd(&b.ctl->fp_report[kInsSeen], kept_n + pruned_n);
-    atomicAdd(&b.ctl->fp_report[kInsKept], kept_n);
-    atomicAdd(&b.ctl->fp_report[kInsPruned], pruned_n);
-    atomicAdd(&b.ctl->fp_report[kWalkerSteps], steps_sum);
-    atomicMax(&b.ctl->fp_report[kMaxEventSteps], steps_max);
-  }
-}
-
+// side (row u or v of event k) is pushed onto its row's lock-free list by
+// k_prep (one atomic exchange per record and graph; the lists depend on the
+// events only, not on the walks). The list head owns the row: a sole record
+// (the vast majority) appends directly, a head with followers applies the
+// row's records in increasing r, i.e. event order. G's appends do not depend
+// on the walks (which read H alone), so k_fp_check + k_fp_write_g run on a
+// second stream CONCURRENTLY with the reach walk, filling the SMs its tail
+// leaves idle; k_fp_write_h appends the kept records to H after the walk and
+// does the per-event accounting. Any violated precondition sets not_simple
+// BEFORE anything is written and the round engine (k_rounds) commits the
+// batch instead. The list heads are left empty for the next batch.
 __device__ __forceinline__ uint32_t rec_row(const DevEvent* ev, uint32_t rec) {
   const DevEvent& e = ev[rec >> 1];
   return (rec & 1) ? e.v : e.u;
@@ -164,23 +125,23 @@ __global__ void k_fp_check(const DevEvent* __restrict__ ev, uint32_t n, BatchDev
       if (other_end(ev, x) == other_end(ev, y)) b.ctl->not_simple = 1;
 }
 
-// Record r's row on one graph: the list head appends the row's records --
-// itself alone, or all of them in increasing r by repeated minimum selection
-// over the short list -- and empties the list head.
-template <int C>
+// Record r's row on one graph: the list head appends the row's records that
+// pass `take` -- itself alone, or all of them in increasing r by repeated
+// minimum selection over the short list -- and empties the list head.
+template <int C, class Take>
 __device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* ev, uint32_t* head,
-                                         const uint32_t* next, uint32_t r, bool write) {
+                                         const uint32_t* next, uint32_t r, bool write, Take take) {
   const uint32_t row = rec_row(ev, r);
   // The row's slab is needed by the head's append: request it alongside the
   // list lookups.
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(g.slab + row));
+  if (write) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.slab + row));
   const uint32_t h = head[row];
   const uint32_t nx = next[r];
   if (h != r) return true;
   bool ok = true;
   if (write) {
     if (nx == kNoSlot) {
-      ok = row_push(g, row, other_end(ev, r), ev[r >> 1].weight);
+      if (take(r)) ok = row_push(g, row, other_end(ev, r), ev[r >> 1].weight);
     } else {
       uint32_t last = 0;
       for (bool first = true; ok; first = false) {
@@ -188,13 +149,23 @@ __device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* e
         for (uint32_t x = r; x != kNoSlot; x = next[x])
           if ((first || x > last) && x < best) best = x;
         if (best == kNoSlot) break;
-        ok = row_push(g, row, other_end(ev, best), ev[best >> 1].weight);
+        if (take(best)) ok = row_push(g, row, other_end(ev, best), ev[best >> 1].weight);
         last = best;
       }
     }
   }
   head[row] = kNoSlot;
   return ok;
+}
+
+// commit_insertion's keep decision (sparsifier.cpp:228-233) for event k.
+__device__ __forceinline__ bool event_kept(const BatchDev& b, const WalkOpts& o, uint32_t k,
+                                           bool& have, unsigned long long& steps) {
+  const uint32_t s = b.slot[k];
+  have = s != kNoSlot;
+  const bool reached = have && b.rout.reached[s] != 0;
+  steps = have ? b.rout.steps[s] : 0ull;
+  return !o.freeze && !(o.K != 0.0 && have && reached);
 }
 
 // Batch epilogue: fast-path report, |E| and pool tops for the host, and the
@@ -236,21 +207,51 @@ __device__ void restore_rows(const DevGraph<kCapG>& G, const BatchDev& b, uint32
   }
 }
 
-// One thread per (record, graph): t = 2 r + (0: G, 1: H).
-__global__ void k_fp_write(DevGraph<kCapG> G, DevGraph<kCapH> H, const DevEvent* __restrict__ ev,
-                           uint32_t n, BatchDev b) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t r = t >> 1;
-  if (r >= n || batch_aborted(b.ctl)) return;
-  const bool write = !b.ctl->not_simple;
-  bool ok;
-  if ((t & 1) == 0) {
-    ok = fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write);
-  } else {
-    if (!b.fp_kept[r >> 1]) return;
-    ok = fp_apply(H, ev, b.fp_head[1], b.fp_next[1], r, write);
+// G appends, one thread per record (runs concurrently with the reach walk).
+__global__ void k_fp_write_g(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, uint32_t n,
+                             BatchDev b) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  // An invalid batch or a violated precondition: only empty the lists.
+  const bool write = !batch_aborted(b.ctl) && !b.ctl->not_simple;
+  if (!fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write, [](uint32_t) { return true; }))
+    atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
+}
+
+// After the reach walk: H appends of the kept records, and each event's
+// decision and report counters (record 2k does event k's accounting).
+__global__ void k_fp_write_h(DevGraph<kCapH> H, const DevEvent* __restrict__ ev, uint32_t n,
+                             WalkOpts o, BatchDev b) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  stamp_commit_start(b.ctl);
+  const bool write = r < n && !batch_aborted(b.ctl) && !b.ctl->not_simple;
+  unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
+  if (r < n) {
+    if (write && (r & 1) == 0) {
+      bool have;
+      const bool kept = event_kept(b, o, r >> 1, have, steps);
+      b.dec[r >> 1] = kept ? 0u : 1u;
+      (kept ? kept_n : pruned_n) = 1;
+    }
+    auto take = [&](uint32_t x) {
+      bool have;
+      unsigned long long st;
+      return event_kept(b, o, x >> 1, have, st);
+    };
+    if (!fp_apply(H, ev, b.fp_head[1], b.fp_next[1], r, write, take))
+      atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
   }
-  if (!ok) atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
+  kept_n = warp_sum(kept_n);
+  pruned_n = warp_sum(pruned_n);
+  const unsigned long long steps_sum = warp_sum(steps);
+  const unsigned long long steps_max = warp_max(steps);
+  if ((threadIdx.x & 31) == 0 && (kept_n | pruned_n)) {
+    atomicAdd(&b.ctl->fp_report[kInsSeen], kept_n + pruned_n);
+    atomicAdd(&b.ctl->fp_report[kInsKept], kept_n);
+    atomicAdd(&b.ctl->fp_report[kInsPruned], pruned_n);
+    atomicAdd(&b.ctl->fp_report[kWalkerSteps], steps_sum);
+    atomicMax(&b.ctl->fp_report[kMaxEventSteps], steps_max);
+  }
 }
 
 // The round engine. Op provides for_rows(k, f) (every row event k reads or
@@ -1165,6 +1166,16 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
           f = 1ull;
           b.wpq[k] = __dadd_rn(gw, e.weight);
         }
+        if (b.ctl->fast) {  // the fast path's append lists (G and H)
+          const uint32_t gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
+          const uint32_t gv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
+          const uint32_t hu = atomicExch(b.fp_head[1] + e.u, 2 * k);
+          const uint32_t hv = atomicExch(b.fp_head[1] + e.v, 2 * k + 1);
+          b.fp_next[0][2 * k] = gu;
+          b.fp_next[0][2 * k + 1] = gv;
+          b.fp_next[1][2 * k] = hu;
+          b.fp_next[1][2 * k + 1] = hv;
+        }
       }
       b.dec[k] = 0;
     } else {
@@ -1688,14 +1699,20 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
   return launch_rounds<true>(op, nb, b, st);
 }
 
-int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                           uint32_t nb, const WalkOpts& o, cudaStream_t st) {
+int launch_fastpath_g(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st) {
   if (nb == 0) return 0;
   const uint32_t n = 2 * nb;
-  k_fp_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, o, b);
   k_fp_check<<<grid_for(n), 256, 0, st>>>(b.events, n, b);
-  k_fp_write<<<grid_for(2ull * n), 256, 0, st>>>(G, H, b.events, n, b);
-  return 3;
+  k_fp_write_g<<<grid_for(n), 256, 0, st>>>(G, b.events, n, b);
+  return 2;
+}
+
+int launch_fastpath_h(const DevGraph<kCapH>& H, const BatchDev& b, uint32_t nb, const WalkOpts& o,
+                      cudaStream_t st) {
+  if (nb == 0) return 0;
+  const uint32_t n = 2 * nb;
+  k_fp_write_h<<<grid_for(n), 256, 0, st>>>(H, b.events, n, o, b);
+  return 1;
 }
 
 int launch_pack(const BatchDev& b, uint32_t lo_r, uint32_t n_r, uint32_t lo_m, uint32_t n_m,

@@ -147,7 +147,6 @@ struct BatchDev {
   uint32_t* fp_cnt[2];
   uint32_t* fp_head[2];
   uint32_t* fp_next[2];
-  uint8_t* fp_kept;
   // Dataflow commit (k_del_flow): one record per (event, row) of the event's
   // row superset; per-event record ranges. Per-vertex list heads and done
   // counters reuse fp_head[0] / fp_cnt[0] (kNoSlot / 0 between batches).
@@ -182,10 +181,14 @@ int launch_prepare(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
 int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b,
                    uint32_t nb, uint32_t n_del, uint64_t counter, uint32_t stamp,
                    const WalkOpts& o, int coop_blocks, cudaStream_t st);
-// Insertion-only batches: sort-based append commit (ctl.fast must be set);
-// k_rounds then only runs if a precondition failed on the device.
-int launch_insert_fastpath(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                           uint32_t nb, const WalkOpts& o, cudaStream_t st);
+// Insertion-only fast path (ctl.fast set; the lists are built by k_prep):
+// G appends (may run concurrently with the reach walk), then H appends and
+// the per-event accounting after it; k_rounds only commits if a
+// precondition failed on the device.
+int launch_fastpath_g(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st);
+int launch_fastpath_h(const DevGraph<kCapH>& H, const BatchDev& b, uint32_t nb, const WalkOpts& o,
+                      cudaStream_t st);
+bool single_pass_enabled();
 // The whole commit in one cooperative launch, epilogue included: insertion
 // batches k_rounds (fast-path appends, or rounds), deletion-only batches
 // k_del_flow (shadow undo + dataflow commit), mixed batches k_rounds_warp.

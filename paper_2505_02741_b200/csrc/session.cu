@@ -161,6 +161,8 @@ struct dyg_session {
   uint64_t stream_gen = 0;  // bumped by every dyg_stream_upload
   // dyg_replay_stream: host stream replayed with its upload pipelined.
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t aux_stream = nullptr;  // fork target inside a batch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevEvent* d_replay = nullptr;
   uint64_t replay_cap = 0;
   uint32_t* d_kinds = nullptr;
@@ -209,7 +211,6 @@ void free_batch(dyg_session* s) {
   dev_free(b.side_slab);
   dev_free(b.side_off);
   for (int i = 0; i < 2; ++i) dev_free(b.fp_next[i]);
-  dev_free(b.fp_kept);
   dev_free(b.fl_base);
   dev_free(b.fl_cnt);
   dev_free(b.fl_promo);
@@ -251,7 +252,6 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     b.cub_temp_bytes = scan_temp_bytes(cap);
     check(cudaMalloc(&b.cub_temp, std::max<size_t>(b.cub_temp_bytes, 16)), "scan temp");
     for (int i = 0; i < 2; ++i) dev_alloc(&b.fp_next[i], 2ull * cap, "append links");
-    dev_alloc(&b.fp_kept, cap, "append kept flags");
     dev_alloc(&b.fl_base, cap, "flow record ranges");
     dev_alloc(&b.fl_cnt, cap, "flow record ranges");
     dev_alloc(&b.fl_promo, cap, "flow fallback flags");
@@ -364,6 +364,7 @@ struct Pending {
   BatchCtl* hctl = nullptr;   // pinned host copy
   uint32_t* hdec = nullptr;   // pinned: decision of a 1-event batch
   uint64_t counter_base = 0;  // update_counter at batch start
+  bool g_appended = false;    // fast path: G appends already enqueued (forked)
 };
 
 void bind_pending(dyg_session* s, Pending& p) {
@@ -409,7 +410,8 @@ void phase_prepare(dyg_session* s, Pending& p) {
   b.abort_flag = s->d_abort;
   b.work = s->d_work;
   const uint32_t use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
-  const uint32_t fast = (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath) ? 1u : 0u;
+  const uint32_t fast =
+      (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath && single_pass_enabled()) ? 1u : 0u;
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
   if (p.n_del > 0) ensure_side_pool(s);
@@ -445,12 +447,23 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     max_r = n_r;
     max_m = n_m;
   }
+  // Insertion fast path: G's appends do not depend on the walk (it reads H
+  // alone); fork them onto the aux stream so they fill the walk's tail.
+  const bool fast = p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath && single_pass_enabled();
+  if (full && fast) {
+    check(cudaEventRecord(s->ev_fork, s->stream), "fork");
+    check(cudaStreamWaitEvent(s->aux_stream, s->ev_fork, 0), "fork");
+    p.launches += launch_fastpath_g(s->G.view(), b, p.nb, s->aux_stream);
+    check(cudaEventRecord(s->ev_join, s->aux_stream), "join");
+    p.g_appended = true;
+  }
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
     p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
                                s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
+  if (p.g_appended) check(cudaStreamWaitEvent(s->stream, s->ev_join, 0), "join");
   if (p.n_del > 0 && !o.freeze && max_m > 0) {
     WalkParams Pd = P;
     Pd.K = std::numeric_limits<double>::infinity();  // sparsifier.cpp:458-459
@@ -472,8 +485,10 @@ void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
-  if (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath)
-    p.launches += launch_insert_fastpath(s->G.view(), s->H.view(), b, p.nb, o, s->stream);
+  if (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath && single_pass_enabled()) {
+    if (!p.g_appended) p.launches += launch_fastpath_g(s->G.view(), b, p.nb, s->stream);
+    p.launches += launch_fastpath_h(s->H.view(), b, p.nb, o, s->stream);
+  }
   p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
   maybe_sync(s, "commit");
   if (download)
@@ -1131,6 +1146,9 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->device = device;
       check(cudaSetDevice(device), "set device");
       check(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream");
+      check(cudaStreamCreateWithFlags(&s->aux_stream, cudaStreamNonBlocking), "aux stream");
+      check(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming), "event");
+      check(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming), "event");
       s->opt = *options;
       s->n = g->n;
       s->debug_sync = std::getenv("DYG_DEBUG_SYNC") != nullptr;
@@ -1200,6 +1218,12 @@ void dyg_session_destroy(dyg_session* s) {
   s->h_kinds = nullptr;
   if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
   s->copy_stream = nullptr;
+  if (s->aux_stream) {
+    cudaStreamSynchronize(s->aux_stream);
+    cudaStreamDestroy(s->aux_stream);
+  }
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   free_batch(s);
   dev_free(s->b.mout.has_path);
   dev_free(s->b.mout.path_len);
