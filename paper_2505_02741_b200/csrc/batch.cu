@@ -1601,34 +1601,16 @@ int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned i
   return 1;
 }
 
-// DYG_SHADOW_ROUNDS=1 selects the dependency-round shadow pass (A/B knob).
-bool shadow_lists_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DYG_SHADOW_ROUNDS");
-    return !(e && std::atoi(e) == 1);
-  }();
-  return on;
-}
-
-// DYG_SINGLE_PASS=0 selects the multi-kernel prepare chain (A/B knob).
-bool single_pass_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DYG_SINGLE_PASS");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
-
 int launch_prepare(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b, uint32_t nb,
                    uint32_t n_del, uint32_t n, uint32_t stamp, const WalkOpts& o,
                    cudaStream_t st) {
   if (nb == 0) return 0;
   const unsigned tiles = grid_for(nb);
-  if (single_pass_enabled() && n_del == 0) {
+  if (o.single_pass && n_del == 0) {
     k_prep<false><<<tiles, 256, 0, st>>>(H, G, b.events, nb, n, o, b);
     return 1;
   }
-  if (single_pass_enabled() && n_del == nb && shadow_lists_enabled()) {
+  if (o.single_pass && n_del == nb && o.shadow_lists) {
     k_val_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, n, b);
     k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, n, b);
     k_prep<true><<<tiles, 256, 0, st>>>(H, G, b.events, nb, n, o, b);
@@ -1646,7 +1628,7 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   k_flags_ins<<<grid_for(nb), 256, 0, st>>>(H, G, b.events, nb, o, b);
   ++l;
   if (n_del > 0) {
-    if (shadow_lists_enabled()) {
+    if (o.shadow_lists) {
       k_sh_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, b);
       k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, G.n, b);
       l += 2;
@@ -1670,21 +1652,11 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   return l + 2;
 }
 
-// DYG_COMMIT_ROUNDS=1 forces the dependency-round engine for deletion-only
-// batches (A/B and testing knob).
-bool flow_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DYG_COMMIT_ROUNDS");
-    return !(e && std::atoi(e) == 1);
-  }();
-  return on;
-}
-
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
                   uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st) {
   CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.mscratch, b.dec, b.ctl, o};
   if (n_del == 0) return launch_rounds<false>(op, nb, b, st);
-  if (n_del == nb && flow_enabled()) {
+  if (n_del == nb && o.flow) {
     CommitOp op_copy = op;
     BatchDev b_copy = b;
     uint32_t nev = nb;

@@ -107,6 +107,12 @@ struct WalkOpts {
   uint64_t seed;
   int filtering;   // K != 0 && !freeze (sparsifier.cpp:409-410)
   int freeze;
+  // Engine selection (per session, from the environment at creation; the
+  // alternatives are A/B and test knobs, all bit-identical):
+  int fastpath;      // insertion fast path      (DYG_NO_FASTPATH disables)
+  int single_pass;   // single-pass prepare      (DYG_SINGLE_PASS=0 disables)
+  int shadow_lists;  // per-row shadow lists     (DYG_SHADOW_ROUNDS=1 disables)
+  int flow;          // dataflow deletion commit (DYG_COMMIT_ROUNDS=1 disables)
 };
 
 // Device buffers of one batch (sized by the session; grown on demand).
@@ -166,7 +172,6 @@ int launch_ctl_init(const CtlInitArgs& a, cudaStream_t st);
 // Graph support: is `n` a k_ctl_init kernel node (then *out = its args)?
 bool ctl_init_node_args(cudaGraphNode_t n, CtlInitArgs* out);
 cudaError_t ctl_init_node_update(cudaGraphExec_t ex, cudaGraphNode_t n, const CtlInitArgs& a);
-bool shadow_lists_enabled();
 int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStream_t st);
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st);
@@ -188,7 +193,6 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
 int launch_fastpath_g(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st);
 int launch_fastpath_h(const DevGraph<kCapH>& H, const BatchDev& b, uint32_t nb, const WalkOpts& o,
                       cudaStream_t st);
-bool single_pass_enabled();
 // The whole commit in one cooperative launch, epilogue included: insertion
 // batches k_rounds (fast-path appends, or rounds), deletion-only batches
 // k_del_flow (shadow undo + dataflow commit), mixed batches k_rounds_warp.

@@ -170,6 +170,10 @@ struct dyg_session {
   uint64_t kinds_cap = 0;
   std::vector<cudaEvent_t> ready;
   bool no_fastpath = false;        // DYG_NO_FASTPATH: force the round engine
+  bool single_pass = true;         // DYG_SINGLE_PASS=0: multi-kernel prepare chain
+  bool shadow_lists = true;        // DYG_SHADOW_ROUNDS=1: dependency-round walk shadow
+  bool flow = true;                // DYG_COMMIT_ROUNDS=1: round-engine deletion commit
+  uint64_t flow_cap = 0;           // DYG_FLOW_CAP: flow record capacity (test knob)
 };
 
 namespace {
@@ -290,7 +294,7 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_free(b.fl_ev);
     dev_free(b.fl_next);
     dev_free(b.fl_rank);
-    b.fl_cap = static_cast<uint64_t>(cap) * 48 + 65536;
+    b.fl_cap = s->flow_cap ? s->flow_cap : static_cast<uint64_t>(cap) * 48 + 65536;
     dev_alloc(&b.fl_row, b.fl_cap, "flow records");
     dev_alloc(&b.fl_ev, b.fl_cap, "flow records");
     dev_alloc(&b.fl_next, b.fl_cap, "flow records");
@@ -319,6 +323,10 @@ WalkOpts walk_opts(const dyg_session* s) {
   o.seed = s->opt.walk.global_seed;
   o.freeze = s->opt.freeze_sparsifier != 0;
   o.filtering = (o.K != 0.0 && !o.freeze) ? 1 : 0;  // sparsifier.cpp:409-410
+  o.fastpath = s->no_fastpath ? 0 : 1;
+  o.single_pass = s->single_pass ? 1 : 0;
+  o.shadow_lists = s->shadow_lists ? 1 : 0;
+  o.flow = s->flow ? 1 : 0;
   return o;
 }
 
@@ -411,13 +419,13 @@ void phase_prepare(dyg_session* s, Pending& p) {
   b.work = s->d_work;
   const uint32_t use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
   const uint32_t fast =
-      (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath && single_pass_enabled()) ? 1u : 0u;
+      (p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass) ? 1u : 0u;
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
   if (p.n_del > 0) ensure_side_pool(s);
   p.launches += launch_ctl_init(
       CtlInitArgs{b.ctl, s->d_epoch, p.nb, use_absent_limit, fast, p.counter_base}, s->stream);
-  if (p.n_del > 0 && !shadow_lists_enabled() && ++s->stamp == 0) {  // stamps restart
+  if (p.n_del > 0 && !o.shadow_lists && ++s->stamp == 0) {  // stamps restart
     check(cudaMemsetAsync(b.mark, 0, sizeof(uint32_t) * s->n, s->stream), "marks");
     s->stamp = 1;
   }
@@ -449,7 +457,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   }
   // Insertion fast path: G's appends do not depend on the walk (it reads H
   // alone); fork them onto the aux stream so they fill the walk's tail.
-  const bool fast = p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath && single_pass_enabled();
+  const bool fast = p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass;
   if (full && fast) {
     check(cudaEventRecord(s->ev_fork, s->stream), "fork");
     check(cudaStreamWaitEvent(s->aux_stream, s->ev_fork, 0), "fork");
@@ -485,7 +493,7 @@ void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
-  if (p.n_del == 0 && p.n_ins > 0 && !s->no_fastpath && single_pass_enabled()) {
+  if (p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass) {
     if (!p.g_appended) p.launches += launch_fastpath_g(s->G.view(), b, p.nb, s->stream);
     p.launches += launch_fastpath_h(s->H.view(), b, p.nb, o, s->stream);
   }
@@ -629,9 +637,7 @@ uint64_t session_fingerprint(dyg_session* s, uint64_t tag) {
   h = fnv(h, &o, sizeof o);
   const void* fixed[] = {s->d_work, s->d_abort, s->d_counts, s->h_ctl};
   h = fnv(h, fixed, sizeof fixed);
-  const uint32_t flags = (s->no_fastpath ? 1u : 0u) | (shadow_lists_enabled() ? 2u : 0u);
-  h = fnv(h, &flags, sizeof flags);
-  if (!shadow_lists_enabled()) h = fnv(h, &s->stamp, sizeof s->stamp);
+  if (!o.shadow_lists) h = fnv(h, &s->stamp, sizeof s->stamp);
   return h;
 }
 
@@ -1153,6 +1159,14 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->n = g->n;
       s->debug_sync = std::getenv("DYG_DEBUG_SYNC") != nullptr;
       s->no_fastpath = std::getenv("DYG_NO_FASTPATH") != nullptr;
+      const auto env_is = [](const char* k, int v) {
+        const char* e = std::getenv(k);
+        return e != nullptr && std::atoi(e) == v;
+      };
+      s->single_pass = !env_is("DYG_SINGLE_PASS", 0);
+      s->shadow_lists = !env_is("DYG_SHADOW_ROUNDS", 1);
+      s->flow = !env_is("DYG_COMMIT_ROUNDS", 1);
+      if (const char* e = std::getenv("DYG_FLOW_CAP")) s->flow_cap = std::strtoull(e, nullptr, 10);
       {
         const char* e = std::getenv("DYG_GRAPHS");
         s->graphs_on = !(e && std::atoi(e) == 0);
