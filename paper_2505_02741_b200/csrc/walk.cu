@@ -425,15 +425,23 @@ __global__ void k_reach_fix(ReachOut out, const uint32_t* __restrict__ nq_dev) {
   if (i < *nq_dev && !out.reached[i]) out.best_bits[i] = 0ull;
 }
 
-// K3: one warp per min-path query.
+// K3: one warp per min-path query: winner, loop erasure, resistance. The
+// winner's raw trace, the erased path and the per-edge 1/w live in shared
+// memory (each erasure step is a ballot over the path so far: from global
+// memory that was ~100 dependent L1/L2 round trips per query).
 template <int C>
 __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
                                                         const uint32_t* __restrict__ nq_dev,
                                                         WalkParams P, MinScratch S, MinOut out) {
+  extern __shared__ __align__(16) unsigned char fin_smem[];
   const uint32_t nq = *nq_dev;
   const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  if (out.t_end && lane == 0) atomicMax(out.t_end, global_ns());
+  const uint32_t T1 = P.T + 1;
+  unsigned char* wbase = fin_smem + static_cast<size_t>(threadIdx.x >> 5) * T1 * 16;
+  double* rv = reinterpret_cast<double*>(wbase);
+  uint32_t* trace = reinterpret_cast<uint32_t*>(wbase + T1 * 8);
+  uint32_t* erased = trace + T1;
   if (qi >= nq) return;
   const uint64_t base = static_cast<uint64_t>(qi) * P.s;
   unsigned long long st = 0;
@@ -465,13 +473,16 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
       out.has_path[qi] = 0;
       out.path_len[qi] = 0;
       out.resistance[qi] = 0.0;
+      if (out.t_end) atomicMax(out.t_end, global_ns());
     }
     return;
   }
-  const uint32_t* trace = S.paths + (base + bidx) * (P.T + 1ull);
+  const uint32_t* gtrace = S.paths + (base + bidx) * static_cast<uint64_t>(T1);
   const uint32_t len = S.steps[base + bidx] + 1;
-  uint32_t* erased = out.paths + static_cast<uint64_t>(qi) * (P.T + 1ull);
-  // loop_erase: a revisit truncates back to the first occurrence.
+  for (uint32_t i = lane; i < len; i += 32) trace[i] = gtrace[i];
+  __syncwarp();
+  // loop_erase (walk.cpp:100-117): a revisit truncates back to the first
+  // occurrence.
   uint32_t elen = 0;
   for (uint32_t i = 0; i < len; ++i) {
     const uint32_t v = trace[i];
@@ -489,7 +500,9 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
     }
     __syncwarp();
   }
-  double* rv = S.rvals + static_cast<uint64_t>(qi) * (P.T + 1ull);
+  uint32_t* gerased = out.paths + static_cast<uint64_t>(qi) * T1;
+  for (uint32_t i = lane; i < elen; i += 32) gerased[i] = erased[i];
+  // resistance = sum of 1/w over the erased path in path order (walk.cpp:140-143)
   for (uint32_t i = lane; i + 1 < elen; i += 32)
     rv[i] = __drcp_rn(edge_weight(g, erased[i], erased[i + 1]));
   __syncwarp();
@@ -499,6 +512,7 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
     out.has_path[qi] = 1;
     out.path_len[qi] = elen;
     out.resistance[qi] = r;
+    if (out.t_end) atomicMax(out.t_end, global_ns());
   }
 }
 
@@ -584,8 +598,20 @@ int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_d
     case 2: launch_walk<C, true, 2, 4, 4>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
     default: launch_walk<C, true, 2, 8, 2>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
   }
-  k_minpath_finish<C><<<blocks_for(static_cast<uint64_t>(nq_max) * 32, 256), 256, 0, st>>>(
-      g, nq_dev, P, scratch, out);
+  // 16 B of shared memory per trace position per warp; long caps get one
+  // warp per block (up to the opt-in shared-memory limit).
+  const size_t per_warp = (static_cast<size_t>(P.T) + 1) * 16;
+  const unsigned warps = per_warp * 8 <= 48 * 1024 ? 8u : 1u;
+  if (per_warp * warps > 48 * 1024) {
+    static size_t granted = 0;
+    if (per_warp * warps > granted) {
+      cudaFuncSetAttribute(k_minpath_finish<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(per_warp * warps));
+      granted = per_warp * warps;
+    }
+  }
+  k_minpath_finish<C><<<blocks_for(static_cast<uint64_t>(nq_max) * 32, 32 * warps), 32 * warps,
+                        per_warp * warps, st>>>(g, nq_dev, P, scratch, out);
   return l;
 }
 
