@@ -830,14 +830,14 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
     if (tid == 0) batch_finish(op.G, op.H, b);
     return;
   }
-  // Undo the in-place walk shadow before anything reads G.
-  restore_rows(op.G, b, tid, nth);
-  grid.sync();
   const uint32_t lim = min(nev, op.limit());
   uint32_t* head = b.fp_head[0];
   uint32_t* done = b.fp_cnt[0];
   uint32_t* mark = b.fp_cnt[1];
   if (tid == 0) ctl->fl_t[0] = global_ns();
+  // Undo the in-place walk shadow before anything reads G (same pass as the
+  // first step of phase 0, which does not read G).
+  restore_rows(op.G, b, tid, nth);
   // Phase 0: which events may run the local fallback. An event whose edge
   // is in batch-start H without a recovered path may. An event whose edge is
   // NOT in batch-start H may only if an earlier fallback inserted its edge
@@ -856,9 +856,13 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
         mark[e.v] = 1;
       }
     }
+  }
+  grid.sync();
+  if (!op.o.freeze) {
+    // Three rotating flags: flag (it + 1) % 3 was last read before the
+    // barrier that ended iteration it - 1, so resetting it here is safe.
     for (uint32_t it = 0;; ++it) {
-      grid.sync();
-      if (tid == 0) ctl->fl_changed[(it + 1) & 1] = 0;
+      if (tid == 0) ctl->fl_changed[(it + 1) % 3] = 0;
       for (uint32_t k = tid; k < lim; k += nth) {
         if (b.fl_promo[k] || op.slot[k] != kNoSlot) continue;
         const DevEvent& e = op.ev[k];
@@ -867,11 +871,11 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
           b.fl_promo[k] = 1;
           mark[e.u] = 1;
           mark[e.v] = 1;
-          ctl->fl_changed[it & 1] = 1;
+          ctl->fl_changed[it % 3] = 1;
         }
       }
       grid.sync();
-      if (!ctl->fl_changed[it & 1]) break;
+      if (!ctl->fl_changed[it % 3]) break;
     }
   }
   if (tid == 0) ctl->fl_t[1] = global_ns();
@@ -943,6 +947,18 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
     // unapplied event overall is always inside its owner's window and ready:
     // no deadlock, and no shared work counter to contend on.
     const uint32_t count = wid < lim ? (lim - wid + nw - 1) / nw : 0;
+    // Pull every row this warp's events will touch (G and H slabs) toward L2
+    // now, so the dependent lookups inside apply_warp hit L2 instead of each
+    // paying a DRAM round trip in sequence.
+    for (uint32_t j = 0; j < count; ++j) {
+      const uint32_t k = wid + j * nw;
+      const uint32_t base = b.fl_base[k], n = b.fl_cnt[k];
+      for (uint32_t t = lane; t < n; t += 32) {
+        const uint32_t x = b.fl_row[base + t];
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(op.G.slab + x));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(op.H.slab + x));
+      }
+    }
     constexpr uint32_t kWin = 8;
     uint32_t jlo = 0;
     uint32_t mask = count >= kWin ? 0xFFu : ((1u << count) - 1u);

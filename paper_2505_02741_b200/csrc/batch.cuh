@@ -75,7 +75,7 @@ struct BatchCtl {
   unsigned int fl_next_ev;   // next event to take (in event order)
   unsigned int fl_overflow;  // record buffer too small: the round engine commits
   unsigned int flow_done;    // k_del_flow committed the batch
-  unsigned int fl_changed[2];  // fallback-promotion fixpoint
+  unsigned int fl_changed[3];  // fallback-promotion fixpoint (rotating)
   unsigned int fl_depth;     // longest chain of row-sharing events
   unsigned long long fl_t[6];  // %globaltimer at the phase boundaries
   unsigned long long counter_base;  // update_counter_ at batch start (:431)
