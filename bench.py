@@ -65,7 +65,8 @@ def make_inputs_product(cfg):
     rows, cols, kind, ins, dele, loc = CONFIGS[cfg]
     gen = D.make_mesh if kind == "mesh" else D.make_grid4
     g = gen(rows, cols, 1)
-    h = D.build_initial_sparsifier(g, 0.10, 1)
+    # The device builder, bit-identical to the host one.
+    h = D.build_initial_sparsifier_gpu(g, 0.10, 1)
     s = D.generate_update_stream(g, D.StreamGenOptions(ins, dele, 10, 7, loc))
     return g, h, s
 

@@ -240,6 +240,17 @@ int dyg_session_restore(dyg_session* s);
 int dyg_session_stats(const dyg_session* s, dyg_stats* out);
 int dyg_session_reset_stats(dyg_session* s);
 
+/* build_initial_sparsifier (sparsifier.cpp:105-159) on `device`, bit-identical
+ * to the reference: maximum spanning tree in (weight desc, (u, v) asc) order,
+ * then off-tree edges by distortion w * R_tree(u, v) descending (ties:
+ * hash_mix(seed ^ (u << 32 | v)) ascending) until density >= target.
+ * row_ptr_out[n + 1]; ids_out / w_out need room for g's nnz (H's rows, in
+ * the order the reference's insert_edge calls build them). Usage error for a
+ * negative target, Data error for a disconnected graph. */
+int dyg_build_initial_sparsifier(const dyg_csr* g, double target_density, uint64_t seed,
+                                 int device, uint64_t* row_ptr_out, uint32_t* ids_out,
+                                 double* w_out);
+
 /* Stateless twin of run_batch (walk.hpp:86-92): uploads g, runs the queries
  * on `device`, returns results in query order. path_buf (nullable) receives
  * MinPath vertices at [i*(T+1)]. */

@@ -18,6 +18,7 @@ from .api import (  # noqa: F401
     UpdateStream,
     WalkConfig,
     build_initial_sparsifier,
+    build_initial_sparsifier_gpu,
     device_count,
     generate_update_stream,
     load_matrix_market,

@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
         "dyg_session_stats": (i32, [vp, vp]),
         "dyg_session_reset_stats": (i32, [vp]),
         "dyg_run_batch": (i32, [C.POINTER(Csr), vp, sz, C.POINTER(WalkCfg), vp, vp, i32]),
+        "dyg_build_initial_sparsifier": (i32, [C.POINTER(Csr), dbl, u64, i32, vp, vp, vp]),
         "dyg_set_stream": (i32, [vp, vp]),
         "dyg_shard_begin": (i32, [vp, vp, vp, sz, u32, C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_uint64)]),

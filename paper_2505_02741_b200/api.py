@@ -215,6 +215,23 @@ def build_initial_sparsifier(g: DynamicGraph, target_density: float, seed: int) 
     return _graph_from(_lib.lib().dygh_build_initial_sparsifier, g._h, target_density, seed)
 
 
+def build_initial_sparsifier_gpu(g: DynamicGraph, target_density: float, seed: int,
+                                 device: int = 0) -> DynamicGraph:
+    """build_initial_sparsifier (sparsifier.cpp:105-159) on the GPU
+    (dyg_build_initial_sparsifier), bit-identical to the host builder."""
+    c = g.csr()
+    n = c.n
+    nnz = int(np.ctypeslib.as_array(C.cast(c.row_ptr, C.POINTER(C.c_uint64)), (n + 1,))[n]) \
+        if n else 0
+    rp = np.zeros(n + 1, np.uint64)
+    ids = np.zeros(max(nnz, 1), np.uint32)
+    w = np.zeros(max(nnz, 1), np.float64)
+    _check(_lib.lib().dyg_build_initial_sparsifier(C.byref(c), float(target_density), int(seed),
+                                                   int(device), ptr(rp), ptr(ids), ptr(w)))
+    m = int(rp[n])
+    return DynamicGraph.from_rows(rp, ids[:m], w[:m])
+
+
 def load_matrix_market(path: str) -> DynamicGraph:
     return _graph_from(_lib.lib().dygh_load_matrix_market, path.encode())
 

@@ -52,6 +52,13 @@ class GraphStore {
   unsigned long long* counters_ = nullptr;  // [0] pool_top, [1] edges
 };
 
+// Initial sparsifier on the device (init_sparsifier.cu): G as a host CSR in
+// row order, H written to host buffers (row_ptr[n + 1]; ids / w with room
+// for G's nnz). Throws DeviceError{1 usage | 2 data | 4 device}.
+void build_initial_sparsifier_device(uint32_t n, const uint64_t* row_ptr, const uint32_t* ids,
+                                     const double* w, double target_density, uint64_t seed,
+                                     uint64_t* out_row_ptr, uint32_t* out_ids, double* out_w);
+
 extern template class GraphStore<kCapH>;
 extern template class GraphStore<kCapG>;
 

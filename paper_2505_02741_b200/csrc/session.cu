@@ -1689,6 +1689,21 @@ int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
 }
 
 // ---- stateless run_batch twin (walk.hpp:86-92) ----------------------------
+int dyg_build_initial_sparsifier(const dyg_csr* g, double target_density, uint64_t seed,
+                                 int device, uint64_t* row_ptr_out, uint32_t* ids_out,
+                                 double* w_out) {
+  return guarded([&] {
+    if (row_ptr_out == nullptr || ids_out == nullptr || w_out == nullptr)
+      fail(DYG_ERR_USAGE, "null argument");
+    check_csr(g, "graph");
+    if (target_density < 0.0) fail(DYG_ERR_USAGE, "target density must be nonnegative");
+    if (g->n == 0) fail(DYG_ERR_DATA, "graph must be connected to build a sparsifier");
+    check(cudaSetDevice(device), "set device");
+    build_initial_sparsifier_device(g->n, g->row_ptr, g->ids, g->w, target_density, seed,
+                                    row_ptr_out, ids_out, w_out);
+  });
+}
+
 int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_queries,
                   const dyg_walk_config* cfg, dyg_walk_result* out, uint32_t* path_buf,
                   int device) {

@@ -16,7 +16,8 @@ rng = np.random.default_rng(1)
 us = np.repeat(np.arange(len(rp) - 1, dtype=np.uint32), np.diff(rp).astype(np.int64))
 m = us < ids
 eu, ev = us[m], ids[m]
-opts = D.SparsifierOptions(D.WalkConfig(100.0, 100, 16, 42), True, False)
+S_WALKERS = int(os.environ.get("SW", "16"))
+opts = D.SparsifierOptions(D.WalkConfig(100.0, 100, S_WALKERS, 42), True, False)
 st = D.SparsifierState(g, h, opts)
 st.snapshot()
 SIZES = [int(x) for x in sys.argv[1:]] or [1, 8, 64, 512, 4096]
@@ -35,5 +36,5 @@ for nq in SIZES:
         s = st.stats()
         res.append((s["minpath_ms"], s["minpath_steps"], s["minpath_tail_ms"], s["commit_ms"], s["total_ms"]))
     mp, steps, tail, cm, tot = res[-1]
-    print(f"deletions={nq:5d} walkers={16*nq:6d} minpath_ms={mp:.4f} steps={steps} "
+    print(f"deletions={nq:5d} walkers={S_WALKERS*nq:6d} minpath_ms={mp:.4f} steps={steps} "
           f"us/step(max chain 100)={1000*mp/100:.2f} commit_ms={cm:.4f} batch_ms={tot:.4f}", flush=True)
