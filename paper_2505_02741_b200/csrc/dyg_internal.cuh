@@ -30,6 +30,10 @@ constexpr uint32_t kInline = 0xFFFFFFFFu;    // slab.ext for inline rows
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
 constexpr int kCapH = 7;   // inline entries per H slab (96 B, split 64 + 32)
 constexpr int kCapG = 10;  // inline entries per G slab (128 B)
+#ifndef DYG_H_SLAB_ALIGN
+#define DYG_H_SLAB_ALIGN 32
+#endif
+constexpr int kHSlabAlign = DYG_H_SLAB_ALIGN;  // 32: 96 B slabs; 128: one line per slab
 
 // rng.hpp:37-41
 __host__ __device__ __forceinline__ uint64_t hash_mix(uint64_t x) {
@@ -76,7 +80,7 @@ struct alignas(128) Slab<kCapG> {
 };
 
 template <>
-struct alignas(32) Slab<kCapH> {
+struct alignas(kHSlabAlign) Slab<kCapH> {
   uint32_t deg;
   uint32_t ext;
   uint32_t id_lo[4];
@@ -87,7 +91,7 @@ struct alignas(32) Slab<kCapH> {
   __host__ __device__ uint32_t& idr(uint32_t i) { return i < 4 ? id_lo[i] : id_hi[i - 4]; }
   __host__ __device__ double& wr(uint32_t i) { return i < 4 ? w_lo[i] : w_hi[i - 4]; }
 };
-static_assert(sizeof(Slab<kCapH>) == 96, "H slab must be 96 B");
+static_assert(sizeof(Slab<kCapH>) == kHSlabAlign || kHSlabAlign == 32, "H slab size");
 static_assert(sizeof(Slab<kCapG>) == 128, "G slab must be 128 B");
 
 // POD view of one device graph, passed by value to kernels.

@@ -64,10 +64,12 @@ template <int C>
 __device__ __forceinline__ bool walk_step(const DevGraph<C>& g, const uint4* head, uint32_t cur,
                                           uint32_t prev, double u01, uint32_t& next, double& ew,
                                           uint32_t& deg) {
-  constexpr int NV = static_cast<int>(sizeof(Slab<C>) / 16);
+  // 16 B chunks holding the row: H entries end at byte 96 whatever the slab
+  // padding.
+  constexpr int NV = C == kCapH ? 6 : static_cast<int>(sizeof(Slab<C>) / 16);
   constexpr int NH = Gather<C>::kChunks;
   union {
-    uint4 v[NV];
+    uint4 v[sizeof(Slab<C>) / 16];
     Slab<C> s;
   } r;
 #pragma unroll
