@@ -286,7 +286,7 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.mscratch.acc, cap * sw, "minpath scratch");
     dev_alloc(&b.mscratch.term, cap * sw, "minpath scratch");
     dev_alloc(&b.mscratch.steps, cap * sw, "minpath scratch");
-    dev_alloc(&b.mscratch.paths, cap * sw * T1, "minpath traces");
+    dev_alloc(&b.mscratch.paths, cap * sw * trace_stride(s->opt.walk.step_cap), "minpath traces");
     dev_alloc(&b.mscratch.rvals, cap * T1, "minpath scratch");
     // Flow records: u, v and a path of <= T+1 vertices or two G rows per
     // deletion; overflow falls back to the round engine.
@@ -1799,7 +1799,7 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
       dev_alloc(&sc.acc, nm * sw, "scratch");
       dev_alloc(&sc.term, nm * sw, "scratch");
       dev_alloc(&sc.steps, nm * sw, "scratch");
-      dev_alloc(&sc.paths, nm * sw * T1, "scratch");
+      dev_alloc(&sc.paths, nm * sw * trace_stride(cfg->step_cap), "scratch");
       dev_alloc(&sc.rvals, nm * T1, "scratch");
       check(cudaMemcpy(d_q, mq.data(), sizeof(MinQuery) * nm, cudaMemcpyHostToDevice), "q");
       launch_minpath(gg.view(), d_q, d_n + 1, counts[1], P, sc, mo, ctr + 1, d_work, st);

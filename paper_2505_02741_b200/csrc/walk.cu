@@ -190,6 +190,7 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long lo
 // raw trace and (acc, terminal, steps) for K3.
 struct Slot {
   uint32_t cur, prev, tgt, steps, widx;
+  uint32_t tb[8];  // min-path: the last 8 trace entries (a shift register)
   bool has;
   uint64_t rng;
   double acc, wpq;
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         w.steps = 0;
         w.acc = 0.0;
         w.has = true;
-        if (kMinPath) S.paths[static_cast<uint64_t>(w.widx) * (P.T + 1ull)] = w.cur;
+        if (kMinPath) w.tb[7] = w.cur;  // trace entry 0
       }
       chunk_pos += take;
       need = __ballot_sync(kFull, !w.has);
@@ -366,7 +367,19 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
           ++w.steps;
           w.prev = w.cur;
           w.cur = next;
-          if (kMinPath) S.paths[static_cast<uint64_t>(w.widx) * (P.T + 1ull) + w.steps] = next;
+          if (kMinPath) {
+            // Trace entry `steps`; every 8th entry completes a 32 B sector,
+            // written whole.
+#pragma unroll
+            for (int j = 0; j < 7; ++j) w.tb[j] = w.tb[j + 1];
+            w.tb[7] = next;
+            if ((w.steps & 7u) == 7u) {
+              uint4* dst = reinterpret_cast<uint4*>(
+                  S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T) + (w.steps - 7));
+              dst[0] = make_uint4(w.tb[0], w.tb[1], w.tb[2], w.tb[3]);
+              dst[1] = make_uint4(w.tb[4], w.tb[5], w.tb[6], w.tb[7]);
+            }
+          }
           if (__dmul_rn(w.wpq, w.acc) > P.K) {
             term = kBudget;
           } else if (next == w.tgt) {
@@ -378,6 +391,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         if (term != 0xFFFFFFFFu) {
           my_steps += w.steps;
           if (kMinPath) {
+            // The trace's last, partial sector: entries steps-r+1 .. steps.
+            const uint32_t r = (w.steps + 1) & 7u;
+            uint32_t* tr = S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T);
+#pragma unroll
+            for (int j = 1; j < 8; ++j)
+              if (static_cast<uint32_t>(j) <= r) tr[w.steps + 1 - j] = w.tb[8 - j];
             S.acc[w.widx] = w.acc;
             S.term[w.widx] = term;
             S.steps[w.widx] = w.steps;
@@ -479,7 +498,7 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
     }
     return;
   }
-  const uint32_t* gtrace = S.paths + (base + bidx) * static_cast<uint64_t>(T1);
+  const uint32_t* gtrace = S.paths + (base + bidx) * trace_stride(P.T);
   const uint32_t len = S.steps[base + bidx] + 1;
   for (uint32_t i = lane; i < len; i += 32) trace[i] = gtrace[i];
   __syncwarp();

@@ -40,6 +40,13 @@ inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t se
   return WalkParams{K, T, s, seed, sh, early};
 }
 
+// Entries per raw min-path trace: T + 1 rounded up to whole 32 B sectors, so
+// the walkers write their traces in full sectors (a partial-sector store
+// costs the HBM a read-modify-write).
+__host__ __device__ inline uint64_t trace_stride(uint32_t T) {
+  return (static_cast<uint64_t>(T) + 1 + 7) & ~7ull;
+}
+
 struct ReachQuery {   // WalkQuery Reach (walk.hpp:71-78)
   uint32_t p, q;
   double w_pq;
@@ -70,7 +77,7 @@ struct MinScratch {
   double* acc;
   uint32_t* term;
   uint32_t* steps;
-  uint32_t* paths;     // [(q*s+i)*(T+1)] raw traces
+  uint32_t* paths;     // [(q*s+i)*trace_stride(T)] raw traces
   double* rvals;       // [q*(T+1)] per-edge 1/w for the resistance sum
 };
 
