@@ -304,7 +304,10 @@ def run_ours(args):
     log(f"[rank {rank}] inputs {time.perf_counter() - t0:.1f}s")
     opts = D.SparsifierOptions(D.WalkConfig(K_BUDGET, T_CAP, WALKERS, WALK_SEED), True, False)
     st = D.SparsifierState(g, h, opts, device=dev)
-    torch_stream = torch.cuda.current_stream()
+    # A dedicated (capturable) stream: the session enqueues each replay as a
+    # CUDA graph; the legacy default stream cannot be captured.
+    torch_stream = torch.cuda.Stream()
+    torch.cuda.set_stream(torch_stream)
     st.set_stream(torch_stream.cuda_stream)
     st.snapshot()
     nb = stream.batch_count

@@ -661,6 +661,10 @@ template <class F>
 CapturedGraph* capture_graph(dyg_session* s, uint64_t key, uint64_t counter, F&& enqueue) {
   cudaGetLastError();
   if (cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    // e.g. the legacy default stream, which cannot be captured
+    if (std::getenv("DYG_GRAPH_DEBUG"))
+      std::fprintf(stderr, "dyg: stream capture unavailable (%s); launching eagerly\n",
+                   cudaGetErrorString(cudaGetLastError()));
     cudaGetLastError();
     s->graphs_on = false;
     return nullptr;
@@ -706,7 +710,7 @@ CapturedGraph* capture_graph(dyg_session* s, uint64_t key, uint64_t counter, F&&
   cg.base = counter;
   cg.cap_base = counter;
   cg.launches = launches;
-  constexpr size_t kMaxGraphs = 8;
+  constexpr size_t kMaxGraphs = 64;  // a whole stream's per-batch graphs
   if (s->graphs.size() >= kMaxGraphs) {  // evict the least recently used
     size_t lru = 0;
     for (size_t i = 1; i < s->graphs.size(); ++i)
@@ -1029,9 +1033,27 @@ void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_
     ensure_batch(s, p.nb, p.n_del);
     if (p.n_del > 0) ensure_side_pool(s);
     check(cudaStreamWaitEvent(s->stream, s->ready[b], 0), "upload wait");
-    phase_prepare(s, p);
-    phase_walk(s, p, true, 0, 0, 0, 0);
-    commit_enqueue(s, p, false);
+    auto enqueue = [&] {
+      Pending q = p;
+      phase_prepare(s, q);
+      phase_walk(s, q, true, 0, 0, 0, 0);
+      commit_enqueue(s, q, false);
+      return q.launches;
+    };
+    CapturedGraph* g = nullptr;
+    if (graphs_usable(s)) {  // one graph per batch slot, reused by later replays
+      uint64_t key = session_fingerprint(s, 3);
+      const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
+                                reinterpret_cast<uint64_t>(p.hctl), p.nb, p.n_ins, p.n_del};
+      key = fnv(key, shape, sizeof shape);
+      g = find_graph(s, key);
+      if (g == nullptr) g = capture_graph(s, key, p.counter_base, enqueue);
+      if (g != nullptr) {
+        launch_graph(s, *g, p.counter_base);
+        p.launches = g->launches;
+      }
+    }
+    if (g == nullptr) p.launches = enqueue();
     counter += p.nb;
   }
   check(cudaMemcpyAsync(s->h_ctls, s->d_ctls, sizeof(BatchCtl) * nbatches, cudaMemcpyDeviceToHost,
