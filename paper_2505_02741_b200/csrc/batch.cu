@@ -1179,8 +1179,11 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
         const double gw = edge_weight(G, e.u, e.v);
         if (gw != 0.0) b.ctl->not_simple = 1;  // fast-path precondition: new key
         if (o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) {
-          f = 1ull;
-          b.wpq[k] = __dadd_rn(gw, e.weight);
+          const double wpq = __dadd_rn(gw, e.weight);
+          // long-walking queries count in the low half, the others (with a
+          // split) in the high half -- no min-path queries in this batch
+          f = (o.split_wpq > 0.0 && wpq > o.split_wpq) ? (1ull << 32) : 1ull;
+          b.wpq[k] = wpq;
         }
         if (b.ctl->fast) {  // the fast path's append lists (G and H)
           const uint32_t gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
@@ -1230,11 +1233,23 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
   __syncthreads();
   const unsigned long long excl = s_prefix + s_warp[wid] + x - f;
   if (k < nb && !aborted) {
-    scatter_event(e, k, f, static_cast<uint32_t>(excl & 0xFFFFFFFFull),
-                  static_cast<uint32_t>(excl >> 32), o.seed, b);
+    if (!kDel && (f >> 32)) {
+      // short-walking reach query: slots from the top of the buffer
+      scatter_event(e, k, 1ull, b.q_cap - 1 - static_cast<uint32_t>(excl >> 32), 0, o.seed, b);
+    } else {
+      scatter_event(e, k, f, static_cast<uint32_t>(excl & 0xFFFFFFFFull),
+                    static_cast<uint32_t>(excl >> 32), o.seed, b);
+    }
     if (k == nb - 1) {
-      b.ctl->nq_reach = static_cast<uint32_t>((excl + f) & 0xFFFFFFFFull);
-      b.ctl->nq_min = static_cast<uint32_t>((excl + f) >> 32);
+      const uint32_t lo = static_cast<uint32_t>((excl + f) & 0xFFFFFFFFull);
+      const uint32_t hi = static_cast<uint32_t>((excl + f) >> 32);
+      if (kDel) {
+        b.ctl->nq_reach = lo;
+        b.ctl->nq_min = hi;
+      } else {
+        b.ctl->nq_reach = lo + hi;
+        b.ctl->nq_long = lo;
+      }
     }
   }
 }

@@ -86,7 +86,7 @@ struct BatchCtl {
   unsigned long long t_batch1;   // batch epilogue
   unsigned long long epoch;      // unique per batch (single-pass scan tile states)
   unsigned int tile_ctr;         // single-pass scan: next tile
-  unsigned int pad_tile;
+  unsigned int nq_long;        // reach queries in the low slots (walk-order split)
 };
 
 // Arguments of the batch control-block initialisation kernel: the only
@@ -113,6 +113,11 @@ struct WalkOpts {
   int single_pass;   // single-pass prepare      (DYG_SINGLE_PASS=0 disables)
   int shadow_lists;  // per-row shadow lists     (DYG_SHADOW_ROUNDS=1 disables)
   int flow;          // dataflow deletion commit (DYG_COMMIT_ROUNDS=1 disables)
+  int pad_opts;
+  // Reach walk order (insertion-only, single-GPU batches): queries whose
+  // w_pq <= split_wpq (the budget lets them walk longest) get the low slots and
+  // are walked first, the rest take slots from the top of the buffer; 0 = off.
+  double split_wpq;
 };
 
 // Device buffers of one batch (sized by the session; grown on demand).
@@ -146,6 +151,7 @@ struct BatchDev {
   // Single-pass (decoupled look-back) query scan: per 256-event tile,
   // {aggregate, inclusive, epoch << 2 | state}; state 1 = aggregate, 2 = inclusive.
   unsigned long long* tile_state;
+  uint32_t q_cap;            // query slot capacity (reach slots are < q_cap)
   void* cub_temp;
   size_t cub_temp_bytes;
   // Insertion fast path ([0] = G, [1] = H): per-vertex append counts and

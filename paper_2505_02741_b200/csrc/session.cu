@@ -174,6 +174,8 @@ struct dyg_session {
   bool shadow_lists = true;        // DYG_SHADOW_ROUNDS=1: dependency-round walk shadow
   bool flow = true;                // DYG_COMMIT_ROUNDS=1: round-engine deletion commit
   uint64_t flow_cap = 0;           // DYG_FLOW_CAP: flow record capacity (test knob)
+  bool reach_split = true;         // DYG_REACH_SPLIT=0: reach walks in slot order
+  double mean_inv_w = 1.0;         // mean 1/w over G's edges (session creation)
 };
 
 namespace {
@@ -259,6 +261,7 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.fl_base, cap, "flow record ranges");
     dev_alloc(&b.fl_cnt, cap, "flow record ranges");
     dev_alloc(&b.fl_promo, cap, "flow fallback flags");
+    b.q_cap = cap;
     dev_alloc(&b.tile_state, 3ull * (cap / 256 + 2), "scan tile states");
     check(cudaMemset(b.tile_state, 0, sizeof(unsigned long long) * 3ull * (cap / 256 + 2)),
           "scan tile states");
@@ -327,6 +330,11 @@ WalkOpts walk_opts(const dyg_session* s) {
   o.single_pass = s->single_pass ? 1 : 0;
   o.shadow_lists = s->shadow_lists ? 1 : 0;
   o.flow = s->flow ? 1 : 0;
+  // Walk-order split threshold: a walker's acc grows by ~E[1/w] per step, so
+  // the budget K / w_pq allows >= 0.8 T steps when w_pq <= K / (0.8 T E[1/w]).
+  o.split_wpq = (s->reach_split && o.filtering && o.T > 0)
+                    ? o.K / (0.8 * static_cast<double>(o.T) * s->mean_inv_w) : 0.0;
+  o.pad_opts = 0;
   return o;
 }
 
@@ -373,6 +381,7 @@ struct Pending {
   uint32_t* hdec = nullptr;   // pinned: decision of a 1-event batch
   uint64_t counter_base = 0;  // update_counter at batch start
   bool g_appended = false;    // fast path: G appends already enqueued (forked)
+  bool shard = false;         // multi-GPU split batch (dyg_shard_*)
 };
 
 void bind_pending(dyg_session* s, Pending& p) {
@@ -407,7 +416,8 @@ void ensure_pools(dyg_session* s, uint64_t n_ins, uint64_t n_del) {
 
 // validate (:405-407), walk shadow (:416-423), query build (:429-457).
 void phase_prepare(dyg_session* s, Pending& p) {
-  const WalkOpts o = walk_opts(s);
+  WalkOpts o = walk_opts(s);
+  if (p.shard) o.split_wpq = 0.0;  // shard ranges need contiguous reach slots
   ensure_batch(s, p.nb, p.n_del);
   ensure_pools(s, p.n_ins, p.n_del);
   BatchDev& b = s->b;
@@ -466,7 +476,11 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     p.g_appended = true;
   }
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
-    ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r};
+    ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r, nullptr, 0};
+    if (full && o.split_wpq > 0.0 && p.n_del == 0 && o.single_pass) {
+      ro.nq_long = &b.ctl->nq_long;
+      ro.cap = b.q_cap;
+    }
     p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
                                s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
@@ -1188,12 +1202,19 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->single_pass = !env_is("DYG_SINGLE_PASS", 0);
       s->shadow_lists = !env_is("DYG_SHADOW_ROUNDS", 1);
       s->flow = !env_is("DYG_COMMIT_ROUNDS", 1);
+      s->reach_split = !env_is("DYG_REACH_SPLIT", 0);
       if (const char* e = std::getenv("DYG_FLOW_CAP")) s->flow_cap = std::strtoull(e, nullptr, 10);
       {
         const char* e = std::getenv("DYG_GRAPHS");
         s->graphs_on = !(e && std::atoi(e) == 0);
       }
       s->G.upload(g->n, g->row_ptr, g->ids, g->w, s->stream);
+      {  // mean 1/w over G (the walk-order split's step-cost estimate)
+        const uint64_t nnz = g->row_ptr[g->n];
+        double acc = 0.0;
+        for (uint64_t i = 0; i < nnz; ++i) acc += 1.0 / g->w[i];
+        s->mean_inv_w = nnz ? acc / static_cast<double>(nnz) : 1.0;
+      }
       s->H.upload(h->n, h->row_ptr, h->ids, h->w, s->stream);
       s->g_edges = g->row_ptr[g->n] / 2;
       s->h_edges = h->row_ptr[h->n] / 2;
@@ -1626,6 +1647,7 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
       p.n_ins = n_ins;
       p.n_del = n_del;
       p.batch = batch_index;
+      p.shard = true;
       phase_prepare(s, p);
       BatchCtl& c = *s->h_ctl;
       check(cudaMemcpyAsync(&c, s->b.ctl, sizeof c, cudaMemcpyDeviceToHost, s->stream), "ctl");

@@ -189,7 +189,7 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long lo
 // atomics into outputs pre-set by k_reach_init. Min-path walkers keep their
 // raw trace and (acc, terminal, steps) for K3.
 struct Slot {
-  uint32_t cur, prev, tgt, steps, widx;
+  uint32_t cur, prev, tgt, steps, widx, qi;
   uint32_t tb[8];  // min-path: the last 8 trace entries (a shift register)
   bool has;
   uint64_t rng;
@@ -200,6 +200,7 @@ struct ChunkSmem {  // per warp: the current 32-item chunk
   uint2 pq[32];
   double w[32];
   unsigned long long seed[32];
+  uint32_t qi[32];  // output slot of the item's query (reach)
   double u[32];  // this step's draw, stored before the fetch wait (see k_walk)
 };
 
@@ -283,9 +284,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
             cs.w[lane] = 1.0;
             qseed = Q.qseed;
           } else {
-            const ReachQuery Q = rq[q];
+            uint32_t qq = q;
+            if (rout.nq_long) {
+              const uint32_t nl = *rout.nq_long;
+              if (q >= nl) qq = rout.cap - 1 - (q - nl);
+            }
+            const ReachQuery Q = rq[qq];
             cs.pq[lane] = make_uint2(Q.p, Q.q);
             cs.w[lane] = Q.w_pq;
+            cs.qi[lane] = qq;
             qseed = Q.qseed;
           }
           cs.seed[lane] = walker_seed_from(qseed, wi);
@@ -302,6 +309,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         w.tgt = pq.y;
         w.wpq = cs.w[item];
         w.rng = cs.seed[item];
+        if (!kMinPath) w.qi = cs.qi[item];
         w.prev = kNoVertex;
         w.steps = 0;
         w.acc = 0.0;
@@ -401,8 +409,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
             S.term[w.widx] = term;
             S.steps[w.widx] = w.steps;
           } else {
-            const uint32_t qi =
-                P.s_shift != kNoShift ? (w.widx >> P.s_shift) : w.widx / P.s;
+            const uint32_t qi = w.qi;
             atomicAdd(&rout.steps[qi], static_cast<unsigned long long>(w.steps));
             if (term == kReached) {
               atomicOr(&rout.reached[qi], 1u);

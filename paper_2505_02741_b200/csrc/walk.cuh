@@ -62,6 +62,10 @@ struct ReachOut {
   uint32_t* reached;
   unsigned long long* steps;
   unsigned long long* best_bits;  // f64 bits of best_estimate
+  // Optional walk-order split: queries [0, *nq_long) sit in slots 0.., the
+  // rest in slots cap-1, cap-2, ... (nq_long null: walk order = slot order).
+  const uint32_t* nq_long;
+  uint32_t cap;
 };
 // Per-query outputs of the min-path walk (RecoveredPath, walk.hpp:35-39).
 struct MinOut {
