@@ -253,8 +253,11 @@ UpdateStream generate_update_stream(const HostGraph& g, const StreamGenOptions& 
         v = static_cast<VertexId>(rng.next_below(n));
       } else {
         // Vertices within `locality` hops of u in BFS discovery order,
-        // u excluded (stream.cpp:90-110).
-        hop.assign(n, std::numeric_limits<std::uint32_t>::max());
+        // u excluded (stream.cpp:90-110). The reference allocates an n-sized
+        // distance array per sample (O(n) each, unusable at C4/C5 with
+        // locality); here one array is reused and only the visited entries
+        // are reset afterwards -- the same BFS, hence the same ball and order.
+        if (hop.size() != n) hop.assign(n, std::numeric_limits<std::uint32_t>::max());
         nearby.clear();
         frontier.clear();
         hop[u] = 0;
@@ -269,6 +272,7 @@ UpdateStream generate_update_stream(const HostGraph& g, const StreamGenOptions& 
             frontier.push_back(nb.id);
           }
         }
+        for (const VertexId x : frontier) hop[x] = std::numeric_limits<std::uint32_t>::max();
         if (nearby.empty()) continue;
         v = nearby[rng.next_below(nearby.size())];
       }
