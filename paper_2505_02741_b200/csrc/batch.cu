@@ -473,6 +473,70 @@ struct CommitOp {
   uint32_t* dec;
   BatchCtl* ctl;
   WalkOpts o;
+  // Keep-shadow deletion commit (k_del_flow, deletion-only batch without an
+  // absent deletion): G stays the walk shadow -- which IS the final G, the
+  // batch's deletions applied in event order -- so the commit neither
+  // restores nor re-deletes G. What a local fallback must read of LIVE G at
+  // event k (the batch-start row minus the row's deletions up to k) comes
+  // from the saved batch-start rows and the shadow's per-row deletion lists.
+  int keep = 0;
+  const uint32_t* save_idx = nullptr;     // vertex -> saved batch-start row
+  const Slab<kCapG>* side_slab = nullptr;
+  const unsigned long long* side_off = nullptr;
+  const uint32_t* side_id = nullptr;
+  const double* side_w = nullptr;
+  const uint32_t* sh_head = nullptr;      // per-row deletion records r = 2k + side
+  const uint32_t* sh_next = nullptr;
+
+  // Entry i of x's batch-start row (keep mode; x is a deletion endpoint).
+  __device__ uint32_t start_deg(uint32_t x) const { return side_slab[save_idx[x]].deg; }
+  __device__ void start_entry(uint32_t x, uint32_t i, uint32_t& id, double& w) const {
+    const uint32_t idx = save_idx[x];
+    const Slab<kCapG>& sl = side_slab[idx];
+    if (sl.ext == kInline) {
+      id = sl.id[i];
+      w = sl.w[i];
+    } else {
+      id = side_id[side_off[idx] + i];
+      w = side_w[side_off[idx] + i];
+    }
+  }
+  // Was (x, y) deleted by an event <= k of this batch?
+  __device__ bool deleted_by(uint32_t x, uint32_t y, uint32_t k) const {
+    for (uint32_t r = sh_head[x]; r != kNoSlot; r = sh_next[r]) {
+      if ((r >> 1) > k) continue;
+      const DevEvent& e = ev[r >> 1];
+      if (((r & 1) ? e.u : e.v) == y) return true;
+    }
+    return false;
+  }
+  // run_local_fallback's view of x at event k (sparsifier.cpp:264-280): the
+  // live degree and the max-weight live neighbour (ties: lowest id).
+  __device__ uint32_t live_best(uint32_t x, uint32_t k, uint32_t& deg, double& bw) const {
+    const uint32_t d = start_deg(x);
+    uint32_t best = kNoVertex;
+    deg = 0;
+    bw = 0.0;
+    for (uint32_t i = 0; i < d; ++i) {
+      uint32_t id;
+      double w;
+      start_entry(x, i, id, w);
+      if (deleted_by(x, id, k)) continue;
+      ++deg;
+      if (best == kNoVertex || w > bw || (w == bw && id < best)) {
+        best = id;
+        bw = w;
+      }
+    }
+    return best;
+  }
+  // Keep mode: an event that can neither recover a path nor fall back
+  // (its edge is not in batch-start H -- promo bit 1 -- and no earlier
+  // fallback can put it there -- promo bit 0) only deletes from G, which the
+  // shadow already did.
+  __device__ bool flow_simple(uint32_t k, const uint8_t* promo, bool keep_g) const {
+    return keep_g && !o.freeze && promo[k] == 0;
+  }
 
   // Events at or past the first failing one never commit (the reference
   // stops there, :525-529). In a deletion-only batch the shadow pass already
@@ -548,7 +612,7 @@ struct CommitOp {
     return s != kNoSlot && mout.has_path[s] != 0;
   }
   template <class F>
-  __device__ uint32_t flow_rows(uint32_t k, uint32_t lane, bool fb, F&& f) const {
+  __device__ uint32_t flow_rows(uint32_t k, uint32_t lane, bool fb, bool keep_g, F&& f) const {
     const DevEvent& e = ev[k];
     const uint32_t* p = nullptr;
     uint32_t n = 2, du = 0, dv = 0;
@@ -558,18 +622,26 @@ struct CommitOp {
         p = path_of(s);
         n += mout.path_len[s];
       } else if (fb) {
-        du = G.slab[e.u].deg;
-        dv = G.slab[e.v].deg;
+        du = keep_g ? start_deg(e.u) : G.slab[e.u].deg;
+        dv = keep_g ? start_deg(e.v) : G.slab[e.v].deg;
         n += du + dv;
       }
     }
     for (uint32_t i = lane; i < n; i += 32) {
       uint32_t r;
-      if (i == 0) r = e.u;
-      else if (i == 1) r = e.v;
-      else if (p) r = p[i - 2];
-      else if (i - 2 < du) r = row(G, e.u).id(i - 2);
-      else r = row(G, e.v).id(i - 2 - du);
+      if (i == 0) {
+        r = e.u;
+      } else if (i == 1) {
+        r = e.v;
+      } else if (p) {
+        r = p[i - 2];
+      } else if (keep_g) {
+        double w;
+        if (i - 2 < du) start_entry(e.u, i - 2, r, w);
+        else start_entry(e.v, i - 2 - du, r, w);
+      } else {
+        r = i - 2 < du ? row(G, e.u).id(i - 2) : row(G, e.v).id(i - 2 - du);
+      }
       f(i, r);
     }
     return n;
@@ -593,7 +665,7 @@ struct CommitOp {
   // path edges' insertions; the appends then go row by row -- row p[j]
   // receives p[j-1] (from edge j-1) before p[j+1] (from edge j), exactly
   // the sequential order.
-  __device__ uint32_t apply_warp(uint32_t k, uint32_t lane, Acc& acc) const {
+  __device__ uint32_t apply_warp(uint32_t k, uint32_t lane, Acc& acc, bool keep_g = false) const {
     constexpr unsigned kAll = 0xFFFFFFFFu;
     const DevEvent e = ev[k];
     if (e.kind == 0) {
@@ -610,12 +682,13 @@ struct CommitOp {
     // row; either row answers the same (rows are symmetric). H is edited only
     // once the G deletion is known to succeed (:491 throws first).
     int found = -1;
-    if (lane < 4) {
+    if (lane < 4 && !(keep_g && lane < 2)) {
       const uint32_t a = (lane & 1) ? v : u, bb = (lane & 1) ? u : v;
       found = lane < 2 ? row_find(G, a, bb) : row_find(H, a, bb);
       if (lane < 2 && found >= 0) row_remove_at(G, a, static_cast<uint32_t>(found));
     }
-    const bool in_g = __shfl_sync(kAll, found, 0) >= 0;
+    // keep mode: the shadow already deleted (u, v) from G, and it existed
+    const bool in_g = keep_g || __shfl_sync(kAll, found, 0) >= 0;
     const bool in_h = __shfl_sync(kAll, found, 2) >= 0;
     if (in_g && in_h && (lane == 2 || lane == 3))
       row_remove_at(H, lane == 2 ? u : v, static_cast<uint32_t>(found));
@@ -687,9 +760,17 @@ struct CommitOp {
       const uint32_t ends[2] = {u, v};
       for (int j = 0; j < 2; ++j) {
         const uint32_t x = ends[j];
-        if (H.slab[x].deg != 0 || G.slab[x].deg == 0) continue;
+        if (H.slab[x].deg != 0) continue;
         double bw = 0.0;
-        const uint32_t b = best_neighbor(G, x, kNoVertex, &bw);
+        uint32_t b;
+        if (keep_g) {  // live G at event k from the batch-start row
+          uint32_t gdeg = 0;
+          b = live_best(x, k, gdeg, bw);
+          if (gdeg == 0) continue;
+        } else {
+          if (G.slab[x].deg == 0) continue;
+          b = best_neighbor(G, x, kNoVertex, &bw);
+        }
         if (insert_edge(H, x, b, bw, acc.dh) < 0) {
           err = kErrPool;
           break;
@@ -826,7 +907,19 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   const uint32_t nw = nth >> 5;
   volatile BatchCtl* ctl = b.ctl;
   stamp_commit_start(b.ctl);
+  // Keep mode: the shadow's per-row deletion lists stay alive for the
+  // live-G reads and are cleared at the end (also on the abort path).
+  auto clear_shadow_lists = [&]() {
+    if (!op.keep) return;
+    for (uint32_t k = tid; k < nev; k += nth) {
+      const DevEvent& e = op.ev[k];
+      if (e.kind != 1 || e.u >= b.n_vertices || e.v >= b.n_vertices) continue;
+      b.fp_head[1][e.u] = kNoSlot;
+      b.fp_head[1][e.v] = kNoSlot;
+    }
+  };
   if (ctl->val_err != ~0ull) {  // uniform
+    clear_shadow_lists();
     if (tid == 0) batch_finish(op.G, op.H, b);
     return;
   }
@@ -835,9 +928,13 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   uint32_t* done = b.fp_cnt[0];
   uint32_t* mark = b.fp_cnt[1];
   if (tid == 0) ctl->fl_t[0] = global_ns();
+  // Keep the walk shadow as the new G when every deletion found its edge
+  // (then the shadow IS the event-order result); otherwise the reference's
+  // partial commit needs batch-start G back (restore, then the full commit).
+  const bool keep = op.keep && ctl->first_absent == 0xFFFFFFFFu;
   // Undo the in-place walk shadow before anything reads G (same pass as the
   // first step of phase 0, which does not read G).
-  restore_rows(op.G, b, tid, nth);
+  if (!keep) restore_rows(op.G, b, tid, nth);
   // Phase 0: which events may run the local fallback. An event whose edge
   // is in batch-start H without a recovered path may. An event whose edge is
   // NOT in batch-start H may only if an earlier fallback inserted its edge
@@ -846,11 +943,15 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   // event's u or v. So: mark the endpoints of fallback-capable events and
   // promote the events touching a marked vertex, to a fixpoint (order-free,
   // hence a superset). Most deletions then list only {u, v}.
+  // promo bit 0: may run the fallback; bit 1: edge in batch-start H.
   if (!op.o.freeze) {
     for (uint32_t k = tid; k < lim; k += nth) {
       const DevEvent& e = op.ev[k];
-      const bool fb = op.slot[k] != kNoSlot && !op.has_path_of(k);
-      b.fl_promo[k] = fb ? 1 : 0;
+      // H is batch-start H until the apply phase. (An event can be in H with
+      // no query: a shadow degree of 0 skips the walk, :448.)
+      const bool in_h = op.slot[k] != kNoSlot || has_edge(op.H, e.u, e.v);
+      const bool fb = in_h && !op.has_path_of(k);
+      b.fl_promo[k] = (fb ? 1 : 0) | (in_h ? 2 : 0);
       if (fb) {
         mark[e.u] = 1;
         mark[e.v] = 1;
@@ -864,7 +965,7 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
     for (uint32_t it = 0;; ++it) {
       if (tid == 0) ctl->fl_changed[(it + 1) % 3] = 0;
       for (uint32_t k = tid; k < lim; k += nth) {
-        if (b.fl_promo[k] || op.slot[k] != kNoSlot) continue;
+        if (b.fl_promo[k]) continue;  // fallback-capable already, or in batch-start H
         const DevEvent& e = op.ev[k];
         if (*reinterpret_cast<volatile uint32_t*>(mark + e.u) ||
             *reinterpret_cast<volatile uint32_t*>(mark + e.v)) {
@@ -889,8 +990,10 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
     const uint32_t passes = (lim + nw - 1) / nw;
     for (uint32_t pass = 0; pass < passes; ++pass) {
       const uint32_t k = pass * nw + wid;
-      const bool fb = k < lim && !op.o.freeze && b.fl_promo[k];
-      const uint32_t n = k < lim ? op.flow_rows(k, lane, fb, [](uint32_t, uint32_t) {}) : 0;
+      const bool fb = k < lim && !op.o.freeze && (b.fl_promo[k] & 1);
+      const bool simple = k < lim && op.flow_simple(k, b.fl_promo, keep);
+      const uint32_t n =
+          (k < lim && !simple) ? op.flow_rows(k, lane, fb, keep, [](uint32_t, uint32_t) {}) : 0;
       if (lane == 0) wcnt[wib] = n;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -917,7 +1020,8 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
         b.fl_base[k] = base;
         b.fl_cnt[k] = n;
       }
-      op.flow_rows(k, lane, fb, [&](uint32_t i, uint32_t r) {
+      if (simple) continue;
+      op.flow_rows(k, lane, fb, keep, [&](uint32_t i, uint32_t r) {
         b.fl_row[base + i] = r;
         b.fl_ev[base + i] = k;
         b.fl_next[base + i] = atomicExch(head + r, base + i);
@@ -974,7 +1078,17 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
         if (!__all_sync(kAll, ready)) continue;
         __threadfence();
         uint32_t e = 0;
-        if ((ctl->commit_err >> 8) > k) e = op.apply_warp(k, lane, acc);
+        if ((ctl->commit_err >> 8) > k) {
+          if (op.flow_simple(k, b.fl_promo, keep)) {  // G: done by the shadow
+            if (lane == 0) {
+              acc.r[kDelSeen] += 1;
+              --acc.dg;
+              op.dec[k] = 0;
+            }
+          } else {
+            e = op.apply_warp(k, lane, acc, keep);
+          }
+        }
         if (lane == 0) {
           b.state[k] = e ? 2 : 1;
           if (e) atomicMin(&b.ctl->commit_err, (static_cast<unsigned long long>(k) << 8) | e);
@@ -1005,15 +1119,20 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
       head[x] = kNoSlot;
       done[x] = 0;
     }
-    if (lane == 0 && b.fl_promo[k]) {
+    if (lane == 0 && (b.fl_promo[k] & 1)) {
       const DevEvent& e = op.ev[k];
       mark[e.u] = 0;
       mark[e.v] = 0;
     }
   }
+  clear_shadow_lists();
   grid.sync();
   if (tid == 0) ctl->fl_t[5] = global_ns();
   if (overflow) {  // record buffer too small: the dependency rounds commit the batch
+    if (keep) {  // they re-apply the deletions: batch-start G first
+      restore_rows(op.G, b, tid, nth);
+      grid.sync();
+    }
     rounds_warp_loop(op, nev, b, grid);
     grid.sync();
   }
@@ -1271,10 +1390,12 @@ __global__ void k_val_link(const DevEvent* __restrict__ ev, uint32_t nb, uint32_
   }
   b.dec[k] = 0;
   if (e.kind != 1) return;
-  const uint32_t hu = atomicExch(b.fp_head[0] + e.u, 2 * k);
-  const uint32_t hv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
-  b.fp_next[0][2 * k] = hu;
-  b.fp_next[0][2 * k + 1] = hv;
+  // Lists in slot [1]: the flow commit may keep them alive (fp_head[0] is
+  // its own record list head).
+  const uint32_t hu = atomicExch(b.fp_head[1] + e.u, 2 * k);
+  const uint32_t hv = atomicExch(b.fp_head[1] + e.v, 2 * k + 1);
+  b.fp_next[1][2 * k] = hu;
+  b.fp_next[1][2 * k + 1] = hv;
 }
 
 __global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t seed,
@@ -1368,23 +1489,24 @@ __global__ void k_sh_link(const DevEvent* __restrict__ ev, uint32_t nb, BatchDev
 }
 
 __global__ void k_sh_apply(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, uint32_t nb,
-                           uint32_t n, BatchDev b) {
+                           uint32_t n, BatchDev b, int list, int keep_lists) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= 2 * nb) return;
   const DevEvent& e = ev[r >> 1];
   if (e.kind != 1 || e.u >= n || e.v >= n || e.u == e.v) return;  // never linked
   const uint32_t row = (r & 1) ? e.v : e.u;
-  uint32_t* head = b.fp_head[0];
+  uint32_t* head = b.fp_head[list];
   if (batch_aborted(b.ctl)) {  // linked before validation finished: just clear
     if (head[row] == r) head[row] = kNoSlot;
     return;
   }
   asm volatile("prefetch.global.L2 [%0];" ::"l"(G.slab + row));
-  const uint32_t* next = b.fp_next[0];
+  const uint32_t* next = b.fp_next[list];
   if (head[row] != r) return;
   // Save the row (the owner is its only writer in this pass).
   const uint32_t idx = atomicAdd(&b.ctl->n_saved, 1u);
   b.saved_rows[idx] = row;
+  b.save_idx[row] = idx;
   const Slab<kCapG> sl = G.slab[row];
   b.side_slab[idx] = sl;
   if (sl.ext != kInline) {
@@ -1409,7 +1531,8 @@ __global__ void k_sh_apply(DevGraph<kCapG> G, const DevEvent* __restrict__ ev, u
     else row_remove_at(G, row, static_cast<uint32_t>(i));
     last = best;
   }
-  head[row] = kNoSlot;
+  // The flow commit keeps the lists for its live-G reads and clears them.
+  if (!keep_lists) head[row] = kNoSlot;
 }
 
 
@@ -1632,6 +1755,12 @@ int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned i
   return 1;
 }
 
+// The deletion-only commit keeps the walk shadow as G (k_del_flow keep mode):
+// needs the single-pass path's kept per-row deletion lists.
+bool keep_shadow_commit(const WalkOpts& o, uint32_t nb, uint32_t n_del) {
+  return n_del == nb && o.keep_shadow && o.single_pass && o.shadow_lists && o.flow;
+}
+
 int launch_prepare(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& b, uint32_t nb,
                    uint32_t n_del, uint32_t n, uint32_t stamp, const WalkOpts& o,
                    cudaStream_t st) {
@@ -1643,7 +1772,8 @@ int launch_prepare(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   }
   if (o.single_pass && n_del == nb && o.shadow_lists) {
     k_val_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, n, b);
-    k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, n, b);
+    k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, n, b, 1,
+                                                    keep_shadow_commit(o, nb, n_del) ? 1 : 0);
     k_prep<true><<<tiles, 256, 0, st>>>(H, G, b.events, nb, n, o, b);
     return 3;
   }
@@ -1661,7 +1791,7 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
   if (n_del > 0) {
     if (o.shadow_lists) {
       k_sh_link<<<grid_for(nb), 256, 0, st>>>(b.events, nb, b);
-      k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, G.n, b);
+      k_sh_apply<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, G.n, b, 0, 0);
       l += 2;
     } else {
       k_save_rows<<<grid_for(2ull * nb), 256, 0, st>>>(G, b.events, nb, stamp, b);
@@ -1689,6 +1819,16 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
   if (n_del == 0) return launch_rounds<false>(op, nb, b, st);
   if (n_del == nb && o.flow) {
     CommitOp op_copy = op;
+    if (keep_shadow_commit(o, nb, n_del)) {
+      op_copy.keep = 1;
+      op_copy.save_idx = b.save_idx;
+      op_copy.side_slab = b.side_slab;
+      op_copy.side_off = b.side_off;
+      op_copy.side_id = b.side_id;
+      op_copy.side_w = b.side_w;
+      op_copy.sh_head = b.fp_head[1];
+      op_copy.sh_next = b.fp_next[1];
+    }
     BatchDev b_copy = b;
     uint32_t nev = nb;
     void* args[] = {&op_copy, &nev, &b_copy};

@@ -113,7 +113,7 @@ struct WalkOpts {
   int single_pass;   // single-pass prepare      (DYG_SINGLE_PASS=0 disables)
   int shadow_lists;  // per-row shadow lists     (DYG_SHADOW_ROUNDS=1 disables)
   int flow;          // dataflow deletion commit (DYG_COMMIT_ROUNDS=1 disables)
-  int pad_opts;
+  int keep_shadow;   // deletion-only batches keep the walk shadow as G (DYG_KEEP_SHADOW=0 disables)
   // Reach walk order (insertion-only, single-GPU batches): queries whose
   // w_pq <= split_wpq (the budget lets them walk longest) get the low slots and
   // are walked first, the rest take slots from the top of the buffer; 0 = off.
@@ -152,6 +152,8 @@ struct BatchDev {
   // {aggregate, inclusive, epoch << 2 | state}; state 1 = aggregate, 2 = inclusive.
   unsigned long long* tile_state;
   uint32_t q_cap;            // query slot capacity (reach slots are < q_cap)
+  uint32_t n_vertices;
+  uint32_t* save_idx;        // per vertex: index of its saved batch-start G row
   void* cub_temp;
   size_t cub_temp_bytes;
   // Insertion fast path ([0] = G, [1] = H): per-vertex append counts and

@@ -175,6 +175,7 @@ struct dyg_session {
   bool flow = true;                // DYG_COMMIT_ROUNDS=1: round-engine deletion commit
   uint64_t flow_cap = 0;           // DYG_FLOW_CAP: flow record capacity (test knob)
   bool reach_split = true;         // DYG_REACH_SPLIT=0: reach walks in slot order
+  bool keep_shadow = true;         // DYG_KEEP_SHADOW=0: deletion commit restores G
   double mean_inv_w = 1.0;         // mean 1/w over G's edges (session creation)
 };
 
@@ -334,7 +335,7 @@ WalkOpts walk_opts(const dyg_session* s) {
   // the budget K / w_pq allows >= 0.8 T steps when w_pq <= K / (0.8 T E[1/w]).
   o.split_wpq = (s->reach_split && o.filtering && o.T > 0)
                     ? o.K / (0.8 * static_cast<double>(o.T) * s->mean_inv_w) : 0.0;
-  o.pad_opts = 0;
+  o.keep_shadow = s->keep_shadow ? 1 : 0;
   return o;
 }
 
@@ -1203,6 +1204,7 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->shadow_lists = !env_is("DYG_SHADOW_ROUNDS", 1);
       s->flow = !env_is("DYG_COMMIT_ROUNDS", 1);
       s->reach_split = !env_is("DYG_REACH_SPLIT", 0);
+      s->keep_shadow = !env_is("DYG_KEEP_SHADOW", 0);
       if (const char* e = std::getenv("DYG_FLOW_CAP")) s->flow_cap = std::strtoull(e, nullptr, 10);
       {
         const char* e = std::getenv("DYG_GRAPHS");
@@ -1239,6 +1241,8 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       }
       check(cudaMemset(s->b.mark, 0, sizeof(uint32_t) * s->n), "row marks");
       dev_alloc(&s->b.fl_depth, s->n, "flow depths");
+      dev_alloc(&s->b.save_idx, s->n, "saved-row index");
+      s->b.n_vertices = s->n;
       check(cudaMemset(s->b.fl_depth, 0, sizeof(uint32_t) * s->n), "flow depths");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
       dev_alloc(&s->b.ctl, 1, "batch ctl");
@@ -1302,6 +1306,7 @@ void dyg_session_destroy(dyg_session* s) {
     dev_free(s->b.fp_head[i]);
   }
   dev_free(s->b.fl_depth);
+  dev_free(s->b.save_idx);
   dev_free(s->b.side_id);
   dev_free(s->b.side_w);
   dev_free(s->d_stream);
