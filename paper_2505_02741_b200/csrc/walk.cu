@@ -52,79 +52,78 @@ __device__ __forceinline__ void cp_async16(uint4* dst, const void* src, uint32_t
                : "memory");
 }
 
-// One sample_neighbor call (walk.cpp:17-37) at `cur` on the gathered slab
-// head, given this step's uniform draw u01. The reference's pass 1 sums
-// candidate weights in row order and its pass 2 re-accumulates the same
-// running sums until target < cumulative; both passes produce the identical
-// sequence of partial sums, so they are computed ONCE (prefix[i]) and pass 2
-// becomes independent compares -- bit-identical, with half the dependent
-// fp64 adds. Rounding fallback = the last candidate. Returns false on a
-// dead end. H rows with more than 4 entries fetch the slab tail here.
+// Entries of a row as 16 B chunks: H entries end at byte 96 whatever the
+// slab padding.
 template <int C>
-__device__ __forceinline__ bool walk_step(const DevGraph<C>& g, const uint4* head, uint32_t cur,
-                                          uint32_t prev, double u01, uint32_t& next, double& ew,
-                                          uint32_t& deg) {
-  // 16 B chunks holding the row: H entries end at byte 96 whatever the slab
-  // padding.
-  constexpr int NV = C == kCapH ? 6 : static_cast<int>(sizeof(Slab<C>) / 16);
-  constexpr int NH = Gather<C>::kChunks;
+struct RowRegs {
+  static constexpr int kChunks = C == kCapH ? 6 : static_cast<int>(sizeof(Slab<C>) / 16);
   union {
     uint4 v[sizeof(Slab<C>) / 16];
     Slab<C> s;
-  } r;
+  };
+};
+
+// sample_neighbor (walk.cpp:17-37) on an inline row held in registers,
+// given this step's uniform draw u01. The reference's pass 1 sums candidate
+// weights in row order and its pass 2 re-accumulates the same running sums
+// until target < cumulative; both passes produce the identical sequence of
+// partial sums, so they are computed ONCE (prefix[i]) and pass 2 becomes
+// independent compares -- bit-identical, with half the dependent fp64 adds.
+// Candidate weights are pre-masked (non-candidates add +0.0, an exact no-op:
+// weights are positive finite, graph.cpp:71), so the chain is DADD after
+// DADD. The prefix is then non-decreasing, so {i : target < prefix[i]} is a
+// suffix whose first index is a candidate (its prefix rose there): the pick
+// is C - popc(hit). None -> the rounding fallback, the last candidate.
+// Returns false on a dead end.
+template <int C>
+__device__ __forceinline__ bool sample_inline(const Slab<C>& s, uint32_t prev, double u01,
+                                              uint32_t& next, double& ew) {
+  const uint32_t deg = s.deg;
+  const uint32_t live = (1u << deg) - 1u;  // deg <= C < 32
+  uint32_t cand = 0;
+  double prefix[C];
+  double total = 0.0;
 #pragma unroll
-  for (int i = 0; i < NH; ++i) r.v[i] = head[i];  // shared-memory reads (LDS.128)
-  deg = r.s.deg;
-  if (r.s.ext == kInline) {
-    if (NH < NV && deg > 4) {
-      const uint4* src = reinterpret_cast<const uint4*>(g.slab + cur);
-#pragma unroll
-      for (int i = NH; i < NV; ++i) r.v[i] = __ldg(src + i);
-    }
-    // Candidate weights pre-masked (non-candidates contribute +0.0, an exact
-    // no-op: weights are positive finite, graph.cpp:71), so the dependent
-    // chain is DADD after DADD with no select in between.
-    uint32_t cand = 0;  // bit i: entry i is a candidate (exists, is not `prev`)
-    double wm[C];
-#pragma unroll
-    for (int i = 0; i < C; ++i) {
-      const bool c = i < static_cast<int>(deg) && r.s.idr(i) != prev;
-      wm[i] = c ? r.s.wr(i) : 0.0;
-      cand |= static_cast<uint32_t>(c) << i;
-    }
-    double prefix[C];
-    double total = 0.0;
-#pragma unroll
-    for (int i = 0; i < C; ++i) {
-      total = __dadd_rn(total, wm[i]);
-      prefix[i] = total;
-    }
-    if (total <= 0.0) return false;
-    const double target = __dmul_rn(u01, total);
-    // The reference picks the first candidate whose running sum exceeds
-    // target: that is the lowest set bit of `hit` (whatever the rounding of
-    // the sums); none -> the rounding fallback, the last candidate.
-    uint32_t hit = 0;
-#pragma unroll
-    for (int i = 0; i < C; ++i)
-      if (target < prefix[i]) hit |= 1u << i;
-    hit &= cand;
-    const int sel = hit ? __ffs(hit) - 1 : 31 - __clz(cand);
-    uint32_t id_sel = r.s.idr(0);
-    double w_sel = r.s.wr(0);
-#pragma unroll
-    for (int i = 1; i < C; ++i) {
-      if (sel == i) {
-        id_sel = r.s.idr(i);
-        w_sel = r.s.wr(i);
-      }
-    }
-    next = id_sel;
-    ew = w_sel;
-    return true;
+  for (int i = 0; i < C; ++i) {
+    const uint32_t id = const_cast<Slab<C>&>(s).idr(i);
+    const bool c = ((live >> i) & 1u) && id != prev;
+    cand |= static_cast<uint32_t>(c) << i;
+    total = __dadd_rn(total, c ? const_cast<Slab<C>&>(s).wr(i) : 0.0);
+    prefix[i] = total;
   }
-  const uint32_t* ids = g.pool_id + r.s.ext;
-  const double* ws = g.pool_w + r.s.ext;
+  if (total <= 0.0) return false;
+  const double target = __dmul_rn(u01, total);
+  uint32_t hit = 0;
+#pragma unroll
+  for (int i = 0; i < C; ++i) hit |= static_cast<uint32_t>(target < prefix[i]) << i;
+  const uint32_t sel = hit ? static_cast<uint32_t>(C - __popc(hit)) : 31u - __clz(cand);
+  // Select entry `sel` by a mux tree (depth log2 C, not a chain of C moves).
+  uint32_t ids[C];
+  double ws[C];
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    ids[i] = const_cast<Slab<C>&>(s).idr(i);
+    ws[i] = const_cast<Slab<C>&>(s).wr(i);
+  }
+#pragma unroll
+  for (int st = 1; st < C; st <<= 1) {
+    const bool up = (sel & static_cast<uint32_t>(st)) != 0;
+#pragma unroll
+    for (int i = 0; i + st < C; i += 2 * st) {
+      ids[i] = up ? ids[i + st] : ids[i];
+      ws[i] = up ? ws[i + st] : ws[i];
+    }
+  }
+  next = ids[0];
+  ew = ws[0];
+  return true;
+}
+
+// sample_neighbor on an overflow-pool row (rows longer than the slab).
+__device__ __forceinline__ bool sample_pool(const uint32_t* __restrict__ ids,
+                                            const double* __restrict__ ws, uint32_t deg,
+                                            uint32_t prev, double u01, uint32_t& next,
+                                            double& ew) {
   double total = 0.0;
   for (uint32_t i = 0; i < deg; ++i)
     if (__ldg(ids + i) != prev) total = __dadd_rn(total, __ldg(ws + i));
@@ -141,6 +140,37 @@ __device__ __forceinline__ bool walk_step(const DevGraph<C>& g, const uint4* hea
     if (target < cum) break;
   }
   return true;
+}
+
+// One step at `cur` on the gathered slab head (shared memory). H rows with
+// more than 4 entries fetch the slab tail here.
+template <int C>
+__device__ __forceinline__ bool walk_step(const DevGraph<C>& g, const uint4* head, uint32_t cur,
+                                          uint32_t prev, double u01, uint32_t& next, double& ew,
+                                          uint32_t& deg) {
+  constexpr int NV = RowRegs<C>::kChunks;
+  constexpr int NH = Gather<C>::kChunks;
+  RowRegs<C> r;
+#pragma unroll
+  for (int i = 0; i < NH; ++i) r.v[i] = head[i];  // shared-memory reads (LDS.128)
+  deg = r.s.deg;
+  if (r.s.ext == kInline) {
+    if (NH < NV && deg > 4) {
+      const uint4* src = reinterpret_cast<const uint4*>(g.slab + cur);
+#pragma unroll
+      for (int i = NH; i < NV; ++i) r.v[i] = __ldg(src + i);
+    }
+    return sample_inline<C>(r.s, prev, u01, next, ew);
+  }
+  return sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, prev, u01, next, ew);
+}
+
+// The whole row of `x` straight into registers (the tail loop).
+template <int C>
+__device__ __forceinline__ void load_row(const DevGraph<C>& g, uint32_t x, RowRegs<C>& r) {
+  const uint4* src = reinterpret_cast<const uint4*>(g.slab + x);
+#pragma unroll
+  for (int i = 0; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
 }
 
 // Uniform draw from the SplitMix64 counter (rng.hpp:7-24): `ctr` already
@@ -321,6 +351,55 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     }
   };
   auto row_of = [&](const Slot& w) { return (w.has && w.steps < P.T) ? w.cur : kNoVertex; };
+  // A walker ended with `term`: its outputs (walk.cpp:82-98 / :119-134).
+  auto finish = [&](Slot& w, uint32_t term) {
+    my_steps += w.steps;
+    if (kMinPath) {
+      // The trace's last, partial sector: entries steps-r+1 .. steps.
+      const uint32_t r = (w.steps + 1) & 7u;
+      uint32_t* tr = S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T);
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (static_cast<uint32_t>(j) <= r) tr[w.steps + 1 - j] = w.tb[8 - j];
+      S.acc[w.widx] = w.acc;
+      S.term[w.widx] = term;
+      S.steps[w.widx] = w.steps;
+    } else {
+      const uint32_t qi = w.qi;
+      atomicAdd(&rout.steps[qi], static_cast<unsigned long long>(w.steps));
+      if (term == kReached) {
+        atomicOr(&rout.reached[qi], 1u);
+        atomicMin(&rout.best_bits[qi],
+                  static_cast<unsigned long long>(__double_as_longlong(w.acc)));
+      }
+    }
+    w.has = false;
+  };
+  // A traversed edge (next, ew): accumulate, trace, and the budget / target
+  // / cap checks in single_walk's order (walk.cpp:62-76).
+  auto advance = [&](Slot& w, uint32_t next, double ew) -> uint32_t {
+    w.acc = __dadd_rn(w.acc, __drcp_rn(ew));
+    ++w.steps;
+    w.prev = w.cur;
+    w.cur = next;
+    if (kMinPath) {
+      // Trace entry `steps`; every 8th entry completes a 32 B sector,
+      // written whole.
+#pragma unroll
+      for (int j = 0; j < 7; ++j) w.tb[j] = w.tb[j + 1];
+      w.tb[7] = next;
+      if ((w.steps & 7u) == 7u) {
+        uint4* dst = reinterpret_cast<uint4*>(
+            S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T) + (w.steps - 7));
+        dst[0] = make_uint4(w.tb[0], w.tb[1], w.tb[2], w.tb[3]);
+        dst[1] = make_uint4(w.tb[4], w.tb[5], w.tb[6], w.tb[7]);
+      }
+    }
+    if (__dmul_rn(w.wpq, w.acc) > P.K) return kBudget;
+    if (next == w.tgt) return kReached;
+    if (w.steps >= P.T) return kStepCap;
+    return 0xFFFFFFFFu;
+  };
 
   Slot sl[NS];
 #pragma unroll
@@ -330,6 +409,17 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     issue_rows(g, row_of(sl[k]), stage0 + k * Gather<C>::kWarpWords);
   }
   for (;;) {
+    // Thin tail (P.early == 2, one slot): the queue is drained, so no lane
+    // takes new work, and at most P.tail_lanes walkers are left in the warp.
+    // Every lane then runs its walker to the end on its own, loading whole
+    // rows straight into registers and requesting the next row right after
+    // sampling -- no warp-wide gather, shuffles or shared staging on the
+    // dependent chain. (With many live lanes the cooperative gather stays:
+    // lane-private row loads cost one L1 wavefront per 16 B chunk.)
+    if (NS == 1 && drained && P.early == 2 &&
+        static_cast<uint32_t>(__popc(__ballot_sync(kFull, sl[0].has))) <=
+            (kMinPath ? P.tail_min : P.tail_reach))
+      break;
     bool any = false;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -370,55 +460,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         issue_rows(g, cont ? next : kNoVertex, stage);
       }
       if (w.has) {
-        if (term == 0xFFFFFFFFu) {
-          w.acc = __dadd_rn(w.acc, __drcp_rn(ew));
-          ++w.steps;
-          w.prev = w.cur;
-          w.cur = next;
-          if (kMinPath) {
-            // Trace entry `steps`; every 8th entry completes a 32 B sector,
-            // written whole.
-#pragma unroll
-            for (int j = 0; j < 7; ++j) w.tb[j] = w.tb[j + 1];
-            w.tb[7] = next;
-            if ((w.steps & 7u) == 7u) {
-              uint4* dst = reinterpret_cast<uint4*>(
-                  S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T) + (w.steps - 7));
-              dst[0] = make_uint4(w.tb[0], w.tb[1], w.tb[2], w.tb[3]);
-              dst[1] = make_uint4(w.tb[4], w.tb[5], w.tb[6], w.tb[7]);
-            }
-          }
-          if (__dmul_rn(w.wpq, w.acc) > P.K) {
-            term = kBudget;
-          } else if (next == w.tgt) {
-            term = kReached;
-          } else if (w.steps >= P.T) {
-            term = kStepCap;
-          }
-        }
-        if (term != 0xFFFFFFFFu) {
-          my_steps += w.steps;
-          if (kMinPath) {
-            // The trace's last, partial sector: entries steps-r+1 .. steps.
-            const uint32_t r = (w.steps + 1) & 7u;
-            uint32_t* tr = S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T);
-#pragma unroll
-            for (int j = 1; j < 8; ++j)
-              if (static_cast<uint32_t>(j) <= r) tr[w.steps + 1 - j] = w.tb[8 - j];
-            S.acc[w.widx] = w.acc;
-            S.term[w.widx] = term;
-            S.steps[w.widx] = w.steps;
-          } else {
-            const uint32_t qi = w.qi;
-            atomicAdd(&rout.steps[qi], static_cast<unsigned long long>(w.steps));
-            if (term == kReached) {
-              atomicOr(&rout.reached[qi], 1u);
-              atomicMin(&rout.best_bits[qi],
-                        static_cast<unsigned long long>(__double_as_longlong(w.acc)));
-            }
-          }
-          w.has = false;
-        }
+        if (term == 0xFFFFFFFFu) term = advance(w, next, ew);
+        if (term != 0xFFFFFFFFu) finish(w, term);
       }
       if (!early) {
         __syncwarp();  // every lane has read its staged row before the slot is refilled
@@ -428,6 +471,50 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       any |= w.has;
     }
     if (!__any_sync(kFull, any)) break;
+  }
+  if (NS == 1 && __any_sync(kFull, sl[0].has)) {  // the thin-tail exit above
+    cp_async_wait<0>();
+    __syncwarp();
+    Slot& w = sl[0];
+    if (w.has) {
+      RowRegs<C> r;
+      if (w.steps < P.T) {  // its current row is staged (head chunks)
+        const uint4* st = stage0 + lane * Gather<C>::kStride;
+#pragma unroll
+        for (int i = 0; i < Gather<C>::kChunks; ++i) r.v[i] = st[i];
+        const uint4* src = reinterpret_cast<const uint4*>(g.slab + w.cur);
+#pragma unroll
+        for (int i = Gather<C>::kChunks; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
+      }
+      double u = u01_of(w.rng + kGamma);
+      for (;;) {
+        uint32_t term = 0xFFFFFFFFu;
+        uint32_t next = kNoVertex;
+        double ew = 0.0;
+        if (w.steps >= P.T) {
+          term = kStepCap;
+        } else {
+          w.rng += kGamma;
+          const uint32_t deg = r.s.deg;
+          const bool ok =
+              r.s.ext == kInline
+                  ? sample_inline<C>(r.s, w.prev, u, next, ew)
+                  : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next, ew);
+          my_bytes += step_bytes(deg);
+          if (!ok) term = kDeadEnd;
+        }
+        if (term == 0xFFFFFFFFu) {
+          if (next != w.tgt && w.steps + 1 < P.T) load_row<C>(g, next, r);
+          u = u01_of(w.rng + kGamma);  // the next draw, while the row is in flight
+          term = advance(w, next, ew);
+        }
+        if (term != 0xFFFFFFFFu) {
+          finish(w, term);
+          break;
+        }
+      }
+    }
+    __syncwarp();
   }
   cp_async_wait<0>();
   add_counters(ctr, my_steps, my_bytes);

@@ -24,7 +24,9 @@ struct WalkParams {
   uint32_t s;        // walkers per query
   uint64_t seed;     // global seed
   uint32_t s_shift;  // log2(s) when s is a power of two, else kNoShift
-  uint32_t early;    // tail mode: request the next row right after sampling
+  uint32_t early;    // tail: 1 = request the next row right after sampling, 2 = + per-lane loop
+  uint32_t tail_reach;  // early == 2: a drained warp with at most this many live
+  uint32_t tail_min;    // walkers (reach / min-path kernel) goes per-lane
 };
 
 inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t seed) {
@@ -35,9 +37,17 @@ inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t se
   }
   static const uint32_t early = [] {
     const char* e = std::getenv("DYG_WALK_EARLY");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 1u;
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 2u;
   }();
-  return WalkParams{K, T, s, seed, sh, early};
+  static const uint32_t tail_reach = [] {
+    const char* e = std::getenv("DYG_TAIL_LANES");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 32u;
+  }();
+  static const uint32_t tail_min = [] {
+    const char* e = std::getenv("DYG_TAIL_LANES_MIN");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 16u;
+  }();
+  return WalkParams{K, T, s, seed, sh, early, tail_reach, tail_min};
 }
 
 // Entries per raw min-path trace: T + 1 rounded up to whole 32 B sectors, so
