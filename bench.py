@@ -458,6 +458,9 @@ def run_ours(args):
             for k in ("promote", "emit", "rank", "apply", "reset")},
         "walk_tail_ms_per_step": {"reach": stats["reach_tail_ms"] / args.steps,
                                   "minpath": stats["minpath_tail_ms"] / args.steps},
+        "gaps_ms_per_step": {"prep": stats["prep_ms"] / args.steps,
+                             "walk_to_commit": stats["walk_commit_gap_ms"] / args.steps,
+                             "between_batches": stats["batch_gap_ms"] / args.steps},
         "clocks": clocks.summary(),
     }
     del launches

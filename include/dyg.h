@@ -150,6 +150,9 @@ typedef struct dyg_stats {
   double flow_ms_apply;
   double flow_ms_reset;
   uint64_t graph_launches;      /* CUDA-graph replays (one per batch or per range) */
+  double prep_ms;               /* batch start -> first walk warp (validation, query build) */
+  double walk_commit_gap_ms;    /* last walk warp -> commit start */
+  double batch_gap_ms;          /* previous batch end -> batch start, inside one replay */
 } dyg_stats;
 
 typedef struct dyg_session dyg_session;

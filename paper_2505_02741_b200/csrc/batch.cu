@@ -69,21 +69,42 @@ __device__ __forceinline__ unsigned long long warp_max(unsigned long long x) {
   }
   return x;
 }
+// Report counters and |E| deltas of a whole block: warp totals, then one
+// atomic per field and BLOCK (per-warp atomics on these few addresses
+// serialise in L2: ~5k warps x 6 fields per deletion commit). Every thread
+// of the block must call it.
 __device__ __forceinline__ void flush_acc(const Acc& a, BatchCtl* ctl, unsigned long long* g_edges,
                                           unsigned long long* h_edges) {
-  const bool lead = (threadIdx.x & 31) == 0;
+  constexpr int kF = kReportFields + 2;
+  __shared__ unsigned long long s_acc[kF][32];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int f = 0; f < kReportFields; ++f) {
     const unsigned long long v = f == kMaxEventSteps ? warp_max(a.r[f]) : warp_sum(a.r[f]);
-    if (lead && v) {
-      if (f == kMaxEventSteps) atomicMax(&ctl->report[f], v);
-      else atomicAdd(&ctl->report[f], v);
-    }
+    if (lane == 0) s_acc[f][wid] = v;
   }
   const unsigned long long dg = warp_sum(static_cast<unsigned long long>(a.dg));
   const unsigned long long dh = warp_sum(static_cast<unsigned long long>(a.dh));
-  if (lead && dg && g_edges) atomicAdd(g_edges, dg);
-  if (lead && dh && h_edges) atomicAdd(h_edges, dh);
+  if (lane == 0) {
+    s_acc[kReportFields][wid] = dg;
+    s_acc[kReportFields + 1][wid] = dh;
+  }
+  __syncthreads();
+  if (threadIdx.x < static_cast<uint32_t>(kF)) {
+    const int f = static_cast<int>(threadIdx.x);
+    unsigned long long v = 0;
+    for (uint32_t w = 0; w < nw; ++w) {
+      const unsigned long long x = s_acc[f][w];
+      v = f == kMaxEventSteps ? (x > v ? x : v) : v + x;
+    }
+    if (v) {
+      if (f == kMaxEventSteps) atomicMax(&ctl->report[f], v);
+      else if (f < kReportFields) atomicAdd(&ctl->report[f], v);
+      else if (f == kReportFields && g_edges) atomicAdd(g_edges, v);
+      else if (f == kReportFields + 1 && h_edges) atomicAdd(h_edges, v);
+    }
+  }
+  __syncthreads();  // s_acc may be reused by a later call
 }
 
 // Insertion fast path. In an insertion-only batch where every key is new to
@@ -130,7 +151,8 @@ __global__ void k_fp_check(const DevEvent* __restrict__ ev, uint32_t n, BatchDev
 // minimum selection over the short list -- and empties the list head.
 template <int C, class Take>
 __device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* ev, uint32_t* head,
-                                         const uint32_t* next, uint32_t r, bool write, Take take) {
+                                         const uint32_t* next, uint32_t r, bool write, Take take,
+                                         bool reset) {
   const uint32_t row = rec_row(ev, r);
   // The row's slab is needed by the head's append: request it alongside the
   // list lookups.
@@ -154,7 +176,7 @@ __device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* e
       }
     }
   }
-  head[row] = kNoSlot;
+  if (reset) head[row] = kNoSlot;
   return ok;
 }
 
@@ -214,43 +236,102 @@ __global__ void k_fp_write_g(DevGraph<kCapG> G, const DevEvent* __restrict__ ev,
   if (r >= n) return;
   // An invalid batch or a violated precondition: only empty the lists.
   const bool write = !batch_aborted(b.ctl) && !b.ctl->not_simple;
-  if (!fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write, [](uint32_t) { return true; }))
+  // The H pass (k_fp_write_h, after the walk) reads the same lists and
+  // empties them.
+  if (!fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write, [](uint32_t) { return true; },
+                /*reset=*/false))
     atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
 }
 
-// After the reach walk: H appends of the kept records, and each event's
-// decision and report counters (record 2k does event k's accounting).
-__global__ void k_fp_write_h(DevGraph<kCapH> H, const DevEvent* __restrict__ ev, uint32_t n,
+// After the reach walk: H appends of the kept records and each event's
+// decision and report counters, one thread per EVENT: its keep decision is
+// read once for both records, and the two rows' list heads, slabs and appends
+// are independent requests in flight together.
+__global__ void k_fp_write_h(DevGraph<kCapH> H, const DevEvent* __restrict__ ev, uint32_t nb,
                              WalkOpts o, BatchDev b) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   stamp_commit_start(b.ctl);
-  const bool write = r < n && !batch_aborted(b.ctl) && !b.ctl->not_simple;
+  const bool write = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
   unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
-  if (r < n) {
-    if (write && (r & 1) == 0) {
+  if (k < nb) {
+    const DevEvent e = ev[k];
+    uint32_t* head = b.fp_head[0];  // the lists k_fp_write_g walked
+    const uint32_t* next = b.fp_next[0];
+    const uint32_t rows[2] = {e.u, e.v};
+    if (write) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(H.slab + rows[0]));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(H.slab + rows[1]));
+    }
+    const uint32_t h[2] = {head[rows[0]], head[rows[1]]};
+    bool kept = false;
+    if (write) {
       bool have;
-      const bool kept = event_kept(b, o, r >> 1, have, steps);
-      b.dec[r >> 1] = kept ? 0u : 1u;
+      kept = event_kept(b, o, k, have, steps);
+      b.dec[k] = kept ? 0u : 1u;
       (kept ? kept_n : pruned_n) = 1;
     }
     auto take = [&](uint32_t x) {
+      if ((x >> 1) == k) return kept;
       bool have;
       unsigned long long st;
       return event_kept(b, o, x >> 1, have, st);
     };
-    if (!fp_apply(H, ev, b.fp_head[1], b.fp_next[1], r, write, take))
-      atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
+    bool ok = true;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const uint32_t r = 2 * k + side;
+      if (h[side] != r) continue;  // not the list head of its row
+      const uint32_t row = rows[side];
+      if (write) {
+        const uint32_t nx = next[r];
+        if (nx == kNoSlot) {
+          if (kept) ok = ok && row_push(H, row, rows[side ^ 1], e.weight);
+        } else {  // the row's records in increasing r
+          uint32_t last = 0;
+          for (bool first = true; ok; first = false) {
+            uint32_t best = kNoSlot;
+            for (uint32_t x = r; x != kNoSlot; x = next[x])
+              if ((first || x > last) && x < best) best = x;
+            if (best == kNoSlot) break;
+            if (take(best)) ok = row_push(H, row, other_end(ev, best), ev[best >> 1].weight);
+            last = best;
+          }
+        }
+      }
+      head[row] = kNoSlot;
+    }
+    if (!ok) atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
   }
+  // Block totals, then one atomic per field and block: per-warp atomics on
+  // these five addresses serialise in L2 (~18k per C5 batch).
+  __shared__ unsigned long long s_red[4][8];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   kept_n = warp_sum(kept_n);
   pruned_n = warp_sum(pruned_n);
   const unsigned long long steps_sum = warp_sum(steps);
   const unsigned long long steps_max = warp_max(steps);
-  if ((threadIdx.x & 31) == 0 && (kept_n | pruned_n)) {
-    atomicAdd(&b.ctl->fp_report[kInsSeen], kept_n + pruned_n);
-    atomicAdd(&b.ctl->fp_report[kInsKept], kept_n);
-    atomicAdd(&b.ctl->fp_report[kInsPruned], pruned_n);
-    atomicAdd(&b.ctl->fp_report[kWalkerSteps], steps_sum);
-    atomicMax(&b.ctl->fp_report[kMaxEventSteps], steps_max);
+  if (lane == 0) {
+    s_red[0][wid] = kept_n;
+    s_red[1][wid] = pruned_n;
+    s_red[2][wid] = steps_sum;
+    s_red[3][wid] = steps_max;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long k = 0, p = 0, st = 0, m = 0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+      k += s_red[0][w];
+      p += s_red[1][w];
+      st += s_red[2][w];
+      m = m > s_red[3][w] ? m : s_red[3][w];
+    }
+    if (k | p) {
+      atomicAdd(&b.ctl->fp_report[kInsSeen], k + p);
+      atomicAdd(&b.ctl->fp_report[kInsKept], k);
+      atomicAdd(&b.ctl->fp_report[kInsPruned], p);
+      atomicAdd(&b.ctl->fp_report[kWalkerSteps], st);
+      atomicMax(&b.ctl->fp_report[kMaxEventSteps], m);
+    }
   }
 }
 
@@ -273,6 +354,7 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
   }
   if constexpr (Op::kCommit) {
     if (ctl->fast && !ctl->not_simple) {  // k_fp_write committed the batch
+      if (tid == 0) ctl->fl_t[0] = global_ns();  // (timeline only)
       if (tid == 0) batch_finish(op.G, op.H, b);
       return;
     }
@@ -1228,48 +1310,37 @@ __device__ __forceinline__ void scatter_event(const DevEvent& e, uint32_t k, uns
   b.slot[k] = s;
 }
 
-// Exclusive prefix of this tile's aggregate over all earlier tiles, by one
-// warp (decoupled look-back, 32 predecessors per step). Per tile:
-// {aggregate, inclusive prefix, epoch << 2 | state} -- separate words for the
-// two values, so a reader that saw state 1 never reads a value the owner
-// rewrote afterwards.
-__device__ unsigned long long tile_lookback(const BatchDev& b, uint32_t tile,
-                                            unsigned long long agg, uint32_t lane) {
-  constexpr unsigned kAll = 0xFFFFFFFFu;
+// Exclusive prefix of this tile's aggregate over all earlier tiles: the tile
+// publishes its aggregate ({value, epoch << 2 | 1}), then the whole block
+// sums every earlier tile's aggregate directly, each thread polling its share
+// of the predecessors. Aggregates are published as soon as each tile's events
+// are processed (all tiles run concurrently), so this waits for the slowest
+// predecessor plus one or two L2 round trips -- a look-back chained through
+// inclusive prefixes propagates only a window of tiles per round trip (C5:
+// 410 tiles, ~13 dependent rounds). Every thread of the block must call it.
+__device__ unsigned long long tile_prefix(const BatchDev& b, uint32_t tile,
+                                          unsigned long long agg) {
+  __shared__ unsigned long long s_part[32];
   const unsigned long long ep = b.ctl->epoch << 2;
   volatile unsigned long long* ts = b.tile_state;
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     ts[3ull * tile] = agg;
-    if (tile == 0) ts[3ull * tile + 1] = agg;
     __threadfence();
-    ts[3ull * tile + 2] = ep | (tile == 0 ? 2ull : 1ull);
+    ts[3ull * tile + 2] = ep | 1ull;
   }
-  if (tile == 0) return 0ull;
-  unsigned long long prefix = 0;
-  int64_t base = static_cast<int64_t>(tile) - 1;
-  for (;;) {
-    const int64_t t = base - static_cast<int64_t>(lane);
-    unsigned long long st = ep | 2ull, v = 0;  // before tile 0: an empty inclusive
-    if (t >= 0) {
-      while (((st = ts[3ull * t + 2]) & ~3ull) != ep || (st & 3ull) == 0) __nanosleep(20);
-      __threadfence();
-      v = (st & 3ull) == 2ull ? ts[3ull * t + 1] : ts[3ull * t];
-    }
-    const unsigned inc = __ballot_sync(kAll, (st & 3ull) == 2ull);
-    const uint32_t stop = inc ? static_cast<uint32_t>(__ffs(inc) - 1) : 31u;
-    unsigned long long part = lane <= stop ? v : 0ull;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(kAll, part, off);
-    prefix += part;
-    if (inc) break;
-    base -= 32;
-  }
-  if (lane == 0) {
-    ts[3ull * tile + 1] = prefix + agg;
+  unsigned long long sum = 0;
+  for (uint32_t j = threadIdx.x; j < tile; j += blockDim.x) {
+    while ((ts[3ull * j + 2] & ~3ull) != ep) __nanosleep(32);
     __threadfence();
-    ts[3ull * tile + 2] = ep | 2ull;
+    sum += ts[3ull * j];
   }
-  return prefix;
+  sum = warp_sum(sum);
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_part[wid] = sum;
+  __syncthreads();
+  unsigned long long pre = 0;
+  for (uint32_t w = 0; w < blockDim.x / 32; ++w) pre += s_part[w];
+  return pre;
 }
 
 // kDel = false: insertion-only batch (validate + insertion flags).
@@ -1281,7 +1352,10 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_warp[8];
   __shared__ unsigned long long s_prefix;
-  if (threadIdx.x == 0) s_tile = atomicAdd(&b.ctl->tile_ctr, 1u);
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(&b.ctl->tile_ctr, 1u);
+    atomicMin(&b.ctl->t_prep0, global_ns());
+  }
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t k = tile * 256 + threadIdx.x;
@@ -1295,31 +1369,62 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
       if (code) {
         atomicMin(&b.ctl->val_err, (static_cast<unsigned long long>(k) << 8) | code);
       } else if (e.kind == 0) {
-        const double gw = edge_weight(G, e.u, e.v);
+        // Every request of the event is independent of the others: the
+        // list links, G's row u (whole, vector loads) and both H degrees go
+        // out together -- one dependent memory round instead of a chain of
+        // six. (This kernel runs for insertion-only single-pass batches, so
+        // ctl->fast == o.fastpath here.)
+        uint32_t gu = 0, gv = 0;
+        if (o.fastpath) {  // the fast path's append lists (one set for G and H)
+          gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
+          gv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
+        }
+        RowRegs<kCapG> gr;
+        const uint4* src = reinterpret_cast<const uint4*>(G.slab + e.u);
+#pragma unroll
+        for (int i = 0; i < RowRegs<kCapG>::kChunks; ++i) gr.v[i] = __ldg(src + i);
+        const uint32_t hdu = H.slab[e.u].deg, hdv = H.slab[e.v].deg;
+        // G.w(u, v) (either row holds it, graph.cpp symmetric storage)
+        double gw = 0.0;
+        if (gr.s.ext == kInline) {
+#pragma unroll
+          for (int i = 0; i < kCapG; ++i)
+            if (static_cast<uint32_t>(i) < gr.s.deg && gr.s.id[i] == e.v) gw = gr.s.w[i];
+        } else {
+          gw = edge_weight(G, e.u, e.v);
+        }
         if (gw != 0.0) b.ctl->not_simple = 1;  // fast-path precondition: new key
-        if (o.filtering && H.slab[e.u].deg > 0 && H.slab[e.v].deg > 0) {
+        if (o.filtering && hdu > 0 && hdv > 0) {
           const double wpq = __dadd_rn(gw, e.weight);
           // long-walking queries count in the low half, the others (with a
           // split) in the high half -- no min-path queries in this batch
           f = (o.split_wpq > 0.0 && wpq > o.split_wpq) ? (1ull << 32) : 1ull;
           b.wpq[k] = wpq;
         }
-        if (b.ctl->fast) {  // the fast path's append lists (G and H)
-          const uint32_t gu = atomicExch(b.fp_head[0] + e.u, 2 * k);
-          const uint32_t gv = atomicExch(b.fp_head[0] + e.v, 2 * k + 1);
-          const uint32_t hu = atomicExch(b.fp_head[1] + e.u, 2 * k);
-          const uint32_t hv = atomicExch(b.fp_head[1] + e.v, 2 * k + 1);
+        if (o.fastpath) {
           b.fp_next[0][2 * k] = gu;
           b.fp_next[0][2 * k + 1] = gv;
-          b.fp_next[1][2 * k] = hu;
-          b.fp_next[1][2 * k + 1] = hv;
         }
       }
       b.dec[k] = 0;
     } else {
-      if (e.kind == 1 && !o.freeze && has_edge(H, e.u, e.v) && G.slab[e.u].deg > 0 &&
-          G.slab[e.v].deg > 0)
-        f = 1ull << 32;
+      if (e.kind == 1 && !o.freeze) {
+        // H's row u (whole) and both shadow-G degrees in one memory round.
+        RowRegs<kCapH> hr;
+        const uint4* src = reinterpret_cast<const uint4*>(H.slab + e.u);
+#pragma unroll
+        for (int i = 0; i < RowRegs<kCapH>::kChunks; ++i) hr.v[i] = __ldg(src + i);
+        const uint32_t gdu = G.slab[e.u].deg, gdv = G.slab[e.v].deg;
+        bool in_h = false;
+        if (hr.s.ext == kInline) {
+#pragma unroll
+          for (int i = 0; i < kCapH; ++i)
+            in_h |= static_cast<uint32_t>(i) < hr.s.deg && hr.s.idr(i) == e.v;
+        } else {
+          in_h = has_edge(H, e.u, e.v);
+        }
+        if (in_h && gdu > 0 && gdv > 0) f = 1ull << 32;
+      }
     }
     b.state[k] = 0;
   }
@@ -1336,21 +1441,18 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
   }
   if (lane == 31) s_warp[wid] = x;
   __syncthreads();
-  if (wid == 0) {
+  if (threadIdx.x == 0) {
     unsigned long long run = 0;  // warp totals -> exclusive warp offsets
-    if (lane == 0) {
-      for (int w = 0; w < 8; ++w) {
-        const unsigned long long t = s_warp[w];
-        s_warp[w] = run;
-        run += t;
-      }
+    for (int w = 0; w < 8; ++w) {
+      const unsigned long long t = s_warp[w];
+      s_warp[w] = run;
+      run += t;
     }
-    run = __shfl_sync(0xFFFFFFFFu, run, 0);
-    const unsigned long long pre = tile_lookback(b, tile, run, lane);
-    if (lane == 0) s_prefix = pre;
+    s_prefix = run;  // the tile's aggregate
   }
   __syncthreads();
-  const unsigned long long excl = s_prefix + s_warp[wid] + x - f;
+  const unsigned long long pre = tile_prefix(b, tile, s_prefix);
+  const unsigned long long excl = pre + s_warp[wid] + x - f;
   if (k < nb && !aborted) {
     if (!kDel && (f >> 32)) {
       // short-walking reach query: slots from the top of the buffer
@@ -1371,6 +1473,7 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
       }
     }
   }
+  if (threadIdx.x == 0) atomicMax(&b.ctl->t_prep1, global_ns());
 }
 
 // Deletion-only batch, first launch: validation + the shadow's row lists.
@@ -1692,6 +1795,7 @@ __global__ void k_ctl_init(CtlInitArgs a) {
     ctl->fast = a.fast;
     ctl->counter_base = a.counter_base;
     ctl->t_commit0 = ~0ull;
+    ctl->t_prep0 = ~0ull;
     ctl->t_batch0 = global_ns();
     ctl->epoch = atomicAdd(a.epoch_ctr, 1ull) + 1ull;
   }
@@ -1853,8 +1957,7 @@ int launch_fastpath_g(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, 
 int launch_fastpath_h(const DevGraph<kCapH>& H, const BatchDev& b, uint32_t nb, const WalkOpts& o,
                       cudaStream_t st) {
   if (nb == 0) return 0;
-  const uint32_t n = 2 * nb;
-  k_fp_write_h<<<grid_for(n), 256, 0, st>>>(H, b.events, n, o, b);
+  k_fp_write_h<<<grid_for(nb), 256, 0, st>>>(H, b.events, nb, o, b);
   return 1;
 }
 

@@ -84,6 +84,7 @@ struct BatchCtl {
   unsigned long long t_commit0;  // first commit kernel (min over blocks)
   unsigned long long t_mp_end;   // k_minpath_finish end (max over blocks)
   unsigned long long t_batch1;   // batch epilogue
+  unsigned long long t_prep0, t_prep1;  // k_prep first block start / last block end
   unsigned long long epoch;      // unique per batch (single-pass scan tile states)
   unsigned int tile_ctr;         // single-pass scan: next tile
   unsigned int nq_long;        // reach queries in the low slots (walk-order split)

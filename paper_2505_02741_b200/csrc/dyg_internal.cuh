@@ -94,6 +94,17 @@ struct alignas(kHSlabAlign) Slab<kCapH> {
 static_assert(sizeof(Slab<kCapH>) == kHSlabAlign || kHSlabAlign == 32, "H slab size");
 static_assert(sizeof(Slab<kCapG>) == 128, "G slab must be 128 B");
 
+// A slab's entries as 16 B chunks, for whole-row vector loads into
+// registers: H entries end at byte 96 whatever the slab padding.
+template <int C>
+struct RowRegs {
+  static constexpr int kChunks = C == kCapH ? 6 : static_cast<int>(sizeof(Slab<C>) / 16);
+  union {
+    uint4 v[sizeof(Slab<C>) / 16];
+    Slab<C> s;
+  };
+};
+
 // POD view of one device graph, passed by value to kernels.
 template <int C>
 struct DevGraph {

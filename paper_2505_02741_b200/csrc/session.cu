@@ -176,6 +176,7 @@ struct dyg_session {
   uint64_t flow_cap = 0;           // DYG_FLOW_CAP: flow record capacity (test knob)
   bool reach_split = true;         // DYG_REACH_SPLIT=0: reach walks in slot order
   bool keep_shadow = true;         // DYG_KEEP_SHADOW=0: deletion commit restores G
+  unsigned long long last_t1 = 0;  // end stamp of the previous batch (stats)
   double mean_inv_w = 1.0;         // mean 1/w over G's edges (session creation)
 };
 
@@ -575,6 +576,33 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   s->stats.minpath_ms += span_ms(c.minpath.t_start, c.t_mp_end);
   s->stats.commit_ms += span_ms(c.t_commit0, c.t_batch1);
   s->stats.total_ms += span_ms(c.t_batch0, c.t_batch1);
+  {
+    const unsigned long long w0 = std::min(c.reach.t_start, c.minpath.t_start);
+    const unsigned long long w1 = std::max(c.reach.t_end == ~0ull ? 0ull : c.reach.t_end,
+                                           c.t_mp_end == ~0ull ? 0ull : c.t_mp_end);
+    if (w0 != ~0ull && w0 > c.t_batch0) s->stats.prep_ms += span_ms(c.t_batch0, w0);
+    if (w1 != 0 && c.t_commit0 > w1) s->stats.walk_commit_gap_ms += span_ms(w1, c.t_commit0);
+    // Consecutive batches of one replay (a gap over 1 ms is a host pause).
+    double gap_prev_us = -1.0;
+    if (s->last_t1 && c.t_batch0 > s->last_t1 && c.t_batch0 - s->last_t1 < 1000000ull) {
+      s->stats.batch_gap_ms += span_ms(s->last_t1, c.t_batch0);
+      gap_prev_us = (c.t_batch0 - s->last_t1) * 1e-3;
+    }
+    s->last_t1 = c.t_batch1;
+    static const bool timeline = std::getenv("DYG_TIMELINE") != nullptr;
+    if (timeline) {  // per-batch device timeline (us from batch start)
+      auto rel = [&](unsigned long long t) {
+        return (t == ~0ull || t == 0 || t < c.t_batch0) ? -1.0 : (t - c.t_batch0) * 1e-3;
+      };
+      std::fprintf(stderr,
+                   "dyg timeline batch %u nb=%u del=%u: reach %.1f-%.1f (drain %.1f) min %.1f-%.1f "
+                   "mp_end %.1f commit0 %.1f fl0 %.1f end %.1f gap_before %.1f prep %.1f-%.1f\n",
+                   p.batch, p.nb, p.n_del, rel(c.reach.t_start), rel(c.reach.t_end),
+                   rel(c.reach.t_drain), rel(c.minpath.t_start), rel(c.minpath.t_end),
+                   rel(c.t_mp_end), rel(c.t_commit0), rel(c.fl_t[0]), rel(c.t_batch1),
+                   gap_prev_us, rel(c.t_prep0), rel(c.t_prep1));
+    }
+  }
   if (fail_k != ~0ull) {
     s->counter = p.counter_base + fail_k + 1;  // ++update_counter_ precedes the throw (:469)
     const uint64_t pos = p.pos ? p.pos[fail_k] : p.pos_base + fail_k;
@@ -1604,6 +1632,7 @@ int dyg_session_reset_stats(dyg_session* s) {
   return guarded([&] {
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     s->stats = dyg_stats{};
+    s->last_t1 = 0;
   });
 }
 

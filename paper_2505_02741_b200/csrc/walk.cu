@@ -52,17 +52,6 @@ __device__ __forceinline__ void cp_async16(uint4* dst, const void* src, uint32_t
                : "memory");
 }
 
-// Entries of a row as 16 B chunks: H entries end at byte 96 whatever the
-// slab padding.
-template <int C>
-struct RowRegs {
-  static constexpr int kChunks = C == kCapH ? 6 : static_cast<int>(sizeof(Slab<C>) / 16);
-  union {
-    uint4 v[sizeof(Slab<C>) / 16];
-    Slab<C> s;
-  };
-};
-
 // sample_neighbor (walk.cpp:17-37) on an inline row held in registers,
 // given this step's uniform draw u01. The reference's pass 1 sums candidate
 // weights in row order and its pass 2 re-accumulates the same running sums
