@@ -254,6 +254,73 @@ int dyg_build_initial_sparsifier(const dyg_csr* g, double target_density, uint64
                                  int device, uint64_t* row_ptr_out, uint32_t* ids_out,
                                  double* w_out);
 
+/* ---- spectral evaluation ----------------------
+ * ConditionOptions (spectral.hpp:78-85). method: 0 Auto (Dense when
+ * n <= dense_cap), 1 Dense, 2 Iterative. Zero-initialised fields take the
+ * reference defaults: tolerance 1e-6, max_iterations 400, dense_cap 5000,
+ * seed 0x5eed (use dyg_condition_options_default). */
+typedef struct dyg_condition_options {
+  int32_t method;
+  uint32_t max_iterations;
+  double tolerance;
+  uint32_t dense_cap;
+  uint32_t pad;
+  uint64_t seed;
+} dyg_condition_options;
+
+/* ConditionEstimate (spectral.hpp:69-76). method: 0 Dense, 1 Iterative.
+ * inner_iterations: CG iterations of the L_H solves (no reference analogue:
+ * the reference factorises L_H exactly). */
+typedef struct dyg_condition_estimate {
+  double kappa;
+  double lambda_max;
+  double lambda_min;
+  int32_t method;
+  uint32_t iterations_used;
+  int32_t converged;
+  uint32_t pad;
+  uint64_t inner_iterations;
+} dyg_condition_estimate;
+
+void dyg_condition_options_default(dyg_condition_options* out);
+/* condition_number(G, H, options) (spectral.cpp:278-303): extreme
+ * generalized eigenvalues of the pencil (L_G, L_H) on the complement of the
+ * constant vector. Dense: cuSOLVER sygvd on the grounded pencil; Iterative:
+ * Lanczos in the L_H inner product (spectral.cpp:151-276) on `device`. */
+int dyg_condition_number(const dyg_csr* g, const dyg_csr* h, const dyg_condition_options* options,
+                         int device, dyg_condition_estimate* out);
+/* calibrate_budget(G, H, probe_fraction, rho, seed) (sparsifier.cpp:561-577):
+ * clamp(rho * kappa, 1, 1e6) from a coarse (tolerance 1e-3) estimate. */
+int dyg_calibrate_budget(const dyg_csr* g, const dyg_csr* h, double probe_fraction, double rho,
+                         uint64_t seed, int device, double* budget);
+/* The same on a session's current G and H; the seed is the session's
+ * walk.global_seed (sparsifier.cpp:579-583). */
+int dyg_session_calibrate_budget(dyg_session* s, double probe_fraction, double rho,
+                                 double* budget);
+int dyg_session_condition_number(dyg_session* s, const dyg_condition_options* options,
+                                 dyg_condition_estimate* out);
+
+/* PcgResult (solver.hpp:44-49); the solution goes to the caller's buffer. */
+typedef struct dyg_pcg_result {
+  uint32_t iterations;
+  int32_t converged;
+  double relative_residual; /* recomputed from scratch */
+  uint64_t inner_iterations;
+  uint64_t energy_count;    /* entries written to energy_trace */
+} dyg_pcg_result;
+
+/* pcg_solve(laplacian(G), rhs, M, tolerance, max_iterations, energy_trace)
+ * (solver.cpp:71-144) with M = Preconditioner::from_graph(H, factor_cap)
+ * (solver.cpp:10-25), or the identity when h == NULL. rhs and x have n
+ * entries; energy_trace (nullable) receives up to energy_cap values of
+ * 0.5 x'L_G x - b'x, one per iteration. factor_cap 0 = the reference's
+ * 2,000,000. */
+int dyg_pcg_solve(const dyg_csr* g, const dyg_csr* h, uint32_t factor_cap, const double* rhs,
+                  double tolerance, uint32_t max_iterations, int device, double* x,
+                  dyg_pcg_result* out, double* energy_trace, size_t energy_cap);
+/* random_rhs(n, seed) (solver.cpp:146-159), on the host. */
+int dyg_random_rhs(uint32_t n, uint64_t seed, double* out);
+
 /* Stateless twin of run_batch (walk.hpp:86-92): uploads g, runs the queries
  * on `device`, returns results in query order. path_buf (nullable) receives
  * MinPath vertices at [i*(T+1)]. */

@@ -30,3 +30,13 @@ from .api import (  # noqa: F401
     save_matrix_market,
     save_update_stream,
 )
+from .spectral import (  # noqa: F401,E402
+    ConditionEstimate,
+    ConditionMethod,
+    ConditionOptions,
+    PcgResult,
+    calibrate_budget,
+    condition_number,
+    pcg_solve,
+    random_rhs,
+)

@@ -66,6 +66,23 @@ class Options(C.Structure):
     _fields_ = [("walk", WalkCfg), ("batched", C.c_int32), ("freeze_sparsifier", C.c_int32)]
 
 
+class CondOpts(C.Structure):  # dyg_condition_options
+    _fields_ = [("method", C.c_int32), ("max_iterations", C.c_uint32), ("tolerance", C.c_double),
+                ("dense_cap", C.c_uint32), ("pad", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class CondEst(C.Structure):  # dyg_condition_estimate
+    _fields_ = [("kappa", C.c_double), ("lambda_max", C.c_double), ("lambda_min", C.c_double),
+                ("method", C.c_int32), ("iterations_used", C.c_uint32), ("converged", C.c_int32),
+                ("pad", C.c_uint32), ("inner_iterations", C.c_uint64)]
+
+
+class PcgRes(C.Structure):  # dyg_pcg_result
+    _fields_ = [("iterations", C.c_uint32), ("converged", C.c_int32),
+                ("relative_residual", C.c_double), ("inner_iterations", C.c_uint64),
+                ("energy_count", C.c_uint64)]
+
+
 _LIB = None
 
 
@@ -110,6 +127,16 @@ def lib() -> C.CDLL:
         "dyg_run_batch": (i32, [C.POINTER(Csr), vp, sz, C.POINTER(WalkCfg), vp, vp, i32]),
         "dyg_build_initial_sparsifier": (i32, [C.POINTER(Csr), dbl, u64, i32, vp, vp, vp]),
         "dyg_set_stream": (i32, [vp, vp]),
+        "dyg_condition_options_default": (None, [C.POINTER(CondOpts)]),
+        "dyg_condition_number": (i32, [C.POINTER(Csr), C.POINTER(Csr), C.POINTER(CondOpts), i32,
+                                       C.POINTER(CondEst)]),
+        "dyg_calibrate_budget": (i32, [C.POINTER(Csr), C.POINTER(Csr), dbl, dbl, u64, i32,
+                                       C.POINTER(C.c_double)]),
+        "dyg_session_condition_number": (i32, [vp, C.POINTER(CondOpts), C.POINTER(CondEst)]),
+        "dyg_session_calibrate_budget": (i32, [vp, dbl, dbl, C.POINTER(C.c_double)]),
+        "dyg_pcg_solve": (i32, [C.POINTER(Csr), C.POINTER(Csr), u32, vp, dbl, u32, i32, vp,
+                                C.POINTER(PcgRes), vp, sz]),
+        "dyg_random_rhs": (i32, [u32, u64, vp]),
         "dyg_shard_begin": (i32, [vp, vp, vp, sz, u32, C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_uint64)]),
         "dyg_shard_record_bytes": (sz, [vp, i32]),

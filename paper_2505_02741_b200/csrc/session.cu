@@ -15,6 +15,7 @@
 #include "../../include/dyg.h"
 #include "batch.cuh"
 #include "graph_store.cuh"
+#include "spectral.cuh"
 
 using namespace dyg;
 
@@ -1151,6 +1152,114 @@ void check_csr(const dyg_csr* c, const char* what) {
     fail(DYG_ERR_USAGE, std::string(what) + " has null row arrays");
 }
 
+// is_connected (graph.cpp) on a host CSR: BFS from vertex 0.
+bool csr_connected(const dyg_csr* c) {
+  if (c->n <= 1) return true;
+  std::vector<uint8_t> seen(c->n, 0);
+  std::vector<uint32_t> stack{0};
+  seen[0] = 1;
+  uint32_t count = 1;
+  while (!stack.empty()) {
+    const uint32_t u = stack.back();
+    stack.pop_back();
+    for (uint64_t i = c->row_ptr[u]; i < c->row_ptr[u + 1]; ++i) {
+      const uint32_t v = c->ids[i];
+      if (v < c->n && !seen[v]) {
+        seen[v] = 1;
+        ++count;
+        stack.push_back(v);
+      }
+    }
+  }
+  return count == c->n;
+}
+
+HostCsrView csr_view(const dyg_csr* c) { return HostCsrView{c->n, c->row_ptr, c->ids, c->w}; }
+
+dyg_condition_options condition_defaults() {
+  dyg_condition_options o{};
+  o.method = 0;
+  o.max_iterations = 400;
+  o.tolerance = 1e-6;
+  o.dense_cap = 5000;
+  o.seed = 0x5eed;
+  return o;
+}
+
+// condition_number (spectral.cpp:278-303) with the reference's checks.
+dyg_condition_estimate condition_number_impl(const dyg_csr* g, const dyg_csr* h,
+                                             const dyg_condition_options& opt, int device) {
+  check_csr(g, "graph");
+  check_csr(h, "sparsifier");
+  if (g->n != h->n) fail(DYG_ERR_USAGE, "graphs must share a vertex set");
+  if (g->n < 2) fail(DYG_ERR_USAGE, "condition number needs at least two vertices");
+  if (!csr_connected(g)) fail(DYG_ERR_DATA, "graph is disconnected");
+  if (!csr_connected(h)) fail(DYG_ERR_DATA, "sparsifier is disconnected");
+  int method = opt.method;
+  if (method == 0) method = g->n <= opt.dense_cap ? 1 : 2;
+  if (method == 1 && g->n > opt.dense_cap) {
+    char buf[128];
+    std::snprintf(buf, sizeof buf, "dense spectral path refused: n = %u exceeds cap %u", g->n,
+                  opt.dense_cap);
+    fail(DYG_ERR_USAGE, buf);
+  }
+  if (dyg_device_count() == 0) fail(DYG_ERR_DEVICE, "no CUDA device visible");
+  check(cudaSetDevice(device), "set device");
+  cudaStream_t st;
+  check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  ConditionResult r;
+  try {
+    DevLapOwner lg(csr_view(g), st), lh(csr_view(h), st);
+    check(cudaStreamSynchronize(st), "laplacian upload");
+    if (method == 1) {
+      r = condition_dense_device(lg.L, lh.L, st);
+    } else {
+      ConditionParams prm;
+      prm.tolerance = opt.tolerance;
+      prm.max_iterations = opt.max_iterations;
+      prm.seed = opt.seed;
+      r = condition_lanczos_device(lg.L, lh.L, prm);
+    }
+  } catch (...) {
+    cudaStreamDestroy(st);
+    throw;
+  }
+  cudaStreamDestroy(st);
+  dyg_condition_estimate e{};
+  e.kappa = r.kappa;
+  e.lambda_max = r.lambda_max;
+  e.lambda_min = r.lambda_min;
+  e.method = r.method;
+  e.iterations_used = r.iterations;
+  e.converged = r.converged;
+  e.inner_iterations = r.inner_iterations;
+  return e;
+}
+
+// calibrate_budget (sparsifier.cpp:561-577).
+double calibrate_impl(const dyg_csr* g, const dyg_csr* h, double probe_fraction, double rho,
+                      uint64_t seed, int device) {
+  if (!(probe_fraction > 0.0) || probe_fraction > 1.0)
+    fail(DYG_ERR_USAGE, "probe fraction must lie in (0, 1]");
+  if (!(rho > 0.0)) fail(DYG_ERR_USAGE, "budget ratio must be positive");
+  check_csr(g, "graph");
+  dyg_condition_options o = condition_defaults();
+  o.seed = seed;
+  o.tolerance = 1e-3;
+  const double probe = std::ceil(probe_fraction * g->n);
+  o.max_iterations = static_cast<uint32_t>(std::clamp(probe, 30.0, 2000.0));
+  const dyg_condition_estimate e = condition_number_impl(g, h, o, device);
+  return std::clamp(rho * e.kappa, 1.0, 1e6);
+}
+
+// A session's G or H as a host CSR (owning buffers).
+struct OwnedCsr {
+  std::vector<uint64_t> rp;
+  std::vector<uint32_t> ids;
+  std::vector<double> w;
+  dyg_csr c{};
+};
+
 bool csr_has_edge(const dyg_csr* c, uint32_t u, uint32_t v) {
   for (uint64_t i = c->row_ptr[u]; i < c->row_ptr[u + 1]; ++i)
     if (c->ids[i] == v) return true;
@@ -1779,6 +1888,135 @@ int dyg_build_initial_sparsifier(const dyg_csr* g, double target_density, uint64
     check(cudaSetDevice(device), "set device");
     build_initial_sparsifier_device(g->n, g->row_ptr, g->ids, g->w, target_density, seed,
                                     row_ptr_out, ids_out, w_out);
+  });
+}
+
+void dyg_condition_options_default(dyg_condition_options* out) {
+  if (out) *out = condition_defaults();
+}
+
+int dyg_condition_number(const dyg_csr* g, const dyg_csr* h, const dyg_condition_options* options,
+                         int device, dyg_condition_estimate* out) {
+  return guarded([&] {
+    if (out == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    const dyg_condition_options o = options ? *options : condition_defaults();
+    *out = condition_number_impl(g, h, o, device);
+  });
+}
+
+int dyg_calibrate_budget(const dyg_csr* g, const dyg_csr* h, double probe_fraction, double rho,
+                         uint64_t seed, int device, double* budget) {
+  return guarded([&] {
+    if (budget == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    *budget = calibrate_impl(g, h, probe_fraction, rho, seed, device);
+  });
+}
+
+namespace {
+void export_owned(dyg_session* s, int which, OwnedCsr& o) {
+  const uint64_t e = which == 0 ? s->g_edges : s->h_edges;
+  o.rp.resize(s->n + 1ull);
+  o.ids.resize(std::max<uint64_t>(2 * e, 1));
+  o.w.resize(std::max<uint64_t>(2 * e, 1));
+  check(cudaSetDevice(s->device), "set device");
+  const uint64_t nnz = which == 0 ? s->G.export_rows(o.rp.data(), o.ids.data(), o.w.data(),
+                                                     o.ids.size(), s->stream)
+                                  : s->H.export_rows(o.rp.data(), o.ids.data(), o.w.data(),
+                                                     o.ids.size(), s->stream);
+  if (nnz > o.ids.size()) fail(DYG_ERR_DEVICE, "row export size mismatch");
+  o.c = dyg_csr{s->n, 0, o.rp.data(), o.ids.data(), o.w.data()};
+}
+}  // namespace
+
+int dyg_session_condition_number(dyg_session* s, const dyg_condition_options* options,
+                                 dyg_condition_estimate* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    OwnedCsr g, h;
+    export_owned(s, 0, g);
+    export_owned(s, 1, h);
+    const dyg_condition_options o = options ? *options : condition_defaults();
+    *out = condition_number_impl(&g.c, &h.c, o, s->device);
+  });
+}
+
+int dyg_session_calibrate_budget(dyg_session* s, double probe_fraction, double rho,
+                                 double* budget) {
+  return guarded([&] {
+    if (s == nullptr || budget == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    OwnedCsr g, h;
+    export_owned(s, 0, g);
+    export_owned(s, 1, h);
+    *budget = calibrate_impl(&g.c, &h.c, probe_fraction, rho, s->opt.walk.global_seed, s->device);
+  });
+}
+
+int dyg_pcg_solve(const dyg_csr* g, const dyg_csr* h, uint32_t factor_cap, const double* rhs,
+                  double tolerance, uint32_t max_iterations, int device, double* x,
+                  dyg_pcg_result* out, double* energy_trace, size_t energy_cap) {
+  return guarded([&] {
+    if (rhs == nullptr || x == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    check_csr(g, "graph");
+    if (h != nullptr) {
+      check_csr(h, "preconditioner graph");
+      if (h->n != g->n) fail(DYG_ERR_USAGE, "solver dimensions disagree");
+      if (!csr_connected(h)) fail(DYG_ERR_DATA, "preconditioner graph is disconnected");
+    }
+    if (factor_cap == 0) factor_cap = 2000000;  // Preconditioner::kDefaultFactorCap
+    if (dyg_device_count() == 0) fail(DYG_ERR_DEVICE, "no CUDA device visible");
+    check(cudaSetDevice(device), "set device");
+    cudaStream_t st;
+    check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    std::vector<double> energy;
+    PcgOutcome r;
+    try {
+      DevLapOwner lg(csr_view(g), st);
+      DevLapOwner* lh = h ? new DevLapOwner(csr_view(h), st) : nullptr;
+      check(cudaStreamSynchronize(st), "laplacian upload");
+      // Factorized (exact) up to factor_cap, InnerCg at 1e-10 beyond (solver.cpp:17-23).
+      const double inner_tol = (h && h->n <= factor_cap) ? 1e-12 : 1e-10;
+      try {
+        r = pcg_device(lg.L, lh ? &lh->L : nullptr, rhs, tolerance, max_iterations, inner_tol, x,
+                       energy_trace ? &energy : nullptr);
+      } catch (...) {
+        delete lh;
+        throw;
+      }
+      delete lh;
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaStreamDestroy(st);
+    out->iterations = r.iterations;
+    out->converged = r.converged;
+    out->relative_residual = r.relative_residual;
+    out->inner_iterations = r.inner_iterations;
+    const size_t ne = std::min(energy.size(), energy_cap);
+    if (energy_trace && ne) std::memcpy(energy_trace, energy.data(), sizeof(double) * ne);
+    out->energy_count = ne;
+  });
+}
+
+int dyg_random_rhs(uint32_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    if (out == nullptr && n) fail(DYG_ERR_USAGE, "null argument");
+    uint64_t state = hash_mix(seed + 0xB0C4ull);
+    auto next_double = [&] {
+      state += kGamma;
+      return static_cast<double>(hash_mix(state) >> 11) * 0x1.0p-53;
+    };
+    for (uint32_t i = 0; i < n; i += 2) {  // Box-Muller on the deterministic stream
+      const double u1 = std::max(next_double(), 1e-300);
+      const double u2 = next_double();
+      const double radius = std::sqrt(-2.0 * std::log(u1));
+      out[i] = radius * std::cos(2.0 * M_PI * u2);
+      if (i + 1 < n) out[i + 1] = radius * std::sin(2.0 * M_PI * u2);
+    }
+    double sum = 0.0;
+    for (uint32_t i = 0; i < n; ++i) sum += out[i];
+    const double mean = n ? sum / n : 0.0;
+    for (uint32_t i = 0; i < n; ++i) out[i] -= mean;
   });
 }
 

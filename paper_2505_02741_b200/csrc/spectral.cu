@@ -1,0 +1,743 @@
+// spectral.cu -- SURVEY.md 8f rows 3-4 on the device: the condition number
+// kappa(L_G, L_H) of the pencil (spectral.cpp:151-276), calibrate_budget
+// (sparsifier.cpp:561-583) and PCG with an L_H preconditioner
+// (solver.cpp:10-144).
+//
+// Everything is Laplacian matrix-vector products and vector algebra over n
+// doubles: HBM-bound streaming (the CSR arrays once per product, the vectors
+// L2-resident up to ~10 M vertices). Layout: the graph as CSR in reference
+// row order (row_ptr u64, ids u32, w f64) plus the weighted degree per row,
+// so L x = dw .* x - A x is one pass over the rows. Reductions are
+// deterministic (fixed block partials summed in a fixed order), so a run is
+// reproducible bit for bit on the same device.
+//
+// Where the reference uses an exact sparse LDLT of the grounded L_H
+// (GroundedLaplacianSolver, laplacian.cpp:57-85) this module solves L_H on the
+// zero-mean subspace by conjugate gradients to a relative residual of 1e-12
+// (the reference's own InnerCg mode, solver.cpp:50-68, at a tighter
+// tolerance); the dense path (n <= dense_cap) is the generalized symmetric
+// eigensolve of the grounded pencil by cuSOLVER (loaded at run time).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "graph_store.cuh"
+#include "spectral.cuh"
+
+namespace dyg {
+
+namespace {
+
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs: partial sums per reduction
+constexpr int kRedThreads = 256;
+
+[[noreturn]] void sfail(int code, const std::string& msg) { throw DeviceError{code, msg}; }
+void scheck(cudaError_t e, const char* what) { cuda_check(e, what); }
+
+template <typename T>
+T* salloc(size_t count, const char* what) {
+  T* p = nullptr;
+  scheck(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * std::max<size_t>(count, 1)), what);
+  return p;
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double s[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, off);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) s[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s[w];
+  return t;  // valid in thread 0
+}
+
+// Weighted degree of every row, summed in row order (laplacian.cpp:14-17).
+__global__ void k_degw(const uint64_t* __restrict__ rp, const double* __restrict__ w, uint32_t n,
+                       double* __restrict__ dw) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (uint64_t i = rp[u]; i < rp[u + 1]; ++i) s += w[i];
+    dw[u] = s;
+  }
+}
+
+// y = L x, and (optionally) partial sums of x . y per block.
+__global__ void __launch_bounds__(kRedThreads) k_lap(DevLap L, const double* __restrict__ x,
+                                                     double* __restrict__ y, double* part,
+                                                     const int* done) {
+  if (done && *done) return;
+  double acc = 0.0;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < L.n; u += gridDim.x * blockDim.x) {
+    const double xu = x[u];
+    double s = 0.0;
+    for (uint64_t i = L.rp[u]; i < L.rp[u + 1]; ++i) s += L.w[i] * x[L.ids[i]];
+    const double yu = L.dw[u] * xu - s;
+    y[u] = yu;
+    acc += xu * yu;
+  }
+  if (part) {
+    const double t = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+
+// Partial sums of x . y (y == nullptr: of x . x; x == nullptr: of y).
+__global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ x,
+                                                     const double* __restrict__ y, uint32_t n,
+                                                     double* part) {
+  double acc = 0.0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double a = x ? x[i] : 1.0;
+    const double b = y ? y[i] : (x ? x[i] : 1.0);
+    acc += a * b;
+  }
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// out = sum of the partials, in block order.
+__global__ void k_final(const double* part, int np, double* out) {
+  __shared__ double s[kRedBlocks];
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s[i] = part[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < np; ++i) t += s[i];
+    *out = t;
+  }
+}
+
+// x[i] += a * y[i]; a = sign * num / den read from device scalars (den == nullptr: 1).
+__global__ void k_axpy(double* __restrict__ x, const double* __restrict__ y, uint32_t n,
+                       const double* num, const double* den, double sign, double scale,
+                       const int* done) {
+  if (done && *done) return;
+  double a = sign * scale;
+  if (num) a *= *num;
+  if (den) a /= *den;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] += a * y[i];
+}
+
+// x[i] = x[i] * a + c.
+__global__ void k_affine(double* __restrict__ x, uint32_t n, double a, double c) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = x[i] * a + c;
+}
+
+// Inner CG step (solver.cpp:56-66) with device scalars sc[]:
+// sc[0] rho, sc[1] pq, sc[2] rho_next, sc[3] target; done flag.
+__global__ void k_cg_xr(double* __restrict__ x, double* __restrict__ r,
+                        const double* __restrict__ p, const double* __restrict__ q, uint32_t n,
+                        const double* sc, double* part, const int* done) {
+  if (*done) return;
+  const double alpha = sc[0] / sc[1];
+  double acc = 0.0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    acc += ri * ri;
+  }
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+__global__ void k_cg_p(double* __restrict__ p, const double* __restrict__ r, uint32_t n,
+                       const double* sc, const int* done) {
+  if (*done) return;
+  const double beta = sc[2] / sc[0];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = r[i] + beta * p[i];
+}
+// Scalar bookkeeping between the two: rho <- rho_next after p is updated.
+__global__ void k_cg_pq(const double* part, int np, double* sc, const int* done) {
+  if (*done) return;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < np; ++i) t += part[i];
+    sc[1] = t;
+  }
+}
+__global__ void k_cg_rr(const double* part, int np, double* sc, int* done, unsigned* iters) {
+  if (*done) return;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < np; ++i) t += part[i];
+    sc[2] = t;
+    *iters += 1;
+  }
+}
+__global__ void k_cg_roll(double* sc, int* done, unsigned* iters, unsigned limit) {
+  if (*done) return;
+  sc[0] = sc[2];
+  if (!(sc[0] > sc[3]) || *iters >= limit) *done = 1;
+}
+
+// c[i] = B_i . w for the m columns (2-D grid: row chunks x columns).
+__global__ void __launch_bounds__(kRedThreads) k_multidot(const double* const* __restrict__ cols,
+                                                          const double* __restrict__ w,
+                                                          uint32_t n, double* part) {
+  const double* b = cols[blockIdx.y];
+  double acc = 0.0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    acc += b[i] * w[i];
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+__global__ void k_multidot_final(const double* part, int np, double* c) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < np; ++i) t += part[blockIdx.x * np + i];
+    c[blockIdx.x] = t;
+  }
+}
+// w -= sum_i c_i B_i.
+__global__ void k_multiaxpy(const double* const* __restrict__ cols, const double* __restrict__ c,
+                            uint32_t m, double* __restrict__ w, uint32_t n) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (uint32_t i = 0; i < m; ++i) acc += c[i] * cols[i][r];
+    w[r] -= acc;
+  }
+}
+
+// Dense grounded Laplacian (vertex 0 removed, laplacian.cpp:28-54), column-major.
+__global__ void k_dense_grounded(DevLap L, double* a, uint32_t m) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < L.n; u += gridDim.x * blockDim.x) {
+    if (u == 0) continue;
+    const uint32_t row = u - 1;
+    a[static_cast<uint64_t>(row) * m + row] += L.dw[u];
+    for (uint64_t i = L.rp[u]; i < L.rp[u + 1]; ++i) {
+      const uint32_t v = L.ids[i];
+      if (v == 0) continue;
+      a[static_cast<uint64_t>(v - 1) * m + row] -= L.w[i];
+    }
+  }
+}
+
+unsigned grid_n(uint32_t n) {
+  return static_cast<unsigned>(std::min<uint64_t>((n + 255ull) / 256ull, 148ull * 16ull));
+}
+
+// SplitMix64 next_double (rng.hpp:7-24) on the host.
+struct HostRng {
+  uint64_t state;
+  double next_double() {
+    state += kGamma;
+    return static_cast<double>(hash_mix(state) >> 11) * 0x1.0p-53;
+  }
+};
+
+// ---------------------------------------------------------------- cuSOLVER
+// Loaded on first use: the dense path is optional and the library carries no
+// link-time dependency on it.
+struct Cusolver {
+  using Create = int (*)(void**);
+  using Destroy = int (*)(void*);
+  using SetStream = int (*)(void*, cudaStream_t);
+  using SygvdSize = int (*)(void*, int, int, int, int, const double*, int, const double*, int,
+                            const double*, int*);
+  using Sygvd = int (*)(void*, int, int, int, int, double*, int, double*, int, double*, double*,
+                        int, int*);
+  Create create = nullptr;
+  Destroy destroy = nullptr;
+  SetStream set_stream = nullptr;
+  SygvdSize sygvd_size = nullptr;
+  Sygvd sygvd = nullptr;
+  bool ok = false;
+};
+
+const Cusolver& cusolver() {
+  static Cusolver c = [] {
+    Cusolver r;
+    void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libcusolver.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return r;
+    r.create = reinterpret_cast<Cusolver::Create>(dlsym(h, "cusolverDnCreate"));
+    r.destroy = reinterpret_cast<Cusolver::Destroy>(dlsym(h, "cusolverDnDestroy"));
+    r.set_stream = reinterpret_cast<Cusolver::SetStream>(dlsym(h, "cusolverDnSetStream"));
+    r.sygvd_size = reinterpret_cast<Cusolver::SygvdSize>(dlsym(h, "cusolverDnDsygvd_bufferSize"));
+    r.sygvd = reinterpret_cast<Cusolver::Sygvd>(dlsym(h, "cusolverDnDsygvd"));
+    r.ok = r.create && r.destroy && r.set_stream && r.sygvd_size && r.sygvd;
+    return r;
+  }();
+  return c;
+}
+
+// Smallest and largest eigenvalue of the symmetric tridiagonal (diag a,
+// off-diagonal b) by Sturm-count bisection to full precision: the Ritz
+// values of tridiagonal_extremes (spectral.cpp:132-145).
+std::pair<double, double> tridiag_extremes(const std::vector<double>& a,
+                                           const std::vector<double>& b) {
+  const size_t m = a.size();
+  double lo = a[0], hi = a[0];
+  for (size_t i = 0; i < m; ++i) {
+    const double r = (i > 0 ? std::fabs(b[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(b[i]) : 0.0);
+    lo = std::min(lo, a[i] - r);
+    hi = std::max(hi, a[i] + r);
+  }
+  // Number of eigenvalues strictly below x.
+  auto count_below = [&](double x) {
+    size_t c = 0;
+    double d = 1.0;
+    for (size_t i = 0; i < m; ++i) {
+      const double off = i > 0 ? b[i - 1] * b[i - 1] : 0.0;
+      d = (a[i] - x) - (i > 0 ? off / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      if (d < 0.0) ++c;
+    }
+    return c;
+  };
+  auto kth = [&](size_t k) {  // the k-th smallest (0-based)
+    double l = lo, h = hi;
+    for (int it = 0; it < 200; ++it) {
+      const double mid = 0.5 * (l + h);
+      if (mid <= l || mid >= h) break;
+      if (count_below(mid) > k) h = mid;
+      else l = mid;
+    }
+    return 0.5 * (l + h);
+  };
+  return {kth(0), kth(m - 1)};
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ DevLap
+DevLapOwner::DevLapOwner(const HostCsrView& g, cudaStream_t st) {
+  L.n = g.n;
+  const uint64_t nnz = g.row_ptr[g.n];
+  L.rp = salloc<uint64_t>(g.n + 1ull, "laplacian rows");
+  L.ids = salloc<uint32_t>(nnz, "laplacian ids");
+  L.w = salloc<double>(nnz, "laplacian weights");
+  L.dw = salloc<double>(g.n, "weighted degrees");
+  scheck(cudaMemcpyAsync(L.rp, g.row_ptr, sizeof(uint64_t) * (g.n + 1ull), cudaMemcpyHostToDevice, st),
+         "laplacian upload");
+  if (nnz) {
+    scheck(cudaMemcpyAsync(L.ids, g.ids, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st),
+           "laplacian upload");
+    scheck(cudaMemcpyAsync(L.w, g.w, sizeof(double) * nnz, cudaMemcpyHostToDevice, st),
+           "laplacian upload");
+  }
+  k_degw<<<grid_n(g.n), 256, 0, st>>>(L.rp, L.w, g.n, L.dw);
+  scheck(cudaGetLastError(), "weighted degrees");
+}
+
+DevLapOwner::~DevLapOwner() {
+  cudaFree(L.rp);
+  cudaFree(L.ids);
+  cudaFree(L.w);
+  cudaFree(L.dw);
+}
+
+// ------------------------------------------------------------ SpectralEngine
+SpectralEngine::SpectralEngine(uint32_t n) : n_(n) {
+  scheck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "spectral stream");
+  part_ = salloc<double>(kRedBlocks, "reduction partials");
+  sc_ = salloc<double>(8, "scalars");
+  done_ = salloc<int>(1, "cg flag");
+  iters_ = salloc<unsigned>(1, "cg iterations");
+  scheck(cudaMallocHost(reinterpret_cast<void**>(&host_), 64), "pinned scalars");
+}
+
+SpectralEngine::~SpectralEngine() {
+  cudaStreamSynchronize(st_);
+  cudaFree(part_);
+  cudaFree(sc_);
+  cudaFree(done_);
+  cudaFree(iters_);
+  for (double* v : scratch_) cudaFree(v);
+  cudaFreeHost(host_);
+  cudaStreamDestroy(st_);
+}
+
+double* SpectralEngine::vec() {
+  double* v = salloc<double>(n_, "spectral vector");
+  scratch_.push_back(v);
+  return v;
+}
+
+void SpectralEngine::lap(const DevLap& L, const double* x, double* y) {
+  k_lap<<<kRedBlocks, kRedThreads, 0, st_>>>(L, x, y, nullptr, nullptr);
+  scheck(cudaGetLastError(), "laplacian product");
+}
+
+double SpectralEngine::fetch(const double* dev_scalar) {
+  scheck(cudaMemcpyAsync(host_, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st_), "scalar");
+  scheck(cudaStreamSynchronize(st_), "spectral sync");
+  return host_[0];
+}
+
+double SpectralEngine::dot(const double* x, const double* y) {
+  k_dot<<<kRedBlocks, kRedThreads, 0, st_>>>(x, y, n_, part_);
+  k_final<<<1, 256, 0, st_>>>(part_, kRedBlocks, sc_ + 7);
+  scheck(cudaGetLastError(), "dot");
+  return fetch(sc_ + 7);
+}
+
+double SpectralEngine::sum(const double* x) {
+  k_dot<<<kRedBlocks, kRedThreads, 0, st_>>>(nullptr, x, n_, part_);  // 1 . x
+  k_final<<<1, 256, 0, st_>>>(part_, kRedBlocks, sc_ + 7);
+  scheck(cudaGetLastError(), "sum");
+  return fetch(sc_ + 7);
+}
+
+// x -= mean(x) (Eigen: x.array() -= x.mean()).
+void SpectralEngine::center(double* x) {
+  const double mean = sum(x) / static_cast<double>(n_);
+  k_affine<<<grid_n(n_), 256, 0, st_>>>(x, n_, 1.0, -mean);
+  scheck(cudaGetLastError(), "center");
+}
+
+void SpectralEngine::axpy_host(double* x, const double* y, double a) {
+  k_axpy<<<grid_n(n_), 256, 0, st_>>>(x, y, n_, nullptr, nullptr, 1.0, a, nullptr);
+  scheck(cudaGetLastError(), "axpy");
+}
+
+void SpectralEngine::scale(double* x, double a) {
+  k_affine<<<grid_n(n_), 256, 0, st_>>>(x, n_, a, 0.0);
+  scheck(cudaGetLastError(), "scale");
+}
+
+void SpectralEngine::copy(double* dst, const double* src) {
+  scheck(cudaMemcpyAsync(dst, src, sizeof(double) * n_, cudaMemcpyDeviceToDevice, st_), "copy");
+}
+
+void SpectralEngine::upload(double* dst, const double* host) {
+  scheck(cudaMemcpyAsync(dst, host, sizeof(double) * n_, cudaMemcpyHostToDevice, st_), "upload");
+}
+
+void SpectralEngine::download(double* host, const double* src) {
+  scheck(cudaMemcpyAsync(host, src, sizeof(double) * n_, cudaMemcpyDeviceToHost, st_), "download");
+  scheck(cudaStreamSynchronize(st_), "download");
+}
+
+// x = L^+ b on the zero-mean subspace by CG (solver.cpp:50-68): b is
+// centred first; stops once r.r <= (tol * |b|)^2 or after 20 n iterations;
+// the result is centred. Scalars stay on the device; the host looks at the
+// done flag every kCheck iterations (the flag freezes every kernel once set,
+// so the result is that of an exact stop).
+uint32_t SpectralEngine::cg_solve(const DevLap& L, const double* b, double* x, double rel_tol,
+                                  double* r, double* p, double* q) {
+  constexpr unsigned kCheck = 16;
+  copy(r, b);
+  center(r);
+  scheck(cudaMemsetAsync(x, 0, sizeof(double) * n_, st_), "cg x");
+  copy(p, r);
+  // rho = r.r ; target = tol^2 * rho
+  k_dot<<<kRedBlocks, kRedThreads, 0, st_>>>(r, nullptr, n_, part_);
+  k_final<<<1, 256, 0, st_>>>(part_, kRedBlocks, sc_ + 0);
+  const double rho0 = fetch(sc_ + 0);
+  const double target = rel_tol * rel_tol * rho0;
+  const uint64_t limit64 = 20ull * n_;
+  const unsigned limit = static_cast<unsigned>(std::min<uint64_t>(limit64, 0xFFFFFFF0ull));
+  host_[2] = target;
+  scheck(cudaMemcpyAsync(sc_ + 3, host_ + 2, sizeof(double), cudaMemcpyHostToDevice, st_), "cg target");
+  const int done0 = (rho0 > target) ? 0 : 1;
+  host_[3] = 0.0;
+  scheck(cudaMemcpyAsync(done_, &done0, sizeof(int), cudaMemcpyHostToDevice, st_), "cg flag");
+  scheck(cudaMemsetAsync(iters_, 0, sizeof(unsigned), st_), "cg iterations");
+  scheck(cudaStreamSynchronize(st_), "cg init");
+  if (done0) {
+    center(x);
+    return 0;
+  }
+  for (uint64_t k = 0;; k += kCheck) {
+    for (unsigned j = 0; j < kCheck; ++j) {
+      k_lap<<<kRedBlocks, kRedThreads, 0, st_>>>(L, p, q, part_, done_);
+      k_cg_pq<<<1, 32, 0, st_>>>(part_, kRedBlocks, sc_, done_);
+      k_cg_xr<<<kRedBlocks, kRedThreads, 0, st_>>>(x, r, p, q, n_, sc_, part_, done_);
+      k_cg_rr<<<1, 32, 0, st_>>>(part_, kRedBlocks, sc_, done_, iters_);
+      k_cg_p<<<grid_n(n_), 256, 0, st_>>>(p, r, n_, sc_, done_);
+      k_cg_roll<<<1, 1, 0, st_>>>(sc_, done_, iters_, limit);
+    }
+    scheck(cudaGetLastError(), "cg");
+    int done = 0;
+    scheck(cudaMemcpyAsync(&host_[4], done_, sizeof(int), cudaMemcpyDeviceToHost, st_), "cg flag");
+    scheck(cudaStreamSynchronize(st_), "cg");
+    std::memcpy(&done, &host_[4], sizeof(int));
+    if (done) break;
+  }
+  unsigned it = 0;
+  scheck(cudaMemcpyAsync(&host_[5], iters_, sizeof(unsigned), cudaMemcpyDeviceToHost, st_), "cg it");
+  scheck(cudaStreamSynchronize(st_), "cg");
+  std::memcpy(&it, &host_[5], sizeof(unsigned));
+  center(x);
+  return it;
+}
+
+// ------------------------------------------------------------ kappa
+ConditionResult condition_dense_device(const DevLap& G, const DevLap& H, cudaStream_t st) {
+  const Cusolver& cs = cusolver();
+  if (!cs.ok) sfail(4, "dense spectral path needs cuSOLVER (libcusolver.so.11 not found)");
+  const uint32_t m = G.n - 1;
+  const uint64_t mm = static_cast<uint64_t>(m) * m;
+  double* a = salloc<double>(mm, "dense L_G");
+  double* b = salloc<double>(mm, "dense L_H");
+  double* wv = salloc<double>(m, "eigenvalues");
+  int* info = salloc<int>(1, "info");
+  ConditionResult res;
+  void* h = nullptr;
+  try {
+    scheck(cudaMemsetAsync(a, 0, sizeof(double) * mm, st), "dense");
+    scheck(cudaMemsetAsync(b, 0, sizeof(double) * mm, st), "dense");
+    k_dense_grounded<<<grid_n(G.n), 256, 0, st>>>(G, a, m);
+    k_dense_grounded<<<grid_n(H.n), 256, 0, st>>>(H, b, m);
+    scheck(cudaGetLastError(), "dense laplacians");
+    if (cs.create(&h) != 0) sfail(4, "cusolverDnCreate failed");
+    cs.set_stream(h, st);
+    int lwork = 0;
+    // itype 1 (A x = l B x), no vectors (0), lower (CUBLAS_FILL_MODE_LOWER = 0)
+    if (cs.sygvd_size(h, 1, 0, 0, static_cast<int>(m), a, static_cast<int>(m), b,
+                      static_cast<int>(m), wv, &lwork) != 0)
+      sfail(3, "generalized eigensolve failed");
+    double* work = salloc<double>(static_cast<size_t>(std::max(lwork, 1)), "eigen workspace");
+    const int st1 = cs.sygvd(h, 1, 0, 0, static_cast<int>(m), a, static_cast<int>(m), b,
+                             static_cast<int>(m), wv, work, lwork, info);
+    int hinfo = 0;
+    double ends[2] = {0.0, 0.0};
+    scheck(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st), "info");
+    scheck(cudaMemcpyAsync(&ends[0], wv, sizeof(double), cudaMemcpyDeviceToHost, st), "eigs");
+    scheck(cudaMemcpyAsync(&ends[1], wv + (m - 1), sizeof(double), cudaMemcpyDeviceToHost, st),
+           "eigs");
+    scheck(cudaStreamSynchronize(st), "dense eigensolve");
+    cudaFree(work);
+    if (st1 != 0 || hinfo != 0) sfail(3, "generalized eigensolve failed");  // spectral.cpp:121-123
+    res.lambda_min = ends[0];
+    res.lambda_max = ends[1];
+    res.kappa = res.lambda_max / res.lambda_min;
+    res.method = 0;
+    res.iterations = 0;
+    res.converged = 1;
+  } catch (...) {
+    if (h) cs.destroy(h);
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(wv);
+    cudaFree(info);
+    throw;
+  }
+  cs.destroy(h);
+  cudaFree(a);
+  cudaFree(b);
+  cudaFree(wv);
+  cudaFree(info);
+  return res;
+}
+
+// condition_number_iterative (spectral.cpp:151-276): Lanczos for the pencil
+// (L_G, L_H) in the L_H inner product, every vector zero-mean, full
+// reorthogonalisation (two Gram-Schmidt passes against the cached L_H q_i;
+// here as classical GS -- all coefficients in one multi-dot, then one
+// multi-axpy -- instead of the reference's one-vector-at-a-time loop).
+ConditionResult condition_lanczos_device(const DevLap& G, const DevLap& H,
+                                         const ConditionParams& prm) {
+  const uint32_t n = G.n;
+  SpectralEngine e(n);
+  cudaStream_t st = e.stream();
+  // Start vector: SplitMix64(hash_mix(seed)), next_double() - 0.5, centred.
+  std::vector<double> q0(n);
+  HostRng rng{hash_mix(prm.seed)};
+  for (uint32_t i = 0; i < n; ++i) q0[i] = rng.next_double() - 0.5;
+  const uint32_t limit = std::min<uint32_t>(prm.max_iterations, n - 1);
+  // Basis columns (q_i and L_H q_i), allocated as the iteration grows.
+  std::vector<double*> basis, basis_b;
+  double** d_basis = salloc<double*>(limit + 1ull, "basis pointers");
+  double** d_basis_b = salloc<double*>(limit + 1ull, "basis pointers");
+  double* coef = salloc<double>(limit + 1ull, "gs coefficients");
+  double* mpart = nullptr;
+  constexpr int kChunks = 64;
+  mpart = salloc<double>(static_cast<size_t>(kChunks) * (limit + 1ull), "gs partials");
+  auto cleanup = [&] {
+    for (double* v : basis) cudaFree(v);
+    for (double* v : basis_b) cudaFree(v);
+    cudaFree(d_basis);
+    cudaFree(d_basis_b);
+    cudaFree(coef);
+    cudaFree(mpart);
+  };
+  ConditionResult est;
+  est.method = 1;
+  est.converged = 0;
+  try {
+    double* q = e.vec();
+    double* bq = e.vec();
+    double* aq = e.vec();
+    double* w = e.vec();
+    double* bw = e.vec();
+    double* r = e.vec();
+    double* p = e.vec();
+    double* tq = e.vec();
+    e.upload(q, q0.data());
+    e.center(q);
+    e.lap(H, q, bq);
+    const double norm0 = std::sqrt(e.dot(q, bq));
+    if (!(norm0 > 0.0)) sfail(3, "degenerate Lanczos start vector");
+    auto push = [&](const double* v, const double* bv, double s) {
+      double* c = salloc<double>(n, "basis vector");
+      double* cb = nullptr;
+      try {
+        cb = salloc<double>(n, "basis vector");
+      } catch (...) {
+        cudaFree(c);
+        throw;
+      }
+      basis.push_back(c);
+      basis_b.push_back(cb);
+      e.copy(c, v);
+      e.copy(cb, bv);
+      e.scale(c, 1.0 / s);
+      e.scale(cb, 1.0 / s);
+      scheck(cudaMemcpyAsync(d_basis + (basis.size() - 1), &basis.back(), sizeof(double*),
+                             cudaMemcpyHostToDevice, st), "basis pointer");
+      scheck(cudaMemcpyAsync(d_basis_b + (basis_b.size() - 1), &basis_b.back(), sizeof(double*),
+                             cudaMemcpyHostToDevice, st), "basis pointer");
+      scheck(cudaStreamSynchronize(st), "basis");  // &basis.back() is a host stack address
+    };
+    push(q, bq, norm0);
+    std::vector<double> alphas, betas;
+    double prev_min = 0.0, prev_max = 0.0;
+    uint32_t stable = 0;
+    for (uint32_t j = 0; j < limit; ++j) {
+      e.lap(G, basis[j], aq);
+      est.inner_iterations += e.cg_solve(H, aq, w, prm.inner_tol, r, p, tq);
+      const double alpha = e.dot(basis[j], aq);
+      alphas.push_back(alpha);
+      e.axpy_host(w, basis[j], -alpha);
+      if (j > 0) e.axpy_host(w, basis[j - 1], -betas[j - 1]);
+      const uint32_t mcols = static_cast<uint32_t>(basis.size());
+      for (int pass = 0; pass < 2; ++pass) {
+        k_multidot<<<dim3(kChunks, mcols), kRedThreads, 0, st>>>(d_basis_b, w, n, mpart);
+        k_multidot_final<<<mcols, 32, 0, st>>>(mpart, kChunks, coef);
+        k_multiaxpy<<<grid_n(n), 256, 0, st>>>(d_basis, coef, mcols, w, n);
+        scheck(cudaGetLastError(), "reorthogonalisation");
+      }
+      e.center(w);
+      e.lap(H, w, bw);
+      const double beta = std::sqrt(std::max(e.dot(w, bw), 0.0));
+      const auto ext = tridiag_extremes(alphas, betas);
+      est.lambda_min = ext.first;
+      est.lambda_max = ext.second;
+      est.iterations = j + 1;
+      if (beta < 1e-13 * std::max(1.0, std::fabs(alpha))) {  // invariant subspace
+        est.converged = 1;
+        break;
+      }
+      if (j > 2) {
+        const double cmin = std::fabs(ext.first - prev_min) / std::max(std::fabs(ext.first), 1e-300);
+        const double cmax = std::fabs(ext.second - prev_max) / std::max(std::fabs(ext.second), 1e-300);
+        if (cmin < prm.tolerance && cmax < prm.tolerance) {
+          if (++stable >= 3) {
+            est.converged = 1;
+            break;
+          }
+        } else {
+          stable = 0;
+        }
+      }
+      prev_min = ext.first;
+      prev_max = ext.second;
+      betas.push_back(beta);
+      push(w, bw, beta);
+    }
+    if (alphas.empty()) sfail(3, "Lanczos made no progress");
+    if (!(est.lambda_min > 0.0))
+      sfail(3, "iterative pencil estimate hit a non-positive eigenvalue");
+    est.kappa = est.lambda_max / est.lambda_min;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  return est;
+}
+
+// pcg_solve (solver.cpp:71-144) for L_G x = b with the L_H preconditioner
+// (H == nullptr: identity). Energy trace optional (per iteration).
+PcgOutcome pcg_device(const DevLap& G, const DevLap* H, const double* rhs_host, double tolerance,
+                      uint32_t max_iterations, double inner_tol, double* x_host,
+                      std::vector<double>* energy) {
+  const uint32_t n = G.n;
+  SpectralEngine e(n);
+  if (max_iterations == 0) max_iterations = 10 * n + 100;
+  double* b = e.vec();
+  double* x = e.vec();
+  double* r = e.vec();
+  double* z = e.vec();
+  double* p = e.vec();
+  double* q = e.vec();
+  double* t1 = e.vec();
+  double* t2 = e.vec();
+  double* t3 = e.vec();
+  e.upload(b, rhs_host);
+  e.center(b);
+  const double b_norm = std::sqrt(e.dot(b, nullptr));
+  PcgOutcome out;
+  scheck(cudaMemsetAsync(x, 0, sizeof(double) * n, e.stream()), "pcg x");
+  if (b_norm == 0.0) {
+    e.download(x_host, x);
+    out.converged = 1;
+    return out;
+  }
+  auto precond = [&](const double* in, double* res) {
+    if (H == nullptr) {
+      e.copy(res, in);
+      e.center(res);
+    } else {
+      out.inner_iterations += e.cg_solve(*H, in, res, inner_tol, t1, t2, t3);
+    }
+  };
+  e.copy(r, b);
+  precond(r, z);
+  e.copy(p, z);
+  double rho = e.dot(r, z);
+  for (uint32_t k = 1; k <= max_iterations; ++k) {
+    e.lap(G, p, q);
+    const double pq = e.dot(p, q);
+    if (!(pq > 0.0)) sfail(3, "PCG breakdown: search direction lost positivity");
+    const double alpha = rho / pq;
+    e.axpy_host(x, p, alpha);
+    e.center(x);
+    e.axpy_host(r, q, -alpha);
+    out.iterations = k;
+    if (energy) {  // 0.5 x'Lx - b'x
+      e.lap(G, x, t1);
+      energy->push_back(0.5 * e.dot(x, t1) - e.dot(b, x));
+    }
+    if (std::sqrt(e.dot(r, nullptr)) <= tolerance * b_norm) {
+      // Recompute the residual from scratch before stopping (:121-133).
+      e.lap(G, x, t1);
+      e.copy(r, b);
+      e.axpy_host(r, t1, -1.0);
+      if (std::sqrt(e.dot(r, nullptr)) <= tolerance * b_norm) break;
+      precond(r, z);
+      e.copy(p, z);
+      rho = e.dot(r, z);
+      continue;
+    }
+    precond(r, z);
+    const double rho_next = e.dot(r, z);
+    // p = z + (rho_next / rho) p
+    e.scale(p, rho_next / rho);
+    e.axpy_host(p, z, 1.0);
+    rho = rho_next;
+  }
+  e.lap(G, x, t1);
+  e.copy(r, b);
+  e.axpy_host(r, t1, -1.0);
+  out.relative_residual = std::sqrt(e.dot(r, nullptr)) / b_norm;
+  out.converged = out.relative_residual <= tolerance ? 1 : 0;
+  e.download(x_host, x);
+  return out;
+}
+
+}  // namespace dyg
