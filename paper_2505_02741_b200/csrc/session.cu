@@ -1218,7 +1218,7 @@ dyg_condition_estimate condition_number_impl(const dyg_csr* g, const dyg_csr* h,
       prm.tolerance = opt.tolerance;
       prm.max_iterations = opt.max_iterations;
       prm.seed = opt.seed;
-      r = condition_lanczos_device(lg.L, lh.L, prm);
+      r = condition_lanczos_device(lg.L, lh.L, csr_view(h), prm);
     }
   } catch (...) {
     cudaStreamDestroy(st);
@@ -1974,10 +1974,12 @@ int dyg_pcg_solve(const dyg_csr* g, const dyg_csr* h, uint32_t factor_cap, const
       DevLapOwner* lh = h ? new DevLapOwner(csr_view(h), st) : nullptr;
       check(cudaStreamSynchronize(st), "laplacian upload");
       // Factorized (exact) up to factor_cap, InnerCg at 1e-10 beyond (solver.cpp:17-23).
-      const double inner_tol = (h && h->n <= factor_cap) ? 1e-12 : 1e-10;
+      const bool factorized = h && h->n <= factor_cap;
+      HostCsrView hv{};
+      if (h) hv = csr_view(h);
       try {
-        r = pcg_device(lg.L, lh ? &lh->L : nullptr, rhs, tolerance, max_iterations, inner_tol, x,
-                       energy_trace ? &energy : nullptr);
+        r = pcg_device(lg.L, lh ? &lh->L : nullptr, h ? &hv : nullptr, factorized, rhs, tolerance,
+                       max_iterations, 1e-10, x, energy_trace ? &energy : nullptr);
       } catch (...) {
         delete lh;
         throw;

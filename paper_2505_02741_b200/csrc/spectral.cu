@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -273,6 +274,92 @@ const Cusolver& cusolver() {
   return c;
 }
 
+// Sparse Cholesky (cuSOLVER low-level csrchol: analysis / factor once, solve
+// many) with a METIS nested-dissection ordering, for the grounded Laplacian
+// solves the reference does with SimplicialLDLT. Loaded at run time.
+struct SpLib {
+  using Create = int (*)(void**);
+  using Destroy = int (*)(void*);
+  using SetStream = int (*)(void*, cudaStream_t);
+  using Metisnd = int (*)(void*, int, int, void*, const int*, const int*, const int64_t*, int*);
+  using PermSize = int (*)(void*, int, int, int, void*, const int*, const int*, const int*,
+                           const int*, size_t*);
+  using Perm = int (*)(void*, int, int, int, void*, int*, int*, const int*, const int*, int*,
+                       void*);
+  using InfoCreate = int (*)(void**);
+  using InfoDestroy = int (*)(void*);
+  using Analysis = int (*)(void*, int, int, void*, const int*, const int*, void*);
+  using BufInfo = int (*)(void*, int, int, void*, const double*, const int*, const int*, void*,
+                          size_t*, size_t*);
+  using Factor = int (*)(void*, int, int, void*, const double*, const int*, const int*, void*,
+                         void*);
+  using ZeroPivot = int (*)(void*, void*, double, int*);
+  using Solve = int (*)(void*, int, const double*, double*, void*, void*);
+  Create create = nullptr;
+  Destroy destroy = nullptr;
+  SetStream set_stream = nullptr;
+  Metisnd metisnd = nullptr;
+  PermSize perm_size = nullptr;
+  Perm perm = nullptr;
+  InfoCreate info_create = nullptr;
+  InfoDestroy info_destroy = nullptr;
+  Analysis analysis = nullptr;
+  BufInfo buf_info = nullptr;
+  Factor factor = nullptr;
+  ZeroPivot zero_pivot = nullptr;
+  Solve solve = nullptr;
+  Create descr_create = nullptr;  // cusparseCreateMatDescr
+  Destroy descr_destroy = nullptr;
+  bool ok = false;
+};
+
+const SpLib& splib() {
+  static SpLib c = [] {
+    SpLib r;
+    void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libcusolver.so", RTLD_NOW | RTLD_LOCAL);
+    void* hs = dlopen("libcusparse.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!hs) hs = dlopen("libcusparse.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h || !hs) return r;
+    auto sym = [&](void* lib, const char* name) { return dlsym(lib, name); };
+    r.create = reinterpret_cast<SpLib::Create>(sym(h, "cusolverSpCreate"));
+    r.destroy = reinterpret_cast<SpLib::Destroy>(sym(h, "cusolverSpDestroy"));
+    r.set_stream = reinterpret_cast<SpLib::SetStream>(sym(h, "cusolverSpSetStream"));
+    r.metisnd = reinterpret_cast<SpLib::Metisnd>(sym(h, "cusolverSpXcsrmetisndHost"));
+    r.perm_size = reinterpret_cast<SpLib::PermSize>(sym(h, "cusolverSpXcsrperm_bufferSizeHost"));
+    r.perm = reinterpret_cast<SpLib::Perm>(sym(h, "cusolverSpXcsrpermHost"));
+    r.info_create = reinterpret_cast<SpLib::InfoCreate>(sym(h, "cusolverSpCreateCsrcholInfo"));
+    r.info_destroy = reinterpret_cast<SpLib::InfoDestroy>(sym(h, "cusolverSpDestroyCsrcholInfo"));
+    r.analysis = reinterpret_cast<SpLib::Analysis>(sym(h, "cusolverSpXcsrcholAnalysis"));
+    r.buf_info = reinterpret_cast<SpLib::BufInfo>(sym(h, "cusolverSpDcsrcholBufferInfo"));
+    r.factor = reinterpret_cast<SpLib::Factor>(sym(h, "cusolverSpDcsrcholFactor"));
+    r.zero_pivot = reinterpret_cast<SpLib::ZeroPivot>(sym(h, "cusolverSpDcsrcholZeroPivot"));
+    r.solve = reinterpret_cast<SpLib::Solve>(sym(h, "cusolverSpDcsrcholSolve"));
+    r.descr_create = reinterpret_cast<SpLib::Create>(sym(hs, "cusparseCreateMatDescr"));
+    r.descr_destroy = reinterpret_cast<SpLib::Destroy>(sym(hs, "cusparseDestroyMatDescr"));
+    r.ok = r.create && r.destroy && r.set_stream && r.metisnd && r.perm_size && r.perm &&
+           r.info_create && r.info_destroy && r.analysis && r.buf_info && r.factor &&
+           r.zero_pivot && r.solve && r.descr_create && r.descr_destroy;
+    return r;
+  }();
+  return c;
+}
+
+// bp[i] = b[1 + p[i]] (grounded, permuted right-hand side).
+__global__ void k_perm_in(const double* __restrict__ b, const int* __restrict__ p,
+                          double* __restrict__ bp, uint32_t m) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    bp[i] = b[1 + p[i]];
+}
+// x[1 + p[i]] = y[i], x[0] = 0.
+__global__ void k_perm_out(const double* __restrict__ y, const int* __restrict__ p,
+                           double* __restrict__ x, uint32_t m) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    x[1 + p[i]] = y[i];
+    if (i == 0) x[0] = 0.0;
+  }
+}
+
 // Smallest and largest eigenvalue of the symmetric tridiagonal (diag a,
 // off-diagonal b) by Sturm-count bisection to full precision: the Ritz
 // values of tridiagonal_extremes (spectral.cpp:132-145).
@@ -475,6 +562,136 @@ uint32_t SpectralEngine::cg_solve(const DevLap& L, const double* b, double* x, d
   return it;
 }
 
+// ------------------------------------------------------------ GroundedChol
+GroundedChol::GroundedChol(const HostCsrView& g, cudaStream_t st) : st_(st) {
+  try {
+    build(g);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
+void GroundedChol::build(const HostCsrView& g) {
+  const SpLib& L = splib();
+  if (!L.ok) sfail(4, "exact Laplacian solves need cuSOLVER/cuSPARSE (libcusolver.so.11)");
+  if (g.n < 2) sfail(1, "grounding requires at least two vertices");  // laplacian.cpp:31
+  m_ = g.n - 1;
+  // Grounded Laplacian (vertex 0 removed, laplacian.cpp:28-54), CSR with
+  // sorted columns, int32 indices.
+  std::vector<int> rp(m_ + 1ull, 0), ci;
+  std::vector<double> val;
+  const uint64_t nnz_all = g.row_ptr[g.n];
+  if (nnz_all + g.n > 0x7FFFFFF0ull) sfail(1, "graph too large for the exact solver");
+  ci.reserve(nnz_all + g.n);
+  val.reserve(nnz_all + g.n);
+  std::vector<std::pair<int, double>> row;
+  for (uint32_t u = 1; u < g.n; ++u) {
+    row.clear();
+    double deg = 0.0;
+    for (uint64_t i = g.row_ptr[u]; i < g.row_ptr[u + 1]; ++i) {
+      deg += g.w[i];
+      if (g.ids[i] != 0) row.emplace_back(static_cast<int>(g.ids[i]) - 1, -g.w[i]);
+    }
+    if (deg > 0.0) row.emplace_back(static_cast<int>(u) - 1, deg);
+    std::sort(row.begin(), row.end(),
+              [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& e : row) {
+      ci.push_back(e.first);
+      val.push_back(e.second);
+    }
+    rp[u] = static_cast<int>(ci.size());
+  }
+  nnz_ = static_cast<int>(ci.size());
+  if (L.create(&handle_) != 0) sfail(4, "cusolverSpCreate failed");
+  L.set_stream(handle_, st_);
+  if (L.descr_create(&descr_) != 0) sfail(4, "cusparseCreateMatDescr failed");
+  // Fill-reducing ordering and the permuted matrix B = A(p, p).
+  std::vector<int> perm(m_);
+  if (L.metisnd(handle_, static_cast<int>(m_), nnz_, descr_, rp.data(), ci.data(), nullptr,
+                perm.data()) != 0)
+    sfail(3, "Laplacian factorization failed (ordering)");
+  size_t pbytes = 0;
+  if (L.perm_size(handle_, static_cast<int>(m_), static_cast<int>(m_), nnz_, descr_, rp.data(),
+                  ci.data(), perm.data(), perm.data(), &pbytes) != 0)
+    sfail(3, "Laplacian factorization failed (permutation)");
+  std::vector<char> pbuf(std::max<size_t>(pbytes, 1));
+  std::vector<int> map(nnz_);
+  for (int i = 0; i < nnz_; ++i) map[i] = i;
+  if (L.perm(handle_, static_cast<int>(m_), static_cast<int>(m_), nnz_, descr_, rp.data(),
+             ci.data(), perm.data(), perm.data(), map.data(), pbuf.data()) != 0)
+    sfail(3, "Laplacian factorization failed (permutation)");
+  std::vector<double> pval(nnz_);
+  for (int i = 0; i < nnz_; ++i) pval[i] = val[map[i]];
+  d_rp_ = salloc<int>(m_ + 1ull, "chol rows");
+  d_ci_ = salloc<int>(nnz_, "chol cols");
+  d_val_ = salloc<double>(nnz_, "chol values");
+  d_perm_ = salloc<int>(m_, "chol permutation");
+  d_bp_ = salloc<double>(m_, "chol rhs");
+  d_xp_ = salloc<double>(m_, "chol solution");
+  scheck(cudaMemcpyAsync(d_rp_, rp.data(), sizeof(int) * (m_ + 1ull), cudaMemcpyHostToDevice, st_),
+         "chol upload");
+  scheck(cudaMemcpyAsync(d_ci_, ci.data(), sizeof(int) * nnz_, cudaMemcpyHostToDevice, st_),
+         "chol upload");
+  scheck(cudaMemcpyAsync(d_val_, pval.data(), sizeof(double) * nnz_, cudaMemcpyHostToDevice, st_),
+         "chol upload");
+  scheck(cudaMemcpyAsync(d_perm_, perm.data(), sizeof(int) * m_, cudaMemcpyHostToDevice, st_),
+         "chol upload");
+  scheck(cudaStreamSynchronize(st_), "chol upload");  // host vectors go out of scope
+  if (L.info_create(&info_) != 0) sfail(4, "csrcholInfo create failed");
+  if (L.analysis(handle_, static_cast<int>(m_), nnz_, descr_, d_rp_, d_ci_, info_) != 0)
+    sfail(3, "Laplacian factorization failed (analysis)");
+  size_t internal = 0, work = 0;
+  if (L.buf_info(handle_, static_cast<int>(m_), nnz_, descr_, d_val_, d_rp_, d_ci_, info_,
+                 &internal, &work) != 0)
+    sfail(3, "Laplacian factorization failed (buffer)");
+  buffer_ = salloc<char>(std::max<size_t>(work, 1), "chol workspace");
+  if (L.factor(handle_, static_cast<int>(m_), nnz_, descr_, d_val_, d_rp_, d_ci_, info_,
+               buffer_) != 0)
+    sfail(3, "Laplacian factorization failed");
+  int pos = -1;
+  L.zero_pivot(handle_, info_, 1e-300, &pos);
+  scheck(cudaStreamSynchronize(st_), "chol factor");
+  if (pos >= 0) sfail(3, "Laplacian factorization failed");  // laplacian.cpp:64-66
+}
+
+GroundedChol::~GroundedChol() { release(); }
+
+void GroundedChol::release() {
+  const SpLib& L = splib();
+  cudaStreamSynchronize(st_);
+  if (info_) L.info_destroy(info_);
+  if (descr_) L.descr_destroy(descr_);
+  if (handle_) L.destroy(handle_);
+  info_ = descr_ = handle_ = nullptr;
+  cudaFree(d_rp_);
+  cudaFree(d_ci_);
+  cudaFree(d_val_);
+  cudaFree(d_perm_);
+  cudaFree(d_bp_);
+  cudaFree(d_xp_);
+  cudaFree(buffer_);
+  d_rp_ = d_ci_ = d_perm_ = nullptr;
+  d_val_ = d_bp_ = d_xp_ = nullptr;
+  buffer_ = nullptr;
+}
+
+// GroundedLaplacianSolver::solve (laplacian.cpp:70-85): centre b, solve the
+// grounded system, x[0] = 0, centre x. b and x may not alias; tmp is scratch.
+void GroundedChol::solve(SpectralEngine& e, const double* b, double* x, double* tmp) {
+  const SpLib& L = splib();
+  e.copy(tmp, b);
+  e.center(tmp);
+  k_perm_in<<<grid_n(m_), 256, 0, e.stream()>>>(tmp, d_perm_, d_bp_, m_);
+  scheck(cudaGetLastError(), "chol rhs");
+  L.set_stream(handle_, e.stream());
+  if (L.solve(handle_, static_cast<int>(m_), d_bp_, d_xp_, info_, buffer_) != 0)
+    sfail(3, "Laplacian solve failed");
+  k_perm_out<<<grid_n(m_), 256, 0, e.stream()>>>(d_xp_, d_perm_, x, m_);
+  scheck(cudaGetLastError(), "chol solution");
+  e.center(x);
+}
+
 // ------------------------------------------------------------ kappa
 ConditionResult condition_dense_device(const DevLap& G, const DevLap& H, cudaStream_t st) {
   const Cusolver& cs = cusolver();
@@ -540,10 +757,11 @@ ConditionResult condition_dense_device(const DevLap& G, const DevLap& H, cudaStr
 // here as classical GS -- all coefficients in one multi-dot, then one
 // multi-axpy -- instead of the reference's one-vector-at-a-time loop).
 ConditionResult condition_lanczos_device(const DevLap& G, const DevLap& H,
-                                         const ConditionParams& prm) {
+                                         const HostCsrView& h_host, const ConditionParams& prm) {
   const uint32_t n = G.n;
   SpectralEngine e(n);
   cudaStream_t st = e.stream();
+  GroundedChol hsolver(h_host, st);  // GroundedLaplacianSolver hsolver(h) (:156)
   // Start vector: SplitMix64(hash_mix(seed)), next_double() - 0.5, centred.
   std::vector<double> q0(n);
   HostRng rng{hash_mix(prm.seed)};
@@ -609,7 +827,7 @@ ConditionResult condition_lanczos_device(const DevLap& G, const DevLap& H,
     uint32_t stable = 0;
     for (uint32_t j = 0; j < limit; ++j) {
       e.lap(G, basis[j], aq);
-      est.inner_iterations += e.cg_solve(H, aq, w, prm.inner_tol, r, p, tq);
+      hsolver.solve(e, aq, w, tq);
       const double alpha = e.dot(basis[j], aq);
       alphas.push_back(alpha);
       e.axpy_host(w, basis[j], -alpha);
@@ -663,11 +881,15 @@ ConditionResult condition_lanczos_device(const DevLap& G, const DevLap& H,
 
 // pcg_solve (solver.cpp:71-144) for L_G x = b with the L_H preconditioner
 // (H == nullptr: identity). Energy trace optional (per iteration).
-PcgOutcome pcg_device(const DevLap& G, const DevLap* H, const double* rhs_host, double tolerance,
-                      uint32_t max_iterations, double inner_tol, double* x_host,
-                      std::vector<double>* energy) {
+PcgOutcome pcg_device(const DevLap& G, const DevLap* H, const HostCsrView* h_host, bool factorized,
+                      const double* rhs_host, double tolerance, uint32_t max_iterations,
+                      double inner_tol, double* x_host, std::vector<double>* energy) {
   const uint32_t n = G.n;
   SpectralEngine e(n);
+  // Preconditioner::from_graph (solver.cpp:10-25): exact factorisation up to
+  // factor_cap vertices, inner CG (relative 1e-10) beyond.
+  std::unique_ptr<GroundedChol> chol;
+  if (H != nullptr && factorized) chol.reset(new GroundedChol(*h_host, e.stream()));
   if (max_iterations == 0) max_iterations = 10 * n + 100;
   double* b = e.vec();
   double* x = e.vec();
@@ -692,6 +914,8 @@ PcgOutcome pcg_device(const DevLap& G, const DevLap* H, const double* rhs_host, 
     if (H == nullptr) {
       e.copy(res, in);
       e.center(res);
+    } else if (chol) {
+      chol->solve(e, in, res, t1);
     } else {
       out.inner_iterations += e.cg_solve(*H, in, res, inner_tol, t1, t2, t3);
     }

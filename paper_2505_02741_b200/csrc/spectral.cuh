@@ -73,6 +73,36 @@ class SpectralEngine {
   std::vector<double*> scratch_;
 };
 
+// GroundedLaplacianSolver (laplacian.cpp:57-85) on the device: sparse
+// Cholesky of the grounded Laplacian (METIS ordering, cuSOLVER csrchol),
+// factorised once, solved many times.
+class GroundedChol {
+ public:
+  GroundedChol(const HostCsrView& g, cudaStream_t st);
+  ~GroundedChol();
+  GroundedChol(const GroundedChol&) = delete;
+  GroundedChol& operator=(const GroundedChol&) = delete;
+  // x = L^+ b on the zero-mean subspace; tmp is an n-vector of scratch.
+  void solve(SpectralEngine& e, const double* b, double* x, double* tmp);
+
+ private:
+  void build(const HostCsrView& g);
+  void release();
+  cudaStream_t st_;
+  uint32_t m_ = 0;
+  int nnz_ = 0;
+  void* handle_ = nullptr;
+  void* descr_ = nullptr;
+  void* info_ = nullptr;
+  int* d_rp_ = nullptr;
+  int* d_ci_ = nullptr;
+  double* d_val_ = nullptr;
+  int* d_perm_ = nullptr;
+  double* d_bp_ = nullptr;
+  double* d_xp_ = nullptr;
+  char* buffer_ = nullptr;
+};
+
 struct ConditionParams {  // ConditionOptions (spectral.hpp:78-85)
   double tolerance = 1e-6;
   uint32_t max_iterations = 400;
@@ -99,9 +129,9 @@ struct PcgOutcome {  // PcgResult (solver.hpp:44-49) without the solution
 
 ConditionResult condition_dense_device(const DevLap& G, const DevLap& H, cudaStream_t st);
 ConditionResult condition_lanczos_device(const DevLap& G, const DevLap& H,
-                                         const ConditionParams& prm);
-PcgOutcome pcg_device(const DevLap& G, const DevLap* H, const double* rhs_host, double tolerance,
-                      uint32_t max_iterations, double inner_tol, double* x_host,
-                      std::vector<double>* energy);
+                                         const HostCsrView& h_host, const ConditionParams& prm);
+PcgOutcome pcg_device(const DevLap& G, const DevLap* H, const HostCsrView* h_host, bool factorized,
+                      const double* rhs_host, double tolerance, uint32_t max_iterations,
+                      double inner_tol, double* x_host, std::vector<double>* energy);
 
 }  // namespace dyg
