@@ -11,12 +11,12 @@
 // deterministic (fixed block partials summed in a fixed order), so a run is
 // reproducible bit for bit on the same device.
 //
-// Where the reference uses an exact sparse LDLT of the grounded L_H
-// (GroundedLaplacianSolver, laplacian.cpp:57-85) this module solves L_H on the
-// zero-mean subspace by conjugate gradients to a relative residual of 1e-12
-// (the reference's own InnerCg mode, solver.cpp:50-68, at a tighter
-// tolerance); the dense path (n <= dense_cap) is the generalized symmetric
-// eigensolve of the grounded pencil by cuSOLVER (loaded at run time).
+// The grounded L_H solves of GroundedLaplacianSolver (laplacian.cpp:57-85)
+// are a sparse Cholesky here too (GroundedChol: METIS ordering, cuSOLVER
+// csrchol factorised once); PCG's InnerCg mode (solver.cpp:50-68) is CG on
+// the device; the dense path (n <= dense_cap) is the generalized symmetric
+// eigensolve of the grounded pencil by cuSOLVER. cuSOLVER / cuSPARSE are
+// loaded at run time (no link-time dependency).
 #include <dlfcn.h>
 
 #include <algorithm>

@@ -7,7 +7,7 @@ Mirrors the reference's spectral.hpp / solver.hpp / calibrate_budget:
   constant vector. Dense (n <= dense_cap): cuSOLVER's generalized symmetric
   eigensolver on the grounded pencil. Iterative: Lanczos in the L_H inner
   product with full reorthogonalisation (spectral.cpp:151-276); the L_H solves
-  are CG to 1e-12 instead of the reference's sparse LDLT.
+  are a sparse Cholesky of the grounded Laplacian, as in the reference.
 * ``calibrate_budget(G, H, probe_fraction, rho, seed)`` --
   sparsifier.cpp:561-583.
 * ``pcg_solve(G, rhs, H, ...)`` -- solver.cpp:71-144 with
