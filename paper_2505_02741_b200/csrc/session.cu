@@ -471,12 +471,23 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   // Insertion fast path: G's appends do not depend on the walk (it reads H
   // alone); fork them onto the aux stream so they fill the walk's tail.
   const bool fast = p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass;
-  if (full && fast) {
-    check(cudaEventRecord(s->ev_fork, s->stream), "fork");
+  // The fork point is recorded before the walk, but the aux kernels are
+  // enqueued after it: the walk's blocks claim the SMs first (its start is
+  // on the batch's critical path; the appends only need to finish by the
+  // commit). DYG_FORK_FIRST=1 enqueues the appends first.
+  static const bool fork_first = [] {
+    const char* e = std::getenv("DYG_FORK_FIRST");
+    return e && std::atoi(e) != 0;
+  }();
+  auto fork_appends = [&] {
     check(cudaStreamWaitEvent(s->aux_stream, s->ev_fork, 0), "fork");
     p.launches += launch_fastpath_g(s->G.view(), b, p.nb, s->aux_stream);
     check(cudaEventRecord(s->ev_join, s->aux_stream), "join");
     p.g_appended = true;
+  };
+  if (full && fast) {
+    check(cudaEventRecord(s->ev_fork, s->stream), "fork");
+    if (fork_first) fork_appends();
   }
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r, nullptr, 0};
@@ -488,6 +499,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                                s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
+  if (full && fast && !fork_first) fork_appends();
   if (p.g_appended) check(cudaStreamWaitEvent(s->stream, s->ev_join, 0), "join");
   if (p.n_del > 0 && !o.freeze && max_m > 0) {
     WalkParams Pd = P;

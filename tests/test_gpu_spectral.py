@@ -1,7 +1,7 @@
 """GPU: condition number, calibrate_budget and PCG of csrc/spectral.cu
 against the restatement (oracle/spectral_ref.py) and dense ground truth.
 Floating-point tolerances (the device sums in a different order and solves
-L_H by CG to 1e-12 where the reference factorises):
+L_H with the same exact grounded factorisation but its own sparse Cholesky):
   kappa (dense path)            rel 1e-9
   kappa (iterative, converged)  rel 1e-6 of the dense truth
   calibrate_budget (coarse)     rel 1e-2 of the restatement
