@@ -1009,6 +1009,17 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   uint32_t* head = b.fp_head[0];
   uint32_t* done = b.fp_cnt[0];
   uint32_t* mark = b.fp_cnt[1];
+  // Balanced apply: the events the apply phase must order ("heavy": every
+  // event but the keep-mode accounting-only ones) are dealt round-robin to
+  // the warps in event order -- warp w owns the heavy events of rank w, w +
+  // nw, ... -- instead of k = w, w + nw, ...: path recoveries (~37 % of a C5
+  // deletion batch, each several dependent row round trips) then spread ~1
+  // per warp instead of clumping Poisson-wise. The accounting-only events
+  // are counted in the reset phase. Ranks come from a bitmap and its word
+  // prefix (one block scans it), so batches up to 32 x kMaxWords events.
+  constexpr uint32_t kMaxWords = 4096;
+  const uint32_t nwords = (lim + 31) / 32;
+  const bool balanced = op.o.flow_balance && nwords <= kMaxWords;
   if (tid == 0) ctl->fl_t[0] = global_ns();
   // Keep the walk shadow as the new G when every deletion found its edge
   // (then the shadow IS the event-order result); otherwise the reference's
@@ -1074,6 +1085,8 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
       const uint32_t k = pass * nw + wid;
       const bool fb = k < lim && !op.o.freeze && (b.fl_promo[k] & 1);
       const bool simple = k < lim && op.flow_simple(k, b.fl_promo, keep);
+      if (balanced && k < lim && !simple && lane == 0)
+        atomicOr(b.fl_heavy + (k >> 5), 1u << (k & 31));
       const uint32_t n =
           (k < lim && !simple) ? op.flow_rows(k, lane, fb, keep, [](uint32_t, uint32_t) {}) : 0;
       if (lane == 0) wcnt[wib] = n;
@@ -1113,6 +1126,7 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
   grid.sync();
   if (tid == 0) ctl->fl_t[2] = global_ns();
   const bool overflow = ctl->fl_overflow != 0;
+  Acc acc{};
   if (!overflow) {
     // Phase 2: ranks.
     const uint32_t total = ctl->fl_top;
@@ -1122,22 +1136,59 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
       for (uint32_t q = head[x]; q != kNoSlot; q = b.fl_next[q]) r += b.fl_ev[q] < k;
       b.fl_rank[p] = r;
     }
+    if (balanced && blockIdx.x == 0) {  // exclusive popcount prefix of the heavy bitmap
+      __shared__ uint32_t s_scan[256];
+      const uint32_t per = (nwords + blockDim.x - 1) / blockDim.x;
+      const uint32_t w0 = threadIdx.x * per;
+      uint32_t local = 0;
+      for (uint32_t w = w0; w < w0 + per && w < nwords; ++w) local += __popc(b.fl_heavy[w]);
+      s_scan[threadIdx.x] = local;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (uint32_t t = 0; t < blockDim.x; ++t) {
+          const uint32_t c = s_scan[t];
+          s_scan[t] = run;
+          run += c;
+        }
+        b.fl_wpre[nwords] = run;
+      }
+      __syncthreads();
+      uint32_t run = s_scan[threadIdx.x];
+      for (uint32_t w = w0; w < w0 + per && w < nwords; ++w) {
+        b.fl_wpre[w] = run;
+        run += __popc(b.fl_heavy[w]);
+      }
+    }
     grid.sync();
     if (tid == 0) ctl->fl_t[3] = global_ns();
     // Phase 3: apply in dataflow order.
-    Acc acc{};
     // Each warp owns events k = wid + j*nw (j = 0, 1, ...) and keeps a
     // window of its 8 lowest unapplied ones, applying whichever is ready
     // (non-blocking readiness polls), so an event stuck behind a long chain
     // does not hold up the warp's independent later events. The lowest
     // unapplied event overall is always inside its owner's window and ready:
     // no deadlock, and no shared work counter to contend on.
-    const uint32_t count = wid < lim ? (lim - wid + nw - 1) / nw : 0;
+    const uint32_t nown = balanced ? b.fl_wpre[nwords] : lim;
+    const uint32_t count = wid < nown ? (nown - wid + nw - 1) / nw : 0;
+    // The warp's j-th event: rank wid + j * nw among the heavy events
+    // (binary search of the word prefix, then the bit within the word).
+    auto ev_of = [&](uint32_t j) -> uint32_t {
+      const uint32_t h = wid + j * nw;
+      if (!balanced) return h;
+      uint32_t lo = 0, hi = nwords;  // fl_wpre[lo] <= h < fl_wpre[hi]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (b.fl_wpre[mid] <= h) lo = mid;
+        else hi = mid;
+      }
+      return lo * 32 + __fns(b.fl_heavy[lo], 0, static_cast<int>(h - b.fl_wpre[lo]) + 1);
+    };
     // Pull every row this warp's events will touch (G and H slabs) toward L2
     // now, so the dependent lookups inside apply_warp hit L2 instead of each
     // paying a DRAM round trip in sequence.
     for (uint32_t j = 0; j < count; ++j) {
-      const uint32_t k = wid + j * nw;
+      const uint32_t k = ev_of(j);
       const uint32_t base = b.fl_base[k], n = b.fl_cnt[k];
       for (uint32_t t = lane; t < n; t += 32) {
         const uint32_t x = b.fl_row[base + t];
@@ -1148,11 +1199,15 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
     constexpr uint32_t kWin = 8;
     uint32_t jlo = 0;
     uint32_t mask = count >= kWin ? 0xFFu : ((1u << count) - 1u);
+    uint32_t kw[kWin];  // the window's event indices
+#pragma unroll
+    for (uint32_t i = 0; i < kWin; ++i) kw[i] = i < count ? ev_of(i) : 0u;
     while (mask) {
       bool progressed = false;
+#pragma unroll
       for (uint32_t i = 0; i < kWin; ++i) {
         if (!((mask >> i) & 1u)) continue;
-        const uint32_t k = wid + (jlo + i) * nw;
+        const uint32_t k = kw[i];
         const uint32_t base = b.fl_base[k], n = b.fl_cnt[k];
         bool ready = true;
         for (uint32_t t = lane; t < n && ready; t += 32)
@@ -1185,11 +1240,15 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
       while (!(mask & 1u) && jlo < count) {
         mask >>= 1;
         ++jlo;
-        if (jlo + kWin - 1 < count) mask |= 1u << (kWin - 1);
+#pragma unroll
+        for (uint32_t i = 0; i + 1 < kWin; ++i) kw[i] = kw[i + 1];
+        if (jlo + kWin - 1 < count) {
+          mask |= 1u << (kWin - 1);
+          kw[kWin - 1] = ev_of(jlo + kWin - 1);
+        }
       }
       if (!progressed) __nanosleep(64);
     }
-    op.flush(acc);
   }
   grid.sync();
   if (tid == 0) ctl->fl_t[4] = global_ns();
@@ -1206,7 +1265,20 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
       mark[e.u] = 0;
       mark[e.v] = 0;
     }
+    // Balanced mode: the accounting-only events, now that commit_err is
+    // final (events at or past a failing one never commit, :525-529).
+    if (lane == 0 && balanced && !overflow && op.flow_simple(k, b.fl_promo, keep)) {
+      b.state[k] = 1;
+      if ((ctl->commit_err >> 8) > k) {
+        acc.r[kDelSeen] += 1;
+        --acc.dg;
+        op.dec[k] = 0;
+      }
+    }
   }
+  if (balanced)
+    for (uint32_t w = tid; w < nwords; w += nth) b.fl_heavy[w] = 0;
+  if (!overflow) op.flush(acc);
   clear_shadow_lists();
   grid.sync();
   if (tid == 0) ctl->fl_t[5] = global_ns();

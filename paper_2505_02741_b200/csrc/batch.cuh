@@ -115,6 +115,7 @@ struct WalkOpts {
   int shadow_lists;  // per-row shadow lists     (DYG_SHADOW_ROUNDS=1 disables)
   int flow;          // dataflow deletion commit (DYG_COMMIT_ROUNDS=1 disables)
   int keep_shadow;   // deletion-only batches keep the walk shadow as G (DYG_KEEP_SHADOW=0 disables)
+  int flow_balance;  // deal the ordered events round-robin to warps (DYG_FLOW_BALANCE=0 disables)
   // Reach walk order (insertion-only, single-GPU batches): queries whose
   // w_pq <= split_wpq (the budget lets them walk longest) get the low slots and
   // are walked first, the rest take slots from the top of the buffer; 0 = off.
@@ -172,6 +173,8 @@ struct BatchDev {
   uint32_t* fl_base;
   uint32_t* fl_cnt;
   uint8_t* fl_promo;   // per event: may run the local fallback
+  uint32_t* fl_heavy;  // bitmap: events the apply phase must order (0 between batches)
+  uint32_t* fl_wpre;   // exclusive popcount prefix of fl_heavy's words
   uint32_t* fl_depth;  // per vertex, 0 between batches
   uint64_t fl_cap;
 };

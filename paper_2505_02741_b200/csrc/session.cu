@@ -177,6 +177,7 @@ struct dyg_session {
   uint64_t flow_cap = 0;           // DYG_FLOW_CAP: flow record capacity (test knob)
   bool reach_split = true;         // DYG_REACH_SPLIT=0: reach walks in slot order
   bool keep_shadow = true;         // DYG_KEEP_SHADOW=0: deletion commit restores G
+  bool flow_balance = true;        // DYG_FLOW_BALANCE=0: static event ownership
   unsigned long long last_t1 = 0;  // end stamp of the previous batch (stats)
   double mean_inv_w = 1.0;         // mean 1/w over G's edges (session creation)
 };
@@ -223,6 +224,8 @@ void free_batch(dyg_session* s) {
   dev_free(b.fl_base);
   dev_free(b.fl_cnt);
   dev_free(b.fl_promo);
+  dev_free(b.fl_heavy);
+  dev_free(b.fl_wpre);
   dev_free(b.tile_state);
   cudaFree(b.cub_temp);
   b.cub_temp = nullptr;
@@ -264,6 +267,9 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.fl_base, cap, "flow record ranges");
     dev_alloc(&b.fl_cnt, cap, "flow record ranges");
     dev_alloc(&b.fl_promo, cap, "flow fallback flags");
+    dev_alloc(&b.fl_heavy, cap / 32 + 2, "flow heavy bitmap");
+    dev_alloc(&b.fl_wpre, cap / 32 + 3, "flow heavy prefix");
+    check(cudaMemset(b.fl_heavy, 0, sizeof(uint32_t) * (cap / 32 + 2)), "flow heavy bitmap");
     b.q_cap = cap;
     dev_alloc(&b.tile_state, 3ull * (cap / 256 + 2), "scan tile states");
     check(cudaMemset(b.tile_state, 0, sizeof(unsigned long long) * 3ull * (cap / 256 + 2)),
@@ -338,6 +344,7 @@ WalkOpts walk_opts(const dyg_session* s) {
   o.split_wpq = (s->reach_split && o.filtering && o.T > 0)
                     ? o.K / (0.8 * static_cast<double>(o.T) * s->mean_inv_w) : 0.0;
   o.keep_shadow = s->keep_shadow ? 1 : 0;
+  o.flow_balance = s->flow_balance ? 1 : 0;
   return o;
 }
 
@@ -1354,6 +1361,7 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->flow = !env_is("DYG_COMMIT_ROUNDS", 1);
       s->reach_split = !env_is("DYG_REACH_SPLIT", 0);
       s->keep_shadow = !env_is("DYG_KEEP_SHADOW", 0);
+      s->flow_balance = !env_is("DYG_FLOW_BALANCE", 0);
       if (const char* e = std::getenv("DYG_FLOW_CAP")) s->flow_cap = std::strtoull(e, nullptr, 10);
       {
         const char* e = std::getenv("DYG_GRAPHS");

@@ -21,6 +21,7 @@ KNOBS = [
     {"DYG_FLOW_CAP": "64"},  # record buffer overflow -> rounds inside k_del_flow
     {"DYG_REACH_SPLIT": "0"},
     {"DYG_KEEP_SHADOW": "0"},
+    {"DYG_FLOW_BALANCE": "0"},
     {"DYG_SINGLE_PASS": "0", "DYG_SHADOW_ROUNDS": "1", "DYG_COMMIT_ROUNDS": "1",
      "DYG_GRAPHS": "0"},
 ]
