@@ -292,10 +292,23 @@ def run_ours(args):
     from paper_2505_02741_b200.parallel import ShardedReplay
 
     rank, world, local = dist_env()
-    if world > 1:
+    force_shard = world == 1 and args.force_shard
+    if world > 1 or force_shard:
         import torch.distributed as dist
+        # rank 0 prints exactly one JSON line on stdout: everything the
+        # collectives' libraries print (NCCL's version banner) goes to stderr
+        # until then.
+        sys.stdout.flush()
+        real_stdout = os.dup(1)
+        os.dup2(2, 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if force_shard:  # the N > 1 code path on one GPU (a world of one rank)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            dist.init_process_group("nccl", rank=0, world_size=1,
+                                    device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -313,9 +326,8 @@ def run_ours(args):
     nb = stream.batch_count
     batches = [stream.batch(b) for b in range(nb)]
     n_events = int(sum(len(e) for e, _ in batches))
-    sharded = ShardedReplay(st, rank, world) if world > 1 else None
-    if world == 1:
-        st.upload_stream(stream)
+    sharded = ShardedReplay(st, rank, world) if (world > 1 or force_shard) else None
+    st.upload_stream(stream)  # device-resident events for the device-timed step
 
     def step_device():
         st.restore()
@@ -323,7 +335,7 @@ def run_ours(args):
             st.replay_uploaded_range(0, nb)  # device-resident replay(stream)
             return
         for b in range(nb):
-            sharded.replay_events(batches[b][0], batches[b][1], b)
+            sharded.replay_uploaded(b)
 
     def step_e2e():
         # The reference-facing replay(stream) from the host stream (page-locked
@@ -347,9 +359,11 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    log(f"[rank {rank}] session ready; warm-up")
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
+    log(f"[rank {rank}] timed steps")
     st.reset_stats()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clocks:
@@ -363,6 +377,7 @@ def run_ours(args):
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     stats = st.stats()
+    log(f"[rank {rank}] device {ms:.3f} ms/step; end-to-end")
     # Diagnostic: the snapshot restore each step begins with (not update work).
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record(torch_stream)
@@ -388,6 +403,7 @@ def run_ours(args):
     barrier()
     e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t) / args.steps)
     estats = st.stats()
+    log(f"[rank {rank}] e2e {e2e_ms:.3f} ms/step")
 
     if rank != 0:
         return
@@ -423,7 +439,8 @@ def run_ours(args):
             "sparsifier_edges": h.edge_count(), "batches": nb, "events_per_step": rep_events,
             "step": "restore(G0,H0) + replay of all batches (10 incremental + 10 decremental)",
             "K": K_BUDGET, "T": T_CAP, "s": WALKERS, "walk_seed": WALK_SEED,
-            "parallelism": f"replicated G/H, walks sharded x{world}" if world > 1 else "1 GPU",
+            "parallelism": (f"replicated G/H, walks sharded x{world}" if (world > 1 or force_shard)
+                            else "1 GPU"),
             "l2": "inputs larger than L2 (G slabs 537 MB + H slabs 268 MB > 126 MB)",
         },
         "e2e": {
@@ -469,8 +486,13 @@ def run_ours(args):
             out["cpu_baseline"] = cpu_baseline(args.config)
         except Exception as exc:  # reported, never silently replaced
             out["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    if world > 1 or force_shard:
+        sys.stdout.flush()
+        os.dup2(real_stdout, 1)
     print(json.dumps(out), flush=True)
     st.close()
+    if world > 1 or force_shard:
+        torch.distributed.destroy_process_group()
 
 
 def main():
@@ -481,6 +503,8 @@ def main():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=sorted(CONFIGS), default="C5")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--force-shard", action="store_true",
+                   help="one GPU through the multi-GPU (sharded, NCCL) code path")
     args = p.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

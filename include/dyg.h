@@ -345,6 +345,10 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
 int dyg_set_stream(dyg_session* s, void* cuda_stream);
 int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* positions,
                     size_t n, uint32_t batch_index, uint64_t* n_reach, uint64_t* n_minpath);
+/* The same for batch `batch_index` of the stream given to dyg_stream_upload
+ * (device-resident events: no per-batch upload). */
+int dyg_shard_begin_uploaded(dyg_session* s, uint32_t batch_index, uint64_t* n_reach,
+                             uint64_t* n_minpath);
 size_t dyg_shard_record_bytes(const dyg_session* s, int minpath);
 int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
                    void* minpath_records);

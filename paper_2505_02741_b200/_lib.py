@@ -140,6 +140,8 @@ def lib() -> C.CDLL:
         "dyg_shard_begin": (i32, [vp, vp, vp, sz, u32, C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_uint64)]),
         "dyg_shard_record_bytes": (sz, [vp, i32]),
+        "dyg_shard_begin_uploaded": (i32, [vp, u32, C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_uint64)]),
         "dyg_shard_walk": (i32, [vp, i32, i32, vp, vp]),
         "dyg_shard_commit": (i32, [vp, i32, vp, vp, vp]),
         "dygh_last_error": (C.c_char_p, []),

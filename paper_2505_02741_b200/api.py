@@ -461,6 +461,13 @@ class SparsifierState:
                                           C.byref(nr), C.byref(nm)))
         return nr.value, nm.value
 
+    def shard_begin_uploaded(self, batch_index):
+        """shard_begin for a batch of the stream given to upload_stream."""
+        nr, nm = C.c_uint64(), C.c_uint64()
+        _check(_lib.lib().dyg_shard_begin_uploaded(self._s, int(batch_index), C.byref(nr),
+                                                   C.byref(nm)))
+        return nr.value, nm.value
+
     def shard_record_bytes(self, minpath: bool) -> int:
         return _lib.lib().dyg_shard_record_bytes(self._s, int(minpath))
 

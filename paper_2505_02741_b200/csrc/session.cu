@@ -1776,17 +1776,19 @@ int dyg_set_stream(dyg_session* s, void* cuda_stream) {
 }
 
 // ---- multi-GPU split ---------------------------------------
-int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* positions, size_t n,
-                    uint32_t batch_index, uint64_t* n_reach, uint64_t* n_minpath) {
-  return guarded([&] {
-    if (s == nullptr || (n && events == nullptr)) fail(DYG_ERR_USAGE, "null argument");
+namespace {
+// dyg_shard_begin's body: `dev` == nullptr uploads `events`, else the batch
+// is already on the device (the uploaded stream) with known kind counts.
+void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* positions,
+                      size_t n, uint32_t batch_index, const DevEvent* dev, uint32_t n_ins0,
+                      uint32_t n_del0, uint64_t* n_reach, uint64_t* n_minpath) {
     if (!s->opt.batched) fail(DYG_ERR_USAGE, "the multi-GPU split needs batched (deferred) mode");
     check(cudaSetDevice(s->device), "set device");
     s->shard_active = false;
     s->shard_host = reinterpret_cast<const DevEvent*>(events);
     s->shard_pos = positions;
-    uint32_t n_ins = 0, n_del = 0;
-    if (n > 0) {
+    uint32_t n_ins = n_ins0, n_del = n_del0;
+    if (n > 0 && dev == nullptr) {
       ensure_batch(s, static_cast<uint32_t>(n), 0);
       upload_events(s, events, n);
       count_kinds(s, static_cast<uint32_t>(n), n_ins, n_del);
@@ -1803,7 +1805,7 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
       Pending p;
       bind_pending(s, p);
       reset_abort(s);
-      p.dev = s->d_events;
+      p.dev = dev ? dev : s->d_events;
       p.host = s->shard_host;
       p.pos = s->shard_pos;
       p.nb = s->shard_nb;
@@ -1823,6 +1825,28 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
     s->shard_active = true;
     if (n_reach) *n_reach = s->shard_nq_r;
     if (n_minpath) *n_minpath = s->shard_nq_m;
+}
+}  // namespace
+
+int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* positions, size_t n,
+                    uint32_t batch_index, uint64_t* n_reach, uint64_t* n_minpath) {
+  return guarded([&] {
+    if (s == nullptr || (n && events == nullptr)) fail(DYG_ERR_USAGE, "null argument");
+    shard_begin_impl(s, events, positions, n, batch_index, nullptr, 0, 0, n_reach, n_minpath);
+  });
+}
+
+int dyg_shard_begin_uploaded(dyg_session* s, uint32_t batch_index, uint64_t* n_reach,
+                             uint64_t* n_minpath) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    if (batch_index >= s->batch_cnt.size()) fail(DYG_ERR_USAGE, "batch index out of range");
+    const uint64_t off = s->batch_off[batch_index];
+    const size_t n = s->batch_cnt[batch_index];
+    shard_begin_impl(s, reinterpret_cast<const dyg_event*>(s->stream_events.data() + off),
+                     s->stream_positions.data() + off, n, batch_index, s->d_stream + off,
+                     static_cast<uint32_t>(s->batch_ins[batch_index]),
+                     static_cast<uint32_t>(s->batch_del[batch_index]), n_reach, n_minpath);
   });
 }
 

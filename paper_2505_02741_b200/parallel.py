@@ -78,18 +78,42 @@ class ShardedReplay:
         self.rbytes = state.shard_record_bytes(False)
         self.mbytes = state.shard_record_bytes(True)
         self.bytes_exchanged = 0
+        self._bufs = {}  # reused record buffers (grown on demand)
 
-    def replay_events(self, events, positions, batch_index: int):
+    def _buf(self, key, nbytes):
         import torch
 
-        nr, nm = self.state.shard_begin(events, positions, batch_index)
+        b = self._bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+            self._bufs[key] = b
+        return b[:nbytes]
+
+    def _exchange(self, nr, nm):
         sr, sm = slots_per_rank(nr, self.world), slots_per_rank(nm, self.world)
-        rloc = torch.empty(sr * self.rbytes, dtype=torch.uint8, device=self.device)
-        mloc = torch.empty(sm * self.mbytes, dtype=torch.uint8, device=self.device)
+        rloc = self._buf("rloc", sr * self.rbytes)
+        mloc = self._buf("mloc", sm * self.mbytes)
         self.state.shard_walk(self.rank, self.world, rloc.data_ptr() if sr else 0,
                               mloc.data_ptr() if sm else 0)
-        rall = allgather_records(rloc, self.world, self.group)
-        mall = allgather_records(mloc, self.world, self.group)
+        rall = self._gather("rall", rloc)
+        mall = self._gather("mall", mloc)
         self.bytes_exchanged += rall.numel() + mall.numel()
         return self.state.shard_commit(self.world, rall.data_ptr() if sr else 0,
                                        mall.data_ptr() if sm else 0)
+
+    def _gather(self, key, local):
+        import torch.distributed as dist
+
+        out = self._buf(key, self.world * local.numel())
+        if local.numel():
+            dist.all_gather_into_tensor(out, local, group=self.group)
+        return out
+
+    def replay_events(self, events, positions, batch_index: int):
+        nr, nm = self.state.shard_begin(events, positions, batch_index)
+        return self._exchange(nr, nm)
+
+    def replay_uploaded(self, batch_index: int):
+        """Batch `batch_index` of the stream given to state.upload_stream."""
+        nr, nm = self.state.shard_begin_uploaded(batch_index)
+        return self._exchange(nr, nm)
