@@ -562,6 +562,7 @@ struct CommitOp {
   // event k (the batch-start row minus the row's deletions up to k) comes
   // from the saved batch-start rows and the shadow's per-row deletion lists.
   int keep = 0;
+  int promo_pre = 0;  // k_prep<del> stored "edge in batch-start H" in fl_promo bit 1
   const uint32_t* save_idx = nullptr;     // vertex -> saved batch-start row
   const Slab<kCapG>* side_slab = nullptr;
   const unsigned long long* side_off = nullptr;
@@ -1042,7 +1043,9 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
       const DevEvent& e = op.ev[k];
       // H is batch-start H until the apply phase. (An event can be in H with
       // no query: a shadow degree of 0 skips the walk, :448.)
-      const bool in_h = op.slot[k] != kNoSlot || has_edge(op.H, e.u, e.v);
+      // The single-pass prepare already looked up batch-start H (promo bit 1).
+      const bool in_h = op.slot[k] != kNoSlot ||
+                        (op.promo_pre ? (b.fl_promo[k] & 2) != 0 : has_edge(op.H, e.u, e.v));
       const bool fb = in_h && !op.has_path_of(k);
       b.fl_promo[k] = (fb ? 1 : 0) | (in_h ? 2 : 0);
       if (fb) {
@@ -1496,6 +1499,7 @@ __global__ void __launch_bounds__(256) k_prep(DevGraph<kCapH> H, DevGraph<kCapG>
           in_h = has_edge(H, e.u, e.v);
         }
         if (in_h && gdu > 0 && gdv > 0) f = 1ull << 32;
+        b.fl_promo[k] = in_h ? 2 : 0;  // for the flow commit's phase 0
       }
     }
     b.state[k] = 0;
@@ -1995,6 +1999,7 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
   if (n_del == 0) return launch_rounds<false>(op, nb, b, st);
   if (n_del == nb && o.flow) {
     CommitOp op_copy = op;
+    op_copy.promo_pre = (o.single_pass && o.shadow_lists && !o.freeze) ? 1 : 0;
     if (keep_shadow_commit(o, nb, n_del)) {
       op_copy.keep = 1;
       op_copy.save_idx = b.save_idx;
