@@ -350,6 +350,9 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
 int dyg_shard_begin_uploaded(dyg_session* s, uint32_t batch_index, uint64_t* n_reach,
                              uint64_t* n_minpath);
 size_t dyg_shard_record_bytes(const dyg_session* s, int minpath);
+/* Enqueues this rank's walk and record packing on the session stream and
+ * returns without waiting: consume the records in stream order (or
+ * synchronise first). */
 int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
                    void* minpath_records);
 int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,

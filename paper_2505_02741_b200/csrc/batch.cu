@@ -2033,6 +2033,18 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
   return launch_rounds<true>(op, nb, b, st);
 }
 
+__global__ void k_set_u32x2(uint32_t* dst, uint32_t a, uint32_t b) {
+  dst[0] = a;
+  dst[1] = b;
+}
+
+// Two device words set in stream order from kernel arguments (a host-buffer
+// copy would race with the next call's rewrite of that buffer).
+int launch_set_u32x2(uint32_t* dst, uint32_t a, uint32_t b, cudaStream_t st) {
+  k_set_u32x2<<<1, 1, 0, st>>>(dst, a, b);
+  return 1;
+}
+
 int launch_fastpath_g(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st) {
   if (nb == 0) return 0;
   const uint32_t n = 2 * nb;

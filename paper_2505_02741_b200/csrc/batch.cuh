@@ -181,6 +181,7 @@ struct BatchDev {
 
 // Host launchers (batch.cu); each returns kernels launched.
 int launch_ctl_init(const CtlInitArgs& a, cudaStream_t st);
+int launch_set_u32x2(uint32_t* dst, uint32_t a, uint32_t b, cudaStream_t st);
 // Graph support: is `n` a k_ctl_init kernel node (then *out = its args)?
 bool ctl_init_node_args(cudaGraphNode_t n, CtlInitArgs* out);
 cudaError_t ctl_init_node_update(cudaGraphExec_t ex, cudaGraphNode_t n, const CtlInitArgs& a);

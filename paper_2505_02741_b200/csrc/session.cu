@@ -139,6 +139,7 @@ struct dyg_session {
   // Multi-GPU split state (dyg_shard_*).
   bool shard_active = false;
   const DevEvent* shard_host = nullptr;  // caller's buffers, valid until dyg_shard_commit
+  const DevEvent* shard_dev = nullptr;   // the batch's events on the device
   const uint64_t* shard_pos = nullptr;
   uint32_t shard_nb = 0, shard_ins = 0, shard_del = 0, shard_batch = 0;
   uint32_t shard_nq_r = 0, shard_nq_m = 0;
@@ -466,10 +467,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   const uint32_t* cnt_m = &b.ctl->nq_min;
   uint32_t max_r = p.n_ins, max_m = p.n_del;
   if (!full) {
-    s->h_counts[0] = n_r;
-    s->h_counts[1] = n_m;
-    check(cudaMemcpyAsync(s->d_counts, s->h_counts, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                          s->stream), "shard counts");
+    p.launches += launch_set_u32x2(s->d_counts, n_r, n_m, s->stream);
     cnt_r = s->d_counts;
     cnt_m = s->d_counts + 1;
     max_r = n_r;
@@ -1787,6 +1785,7 @@ void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* p
     s->shard_active = false;
     s->shard_host = reinterpret_cast<const DevEvent*>(events);
     s->shard_pos = positions;
+    s->shard_dev = dev ? dev : s->d_events;
     uint32_t n_ins = n_ins0, n_del = n_del0;
     if (n > 0 && dev == nullptr) {
       ensure_batch(s, static_cast<uint32_t>(n), 0);
@@ -1805,7 +1804,7 @@ void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* p
       Pending p;
       bind_pending(s, p);
       reset_abort(s);
-      p.dev = dev ? dev : s->d_events;
+      p.dev = s->shard_dev;
       p.host = s->shard_host;
       p.pos = s->shard_pos;
       p.nb = s->shard_nb;
@@ -1882,7 +1881,9 @@ int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
     phase_walk(s, p, false, lo_r, n_r, lo_m, n_m);
     p.launches += launch_pack(s->b, lo_r, n_r, lo_m, n_m, sl_r, sl_m, s->opt.walk.step_cap,
                               reach_records, minpath_records, s->stream);
-    check(cudaStreamSynchronize(s->stream), "shard walk");
+    // No host sync: the records are consumed in stream order (the all-gather
+    // is enqueued on the session's stream).
+    maybe_sync(s, "shard walk");
     s->shard_launches += p.launches;
   });
 }
@@ -1904,7 +1905,7 @@ int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
     Pending p;
     bind_pending(s, p);
     p.counter_base = s->shard_counter;
-    p.dev = s->d_events;
+    p.dev = s->shard_dev;
     p.host = s->shard_host;
     p.pos = s->shard_pos;
     p.nb = s->shard_nb;

@@ -12,8 +12,9 @@ from tests.parity import same_rows, to_dyg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_sharded_replay_equals_single(oracle, dyg, world):
+@pytest.mark.parametrize("world,uploaded", [(1, False), (2, False), (3, False), (8, False),
+                                            (1, True), (3, True)])
+def test_sharded_replay_equals_single(oracle, dyg, world, uploaded):
     import torch
 
     c = O.CONFIGS["C2"]
@@ -23,10 +24,12 @@ def test_sharded_replay_equals_single(oracle, dyg, world):
     sh = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
     stream = dyg.UpdateStream(s.events(), s.batch_count)
     rb, mb = sh.shard_record_bytes(False), sh.shard_record_bytes(True)
+    if uploaded:  # dyg_shard_begin_uploaded: the batch from the device-resident stream
+        sh.upload_stream(stream)
     for b in range(s.batch_count):
         r1 = ref.replay_batch(stream, b)
         ev, pos = stream.batch(b)
-        nr, nm = sh.shard_begin(ev, pos, b)
+        nr, nm = sh.shard_begin_uploaded(b) if uploaded else sh.shard_begin(ev, pos, b)
         sr, sm = -(-nr // world), -(-nm // world)
         rall = torch.zeros(max(1, world * sr * rb), dtype=torch.uint8, device="cuda")
         mall = torch.zeros(max(1, world * sm * mb), dtype=torch.uint8, device="cuda")
