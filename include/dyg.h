@@ -333,12 +333,15 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
  * dyg_shard_walk(rank, world), which runs the walk phase for the contiguous
  * query range [floor(nq*rank/world), floor(nq*(rank+1)/world)) and writes a
  * fixed-size record per query slot into `records` (device pointer,
- * dyg_shard_record_bytes() bytes per slot, `slots` slots = ceil(nq/world) on
- * every rank, unused slots zeroed). The caller all-gathers the records
+ * dyg_shard_record_bytes() bytes per slot, `slots` slots = ceil(nq_max/world)
+ * on every rank, unused slots zeroed). The caller all-gathers the records
  * (NCCL over NVLink) into `gathered` (world*slots slots, rank-major) and
  * calls dyg_shard_commit, which applies the identical deterministic commit on
- * every replica. dyg_shard_begin returns the query counts so the caller can
- * size buffers. The event and position buffers passed to dyg_shard_begin
+ * every replica. dyg_shard_begin returns nq_max for both kinds -- upper
+ * bounds of the query counts (the batch's insertions and deletions), so the
+ * caller sizes buffers without a host round trip; the exact counts stay on
+ * the device. Begin and walk only enqueue (stream order); validation errors
+ * surface at dyg_shard_commit. The event and position buffers passed to dyg_shard_begin
  * must stay valid until dyg_shard_commit returns (error messages read them).
  * The session stream may be replaced by the caller's (dyg_set_stream) so
  * the collective is stream-ordered with the kernels. */

@@ -1720,22 +1720,50 @@ unsigned grid_for(uint64_t n, unsigned bs = 256) {
   return static_cast<unsigned>((n + bs - 1) / bs);
 }
 
-__global__ void k_pack_reach(ReachOut r, uint32_t lo, uint32_t n, uint32_t slots,
+// Rank's contiguous query ranges [floor(nq*r/W), floor(nq*(r+1)/W)) from
+// the device counts of the prepare, and its queries moved to
+// the front of rq_sh / mq_sh, so the walk runs on [0, n) with a device count.
+__global__ void k_shard_range(const BatchCtl* ctl, int rank, int world, uint32_t* rng) {
+  const unsigned long long nr = ctl->nq_reach, nm = ctl->nq_min;
+  const uint32_t lr = static_cast<uint32_t>(nr * rank / world);
+  const uint32_t lm = static_cast<uint32_t>(nm * rank / world);
+  rng[0] = lr;
+  rng[1] = static_cast<uint32_t>(nr * (rank + 1) / world) - lr;
+  rng[2] = lm;
+  rng[3] = static_cast<uint32_t>(nm * (rank + 1) / world) - lm;
+}
+__global__ void k_shard_gather(const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
+                               ReachQuery* rq_sh, MinQuery* mq_sh, const uint32_t* rng,
+                               uint32_t max_n) {
+  const uint32_t lr = rng[0], nr = rng[1], lm = rng[2], nm = rng[3];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < max_n;
+       i += gridDim.x * blockDim.x) {
+    if (i < nr) rq_sh[i] = rq[lr + i];
+    if (i < nm) mq_sh[i] = mq[lm + i];
+  }
+}
+
+// The rank's walk results sit at [0, n) (its queries were moved to the
+// front, launch_shard_range); n is the device count.
+__global__ void k_pack_reach(ReachOut r, const uint32_t* n_dev, uint32_t slots,
                              ReachRecord* rec) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= slots) return;
+  const uint32_t n = *n_dev;
   ReachRecord x{0, 0, 0ull};
   if (i < n) {
-    x.reached = r.reached[lo + i];
-    x.steps = r.steps[lo + i];
+    x.reached = r.reached[i];
+    x.steps = r.steps[i];
   }
   rec[i] = x;
 }
 
-__global__ void k_pack_min(MinOut m, uint32_t lo, uint32_t n, uint32_t slots, uint32_t T,
+__global__ void k_pack_min(MinOut m, const uint32_t* n_dev, uint32_t slots, uint32_t T,
                            uint8_t* rec, size_t rec_bytes) {
   const uint32_t i = blockIdx.x;
   if (i >= slots) return;
+  const uint32_t n = *n_dev;
+  constexpr uint32_t lo = 0;
   uint8_t* base = rec + static_cast<size_t>(i) * rec_bytes;
   MinRecordHead* h = reinterpret_cast<MinRecordHead*>(base);
   uint32_t* path = reinterpret_cast<uint32_t*>(base + sizeof(MinRecordHead));
@@ -1764,9 +1792,10 @@ __device__ __forceinline__ void locate(uint32_t q, uint32_t nq, int world, uint3
   *idx = q - static_cast<uint32_t>((static_cast<unsigned long long>(nq) * r) / world);
 }
 
-__global__ void k_unpack_reach(ReachOut r, uint32_t nq, int world, uint32_t slots,
+__global__ void k_unpack_reach(ReachOut r, const uint32_t* nq_dev, int world, uint32_t slots,
                                const ReachRecord* rec) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nq = *nq_dev;
   if (q >= nq) return;
   uint32_t rank, idx;
   locate(q, nq, world, &rank, &idx);
@@ -1775,9 +1804,10 @@ __global__ void k_unpack_reach(ReachOut r, uint32_t nq, int world, uint32_t slot
   r.steps[q] = x.steps;
 }
 
-__global__ void k_unpack_min(MinOut m, uint32_t nq, int world, uint32_t slots, uint32_t T,
-                             const uint8_t* rec, size_t rec_bytes) {
+__global__ void k_unpack_min(MinOut m, const uint32_t* nq_dev, int world, uint32_t slots,
+                             uint32_t T, const uint8_t* rec, size_t rec_bytes) {
   const uint32_t q = blockIdx.x;
+  const uint32_t nq = *nq_dev;
   if (q >= nq) return;
   uint32_t rank, idx;
   locate(q, nq, world, &rank, &idx);
@@ -2060,35 +2090,45 @@ int launch_fastpath_h(const DevGraph<kCapH>& H, const BatchDev& b, uint32_t nb, 
   return 1;
 }
 
-int launch_pack(const BatchDev& b, uint32_t lo_r, uint32_t n_r, uint32_t lo_m, uint32_t n_m,
-                uint32_t slots_r, uint32_t slots_m, uint32_t T, void* rrec, void* mrec,
-                cudaStream_t st) {
+int launch_shard_range(const BatchDev& b, int rank, int world, uint32_t* rng, uint32_t max_r,
+                       uint32_t max_m, cudaStream_t st) {
+  k_shard_range<<<1, 1, 0, st>>>(b.ctl, rank, world, rng);
+  const uint32_t mx = max_r > max_m ? max_r : max_m;
+  if (mx == 0) return 1;
+  k_shard_gather<<<grid_for(mx), 256, 0, st>>>(b.rq, b.mq, b.rq_sh, b.mq_sh, rng, mx);
+  return 2;
+}
+
+int launch_pack(const BatchDev& b, const uint32_t* rng, uint32_t slots_r, uint32_t slots_m,
+                uint32_t T, void* rrec, void* mrec, cudaStream_t st) {
   int l = 0;
   if (slots_r) {
-    k_pack_reach<<<grid_for(slots_r), 256, 0, st>>>(b.rout, lo_r, n_r, slots_r,
+    k_pack_reach<<<grid_for(slots_r), 256, 0, st>>>(b.rout, rng + 1, slots_r,
                                                      static_cast<ReachRecord*>(rrec));
     ++l;
   }
   if (slots_m) {
-    k_pack_min<<<slots_m, 128, 0, st>>>(b.mout, lo_m, n_m, slots_m, T, static_cast<uint8_t*>(mrec),
+    k_pack_min<<<slots_m, 128, 0, st>>>(b.mout, rng + 3, slots_m, T, static_cast<uint8_t*>(mrec),
                                         min_record_bytes(T));
     ++l;
   }
   return l;
 }
 
-int launch_unpack(const BatchDev& b, uint32_t nq_r, uint32_t nq_m, int world, uint32_t slots_r,
+// Gathered rank-major records -> query order (device query counts; max_r /
+// max_m bound them for the grids).
+int launch_unpack(const BatchDev& b, uint32_t max_r, uint32_t max_m, int world, uint32_t slots_r,
                   uint32_t slots_m, uint32_t T, const void* rrec, const void* mrec,
                   cudaStream_t st) {
   int l = 0;
-  if (nq_r) {
-    k_unpack_reach<<<grid_for(nq_r), 256, 0, st>>>(b.rout, nq_r, world, slots_r,
-                                                   static_cast<const ReachRecord*>(rrec));
+  if (max_r && slots_r) {
+    k_unpack_reach<<<grid_for(max_r), 256, 0, st>>>(b.rout, &b.ctl->nq_reach, world, slots_r,
+                                                    static_cast<const ReachRecord*>(rrec));
     ++l;
   }
-  if (nq_m) {
-    k_unpack_min<<<nq_m, 128, 0, st>>>(b.mout, nq_m, world, slots_m, T,
-                                       static_cast<const uint8_t*>(mrec), min_record_bytes(T));
+  if (max_m && slots_m) {
+    k_unpack_min<<<max_m, 128, 0, st>>>(b.mout, &b.ctl->nq_min, world, slots_m, T,
+                                        static_cast<const uint8_t*>(mrec), min_record_bytes(T));
     ++l;
   }
   return l;

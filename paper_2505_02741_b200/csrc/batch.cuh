@@ -155,6 +155,8 @@ struct BatchDev {
   unsigned long long* tile_state;
   uint32_t q_cap;            // query slot capacity (reach slots are < q_cap)
   uint32_t n_vertices;
+  ReachQuery* rq_sh;  // multi-GPU split: this rank's query range, moved to the front
+  MinQuery* mq_sh;
   uint32_t* save_idx;        // per vertex: index of its saved batch-start G row
   void* cub_temp;
   size_t cub_temp_bytes;
@@ -182,6 +184,10 @@ struct BatchDev {
 // Host launchers (batch.cu); each returns kernels launched.
 int launch_ctl_init(const CtlInitArgs& a, cudaStream_t st);
 int launch_set_u32x2(uint32_t* dst, uint32_t a, uint32_t b, cudaStream_t st);
+// Multi-GPU split: rank's query ranges from the device counts (rng[0..3] =
+// lo_r, n_r, lo_m, n_m) and the range's queries copied to rq_sh / mq_sh.
+int launch_shard_range(const BatchDev& b, int rank, int world, uint32_t* rng, uint32_t max_r,
+                       uint32_t max_m, cudaStream_t st);
 // Graph support: is `n` a k_ctl_init kernel node (then *out = its args)?
 bool ctl_init_node_args(cudaGraphNode_t n, CtlInitArgs* out);
 cudaError_t ctl_init_node_update(cudaGraphExec_t ex, cudaGraphNode_t n, const CtlInitArgs& a);
@@ -230,11 +236,10 @@ inline size_t min_record_bytes(uint32_t T) {
   return (sizeof(MinRecordHead) + 4ull * (T + 1ull) + 7ull) & ~7ull;
 }
 // Pack this rank's queries [lo, hi) into `slots` records (rest zeroed).
-int launch_pack(const BatchDev& b, uint32_t lo_r, uint32_t n_r, uint32_t lo_m, uint32_t n_m,
-                uint32_t slots_r, uint32_t slots_m, uint32_t T, void* rrec, void* mrec,
-                cudaStream_t st);
+int launch_pack(const BatchDev& b, const uint32_t* rng, uint32_t slots_r, uint32_t slots_m,
+                uint32_t T, void* rrec, void* mrec, cudaStream_t st);
 // Scatter rank-major gathered records back to query order.
-int launch_unpack(const BatchDev& b, uint32_t nq_r, uint32_t nq_m, int world, uint32_t slots_r,
+int launch_unpack(const BatchDev& b, uint32_t max_r, uint32_t max_m, int world, uint32_t slots_r,
                   uint32_t slots_m, uint32_t T, const void* rrec, const void* mrec,
                   cudaStream_t st);
 // Co-resident blocks for the cooperative round kernels.

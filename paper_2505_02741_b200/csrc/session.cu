@@ -134,7 +134,7 @@ struct dyg_session {
 
   // Last-batch outputs (immediate mode / apply_*).
   uint32_t last_dec = 0;
-  uint32_t* d_counts = nullptr;   // [0..1] shard query counts, [2..3] batch kind counts
+  uint32_t* d_counts = nullptr;   // [2..3] batch kind counts, [4..7] shard ranges
   uint32_t* h_counts = nullptr;   // pinned: [0..1] shard counts, [2] decision, [4..5] kinds
   // Multi-GPU split state (dyg_shard_*).
   bool shard_active = false;
@@ -199,6 +199,8 @@ void free_batch(dyg_session* s) {
   dev_free(b.scan_out);
   dev_free(b.rq);
   dev_free(b.mq);
+  dev_free(b.rq_sh);
+  dev_free(b.mq_sh);
   dev_free(b.rout.reached);
   dev_free(b.rout.steps);
   dev_free(b.rout.best_bits);
@@ -251,6 +253,8 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.scan_out, cap, "batch scan");
     dev_alloc(&b.rq, cap, "reach queries");
     dev_alloc(&b.mq, cap, "minpath queries");
+    dev_alloc(&b.rq_sh, cap, "shard reach queries");
+    dev_alloc(&b.mq_sh, cap, "shard minpath queries");
     dev_alloc(&b.rout.reached, cap, "reach out");
     dev_alloc(&b.rout.steps, cap, "reach out");
     dev_alloc(&b.rout.best_bits, cap, "reach out");
@@ -466,12 +470,16 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   const uint32_t* cnt_r = &b.ctl->nq_reach;
   const uint32_t* cnt_m = &b.ctl->nq_min;
   uint32_t max_r = p.n_ins, max_m = p.n_del;
-  if (!full) {
-    p.launches += launch_set_u32x2(s->d_counts, n_r, n_m, s->stream);
-    cnt_r = s->d_counts;
-    cnt_m = s->d_counts + 1;
-    max_r = n_r;
+  const ReachQuery* rq = b.rq;
+  const MinQuery* mq = b.mq;
+  if (!full) {  // a shard range: its queries at [0, n) of rq_sh / mq_sh (launch_shard_range)
+    cnt_r = s->d_counts + 5;
+    cnt_m = s->d_counts + 7;
+    max_r = n_r;  // upper bounds of the range sizes
     max_m = n_m;
+    rq = b.rq_sh;
+    mq = b.mq_sh;
+    lo_r = lo_m = 0;
   }
   // Insertion fast path: G's appends do not depend on the walk (it reads H
   // alone); fork them onto the aux stream so they fill the walk's tail.
@@ -500,7 +508,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
       ro.nq_long = &b.ctl->nq_long;
       ro.cap = b.q_cap;
     }
-    p.launches += launch_reach(s->H.view(), b.rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
+    p.launches += launch_reach(s->H.view(), rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
                                s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
@@ -515,7 +523,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     // k_scatter reset the work counter; a mixed batch's reach walk used it,
     // and a shard range walk may follow another range's walk.
     const bool reset = !full || (p.n_ins > 0 && o.filtering);
-    p.launches += launch_minpath(s->G.view(), b.mq + lo_m, cnt_m, max_m, Pd, b.mscratch, mo,
+    p.launches += launch_minpath(s->G.view(), mq + lo_m, cnt_m, max_m, Pd, b.mscratch, mo,
                                  &b.ctl->minpath, s->d_work, s->stream, reset);
     maybe_sync(s, "minpath walks");
   }
@@ -1401,7 +1409,7 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       check(cudaMemset(s->b.fl_depth, 0, sizeof(uint32_t) * s->n), "flow depths");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
       dev_alloc(&s->b.ctl, 1, "batch ctl");
-      dev_alloc(&s->d_counts, 4, "shard / kind counts");
+      dev_alloc(&s->d_counts, 8, "shard / kind counts");
       check(cudaMallocHost(reinterpret_cast<void**>(&s->h_counts), 8 * sizeof(uint32_t)),
             "pinned counts");
       check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctl), sizeof(BatchCtl)), "pinned ctl");
@@ -1813,13 +1821,13 @@ void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* p
       p.batch = batch_index;
       p.shard = true;
       phase_prepare(s, p);
-      BatchCtl& c = *s->h_ctl;
-      check(cudaMemcpyAsync(&c, s->b.ctl, sizeof c, cudaMemcpyDeviceToHost, s->stream), "ctl");
-      check(cudaStreamSynchronize(s->stream), "shard prepare");
+      // No host round trip: the exchange is sized by upper bounds of the
+      // query counts (a reach query per insertion at most, a min-path query
+      // per deletion); the walk and the commit read the exact counts on the
+      // device. Validation errors surface at dyg_shard_commit.
       s->shard_launches = p.launches;
-      if (c.val_err != ~0ull) fail_validation(s, p, c.val_err);
-      s->shard_nq_r = c.nq_reach;
-      s->shard_nq_m = c.nq_min;
+      s->shard_nq_r = n_ins;
+      s->shard_nq_m = n_del;
     }
     s->shard_active = true;
     if (n_reach) *n_reach = s->shard_nq_r;
@@ -1868,6 +1876,8 @@ int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
       *cnt = static_cast<uint32_t>(b - a);
       *slots = static_cast<uint32_t>((static_cast<uint64_t>(nq) + world - 1) / world);
     };
+    // Slots per rank from the host bounds; the ranges themselves come from
+    // the device counts (launch_shard_range).
     uint32_t lo_r, n_r, sl_r, lo_m, n_m, sl_m;
     range(s->shard_nq_r, &lo_r, &n_r, &sl_r);
     range(s->shard_nq_m, &lo_m, &n_m, &sl_m);
@@ -1878,8 +1888,10 @@ int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
     p.nb = s->shard_nb;
     p.n_ins = s->shard_ins;
     p.n_del = s->shard_del;
-    phase_walk(s, p, false, lo_r, n_r, lo_m, n_m);
-    p.launches += launch_pack(s->b, lo_r, n_r, lo_m, n_m, sl_r, sl_m, s->opt.walk.step_cap,
+    s->b.ctl = p.dctl;
+    p.launches += launch_shard_range(s->b, rank, world, s->d_counts + 4, sl_r, sl_m, s->stream);
+    phase_walk(s, p, false, 0, sl_r, 0, sl_m);
+    p.launches += launch_pack(s->b, s->d_counts + 4, sl_r, sl_m, s->opt.walk.step_cap,
                               reach_records, minpath_records, s->stream);
     // No host sync: the records are consumed in stream order (the all-gather
     // is enqueued on the session's stream).
@@ -1914,6 +1926,7 @@ int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
     p.batch = s->shard_batch;
     p.wall0 = s->shard_wall0;
     p.launches = s->shard_launches;
+    s->b.ctl = p.dctl;
     p.launches += launch_unpack(s->b, s->shard_nq_r, s->shard_nq_m, world, sl_r, sl_m,
                                 s->opt.walk.step_cap, reach_gathered, minpath_gathered, s->stream);
     phase_commit(s, p, out);
