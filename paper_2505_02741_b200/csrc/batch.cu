@@ -1202,12 +1202,17 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
     constexpr uint32_t kWin = 8;
     uint32_t jlo = 0;
     uint32_t mask = count >= kWin ? 0xFFu : ((1u << count) - 1u);
-    uint32_t kw[kWin];  // the window's event indices
-#pragma unroll
-    for (uint32_t i = 0; i < kWin; ++i) kw[i] = i < count ? ev_of(i) : 0u;
+    // The window's event indices (shared memory: registers are the limit
+    // at 4 blocks per SM).
+    __shared__ uint32_t s_kw[8][kWin];
+    uint32_t* kw = s_kw[threadIdx.x >> 5];
+    for (uint32_t i = 0; i < kWin; ++i) {
+      const uint32_t v = i < count ? ev_of(i) : 0u;
+      if (lane == 0) kw[i] = v;
+    }
+    __syncwarp();
     while (mask) {
       bool progressed = false;
-#pragma unroll
       for (uint32_t i = 0; i < kWin; ++i) {
         if (!((mask >> i) & 1u)) continue;
         const uint32_t k = kw[i];
@@ -1243,12 +1248,17 @@ __global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, 
       while (!(mask & 1u) && jlo < count) {
         mask >>= 1;
         ++jlo;
-#pragma unroll
-        for (uint32_t i = 0; i + 1 < kWin; ++i) kw[i] = kw[i + 1];
+        uint32_t nxt = 0;
         if (jlo + kWin - 1 < count) {
           mask |= 1u << (kWin - 1);
-          kw[kWin - 1] = ev_of(jlo + kWin - 1);
+          nxt = ev_of(jlo + kWin - 1);
         }
+        __syncwarp();
+        if (lane == 0) {
+          for (uint32_t i = 0; i + 1 < kWin; ++i) kw[i] = kw[i + 1];
+          kw[kWin - 1] = nxt;
+        }
+        __syncwarp();
       }
       if (!progressed) __nanosleep(64);
     }
