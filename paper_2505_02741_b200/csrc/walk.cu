@@ -674,6 +674,8 @@ int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_d
     case 2: launch_walk<C, false, 2, 8, 3>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
     case 3: launch_walk<C, false, 2, 4, 5>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
     case 4: launch_walk<C, false, 3, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
+    case 5: launch_walk<C, false, 1, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
+    case 6: launch_walk<C, false, 1, 4, 6>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
     default: launch_walk<C, false, 2, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
   }
   if (standalone) {
