@@ -334,8 +334,7 @@ def run_ours(args):
         if sharded is None:
             st.replay_uploaded_range(0, nb)  # device-resident replay(stream)
             return
-        for b in range(nb):
-            sharded.replay_uploaded(b)
+        sharded.replay_uploaded_range(0, nb)
 
     def step_e2e():
         # The reference-facing replay(stream) from the host stream (page-locked

@@ -360,6 +360,16 @@ int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
                    void* minpath_records);
 int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
                      const void* minpath_gathered, dyg_batch_report* out);
+/* The commit enqueued without waiting: the next dyg_shard_begin plans its
+ * update counter and pool headroom past it, so a whole range of batches is
+ * enqueued with no host round trip (a failed batch raises the device abort
+ * flag and the later ones do nothing, as in dyg_replay_uploaded_range).
+ * dyg_shard_finish waits, then returns the pending batches' reports in order
+ * (up to `cap`; *n_out = reports produced) and fails at the first failing
+ * batch. At most 256 commits may be pending. */
+int dyg_shard_commit_async(dyg_session* s, int world, const void* reach_gathered,
+                           const void* minpath_gathered);
+int dyg_shard_finish(dyg_session* s, dyg_batch_report* out, size_t cap, size_t* n_out);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

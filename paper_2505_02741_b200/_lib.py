@@ -144,6 +144,8 @@ def lib() -> C.CDLL:
                                            C.POINTER(C.c_uint64)]),
         "dyg_shard_walk": (i32, [vp, i32, i32, vp, vp]),
         "dyg_shard_commit": (i32, [vp, i32, vp, vp, vp]),
+        "dyg_shard_commit_async": (i32, [vp, i32, vp, vp]),
+        "dyg_shard_finish": (i32, [vp, vp, sz, C.POINTER(C.c_size_t)]),
         "dygh_last_error": (C.c_char_p, []),
         "dygh_graph_new": (i32, [u32, pvp]),
         "dygh_graph_from_csr": (i32, [C.POINTER(Csr), pvp]),

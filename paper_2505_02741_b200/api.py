@@ -481,6 +481,17 @@ class SparsifierState:
                                            C.c_void_p(min_ptr), ptr(rep)))
         return BatchReport.from_record(rep[0])
 
+    def shard_commit_async(self, world, reach_ptr, min_ptr) -> None:
+        _check(_lib.lib().dyg_shard_commit_async(self._s, world, C.c_void_p(reach_ptr),
+                                                 C.c_void_p(min_ptr)))
+
+    def shard_finish(self, max_reports: int = 256):
+        """Reports of the pending asynchronous shard commits, in order."""
+        reps = np.zeros(max(int(max_reports), 1), REPORT_DTYPE)
+        n = C.c_size_t(0)
+        _check(_lib.lib().dyg_shard_finish(self._s, ptr(reps), int(max_reports), C.byref(n)))
+        return [BatchReport.from_record(reps[i]) for i in range(min(n.value, max_reports))]
+
     def set_stream(self, cuda_stream_handle: int) -> None:
         _check(_lib.lib().dyg_set_stream(self._s, C.c_void_p(cuda_stream_handle)))
 

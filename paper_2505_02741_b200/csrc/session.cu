@@ -96,6 +96,10 @@ uint64_t fnv(uint64_t h, const void* p, size_t n) {
 
 }  // namespace
 
+namespace {
+struct Pending;  // one batch in flight (below)
+}  // namespace
+
 struct dyg_session {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -146,6 +150,13 @@ struct dyg_session {
   std::chrono::steady_clock::time_point shard_wall0;
   int shard_launches = 0;
   uint64_t shard_counter = 0;
+  // Asynchronous shard commits (dyg_shard_commit_async) not yet finalised:
+  // their control blocks land in a pinned ring; the next batch plans its
+  // update counter and pool headroom past them.
+  std::vector<Pending> shard_pending;
+  BatchCtl* h_shard_ctls = nullptr;
+  uint64_t shard_next_counter = 0;
+  uint64_t shard_pend_g = 0, shard_pend_h = 0;
 
   dyg_stats stats{};
   BatchCtl* d_ctls = nullptr;      // batch-range control blocks
@@ -425,8 +436,9 @@ void ensure_pools(dyg_session* s, uint64_t n_ins, uint64_t n_del) {
   const uint64_t T1 = static_cast<uint64_t>(s->opt.walk.step_cap) + 1;
   const uint64_t g_app = 2ull * n_ins;
   const uint64_t h_app = 2ull * n_ins + n_del * (2 * T1 + 4);
-  s->G.ensure_pool(s->g_top, 4 * g_app + (1u << 16), s->stream);
-  s->H.ensure_pool(s->h_top, 4 * h_app + (1u << 16), s->stream);
+  // (+ the worst-case appends of asynchronous shard commits not yet read back)
+  s->G.ensure_pool(s->g_top + s->shard_pend_g, 4 * g_app + (1u << 16), s->stream);
+  s->H.ensure_pool(s->h_top + s->shard_pend_h, 4 * h_app + (1u << 16), s->stream);
 }
 
 // validate (:405-407), walk shadow (:416-423), query build (:429-457).
@@ -1478,6 +1490,7 @@ void dyg_session_destroy(dyg_session* s) {
   dev_free(s->d_counts);
   dev_free(s->d_ctls);
   if (s->h_ctls) cudaFreeHost(s->h_ctls);
+  if (s->h_shard_ctls) cudaFreeHost(s->h_shard_ctls);
   dev_free(s->d_abort);
   dev_free(s->d_epoch);
   s->G.release();
@@ -1805,13 +1818,17 @@ void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* p
     s->shard_del = n_del;
     s->shard_batch = batch_index;
     s->shard_wall0 = std::chrono::steady_clock::now();
-    s->shard_counter = s->counter;
+    const bool chained = !s->shard_pending.empty();  // after asynchronous commits
+    s->shard_counter = chained ? s->shard_next_counter : s->counter;
     s->shard_nq_r = s->shard_nq_m = 0;
     if (n > 0) {
       ensure_batch(s, static_cast<uint32_t>(n), n_del);
       Pending p;
       bind_pending(s, p);
-      reset_abort(s);
+      p.counter_base = s->shard_counter;
+      // A chained batch keeps the device abort flag: after a failed earlier
+      // batch it does nothing (as in a range replay).
+      if (!chained) reset_abort(s);
       p.dev = s->shard_dev;
       p.host = s->shard_host;
       p.pos = s->shard_pos;
@@ -1900,18 +1917,11 @@ int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
   });
 }
 
-int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
-                     const void* minpath_gathered, dyg_batch_report* out) {
-  return guarded([&] {
-    if (s == nullptr || out == nullptr || !s->shard_active)
-      fail(DYG_ERR_USAGE, "no shard batch in progress");
-    if (world < 1) fail(DYG_ERR_USAGE, "invalid world");
-    check(cudaSetDevice(s->device), "set device");
-    s->shard_active = false;
-    if (s->shard_nb == 0) {
-      empty_report(s, s->shard_batch, out);
-      return;
-    }
+namespace {
+// The commit-side Pending of the shard batch in progress, with the unpack of
+// the gathered records enqueued.
+Pending shard_commit_pending(dyg_session* s, int world, const void* reach_gathered,
+                             const void* minpath_gathered) {
     const uint32_t sl_r = static_cast<uint32_t>((s->shard_nq_r + world - 1ull) / world);
     const uint32_t sl_m = static_cast<uint32_t>((s->shard_nq_m + world - 1ull) / world);
     Pending p;
@@ -1929,7 +1939,78 @@ int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
     s->b.ctl = p.dctl;
     p.launches += launch_unpack(s->b, s->shard_nq_r, s->shard_nq_m, world, sl_r, sl_m,
                                 s->opt.walk.step_cap, reach_gathered, minpath_gathered, s->stream);
+    return p;
+}
+}  // namespace
+
+int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
+                     const void* minpath_gathered, dyg_batch_report* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr || !s->shard_active)
+      fail(DYG_ERR_USAGE, "no shard batch in progress");
+    if (world < 1) fail(DYG_ERR_USAGE, "invalid world");
+    if (!s->shard_pending.empty())
+      fail(DYG_ERR_USAGE, "asynchronous shard commits pending: call dyg_shard_finish first");
+    check(cudaSetDevice(s->device), "set device");
+    s->shard_active = false;
+    if (s->shard_nb == 0) {
+      empty_report(s, s->shard_batch, out);
+      return;
+    }
+    Pending p = shard_commit_pending(s, world, reach_gathered, minpath_gathered);
     phase_commit(s, p, out);
+  });
+}
+
+int dyg_shard_commit_async(dyg_session* s, int world, const void* reach_gathered,
+                           const void* minpath_gathered) {
+  return guarded([&] {
+    if (s == nullptr || !s->shard_active) fail(DYG_ERR_USAGE, "no shard batch in progress");
+    if (world < 1) fail(DYG_ERR_USAGE, "invalid world");
+    constexpr size_t kRing = 256;
+    if (s->shard_pending.size() >= kRing)
+      fail(DYG_ERR_USAGE, "too many asynchronous shard commits: call dyg_shard_finish");
+    check(cudaSetDevice(s->device), "set device");
+    if (s->h_shard_ctls == nullptr)
+      check(cudaMallocHost(reinterpret_cast<void**>(&s->h_shard_ctls), sizeof(BatchCtl) * kRing),
+            "pinned shard control blocks");
+    s->shard_active = false;
+    Pending p;
+    if (s->shard_nb == 0) {  // an empty batch: reported at finish
+      p.batch = s->shard_batch;
+      p.nb = 0;
+      s->shard_pending.push_back(p);
+      s->shard_next_counter = s->shard_counter;
+      return;
+    }
+    p = shard_commit_pending(s, world, reach_gathered, minpath_gathered);
+    p.hctl = s->h_shard_ctls + s->shard_pending.size();
+    commit_enqueue(s, p, true);
+    s->shard_pending.push_back(p);
+    s->shard_next_counter = p.counter_base + p.nb;
+    const uint64_t T1 = static_cast<uint64_t>(s->opt.walk.step_cap) + 1;
+    s->shard_pend_g += 2ull * p.n_ins;
+    s->shard_pend_h += 2ull * p.n_ins + p.n_del * (2 * T1 + 4);
+  });
+}
+
+int dyg_shard_finish(dyg_session* s, dyg_batch_report* out, size_t cap, size_t* n_out) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    if (n_out) *n_out = 0;
+    if (s->shard_pending.empty()) return;
+    check(cudaSetDevice(s->device), "set device");
+    std::vector<Pending> ps;
+    ps.swap(s->shard_pending);
+    s->shard_pend_g = s->shard_pend_h = 0;
+    check(cudaStreamSynchronize(s->stream), "shard commits");
+    for (size_t i = 0; i < ps.size(); ++i) {
+      dyg_batch_report rep{};
+      if (ps[i].nb == 0) empty_report(s, ps[i].batch, &rep);
+      else commit_finalize(s, ps[i], &rep);  // throws at the first failing batch
+      if (out && i < cap) out[i] = rep;
+      if (n_out) *n_out = i + 1;
+    }
   });
 }
 

@@ -89,7 +89,7 @@ class ShardedReplay:
             self._bufs[key] = b
         return b[:nbytes]
 
-    def _exchange(self, nr, nm):
+    def _exchange(self, nr, nm, commit=True):
         sr, sm = slots_per_rank(nr, self.world), slots_per_rank(nm, self.world)
         rloc = self._buf("rloc", sr * self.rbytes)
         mloc = self._buf("mloc", sm * self.mbytes)
@@ -98,6 +98,12 @@ class ShardedReplay:
         rall = self._gather("rall", rloc)
         mall = self._gather("mall", mloc)
         self.bytes_exchanged += rall.numel() + mall.numel()
+        if not commit:
+            # Enqueued only: the record buffers are reused by the next batch in
+            # stream order, after this batch's unpack has read them.
+            self.state.shard_commit_async(self.world, rall.data_ptr() if sr else 0,
+                                          mall.data_ptr() if sm else 0)
+            return None
         return self.state.shard_commit(self.world, rall.data_ptr() if sr else 0,
                                        mall.data_ptr() if sm else 0)
 
@@ -117,3 +123,14 @@ class ShardedReplay:
         """Batch `batch_index` of the stream given to state.upload_stream."""
         nr, nm = self.state.shard_begin_uploaded(batch_index)
         return self._exchange(nr, nm)
+
+    def replay_uploaded_range(self, first: int, count: int):
+        """Batches [first, first + count) of the uploaded stream with no host
+        round trip between them (asynchronous commits); their reports."""
+        reports = []
+        for b in range(first, first + count):
+            nr, nm = self.state.shard_begin_uploaded(b)
+            self._exchange(nr, nm, commit=False)
+            if len(reports) + 256 <= b - first + 1:  # the pending ring is 256 deep
+                reports += self.state.shard_finish()
+        return reports + self.state.shard_finish()

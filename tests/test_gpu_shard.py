@@ -41,3 +41,39 @@ def test_sharded_replay_equals_single(oracle, dyg, world, uploaded):
             assert getattr(r1, f) == getattr(r2, f), (world, b, f)
     assert same_rows(ref.rows(0), sh.rows(0)) and same_rows(ref.rows(1), sh.rows(1))
     assert ref.update_counter == sh.update_counter
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_sharded_async_commits_equal_single(oracle, dyg, world):
+    """dyg_shard_commit_async for every batch, one dyg_shard_finish at the end:
+    the batches chain on the device (planned update counter and pool
+    headroom) and must still equal the unsharded replay bit for bit."""
+    import torch
+
+    c = O.CONFIGS["C2"]
+    g, h, s = O.build_config(oracle, c)
+    opts = dyg.SparsifierOptions(dyg.WalkConfig(c.K, c.T, c.s, c.walk_seed), True, False)
+    ref = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
+    sh = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
+    stream = dyg.UpdateStream(s.events(), s.batch_count)
+    sh.upload_stream(stream)
+    rb, mb = sh.shard_record_bytes(False), sh.shard_record_bytes(True)
+    keep = []  # record buffers live until the commits have run
+    for b in range(s.batch_count):
+        nr, nm = sh.shard_begin_uploaded(b)
+        sr, sm = -(-nr // world), -(-nm // world)
+        rall = torch.zeros(max(1, world * sr * rb), dtype=torch.uint8, device="cuda")
+        mall = torch.zeros(max(1, world * sm * mb), dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        for r in range(world):
+            sh.shard_walk(r, world, rall.data_ptr() + r * sr * rb, mall.data_ptr() + r * sm * mb)
+        sh.shard_commit_async(world, rall.data_ptr(), mall.data_ptr())
+        keep += [rall, mall]
+    reps = sh.shard_finish()
+    assert len(reps) == s.batch_count
+    for b in range(s.batch_count):
+        r1 = ref.replay_batch(stream, b)
+        for f in O.REPORT_EXACT:
+            assert getattr(r1, f) == getattr(reps[b], f), (world, b, f)
+    assert same_rows(ref.rows(0), sh.rows(0)) and same_rows(ref.rows(1), sh.rows(1))
+    assert ref.update_counter == sh.update_counter
