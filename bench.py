@@ -440,7 +440,7 @@ def run_ours(args):
             "K": K_BUDGET, "T": T_CAP, "s": WALKERS, "walk_seed": WALK_SEED,
             "parallelism": (f"replicated G/H, walks sharded x{world}" if (world > 1 or force_shard)
                             else "1 GPU"),
-            "l2": "inputs larger than L2 (G slabs 537 MB + H slabs 268 MB > 126 MB)",
+            "l2": "inputs larger than L2 (G slabs 537 MB + H slabs 403 MB > 126 MB)",
         },
         "e2e": {
             "value": rep_events / (e2e_ms * 1e-3), "unit": UNIT,
