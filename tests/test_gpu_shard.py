@@ -77,3 +77,48 @@ def test_sharded_async_commits_equal_single(oracle, dyg, world):
             assert getattr(r1, f) == getattr(reps[b], f), (world, b, f)
     assert same_rows(ref.rows(0), sh.rows(0)) and same_rows(ref.rows(1), sh.rows(1))
     assert ref.update_counter == sh.update_counter
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_sharded_async_stops_at_failing_batch(oracle, dyg, world):
+    """A failing batch inside a chain of asynchronous shard commits: the
+    device abort flag stops the later batches (already enqueued), and
+    dyg_shard_finish reports the reference's error for the failing one."""
+    import torch
+
+    g = oracle.make_mesh(9, 9, 3)
+    h = oracle.build_initial_sparsifier(g, 0.1, 3)
+    rp, ids, _ = g.export()
+    edges = [(u, int(ids[i])) for u in range(len(rp) - 1) for i in range(rp[u], rp[u + 1])
+             if u < ids[i]]
+    ev = [(0, 0, 40, 0, 1.0), (0, 1, 50, 0, 1.0),            # batch 0: insertions
+          (1, edges[0][0], edges[0][1], 1, 0.0),             # batch 1: deletions,
+          (1, edges[0][0], edges[0][1], 1, 0.0),             #   the second fails
+          (0, 2, 60, 2, 1.0)]                                # batch 2: never commits
+    ev = np.array(ev, dtype=O.EVENT_DTYPE)
+    ost = oracle.state(g, h, K=10.0, T=30, s=8, seed=3)
+    ostream = oracle.stream(ev, 3)
+    ost.replay_batch(ostream, 0)
+    with pytest.raises(O.OracleError) as oe:
+        ost.replay_batch(ostream, 1)
+    sh = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h),
+                             dyg.SparsifierOptions(dyg.WalkConfig(10.0, 30, 8, 3), True, False))
+    sh.upload_stream(dyg.UpdateStream(ev, 3))
+    rb, mb = sh.shard_record_bytes(False), sh.shard_record_bytes(True)
+    keep = []
+    for b in range(3):
+        nr, nm = sh.shard_begin_uploaded(b)
+        sr, sm = -(-nr // world), -(-nm // world)
+        rall = torch.zeros(max(1, world * sr * rb), dtype=torch.uint8, device="cuda")
+        mall = torch.zeros(max(1, world * sm * mb), dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        for r in range(world):
+            sh.shard_walk(r, world, rall.data_ptr() + r * sr * rb, mall.data_ptr() + r * sm * mb)
+        sh.shard_commit_async(world, rall.data_ptr(), mall.data_ptr())
+        keep += [rall, mall]
+    with pytest.raises(dyg.Error) as de:
+        sh.shard_finish()
+    assert str(de.value) == oe.value.message
+    assert sh.update_counter == ost.update_counter
+    assert same_rows(ost.graph().export(), sh.rows(0))
+    assert same_rows(ost.sparsifier().export(), sh.rows(1))
