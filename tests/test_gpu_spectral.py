@@ -122,3 +122,20 @@ def test_errors(mesh):
     assert ei.value.kind == D.ErrorKind.Data
     r = D.pcg_solve(g, np.ones(g.vertex_count()))  # zero after centring
     assert r.converged and r.iterations == 0 and not r.solution.any()
+
+
+def test_session_spectral_after_updates(mesh):
+    """The session overloads read the CURRENT graph and sparsifier (after a
+    replay), not the ones the session was created with."""
+    g, h = mesh
+    st = D.SparsifierState(g, h, D.SparsifierOptions(D.WalkConfig(10.0, 100, 16, 42), True, False))
+    s = D.generate_update_stream(g, D.StreamGenOptions(0.2, 0.05, 2, 9, 0))
+    st.replay(s)
+    g2, h2 = st.graph(), st.sparsifier()
+    e_state = D.condition_number(st)
+    e_rows = D.condition_number(g2, h2)
+    assert e_state.kappa == pytest.approx(e_rows.kappa, rel=1e-12)
+    d = S.condition_dense(S.laplacian(*rows(g2)), S.laplacian(*rows(h2)))
+    assert e_state.kappa == pytest.approx(d["kappa"], rel=1e-9)
+    assert D.calibrate_budget(st, probe_fraction=0.05, rho=1.0) == pytest.approx(
+        min(max(d["kappa"], 1.0), 1e6), rel=1e-9)
