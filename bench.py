@@ -274,7 +274,8 @@ def gather_block(stats, n):
     out = {}
     for key, ms, steps, row, table in (
             ("k_reach", stats["reach_ms"], stats["reach_steps"], 64, 96 * n / 2**20),
-            ("k_minpath", stats["minpath_ms"], stats["minpath_steps"], 128, 128 * n / 2**20)):
+            ("k_minpath", stats["minpath_walk_ms"], stats["minpath_steps"], 128,
+             128 * n / 2**20)):
         if ms <= 0:
             continue
         rate = steps / (ms * 1e-3)
@@ -282,6 +283,8 @@ def gather_block(stats, n):
         out[key] = {"steps_per_s": rate, "row_bytes": row, "table_mb": round(table, 1),
                     "ceiling_rows_per_s": ceil, "frac": rate / ceil}
     out["source"] = "profiles/gather_peak_r1.txt (tools/gather_peak.cu, measured on this pool)"
+    out["durations"] = ("device stamps per launch: K1 first warp start to last warp exit; "
+                        "K2 likewise (the winner kernel K3 excluded)")
     return out
 
 

@@ -153,6 +153,7 @@ typedef struct dyg_stats {
   double prep_ms;               /* batch start -> first walk warp (validation, query build) */
   double walk_commit_gap_ms;    /* last walk warp -> commit start */
   double batch_gap_ms;          /* previous batch end -> batch start, inside one replay */
+  double minpath_walk_ms;       /* the min-path walk kernel alone (minpath_ms adds the winner) */
 } dyg_stats;
 
 typedef struct dyg_session dyg_session;

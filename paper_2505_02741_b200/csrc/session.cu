@@ -612,6 +612,7 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   // 8 per batch were 0.67 ms of a 10 ms C5 step).
   s->stats.reach_ms += span_ms(c.reach.t_start, c.reach.t_end);
   s->stats.minpath_ms += span_ms(c.minpath.t_start, c.t_mp_end);
+  s->stats.minpath_walk_ms += span_ms(c.minpath.t_start, c.minpath.t_end);
   s->stats.commit_ms += span_ms(c.t_commit0, c.t_batch1);
   s->stats.total_ms += span_ms(c.t_batch0, c.t_batch1);
   {
