@@ -775,9 +775,9 @@ ConditionResult condition_lanczos_device(const DevLap& G, const DevLap& H,
   double* mpart = nullptr;
   constexpr int kChunks = 64;
   mpart = salloc<double>(static_cast<size_t>(kChunks) * (limit + 1ull), "gs partials");
+  std::vector<double*> blocks;  // basis storage, kBlockCols column pairs per allocation
   auto cleanup = [&] {
-    for (double* v : basis) cudaFree(v);
-    for (double* v : basis_b) cudaFree(v);
+    for (double* v : blocks) cudaFree(v);
     cudaFree(d_basis);
     cudaFree(d_basis_b);
     cudaFree(coef);
@@ -800,15 +800,14 @@ ConditionResult condition_lanczos_device(const DevLap& G, const DevLap& H,
     e.lap(H, q, bq);
     const double norm0 = std::sqrt(e.dot(q, bq));
     if (!(norm0 > 0.0)) sfail(3, "degenerate Lanczos start vector");
+    constexpr size_t kBlockCols = 32;  // one allocation per 32 basis columns (q and L_H q)
     auto push = [&](const double* v, const double* bv, double s) {
-      double* c = salloc<double>(n, "basis vector");
-      double* cb = nullptr;
-      try {
-        cb = salloc<double>(n, "basis vector");
-      } catch (...) {
-        cudaFree(c);
-        throw;
-      }
+      const size_t j = basis.size();
+      if (j % kBlockCols == 0)
+        blocks.push_back(salloc<double>(2 * kBlockCols * static_cast<size_t>(n), "basis block"));
+      double* blk = blocks.back() + 2 * (j % kBlockCols) * static_cast<size_t>(n);
+      double* c = blk;
+      double* cb = blk + n;
       basis.push_back(c);
       basis_b.push_back(cb);
       e.copy(c, v);
