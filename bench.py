@@ -208,16 +208,28 @@ def cpu_baseline(cfg: str):
     ins_b = 0
     del_b = nb // 2 if nb > 10 else None
     events, wall = 0, 0.0
-    for b in [ins_b] + ([del_b] if del_b is not None else []):
+    split = {}
+    for name, b in [("insertion", ins_b)] + ([("deletion", del_b)] if del_b is not None else []):
         st = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED)
         sel = ev[ev["batch_index"] == b].copy()
         sel["batch_index"] = 0
         t = time.perf_counter()
         st.replay_batch(orc.stream(sel, 1), 0)
-        wall += time.perf_counter() - t
+        dt = time.perf_counter() - t
+        wall += dt
         events += len(sel)
+        split[name] = {"events": int(len(sel)), "s": round(dt, 3),
+                       "edge_updates_per_s": len(sel) / dt}
+    cpu_model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")),
+                             "")
+    except OSError:
+        pass
     return {"value": events / wall, "unit": UNIT,
             "cores": cores if kind == "reference" else 1, "kind": kind,
+            "per_batch_kind": split, "cpu_model": cpu_model, "nproc": os.cpu_count(),
             "sample": (f"{cfg}: insertion batch 0 + deletion batch {del_b} replayed from the "
                        f"initial state ({events} events, {wall:.2f} s, setup {setup:.1f} s "
                        "excluded), SparsifierState::replay_batch batched mode")}
