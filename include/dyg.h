@@ -343,7 +343,11 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
  * caller sizes buffers without a host round trip; the exact counts stay on
  * the device. Begin and walk only enqueue (stream order); validation errors
  * surface at dyg_shard_commit. The event and position buffers passed to dyg_shard_begin
- * must stay valid until dyg_shard_commit returns (error messages read them).
+ * must stay valid until the batch's commit is reported -- dyg_shard_commit, or
+ * dyg_shard_finish after dyg_shard_commit_async (error messages read them).
+ * While asynchronous commits are pending, every other entry point that reads
+ * or writes the session's state fails with DYG_ERR_USAGE, and
+ * dyg_update_counter / dyg_last_event_steps report the last settled state.
  * The session stream may be replaced by the caller's (dyg_set_stream) so
  * the collective is stream-ordered with the kernels. */
 int dyg_set_stream(dyg_session* s, void* cuda_stream);

@@ -326,6 +326,7 @@ class SparsifierState:
         L = _lib.lib()
         self._options = options
         self._s = None
+        self._shard_keep = []
         g, h = graph.csr(), sparsifier.csr()
         opt = _options_struct(options)
         s = C.c_void_p()
@@ -455,7 +456,9 @@ class SparsifierState:
     def shard_begin(self, events, positions, batch_index):
         ev = np.ascontiguousarray(events, EVENT_DTYPE)
         pos = np.ascontiguousarray(positions, np.uint64)
-        self._shard_keep = (ev, pos)  # the library reads them until shard_commit
+        # The library reads them (error messages) until the batch's commit has
+        # been reported: shard_commit, or shard_finish for asynchronous commits.
+        self._shard_keep.append((ev, pos))
         nr, nm = C.c_uint64(), C.c_uint64()
         _check(_lib.lib().dyg_shard_begin(self._s, ptr(ev), ptr(pos), len(ev), batch_index,
                                           C.byref(nr), C.byref(nm)))
@@ -477,8 +480,11 @@ class SparsifierState:
 
     def shard_commit(self, world, reach_ptr, min_ptr) -> BatchReport:
         rep = np.zeros(1, REPORT_DTYPE)
-        _check(_lib.lib().dyg_shard_commit(self._s, world, C.c_void_p(reach_ptr),
-                                           C.c_void_p(min_ptr), ptr(rep)))
+        try:
+            _check(_lib.lib().dyg_shard_commit(self._s, world, C.c_void_p(reach_ptr),
+                                               C.c_void_p(min_ptr), ptr(rep)))
+        finally:
+            self._shard_keep.clear()
         return BatchReport.from_record(rep[0])
 
     def shard_commit_async(self, world, reach_ptr, min_ptr) -> None:
@@ -489,7 +495,11 @@ class SparsifierState:
         """Reports of the pending asynchronous shard commits, in order."""
         reps = np.zeros(max(int(max_reports), 1), REPORT_DTYPE)
         n = C.c_size_t(0)
-        _check(_lib.lib().dyg_shard_finish(self._s, ptr(reps), int(max_reports), C.byref(n)))
+        try:
+            _check(_lib.lib().dyg_shard_finish(self._s, ptr(reps), int(max_reports),
+                                               C.byref(n)))
+        finally:
+            self._shard_keep.clear()
         return [BatchReport.from_record(reps[i]) for i in range(min(n.value, max_reports))]
 
     def set_stream(self, cuda_stream_handle: int) -> None:

@@ -2054,17 +2054,7 @@ int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const Batc
     uint32_t nev = nb;
     void* args[] = {&op_copy, &nev, &b_copy};
     const int need = static_cast<int>(grid_for(static_cast<uint64_t>(nb) * 32));
-    int cap = coop_blocks_for(k_del_flow);
-    static const int per_sm = [] {  // DYG_FLOW_BLOCKS: resident blocks per SM (tuning)
-      const char* e = std::getenv("DYG_FLOW_BLOCKS");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (per_sm > 0) {
-      int dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cap = std::min(cap, per_sm * sms);
-    }
+    const int cap = coop_blocks_for(k_del_flow);
     cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_del_flow),
                                            dim3(need < cap ? need : cap), dim3(256), args, 0, st),
                "cooperative flow launch");

@@ -499,11 +499,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   // The fork point is recorded before the walk, but the aux kernels are
   // enqueued after it: the walk's blocks claim the SMs first (its start is
   // on the batch's critical path; the appends only need to finish by the
-  // commit). DYG_FORK_FIRST=1 enqueues the appends first.
-  static const bool fork_first = [] {
-    const char* e = std::getenv("DYG_FORK_FIRST");
-    return e && std::atoi(e) != 0;
-  }();
+  // commit).
   auto fork_appends = [&] {
     check(cudaStreamWaitEvent(s->aux_stream, s->ev_fork, 0), "fork");
     p.launches += launch_fastpath_g(s->G.view(), b, p.nb, s->aux_stream);
@@ -512,7 +508,6 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   };
   if (full && fast) {
     check(cudaEventRecord(s->ev_fork, s->stream), "fork");
-    if (fork_first) fork_appends();
   }
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
     ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r, nullptr, 0};
@@ -524,7 +519,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                                s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
-  if (full && fast && !fork_first) fork_appends();
+  if (full && fast) fork_appends();
   if (p.g_appended) check(cudaStreamWaitEvent(s->stream, s->ev_join, 0), "join");
   if (p.n_del > 0 && !o.freeze && max_m > 0) {
     WalkParams Pd = P;
@@ -1502,9 +1497,18 @@ void dyg_session_destroy(dyg_session* s) {
   delete s;
 }
 
+// Asynchronous shard commits leave the host-side counter, edge counts and
+// pool tops behind the device until dyg_shard_finish; every other entry
+// point that reads or writes session state refuses to run until then.
+static void require_settled(const dyg_session* s) {
+  if (s != nullptr && !s->shard_pending.empty())
+    fail(DYG_ERR_USAGE, "asynchronous shard commits pending: call dyg_shard_finish first");
+}
+
 int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* positions,
                       size_t n, uint32_t batch_index, dyg_batch_report* out) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || out == nullptr || (n && events == nullptr))
       fail(DYG_ERR_USAGE, "null argument");
     check(cudaSetDevice(s->device), "set device");
@@ -1520,6 +1524,7 @@ int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* p
 int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
                      uint32_t batch_count, uint32_t batch_index, dyg_batch_report* out) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || out == nullptr || (n_events && events == nullptr))
       fail(DYG_ERR_USAGE, "null argument");
     // sparsifier.cpp:541-548
@@ -1544,6 +1549,7 @@ int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
 int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
                       uint32_t batch_count) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || (n_events && events == nullptr)) fail(DYG_ERR_USAGE, "null argument");
     check(cudaSetDevice(s->device), "set device");
     uint32_t nbatches = batch_count;
@@ -1578,6 +1584,7 @@ int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
 
 int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* out) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
     if (!s->have_stream) fail(DYG_ERR_USAGE, "no stream uploaded");
     if (batch_index >= s->stream_batches && s->stream_batches > 0)
@@ -1605,6 +1612,7 @@ int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* 
 int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
                               dyg_batch_report* out) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || (count && out == nullptr)) fail(DYG_ERR_USAGE, "null argument");
     if (!s->have_stream) fail(DYG_ERR_USAGE, "no stream uploaded");
     if (count && static_cast<uint64_t>(first) + count > s->stream_batches && s->stream_batches > 0)
@@ -1619,6 +1627,7 @@ int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
                       const uint64_t* batch_offsets, uint32_t batch_count,
                       dyg_batch_report* out) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || (batch_count && out == nullptr) || (n_events && events == nullptr))
       fail(DYG_ERR_USAGE, "null argument");
     check(cudaSetDevice(s->device), "set device");
@@ -1663,6 +1672,7 @@ int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
 
 int dyg_apply_insertion(dyg_session* s, uint32_t u, uint32_t v, double w, int* decision) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     check(cudaSetDevice(s->device), "set device");
     // apply_insertion validates through insert_edge (graph.cpp:64-73).
@@ -1684,6 +1694,7 @@ int dyg_apply_insertion(dyg_session* s, uint32_t u, uint32_t v, double w, int* d
 
 int dyg_apply_deletion(dyg_session* s, uint32_t u, uint32_t v, int* kind, uint32_t* edges_added) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     check(cudaSetDevice(s->device), "set device");
     if (u >= s->n || v >= s->n) {
@@ -1716,6 +1727,7 @@ uint64_t dyg_update_counter(const dyg_session* s) { return s ? s->counter : 0; }
 
 int dyg_graph_info(const dyg_session* s, int which, uint32_t* n, uint64_t* edges, double* density) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     const uint64_t e = which == 0 ? s->g_edges : s->h_edges;
     if (n) *n = s->n;
@@ -1727,6 +1739,7 @@ int dyg_graph_info(const dyg_session* s, int which, uint32_t* n, uint64_t* edges
 int dyg_export_rows(dyg_session* s, int which, uint64_t* row_ptr, uint32_t* ids, double* w,
                     uint64_t capacity) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || row_ptr == nullptr) fail(DYG_ERR_USAGE, "null argument");
     check(cudaSetDevice(s->device), "set device");
     const uint64_t nnz = which == 0 ? s->G.export_rows(row_ptr, ids, w, capacity, s->stream)
@@ -1737,6 +1750,7 @@ int dyg_export_rows(dyg_session* s, int which, uint64_t* row_ptr, uint32_t* ids,
 
 int dyg_session_snapshot(dyg_session* s) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     check(cudaSetDevice(s->device), "set device");
     s->G_snap.copy_from(s->G, s->stream);
@@ -1753,6 +1767,7 @@ int dyg_session_snapshot(dyg_session* s) {
 
 int dyg_session_restore(dyg_session* s) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     if (!s->have_snap) fail(DYG_ERR_USAGE, "no snapshot taken");
     check(cudaSetDevice(s->device), "set device");
@@ -1787,6 +1802,7 @@ int dyg_session_reset_stats(dyg_session* s) {
 
 int dyg_set_stream(dyg_session* s, void* cuda_stream) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     check(cudaStreamSynchronize(s->stream), "set stream");
     if (s->own_stream) cudaStreamDestroy(s->stream);
@@ -2071,6 +2087,7 @@ void export_owned(dyg_session* s, int which, OwnedCsr& o) {
 int dyg_session_condition_number(dyg_session* s, const dyg_condition_options* options,
                                  dyg_condition_estimate* out) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
     OwnedCsr g, h;
     export_owned(s, 0, g);
@@ -2083,6 +2100,7 @@ int dyg_session_condition_number(dyg_session* s, const dyg_condition_options* op
 int dyg_session_calibrate_budget(dyg_session* s, double probe_fraction, double rho,
                                  double* budget) {
   return guarded([&] {
+    require_settled(s);
     if (s == nullptr || budget == nullptr) fail(DYG_ERR_USAGE, "null argument");
     OwnedCsr g, h;
     export_owned(s, 0, g);

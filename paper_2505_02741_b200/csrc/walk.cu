@@ -181,22 +181,16 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long lo
   }
 }
 
-// K1/K2 as persistent, software-pipelined lane-refill kernels.
+// K1/K2 as persistent lane-refill kernels.
 //
 // Refill: walk lengths are long-tailed (most insertion walkers dead-end
 // within a few steps, a few run to T), so a static lane<->walker mapping
 // leaves most lanes idle (ncu: 6.4 of 32 lanes active). A lane that finishes
 // a walker takes the next work item (query = w / s, walker = w % s) from a
 // warp-local chunk of 32 items whose queries are prefetched with one
-// coalesced load (one global atomic per 32 walkers).
-//
-// Pipelining: every lane carries NS walker SLOTS. Each slot has its own
-// staging buffer and cp.async group; while slot k's sample runs, the row
-// fetches of the other slots are in flight (wait_group NS-1 retires exactly
-// the oldest group). ncu on the single-slot kernel: 50 % of warp stalls were
-// the dependent row fetch and the schedulers idled half the cycles with the
-// issue slots only 47 % busy -- the fetch of one walker now overlaps the
-// arithmetic of another.
+// coalesced load (one global atomic per 32 walkers). Latency is hidden by
+// resident warps (24 / 16 per SM), not by several walker slots per lane:
+// 2-3 slots with pipelined cp.async groups measured slower (DESIGN 4).
 //
 // Per-walker semantics are single_walk's (walk.cpp:41-80): cap at the loop
 // top, then after each traversed edge budget before target. A walker whose
@@ -223,10 +217,10 @@ struct ChunkSmem {  // per warp: the current 32-item chunk
   double u[32];  // this step's draw, stored before the fetch wait (see k_walk)
 };
 
-template <int C, int NS, int kWarps>
+template <int C, int kWarps>
 struct WalkLayout {
-  static constexpr size_t kStageBytes = sizeof(uint4) * Gather<C>::kWarpWords;  // one slot
-  static constexpr size_t kWarpBytes = NS * kStageBytes + sizeof(ChunkSmem);
+  static constexpr size_t kStageBytes = sizeof(uint4) * Gather<C>::kWarpWords;
+  static constexpr size_t kWarpBytes = kStageBytes + sizeof(ChunkSmem);
   static constexpr size_t kBytes = kWarps * kWarpBytes;
 };
 
@@ -257,18 +251,21 @@ __device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row
   cp_async_commit();
 }
 
-template <int C, bool kMinPath, int NS, int kWarps, int kMinBlocks>
+template <int C, bool kMinPath, int kWarps, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_walk(DevGraph<C> g, const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
            const uint32_t* __restrict__ nq_dev, WalkParams P, ReachOut rout, MinScratch S,
            WalkCounters* ctr, unsigned int* __restrict__ work) {
-  using L = WalkLayout<C, NS, kWarps>;
+  using L = WalkLayout<C, kWarps>;
+  // A drained warp with at most this many live walkers finishes them
+  // lane by lane (the thin tail below).
+  constexpr uint32_t kTailLanes = kMinPath ? 16u : 32u;
   extern __shared__ __align__(16) unsigned char walk_smem[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned char* wbase = walk_smem + warp * L::kWarpBytes;
   uint4* stage0 = reinterpret_cast<uint4*>(wbase);
-  ChunkSmem& cs = *reinterpret_cast<ChunkSmem*>(wbase + NS * L::kStageBytes);
+  ChunkSmem& cs = *reinterpret_cast<ChunkSmem*>(wbase + L::kStageBytes);
   const uint32_t total_work = *nq_dev * P.s;
   const unsigned long long t0 = global_ns();
   uint32_t chunk_base = 0, chunk_pos = 32, chunk_end = 32;
@@ -390,81 +387,68 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     return 0xFFFFFFFFu;
   };
 
-  Slot sl[NS];
-#pragma unroll
-  for (int k = 0; k < NS; ++k) {
-    sl[k].has = false;
-    refill(sl[k]);
-    issue_rows(g, row_of(sl[k]), stage0 + k * Gather<C>::kWarpWords);
-  }
+  Slot w;
+  w.has = false;
+  refill(w);
+  issue_rows(g, row_of(w), stage0);
   for (;;) {
-    // Thin tail (P.early == 2, one slot): the queue is drained, so no lane
-    // takes new work, and at most P.tail_lanes walkers are left in the warp.
-    // Every lane then runs its walker to the end on its own, loading whole
-    // rows straight into registers and requesting the next row right after
-    // sampling -- no warp-wide gather, shuffles or shared staging on the
-    // dependent chain. (With many live lanes the cooperative gather stays:
-    // lane-private row loads cost one L1 wavefront per 16 B chunk.)
-    if (NS == 1 && drained && P.early == 2 &&
-        static_cast<uint32_t>(__popc(__ballot_sync(kFull, sl[0].has))) <=
-            (kMinPath ? P.tail_min : P.tail_reach))
+    // Thin tail: the queue is drained, so no lane takes new work, and at
+    // most kTailLanes walkers are left in the warp. Every lane then runs its
+    // walker to the end on its own, loading whole rows straight into
+    // registers and requesting the next row right after sampling -- no
+    // warp-wide gather, shuffles or shared staging on the dependent chain.
+    // (With many live lanes the cooperative gather stays: lane-private row
+    // loads cost one L1 wavefront per 16 B chunk.)
+    if (drained && static_cast<uint32_t>(__popc(__ballot_sync(kFull, w.has))) <= kTailLanes)
       break;
-    bool any = false;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      Slot& w = sl[k];
-      uint4* stage = stage0 + k * Gather<C>::kWarpWords;
-      // This step's uniform draw (draw k = steps + 1) does not depend on the
-      // row: computed while the fetch is in flight. The shared store pins it
-      // before the wait (ptxas otherwise sinks the hash below the DEPBAR, onto
-      // the dependent chain).
-      const double u = u01_of(w.rng + kGamma);
-      *reinterpret_cast<volatile double*>(&cs.u[lane]) = u;
-      cp_async_wait<NS - 1>();  // slot k's group is the oldest outstanding
-      __syncwarp();
-      // Once the queue is drained no refill follows, so the next row can be
-      // requested right after sampling, before the reciprocal / budget
-      // arithmetic: in the tail every walker is a chain of dependent steps
-      // and this takes that arithmetic off the chain. A walker the budget
-      // then ends wastes its fetch (the memory system is idle by then).
-      const bool early = drained && P.early;
-      uint32_t term = 0xFFFFFFFFu;
-      uint32_t next = kNoVertex;
-      double ew = 0.0;
-      if (w.has) {
-        if (w.steps >= P.T) {
-          term = kStepCap;
-        } else {
-          w.rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
-          uint32_t deg = 0;
-          const bool ok =
-              walk_step(g, stage + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
-          my_bytes += step_bytes(deg);
-          if (!ok) term = kDeadEnd;
-        }
-      }
-      if (early) {
-        __syncwarp();  // every lane has read its staged row
-        const bool cont = w.has && term == 0xFFFFFFFFu && next != w.tgt && w.steps + 1 < P.T;
-        issue_rows(g, cont ? next : kNoVertex, stage);
-      }
-      if (w.has) {
-        if (term == 0xFFFFFFFFu) term = advance(w, next, ew);
-        if (term != 0xFFFFFFFFu) finish(w, term);
-      }
-      if (!early) {
-        __syncwarp();  // every lane has read its staged row before the slot is refilled
-        refill(w);
-        issue_rows(g, row_of(w), stage);
-      }
-      any |= w.has;
-    }
-    if (!__any_sync(kFull, any)) break;
-  }
-  if (NS == 1 && __any_sync(kFull, sl[0].has)) {  // the thin-tail exit above
+    // This step's uniform draw (draw k = steps + 1) does not depend on the
+    // row: computed while the fetch is in flight. The shared store pins it
+    // before the wait (ptxas otherwise sinks the hash below the DEPBAR, onto
+    // the dependent chain).
+    const double u = u01_of(w.rng + kGamma);
+    *reinterpret_cast<volatile double*>(&cs.u[lane]) = u;
     cp_async_wait<0>();
     __syncwarp();
-    Slot& w = sl[0];
+    // Once the queue is drained no refill follows, so the next row can be
+    // requested right after sampling, before the reciprocal / budget
+    // arithmetic: in the tail every walker is a chain of dependent steps
+    // and this takes that arithmetic off the chain. A walker the budget
+    // then ends wastes its fetch (the memory system is idle by then).
+    const bool early = drained;
+    uint32_t term = 0xFFFFFFFFu;
+    uint32_t next = kNoVertex;
+    double ew = 0.0;
+    if (w.has) {
+      if (w.steps >= P.T) {
+        term = kStepCap;
+      } else {
+        w.rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
+        uint32_t deg = 0;
+        const bool ok =
+            walk_step(g, stage0 + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
+        my_bytes += step_bytes(deg);
+        if (!ok) term = kDeadEnd;
+      }
+    }
+    if (early) {
+      __syncwarp();  // every lane has read its staged row
+      const bool cont = w.has && term == 0xFFFFFFFFu && next != w.tgt && w.steps + 1 < P.T;
+      issue_rows(g, cont ? next : kNoVertex, stage0);
+    }
+    if (w.has) {
+      if (term == 0xFFFFFFFFu) term = advance(w, next, ew);
+      if (term != 0xFFFFFFFFu) finish(w, term);
+    }
+    if (!early) {
+      __syncwarp();  // every lane has read its staged row before the slot is refilled
+      refill(w);
+      issue_rows(g, row_of(w), stage0);
+    }
+    if (!__any_sync(kFull, w.has)) break;
+  }
+  if (__any_sync(kFull, w.has)) {  // the thin-tail exit above
+    cp_async_wait<0>();
+    __syncwarp();
     if (w.has) {
       RowRegs<C> r;
       if (w.steps < P.T) {  // its current row is staged (head chunks)
@@ -633,28 +617,36 @@ unsigned persistent_blocks(K kernel, uint64_t work, int threads, size_t smem) {
   return need < b ? need : b;
 }
 
-// One walk-kernel configuration: slots per lane, warps per block, minimum
-// resident blocks (register budget).
-template <int C, bool kMinPath, int NS, int kWarps, int kMinBlocks>
+// Opt-in dynamic shared memory is a per-device function attribute: set it
+// once per (kernel, device) and check the result (a second device in the
+// same process needs its own opt-in).
+template <typename K>
+bool smem_opt_in(K kernel, size_t bytes) {
+  constexpr int kMaxDev = 64;
+  static size_t granted[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return false;
+  if (granted[dev] >= bytes) return true;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(bytes)) != cudaSuccess)
+    return false;
+  granted[dev] = bytes;
+  return true;
+}
+
+// The walk kernel: 8 warps per block; reach walks keep 3 blocks per SM,
+// min-path walks 2 (register budget).
+template <int C, bool kMinPath>
 void launch_walk(const DevGraph<C>& g, const ReachQuery* rq, const MinQuery* mq,
                  const uint32_t* nq_dev, uint64_t threads, const WalkParams& P, ReachOut ro,
                  MinScratch S, WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
-  auto k = k_walk<C, kMinPath, NS, kWarps, kMinBlocks>;
-  constexpr size_t smem = WalkLayout<C, NS, kWarps>::kBytes;
-  static bool attr = [&] {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    return true;
-  }();
-  (void)attr;
+  constexpr int kWarps = 8;
+  constexpr int kMinBlocks = kMinPath ? 2 : 3;
+  auto k = k_walk<C, kMinPath, kWarps, kMinBlocks>;
+  constexpr size_t smem = WalkLayout<C, kWarps>::kBytes;
+  smem_opt_in(k, smem);
   k<<<persistent_blocks(k, threads, kWarps * 32, smem), kWarps * 32, smem, st>>>(
       g, rq, mq, nq_dev, P, ro, S, ctr, work);
-}
-
-// Walk-kernel variant (tuning knob, default = the measured best):
-// DYG_WALK_REACH / DYG_WALK_MIN = index into the tables below.
-int walk_variant(const char* env, int dflt) {
-  const char* e = std::getenv(env);
-  return e ? std::atoi(e) : dflt;
 }
 
 template <int C>
@@ -663,21 +655,12 @@ int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_d
                  unsigned int* work, cudaStream_t st, bool standalone) {
   if (nq_max == 0) return 0;
   int l = 1;
-  static const int v = walk_variant("DYG_WALK_REACH", 0);
   if (standalone) {
     k_reach_init<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_max, work);
     ++l;
   }
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
-  switch (v) {
-    case 0: launch_walk<C, false, 1, 8, 3>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
-    case 2: launch_walk<C, false, 2, 8, 3>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
-    case 3: launch_walk<C, false, 2, 4, 5>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
-    case 4: launch_walk<C, false, 3, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
-    case 5: launch_walk<C, false, 1, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
-    case 6: launch_walk<C, false, 1, 4, 6>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
-    default: launch_walk<C, false, 2, 8, 2>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st); break;
-  }
+  launch_walk<C, false>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st);
   if (standalone) {
     k_reach_fix<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_dev);
     ++l;
@@ -693,29 +676,17 @@ int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_d
                    WalkCounters* ctr, unsigned int* work, cudaStream_t st, bool reset_work) {
   if (nq_max == 0) return 0;
   int l = 2;
-  static const int v = walk_variant("DYG_WALK_MIN", 0);
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
   if (reset_work) {
     k_zero<<<1, 1, 0, st>>>(work);
     ++l;
   }
-  switch (v) {
-    case 0: launch_walk<C, true, 1, 8, 2>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
-    case 2: launch_walk<C, true, 2, 4, 4>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
-    default: launch_walk<C, true, 2, 8, 2>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st); break;
-  }
+  launch_walk<C, true>(g, nullptr, q, nq_dev, threads, P, ReachOut{}, scratch, ctr, work, st);
   // 16 B of shared memory per trace position per warp; long caps get one
   // warp per block (up to the opt-in shared-memory limit).
   const size_t per_warp = (static_cast<size_t>(P.T) + 1) * 16;
   const unsigned warps = per_warp * 8 <= 48 * 1024 ? 8u : 1u;
-  if (per_warp * warps > 48 * 1024) {
-    static size_t granted = 0;
-    if (per_warp * warps > granted) {
-      cudaFuncSetAttribute(k_minpath_finish<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(per_warp * warps));
-      granted = per_warp * warps;
-    }
-  }
+  if (per_warp * warps > 48 * 1024) smem_opt_in(k_minpath_finish<C>, per_warp * warps);
   k_minpath_finish<C><<<blocks_for(static_cast<uint64_t>(nq_max) * 32, 32 * warps), 32 * warps,
                         per_warp * warps, st>>>(g, nq_dev, P, scratch, out);
   return l;

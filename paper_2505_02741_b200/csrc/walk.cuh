@@ -8,8 +8,6 @@
 // explicit _rn intrinsics (no FMA contraction).
 #pragma once
 
-#include <cstdlib>
-
 #include "dyg_internal.cuh"
 
 namespace dyg {
@@ -24,9 +22,6 @@ struct WalkParams {
   uint32_t s;        // walkers per query
   uint64_t seed;     // global seed
   uint32_t s_shift;  // log2(s) when s is a power of two, else kNoShift
-  uint32_t early;    // tail: 1 = request the next row right after sampling, 2 = + per-lane loop
-  uint32_t tail_reach;  // early == 2: a drained warp with at most this many live
-  uint32_t tail_min;    // walkers (reach / min-path kernel) goes per-lane
 };
 
 inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t seed) {
@@ -35,19 +30,7 @@ inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t se
     sh = 0;
     while ((1u << sh) != s) ++sh;
   }
-  static const uint32_t early = [] {
-    const char* e = std::getenv("DYG_WALK_EARLY");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 2u;
-  }();
-  static const uint32_t tail_reach = [] {
-    const char* e = std::getenv("DYG_TAIL_LANES");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 32u;
-  }();
-  static const uint32_t tail_min = [] {
-    const char* e = std::getenv("DYG_TAIL_LANES_MIN");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 16u;
-  }();
-  return WalkParams{K, T, s, seed, sh, early, tail_reach, tail_min};
+  return WalkParams{K, T, s, seed, sh};
 }
 
 // Entries per raw min-path trace: T + 1 rounded up to whole 32 B sectors, so

@@ -91,7 +91,7 @@ def condition_number(g: DynamicGraph | SparsifierState, h: DynamicGraph | None =
 
 
 def calibrate_budget(g: DynamicGraph | SparsifierState, h: DynamicGraph | None = None,
-                     probe_fraction: float = 0.05, rho: float = 1.0, seed: int = 0,
+                     probe_fraction: float = 0.05, rho: float = 0.1, seed: int = 0,
                      device: int = 0) -> float:
     """calibrate_budget (sparsifier.cpp:561-583): clamp(rho * kappa, 1, 1e6)
     from a coarse Lanczos estimate. With a SparsifierState the seed is its

@@ -122,3 +122,56 @@ def test_sharded_async_stops_at_failing_batch(oracle, dyg, world):
     assert sh.update_counter == ost.update_counter
     assert same_rows(ost.graph().export(), sh.rows(0))
     assert same_rows(ost.sparsifier().export(), sh.rows(1))
+
+
+def test_async_commits_host_events_and_settled_guard(oracle, dyg):
+    """Asynchronous commits of batches begun from HOST event arrays: the
+    Python layer keeps every pending batch's buffers alive until
+    shard_finish (its error path reads the failing batch's events), and while
+    commits are pending every state-reading entry point refuses with a Usage
+    error instead of reading stale host-side counters."""
+    import gc
+
+    import torch
+
+    g = oracle.make_mesh(9, 9, 3)
+    h = oracle.build_initial_sparsifier(g, 0.1, 3)
+    rp, ids, _ = g.export()
+    edges = [(u, int(ids[i])) for u in range(len(rp) - 1) for i in range(rp[u], rp[u + 1])
+             if u < ids[i]]
+    ev = [(0, 0, 40, 0, 1.0), (0, 1, 50, 0, 1.0),
+          (1, edges[3][0], edges[3][1], 1, 0.0),
+          (1, edges[3][0], edges[3][1], 1, 0.0),             # fails: already deleted
+          (0, 2, 60, 2, 1.0)]
+    ev = np.array(ev, dtype=O.EVENT_DTYPE)
+    ost = oracle.state(g, h, K=10.0, T=30, s=8, seed=3)
+    ostream = oracle.stream(ev, 3)
+    ost.replay_batch(ostream, 0)
+    with pytest.raises(O.OracleError) as oe:
+        ost.replay_batch(ostream, 1)
+    sh = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h),
+                             dyg.SparsifierOptions(dyg.WalkConfig(10.0, 30, 8, 3), True, False))
+    stream = dyg.UpdateStream(ev, 3)
+    rb, mb = sh.shard_record_bytes(False), sh.shard_record_bytes(True)
+    keep = []
+    for b in range(3):
+        bev, bpos = stream.batch(b)
+        nr, nm = sh.shard_begin(np.array(bev, copy=True), np.array(bpos, copy=True), b)
+        gc.collect()  # the caller's copies are gone; the session's must not be
+        rall = torch.zeros(max(1, nr * rb), dtype=torch.uint8, device="cuda")
+        mall = torch.zeros(max(1, nm * mb), dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()
+        sh.shard_walk(0, 1, rall.data_ptr(), mall.data_ptr())
+        sh.shard_commit_async(1, rall.data_ptr(), mall.data_ptr())
+        keep += [rall, mall]
+    for call in (lambda: sh.rows(0), lambda: sh.replay_batch(stream, 0), sh.snapshot,
+                 lambda: sh.apply_insertion(3, 70, 1.0)):
+        with pytest.raises(dyg.Error) as ue:
+            call()
+        assert ue.value.kind == 1 and "dyg_shard_finish" in str(ue.value)
+    with pytest.raises(dyg.Error) as de:
+        sh.shard_finish()
+    assert str(de.value) == oe.value.message
+    assert sh.update_counter == ost.update_counter
+    assert same_rows(ost.graph().export(), sh.rows(0))
+    assert same_rows(ost.sparsifier().export(), sh.rows(1))
