@@ -47,6 +47,13 @@ WORKLOAD_NAMES = {
     "C5": "delaunay_n22-shaped mesh 2048x2048",
 }
 K_BUDGET, T_CAP, WALKERS, WALK_SEED = 100.0, 100, 16, 42
+
+
+def workload_name(cfg, scale=1):
+    if scale == 1:
+        return WORKLOAD_NAMES[cfg]
+    rows, cols = config_shape(cfg, scale)[:2]
+    return f"{WORKLOAD_NAMES[cfg]} widened x{scale} for weak scaling ({rows}x{cols})"
 METRIC = "edge updates/sec (T_update per batch) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "edge_updates/s"
 
@@ -60,9 +67,17 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def make_inputs_product(cfg):
-    import paper_2505_02741_b200 as D
+def config_shape(cfg, scale=1):
+    """(rows, cols, generator, insert fraction, delete fraction, locality);
+    weak scaling widens the mesh by the GPU count (n, m and the events per
+    batch all grow by exactly `scale`)."""
     rows, cols, kind, ins, dele, loc = CONFIGS[cfg]
+    return rows, cols * scale, kind, ins, dele, loc
+
+
+def make_inputs_product(cfg, scale=1):
+    import paper_2505_02741_b200 as D
+    rows, cols, kind, ins, dele, loc = config_shape(cfg, scale)
     gen = D.make_mesh if kind == "mesh" else D.make_grid4
     g = gen(rows, cols, 1)
     # The device builder (SURVEY.md 8f row 1), bit-identical to the host one.
@@ -71,12 +86,35 @@ def make_inputs_product(cfg):
     return g, h, s
 
 
-def make_inputs_oracle(orc, cfg):
-    rows, cols, kind, ins, dele, loc = CONFIGS[cfg]
+def make_inputs_oracle(orc, cfg, scale=1):
+    rows, cols, kind, ins, dele, loc = config_shape(cfg, scale)
     g = orc.make_mesh(rows, cols, 1) if kind == "mesh" else orc.make_grid4(rows, cols, 1)
     h = orc.build_initial_sparsifier(g, 0.10, 1)
     s = orc.generate_stream(g, ins, dele, 10, 7, loc)
     return g, h, s
+
+
+def digest(*arrays) -> str:
+    """blake2b over the raw bytes of row exports / event arrays: the two arms'
+    inputs and the replicas' states are compared through these."""
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).view(np.uint8).data)
+    return h.hexdigest()
+
+
+def inputs_digest(g_rows, h_rows, events) -> dict:
+    return {"G": digest(*g_rows), "H0": digest(*h_rows), "stream": digest(events)}
+
+
+REPORT_KEYS = ("insertions_seen", "insertions_kept", "insertions_pruned", "deletions_seen",
+               "deletions_in_sparsifier", "paths_recovered", "edges_recovered",
+               "fallback_activations", "walker_steps", "max_event_steps")
+
+
+def report_tuple(reps) -> tuple:
+    return tuple(tuple(int(getattr(r, k)) for k in REPORT_KEYS) for r in reps)
 
 
 class ClockSampler:
@@ -191,35 +229,36 @@ def load_traffic(kernel: str):
         return None
 
 
-def cpu_baseline(cfg: str):
-    """The reference CPU implementation on this host, bounded sample: the
-    first insertion batch and the first deletion batch of the stream, each
-    replayed (deferred mode) from the initial state, all host threads."""
+def cpu_baseline(cfg: str, product_inputs: dict | None = None, scale: int = 1):
+    """The reference CPU implementation on this host: the WHOLE stream of the
+    config replayed (deferred mode, SparsifierState::replay_batch per batch)
+    from the initial state on all host threads, timed per batch kind. Its
+    inputs come from the reference's own generators; their digests must equal
+    the product arm's."""
     from oracle import oracle as O
     kind = "reference" if O.available("reference") else "port"
     orc = O.load("reference" if kind == "reference" else "restate")
     cores = os.cpu_count() or 1
     os.environ["DYSPARSE_THREADS"] = str(cores)
     t0 = time.perf_counter()
-    g, h, s = make_inputs_oracle(orc, cfg)
+    g, h, s = make_inputs_oracle(orc, cfg, scale)
     setup = time.perf_counter() - t0
     ev = s.events()
-    nb = s.batch_count
-    ins_b = 0
-    del_b = nb // 2 if nb > 10 else None
-    events, wall = 0, 0.0
-    split = {}
-    for name, b in [("insertion", ins_b)] + ([("deletion", del_b)] if del_b is not None else []):
-        st = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED)
-        sel = ev[ev["batch_index"] == b].copy()
-        sel["batch_index"] = 0
+    ref_inputs = inputs_digest(g.export(), h.export(), ev)
+    if product_inputs is not None and ref_inputs != product_inputs:
+        raise RuntimeError(f"inputs differ: product {product_inputs} reference {ref_inputs}")
+    st = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED)
+    split = {"insertion": [0, 0.0, 0], "deletion": [0, 0.0, 0]}
+    for b in range(s.batch_count):
         t = time.perf_counter()
-        st.replay_batch(orc.stream(sel, 1), 0)
+        r = st.replay_batch(s, b)
         dt = time.perf_counter() - t
-        wall += dt
-        events += len(sel)
-        split[name] = {"events": int(len(sel)), "s": round(dt, 3),
-                       "edge_updates_per_s": len(sel) / dt}
+        k = "deletion" if r["deletions_seen"] else "insertion"
+        split[k][0] += int(r["insertions_seen"] + r["deletions_seen"])
+        split[k][1] += dt
+        split[k][2] += 1
+    events = sum(v[0] for v in split.values())
+    wall = sum(v[1] for v in split.values())
     cpu_model = ""
     try:
         with open("/proc/cpuinfo") as f:
@@ -229,10 +268,15 @@ def cpu_baseline(cfg: str):
         pass
     return {"value": events / wall, "unit": UNIT,
             "cores": cores if kind == "reference" else 1, "kind": kind,
-            "per_batch_kind": split, "cpu_model": cpu_model, "nproc": os.cpu_count(),
-            "sample": (f"{cfg}: insertion batch 0 + deletion batch {del_b} replayed from the "
-                       f"initial state ({events} events, {wall:.2f} s, setup {setup:.1f} s "
-                       "excluded), SparsifierState::replay_batch batched mode")}
+            "per_batch_kind": {k: {"batches": v[2], "events": v[0], "s": round(v[1], 3),
+                                   "t_update_ms_per_batch": 1e3 * v[1] / v[2],
+                                   "edge_updates_per_s": v[0] / v[1]}
+                               for k, v in split.items() if v[2]},
+            "cpu_model": cpu_model, "nproc": os.cpu_count(),
+            "inputs": ref_inputs, "inputs_match_product": product_inputs is not None,
+            "sample": (f"{cfg}: all {s.batch_count} batches ({events} events) replayed from the "
+                       f"initial state in {wall:.2f} s (setup {setup:.1f} s excluded), "
+                       "SparsifierState::replay_batch batched mode")}
 
 
 def run_reference_arm(args):
@@ -244,34 +288,41 @@ def run_reference_arm(args):
     orc = O.load("reference" if kind == "reference" else "restate")
     cores = os.cpu_count() or 1
     os.environ["DYSPARSE_THREADS"] = str(cores)
-    g, h, s = make_inputs_oracle(orc, args.config)
+    scale = world if args.scaling == "weak" else 1
+    g, h, s = make_inputs_oracle(orc, args.config, scale)
     nb = s.batch_count
+    ref_inputs = inputs_digest(g.export(), h.export(), s.events())
     st = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED)
     b = 0
 
     def step():
+        """One batch, in stream order; only replay_batch is timed (the
+        state is rebuilt from (G0, H0) outside the clock after the last)."""
         nonlocal st, b
         if b == nb:
             st, b = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED), 0
+        t = time.perf_counter()
         r = st.replay_batch(s, b)
+        dt = time.perf_counter() - t
         b += 1
-        return int(r["insertions_seen"] + r["deletions_seen"])
+        return int(r["insertions_seen"] + r["deletions_seen"]), dt
 
     for _ in range(args.warmup):
         step()
-    events, t0 = 0, time.perf_counter()
+    events, el = 0, 0.0
     for _ in range(args.steps):
-        events += step()
-    el = time.perf_counter() - t0
+        e, dt = step()
+        events += e
+        el += dt
     v = events / el
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generators)",
-        "config": {"workload": WORKLOAD_NAMES[args.config], "config": args.config,
+        "config": {"workload": workload_name(args.config, scale), "config": args.config,
                    "step": "one deferred batch of the stream, in order",
-                   "K": K_BUDGET, "T": T_CAP, "s": WALKERS},
+                   "K": K_BUDGET, "T": T_CAP, "s": WALKERS, "inputs": ref_inputs},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores if kind == "reference" else 1,
                          "kind": kind,
                          "sample": f"{args.steps} consecutive batches of {args.config}"},
@@ -328,7 +379,9 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     t0 = time.perf_counter()
-    g, h, stream = make_inputs_product(args.config)
+    scale = world if args.scaling == "weak" else 1
+    g, h, stream = make_inputs_product(args.config, scale)
+    prod_inputs = inputs_digest(g.rows(), h.rows(), stream.events)
     log(f"[rank {rank}] inputs {time.perf_counter() - t0:.1f}s")
     opts = D.SparsifierOptions(D.WalkConfig(K_BUDGET, T_CAP, WALKERS, WALK_SEED), True, False)
     st = D.SparsifierState(g, h, opts, device=dev)
@@ -347,9 +400,8 @@ def run_ours(args):
     def step_device():
         st.restore()
         if sharded is None:
-            st.replay_uploaded_range(0, nb)  # device-resident replay(stream)
-            return
-        sharded.replay_uploaded_range(0, nb)
+            return st.replay_uploaded_range(0, nb)  # device-resident replay(stream)
+        return sharded.replay_uploaded_range(0, nb)
 
     def step_e2e():
         # The reference-facing replay(stream) from the host stream (page-locked
@@ -357,10 +409,11 @@ def run_ours(args):
         # reports come back; the library pipelines the uploads with the work.
         st.restore()
         if sharded is None:
-            st.replay(stream)
-            return
-        for b in range(nb):
-            sharded.replay_events(batches[b][0], batches[b][1], b)
+            return st.replay(stream).batches
+        return sharded.replay_stream(stream)
+
+    def state_digest():
+        return digest(*st.rows(0)), digest(*st.rows(1))
 
     def barrier():
         if world > 1:
@@ -374,7 +427,9 @@ def run_ours(args):
         return float(t.item())
 
     log(f"[rank {rank}] session ready; warm-up")
-    for _ in range(args.warmup):
+    first_reports = report_tuple(step_device())
+    first_state = state_digest()
+    for _ in range(args.warmup - 1):
         step_device()
     torch.cuda.synchronize()
     log(f"[rank {rank}] timed steps")
@@ -383,9 +438,10 @@ def run_ours(args):
     with ClockSampler(dev) as clocks:
         barrier()
         torch.cuda.synchronize()
+        timed_reports = []
         ev0.record(torch_stream)
         for _ in range(args.steps):
-            step_device()
+            timed_reports.append(step_device())
         ev1.record(torch_stream)
         torch.cuda.synchronize()
         barrier()
@@ -400,7 +456,24 @@ def run_ours(args):
     r1.record(torch_stream)
     torch.cuda.synchronize()
     restore_ms = r0.elapsed_time(r1) / 3
-    # Check the final state of the last timed step against the first run.
+    # Self-check: every timed step reported what the first replay reported,
+    # and the last one left the first replay's G and H (row digests).
+    for reps in timed_reports:
+        if report_tuple(reps) != first_reports:
+            raise RuntimeError("a timed device replay reported differently from the first")
+    if state_digest() != first_state:
+        raise RuntimeError("the timed device replays ended in a different G/H state")
+    kinds = {"insertion": [0, 0.0, 0], "deletion": [0, 0.0, 0]}
+    for reps in timed_reports:
+        for r in reps:
+            k = kinds["deletion" if r.deletions_seen else "insertion"]
+            k[0] += int(r.insertions_seen + r.deletions_seen)
+            k[1] += r.wall_ms
+            k[2] += 1
+    t_update = {k: {"batches_per_step": v[2] // args.steps,
+                    "t_update_ms_per_batch": v[1] / v[2],
+                    "edge_updates_per_s": v[0] / (v[1] * 1e-3)}
+                for k, v in kinds.items() if v[2]}
     rep_events = n_events
 
     # End-to-end through the C-ABI with host buffers.
@@ -411,11 +484,15 @@ def run_ours(args):
     st.reset_stats()
     barrier()
     t = time.perf_counter()
+    e2e_reports = []
     for _ in range(args.steps):
-        step_e2e()
+        e2e_reports.append(step_e2e())
     torch.cuda.synchronize()
     barrier()
     e2e_ms = max_over_ranks(1e3 * (time.perf_counter() - t) / args.steps)
+    if any(report_tuple(r) != first_reports for r in e2e_reports) or \
+            state_digest() != first_state:
+        raise RuntimeError("an end-to-end replay differs from the first device replay")
     estats = st.stats()
     log(f"[rank {rank}] e2e {e2e_ms:.3f} ms/step")
 
@@ -442,21 +519,27 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (reference generators: make_mesh, build_initial_sparsifier, "
                 "generate_update_stream; bit-identical inputs)",
         "config": {
-            "workload": WORKLOAD_NAMES[args.config], "config": args.config,
+            "workload": workload_name(args.config, scale), "config": args.config,
             "vertices": g.vertex_count(), "edges": g.edge_count(),
             "sparsifier_edges": h.edge_count(), "batches": nb, "events_per_step": rep_events,
-            "step": "restore(G0,H0) + replay of all batches (10 incremental + 10 decremental)",
+            "step": (f"restore(G0,H0) + replay of all batches ({kinds['insertion'][2] // args.steps}"
+                     f" incremental + {kinds['deletion'][2] // args.steps} decremental)"),
             "K": K_BUDGET, "T": T_CAP, "s": WALKERS, "walk_seed": WALK_SEED,
             "parallelism": (f"replicated G/H, walks sharded x{world}" if (world > 1 or force_shard)
                             else "1 GPU"),
-            "l2": "inputs larger than L2 (G slabs 537 MB + H slabs 403 MB > 126 MB)",
+            "l2": (f"inputs larger than L2 (G slabs {g.vertex_count() * 128 / 1e6:.0f} MB + "
+                   f"H slabs {g.vertex_count() * 96 / 1e6:.0f} MB > 126 MB)"),
+            "inputs": prod_inputs,
         },
+        "self_check": ("every timed step's reports equal the first replay's, and the final "
+                       "G/H row digests equal the first replay's (device and e2e)"),
+        "t_update_per_batch_kind": t_update,
         "e2e": {
             "value": rep_events / (e2e_ms * 1e-3), "unit": UNIT,
             "h2d_bytes_per_step": int(estats["h2d_bytes"] // args.steps),
@@ -497,7 +580,7 @@ def run_ours(args):
     del launches
     if world == 1 and not args.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = cpu_baseline(args.config)
+            out["cpu_baseline"] = cpu_baseline(args.config, prod_inputs, scale)
         except Exception as exc:  # reported, never silently replaced
             out["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if world > 1 or force_shard:
@@ -517,6 +600,9 @@ def main():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=sorted(CONFIGS), default="C5")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="weak: the mesh is widened by the GPU count (cols x N), so the "
+                        "events and queries per batch grow with N")
     p.add_argument("--force-shard", action="store_true",
                    help="one GPU through the multi-GPU (sharded, NCCL) code path")
     args = p.parse_args()

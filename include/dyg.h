@@ -99,8 +99,9 @@ typedef struct dyg_walk_result {
   double resistance;
 } dyg_walk_result;
 
-/* BatchReport (sparsifier.hpp:44-59). wall_ms is device time of the batch
- * (CUDA events) plus host staging. */
+/* BatchReport (sparsifier.hpp:44-59). wall_ms is the batch's T_update on the
+ * device: its first kernel's start to its commit's end (%globaltimer stamps
+ * the kernels write), host staging excluded. */
 typedef struct dyg_batch_report {
   uint32_t batch_index;
   uint32_t pad;

@@ -659,8 +659,10 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   rep.max_event_steps = c.report[kMaxEventSteps];
   rep.density_graph = density_of(s->g_edges, s->n);
   rep.density_sparsifier = density_of(s->h_edges, s->n);
-  rep.wall_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - p.wall0).count();
+  // T_update of the batch on the device: its first kernel's start stamp to
+  // the commit's end stamp (in a range replay the host finalises all batches
+  // after one synchronisation, so host time would not be per batch).
+  rep.wall_ms = span_ms(c.t_batch0, c.t_batch1);
   *out = rep;
 }
 
@@ -1770,6 +1772,7 @@ int dyg_session_restore(dyg_session* s) {
     require_settled(s);
     if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
     if (!s->have_snap) fail(DYG_ERR_USAGE, "no snapshot taken");
+    s->last_t1 = 0;  // the restore is not a gap between batches of one replay
     check(cudaSetDevice(s->device), "set device");
     s->G.copy_from(s->G_snap, s->stream);
     s->H.copy_from(s->H_snap, s->stream);

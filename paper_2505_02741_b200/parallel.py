@@ -128,9 +128,23 @@ class ShardedReplay:
         """Batches [first, first + count) of the uploaded stream with no host
         round trip between them (asynchronous commits); their reports."""
         reports = []
-        for b in range(first, first + count):
+        for i, b in enumerate(range(first, first + count)):
             nr, nm = self.state.shard_begin_uploaded(b)
             self._exchange(nr, nm, commit=False)
-            if len(reports) + 256 <= b - first + 1:  # the pending ring is 256 deep
+            if (i + 1) % 256 == 0:  # the pending ring is 256 deep
+                reports += self.state.shard_finish()
+        return reports + self.state.shard_finish()
+
+    def replay_stream(self, stream):
+        """replay(stream) (sparsifier.cpp:550-559) from a host UpdateStream:
+        each batch's events are uploaded by its dyg_shard_begin and its commit
+        is enqueued asynchronously, so the batches chain on the device with
+        one host synchronisation per stream (dyg_shard_finish); the reports."""
+        reports = []
+        for b in range(stream.batch_count):
+            ev, pos = stream.batch(b)
+            nr, nm = self.state.shard_begin(ev, pos, b)
+            self._exchange(nr, nm, commit=False)
+            if (b + 1) % 256 == 0:
                 reports += self.state.shard_finish()
         return reports + self.state.shard_finish()
