@@ -447,6 +447,7 @@ def run_ours(args):
         barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     stats = st.stats()
+    timed_state = state_digest()  # before the restore diagnostic below
     log(f"[rank {rank}] device {ms:.3f} ms/step; end-to-end")
     # Diagnostic: the snapshot restore each step begins with (not update work).
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -461,7 +462,7 @@ def run_ours(args):
     for reps in timed_reports:
         if report_tuple(reps) != first_reports:
             raise RuntimeError("a timed device replay reported differently from the first")
-    if state_digest() != first_state:
+    if timed_state != first_state:
         raise RuntimeError("the timed device replays ended in a different G/H state")
     kinds = {"insertion": [0, 0.0, 0], "deletion": [0, 0.0, 0]}
     for reps in timed_reports:

@@ -42,6 +42,21 @@ extern "C" {
 #define DYG_ERR_NUMERIC 3 /* ErrorKind::Numeric */
 #define DYG_ERR_DEVICE 4  /* CUDA error or missing device (no reference analogue) */
 
+/* Per-event decisions (the optional per_event_decision outputs below), one
+ * byte per event. Insertions: InsertionDecision (sparsifier.hpp:36), what
+ * commit_insertion returns (sparsifier.cpp:220-241). Deletions:
+ * DeletionOutcome::Kind (sparsifier.hpp:38-42) as replay_batch_deferred
+ * resolves it at commit (sparsifier.cpp:489-523): not in live H -> GraphOnly,
+ * a recovered path -> PathRecovered, the local fallback (or freeze) ->
+ * LocalFallback. Events that did not commit (validation error, the failing
+ * event and every event after it, :525-529) stay DYG_DECISION_NONE. */
+#define DYG_DECISION_KEPT 0
+#define DYG_DECISION_PRUNED 1
+#define DYG_DECISION_GRAPH_ONLY 2
+#define DYG_DECISION_PATH_RECOVERED 3
+#define DYG_DECISION_LOCAL_FALLBACK 4
+#define DYG_DECISION_NONE 255
+
 /* Graph rows in reference row order: row u is DynamicGraph::neighbors(u)
  * (graph.hpp:37-38), flattened. row_ptr has n+1 entries; ids/w have
  * row_ptr[n] = 2|E| entries. Every edge appears in both endpoint rows with
@@ -183,15 +198,19 @@ void dyg_session_destroy(dyg_session* s);
  * stream is `events[0..n_events)` with `batch_count` (UpdateStream,
  * stream.hpp:20-23); events of batch b are found by scanning, as the
  * reference does (sparsifier.cpp:401-404). Deferred or immediate mode per
- * options.batched. */
+ * options.batched. per_event_decision (nullable): one DYG_DECISION_* per
+ * event OF THE BATCH, in stream order (k-th event of batch b at [k]). */
 int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
-                     uint32_t batch_count, uint32_t batch_index, dyg_batch_report* out);
+                     uint32_t batch_count, uint32_t batch_index, dyg_batch_report* out,
+                     uint8_t* per_event_decision);
 
 /* The same for a batch already extracted by the caller: `events` are the
  * batch's events in stream order and `positions` their stream indices (used
- * in error messages; NULL means 0..n-1). */
+ * in error messages; NULL means 0..n-1). per_event_decision (nullable):
+ * n entries, [k] for events[k]. */
 int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* positions,
-                      size_t n, uint32_t batch_index, dyg_batch_report* out);
+                      size_t n, uint32_t batch_index, dyg_batch_report* out,
+                      uint8_t* per_event_decision);
 
 /* SparsifierState::replay(stream) (sparsifier.cpp:550-559) from a host
  * stream: out[b] for every batch b < batch_count. Events grouped by batch
@@ -200,10 +219,11 @@ int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* p
  * batches overlapping the work on earlier ones; ungrouped streams replay
  * batch by batch. On an error the batches before the failing one are
  * committed and reported, the failing one returns the reference's error and
- * later ones do not run. */
+ * later ones do not run. per_event_decision (nullable): n_events entries,
+ * indexed by stream position. */
 int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
                       const uint64_t* batch_offsets, uint32_t batch_count,
-                      dyg_batch_report* out);
+                      dyg_batch_report* out, uint8_t* per_event_decision);
 
 /* Device-resident stream: upload once, then replay batches with no per-batch
  * host->device traffic (used for the kernel-level benchmark). */
@@ -214,9 +234,11 @@ int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* 
  * uploaded stream (sparsifier.cpp:550-559): all batches are enqueued back to
  * back with one host synchronisation; out[i] is batch first + i. On an error
  * the batches before the failing one are committed and reported, the
- * failing one returns the reference's error, and later ones do not run. */
+ * failing one returns the reference's error, and later ones do not run.
+ * per_event_decision (nullable): indexed by position in the uploaded stream
+ * (entries of batches outside the range are left untouched). */
 int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
-                              dyg_batch_report* out);
+                              dyg_batch_report* out, uint8_t* per_event_decision);
 
 /* SparsifierState::apply_insertion / apply_deletion (sparsifier.cpp:243-317).
  * decision: 0 Kept, 1 Pruned (InsertionDecision). kind: 0 GraphOnly,

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "dyg.h"
+#include "dyg_adapter.hpp"
 
 namespace dyg {
 
@@ -140,43 +141,26 @@ struct UpdateReport {
   double final_density_sparsifier = 0.0;
 };
 
-// SparsifierState (sparsifier.hpp:71-112) with G and H device-resident.
-class GpuSparsifierState {
- public:
-  GpuSparsifierState(const HostGraph& graph, const HostGraph& sparsifier,
-                     SparsifierOptions options, int device = 0);
-  ~GpuSparsifierState();
-  GpuSparsifierState(const GpuSparsifierState&) = delete;
-  GpuSparsifierState& operator=(const GpuSparsifierState&) = delete;
-
-  // The reference returns const DynamicGraph&; the device rows are exported
-  // (row order preserved) into a HostGraph.
-  HostGraph graph() const;
-  HostGraph sparsifier() const;
-  const SparsifierOptions& options() const { return options_; }
-  std::uint64_t update_counter() const;
-
-  InsertionDecision apply_insertion(VertexId u, VertexId v, double weight);
-  DeletionOutcome apply_deletion(VertexId u, VertexId v);
-  std::uint64_t last_event_steps() const;
-
-  BatchReport replay_batch(const UpdateStream& stream, std::uint32_t batch_index);
-  UpdateReport replay(const UpdateStream& stream);
-  // dyGRASS.incremental() / .decremental(): a deferred batch of
-  // insertions / deletions.
-  BatchReport incremental(const UpdateStream& stream, std::uint32_t batch_index) {
-    return replay_batch(stream, batch_index);
+// SparsifierState (sparsifier.hpp:71-112) with G and H device-resident, on
+// this library's host types: the header-only adapter (dyg_adapter.hpp)
+// instantiated with them. (A caller of the reference keeps its own types:
+// dyg_dysparse.hpp.)
+struct HostTraits {
+  using Graph = HostGraph;
+  using Stream = UpdateStream;
+  using Options = SparsifierOptions;
+  using InsertionDecision = dyg::InsertionDecision;
+  using DeletionOutcome = dyg::DeletionOutcome;
+  using BatchReport = dyg::BatchReport;
+  using UpdateReport = dyg::UpdateReport;
+  static Graph make_graph(std::uint32_t n, const std::uint64_t* row_ptr,
+                          const std::uint32_t* ids, const double* w) {
+    return HostGraph::from_csr(dyg_csr{n, 0, row_ptr, ids, w});  // exact row order
   }
-  BatchReport decremental(const UpdateStream& stream, std::uint32_t batch_index) {
-    return replay_batch(stream, batch_index);
+  [[noreturn]] static void raise(int kind, const std::string& message) {
+    throw Error(static_cast<ErrorKind>(kind), message);
   }
-
-  dyg_session* session() const { return session_; }
-
- private:
-  HostGraph export_graph(int which) const;
-  dyg_session* session_ = nullptr;
-  SparsifierOptions options_;
 };
+using GpuSparsifierState = SparsifierStateAdapter<HostTraits>;
 
 }  // namespace dyg

@@ -145,6 +145,8 @@ class Oracle:
             "orc_stream_load": (vp, [C.c_char_p]),
             "orc_stream_save": (i32, [vp, C.c_char_p]),
         }
+        if which == "reference":
+            sig["orc_state_replay_batch_decisions"] = (i32, [vp, vp, u32, vp, vp])
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
             fn.restype = res
@@ -315,6 +317,16 @@ class State:
         rep = np.zeros(1, REPORT_DTYPE)
         self.o._check(self.o.lib.orc_state_replay_batch(self.h, stream.h, b, _ptr(rep)))
         return rep[0]
+
+    def replay_batch_decisions(self, stream: Stream, b: int):
+        """(report, decisions u8[events of batch b]) -- reference build only;
+        DYG_DECISION_* codes, 255 for events that did not commit."""
+        n = int((stream.events()["batch_index"] == b).sum())
+        rep = np.zeros(1, REPORT_DTYPE)
+        dec = np.full(max(n, 1), 255, np.uint8)
+        self.o._check(self.o.lib.orc_state_replay_batch_decisions(self.h, stream.h, b, _ptr(rep),
+                                                                 _ptr(dec)))
+        return rep[0], dec[:n]
 
     def graph(self) -> Graph:
         return Graph(self.o, self.o.lib.orc_state_graph(self.h), owned=False)

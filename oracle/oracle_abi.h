@@ -137,6 +137,11 @@ void* orc_state_new(const void* g, const void* h, const orc_walk_config* cfg, in
 void orc_state_free(void* st);
 int orc_state_replay_batch(void* st, const void* stream, uint32_t batch_index,
                            orc_report* out);
+/* Reference build only: replay_batch plus the per-event decisions
+ * (DYG_DECISION_* codes, one per event of the batch), derived from the
+ * reference's pieces and pinned to its own replay (ref/decisions.hpp). */
+int orc_state_replay_batch_decisions(void* st, const void* stream, uint32_t batch_index,
+                                     orc_report* out, uint8_t* decisions);
 const void* orc_state_graph(const void* st);
 const void* orc_state_sparsifier(const void* st);
 uint64_t orc_state_update_counter(const void* st);

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../oracle_abi.h"
+#include "decisions.hpp"
 #include "graph.hpp"
 #include "matrix_market.hpp"
 #include "rng.hpp"
@@ -288,6 +289,34 @@ int orc_state_replay_batch(void* st, const void* stream, uint32_t batch_index, o
     out->density_graph = r.density_graph;
     out->density_sparsifier = r.density_sparsifier;
   });
+}
+// replay_batch plus each event's decision (DYG_DECISION_* codes), derived
+// from the reference's own pieces and pinned to its replay (decisions.hpp).
+int orc_state_replay_batch_decisions(void* st, const void* stream, uint32_t batch_index,
+                                     orc_report* out, uint8_t* decisions) {
+  std::vector<uint8_t> dec;
+  const int rc = guarded([&] {
+    BatchReport r = dyg_oracle::replay_batch_with_decisions(
+        static_cast<State*>(st)->state, *static_cast<const UpdateStream*>(stream), batch_index,
+        dec);
+    std::memset(out, 0, sizeof(*out));
+    out->batch_index = r.batch_index;
+    out->insertions_seen = r.insertions_seen;
+    out->insertions_kept = r.insertions_kept;
+    out->insertions_pruned = r.insertions_pruned;
+    out->deletions_seen = r.deletions_seen;
+    out->deletions_in_sparsifier = r.deletions_in_sparsifier;
+    out->paths_recovered = r.paths_recovered;
+    out->edges_recovered = r.edges_recovered;
+    out->fallback_activations = r.fallback_activations;
+    out->walker_steps = r.walker_steps;
+    out->max_event_steps = r.max_event_steps;
+    out->wall_ms = r.wall_ms;
+    out->density_graph = r.density_graph;
+    out->density_sparsifier = r.density_sparsifier;
+  });
+  if (!dec.empty()) std::memcpy(decisions, dec.data(), dec.size());
+  return rc;
 }
 const void* orc_state_graph(const void* st) {
   return &static_cast<const State*>(st)->state.graph();

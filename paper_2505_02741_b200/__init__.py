@@ -10,6 +10,7 @@ from .api import (  # noqa: F401
     DynamicGraph,
     Error,
     ErrorKind,
+    Decision,
     InsertionDecision,
     SparsifierOptions,
     SparsifierState,

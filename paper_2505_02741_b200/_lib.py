@@ -107,12 +107,12 @@ def lib() -> C.CDLL:
         "dyg_host_free": (None, [vp]),
         "dyg_session_create": (i32, [C.POINTER(Csr), C.POINTER(Csr), C.POINTER(Options), i32, pvp]),
         "dyg_session_destroy": (None, [vp]),
-        "dyg_replay_batch": (i32, [vp, vp, sz, u32, u32, vp]),
-        "dyg_replay_events": (i32, [vp, vp, vp, sz, u32, vp]),
+        "dyg_replay_batch": (i32, [vp, vp, sz, u32, u32, vp, vp]),
+        "dyg_replay_events": (i32, [vp, vp, vp, sz, u32, vp, vp]),
         "dyg_stream_upload": (i32, [vp, vp, sz, u32]),
-        "dyg_replay_stream": (i32, [vp, vp, sz, vp, u32, vp]),
+        "dyg_replay_stream": (i32, [vp, vp, sz, vp, u32, vp, vp]),
         "dyg_replay_uploaded": (i32, [vp, u32, vp]),
-        "dyg_replay_uploaded_range": (i32, [vp, u32, u32, vp]),
+        "dyg_replay_uploaded_range": (i32, [vp, u32, u32, vp, vp]),
         "dyg_apply_insertion": (i32, [vp, u32, u32, dbl, C.POINTER(C.c_int)]),
         "dyg_apply_deletion": (i32, [vp, u32, u32, C.POINTER(C.c_int), C.POINTER(C.c_uint32)]),
         "dyg_last_event_steps": (u64, [vp]),

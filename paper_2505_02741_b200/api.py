@@ -318,6 +318,27 @@ def _options_struct(o: SparsifierOptions) -> _lib.Options:
                                      w.global_seed), int(o.batched), int(o.freeze_sparsifier))
 
 
+class Decision(enum.IntEnum):
+    """DYG_DECISION_* (include/dyg.h): InsertionDecision (sparsifier.hpp:36)
+    for insertions, 2 + DeletionOutcome::Kind (sparsifier.hpp:38-42) for
+    deletions; NONE for events that did not commit."""
+    Kept = 0
+    Pruned = 1
+    GraphOnly = 2
+    PathRecovered = 3
+    LocalFallback = 4
+    NONE = 255
+
+
+def _dec_ptr(decisions):
+    if decisions is None:
+        return None
+    if not (isinstance(decisions, np.ndarray) and decisions.dtype == np.uint8
+            and decisions.flags.c_contiguous and decisions.flags.writeable):
+        raise TypeError("decisions must be a writeable contiguous uint8 numpy array")
+    return ptr(decisions)
+
+
 class SparsifierState:
     """sparsifier.hpp:71-112 with G and H device-resident on `device`."""
 
@@ -382,34 +403,46 @@ class SparsifierState:
         _check(_lib.lib().dyg_apply_deletion(self._s, u, v, C.byref(k), C.byref(a)))
         return DeletionOutcome(DeletionOutcome.Kind(k.value), a.value)
 
-    def replay_batch(self, stream: UpdateStream, batch_index: int) -> BatchReport:
+    def replay_batch(self, stream: UpdateStream, batch_index: int,
+                     decisions: np.ndarray | None = None) -> BatchReport:
+        """sparsifier.cpp:541-548. `decisions` (optional uint8 array, one
+        entry per event of the batch) receives each event's DYG_DECISION_*
+        (Decision) in stream order."""
         rep = np.zeros(1, REPORT_DTYPE)
         ev = stream.events
+        if decisions is not None and len(decisions) < len(stream.batch(batch_index)[0]):
+            raise ValueError("decisions needs one entry per event of the batch")
         _check(_lib.lib().dyg_replay_batch(self._s, ptr(ev), len(ev), stream.batch_count,
-                                           batch_index, ptr(rep)))
+                                           batch_index, ptr(rep), _dec_ptr(decisions)))
         return BatchReport.from_record(rep[0])
 
     def replay_events(self, events: np.ndarray, positions: np.ndarray | None,
-                      batch_index: int) -> BatchReport:
+                      batch_index: int, decisions: np.ndarray | None = None) -> BatchReport:
         """One already-extracted batch (events in stream order)."""
         ev = np.ascontiguousarray(events, EVENT_DTYPE)
         pos = None if positions is None else np.ascontiguousarray(positions, np.uint64)
         rep = np.zeros(1, REPORT_DTYPE)
+        if decisions is not None and len(decisions) < len(ev):
+            raise ValueError("decisions needs one entry per event")
         _check(_lib.lib().dyg_replay_events(self._s, ptr(ev), ptr(pos) if pos is not None else None,
-                                            len(ev), batch_index, ptr(rep)))
+                                            len(ev), batch_index, ptr(rep), _dec_ptr(decisions)))
         return BatchReport.from_record(rep[0])
 
-    def replay(self, stream: UpdateStream) -> UpdateReport:
+    def replay(self, stream: UpdateStream, decisions: np.ndarray | None = None) -> UpdateReport:
         """sparsifier.cpp:550-559. One library call: the host stream's upload
-        is pipelined with the batches (dyg_replay_stream)."""
+        is pipelined with the batches (dyg_replay_stream). `decisions`
+        (optional uint8 array, one entry per stream event) receives every
+        event's DYG_DECISION_*, indexed by stream position."""
         out = UpdateReport()
         n = stream.batch_count
+        if decisions is not None and len(decisions) < len(stream.events):
+            raise ValueError("decisions needs one entry per stream event")
         if n:
             off = stream.batch_offsets()
             rep = np.zeros(n, REPORT_DTYPE)
             _check(_lib.lib().dyg_replay_stream(
                 self._s, ptr(stream.events), len(stream.events),
-                ptr(off) if off is not None else None, n, ptr(rep)))
+                ptr(off) if off is not None else None, n, ptr(rep), _dec_ptr(decisions)))
             out.batches = [BatchReport.from_record(r) for r in rep]
         out.final_density_graph = self.info(0)[2]
         out.final_density_sparsifier = self.info(1)[2]
@@ -431,11 +464,14 @@ class SparsifierState:
         _check(_lib.lib().dyg_replay_uploaded(self._s, batch_index, ptr(rep)))
         return BatchReport.from_record(rep[0])
 
-    def replay_uploaded_range(self, first: int, count: int) -> list:
+    def replay_uploaded_range(self, first: int, count: int,
+                              decisions: np.ndarray | None = None) -> list:
         """Batches [first, first+count) of the uploaded stream, enqueued back to
-        back with one host sync (the device-side replay())."""
+        back with one host sync (the device-side replay()). `decisions`: as in
+        replay(), indexed by position in the uploaded stream."""
         rep = np.zeros(max(count, 1), REPORT_DTYPE)
-        _check(_lib.lib().dyg_replay_uploaded_range(self._s, first, count, ptr(rep)))
+        _check(_lib.lib().dyg_replay_uploaded_range(self._s, first, count, ptr(rep),
+                                                    _dec_ptr(decisions)))
         return [BatchReport.from_record(rep[i]) for i in range(count)]
 
     def snapshot(self) -> None:

@@ -1962,6 +1962,24 @@ __global__ void k_count_kinds(const DevEvent* __restrict__ ev, uint32_t nb, uint
   }
 }
 
+__global__ void k_export_decisions(const uint32_t* __restrict__ dec,
+                                   const DevEvent* __restrict__ ev, uint32_t nb,
+                                   uint8_t* __restrict__ out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  // dec[k]: insertion 0 Kept / 1 Pruned; deletion 0 GraphOnly /
+  // 1 PathRecovered / 2 LocalFallback, edges added in bits 8+.
+  const uint32_t d = dec[k] & 0xFFu;
+  out[k] = static_cast<uint8_t>(ev[k].kind == 0 ? d : 2u + d);
+}
+
+int launch_export_decisions(const uint32_t* dec, const DevEvent* ev, uint32_t nb, uint8_t* out,
+                            cudaStream_t st) {
+  if (nb == 0) return 0;
+  k_export_decisions<<<grid_for(nb), 256, 0, st>>>(dec, ev, nb, out);
+  return 1;
+}
+
 int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStream_t st) {
   cuda_check(cudaMemsetAsync(out, 0, 2 * sizeof(uint32_t), st), "kind counts");
   k_count_kinds<<<grid_for(nb), 256, 0, st>>>(ev, nb, out);

@@ -192,6 +192,11 @@ int launch_shard_range(const BatchDev& b, int rank, int world, uint32_t* rng, ui
 bool ctl_init_node_args(cudaGraphNode_t n, CtlInitArgs* out);
 cudaError_t ctl_init_node_update(cudaGraphExec_t ex, cudaGraphNode_t n, const CtlInitArgs& a);
 int launch_count_kinds(const DevEvent* ev, uint32_t nb, uint32_t* out, cudaStream_t st);
+// Per-event decisions of a committed batch in the ABI's codes
+// (DYG_DECISION_*): insertions InsertionDecision (sparsifier.hpp:36),
+// deletions 2 + DeletionOutcome::Kind (sparsifier.hpp:38-42).
+int launch_export_decisions(const uint32_t* dec, const DevEvent* ev, uint32_t nb, uint8_t* out,
+                            cudaStream_t st);
 int launch_validate(const BatchDev& b, uint32_t nb, uint32_t n, const unsigned int* abort_flag,
                     cudaStream_t st);
 // Validation + walk shadow + query build: single-pass kernels for

@@ -138,6 +138,11 @@ struct dyg_session {
 
   // Last-batch outputs (immediate mode / apply_*).
   uint32_t last_dec = 0;
+  // Per-event decisions requested by the caller (device staging and its
+  // pinned host copy, one byte per event of a batch / range / stream).
+  uint8_t* d_dec = nullptr;
+  uint8_t* h_dec = nullptr;
+  uint64_t dec_cap = 0;
   uint32_t* d_counts = nullptr;   // [2..3] batch kind counts, [4..7] shard ranges
   uint32_t* h_counts = nullptr;   // pinned: [0..1] shard counts, [2] decision, [4..5] kinds
   // Multi-GPU split state (dyg_shard_*).
@@ -408,7 +413,43 @@ struct Pending {
   uint64_t counter_base = 0;  // update_counter at batch start
   bool g_appended = false;    // fast path: G appends already enqueued (forked)
   bool shard = false;         // multi-GPU split batch (dyg_shard_*)
+  // Per-event decisions (nullable): the commit exports them to dec_dev and
+  // copies them to dec_pin; deliver_decisions writes the caller's buffer at
+  // dec_dst[k] (dec_idx null) or dec_dst[dec_idx[k]].
+  uint8_t* dec_dev = nullptr;
+  uint8_t* dec_pin = nullptr;
+  uint8_t* dec_dst = nullptr;
+  const uint64_t* dec_idx = nullptr;
 };
+
+// Staging for up to `n` per-event decisions.
+void ensure_decisions(dyg_session* s, uint64_t n) {
+  if (n <= s->dec_cap) return;
+  if (s->d_dec) cudaFree(s->d_dec);
+  if (s->h_dec) cudaFreeHost(s->h_dec);
+  s->d_dec = nullptr;
+  s->h_dec = nullptr;
+  s->dec_cap = 0;
+  check(cudaMalloc(reinterpret_cast<void**>(&s->d_dec), n), "decision staging");
+  check(cudaMallocHost(reinterpret_cast<void**>(&s->h_dec), n), "pinned decisions");
+  s->dec_cap = n;
+}
+
+// After the batch's stream work has completed and BEFORE commit_finalize
+// (which throws for a failing batch): the events that committed get their
+// decisions, the rest (a validation error, the failing event and those
+// after it, :525-529) keep DYG_DECISION_NONE.
+void deliver_decisions(const Pending& p) {
+  if (p.dec_dst == nullptr || p.nb == 0) return;
+  const BatchCtl& c = *p.hctl;
+  uint64_t lim = p.nb;
+  if (c.val_err != ~0ull) lim = 0;
+  if (c.commit_err != ~0ull) lim = std::min<uint64_t>(lim, c.commit_err >> 8);
+  if (c.use_absent_limit && c.first_absent != 0xFFFFFFFFu)
+    lim = std::min<uint64_t>(lim, c.first_absent);
+  for (uint64_t k = 0; k < p.nb; ++k)
+    p.dec_dst[p.dec_idx ? p.dec_idx[k] : k] = k < lim ? p.dec_pin[k] : DYG_DECISION_NONE;
+}
 
 void bind_pending(dyg_session* s, Pending& p) {
   p.dctl = s->b.ctl;
@@ -554,6 +595,11 @@ void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   if (p.nb == 1)
     check(cudaMemcpyAsync(p.hdec, b.dec, sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream),
           "decision download");
+  if (p.dec_dev) {
+    p.launches += launch_export_decisions(b.dec, p.dev, p.nb, p.dec_dev, s->stream);
+    check(cudaMemcpyAsync(p.dec_pin, p.dec_dev, p.nb, cudaMemcpyDeviceToHost, s->stream),
+          "decisions download");
+  }
 }
 
 // After the stream has synchronised: error mapping (:525-529), counters and
@@ -817,13 +863,21 @@ void launch_graph(dyg_session* s, CapturedGraph& g, uint64_t counter) {
 
 void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* host_events,
                   const uint64_t* positions, uint32_t nb, uint32_t n_ins, uint32_t n_del,
-                  uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs) {
+                  uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs,
+                  uint8_t* dec_dst = nullptr, const uint64_t* dec_idx = nullptr) {
   if (nb == 0) {
     empty_report(s, batch_index, out);
     return;
   }
   Pending p;
   bind_pending(s, p);
+  if (dec_dst) {
+    ensure_decisions(s, nb);
+    p.dec_dev = s->d_dec;
+    p.dec_pin = s->h_dec;
+    p.dec_dst = dec_dst;
+    p.dec_idx = dec_idx;
+  }
   p.wall0 = std::chrono::steady_clock::now();
   p.dev = dev_events;
   p.host = host_events;
@@ -842,7 +896,7 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
     uint64_t key = session_fingerprint(s, 1);
     const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
                               reinterpret_cast<uint64_t>(p.hctl), reinterpret_cast<uint64_t>(p.hdec),
-                              nb, n_ins, n_del};
+                              reinterpret_cast<uint64_t>(p.dec_dev), nb, n_ins, n_del};
     key = fnv(key, shape, sizeof shape);
     CapturedGraph* g = find_graph(s, key);
     if (g == nullptr) {
@@ -858,13 +912,17 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
       launch_graph(s, *g, p.counter_base);
       p.launches = g->launches;
       check(cudaStreamSynchronize(s->stream), "batch");
+      deliver_decisions(p);
       commit_finalize(s, p, out);
       return;
     }
   }
   phase_prepare(s, p);
   phase_walk(s, p, true, 0, 0, 0, 0);
-  phase_commit(s, p, out);
+  commit_enqueue(s, p);
+  check(cudaStreamSynchronize(s->stream), "batch");
+  deliver_decisions(p);
+  commit_finalize(s, p, out);
 }
 
 // True when p is page-locked host memory the DMA engines can read directly.
@@ -907,14 +965,16 @@ void count_kinds(dyg_session* s, uint32_t nb, uint32_t& n_ins, uint32_t& n_del) 
 }
 
 void run_host_batch(dyg_session* s, const dyg_event* ev, const uint64_t* positions, size_t nb,
-                    uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs) {
+                    uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs,
+                    uint8_t* dec_dst = nullptr, const uint64_t* dec_idx = nullptr) {
   ensure_batch(s, static_cast<uint32_t>(nb), 0);
   upload_events(s, ev, nb);
   uint32_t n_ins = 0, n_del = 0;
   count_kinds(s, static_cast<uint32_t>(nb), n_ins, n_del);
   ensure_batch(s, static_cast<uint32_t>(nb), n_del);
   run_deferred(s, s->d_events, reinterpret_cast<const DevEvent*>(ev), positions,
-               static_cast<uint32_t>(nb), n_ins, n_del, batch_index, out, immediate_msgs);
+               static_cast<uint32_t>(nb), n_ins, n_del, batch_index, out, immediate_msgs, dec_dst,
+               dec_idx);
 }
 
 // Device-resident stream, batches [first, first + count) enqueued back to
@@ -922,7 +982,8 @@ void run_host_batch(dyg_session* s, const dyg_event* ev, const uint64_t* positio
 // sparsifier.cpp:550-559). Buffers and pool headroom are sized for the whole
 // range up front; a failing batch raises the device abort flag so the later
 // batches of the range do nothing, and the error is reported for it.
-void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batch_report* out) {
+void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batch_report* out,
+                        uint8_t* dec_dst = nullptr) {
   if (count == 0) return;
   uint64_t sum_ins = 0, sum_del = 0;
   uint32_t max_nb = 0, max_nd = 0;
@@ -937,6 +998,7 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
   ensure_batch(s, std::max<uint32_t>(max_nb, 1), max_nd);
   ensure_pools(s, sum_ins, sum_del);
   if (sum_del > 0) ensure_side_pool(s);
+  if (dec_dst) ensure_decisions(s, sum_ins + sum_del);
   if (s->ctl_cap < count) {
     dev_free(s->d_ctls);
     if (s->h_ctls) cudaFreeHost(s->h_ctls);
@@ -952,7 +1014,7 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
   reset_abort(s);
   // Host-side description of every batch (also what commit_finalize reads).
   {
-    uint64_t counter = counter0;
+    uint64_t counter = counter0, dec_off = 0;
     for (uint32_t i = 0; i < count; ++i) {
       const uint32_t b = first + i;
       Pending& p = ps[i];
@@ -970,6 +1032,13 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
       p.nb = static_cast<uint32_t>(s->batch_cnt[b]);
       p.n_ins = static_cast<uint32_t>(s->batch_ins[b]);
       p.n_del = static_cast<uint32_t>(s->batch_del[b]);
+      if (dec_dst) {  // indexed by stream position
+        p.dec_dev = s->d_dec + dec_off;
+        p.dec_pin = s->h_dec + dec_off;
+        p.dec_dst = dec_dst;
+        p.dec_idx = p.pos;
+        dec_off += p.nb;
+      }
       counter += p.nb;
     }
   }
@@ -994,7 +1063,8 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
     uint64_t key = session_fingerprint(s, 2);
     const uint64_t shape[] = {first, count, s->stream_gen, reinterpret_cast<uint64_t>(s->d_stream),
                               reinterpret_cast<uint64_t>(s->d_ctls),
-                              reinterpret_cast<uint64_t>(s->h_ctls)};
+                              reinterpret_cast<uint64_t>(s->h_ctls),
+                              dec_dst ? reinterpret_cast<uint64_t>(s->d_dec) : 0ull};
     key = fnv(key, shape, sizeof shape);
     g = find_graph(s, key);
     if (g == nullptr) g = capture_graph(s, key, counter0, enqueue);
@@ -1013,6 +1083,7 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
       empty_report(s, ps[i].batch, &out[i]);
       continue;
     }
+    deliver_decisions(ps[i]);
     commit_finalize(s, ps[i], &out[i]);  // throws at the first failing batch
   }
 }
@@ -1026,8 +1097,9 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
 // runs. One synchronisation at the end; reports as in the uploaded-range
 // replay (a failing batch stops the ones after it).
 void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_t* off,
-                uint32_t nbatches, dyg_batch_report* out) {
+                uint32_t nbatches, dyg_batch_report* out, uint8_t* dec_dst = nullptr) {
   if (nbatches == 0) return;
+  if (dec_dst) ensure_decisions(s, n);
   uint64_t max_nb = 1;
   for (uint32_t b = 0; b < nbatches; ++b) max_nb = std::max<uint64_t>(max_nb, off[b + 1] - off[b]);
   if (max_nb > 0xFFFFFFF0ull) fail(DYG_ERR_USAGE, "batch too large");
@@ -1097,6 +1169,11 @@ void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_
     p.host = reinterpret_cast<const DevEvent*>(events + off[b]);
     p.pos = nullptr;
     p.pos_base = off[b];
+    if (dec_dst) {  // indexed by stream position (grouped: off[b] + k)
+      p.dec_dev = s->d_dec + off[b];
+      p.dec_pin = s->h_dec + off[b];
+      p.dec_dst = dec_dst + off[b];
+    }
     check(cudaEventSynchronize(s->ready[b]), "upload");
     p.n_ins = s->h_kinds[2ull * b];
     p.n_del = s->h_kinds[2ull * b + 1];
@@ -1123,7 +1200,8 @@ void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_
     if (graphs_usable(s)) {  // one graph per batch slot, reused by later replays
       uint64_t key = session_fingerprint(s, 3);
       const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
-                                reinterpret_cast<uint64_t>(p.hctl), p.nb, p.n_ins, p.n_del};
+                                reinterpret_cast<uint64_t>(p.hctl),
+                                reinterpret_cast<uint64_t>(p.dec_dev), p.nb, p.n_ins, p.n_del};
       key = fnv(key, shape, sizeof shape);
       g = find_graph(s, key);
       if (g == nullptr) g = capture_graph(s, key, p.counter_base, enqueue);
@@ -1143,6 +1221,7 @@ void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_
       empty_report(s, b, &out[b]);
       continue;
     }
+    deliver_decisions(ps[b]);
     commit_finalize(s, ps[b], &out[b]);  // throws at the first failing batch
   }
 }
@@ -1163,7 +1242,8 @@ void accumulate(dyg_batch_report& acc, const dyg_batch_report& r) {
 // replay_batch_immediate (sparsifier.cpp:347-393) as 1-event deferred
 // batches (identical decisions).
 void run_immediate(dyg_session* s, const dyg_event* ev, const uint64_t* positions, size_t nb,
-                   uint32_t batch_index, dyg_batch_report* out) {
+                   uint32_t batch_index, dyg_batch_report* out, uint8_t* dec_dst = nullptr,
+                   const uint64_t* dec_idx = nullptr) {
   const auto wall0 = std::chrono::steady_clock::now();
   dyg_batch_report acc{};
   acc.batch_index = batch_index;
@@ -1171,6 +1251,9 @@ void run_immediate(dyg_session* s, const dyg_event* ev, const uint64_t* position
     dyg_batch_report r{};
     const uint64_t pos = positions ? positions[i] : i;
     run_host_batch(s, ev + i, &pos, 1, batch_index, &r, true);
+    if (dec_dst)
+      dec_dst[dec_idx ? dec_idx[i] : i] =
+          static_cast<uint8_t>(ev[i].kind == 0 ? (s->last_dec & 0xFF) : 2 + (s->last_dec & 0xFF));
     accumulate(acc, r);
   }
   acc.density_graph = density_of(s->g_edges, s->n);
@@ -1508,23 +1591,26 @@ static void require_settled(const dyg_session* s) {
 }
 
 int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* positions,
-                      size_t n, uint32_t batch_index, dyg_batch_report* out) {
+                      size_t n, uint32_t batch_index, dyg_batch_report* out,
+                      uint8_t* per_event_decision) {
   return guarded([&] {
     require_settled(s);
     if (s == nullptr || out == nullptr || (n && events == nullptr))
       fail(DYG_ERR_USAGE, "null argument");
     check(cudaSetDevice(s->device), "set device");
     if (n > 0xFFFFFFF0ull) fail(DYG_ERR_USAGE, "batch too large");
+    if (per_event_decision) std::memset(per_event_decision, DYG_DECISION_NONE, n);
     if (s->opt.batched) {
-      run_host_batch(s, events, positions, n, batch_index, out, false);
+      run_host_batch(s, events, positions, n, batch_index, out, false, per_event_decision);
     } else {
-      run_immediate(s, events, positions, n, batch_index, out);
+      run_immediate(s, events, positions, n, batch_index, out, per_event_decision);
     }
   });
 }
 
 int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
-                     uint32_t batch_count, uint32_t batch_index, dyg_batch_report* out) {
+                     uint32_t batch_count, uint32_t batch_index, dyg_batch_report* out,
+                     uint8_t* per_event_decision) {
   return guarded([&] {
     require_settled(s);
     if (s == nullptr || out == nullptr || (n_events && events == nullptr))
@@ -1540,10 +1626,12 @@ int dyg_replay_batch(dyg_session* s, const dyg_event* events, size_t n_events,
       }
     }
     check(cudaSetDevice(s->device), "set device");
+    if (per_event_decision) std::memset(per_event_decision, DYG_DECISION_NONE, sel.size());
     if (s->opt.batched) {
-      run_host_batch(s, sel.data(), pos.data(), sel.size(), batch_index, out, false);
+      run_host_batch(s, sel.data(), pos.data(), sel.size(), batch_index, out, false,
+                     per_event_decision);
     } else {
-      run_immediate(s, sel.data(), pos.data(), sel.size(), batch_index, out);
+      run_immediate(s, sel.data(), pos.data(), sel.size(), batch_index, out, per_event_decision);
     }
   });
 }
@@ -1612,7 +1700,7 @@ int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* 
 }
 
 int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
-                              dyg_batch_report* out) {
+                              dyg_batch_report* out, uint8_t* per_event_decision) {
   return guarded([&] {
     require_settled(s);
     if (s == nullptr || (count && out == nullptr)) fail(DYG_ERR_USAGE, "null argument");
@@ -1621,13 +1709,17 @@ int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
       fail(DYG_ERR_USAGE, "batch index out of range");
     if (!s->opt.batched) fail(DYG_ERR_USAGE, "batch ranges need batched (deferred) mode");
     check(cudaSetDevice(s->device), "set device");
-    run_uploaded_range(s, first, count, out);
+    if (per_event_decision)
+      for (uint32_t b = first; b < first + count && b < s->batch_cnt.size(); ++b)
+        for (uint64_t k = s->batch_off[b]; k < s->batch_off[b + 1]; ++k)
+          per_event_decision[s->stream_positions[k]] = DYG_DECISION_NONE;
+    run_uploaded_range(s, first, count, out, per_event_decision);
   });
 }
 
 int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
                       const uint64_t* batch_offsets, uint32_t batch_count,
-                      dyg_batch_report* out) {
+                      dyg_batch_report* out, uint8_t* per_event_decision) {
   return guarded([&] {
     require_settled(s);
     if (s == nullptr || (batch_count && out == nullptr) || (n_events && events == nullptr))
@@ -1651,8 +1743,9 @@ int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
     } else if (o[batch_count] != n_events || o[0] != 0) {
       fail(DYG_ERR_USAGE, "batch offsets do not cover the events");
     }
+    if (per_event_decision) std::memset(per_event_decision, DYG_DECISION_NONE, n_events);
     if (grouped && s->opt.batched) {
-      run_stream(s, events, n_events, o, batch_count, out);
+      run_stream(s, events, n_events, o, batch_count, out, per_event_decision);
       return;
     }
     // Ungrouped events or immediate mode: the per-batch reference path.
@@ -1665,9 +1758,11 @@ int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
           pos.push_back(i);
         }
       if (s->opt.batched)
-        run_host_batch(s, ev.data(), pos.data(), ev.size(), b, &out[b], false);
+        run_host_batch(s, ev.data(), pos.data(), ev.size(), b, &out[b], false, per_event_decision,
+                       pos.data());
       else
-        run_immediate(s, ev.data(), pos.data(), ev.size(), b, &out[b]);
+        run_immediate(s, ev.data(), pos.data(), ev.size(), b, &out[b], per_event_decision,
+                      pos.data());
     }
   });
 }

@@ -104,7 +104,22 @@ def test_run_batch_usage_errors_before_device(dyg):
 
 def test_null_arguments_are_usage_errors():
     L = _lib.lib()
-    assert L.dyg_replay_batch(None, None, 0, 0, 0, None) == 1
+    assert L.dyg_replay_batch(None, None, 0, 0, 0, None, None) == 1
     assert L.dyg_session_snapshot(None) == 1
     assert L.dyg_update_counter(None) == 0
     L.dyg_session_destroy(None)  # no-op
+
+
+def test_dysparse_adapter_compiles_against_reference_headers(tmp_path):
+    """include/dyg_dysparse.hpp instantiates the adapter with the reference's
+    own types (needs /root/reference for its headers)."""
+    ref = "/root/reference/proj"
+    if not os.path.isdir(ref):
+        pytest.skip("reference headers absent")
+    inc = os.path.join(os.path.dirname(os.path.dirname(LIB)), "include")
+    repo = os.path.dirname(inc)
+    subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", "-I", inc,
+                    "-I", os.path.join(repo, "oracle", "ref"),
+                    "-I", os.path.join(repo, "oracle", "ref", "fake_eigen"),
+                    "-I", os.path.join(ref, "src"), "-I", os.path.join(ref, "tests"),
+                    os.path.join(repo, "tests", "cpp", "adapter_test.cpp")], check=True)

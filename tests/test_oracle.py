@@ -243,3 +243,20 @@ def test_restatement_errors_match_reference(restate, reference):
                     st.replay_batch(orc.stream(ev, 1), 0)
                 msgs.append((e.value.kind, e.value.message, st.update_counter))
             assert msgs[0] == msgs[1]
+
+
+@pytest.mark.parametrize("batched", [True, False])
+def test_reference_decisions_agree_with_reports(reference, batched):
+    """oracle/ref/decisions.cpp: the per-event decisions it derives (and pins
+    to the reference's own replay -- a divergence raises) add up to every
+    batch's counters (sparsifier.cpp:466-533)."""
+    c = O.CONFIGS["C2"]
+    g, h, s = O.build_config(reference, c)
+    st = reference.state(g, h, K=c.K, T=c.T, s=c.s, seed=c.walk_seed, batched=batched)
+    for b in range(s.batch_count):
+        r, d = st.replay_batch_decisions(s, b)
+        cnt = np.bincount(d, minlength=256)
+        assert cnt[0] == r["insertions_kept"] and cnt[1] == r["insertions_pruned"]
+        assert cnt[2] + cnt[3] + cnt[4] == r["deletions_seen"]
+        assert cnt[3] == r["paths_recovered"] and cnt[4] == r["fallback_activations"]
+        assert cnt[255] == 0
