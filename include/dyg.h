@@ -226,7 +226,10 @@ int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
                       dyg_batch_report* out, uint8_t* per_event_decision);
 
 /* Device-resident stream: upload once, then replay batches with no per-batch
- * host->device traffic (used for the kernel-level benchmark). */
+ * host->device traffic (used for the kernel-level benchmark). Events already
+ * grouped by batch in page-locked memory (dyg_host_alloc) are DMA'd
+ * asynchronously, stream-ordered before any later replay: keep that buffer
+ * unchanged until the next replay call returns. */
 int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
                       uint32_t batch_count);
 int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* out);

@@ -324,8 +324,12 @@ class State:
         n = int((stream.events()["batch_index"] == b).sum())
         rep = np.zeros(1, REPORT_DTYPE)
         dec = np.full(max(n, 1), 255, np.uint8)
-        self.o._check(self.o.lib.orc_state_replay_batch_decisions(self.h, stream.h, b, _ptr(rep),
-                                                                 _ptr(dec)))
+        try:
+            self.o._check(self.o.lib.orc_state_replay_batch_decisions(self.h, stream.h, b,
+                                                                     _ptr(rep), _ptr(dec)))
+        except OracleError as e:
+            e.decisions = dec[:n]  # the events that committed before the error
+            raise
         return rep[0], dec[:n]
 
     def graph(self) -> Graph:

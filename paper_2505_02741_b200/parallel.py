@@ -137,14 +137,8 @@ class ShardedReplay:
 
     def replay_stream(self, stream):
         """replay(stream) (sparsifier.cpp:550-559) from a host UpdateStream:
-        each batch's events are uploaded by its dyg_shard_begin and its commit
-        is enqueued asynchronously, so the batches chain on the device with
-        one host synchronisation per stream (dyg_shard_finish); the reports."""
-        reports = []
-        for b in range(stream.batch_count):
-            ev, pos = stream.batch(b)
-            nr, nm = self.state.shard_begin(ev, pos, b)
-            self._exchange(nr, nm, commit=False)
-            if (b + 1) % 256 == 0:
-                reports += self.state.shard_finish()
-        return reports + self.state.shard_finish()
+        the events are uploaded once (dyg_stream_upload), then the batches
+        chain on the device with asynchronous commits and one host
+        synchronisation (replay_uploaded_range); the reports."""
+        self.state.upload_stream(stream)
+        return self.replay_uploaded_range(0, stream.batch_count)

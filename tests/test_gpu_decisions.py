@@ -37,6 +37,7 @@ def replay_both(dyg, ref, g, h, ev, nb, K=100.0, T=100, s=16, seed=42, batched=T
             o_dec[sel] = d
         except O.OracleError as e:
             assert "diverged" not in e.message, e.message
+            o_dec[sel] = e.decisions
             o_err = e
             break
     d_dec = np.full(len(ev), 255, np.uint8)
