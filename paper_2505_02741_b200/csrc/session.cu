@@ -150,6 +150,7 @@ struct dyg_session {
   const DevEvent* shard_host = nullptr;  // caller's buffers, valid until dyg_shard_commit
   const DevEvent* shard_dev = nullptr;   // the batch's events on the device
   const uint64_t* shard_pos = nullptr;
+  uint64_t shard_pos_base = 0;           // stream position of event 0 when shard_pos is null
   uint32_t shard_nb = 0, shard_ins = 0, shard_del = 0, shard_batch = 0;
   uint32_t shard_nq_r = 0, shard_nq_m = 0;
   std::chrono::steady_clock::time_point shard_wall0;
@@ -459,10 +460,20 @@ void bind_pending(dyg_session* s, Pending& p) {
   p.counter_base = s->counter;
 }
 
+// Event k of a pending batch for an error message: the host copy when there
+// is one, else read back from the device (uploaded streams keep no host copy
+// when they were DMA'd straight from the caller's page-locked buffer).
+DevEvent event_at(const Pending& p, uint64_t k) {
+  if (p.host) return p.host[k];
+  DevEvent e{};
+  check(cudaMemcpy(&e, p.dev + k, sizeof e, cudaMemcpyDeviceToHost), "event read-back");
+  return e;
+}
+
 [[noreturn]] void fail_validation(dyg_session* s, const Pending& p, unsigned long long val_err) {
   const uint32_t k = static_cast<uint32_t>(val_err >> 8);
   const uint64_t pos = p.pos ? p.pos[k] : p.pos_base + k;
-  std::string msg = event_error_message(static_cast<uint32_t>(val_err & 0xFF), pos, p.host[k]);
+  std::string msg = event_error_message(static_cast<uint32_t>(val_err & 0xFF), pos, event_at(p, k));
   if (p.imm_msgs) {
     char pre[64];
     std::snprintf(pre, sizeof pre, "event %llu: ", static_cast<unsigned long long>(pos));
@@ -688,7 +699,7 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
     s->counter = p.counter_base + fail_k + 1;  // ++update_counter_ precedes the throw (:469)
     const uint64_t pos = p.pos ? p.pos[fail_k] : p.pos_base + fail_k;
     fail(fail_code == kErrPool ? DYG_ERR_DEVICE : DYG_ERR_DATA,
-         event_error_message(fail_code, pos, p.host[fail_k]));
+         event_error_message(fail_code, pos, event_at(p, fail_k)));
   }
   s->counter = p.counter_base + p.nb;
   s->last_dec = p.nb == 1 ? *p.hdec : 0;
@@ -865,7 +876,8 @@ void launch_graph(dyg_session* s, CapturedGraph& g, uint64_t counter) {
 void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* host_events,
                   const uint64_t* positions, uint32_t nb, uint32_t n_ins, uint32_t n_del,
                   uint32_t batch_index, dyg_batch_report* out, bool immediate_msgs,
-                  uint8_t* dec_dst = nullptr, const uint64_t* dec_idx = nullptr) {
+                  uint8_t* dec_dst = nullptr, const uint64_t* dec_idx = nullptr,
+                  uint64_t pos_base = 0) {
   if (nb == 0) {
     empty_report(s, batch_index, out);
     return;
@@ -883,6 +895,7 @@ void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* ho
   p.dev = dev_events;
   p.host = host_events;
   p.pos = positions;
+  p.pos_base = pos_base;
   p.nb = nb;
   p.n_ins = n_ins;
   p.n_del = n_del;
@@ -978,6 +991,17 @@ void run_host_batch(dyg_session* s, const dyg_event* ev, const uint64_t* positio
                dec_idx);
 }
 
+// Host copy / stream positions of uploaded event `off` (nullptr when the
+// stream was DMA'd from a grouped page-locked buffer: positions are then the
+// identity and events are read back from the device on an error).
+const DevEvent* uploaded_host(const dyg_session* s, uint64_t off) {
+  return s->stream_events.empty() ? nullptr
+                                  : reinterpret_cast<const DevEvent*>(s->stream_events.data() + off);
+}
+const uint64_t* uploaded_pos(const dyg_session* s, uint64_t off) {
+  return s->stream_positions.empty() ? nullptr : s->stream_positions.data() + off;
+}
+
 // Device-resident stream, batches [first, first + count) enqueued back to
 // back; one host sync at the end (the device-side replay(stream),
 // sparsifier.cpp:550-559). Buffers and pool headroom are sized for the whole
@@ -1028,15 +1052,16 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
       if (b >= s->batch_cnt.size() || s->batch_cnt[b] == 0) continue;
       const uint64_t off = s->batch_off[b];
       p.dev = s->d_stream + off;
-      p.host = reinterpret_cast<const DevEvent*>(s->stream_events.data() + off);
-      p.pos = s->stream_positions.data() + off;
+      p.host = uploaded_host(s, off);
+      p.pos = uploaded_pos(s, off);
+      p.pos_base = off;
       p.nb = static_cast<uint32_t>(s->batch_cnt[b]);
       p.n_ins = static_cast<uint32_t>(s->batch_ins[b]);
       p.n_del = static_cast<uint32_t>(s->batch_del[b]);
       if (dec_dst) {  // indexed by stream position
         p.dec_dev = s->d_dec + dec_off;
         p.dec_pin = s->h_dec + dec_off;
-        p.dec_dst = dec_dst;
+        p.dec_dst = p.pos ? dec_dst : dec_dst + off;
         p.dec_idx = p.pos;
         dec_off += p.nb;
       }
@@ -1668,18 +1693,19 @@ int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
       dev_alloc(&s->d_stream, std::max<size_t>(n_events, 1), "stream");
       s->stream_cap = std::max<size_t>(n_events, 1);
     }
-    s->stream_events.resize(n_events);
-    s->stream_positions.resize(n_events);
     if (grouped && host_pinned(events)) {
       // Already in batch order and page-locked: DMA straight from the
-      // caller's buffer (stream-ordered before any replay), and keep the
-      // host copy for error messages while it runs.
+      // caller's buffer, stream-ordered before any replay. No host copy:
+      // positions are the identity, and an error message reads its event
+      // back from the device.
+      s->stream_events.clear();
+      s->stream_positions.clear();
       if (n_events)
         check(cudaMemcpyAsync(s->d_stream, events, sizeof(DevEvent) * n_events,
                               cudaMemcpyHostToDevice, s->stream), "stream upload");
-      std::memcpy(s->stream_events.data(), events, sizeof(dyg_event) * n_events);
-      for (size_t i = 0; i < n_events; ++i) s->stream_positions[i] = i;
     } else {
+      s->stream_events.resize(n_events);
+      s->stream_positions.resize(n_events);
       std::vector<uint64_t> fill(s->batch_off.begin(), s->batch_off.end() - 1);
       for (size_t i = 0; i < n_events; ++i) {
         const uint64_t at = fill[events[i].batch_index]++;
@@ -1711,15 +1737,23 @@ int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* 
     const uint64_t off = s->batch_off[batch_index];
     const uint32_t nb = static_cast<uint32_t>(s->batch_cnt[batch_index]);
     if (!s->opt.batched) {
-      run_immediate(s, s->stream_events.data() + off, s->stream_positions.data() + off, nb,
-                    batch_index, out);
+      std::vector<dyg_event> ev(nb);
+      std::vector<uint64_t> pos(nb);
+      if (uploaded_host(s, off)) {
+        std::memcpy(ev.data(), s->stream_events.data() + off, sizeof(dyg_event) * nb);
+        std::memcpy(pos.data(), s->stream_positions.data() + off, sizeof(uint64_t) * nb);
+      } else {
+        check(cudaMemcpy(ev.data(), s->d_stream + off, sizeof(dyg_event) * nb,
+                         cudaMemcpyDeviceToHost), "batch read-back");
+        for (uint32_t i = 0; i < nb; ++i) pos[i] = off + i;
+      }
+      run_immediate(s, ev.data(), pos.data(), nb, batch_index, out);
       return;
     }
-    run_deferred(s, s->d_stream + off,
-                 reinterpret_cast<const DevEvent*>(s->stream_events.data() + off),
-                 s->stream_positions.data() + off, nb,
+    run_deferred(s, s->d_stream + off, uploaded_host(s, off), uploaded_pos(s, off), nb,
                  static_cast<uint32_t>(s->batch_ins[batch_index]),
-                 static_cast<uint32_t>(s->batch_del[batch_index]), batch_index, out, false);
+                 static_cast<uint32_t>(s->batch_del[batch_index]), batch_index, out, false,
+                 nullptr, nullptr, off);
   });
 }
 
@@ -1736,7 +1770,8 @@ int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
     if (per_event_decision)
       for (uint32_t b = first; b < first + count && b < s->batch_cnt.size(); ++b)
         for (uint64_t k = s->batch_off[b]; k < s->batch_off[b + 1]; ++k)
-          per_event_decision[s->stream_positions[k]] = DYG_DECISION_NONE;
+          per_event_decision[s->stream_positions.empty() ? k : s->stream_positions[k]] =
+              DYG_DECISION_NONE;
     run_uploaded_range(s, first, count, out, per_event_decision);
   });
 }
@@ -1971,6 +2006,7 @@ void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* p
       p.dev = s->shard_dev;
       p.host = s->shard_host;
       p.pos = s->shard_pos;
+      p.pos_base = s->shard_pos_base;
       p.nb = s->shard_nb;
       p.n_ins = n_ins;
       p.n_del = n_del;
@@ -1995,6 +2031,7 @@ int dyg_shard_begin(dyg_session* s, const dyg_event* events, const uint64_t* pos
                     uint32_t batch_index, uint64_t* n_reach, uint64_t* n_minpath) {
   return guarded([&] {
     if (s == nullptr || (n && events == nullptr)) fail(DYG_ERR_USAGE, "null argument");
+    s->shard_pos_base = 0;
     shard_begin_impl(s, events, positions, n, batch_index, nullptr, 0, 0, n_reach, n_minpath);
   });
 }
@@ -2006,8 +2043,9 @@ int dyg_shard_begin_uploaded(dyg_session* s, uint32_t batch_index, uint64_t* n_r
     if (batch_index >= s->batch_cnt.size()) fail(DYG_ERR_USAGE, "batch index out of range");
     const uint64_t off = s->batch_off[batch_index];
     const size_t n = s->batch_cnt[batch_index];
-    shard_begin_impl(s, reinterpret_cast<const dyg_event*>(s->stream_events.data() + off),
-                     s->stream_positions.data() + off, n, batch_index, s->d_stream + off,
+    s->shard_pos_base = off;
+    shard_begin_impl(s, reinterpret_cast<const dyg_event*>(uploaded_host(s, off)),
+                     uploaded_pos(s, off), n, batch_index, s->d_stream + off,
                      static_cast<uint32_t>(s->batch_ins[batch_index]),
                      static_cast<uint32_t>(s->batch_del[batch_index]), n_reach, n_minpath);
   });
@@ -2069,6 +2107,7 @@ Pending shard_commit_pending(dyg_session* s, int world, const void* reach_gather
     p.dev = s->shard_dev;
     p.host = s->shard_host;
     p.pos = s->shard_pos;
+    p.pos_base = s->shard_pos_base;
     p.nb = s->shard_nb;
     p.n_ins = s->shard_ins;
     p.n_del = s->shard_del;
