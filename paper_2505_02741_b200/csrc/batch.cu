@@ -154,6 +154,7 @@ __device__ __forceinline__ bool fp_apply(const DevGraph<C>& g, const DevEvent* e
                                          const uint32_t* next, uint32_t r, bool write, Take take,
                                          bool reset) {
   const uint32_t row = rec_row(ev, r);
+  if (row >= g.n) return true;  // an invalid event (the batch fails validation): never linked
   // The row's slab is needed by the head's append: request it alongside the
   // list lookups.
   if (write) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.slab + row));
@@ -262,7 +263,10 @@ __global__ void k_fp_write_h(DevGraph<kCapH> H, const DevEvent* __restrict__ ev,
       asm volatile("prefetch.global.L2 [%0];" ::"l"(H.slab + rows[0]));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(H.slab + rows[1]));
     }
-    const uint32_t h[2] = {head[rows[0]], head[rows[1]]};
+    // An out-of-range endpoint fails validation (write is then false) and
+    // was never linked: no list to read.
+    const uint32_t h[2] = {e.u < H.n ? head[rows[0]] : kNoSlot,
+                           e.v < H.n ? head[rows[1]] : kNoSlot};
     bool kept = false;
     if (write) {
       bool have;

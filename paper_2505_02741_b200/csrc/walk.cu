@@ -162,6 +162,107 @@ __device__ __forceinline__ void load_row(const DevGraph<C>& g, uint32_t x, RowRe
   for (int i = 0; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
 }
 
+// ---- reach walks on the compact walk image of H (walk_image.cuh) ----------
+// Entry i of an image row held as uint4 blocks v[2j] (ids / deg) and v[2j+1]
+// (weights), j = i / 2.
+__device__ __forceinline__ uint32_t img_id(const uint4* v, int i) {
+  const uint4 lo = v[2 * (i >> 1)];
+  return i < 2 ? ((i & 1) ? lo.z : lo.y) : ((i & 1) ? lo.y : lo.x);
+}
+__device__ __forceinline__ double img_w(const uint4* v, int i) {
+  const uint4 hi = v[2 * (i >> 1) + 1];
+  return (i & 1) ? __hiloint2double(static_cast<int>(hi.w), static_cast<int>(hi.z))
+                 : __hiloint2double(static_cast<int>(hi.y), static_cast<int>(hi.x));
+}
+
+// sample_neighbor (walk.cpp:17-37) on the first CC entries of an image row
+// (deg <= CC): the same single-pass masked prefix and suffix-popc pick as
+// sample_inline, over entries in row order.
+template <int CC>
+__device__ __forceinline__ bool sample_img(const uint4* v, uint32_t deg, uint32_t prev,
+                                           double u01, uint32_t& next, double& ew) {
+  const uint32_t live = (1u << deg) - 1u;
+  uint32_t cand = 0;
+  double prefix[CC];
+  uint32_t ids[CC];
+  double ws[CC];
+  double total = 0.0;
+#pragma unroll
+  for (int i = 0; i < CC; ++i) {
+    ids[i] = img_id(v, i);
+    ws[i] = img_w(v, i);
+    const bool c = ((live >> i) & 1u) && ids[i] != prev;
+    cand |= static_cast<uint32_t>(c) << i;
+    total = __dadd_rn(total, c ? ws[i] : 0.0);
+    prefix[i] = total;
+  }
+  if (total <= 0.0) return false;
+  const double target = __dmul_rn(u01, total);
+  uint32_t hit = 0;
+#pragma unroll
+  for (int i = 0; i < CC; ++i) hit |= static_cast<uint32_t>(target < prefix[i]) << i;
+  const uint32_t sel = hit ? static_cast<uint32_t>(CC - __popc(hit)) : 31u - __clz(cand);
+#pragma unroll
+  for (int st = 1; st < CC; st <<= 1) {
+    const bool up = (sel & static_cast<uint32_t>(st)) != 0;
+#pragma unroll
+    for (int i = 0; i + st < CC; i += 2 * st) {
+      ids[i] = up ? ids[i + st] : ids[i];
+      ws[i] = up ? ws[i + st] : ws[i];
+    }
+  }
+  next = ids[0];
+  ew = ws[0];
+  return true;
+}
+
+// One step on an image row whose first two blocks are in v[0..3] (staged or
+// loaded); rows of degree 5..8 fetch blocks 2-3 (`loc` = the row's image
+// location), rows beyond 8 entries sample H's overflow pool.
+__device__ __forceinline__ bool img_step(const DevGraph<kCapH>& h, const WalkImage& img,
+                                         uint4* v, uint32_t loc, uint32_t prev, double u01,
+                                         uint32_t& next, double& ew, uint32_t& deg) {
+  deg = v[0].x;
+  if (deg <= 4) return sample_img<4>(v, deg, prev, u01, next, ew);
+  if (deg <= kImgMaxInline) {
+    const uint4* src = img.rec + 2ull * (loc >> 3);
+    v[4] = __ldg(src + 4);
+    v[5] = __ldg(src + 5);
+    if (deg > 6) {
+      v[6] = __ldg(src + 6);
+      v[7] = __ldg(src + 7);
+    } else {
+      v[6] = v[7] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    return sample_img<8>(v, deg, prev, u01, next, ew);
+  }
+  const uint32_t ext = v[0].w;
+  return sample_pool(h.pool_id + ext, h.pool_w + ext, deg, prev, u01, next, ew);
+}
+
+// The whole image row of x straight into registers (the thin tail): its
+// location, then all of its blocks in one round trip. Returns the location.
+__device__ __forceinline__ uint32_t img_load(const WalkImage& img, uint32_t x, uint4* v) {
+  const uint32_t loc = __ldg(img.loc + x);
+  const uint4* src = img.rec + 2ull * (loc >> 3);
+  const uint32_t f = loc & 7u;
+  v[0] = __ldg(src);
+  v[1] = __ldg(src + 1);
+  if (f >= 2) {
+    v[2] = __ldg(src + 2);
+    v[3] = __ldg(src + 3);
+  }
+  if (f >= 3) {
+    v[4] = __ldg(src + 4);
+    v[5] = __ldg(src + 5);
+  }
+  if (f >= 4) {
+    v[6] = __ldg(src + 6);
+    v[7] = __ldg(src + 7);
+  }
+  return loc;
+}
+
 // Uniform draw from the SplitMix64 counter (rng.hpp:7-24): `ctr` already
 // advanced by gamma for this draw.
 __device__ __forceinline__ double u01_of(uint64_t ctr) {
@@ -203,6 +304,7 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long lo
 // raw trace and (acc, terminal, steps) for K3.
 struct Slot {
   uint32_t cur, prev, tgt, steps, widx, qi;
+  uint32_t loc;    // reach: image location of cur (walk_image.cuh)
   uint32_t tb[8];  // min-path: the last 8 trace entries (a shift register)
   bool has;
   uint64_t rng;
@@ -251,11 +353,39 @@ __device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row
   cp_async_commit();
 }
 
+// The same for reach walks on the walk image: each lane first looks up its
+// row's location (an L2 hit: the table is 4 B per vertex), then the warp
+// gathers the rows' first two blocks (64 B), zero-filling past a one-block
+// row. Returns this lane's location.
+__device__ __forceinline__ uint32_t issue_rows_img(const WalkImage& img, uint32_t my_row,
+                                                   uint4* stage) {
+  using Gt = Gather<kCapH>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t sub = lane / Gt::kLanesPerRow;
+  const uint32_t chunk = lane % Gt::kLanesPerRow;
+  uint32_t loc = 0;
+  if (my_row != kNoVertex) loc = __ldg(img.loc + my_row);
+  if (__any_sync(kFull, my_row != kNoVertex)) {
+#pragma unroll
+    for (int j = 0; j < Gt::kRounds; ++j) {
+      const uint32_t r = j * Gt::kRowsPerRound + sub;
+      const uint32_t u = __shfl_sync(kFull, my_row, r);
+      const uint32_t l = __shfl_sync(kFull, loc, r);
+      const uint32_t f = l & 7u;
+      const bool live = u != kNoVertex && chunk < (f >= 2 ? 4u : 2u);
+      const uint4* src = img.rec + (live ? 2ull * (l >> 3) + chunk : 0ull);
+      cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
+    }
+  }
+  cp_async_commit();
+  return loc;
+}
+
 template <int C, bool kMinPath, int kWarps, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_walk(DevGraph<C> g, const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
            const uint32_t* __restrict__ nq_dev, WalkParams P, ReachOut rout, MinScratch S,
-           WalkCounters* ctr, unsigned int* __restrict__ work) {
+           WalkCounters* ctr, unsigned int* __restrict__ work, WalkImage img) {
   using L = WalkLayout<C, kWarps>;
   // A drained warp with at most this many live walkers finishes them
   // lane by lane (the thin tail below).
@@ -387,10 +517,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     return 0xFFFFFFFFu;
   };
 
+  // Row fetch of this step: the walk image for reach walks, G's slabs for
+  // min-path walks.
+  auto issue = [&](Slot& w, uint32_t r) {
+    if constexpr (kMinPath) issue_rows(g, r, stage0);
+    else w.loc = issue_rows_img(img, r, stage0);
+  };
   Slot w;
   w.has = false;
   refill(w);
-  issue_rows(g, row_of(w), stage0);
+  issue(w, row_of(w));
   for (;;) {
     // Thin tail: the queue is drained, so no lane takes new work, and at
     // most kTailLanes walkers are left in the warp. Every lane then runs its
@@ -424,8 +560,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       } else {
         w.rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
         uint32_t deg = 0;
-        const bool ok =
-            walk_step(g, stage0 + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
+        bool ok;
+        if constexpr (kMinPath) {
+          ok = walk_step(g, stage0 + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
+        } else {
+          uint4 v[8];
+          const uint4* st = stage0 + lane * Gather<C>::kStride;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = st[i];  // shared-memory reads (LDS.128)
+          ok = img_step(g, img, v, w.loc, w.prev, u, next, ew, deg);
+        }
         my_bytes += step_bytes(deg);
         if (!ok) term = kDeadEnd;
       }
@@ -433,7 +577,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (early) {
       __syncwarp();  // every lane has read its staged row
       const bool cont = w.has && term == 0xFFFFFFFFu && next != w.tgt && w.steps + 1 < P.T;
-      issue_rows(g, cont ? next : kNoVertex, stage0);
+      issue(w, cont ? next : kNoVertex);
     }
     if (w.has) {
       if (term == 0xFFFFFFFFu) term = advance(w, next, ew);
@@ -442,7 +586,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (!early) {
       __syncwarp();  // every lane has read its staged row before the slot is refilled
       refill(w);
-      issue_rows(g, row_of(w), stage0);
+      issue(w, row_of(w));
     }
     if (!__any_sync(kFull, w.has)) break;
   }
@@ -450,14 +594,23 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     cp_async_wait<0>();
     __syncwarp();
     if (w.has) {
+      // Min-path walks: whole G slabs in registers. Reach walks: whole image
+      // rows (every block in one round trip, the location first).
       RowRegs<C> r;
-      if (w.steps < P.T) {  // its current row is staged (head chunks)
+      uint4 v[8];
+      uint32_t loc = w.loc;
+      if (w.steps < P.T) {  // its current row is staged (the first chunks)
         const uint4* st = stage0 + lane * Gather<C>::kStride;
+        if constexpr (kMinPath) {
 #pragma unroll
-        for (int i = 0; i < Gather<C>::kChunks; ++i) r.v[i] = st[i];
-        const uint4* src = reinterpret_cast<const uint4*>(g.slab + w.cur);
+          for (int i = 0; i < Gather<C>::kChunks; ++i) r.v[i] = st[i];
+          const uint4* src = reinterpret_cast<const uint4*>(g.slab + w.cur);
 #pragma unroll
-        for (int i = Gather<C>::kChunks; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
+          for (int i = Gather<C>::kChunks; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = st[i];
+        }
       }
       double u = u01_of(w.rng + kGamma);
       for (;;) {
@@ -468,16 +621,25 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
           term = kStepCap;
         } else {
           w.rng += kGamma;
-          const uint32_t deg = r.s.deg;
-          const bool ok =
-              r.s.ext == kInline
-                  ? sample_inline<C>(r.s, w.prev, u, next, ew)
-                  : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next, ew);
+          uint32_t deg;
+          bool ok;
+          if constexpr (kMinPath) {
+            deg = r.s.deg;
+            ok = r.s.ext == kInline
+                     ? sample_inline<C>(r.s, w.prev, u, next, ew)
+                     : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next,
+                                   ew);
+          } else {
+            ok = img_step(g, img, v, loc, w.prev, u, next, ew, deg);
+          }
           my_bytes += step_bytes(deg);
           if (!ok) term = kDeadEnd;
         }
         if (term == 0xFFFFFFFFu) {
-          if (next != w.tgt && w.steps + 1 < P.T) load_row<C>(g, next, r);
+          if (next != w.tgt && w.steps + 1 < P.T) {
+            if constexpr (kMinPath) load_row<C>(g, next, r);
+            else loc = img_load(img, next, v);
+          }
           u = u01_of(w.rng + kGamma);  // the next draw, while the row is in flight
           term = advance(w, next, ew);
         }
@@ -639,20 +801,21 @@ bool smem_opt_in(K kernel, size_t bytes) {
 template <int C, bool kMinPath>
 void launch_walk(const DevGraph<C>& g, const ReachQuery* rq, const MinQuery* mq,
                  const uint32_t* nq_dev, uint64_t threads, const WalkParams& P, ReachOut ro,
-                 MinScratch S, WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
+                 MinScratch S, WalkCounters* ctr, unsigned int* work, cudaStream_t st,
+                 WalkImage img = WalkImage{}) {
   constexpr int kWarps = 8;
   constexpr int kMinBlocks = kMinPath ? 2 : 3;
   auto k = k_walk<C, kMinPath, kWarps, kMinBlocks>;
   constexpr size_t smem = WalkLayout<C, kWarps>::kBytes;
   smem_opt_in(k, smem);
   k<<<persistent_blocks(k, threads, kWarps * 32, smem), kWarps * 32, smem, st>>>(
-      g, rq, mq, nq_dev, P, ro, S, ctr, work);
+      g, rq, mq, nq_dev, P, ro, S, ctr, work, img);
 }
 
 template <int C>
-int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
-                 uint32_t nq_max, const WalkParams& P, ReachOut out, WalkCounters* ctr,
-                 unsigned int* work, cudaStream_t st, bool standalone) {
+int launch_reach(const DevGraph<C>& g, const WalkImage& img, const ReachQuery* q,
+                 const uint32_t* nq_dev, uint32_t nq_max, const WalkParams& P, ReachOut out,
+                 WalkCounters* ctr, unsigned int* work, cudaStream_t st, bool standalone) {
   if (nq_max == 0) return 0;
   int l = 1;
   if (standalone) {
@@ -660,7 +823,7 @@ int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_d
     ++l;
   }
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
-  launch_walk<C, false>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st);
+  launch_walk<C, false>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st, img);
   if (standalone) {
     k_reach_fix<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_dev);
     ++l;
@@ -692,9 +855,9 @@ int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_d
   return l;
 }
 
-template int launch_reach<kCapH>(const DevGraph<kCapH>&, const ReachQuery*, const uint32_t*,
-                                 uint32_t, const WalkParams&, ReachOut, WalkCounters*,
-                                 unsigned int*, cudaStream_t, bool);
+template int launch_reach<kCapH>(const DevGraph<kCapH>&, const WalkImage&, const ReachQuery*,
+                                 const uint32_t*, uint32_t, const WalkParams&, ReachOut,
+                                 WalkCounters*, unsigned int*, cudaStream_t, bool);
 template int launch_minpath<kCapG>(const DevGraph<kCapG>&, const MinQuery*, const uint32_t*,
                                    uint32_t, const WalkParams&, MinScratch, MinOut,
                                    WalkCounters*, unsigned int*, cudaStream_t, bool);

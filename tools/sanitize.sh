@@ -9,7 +9,7 @@ SEL="tests/test_gpu_replay.py tests/test_gpu_walks.py tests/test_gpu_shard.py te
 for t in $TOOLS; do
   extra=""
   [ "$t" = "memcheck" ] && extra="--leak-check no"
-  [ "$t" = "initcheck" ] && extra="--track-unused-memory no"
+  [ "$t" = "initcheck" ] && extra="--track-unused-memory"
   timeout 2400 compute-sanitizer --tool $t $extra --target-processes all --print-limit 50 \
     --log-file gpurun_out/san_$t.log \
     python -m pytest -q -m gpu $SEL -k "not c3 and not slow" -p no:cacheprovider \
