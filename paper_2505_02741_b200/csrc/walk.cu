@@ -163,33 +163,40 @@ __device__ __forceinline__ void load_row(const DevGraph<C>& g, uint32_t x, RowRe
 }
 
 // ---- reach walks on the compact walk image of H (walk_image.cuh) ----------
-// Entry i of an image row held as uint4 blocks v[2j] (ids / deg) and v[2j+1]
-// (weights), j = i / 2.
+// Entry i of an image row held as uint4 blocks: v[2j] = {id(2j), id(2j+1),
+// loc(2j), loc(2j+1)}, v[2j+1] = {w(2j), w(2j+1)}, j = i / 2.
 __device__ __forceinline__ uint32_t img_id(const uint4* v, int i) {
-  const uint4 lo = v[2 * (i >> 1)];
-  return i < 2 ? ((i & 1) ? lo.z : lo.y) : ((i & 1) ? lo.y : lo.x);
+  const uint4 a = v[2 * (i >> 1)];
+  return (i & 1) ? a.y : a.x;
+}
+__device__ __forceinline__ uint32_t img_loc(const uint4* v, int i) {
+  const uint4 a = v[2 * (i >> 1)];
+  return (i & 1) ? a.w : a.z;
 }
 __device__ __forceinline__ double img_w(const uint4* v, int i) {
-  const uint4 hi = v[2 * (i >> 1) + 1];
-  return (i & 1) ? __hiloint2double(static_cast<int>(hi.w), static_cast<int>(hi.z))
-                 : __hiloint2double(static_cast<int>(hi.y), static_cast<int>(hi.x));
+  const uint4 b = v[2 * (i >> 1) + 1];
+  return (i & 1) ? __hiloint2double(static_cast<int>(b.w), static_cast<int>(b.z))
+                 : __hiloint2double(static_cast<int>(b.y), static_cast<int>(b.x));
 }
 
 // sample_neighbor (walk.cpp:17-37) on the first CC entries of an image row
 // (deg <= CC): the same single-pass masked prefix and suffix-popc pick as
-// sample_inline, over entries in row order.
+// sample_inline, over entries in row order; also returns the chosen
+// neighbour's loc (the next row's address and size).
 template <int CC>
 __device__ __forceinline__ bool sample_img(const uint4* v, uint32_t deg, uint32_t prev,
-                                           double u01, uint32_t& next, double& ew) {
+                                           double u01, uint32_t& next, uint32_t& nloc,
+                                           double& ew) {
   const uint32_t live = (1u << deg) - 1u;
   uint32_t cand = 0;
   double prefix[CC];
-  uint32_t ids[CC];
+  uint32_t ids[CC], locs[CC];
   double ws[CC];
   double total = 0.0;
 #pragma unroll
   for (int i = 0; i < CC; ++i) {
     ids[i] = img_id(v, i);
+    locs[i] = img_loc(v, i);
     ws[i] = img_w(v, i);
     const bool c = ((live >> i) & 1u) && ids[i] != prev;
     cand |= static_cast<uint32_t>(c) << i;
@@ -208,24 +215,27 @@ __device__ __forceinline__ bool sample_img(const uint4* v, uint32_t deg, uint32_
 #pragma unroll
     for (int i = 0; i + st < CC; i += 2 * st) {
       ids[i] = up ? ids[i + st] : ids[i];
+      locs[i] = up ? locs[i + st] : locs[i];
       ws[i] = up ? ws[i + st] : ws[i];
     }
   }
   next = ids[0];
+  nloc = locs[0];
   ew = ws[0];
   return true;
 }
 
-// One step on an image row whose first two blocks are in v[0..3] (staged or
-// loaded); rows of degree 5..8 fetch blocks 2-3 (`loc` = the row's image
-// location), rows beyond 8 entries sample H's overflow pool.
+// One step on the image row at `loc` whose first two blocks are in v[0..3]
+// (staged or loaded): rows of degree 5..8 fetch blocks 2-3, pool rows (more
+// than 8 entries) sample H's overflow pool and look the next loc up.
 __device__ __forceinline__ bool img_step(const DevGraph<kCapH>& h, const WalkImage& img,
                                          uint4* v, uint32_t loc, uint32_t prev, double u01,
-                                         uint32_t& next, double& ew, uint32_t& deg) {
-  deg = v[0].x;
-  if (deg <= 4) return sample_img<4>(v, deg, prev, u01, next, ew);
+                                         uint32_t& next, uint32_t& nloc, double& ew,
+                                         uint32_t& deg) {
+  deg = loc & 15u;
+  if (deg <= 4) return sample_img<4>(v, deg, prev, u01, next, nloc, ew);
   if (deg <= kImgMaxInline) {
-    const uint4* src = img.rec + 2ull * (loc >> 3);
+    const uint4* src = img.rec + 2ull * (loc >> 4);
     v[4] = __ldg(src + 4);
     v[5] = __ldg(src + 5);
     if (deg > 6) {
@@ -234,33 +244,34 @@ __device__ __forceinline__ bool img_step(const DevGraph<kCapH>& h, const WalkIma
     } else {
       v[6] = v[7] = make_uint4(0u, 0u, 0u, 0u);
     }
-    return sample_img<8>(v, deg, prev, u01, next, ew);
+    return sample_img<8>(v, deg, prev, u01, next, nloc, ew);
   }
-  const uint32_t ext = v[0].w;
-  return sample_pool(h.pool_id + ext, h.pool_w + ext, deg, prev, u01, next, ew);
+  deg = v[0].x;
+  const uint32_t ext = v[0].y;
+  const bool ok = sample_pool(h.pool_id + ext, h.pool_w + ext, deg, prev, u01, next, ew);
+  if (ok) nloc = __ldg(img.loc + next);
+  return ok;
 }
 
-// The whole image row of x straight into registers (the thin tail): its
-// location, then all of its blocks in one round trip. Returns the location.
-__device__ __forceinline__ uint32_t img_load(const WalkImage& img, uint32_t x, uint4* v) {
-  const uint32_t loc = __ldg(img.loc + x);
-  const uint4* src = img.rec + 2ull * (loc >> 3);
-  const uint32_t f = loc & 7u;
+// The whole image row at `loc` straight into registers (the thin tail):
+// every block of it in one round trip.
+__device__ __forceinline__ void img_load(const WalkImage& img, uint32_t loc, uint4* v) {
+  const uint4* src = img.rec + 2ull * (loc >> 4);
+  const uint32_t d = loc & 15u;
   v[0] = __ldg(src);
   v[1] = __ldg(src + 1);
-  if (f >= 2) {
+  if (d >= 3 && d <= kImgMaxInline) {
     v[2] = __ldg(src + 2);
     v[3] = __ldg(src + 3);
   }
-  if (f >= 3) {
+  if (d >= 5 && d <= kImgMaxInline) {
     v[4] = __ldg(src + 4);
     v[5] = __ldg(src + 5);
   }
-  if (f >= 4) {
+  if (d >= 7 && d <= kImgMaxInline) {
     v[6] = __ldg(src + 6);
     v[7] = __ldg(src + 7);
   }
-  return loc;
 }
 
 // Uniform draw from the SplitMix64 counter (rng.hpp:7-24): `ctr` already
@@ -316,6 +327,7 @@ struct ChunkSmem {  // per warp: the current 32-item chunk
   double w[32];
   unsigned long long seed[32];
   uint32_t qi[32];  // output slot of the item's query (reach)
+  uint32_t loc[32];  // image loc of the item's start vertex (reach)
   double u[32];  // this step's draw, stored before the fetch wait (see k_walk)
 };
 
@@ -353,32 +365,30 @@ __device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row
   cp_async_commit();
 }
 
-// The same for reach walks on the walk image: each lane first looks up its
-// row's location (an L2 hit: the table is 4 B per vertex), then the warp
-// gathers the rows' first two blocks (64 B), zero-filling past a one-block
-// row. Returns this lane's location.
-__device__ __forceinline__ uint32_t issue_rows_img(const WalkImage& img, uint32_t my_row,
-                                                   uint4* stage) {
+// The same for reach walks on the walk image: the rows' locs come with the
+// walkers (each sampled entry carries its neighbour's), so the warp gathers
+// each row's first two blocks (64 B) directly, zero-filling past a one-block
+// row.
+__device__ __forceinline__ void issue_rows_img(const WalkImage& img, uint32_t my_row,
+                                               uint32_t my_loc, uint4* stage) {
   using Gt = Gather<kCapH>;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t sub = lane / Gt::kLanesPerRow;
   const uint32_t chunk = lane % Gt::kLanesPerRow;
-  uint32_t loc = 0;
-  if (my_row != kNoVertex) loc = __ldg(img.loc + my_row);
   if (__any_sync(kFull, my_row != kNoVertex)) {
 #pragma unroll
     for (int j = 0; j < Gt::kRounds; ++j) {
       const uint32_t r = j * Gt::kRowsPerRound + sub;
       const uint32_t u = __shfl_sync(kFull, my_row, r);
-      const uint32_t l = __shfl_sync(kFull, loc, r);
-      const uint32_t f = l & 7u;
-      const bool live = u != kNoVertex && chunk < (f >= 2 ? 4u : 2u);
-      const uint4* src = img.rec + (live ? 2ull * (l >> 3) + chunk : 0ull);
+      const uint32_t l = __shfl_sync(kFull, my_loc, r);
+      const uint32_t d = l & 15u;
+      const bool two = d >= 3 && d <= kImgMaxInline;
+      const bool live = u != kNoVertex && chunk < (two ? 4u : 2u);
+      const uint4* src = img.rec + (live ? 2ull * (l >> 4) + chunk : 0ull);
       cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
     }
   }
   cp_async_commit();
-  return loc;
 }
 
 template <int C, bool kMinPath, int kWarps, int kMinBlocks>
@@ -439,6 +449,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
             cs.pq[lane] = make_uint2(Q.p, Q.q);
             cs.w[lane] = Q.w_pq;
             cs.qi[lane] = qq;
+            cs.loc[lane] = __ldg(img.loc + Q.p);
             qseed = Q.qseed;
           }
           cs.seed[lane] = walker_seed_from(qseed, wi);
@@ -455,7 +466,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         w.tgt = pq.y;
         w.wpq = cs.w[item];
         w.rng = cs.seed[item];
-        if (!kMinPath) w.qi = cs.qi[item];
+        if (!kMinPath) {
+          w.qi = cs.qi[item];
+          w.loc = cs.loc[item];
+        }
         w.prev = kNoVertex;
         w.steps = 0;
         w.acc = 0.0;
@@ -519,14 +533,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
 
   // Row fetch of this step: the walk image for reach walks, G's slabs for
   // min-path walks.
-  auto issue = [&](Slot& w, uint32_t r) {
+  auto issue = [&](uint32_t r, uint32_t l) {
     if constexpr (kMinPath) issue_rows(g, r, stage0);
-    else w.loc = issue_rows_img(img, r, stage0);
+    else issue_rows_img(img, r, l, stage0);
   };
   Slot w;
   w.has = false;
   refill(w);
-  issue(w, row_of(w));
+  issue(row_of(w), w.loc);
   for (;;) {
     // Thin tail: the queue is drained, so no lane takes new work, and at
     // most kTailLanes walkers are left in the warp. Every lane then runs its
@@ -552,7 +566,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     // then ends wastes its fetch (the memory system is idle by then).
     const bool early = drained;
     uint32_t term = 0xFFFFFFFFu;
-    uint32_t next = kNoVertex;
+    uint32_t next = kNoVertex, nloc = 0;
     double ew = 0.0;
     if (w.has) {
       if (w.steps >= P.T) {
@@ -568,7 +582,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
           const uint4* st = stage0 + lane * Gather<C>::kStride;
 #pragma unroll
           for (int i = 0; i < 4; ++i) v[i] = st[i];  // shared-memory reads (LDS.128)
-          ok = img_step(g, img, v, w.loc, w.prev, u, next, ew, deg);
+          ok = img_step(g, img, v, w.loc, w.prev, u, next, nloc, ew, deg);
         }
         my_bytes += step_bytes(deg);
         if (!ok) term = kDeadEnd;
@@ -577,16 +591,19 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (early) {
       __syncwarp();  // every lane has read its staged row
       const bool cont = w.has && term == 0xFFFFFFFFu && next != w.tgt && w.steps + 1 < P.T;
-      issue(w, cont ? next : kNoVertex);
+      issue(cont ? next : kNoVertex, nloc);
     }
     if (w.has) {
-      if (term == 0xFFFFFFFFu) term = advance(w, next, ew);
+      if (term == 0xFFFFFFFFu) {
+        term = advance(w, next, ew);
+        w.loc = nloc;
+      }
       if (term != 0xFFFFFFFFu) finish(w, term);
     }
     if (!early) {
       __syncwarp();  // every lane has read its staged row before the slot is refilled
       refill(w);
-      issue(w, row_of(w));
+      issue(row_of(w), w.loc);
     }
     if (!__any_sync(kFull, w.has)) break;
   }
@@ -598,7 +615,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       // rows (every block in one round trip, the location first).
       RowRegs<C> r;
       uint4 v[8];
-      uint32_t loc = w.loc;
       if (w.steps < P.T) {  // its current row is staged (the first chunks)
         const uint4* st = stage0 + lane * Gather<C>::kStride;
         if constexpr (kMinPath) {
@@ -615,7 +631,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       double u = u01_of(w.rng + kGamma);
       for (;;) {
         uint32_t term = 0xFFFFFFFFu;
-        uint32_t next = kNoVertex;
+        uint32_t next = kNoVertex, nloc = 0;
         double ew = 0.0;
         if (w.steps >= P.T) {
           term = kStepCap;
@@ -630,7 +646,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
                      : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next,
                                    ew);
           } else {
-            ok = img_step(g, img, v, loc, w.prev, u, next, ew, deg);
+            ok = img_step(g, img, v, w.loc, w.prev, u, next, nloc, ew, deg);
           }
           my_bytes += step_bytes(deg);
           if (!ok) term = kDeadEnd;
@@ -638,10 +654,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         if (term == 0xFFFFFFFFu) {
           if (next != w.tgt && w.steps + 1 < P.T) {
             if constexpr (kMinPath) load_row<C>(g, next, r);
-            else loc = img_load(img, next, v);
+            else img_load(img, nloc, v);
           }
           u = u01_of(w.rng + kGamma);  // the next draw, while the row is in flight
           term = advance(w, next, ew);
+          w.loc = nloc;
         }
         if (term != 0xFFFFFFFFu) {
           finish(w, term);

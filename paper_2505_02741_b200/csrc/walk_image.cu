@@ -14,17 +14,22 @@ namespace dyg {
 
 namespace {
 
+constexpr unsigned kFullMask = 0xFFFFFFFFu;
+constexpr uint32_t kChanged = 0x80000000u;  // list entry: the row's loc changed
+
 unsigned grid_of(uint64_t n, unsigned bs = 256) {
   return static_cast<unsigned>(std::min<uint64_t>((n + bs - 1) / bs, 148ull * 64));
 }
 
-// Row v of H as image blocks at `block` (entries in row order).
-__device__ void write_record(const DevGraph<kCapH>& h, uint32_t v, uint4* rec, uint64_t block) {
+// Row v of H as image blocks at `block`: entries in row order, each with its
+// neighbour's current loc.
+__device__ void write_record(const DevGraph<kCapH>& h, uint32_t v, uint4* rec, uint64_t block,
+                             const uint32_t* loc) {
   const RowRef<kCapH> r = row(h, v);
   const uint32_t d = r.deg();
   uint4* out = rec + 2 * block;
   if (d > kImgMaxInline) {
-    out[0] = make_uint4(d, 0u, 0u, r.s->ext);
+    out[0] = make_uint4(d, r.s->ext, 0u, 0u);
     out[1] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
@@ -32,9 +37,10 @@ __device__ void write_record(const DevGraph<kCapH>& h, uint32_t v, uint4* rec, u
   for (uint32_t j = 0; j < nb; ++j) {
     const uint32_t i0 = 2 * j, i1 = 2 * j + 1;
     const uint32_t id0 = i0 < d ? r.id(i0) : 0u, id1 = i1 < d ? r.id(i1) : 0u;
+    const uint32_t l0 = i0 < d ? loc[id0] : 0u, l1 = i1 < d ? loc[id1] : 0u;
     const double w0 = i0 < d ? r.w(i0) : 0.0, w1 = i1 < d ? r.w(i1) : 0.0;
     const unsigned long long b0 = __double_as_longlong(w0), b1 = __double_as_longlong(w1);
-    out[2 * j] = j == 0 ? make_uint4(d, id0, id1, 0u) : make_uint4(id0, id1, 0u, 0u);
+    out[2 * j] = make_uint4(id0, id1, l0, l1);
     out[2 * j + 1] = make_uint4(static_cast<uint32_t>(b0), static_cast<uint32_t>(b0 >> 32),
                                 static_cast<uint32_t>(b1), static_cast<uint32_t>(b1 >> 32));
   }
@@ -45,13 +51,19 @@ __global__ void k_img_blocks(DevGraph<kCapH> h, unsigned long long* blocks) {
     blocks[v] = image_blocks(h.slab[v].deg);
 }
 
-__global__ void k_img_write_all(DevGraph<kCapH> h, const unsigned long long* __restrict__ base,
-                                uint32_t* loc, uint8_t* alloc, uint8_t* dirty, uint4* rec) {
+__global__ void k_img_loc_all(DevGraph<kCapH> h, const unsigned long long* __restrict__ base,
+                              uint32_t* loc, uint8_t* alloc) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < h.n; v += gridDim.x * blockDim.x) {
     const uint32_t d = h.slab[v].deg;
-    write_record(h, v, rec, base[v]);
-    loc[v] = static_cast<uint32_t>(base[v] << 3) | image_fetch(d);
+    loc[v] = make_loc(base[v], d);
     alloc[v] = static_cast<uint8_t>(image_blocks(d));
+  }
+}
+
+__global__ void k_img_write_all(DevGraph<kCapH> h, const uint32_t* __restrict__ loc,
+                                uint8_t* dirty, uint4* rec) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < h.n; v += gridDim.x * blockDim.x) {
+    write_record(h, v, rec, loc[v] >> 4, loc);
     dirty[v] = 0;
   }
 }
@@ -60,62 +72,21 @@ struct ImgDev {
   uint32_t* loc;
   uint8_t* alloc;
   uint8_t* dirty;
+  uint32_t* list;
   uint4* rec;
-  unsigned long long* top;    // [0] blocks handed out, [1] overflow flag
-  unsigned long long* sums;   // per-block scratch of the compaction scan
+  unsigned long long* ctr;    // [0] blocks handed out, [1] overflow, [2] listed rows
+  unsigned long long* sums;   // per-block scratch of the rebuild scan
   unsigned long long cap;
 };
 
-// The flagged rows: rewritten in place, or in new blocks when they outgrew
-// their allocation (one atomic per warp). Should the block pool run out, the
-// whole image is compacted in the same launch: every row rewritten
-// contiguously from H's slabs (a grid-wide scan of the block counts), so the
-// image is always complete when the walk starts. Cooperative launch.
-__global__ void __launch_bounds__(512) k_img_sync(DevGraph<kCapH> h, ImgDev d) {
-  cg::grid_group grid = cg::this_grid();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < h.n; base += stride) {
-    const uint32_t v = base + threadIdx.x;
-    const bool flagged = v < h.n && d.dirty[v] != 0;
-    if (!__any_sync(0xFFFFFFFFu, flagged)) continue;
-    uint32_t deg = 0, need = 0, grow = 0;
-    if (flagged) {
-      d.dirty[v] = 0;
-      deg = h.slab[v].deg;
-      need = image_blocks(deg);
-      grow = need > d.alloc[v] ? need : 0;
-    }
-    uint32_t off = grow;  // inclusive warp prefix of the grown rows' blocks
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, off, o);
-      if (lane >= static_cast<uint32_t>(o)) off += x;
-    }
-    const uint32_t total = __shfl_sync(0xFFFFFFFFu, off, 31);
-    unsigned long long first = 0;
-    if (lane == 31 && total) first = atomicAdd(d.top, static_cast<unsigned long long>(total));
-    first = __shfl_sync(0xFFFFFFFFu, first, 31);
-    if (!flagged) continue;
-    if (grow && first + total > d.cap) {
-      atomicOr(d.top + 1, 1ull);  // out of blocks: compacted below
-      continue;
-    }
-    uint64_t block;
-    if (grow) {
-      block = first + off - grow;
-      d.alloc[v] = static_cast<uint8_t>(need);
-    } else {
-      block = d.loc[v] >> 3;
-    }
-    write_record(h, v, d.rec, block);
-    d.loc[v] = static_cast<uint32_t>(block << 3) | image_fetch(deg);
-  }
-  grid.sync();
-  const bool overflow = *reinterpret_cast<volatile unsigned long long*>(d.top + 1) != 0;
-  if (!overflow) return;  // uniform: read after the grid barrier
-  // Compaction: block b owns vertices [lo, hi), thread t of it the
-  // contiguous sub-range [tlo, thi).
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// The whole image rebuilt contiguously from H's slabs (the block pool ran
+// out). Block b owns vertices [lo, hi), thread t of it a contiguous
+// sub-range; a grid-wide scan of the block counts places the rows.
+__device__ void rebuild_all(const DevGraph<kCapH>& h, const ImgDev& d, cg::grid_group& grid) {
   __shared__ unsigned long long s_scan[512];
   const uint32_t per_block = (h.n + gridDim.x - 1) / gridDim.x;
   const uint32_t lo = min(h.n, blockIdx.x * per_block), hi = min(h.n, lo + per_block);
@@ -138,19 +109,109 @@ __global__ void __launch_bounds__(512) k_img_sync(DevGraph<kCapH> h, ImgDev d) {
   at += s_scan[threadIdx.x] - mine;
   for (uint32_t v = tlo; v < thi; ++v) {
     const uint32_t deg = h.slab[v].deg;
-    write_record(h, v, d.rec, at);
-    d.loc[v] = static_cast<uint32_t>(at << 3) | image_fetch(deg);
+    d.loc[v] = make_loc(at, deg);
     d.alloc[v] = static_cast<uint8_t>(image_blocks(deg));
-    d.dirty[v] = 0;
     at += image_blocks(deg);
   }
   grid.sync();
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) {
+  for (uint32_t v = tlo; v < thi; ++v) {
+    write_record(h, v, d.rec, d.loc[v] >> 4, d.loc);
+    d.dirty[v] = 0;
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long total = 0;
     for (uint32_t b = 0; b < gridDim.x; ++b) total += d.sums[b];
-    d.top[0] = total;  // the compact image's size
-    d.top[1] = 0;
+    d.ctr[0] = total;
+    d.ctr[1] = 0;
+    d.ctr[2] = 0;
   }
+}
+
+// One cooperative launch: the passes A-D of walk_image.cuh.
+__global__ void __launch_bounds__(512) k_img_sync(DevGraph<kCapH> h, ImgDev d) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  // (A) list the flagged rows; new loc (and blocks when a row outgrew its own).
+  for (uint32_t base = blockIdx.x * blockDim.x; base < h.n; base += stride) {
+    const uint32_t v = base + threadIdx.x;
+    const bool flagged = v < h.n && d.dirty[v] != 0;
+    const unsigned fl = __ballot_sync(kFullMask, flagged);
+    if (!fl) continue;
+    uint32_t deg = 0, grow = 0;
+    if (flagged) {
+      deg = h.slab[v].deg;
+      const uint32_t need = image_blocks(deg);
+      grow = need > d.alloc[v] ? need : 0;
+    }
+    uint32_t off = grow;  // inclusive warp prefix of the grown rows' blocks
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(kFullMask, off, o);
+      if (lane >= static_cast<uint32_t>(o)) off += x;
+    }
+    const uint32_t total = __shfl_sync(kFullMask, off, 31);
+    unsigned long long first = 0, slot = 0;
+    if (lane == 31 && total) first = atomicAdd(d.ctr, static_cast<unsigned long long>(total));
+    if (lane == 0) slot = atomicAdd(d.ctr + 2, static_cast<unsigned long long>(__popc(fl)));
+    first = __shfl_sync(kFullMask, first, 31);
+    slot = __shfl_sync(kFullMask, slot, 0);
+    if (!flagged) continue;
+    uint64_t block = d.loc[v] >> 4;
+    if (grow) {
+      if (first + total > d.cap) {
+        atomicOr(d.ctr + 1, 1ull);  // out of blocks: rebuilt below
+        continue;
+      }
+      block = first + off - grow;
+      d.alloc[v] = static_cast<uint8_t>(grow);
+    }
+    const uint32_t nl = make_loc(block, deg);
+    const bool changed = nl != d.loc[v];
+    d.loc[v] = nl;
+    d.list[slot + __popc(fl & ((1u << lane) - 1u))] = v | (changed ? kChanged : 0u);
+  }
+  grid.sync();
+  if (vload(d.ctr + 1) != 0) {  // uniform: read after the grid barrier
+    rebuild_all(h, d, grid);
+    return;
+  }
+  const uint32_t listed = static_cast<uint32_t>(vload(d.ctr + 2));
+  // (B) rewrite the listed rows (their neighbours' locs are final now).
+  for (uint32_t i = gtid; i < listed; i += stride) {
+    const uint32_t v = d.list[i] & ~kChanged;
+    write_record(h, v, d.rec, d.loc[v] >> 4, d.loc);
+  }
+  grid.sync();
+  // (C) an unflagged neighbour y holds the old loc of a changed row v in its
+  // record (its row is unchanged, so it has the entry): patch it.
+  for (uint32_t i = gtid; i < listed; i += stride) {
+    const uint32_t e = d.list[i];
+    if (!(e & kChanged)) continue;
+    const uint32_t v = e & ~kChanged;
+    const uint32_t lv = d.loc[v];
+    const RowRef<kCapH> r = row(h, v);
+    const uint32_t deg = r.deg();
+    for (uint32_t k = 0; k < deg; ++k) {
+      const uint32_t y = r.id(k);
+      if (d.dirty[y]) continue;
+      const uint32_t ly = d.loc[y];
+      const uint32_t dy = ly & 15u;
+      if (dy == kLocPool) continue;  // pool rows hold ids only
+      uint32_t* words = reinterpret_cast<uint32_t*>(d.rec + 2ull * (ly >> 4));
+      for (uint32_t j = 0; j < dy; ++j)
+        if (words[8 * (j >> 1) + (j & 1)] == v) {
+          words[8 * (j >> 1) + 2 + (j & 1)] = lv;
+          break;
+        }
+    }
+  }
+  grid.sync();
+  // (D) clear the flags.
+  for (uint32_t i = gtid; i < listed; i += stride) d.dirty[d.list[i] & ~kChanged] = 0;
+  if (gtid == 0) d.ctr[2] = 0;
 }
 
 __global__ void k_img_copy(const unsigned long long* __restrict__ top, const uint4* __restrict__ src,
@@ -169,14 +230,16 @@ void WalkImageStore::release() {
   cudaFree(loc_);
   cudaFree(alloc_);
   cudaFree(dirty_);
+  cudaFree(list_);
   cudaFree(rec_);
-  cudaFree(top_);
+  cudaFree(ctr_);
   cudaFree(sums_);
   loc_ = nullptr;
   alloc_ = nullptr;
   dirty_ = nullptr;
+  list_ = nullptr;
   rec_ = nullptr;
-  top_ = nullptr;
+  ctr_ = nullptr;
   sums_ = nullptr;
   n_ = 0;
   cap_ = 0;
@@ -194,8 +257,9 @@ void WalkImageStore::allocate(uint32_t n, uint64_t cap_blocks) {
     cuda_check(cudaMalloc(&alloc_, m), "image alloc");
     cuda_check(cudaMalloc(&dirty_, m), "image flags");
     cuda_check(cudaMemset(dirty_, 0, m), "image flags");
-    cuda_check(cudaMalloc(&top_, 2 * sizeof(unsigned long long)), "image top");
-    cuda_check(cudaMemset(top_, 0, 2 * sizeof(unsigned long long)), "image top");
+    cuda_check(cudaMalloc(&list_, sizeof(uint32_t) * m), "image list");
+    cuda_check(cudaMalloc(&ctr_, 3 * sizeof(unsigned long long)), "image counters");
+    cuda_check(cudaMemset(ctr_, 0, 3 * sizeof(unsigned long long)), "image counters");
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -204,6 +268,8 @@ void WalkImageStore::allocate(uint32_t n, uint64_t cap_blocks) {
     cuda_check(cudaMalloc(&sums_, sizeof(unsigned long long) * grid_), "image scan");
   }
   if (cap_blocks > cap_) {
+    // The loc encoding holds 28 bits of block index.
+    if (cap_blocks >= (1ull << 28)) throw DeviceError{4, "walk image too large"};
     cudaFree(rec_);
     rec_ = nullptr;
     cuda_check(cudaMalloc(&rec_, 32ull * cap_blocks), "image blocks");
@@ -228,12 +294,13 @@ void WalkImageStore::build(const DevGraph<kCapH>& h, cudaStream_t st) {
   cuda_check(cudaMemcpyAsync(&total, base + n, sizeof total, cudaMemcpyDeviceToHost, st),
              "image size");
   cuda_check(cudaStreamSynchronize(st), "image size");
-  // Room for rows that outgrow their blocks between compactions, and at
-  // least what any compact image of this H can need (ensure_capacity).
+  // Room for rows that outgrow their blocks between rebuilds, and at least
+  // what any compact image of this H can need (ensure_capacity).
   allocate(n, std::max<uint64_t>(cap_, total + std::max<uint64_t>(total, 2ull * n) + 64));
-  k_img_write_all<<<grid_of(n), 256, 0, st>>>(h, base, loc_, alloc_, dirty_, rec_);
-  const unsigned long long init[2] = {total, 0ull};
-  cuda_check(cudaMemcpyAsync(top_, init, sizeof init, cudaMemcpyHostToDevice, st), "image top");
+  k_img_loc_all<<<grid_of(n), 256, 0, st>>>(h, base, loc_, alloc_);
+  k_img_write_all<<<grid_of(n), 256, 0, st>>>(h, loc_, dirty_, rec_);
+  const unsigned long long init[3] = {total, 0ull, 0ull};
+  cuda_check(cudaMemcpyAsync(ctr_, init, sizeof init, cudaMemcpyHostToDevice, st), "image top");
   cuda_check(cudaGetLastError(), "image build");
   cuda_check(cudaStreamSynchronize(st), "image build");
   cudaFree(d_temp);
@@ -243,7 +310,7 @@ void WalkImageStore::build(const DevGraph<kCapH>& h, cudaStream_t st) {
 }
 
 int WalkImageStore::sync(const DevGraph<kCapH>& h, cudaStream_t st) {
-  ImgDev d{loc_, alloc_, dirty_, rec_, top_, sums_, cap_};
+  ImgDev d{loc_, alloc_, dirty_, list_, rec_, ctr_, sums_, cap_};
   DevGraph<kCapH> hv = h;
   void* args[] = {&hv, &d};
   cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_img_sync), dim3(grid_),
@@ -256,7 +323,7 @@ void WalkImageStore::ensure_capacity(const DevGraph<kCapH>& h, uint64_t h_edges_
                                      cudaStream_t st) {
   // A compact image needs sum(max(1, ceil(deg / 2))) <= |E_H| + n blocks
   // (2|E_H| entries, two per block, plus one block per row), so with that
-  // much room k_img_sync can always compact in place.
+  // much room k_img_sync can always rebuild in place.
   const uint64_t bound = h_edges_bound + n_ + 64;
   if (bound <= cap_) return;
   allocate(n_, 2 * bound);
@@ -269,10 +336,10 @@ void WalkImageStore::copy_from(const WalkImageStore& o, cudaStream_t st) {
   cuda_check(cudaMemcpyAsync(loc_, o.loc_, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st),
              "image copy");
   cuda_check(cudaMemcpyAsync(alloc_, o.alloc_, n, cudaMemcpyDeviceToDevice, st), "image copy");
-  cuda_check(cudaMemcpyAsync(top_, o.top_, 2 * sizeof(unsigned long long),
+  cuda_check(cudaMemcpyAsync(ctr_, o.ctr_, 3 * sizeof(unsigned long long),
                              cudaMemcpyDeviceToDevice, st), "image copy");
   cuda_check(cudaMemsetAsync(dirty_, 0, n, st), "image copy");
-  k_img_copy<<<148 * 4, 256, 0, st>>>(o.top_, o.rec_, rec_);
+  k_img_copy<<<148 * 4, 256, 0, st>>>(o.ctr_, o.rec_, rec_);
   cuda_check(cudaGetLastError(), "image copy");
   built_ = o.built_;
 }
