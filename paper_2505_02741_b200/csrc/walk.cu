@@ -35,8 +35,12 @@ inline unsigned blocks_for(uint64_t threads, unsigned per_block) {
 // they need no row this iteration.
 template <int C>
 struct Gather {
-  static constexpr int kChunks = C == kCapH ? 4 : 8;   // 16 B chunks fetched
-  static constexpr int kLanesPerRow = kChunks;
+  static constexpr int kChunks = 8;                    // 16 B chunks staged per row
+  // G slabs: 8 lanes x 16 B per 128 B row. H image rows (<= 4 blocks of
+  // 32 B): 4 lanes per row, each copying chunks c and c + 4 -- the whole
+  // row in ONE round trip (a row of 5-8 entries fetched after its first two
+  // blocks made ~90 % of warp steps wait for a second dependent fetch).
+  static constexpr int kLanesPerRow = C == kCapH ? 4 : 8;
   static constexpr int kRowsPerRound = 32 / kLanesPerRow;
   static constexpr int kRounds = 32 / kRowsPerRound;
   static constexpr int kStride = kChunks + 1;          // uint4 per staged row
@@ -225,27 +229,16 @@ __device__ __forceinline__ bool sample_img(const uint4* v, uint32_t deg, uint32_
   return true;
 }
 
-// One step on the image row at `loc` whose first two blocks are in v[0..3]
-// (staged or loaded): rows of degree 5..8 fetch blocks 2-3, pool rows (more
-// than 8 entries) sample H's overflow pool and look the next loc up.
+// One step on the image row at `loc`, all of whose blocks are in v[]
+// (staged or loaded); pool rows (more than 8 entries) sample H's overflow
+// pool and look the next loc up.
 __device__ __forceinline__ bool img_step(const DevGraph<kCapH>& h, const WalkImage& img,
-                                         uint4* v, uint32_t loc, uint32_t prev, double u01,
+                                         const uint4* v, uint32_t loc, uint32_t prev, double u01,
                                          uint32_t& next, uint32_t& nloc, double& ew,
                                          uint32_t& deg) {
   deg = loc & 15u;
   if (deg <= 4) return sample_img<4>(v, deg, prev, u01, next, nloc, ew);
-  if (deg <= kImgMaxInline) {
-    const uint4* src = img.rec + 2ull * (loc >> 4);
-    v[4] = __ldg(src + 4);
-    v[5] = __ldg(src + 5);
-    if (deg > 6) {
-      v[6] = __ldg(src + 6);
-      v[7] = __ldg(src + 7);
-    } else {
-      v[6] = v[7] = make_uint4(0u, 0u, 0u, 0u);
-    }
-    return sample_img<8>(v, deg, prev, u01, next, nloc, ew);
-  }
+  if (deg <= kImgMaxInline) return sample_img<8>(v, deg, prev, u01, next, nloc, ew);
   deg = v[0].x;
   const uint32_t ext = v[0].y;
   const bool ok = sample_pool(h.pool_id + ext, h.pool_w + ext, deg, prev, u01, next, ew);
@@ -382,10 +375,12 @@ __device__ __forceinline__ void issue_rows_img(const WalkImage& img, uint32_t my
       const uint32_t u = __shfl_sync(kFull, my_row, r);
       const uint32_t l = __shfl_sync(kFull, my_loc, r);
       const uint32_t d = l & 15u;
-      const bool two = d >= 3 && d <= kImgMaxInline;
-      const bool live = u != kNoVertex && chunk < (two ? 4u : 2u);
-      const uint4* src = img.rec + (live ? 2ull * (l >> 4) + chunk : 0ull);
-      cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
+      const uint32_t chunks = d <= kImgMaxInline ? 2u * image_blocks(d) : 2u;
+      const bool live = u != kNoVertex && chunk < chunks;
+      const bool live2 = u != kNoVertex && chunk + 4 < chunks;
+      const uint64_t at = 2ull * (l >> 4) + chunk;
+      cp_async16(stage + r * Gt::kStride + chunk, img.rec + (live ? at : 0ull), live ? 16u : 0u);
+      if (live2) cp_async16(stage + r * Gt::kStride + chunk + 4, img.rec + at + 4, 16u);
     }
   }
   cp_async_commit();
@@ -582,6 +577,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
           const uint4* st = stage0 + lane * Gather<C>::kStride;
 #pragma unroll
           for (int i = 0; i < 4; ++i) v[i] = st[i];  // shared-memory reads (LDS.128)
+          if ((w.loc & 15u) > 4u) {
+#pragma unroll
+            for (int i = 4; i < 8; ++i) v[i] = st[i];
+          }
           ok = img_step(g, img, v, w.loc, w.prev, u, next, nloc, ew, deg);
         }
         my_bytes += step_bytes(deg);
@@ -625,7 +624,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
           for (int i = Gather<C>::kChunks; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
         } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = st[i];
+          for (int i = 0; i < 8; ++i) v[i] = st[i];
         }
       }
       double u = u01_of(w.rng + kGamma);

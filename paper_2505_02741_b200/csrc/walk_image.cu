@@ -15,7 +15,6 @@ namespace dyg {
 namespace {
 
 constexpr unsigned kFullMask = 0xFFFFFFFFu;
-constexpr uint32_t kChanged = 0x80000000u;  // list entry: the row's loc changed
 
 unsigned grid_of(uint64_t n, unsigned bs = 256) {
   return static_cast<unsigned>(std::min<uint64_t>((n + bs - 1) / bs, 148ull * 64));
@@ -128,36 +127,55 @@ __device__ void rebuild_all(const DevGraph<kCapH>& h, const ImgDev& d, cg::grid_
   }
 }
 
-// One cooperative launch: the passes A-D of walk_image.cuh.
+// Block-wide exclusive sum of x (blockDim.x == 512); *total receives the sum.
+__device__ __forceinline__ uint32_t block_exclusive(uint32_t x, uint32_t* total) {
+  __shared__ uint32_t s_warp[16];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFullMask, inc, o);
+    if (lane >= static_cast<uint32_t>(o)) inc += y;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  uint32_t before = 0, sum = 0;
+  for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+    const uint32_t t = s_warp[w];
+    before += w < wid ? t : 0u;
+    sum += t;
+  }
+  __syncthreads();
+  *total = sum;
+  return before + inc - x;
+}
+
+// One cooperative launch: the passes A-D of walk_image.cuh. Flag values:
+// 1 = row changed, 2 = row changed and its loc moved.
 __global__ void __launch_bounds__(512) k_img_sync(DevGraph<kCapH> h, ImgDev d) {
   cg::grid_group grid = cg::this_grid();
-  const uint32_t lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * blockDim.x;
   const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  // (A) list the flagged rows; new loc (and blocks when a row outgrew its own).
-  for (uint32_t base = blockIdx.x * blockDim.x; base < h.n; base += stride) {
-    const uint32_t v = base + threadIdx.x;
+  __shared__ unsigned long long s_first;
+  // (A) new loc for every flagged row (and blocks when it outgrew its own;
+  // one allocation per block and iteration).
+  const uint32_t rounds = (h.n + stride - 1) / stride;
+  for (uint32_t it = 0; it < rounds; ++it) {
+    const uint32_t v = it * stride + gtid;
     const bool flagged = v < h.n && d.dirty[v] != 0;
-    const unsigned fl = __ballot_sync(kFullMask, flagged);
-    if (!fl) continue;
     uint32_t deg = 0, grow = 0;
     if (flagged) {
       deg = h.slab[v].deg;
       const uint32_t need = image_blocks(deg);
       grow = need > d.alloc[v] ? need : 0;
     }
-    uint32_t off = grow;  // inclusive warp prefix of the grown rows' blocks
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t x = __shfl_up_sync(kFullMask, off, o);
-      if (lane >= static_cast<uint32_t>(o)) off += x;
-    }
-    const uint32_t total = __shfl_sync(kFullMask, off, 31);
-    unsigned long long first = 0, slot = 0;
-    if (lane == 31 && total) first = atomicAdd(d.ctr, static_cast<unsigned long long>(total));
-    if (lane == 0) slot = atomicAdd(d.ctr + 2, static_cast<unsigned long long>(__popc(fl)));
-    first = __shfl_sync(kFullMask, first, 31);
-    slot = __shfl_sync(kFullMask, slot, 0);
+    uint32_t total;
+    const uint32_t off = block_exclusive(grow, &total);
+    if (threadIdx.x == 0)
+      s_first = total ? atomicAdd(d.ctr, static_cast<unsigned long long>(total)) : 0ull;
+    __syncthreads();
+    const unsigned long long first = s_first;
+    __syncthreads();
     if (!flagged) continue;
     uint64_t block = d.loc[v] >> 4;
     if (grow) {
@@ -165,32 +183,26 @@ __global__ void __launch_bounds__(512) k_img_sync(DevGraph<kCapH> h, ImgDev d) {
         atomicOr(d.ctr + 1, 1ull);  // out of blocks: rebuilt below
         continue;
       }
-      block = first + off - grow;
+      block = first + off;
       d.alloc[v] = static_cast<uint8_t>(grow);
     }
     const uint32_t nl = make_loc(block, deg);
-    const bool changed = nl != d.loc[v];
+    if (nl != d.loc[v]) d.dirty[v] = 2;
     d.loc[v] = nl;
-    d.list[slot + __popc(fl & ((1u << lane) - 1u))] = v | (changed ? kChanged : 0u);
   }
   grid.sync();
   if (vload(d.ctr + 1) != 0) {  // uniform: read after the grid barrier
     rebuild_all(h, d, grid);
     return;
   }
-  const uint32_t listed = static_cast<uint32_t>(vload(d.ctr + 2));
-  // (B) rewrite the listed rows (their neighbours' locs are final now).
-  for (uint32_t i = gtid; i < listed; i += stride) {
-    const uint32_t v = d.list[i] & ~kChanged;
-    write_record(h, v, d.rec, d.loc[v] >> 4, d.loc);
-  }
+  // (B) rewrite the flagged rows (their neighbours' locs are final now).
+  for (uint32_t v = gtid; v < h.n; v += stride)
+    if (d.dirty[v]) write_record(h, v, d.rec, d.loc[v] >> 4, d.loc);
   grid.sync();
-  // (C) an unflagged neighbour y holds the old loc of a changed row v in its
+  // (C) an unflagged neighbour y holds the old loc of a moved row v in its
   // record (its row is unchanged, so it has the entry): patch it.
-  for (uint32_t i = gtid; i < listed; i += stride) {
-    const uint32_t e = d.list[i];
-    if (!(e & kChanged)) continue;
-    const uint32_t v = e & ~kChanged;
+  for (uint32_t v = gtid; v < h.n; v += stride) {
+    if (d.dirty[v] != 2) continue;
     const uint32_t lv = d.loc[v];
     const RowRef<kCapH> r = row(h, v);
     const uint32_t deg = r.deg();
@@ -210,8 +222,8 @@ __global__ void __launch_bounds__(512) k_img_sync(DevGraph<kCapH> h, ImgDev d) {
   }
   grid.sync();
   // (D) clear the flags.
-  for (uint32_t i = gtid; i < listed; i += stride) d.dirty[d.list[i] & ~kChanged] = 0;
-  if (gtid == 0) d.ctr[2] = 0;
+  for (uint32_t v = gtid; v < h.n; v += stride)
+    if (d.dirty[v]) d.dirty[v] = 0;
 }
 
 __global__ void k_img_copy(const unsigned long long* __restrict__ top, const uint4* __restrict__ src,
