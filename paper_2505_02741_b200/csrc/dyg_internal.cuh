@@ -116,15 +116,7 @@ struct DevGraph {
   unsigned long long pool_cap;
   unsigned long long* edges;      // |E| (device counter)
   uint32_t n;
-  // H only: per-row "changed" flags for the walk image (walk_image.cuh);
-  // every row mutation below sets them (nullptr: not tracked).
-  uint8_t* dirty;
 };
-
-template <int C>
-__device__ __forceinline__ void mark_dirty(const DevGraph<C>& g, uint32_t u) {
-  if (g.dirty) g.dirty[u] = 1;
-}
 
 // ---------------------------------------------------------------- rows
 // Index-based view of row u (inline slab or overflow block).
@@ -185,7 +177,6 @@ __device__ __forceinline__ bool row_push(const DevGraph<C>& g, uint32_t u, uint3
                                          double w) {
   Slab<C>& s = g.slab[u];
   const uint32_t d = s.deg;
-  mark_dirty(g, u);
   if (s.ext == kInline) {
     if (d < C) {
       s.idr(d) = id;
@@ -223,7 +214,6 @@ template <int C>
 __device__ __forceinline__ void row_remove_at(const DevGraph<C>& g, uint32_t u, uint32_t i) {
   const RowRef<C> r = row(g, u);
   const uint32_t last = r.deg() - 1;
-  mark_dirty(g, u);
   r.set(i, r.id(last), r.w(last));
   r.s->deg = last;
 }
@@ -240,8 +230,6 @@ __device__ __forceinline__ int insert_edge(const DevGraph<C>& g, uint32_t u, uin
     const double nw = __dadd_rn(ru.w(static_cast<uint32_t>(i)), w);
     ru.set_w(static_cast<uint32_t>(i), nw);
     row(g, v).set_w(static_cast<uint32_t>(row_find(g, v, u)), nw);
-    mark_dirty(g, u);
-    mark_dirty(g, v);
     return 1;
   }
   if (!row_push(g, u, v, w)) return -1;

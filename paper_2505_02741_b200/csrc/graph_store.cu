@@ -105,7 +105,6 @@ void GraphStore<C>::release() {
   cudaFree(v_.pool_w);
   cudaFree(counters_);
   v_ = DevGraph<C>{};
-  v_.dirty = dirty_;
   counters_ = nullptr;
 }
 

@@ -45,15 +45,11 @@ class GraphStore {
   unsigned long long* pool_top_ptr() const { return v_.pool_top; }
   bool allocated() const { return v_.slab != nullptr; }
   void release();
-  // Row-change flags the device mutators set (the walk image's sync input);
-  // kept across reallocations.
-  void set_dirty(uint8_t* dirty) { dirty_ = dirty; v_.dirty = dirty; }
 
  private:
   void allocate(uint32_t n, uint64_t pool_cap);
   DevGraph<C> v_{};
   unsigned long long* counters_ = nullptr;  // [0] pool_top, [1] edges
-  uint8_t* dirty_ = nullptr;                 // not owned
 };
 
 // Initial sparsifier on the device (init_sparsifier.cu): G as a host CSR in

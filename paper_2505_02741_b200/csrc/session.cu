@@ -110,7 +110,6 @@ struct dyg_session {
 
   GraphStore<kCapG> G, G_snap;
   GraphStore<kCapH> H, H_snap;
-  WalkImageStore img, img_snap;  // K1's compact view of H (walk_image.cuh)
   uint64_t counter = 0, counter_snap = 0;
   uint64_t g_edges = 0, h_edges = 0, g_top = 0, h_top = 0;
   uint64_t g_edges_snap = 0, h_edges_snap = 0, g_top_snap = 0, h_top_snap = 0;
@@ -493,11 +492,6 @@ void ensure_pools(dyg_session* s, uint64_t n_ins, uint64_t n_del) {
   // (+ the worst-case appends of asynchronous shard commits not yet read back)
   s->G.ensure_pool(s->g_top + s->shard_pend_g, 4 * g_app + (1u << 16), s->stream);
   s->H.ensure_pool(s->h_top + s->shard_pend_h, 4 * h_app + (1u << 16), s->stream);
-  // H's edges can grow by one per insertion and T + 2 per deletion (a
-  // recovered path, or the two fallback edges): the walk image keeps room
-  // to compact any H that large.
-  s->img.ensure_capacity(s->H.view(),
-                         s->h_edges + s->shard_pend_h / 2 + n_ins + n_del * (T1 + 1), s->stream);
 }
 
 // validate (:405-407), walk shadow (:416-423), query build (:429-457).
@@ -574,9 +568,8 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
       ro.nq_long = &b.ctl->nq_long;
       ro.cap = b.q_cap;
     }
-    p.launches += s->img.sync(s->H.view(), s->stream);  // the image == batch-start H
-    p.launches += launch_reach(s->H.view(), s->img.view(), rq + lo_r, cnt_r, max_r, P, ro,
-                               &b.ctl->reach, s->d_work, s->stream, /*standalone=*/!full);
+    p.launches += launch_reach(s->H.view(), rq + lo_r, cnt_r, max_r, P, ro, &b.ctl->reach,
+                               s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
   if (full && fast) fork_appends();
@@ -771,13 +764,6 @@ uint64_t session_fingerprint(dyg_session* s, uint64_t tag) {
   };
   add_graph(s->G.view());
   add_graph(s->H.view());
-  {
-    const WalkImage iv = s->img.view();
-    const uint64_t img[] = {reinterpret_cast<uint64_t>(iv.loc), reinterpret_cast<uint64_t>(iv.rec),
-                            s->img.capacity_blocks(),
-                            reinterpret_cast<uint64_t>(s->H.view().dirty)};
-    h = fnv(h, img, sizeof img);
-  }
   BatchDev b = s->b;  // all buffer pointers and capacities; per-batch fields blanked
   b.ctl = nullptr;
   b.events = nullptr;
@@ -1514,8 +1500,6 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
         s->mean_inv_w = nnz ? acc / static_cast<double>(nnz) : 1.0;
       }
       s->H.upload(h->n, h->row_ptr, h->ids, h->w, s->stream);
-      s->img.build(s->H.view(), s->stream);
-      s->H.set_dirty(s->img.dirty());
       s->g_edges = g->row_ptr[g->n] / 2;
       s->h_edges = h->row_ptr[h->n] / 2;
       s->g_top = 0;
@@ -1927,8 +1911,6 @@ int dyg_session_snapshot(dyg_session* s) {
     check(cudaSetDevice(s->device), "set device");
     s->G_snap.copy_from(s->G, s->stream);
     s->H_snap.copy_from(s->H, s->stream);
-    s->stats.kernel_launches += s->img.sync(s->H.view(), s->stream);  // image == H
-    s->img_snap.copy_from(s->img, s->stream);
     check(cudaStreamSynchronize(s->stream), "snapshot");
     s->counter_snap = s->counter;
     s->g_edges_snap = s->g_edges;
@@ -1948,8 +1930,7 @@ int dyg_session_restore(dyg_session* s) {
     check(cudaSetDevice(s->device), "set device");
     s->G.copy_from(s->G_snap, s->stream);
     s->H.copy_from(s->H_snap, s->stream);
-    s->img.copy_from(s->img_snap, s->stream);
-    s->stats.kernel_launches += 3;
+    s->stats.kernel_launches += 2;
     s->counter = s->counter_snap;
     s->g_edges = s->g_edges_snap;
     s->h_edges = s->h_edges_snap;
@@ -2411,8 +2392,6 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
     if (!rq.empty()) {
       GraphStore<kCapH> gh;
       gh.upload(g->n, g->row_ptr, g->ids, g->w, st);
-      WalkImageStore img;
-      img.build(gh.view(), st);
       ReachQuery* d_q = nullptr;
       ReachOut ro{};
       dev_alloc(&d_q, rq.size(), "queries");
@@ -2420,7 +2399,7 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
       dev_alloc(&ro.steps, rq.size(), "out");
       dev_alloc(&ro.best_bits, rq.size(), "out");
       check(cudaMemcpy(d_q, rq.data(), sizeof(ReachQuery) * rq.size(), cudaMemcpyHostToDevice), "q");
-      launch_reach(gh.view(), img.view(), d_q, d_n, counts[0], P, ro, ctr, d_work, st);
+      launch_reach(gh.view(), d_q, d_n, counts[0], P, ro, ctr, d_work, st);
       check(cudaGetLastError(), "reach launch");
       check(cudaStreamSynchronize(st), "reach");
       std::vector<uint32_t> reached(rq.size());

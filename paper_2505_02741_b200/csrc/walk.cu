@@ -35,12 +35,8 @@ inline unsigned blocks_for(uint64_t threads, unsigned per_block) {
 // they need no row this iteration.
 template <int C>
 struct Gather {
-  static constexpr int kChunks = 8;                    // 16 B chunks staged per row
-  // G slabs: 8 lanes x 16 B per 128 B row. H image rows (<= 4 blocks of
-  // 32 B): 4 lanes per row, each copying chunks c and c + 4 -- the whole
-  // row in ONE round trip (a row of 5-8 entries fetched after its first two
-  // blocks made ~90 % of warp steps wait for a second dependent fetch).
-  static constexpr int kLanesPerRow = C == kCapH ? 4 : 8;
+  static constexpr int kChunks = C == kCapH ? 4 : 8;   // 16 B chunks fetched
+  static constexpr int kLanesPerRow = kChunks;
   static constexpr int kRowsPerRound = 32 / kLanesPerRow;
   static constexpr int kRounds = 32 / kRowsPerRound;
   static constexpr int kStride = kChunks + 1;          // uint4 per staged row
@@ -166,107 +162,6 @@ __device__ __forceinline__ void load_row(const DevGraph<C>& g, uint32_t x, RowRe
   for (int i = 0; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
 }
 
-// ---- reach walks on the compact walk image of H (walk_image.cuh) ----------
-// Entry i of an image row held as uint4 blocks: v[2j] = {id(2j), id(2j+1),
-// loc(2j), loc(2j+1)}, v[2j+1] = {w(2j), w(2j+1)}, j = i / 2.
-__device__ __forceinline__ uint32_t img_id(const uint4* v, int i) {
-  const uint4 a = v[2 * (i >> 1)];
-  return (i & 1) ? a.y : a.x;
-}
-__device__ __forceinline__ uint32_t img_loc(const uint4* v, int i) {
-  const uint4 a = v[2 * (i >> 1)];
-  return (i & 1) ? a.w : a.z;
-}
-__device__ __forceinline__ double img_w(const uint4* v, int i) {
-  const uint4 b = v[2 * (i >> 1) + 1];
-  return (i & 1) ? __hiloint2double(static_cast<int>(b.w), static_cast<int>(b.z))
-                 : __hiloint2double(static_cast<int>(b.y), static_cast<int>(b.x));
-}
-
-// sample_neighbor (walk.cpp:17-37) on the first CC entries of an image row
-// (deg <= CC): the same single-pass masked prefix and suffix-popc pick as
-// sample_inline, over entries in row order; also returns the chosen
-// neighbour's loc (the next row's address and size).
-template <int CC>
-__device__ __forceinline__ bool sample_img(const uint4* v, uint32_t deg, uint32_t prev,
-                                           double u01, uint32_t& next, uint32_t& nloc,
-                                           double& ew) {
-  const uint32_t live = (1u << deg) - 1u;
-  uint32_t cand = 0;
-  double prefix[CC];
-  uint32_t ids[CC], locs[CC];
-  double ws[CC];
-  double total = 0.0;
-#pragma unroll
-  for (int i = 0; i < CC; ++i) {
-    ids[i] = img_id(v, i);
-    locs[i] = img_loc(v, i);
-    ws[i] = img_w(v, i);
-    const bool c = ((live >> i) & 1u) && ids[i] != prev;
-    cand |= static_cast<uint32_t>(c) << i;
-    total = __dadd_rn(total, c ? ws[i] : 0.0);
-    prefix[i] = total;
-  }
-  if (total <= 0.0) return false;
-  const double target = __dmul_rn(u01, total);
-  uint32_t hit = 0;
-#pragma unroll
-  for (int i = 0; i < CC; ++i) hit |= static_cast<uint32_t>(target < prefix[i]) << i;
-  const uint32_t sel = hit ? static_cast<uint32_t>(CC - __popc(hit)) : 31u - __clz(cand);
-#pragma unroll
-  for (int st = 1; st < CC; st <<= 1) {
-    const bool up = (sel & static_cast<uint32_t>(st)) != 0;
-#pragma unroll
-    for (int i = 0; i + st < CC; i += 2 * st) {
-      ids[i] = up ? ids[i + st] : ids[i];
-      locs[i] = up ? locs[i + st] : locs[i];
-      ws[i] = up ? ws[i + st] : ws[i];
-    }
-  }
-  next = ids[0];
-  nloc = locs[0];
-  ew = ws[0];
-  return true;
-}
-
-// One step on the image row at `loc`, all of whose blocks are in v[]
-// (staged or loaded); pool rows (more than 8 entries) sample H's overflow
-// pool and look the next loc up.
-__device__ __forceinline__ bool img_step(const DevGraph<kCapH>& h, const WalkImage& img,
-                                         const uint4* v, uint32_t loc, uint32_t prev, double u01,
-                                         uint32_t& next, uint32_t& nloc, double& ew,
-                                         uint32_t& deg) {
-  deg = loc & 15u;
-  if (deg <= 4) return sample_img<4>(v, deg, prev, u01, next, nloc, ew);
-  if (deg <= kImgMaxInline) return sample_img<8>(v, deg, prev, u01, next, nloc, ew);
-  deg = v[0].x;
-  const uint32_t ext = v[0].y;
-  const bool ok = sample_pool(h.pool_id + ext, h.pool_w + ext, deg, prev, u01, next, ew);
-  if (ok) nloc = __ldg(img.loc + next);
-  return ok;
-}
-
-// The whole image row at `loc` straight into registers (the thin tail):
-// every block of it in one round trip.
-__device__ __forceinline__ void img_load(const WalkImage& img, uint32_t loc, uint4* v) {
-  const uint4* src = img.rec + 2ull * (loc >> 4);
-  const uint32_t d = loc & 15u;
-  v[0] = __ldg(src);
-  v[1] = __ldg(src + 1);
-  if (d >= 3 && d <= kImgMaxInline) {
-    v[2] = __ldg(src + 2);
-    v[3] = __ldg(src + 3);
-  }
-  if (d >= 5 && d <= kImgMaxInline) {
-    v[4] = __ldg(src + 4);
-    v[5] = __ldg(src + 5);
-  }
-  if (d >= 7 && d <= kImgMaxInline) {
-    v[6] = __ldg(src + 6);
-    v[7] = __ldg(src + 7);
-  }
-}
-
 // Uniform draw from the SplitMix64 counter (rng.hpp:7-24): `ctr` already
 // advanced by gamma for this draw.
 __device__ __forceinline__ double u01_of(uint64_t ctr) {
@@ -308,7 +203,6 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long lo
 // raw trace and (acc, terminal, steps) for K3.
 struct Slot {
   uint32_t cur, prev, tgt, steps, widx, qi;
-  uint32_t loc;    // reach: image location of cur (walk_image.cuh)
   uint32_t tb[8];  // min-path: the last 8 trace entries (a shift register)
   bool has;
   uint64_t rng;
@@ -320,7 +214,6 @@ struct ChunkSmem {  // per warp: the current 32-item chunk
   double w[32];
   unsigned long long seed[32];
   uint32_t qi[32];  // output slot of the item's query (reach)
-  uint32_t loc[32];  // image loc of the item's start vertex (reach)
   double u[32];  // this step's draw, stored before the fetch wait (see k_walk)
 };
 
@@ -358,39 +251,11 @@ __device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row
   cp_async_commit();
 }
 
-// The same for reach walks on the walk image: the rows' locs come with the
-// walkers (each sampled entry carries its neighbour's), so the warp gathers
-// each row's first two blocks (64 B) directly, zero-filling past a one-block
-// row.
-__device__ __forceinline__ void issue_rows_img(const WalkImage& img, uint32_t my_row,
-                                               uint32_t my_loc, uint4* stage) {
-  using Gt = Gather<kCapH>;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t sub = lane / Gt::kLanesPerRow;
-  const uint32_t chunk = lane % Gt::kLanesPerRow;
-  if (__any_sync(kFull, my_row != kNoVertex)) {
-#pragma unroll
-    for (int j = 0; j < Gt::kRounds; ++j) {
-      const uint32_t r = j * Gt::kRowsPerRound + sub;
-      const uint32_t u = __shfl_sync(kFull, my_row, r);
-      const uint32_t l = __shfl_sync(kFull, my_loc, r);
-      const uint32_t d = l & 15u;
-      const uint32_t chunks = d <= kImgMaxInline ? 2u * image_blocks(d) : 2u;
-      const bool live = u != kNoVertex && chunk < chunks;
-      const bool live2 = u != kNoVertex && chunk + 4 < chunks;
-      const uint64_t at = 2ull * (l >> 4) + chunk;
-      cp_async16(stage + r * Gt::kStride + chunk, img.rec + (live ? at : 0ull), live ? 16u : 0u);
-      if (live2) cp_async16(stage + r * Gt::kStride + chunk + 4, img.rec + at + 4, 16u);
-    }
-  }
-  cp_async_commit();
-}
-
 template <int C, bool kMinPath, int kWarps, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_walk(DevGraph<C> g, const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
            const uint32_t* __restrict__ nq_dev, WalkParams P, ReachOut rout, MinScratch S,
-           WalkCounters* ctr, unsigned int* __restrict__ work, WalkImage img) {
+           WalkCounters* ctr, unsigned int* __restrict__ work) {
   using L = WalkLayout<C, kWarps>;
   // A drained warp with at most this many live walkers finishes them
   // lane by lane (the thin tail below).
@@ -444,7 +309,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
             cs.pq[lane] = make_uint2(Q.p, Q.q);
             cs.w[lane] = Q.w_pq;
             cs.qi[lane] = qq;
-            cs.loc[lane] = __ldg(img.loc + Q.p);
             qseed = Q.qseed;
           }
           cs.seed[lane] = walker_seed_from(qseed, wi);
@@ -461,10 +325,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         w.tgt = pq.y;
         w.wpq = cs.w[item];
         w.rng = cs.seed[item];
-        if (!kMinPath) {
-          w.qi = cs.qi[item];
-          w.loc = cs.loc[item];
-        }
+        if (!kMinPath) w.qi = cs.qi[item];
         w.prev = kNoVertex;
         w.steps = 0;
         w.acc = 0.0;
@@ -526,16 +387,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     return 0xFFFFFFFFu;
   };
 
-  // Row fetch of this step: the walk image for reach walks, G's slabs for
-  // min-path walks.
-  auto issue = [&](uint32_t r, uint32_t l) {
-    if constexpr (kMinPath) issue_rows(g, r, stage0);
-    else issue_rows_img(img, r, l, stage0);
-  };
   Slot w;
   w.has = false;
   refill(w);
-  issue(row_of(w), w.loc);
+  issue_rows(g, row_of(w), stage0);
   for (;;) {
     // Thin tail: the queue is drained, so no lane takes new work, and at
     // most kTailLanes walkers are left in the warp. Every lane then runs its
@@ -561,7 +416,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     // then ends wastes its fetch (the memory system is idle by then).
     const bool early = drained;
     uint32_t term = 0xFFFFFFFFu;
-    uint32_t next = kNoVertex, nloc = 0;
+    uint32_t next = kNoVertex;
     double ew = 0.0;
     if (w.has) {
       if (w.steps >= P.T) {
@@ -569,20 +424,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       } else {
         w.rng += kGamma;  // draw k = steps + 1 (rng.hpp:7-13)
         uint32_t deg = 0;
-        bool ok;
-        if constexpr (kMinPath) {
-          ok = walk_step(g, stage0 + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
-        } else {
-          uint4 v[8];
-          const uint4* st = stage0 + lane * Gather<C>::kStride;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[i] = st[i];  // shared-memory reads (LDS.128)
-          if ((w.loc & 15u) > 4u) {
-#pragma unroll
-            for (int i = 4; i < 8; ++i) v[i] = st[i];
-          }
-          ok = img_step(g, img, v, w.loc, w.prev, u, next, nloc, ew, deg);
-        }
+        const bool ok =
+            walk_step(g, stage0 + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
         my_bytes += step_bytes(deg);
         if (!ok) term = kDeadEnd;
       }
@@ -590,19 +433,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (early) {
       __syncwarp();  // every lane has read its staged row
       const bool cont = w.has && term == 0xFFFFFFFFu && next != w.tgt && w.steps + 1 < P.T;
-      issue(cont ? next : kNoVertex, nloc);
+      issue_rows(g, cont ? next : kNoVertex, stage0);
     }
     if (w.has) {
-      if (term == 0xFFFFFFFFu) {
-        term = advance(w, next, ew);
-        w.loc = nloc;
-      }
+      if (term == 0xFFFFFFFFu) term = advance(w, next, ew);
       if (term != 0xFFFFFFFFu) finish(w, term);
     }
     if (!early) {
       __syncwarp();  // every lane has read its staged row before the slot is refilled
       refill(w);
-      issue(row_of(w), w.loc);
+      issue_rows(g, row_of(w), stage0);
     }
     if (!__any_sync(kFull, w.has)) break;
   }
@@ -610,54 +450,36 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     cp_async_wait<0>();
     __syncwarp();
     if (w.has) {
-      // Min-path walks: whole G slabs in registers. Reach walks: whole image
-      // rows (every block in one round trip, the location first).
       RowRegs<C> r;
-      uint4 v[8];
-      if (w.steps < P.T) {  // its current row is staged (the first chunks)
+      if (w.steps < P.T) {  // its current row is staged (head chunks)
         const uint4* st = stage0 + lane * Gather<C>::kStride;
-        if constexpr (kMinPath) {
 #pragma unroll
-          for (int i = 0; i < Gather<C>::kChunks; ++i) r.v[i] = st[i];
-          const uint4* src = reinterpret_cast<const uint4*>(g.slab + w.cur);
+        for (int i = 0; i < Gather<C>::kChunks; ++i) r.v[i] = st[i];
+        const uint4* src = reinterpret_cast<const uint4*>(g.slab + w.cur);
 #pragma unroll
-          for (int i = Gather<C>::kChunks; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = st[i];
-        }
+        for (int i = Gather<C>::kChunks; i < RowRegs<C>::kChunks; ++i) r.v[i] = __ldg(src + i);
       }
       double u = u01_of(w.rng + kGamma);
       for (;;) {
         uint32_t term = 0xFFFFFFFFu;
-        uint32_t next = kNoVertex, nloc = 0;
+        uint32_t next = kNoVertex;
         double ew = 0.0;
         if (w.steps >= P.T) {
           term = kStepCap;
         } else {
           w.rng += kGamma;
-          uint32_t deg;
-          bool ok;
-          if constexpr (kMinPath) {
-            deg = r.s.deg;
-            ok = r.s.ext == kInline
-                     ? sample_inline<C>(r.s, w.prev, u, next, ew)
-                     : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next,
-                                   ew);
-          } else {
-            ok = img_step(g, img, v, w.loc, w.prev, u, next, nloc, ew, deg);
-          }
+          const uint32_t deg = r.s.deg;
+          const bool ok =
+              r.s.ext == kInline
+                  ? sample_inline<C>(r.s, w.prev, u, next, ew)
+                  : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next, ew);
           my_bytes += step_bytes(deg);
           if (!ok) term = kDeadEnd;
         }
         if (term == 0xFFFFFFFFu) {
-          if (next != w.tgt && w.steps + 1 < P.T) {
-            if constexpr (kMinPath) load_row<C>(g, next, r);
-            else img_load(img, nloc, v);
-          }
+          if (next != w.tgt && w.steps + 1 < P.T) load_row<C>(g, next, r);
           u = u01_of(w.rng + kGamma);  // the next draw, while the row is in flight
           term = advance(w, next, ew);
-          w.loc = nloc;
         }
         if (term != 0xFFFFFFFFu) {
           finish(w, term);
@@ -817,21 +639,20 @@ bool smem_opt_in(K kernel, size_t bytes) {
 template <int C, bool kMinPath>
 void launch_walk(const DevGraph<C>& g, const ReachQuery* rq, const MinQuery* mq,
                  const uint32_t* nq_dev, uint64_t threads, const WalkParams& P, ReachOut ro,
-                 MinScratch S, WalkCounters* ctr, unsigned int* work, cudaStream_t st,
-                 WalkImage img = WalkImage{}) {
+                 MinScratch S, WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
   constexpr int kWarps = 8;
   constexpr int kMinBlocks = kMinPath ? 2 : 3;
   auto k = k_walk<C, kMinPath, kWarps, kMinBlocks>;
   constexpr size_t smem = WalkLayout<C, kWarps>::kBytes;
   smem_opt_in(k, smem);
   k<<<persistent_blocks(k, threads, kWarps * 32, smem), kWarps * 32, smem, st>>>(
-      g, rq, mq, nq_dev, P, ro, S, ctr, work, img);
+      g, rq, mq, nq_dev, P, ro, S, ctr, work);
 }
 
 template <int C>
-int launch_reach(const DevGraph<C>& g, const WalkImage& img, const ReachQuery* q,
-                 const uint32_t* nq_dev, uint32_t nq_max, const WalkParams& P, ReachOut out,
-                 WalkCounters* ctr, unsigned int* work, cudaStream_t st, bool standalone) {
+int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
+                 uint32_t nq_max, const WalkParams& P, ReachOut out, WalkCounters* ctr,
+                 unsigned int* work, cudaStream_t st, bool standalone) {
   if (nq_max == 0) return 0;
   int l = 1;
   if (standalone) {
@@ -839,7 +660,7 @@ int launch_reach(const DevGraph<C>& g, const WalkImage& img, const ReachQuery* q
     ++l;
   }
   const uint64_t threads = static_cast<uint64_t>(nq_max) * P.s;
-  launch_walk<C, false>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st, img);
+  launch_walk<C, false>(g, q, nullptr, nq_dev, threads, P, out, MinScratch{}, ctr, work, st);
   if (standalone) {
     k_reach_fix<<<blocks_for(nq_max, 256), 256, 0, st>>>(out, nq_dev);
     ++l;
@@ -871,9 +692,9 @@ int launch_minpath(const DevGraph<C>& g, const MinQuery* q, const uint32_t* nq_d
   return l;
 }
 
-template int launch_reach<kCapH>(const DevGraph<kCapH>&, const WalkImage&, const ReachQuery*,
-                                 const uint32_t*, uint32_t, const WalkParams&, ReachOut,
-                                 WalkCounters*, unsigned int*, cudaStream_t, bool);
+template int launch_reach<kCapH>(const DevGraph<kCapH>&, const ReachQuery*, const uint32_t*,
+                                 uint32_t, const WalkParams&, ReachOut, WalkCounters*,
+                                 unsigned int*, cudaStream_t, bool);
 template int launch_minpath<kCapG>(const DevGraph<kCapG>&, const MinQuery*, const uint32_t*,
                                    uint32_t, const WalkParams&, MinScratch, MinOut,
                                    WalkCounters*, unsigned int*, cudaStream_t, bool);

@@ -9,7 +9,6 @@
 #pragma once
 
 #include "dyg_internal.cuh"
-#include "walk_image.cuh"
 
 namespace dyg {
 
@@ -96,16 +95,14 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-// Host launchers (walk.cu). Reach walks read H through its walk image
-// (walk_image.cuh), synchronised with H by the caller; min-path walks read
-// G's slabs. nq_dev: device count of queries (nq_max bounds
+// Host launchers (walk.cu). nq_dev: device count of queries (nq_max bounds
 // the launch); work: a device u32 work counter. Standalone (run_batch) the
 // launchers reset it and initialise / finalise the reach outputs; inside a
 // session batch k_scatter does both and best_estimate is not needed.
 // stream: session stream. Each returns the number of kernels launched.
 template <int C>
-int launch_reach(const DevGraph<C>& g, const WalkImage& img, const ReachQuery* q,
-                 const uint32_t* nq_dev, uint32_t nq_max, const WalkParams& P, ReachOut out,
+int launch_reach(const DevGraph<C>& g, const ReachQuery* q, const uint32_t* nq_dev,
+                 uint32_t nq_max, const WalkParams& P, ReachOut out,
                  WalkCounters* ctr, unsigned int* work, cudaStream_t st,
                  bool standalone = true);
 template <int C>
