@@ -267,6 +267,18 @@ int dyg_export_rows(dyg_session* s, int which, uint64_t* row_ptr, uint32_t* ids,
 int dyg_session_snapshot(dyg_session* s);
 int dyg_session_restore(dyg_session* s);
 
+/* Cross-process checkpoint / resume (no reference counterpart --
+ * the reference's SparsifierState lives in one process). Saves (options,
+ * update_counter, G rows, H rows) in reference row order with a checksum;
+ * a session loaded from it continues with the same walker keys
+ * (sparsifier.cpp:431) and adjacency order, so replaying the rest of a
+ * stream gives what the uninterrupted session would have. DYG_ERR_DATA on
+ * an unreadable, truncated or corrupt file. */
+int dyg_session_save(dyg_session* s, const char* path);
+/* SparsifierState::options() (sparsifier.hpp:75). */
+int dyg_session_options(const dyg_session* s, dyg_options* out);
+int dyg_session_load(const char* path, int device, dyg_session** out);
+
 int dyg_session_stats(const dyg_session* s, dyg_stats* out);
 int dyg_session_reset_stats(dyg_session* s);
 

@@ -122,6 +122,9 @@ def lib() -> C.CDLL:
         "dyg_export_rows": (i32, [vp, i32, vp, vp, vp, u64]),
         "dyg_session_snapshot": (i32, [vp]),
         "dyg_session_restore": (i32, [vp]),
+        "dyg_session_save": (i32, [vp, C.c_char_p]),
+        "dyg_session_load": (i32, [C.c_char_p, i32, pvp]),
+        "dyg_session_options": (i32, [vp, C.POINTER(Options)]),
         "dyg_session_stats": (i32, [vp, vp]),
         "dyg_session_reset_stats": (i32, [vp]),
         "dyg_run_batch": (i32, [C.POINTER(Csr), vp, sz, C.POINTER(WalkCfg), vp, vp, i32]),

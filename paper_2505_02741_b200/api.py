@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field, fields
 
 import numpy as np
@@ -479,6 +480,30 @@ class SparsifierState:
 
     def restore(self) -> None:
         _check(_lib.lib().dyg_session_restore(self._s))
+
+    def save(self, path: str) -> None:
+        """Cross-process checkpoint: options, update_counter and both graphs
+        in row order (dyg_session_save)."""
+        _check(_lib.lib().dyg_session_save(self._s, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "SparsifierState":
+        """Resume a checkpoint written by save(): same rows, same update
+        counter, so the rest of a stream replays as it would have."""
+        L = _lib.lib()
+        s = C.c_void_p()
+        _check(L.dyg_session_load(os.fsencode(path), device, C.byref(s)))
+        self = cls.__new__(cls)
+        self._s = s
+        self._shard_keep = []
+        opt = _lib.Options()
+        _check(L.dyg_session_options(s, C.byref(opt)))
+        w = opt.walk
+        self._options = SparsifierOptions(
+            WalkConfig(w.distortion_threshold, w.step_cap, w.walker_count, w.global_seed),
+            bool(opt.batched), bool(opt.freeze_sparsifier))
+        self._n = self.info(0)[0]
+        return self
 
     def stats(self) -> dict:
         st = np.zeros(1, STATS_DTYPE)

@@ -1940,6 +1940,142 @@ int dyg_session_restore(dyg_session* s) {
   });
 }
 
+// ---- cross-process checkpoint (SURVEY.md 5 "checkpoint / resume") --------
+// A checkpoint is (options, update_counter, G rows, H rows) in reference row
+// order: exactly the state SparsifierState carries (sparsifier.hpp:105-111),
+// so a session resumed from it walks with the same keys
+// (walker_seed(seed, update_id, i), sparsifier.cpp:431) and samples the same
+// adjacency order as the one that wrote it. Layout (little-endian):
+//   "DYGCKPT1" | dyg_options | u64 counter | 2 x {u32 n, u32 0, u64 nnz,
+//   u64 row_ptr[n+1], u32 ids[nnz], f64 w[nnz]} | u64 FNV-1a of all before.
+namespace {
+
+constexpr char kCkptMagic[8] = {'D', 'Y', 'G', 'C', 'K', 'P', 'T', '1'};
+
+struct CkptFile {
+  std::FILE* f = nullptr;
+  uint64_t h = 1469598103934665603ull;
+  ~CkptFile() {
+    if (f) std::fclose(f);
+  }
+  void hash(const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  }
+  void put(const void* p, size_t n, const std::string& path) {
+    hash(p, n);
+    if (n && std::fwrite(p, 1, n, f) != n) fail(DYG_ERR_DATA, "cannot write checkpoint " + path);
+  }
+  void get(void* p, size_t n, const std::string& path) {
+    if (n && std::fread(p, 1, n, f) != n)
+      fail(DYG_ERR_DATA, "truncated checkpoint " + path);
+    hash(p, n);
+  }
+};
+
+struct HostRows {
+  uint32_t n = 0;
+  std::vector<uint64_t> row_ptr;
+  std::vector<uint32_t> ids;
+  std::vector<double> w;
+  dyg_csr csr() const { return dyg_csr{n, 0, row_ptr.data(), ids.data(), w.data()}; }
+};
+
+}  // namespace
+
+int dyg_session_options(const dyg_session* s, dyg_options* out) {
+  return guarded([&] {
+    if (s == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    *out = s->opt;
+  });
+}
+
+int dyg_session_save(dyg_session* s, const char* path) {
+  return guarded([&] {
+    require_settled(s);
+    if (s == nullptr || path == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    check(cudaSetDevice(s->device), "set device");
+    HostRows rows[2];
+    for (int which = 0; which < 2; ++which) {
+      HostRows& r = rows[which];
+      r.n = s->n;
+      r.row_ptr.resize(static_cast<size_t>(s->n) + 1);
+      const uint64_t nnz = 2 * (which == 0 ? s->g_edges : s->h_edges);
+      r.ids.resize(nnz);
+      r.w.resize(nnz);
+      const uint64_t got = which == 0
+                               ? s->G.export_rows(r.row_ptr.data(), r.ids.data(), r.w.data(), nnz, s->stream)
+                               : s->H.export_rows(r.row_ptr.data(), r.ids.data(), r.w.data(), nnz, s->stream);
+      if (got != nnz) fail(DYG_ERR_DEVICE, "checkpoint: edge count mismatch on export");
+    }
+    CkptFile out;
+    const std::string p(path);
+    out.f = std::fopen(path, "wb");
+    if (out.f == nullptr) fail(DYG_ERR_DATA, "cannot open checkpoint " + p + " for writing");
+    out.put(kCkptMagic, sizeof kCkptMagic, p);
+    out.put(&s->opt, sizeof s->opt, p);
+    out.put(&s->counter, sizeof s->counter, p);
+    for (const HostRows& r : rows) {
+      const uint32_t hdr[2] = {r.n, 0};
+      const uint64_t nnz = r.ids.size();
+      out.put(hdr, sizeof hdr, p);
+      out.put(&nnz, sizeof nnz, p);
+      out.put(r.row_ptr.data(), r.row_ptr.size() * sizeof(uint64_t), p);
+      out.put(r.ids.data(), nnz * sizeof(uint32_t), p);
+      out.put(r.w.data(), nnz * sizeof(double), p);
+    }
+    const uint64_t sum = out.h;
+    out.put(&sum, sizeof sum, p);
+    if (std::fflush(out.f) != 0) fail(DYG_ERR_DATA, "cannot write checkpoint " + p);
+  });
+}
+
+int dyg_session_load(const char* path, int device, dyg_session** out) {
+  int rc = guarded([&] {
+    if (path == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    *out = nullptr;
+    CkptFile in;
+    const std::string p(path);
+    in.f = std::fopen(path, "rb");
+    if (in.f == nullptr) fail(DYG_ERR_DATA, "cannot open checkpoint " + p);
+    char magic[8];
+    in.get(magic, sizeof magic, p);
+    if (std::memcmp(magic, kCkptMagic, sizeof magic) != 0)
+      fail(DYG_ERR_DATA, "not a checkpoint file: " + p);
+    dyg_options opt{};
+    uint64_t counter = 0;
+    in.get(&opt, sizeof opt, p);
+    in.get(&counter, sizeof counter, p);
+    HostRows rows[2];
+    for (HostRows& r : rows) {
+      uint32_t hdr[2];
+      uint64_t nnz = 0;
+      in.get(hdr, sizeof hdr, p);
+      in.get(&nnz, sizeof nnz, p);
+      if (nnz > (1ull << 40) || hdr[0] == 0xFFFFFFFFu) fail(DYG_ERR_DATA, "corrupt checkpoint " + p);
+      r.n = hdr[0];
+      r.row_ptr.resize(static_cast<size_t>(r.n) + 1);
+      r.ids.resize(nnz);
+      r.w.resize(nnz);
+      in.get(r.row_ptr.data(), r.row_ptr.size() * sizeof(uint64_t), p);
+      in.get(r.ids.data(), nnz * sizeof(uint32_t), p);
+      in.get(r.w.data(), nnz * sizeof(double), p);
+      if (r.row_ptr[0] != 0 || r.row_ptr[r.n] != nnz) fail(DYG_ERR_DATA, "corrupt checkpoint " + p);
+    }
+    const uint64_t want = in.h;
+    uint64_t sum = 0;
+    in.get(&sum, sizeof sum, p);
+    if (sum != want) fail(DYG_ERR_DATA, "checkpoint checksum mismatch: " + p);
+    const dyg_csr g = rows[0].csr(), h = rows[1].csr();
+    dyg_session* s = nullptr;
+    const int created = dyg_session_create(&g, &h, &opt, device, &s);
+    if (created != DYG_OK) fail(created, std::string(g_last_error));
+    s->counter = counter;
+    *out = s;
+  });
+  return rc;
+}
+
 int dyg_session_stats(const dyg_session* s, dyg_stats* out) {
   return guarded([&] {
     if (s == nullptr || out == nullptr) fail(DYG_ERR_USAGE, "null argument");

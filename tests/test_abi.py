@@ -123,3 +123,23 @@ def test_dysparse_adapter_compiles_against_reference_headers(tmp_path):
                     "-I", os.path.join(repo, "oracle", "ref", "fake_eigen"),
                     "-I", os.path.join(ref, "src"), "-I", os.path.join(ref, "tests"),
                     os.path.join(repo, "tests", "cpp", "adapter_test.cpp")], check=True)
+
+
+def test_checkpoint_file_errors_before_device(dyg, tmp_path):
+    """dyg_session_load reads and checks the whole file before touching a
+    device: missing, foreign, truncated and corrupted files are Data errors."""
+    with pytest.raises(dyg.Error) as e:
+        dyg.SparsifierState.load(str(tmp_path / "missing.ckpt"))
+    assert e.value.kind == dyg.ErrorKind.Data and "cannot open checkpoint" in str(e.value)
+    foreign = tmp_path / "foreign.ckpt"
+    foreign.write_bytes(b"NOTACKPT" + bytes(64))
+    with pytest.raises(dyg.Error) as e:
+        dyg.SparsifierState.load(str(foreign))
+    assert e.value.kind == dyg.ErrorKind.Data and "not a checkpoint file" in str(e.value)
+    trunc = tmp_path / "trunc.ckpt"
+    trunc.write_bytes(b"DYGCKPT1" + bytes(20))
+    with pytest.raises(dyg.Error) as e:
+        dyg.SparsifierState.load(str(trunc))
+    assert e.value.kind == dyg.ErrorKind.Data and "truncated checkpoint" in str(e.value)
+    L = _lib.lib()
+    assert L.dyg_session_save(None, b"x") == 1

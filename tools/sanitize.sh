@@ -9,12 +9,11 @@ SEL="tests/test_gpu_replay.py tests/test_gpu_walks.py tests/test_gpu_shard.py te
 for t in $TOOLS; do
   extra=""
   [ "$t" = "memcheck" ] && extra="--leak-check no"
-  [ "$t" = "initcheck" ] && extra="--track-unused-memory"
-  timeout 2400 compute-sanitizer --tool $t $extra --target-processes all --print-limit 50 \
-    --log-file gpurun_out/san_$t.log \
+  timeout ${SAN_TIMEOUT:-1200} compute-sanitizer --tool $t $extra --target-processes all --print-limit 50 \
+    --log-file gpurun_out/san_$t.%p.log \
     python -m pytest -q -m gpu $SEL -k "not c3 and not slow" -p no:cacheprovider \
     > gpurun_out/san_${t}_pytest.log 2>&1
   echo "$t exit $?"
-  grep -h "ERROR SUMMARY" gpurun_out/san_$t.log | sort | uniq -c | head
+  grep -h "ERROR SUMMARY" gpurun_out/san_$t.*.log | sort | uniq -c | head
   tail -2 gpurun_out/san_${t}_pytest.log
 done
