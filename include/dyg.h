@@ -232,6 +232,15 @@ int dyg_replay_stream(dyg_session* s, const dyg_event* events, size_t n_events,
  * unchanged until the next replay call returns. */
 int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
                       uint32_t batch_count);
+/* The same upload for a stream grouped by batch (batch b =
+ * events[batch_offsets[b] .. batch_offsets[b+1]), as in dyg_replay_stream):
+ * from page-locked memory it returns at once -- each batch is DMA'd and its
+ * kinds counted on a copy stream, and dyg_shard_begin_uploaded(b) waits for
+ * batch b alone, so the upload overlaps the earlier batches' work. `events`
+ * must stay valid until the next upload or the session's destruction.
+ * Pageable events fall back to dyg_stream_upload. */
+int dyg_stream_upload_batches(dyg_session* s, const dyg_event* events, size_t n_events,
+                              const uint64_t* batch_offsets, uint32_t batch_count);
 int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* out);
 /* SparsifierState::replay over batches [first, first + count) of the
  * uploaded stream (sparsifier.cpp:550-559): all batches are enqueued back to

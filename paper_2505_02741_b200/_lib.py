@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
         "dyg_replay_batch": (i32, [vp, vp, sz, u32, u32, vp, vp]),
         "dyg_replay_events": (i32, [vp, vp, vp, sz, u32, vp, vp]),
         "dyg_stream_upload": (i32, [vp, vp, sz, u32]),
+        "dyg_stream_upload_batches": (i32, [vp, vp, sz, vp, u32]),
         "dyg_replay_stream": (i32, [vp, vp, sz, vp, u32, vp, vp]),
         "dyg_replay_uploaded": (i32, [vp, u32, vp]),
         "dyg_replay_uploaded_range": (i32, [vp, u32, u32, vp, vp]),

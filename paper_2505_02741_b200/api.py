@@ -457,6 +457,16 @@ class SparsifierState:
         return self.replay_batch(stream, batch_index)
 
     def upload_stream(self, stream: UpdateStream) -> None:
+        """Device-resident copy of the stream. A stream grouped by batch
+        uploads asynchronously, batch by batch (dyg_stream_upload_batches);
+        the stream must then outlive the uploaded replays."""
+        off = stream.batch_offsets()
+        if off is not None and stream.batch_count:
+            self._uploaded = (stream, off)  # the DMA reads them after this returns
+            _check(_lib.lib().dyg_stream_upload_batches(self._s, ptr(stream.events),
+                                                        len(stream.events), ptr(off),
+                                                        stream.batch_count))
+            return
         _check(_lib.lib().dyg_stream_upload(self._s, ptr(stream.events), len(stream.events),
                                             stream.batch_count))
 

@@ -189,6 +189,15 @@ struct dyg_session {
   uint32_t* h_kinds = nullptr;
   uint64_t kinds_cap = 0;
   std::vector<cudaEvent_t> ready;
+  // dyg_stream_upload_batches: per-batch uploads + device kind counts on the
+  // copy stream; batch_ins / batch_del are filled as each batch lands.
+  std::vector<cudaEvent_t> up_ready;
+  std::vector<uint8_t> up_settled;
+  uint32_t* d_up_kinds = nullptr;
+  uint32_t* h_up_kinds = nullptr;
+  uint64_t up_kinds_cap = 0;
+  bool up_pending = false;
+  cudaEvent_t ev_up_fence = nullptr;
   bool no_fastpath = false;        // DYG_NO_FASTPATH: force the round engine
   bool single_pass = true;         // DYG_SINGLE_PASS=0: multi-kernel prepare chain
   bool shadow_lists = true;        // DYG_SHADOW_ROUNDS=1: dependency-round walk shadow
@@ -991,6 +1000,29 @@ void run_host_batch(dyg_session* s, const dyg_event* ev, const uint64_t* positio
                dec_idx);
 }
 
+// Kind counts of an asynchronously uploaded stream (dyg_stream_upload_batches):
+// batch b's counts are read once its upload and count have landed; with
+// b == ~0u every batch is settled and the structure fingerprint computed.
+void settle_upload(dyg_session* s, uint32_t b) {
+  if (!s->up_pending) return;
+  const uint32_t nbat = static_cast<uint32_t>(s->batch_cnt.size());
+  const uint32_t lo = b == ~0u ? 0 : b, hi = b == ~0u ? nbat : std::min(b + 1, nbat);
+  for (uint32_t k = lo; k < hi; ++k) {
+    if (s->up_settled[k]) continue;
+    check(cudaEventSynchronize(s->up_ready[k]), "stream upload");
+    s->batch_ins[k] = s->h_up_kinds[2ull * k];
+    s->batch_del[k] = s->h_up_kinds[2ull * k + 1];
+    s->up_settled[k] = 1;
+  }
+  if (b == ~0u) {
+    s->stream_gen = fnv(fnv(fnv(0xcbf29ce484222325ull, s->batch_off.data(),
+                                sizeof(uint64_t) * s->batch_off.size()),
+                            s->batch_ins.data(), sizeof(uint64_t) * nbat),
+                        s->batch_del.data(), sizeof(uint64_t) * nbat);
+    s->up_pending = false;
+  }
+}
+
 // Host copy / stream positions of uploaded event `off` (nullptr when the
 // stream was DMA'd from a grouped page-locked buffer: positions are then the
 // identity and events are read back from the device on an error).
@@ -1599,6 +1631,10 @@ void dyg_session_destroy(dyg_session* s) {
   if (s->h_ctls) cudaFreeHost(s->h_ctls);
   if (s->h_shard_ctls) cudaFreeHost(s->h_shard_ctls);
   dev_free(s->d_abort);
+  dev_free(s->d_up_kinds);
+  if (s->h_up_kinds) cudaFreeHost(s->h_up_kinds);
+  for (cudaEvent_t e : s->up_ready) cudaEventDestroy(e);
+  if (s->ev_up_fence) cudaEventDestroy(s->ev_up_fence);
   dev_free(s->d_epoch);
   s->G.release();
   s->G_snap.release();
@@ -1668,6 +1704,7 @@ int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
     require_settled(s);
     if (s == nullptr || (n_events && events == nullptr)) fail(DYG_ERR_USAGE, "null argument");
     check(cudaSetDevice(s->device), "set device");
+    settle_upload(s, ~0u);
     uint32_t nbatches = batch_count;
     for (size_t i = 0; i < n_events; ++i) nbatches = std::max(nbatches, events[i].batch_index + 1);
     s->batch_cnt.assign(nbatches, 0);
@@ -1722,6 +1759,85 @@ int dyg_stream_upload(dyg_session* s, const dyg_event* events, size_t n_events,
   });
 }
 
+int dyg_stream_upload_batches(dyg_session* s, const dyg_event* events, size_t n_events,
+                              const uint64_t* batch_offsets, uint32_t batch_count) {
+  return guarded([&] {
+    require_settled(s);
+    if (s == nullptr || batch_offsets == nullptr || (n_events && events == nullptr))
+      fail(DYG_ERR_USAGE, "null argument");
+    if (batch_offsets[0] != 0 || batch_offsets[batch_count] != n_events)
+      fail(DYG_ERR_USAGE, "batch offsets do not cover the events");
+    for (uint32_t b = 0; b < batch_count; ++b)
+      if (batch_offsets[b + 1] < batch_offsets[b]) fail(DYG_ERR_USAGE, "batch offsets must not decrease");
+    if (!host_pinned(events)) {  // pageable: the synchronous grouping path
+      if (dyg_stream_upload(s, events, n_events, batch_count) != DYG_OK)
+        fail(DYG_ERR_USAGE, std::string(g_last_error));
+      return;
+    }
+    check(cudaSetDevice(s->device), "set device");
+    settle_upload(s, ~0u);  // a previous asynchronous upload has landed
+    if (s->copy_stream == nullptr)
+      check(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking), "copy stream");
+    if (s->ev_up_fence == nullptr)
+      check(cudaEventCreateWithFlags(&s->ev_up_fence, cudaEventDisableTiming), "event");
+    if (s->stream_cap < n_events || s->d_stream == nullptr) {
+      check(cudaStreamSynchronize(s->stream), "stream buffer");
+      dev_free(s->d_stream);
+      dev_alloc(&s->d_stream, std::max<size_t>(n_events, 1), "stream");
+      s->stream_cap = std::max<size_t>(n_events, 1);
+    }
+    if (s->up_kinds_cap < batch_count) {
+      check(cudaStreamSynchronize(s->copy_stream), "kind counts");
+      dev_free(s->d_up_kinds);
+      if (s->h_up_kinds) cudaFreeHost(s->h_up_kinds);
+      s->h_up_kinds = nullptr;
+      dev_alloc(&s->d_up_kinds, 2ull * batch_count, "kind counts");
+      check(cudaMallocHost(reinterpret_cast<void**>(&s->h_up_kinds),
+                           2 * sizeof(uint32_t) * std::max<uint32_t>(batch_count, 1)),
+            "pinned kind counts");
+      s->up_kinds_cap = batch_count;
+    }
+    while (s->up_ready.size() < batch_count) {
+      cudaEvent_t e;
+      check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      s->up_ready.push_back(e);
+    }
+    s->batch_off.assign(batch_offsets, batch_offsets + batch_count + 1ull);
+    s->batch_cnt.assign(batch_count, 0);
+    for (uint32_t b = 0; b < batch_count; ++b) s->batch_cnt[b] = batch_offsets[b + 1] - batch_offsets[b];
+    s->batch_ins.assign(batch_count, 0);
+    s->batch_del.assign(batch_count, 0);
+    s->up_settled.assign(batch_count, 0);
+    s->stream_events.clear();
+    s->stream_positions.clear();
+    // The copy stream overwrites d_stream only after the session's enqueued
+    // work (which may still read the previous stream) is done.
+    check(cudaEventRecord(s->ev_up_fence, s->stream), "upload fence");
+    check(cudaStreamWaitEvent(s->copy_stream, s->ev_up_fence, 0), "upload fence");
+    for (uint32_t b = 0; b < batch_count; ++b) {
+      const uint64_t nb = s->batch_cnt[b];
+      if (nb) {
+        check(cudaMemcpyAsync(s->d_stream + batch_offsets[b], events + batch_offsets[b],
+                              sizeof(DevEvent) * nb, cudaMemcpyHostToDevice, s->copy_stream),
+              "stream upload");
+        s->stats.kernel_launches += launch_count_kinds(s->d_stream + batch_offsets[b],
+                                                       static_cast<uint32_t>(nb),
+                                                       s->d_up_kinds + 2ull * b, s->copy_stream);
+        check(cudaMemcpyAsync(s->h_up_kinds + 2ull * b, s->d_up_kinds + 2ull * b,
+                              2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->copy_stream),
+              "kind counts");
+      } else {
+        s->h_up_kinds[2ull * b] = s->h_up_kinds[2ull * b + 1] = 0;
+      }
+      check(cudaEventRecord(s->up_ready[b], s->copy_stream), "upload event");
+    }
+    s->stats.h2d_bytes += sizeof(DevEvent) * n_events;
+    s->stream_batches = batch_count;
+    s->have_stream = true;
+    s->up_pending = true;
+  });
+}
+
 int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* out) {
   return guarded([&] {
     require_settled(s);
@@ -1730,6 +1846,7 @@ int dyg_replay_uploaded(dyg_session* s, uint32_t batch_index, dyg_batch_report* 
     if (batch_index >= s->stream_batches && s->stream_batches > 0)
       fail(DYG_ERR_USAGE, "batch index out of range");
     check(cudaSetDevice(s->device), "set device");
+    settle_upload(s, ~0u);
     if (batch_index >= s->batch_cnt.size()) {
       run_deferred(s, nullptr, nullptr, nullptr, 0, 0, 0, batch_index, out, false);
       return;
@@ -1767,6 +1884,7 @@ int dyg_replay_uploaded_range(dyg_session* s, uint32_t first, uint32_t count,
       fail(DYG_ERR_USAGE, "batch index out of range");
     if (!s->opt.batched) fail(DYG_ERR_USAGE, "batch ranges need batched (deferred) mode");
     check(cudaSetDevice(s->device), "set device");
+    settle_upload(s, ~0u);
     if (per_event_decision)
       for (uint32_t b = first; b < first + count && b < s->batch_cnt.size(); ++b)
         for (uint64_t k = s->batch_off[b]; k < s->batch_off[b + 1]; ++k)
@@ -2177,6 +2295,13 @@ int dyg_shard_begin_uploaded(dyg_session* s, uint32_t batch_index, uint64_t* n_r
   return guarded([&] {
     if (s == nullptr) fail(DYG_ERR_USAGE, "null argument");
     if (batch_index >= s->batch_cnt.size()) fail(DYG_ERR_USAGE, "batch index out of range");
+    check(cudaSetDevice(s->device), "set device");
+    if (s->up_pending) {
+      // Only this batch has to have landed: later uploads keep overlapping
+      // the work enqueued before them.
+      settle_upload(s, batch_index);
+      check(cudaStreamWaitEvent(s->stream, s->up_ready[batch_index], 0), "upload wait");
+    }
     const uint64_t off = s->batch_off[batch_index];
     const size_t n = s->batch_cnt[batch_index];
     s->shard_pos_base = off;
