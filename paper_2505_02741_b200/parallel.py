@@ -78,6 +78,9 @@ class ShardedReplay:
         self.rbytes = state.shard_record_bytes(False)
         self.mbytes = state.shard_record_bytes(True)
         self.bytes_exchanged = 0
+        import torch.distributed as dist
+
+        self._nccl = dist.get_backend(group) == "nccl"
         self._bufs = {}  # reused record buffers (grown on demand)
 
     def _buf(self, key, nbytes):
@@ -108,11 +111,22 @@ class ShardedReplay:
                                        mall.data_ptr() if sm else 0)
 
     def _gather(self, key, local):
+        import torch
         import torch.distributed as dist
 
         out = self._buf(key, self.world * local.numel())
-        if local.numel():
+        if not local.numel():
+            return out
+        if self._nccl:
             dist.all_gather_into_tensor(out, local, group=self.group)
+        else:
+            # A host-side backend (gloo: several ranks sharing one GPU in the
+            # tests): stage the records through host memory, rank-major as
+            # NCCL lays them out.
+            host = local.cpu()
+            parts = [torch.empty_like(host) for _ in range(self.world)]
+            dist.all_gather(parts, host, group=self.group)
+            out.copy_(torch.cat(parts).to(out.device))
         return out
 
     def replay_events(self, events, positions, batch_index: int):
