@@ -368,6 +368,11 @@ int dyg_pcg_solve(const dyg_csr* g, const dyg_csr* h, uint32_t factor_cap, const
                   dyg_pcg_result* out, double* energy_trace, size_t energy_cap);
 /* random_rhs(n, seed) (solver.cpp:146-159), on the host. */
 int dyg_random_rhs(uint32_t n, uint64_t seed, double* out);
+/* Exact Laplacian solves reuse a fill-reducing ordering for an identical H
+ * sparsity pattern, or one differing in at most 5 % of its nonzeros (H
+ * between batches); cumulative counts of exact hits, near hits and fresh
+ * orderings in this process. No reference counterpart. */
+int dyg_spectral_ordering_stats(uint64_t* hits, uint64_t* near_hits, uint64_t* misses);
 
 /* Stateless twin of run_batch (walk.hpp:86-92): uploads g, runs the queries
  * on `device`, returns results in query order. path_buf (nullable) receives

@@ -124,6 +124,7 @@ def lib() -> C.CDLL:
         "dyg_session_snapshot": (i32, [vp]),
         "dyg_session_restore": (i32, [vp]),
         "dyg_session_save": (i32, [vp, C.c_char_p]),
+        "dyg_spectral_ordering_stats": (i32, [C.POINTER(C.c_uint64)] * 3),
         "dyg_session_load": (i32, [C.c_char_p, i32, pvp]),
         "dyg_session_options": (i32, [vp, C.POINTER(Options)]),
         "dyg_session_stats": (i32, [vp, vp]),

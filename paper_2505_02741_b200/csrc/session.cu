@@ -2580,6 +2580,13 @@ int dyg_pcg_solve(const dyg_csr* g, const dyg_csr* h, uint32_t factor_cap, const
   });
 }
 
+int dyg_spectral_ordering_stats(uint64_t* hits, uint64_t* near_hits, uint64_t* misses) {
+  return guarded([&] {
+    if (hits == nullptr || near_hits == nullptr || misses == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    ordering_cache_stats(hits, near_hits, misses);
+  });
+}
+
 int dyg_random_rhs(uint32_t n, uint64_t seed, double* out) {
   return guarded([&] {
     if (out == nullptr && n) fail(DYG_ERR_USAGE, "null argument");

@@ -73,6 +73,10 @@ class SpectralEngine {
   std::vector<double*> scratch_;
 };
 
+// Fill-reducing orderings reused across factorisations (spectral.cu):
+// cumulative exact-pattern hits, near-pattern hits and fresh orderings.
+void ordering_cache_stats(uint64_t* hits, uint64_t* near_hits, uint64_t* misses);
+
 // GroundedLaplacianSolver (laplacian.cpp:57-85) on the device: sparse
 // Cholesky of the grounded Laplacian (METIS ordering, cuSOLVER csrchol),
 // factorised once, solved many times.

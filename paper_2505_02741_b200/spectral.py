@@ -139,3 +139,12 @@ def random_rhs(n: int, seed: int) -> np.ndarray:
     out = np.zeros(max(int(n), 1), np.float64)
     _check(_lib.lib().dyg_random_rhs(int(n), int(seed), ptr(out)))
     return out[: int(n)]
+
+
+def ordering_cache_stats() -> dict:
+    """Fill-reducing orderings reused by the exact Laplacian solves in this
+    process: exact-pattern hits, near-pattern hits (<= 5 % of nonzeros
+    differ) and fresh orderings (dyg_spectral_ordering_stats)."""
+    v = [C.c_uint64() for _ in range(3)]
+    _check(_lib.lib().dyg_spectral_ordering_stats(*[C.byref(x) for x in v]))
+    return {"hits": v[0].value, "near_hits": v[1].value, "misses": v[2].value}

@@ -139,3 +139,35 @@ def test_session_spectral_after_updates(mesh):
     assert e_state.kappa == pytest.approx(d["kappa"], rel=1e-9)
     assert D.calibrate_budget(st, probe_fraction=0.05, rho=1.0) == pytest.approx(
         min(max(d["kappa"], 1.0), 1e6), rel=1e-9)
+
+
+def test_ordering_reused_for_same_and_nearby_patterns():
+    """kappa twice on one H reuses the ordering (exact pattern); after a
+    small edit of H (one added edge) the cached ordering is reused as a near
+    pattern; the results match fresh-ordering results to solver precision."""
+    from paper_2505_02741_b200.spectral import ordering_cache_stats
+
+    g = D.make_mesh(48, 40, 3)
+    h = D.build_initial_sparsifier(g, 0.10, 3)
+    o = D.ConditionOptions(method=D.ConditionMethod.Iterative, tolerance=1e-9)
+    s0 = ordering_cache_stats()
+    e1 = D.condition_number(g, h, o)
+    s1 = ordering_cache_stats()
+    assert s1["misses"] == s0["misses"] + 1
+    e2 = D.condition_number(g, h, o)
+    s2 = ordering_cache_stats()
+    assert s2["hits"] == s1["hits"] + 1 and s2["misses"] == s1["misses"]
+    assert e2.kappa == e1.kappa  # the same ordering: the same factorisation
+    # One more edge of G in H: a near pattern.
+    rp, ids, w = (np.asarray(x) for x in h.rows())
+    grp, gids, gw = (np.asarray(x) for x in g.rows())
+    have = {(u, int(v)) for u in range(len(rp) - 1) for v in ids[rp[u]:rp[u + 1]]}
+    u = next(u for u in range(len(grp) - 1)
+             if any((u, int(v)) not in have for v in gids[grp[u]:grp[u + 1]]))
+    k = next(i for i in range(grp[u], grp[u + 1]) if (u, int(gids[i])) not in have)
+    h.insert_edge(u, int(gids[k]), float(gw[k]))
+    e3 = D.condition_number(g, h, o)
+    s3 = ordering_cache_stats()
+    assert s3["near_hits"] == s2["near_hits"] + 1 and s3["misses"] == s2["misses"]
+    ref = S.condition_iterative(S.laplacian(*rows(g)), S.laplacian(*rows(h)), 1e-9, 400)
+    assert e3.kappa == pytest.approx(ref["kappa"], rel=1e-6)
