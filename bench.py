@@ -351,6 +351,21 @@ def gather_block(stats, n):
     return out
 
 
+def walk_phase_fracs(stats, walk_key, wms, wbytes, peak):
+    """The dominant walk kernel split at the moment its work queue drains:
+    the bulk (the GPU full of walkers, access-rate bound) and the tail (the
+    last walkers' dependent row fetches, latency bound). Bytes are the
+    kernel's own per-step counts, times its device stamps."""
+    k = "reach" if walk_key.startswith("k_reach") else "minpath"
+    t_ms, t_bytes = stats[f"{k}_tail_ms"], stats[f"{k}_tail_row_bytes"]
+    b_ms, b_bytes = wms - t_ms, wbytes - t_bytes
+    if not peak or b_ms <= 0 or t_ms <= 0:
+        return {}
+    return {"frac_bulk": b_bytes / (b_ms * 1e-3) / 1e9 / peak,
+            "frac_tail": t_bytes / (t_ms * 1e-3) / 1e9 / peak,
+            "tail_share_of_time": t_ms / wms, "tail_share_of_bytes": t_bytes / wbytes}
+
+
 def run_ours(args):
     import torch
 
@@ -552,6 +567,7 @@ def run_ours(args):
             "kernel": walk_key, "bound": "hbm", "achieved": achieved, "peak": peak,
             "peak_source": peak_src, "unit": "GB/s",
             "frac": achieved / peak if peak else None,
+            **walk_phase_fracs(stats, walk_key, wms, wbytes, peak),
             "traffic": load_traffic(walk_key.split(" ")[0]),
             "algorithmic_bytes_per_launch": wbytes / max(1, stats["batches"] // 2),
             "avg_launch_ms": wms / max(1, stats["batches"] // 2),

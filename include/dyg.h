@@ -170,6 +170,8 @@ typedef struct dyg_stats {
   double walk_commit_gap_ms;    /* last walk warp -> commit start */
   double batch_gap_ms;          /* previous batch end -> batch start, inside one replay */
   double minpath_walk_ms;       /* the min-path walk kernel alone (minpath_ms adds the winner) */
+  uint64_t reach_tail_row_bytes;   /* reach_row_bytes of steps after the work queue drained */
+  uint64_t minpath_tail_row_bytes;
 } dyg_stats;
 
 typedef struct dyg_session dyg_session;

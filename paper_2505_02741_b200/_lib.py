@@ -47,7 +47,8 @@ STATS_FIELDS = (
     ("commit_rounds_deletion", "u8"), ("flow_ms_promote", "f8"), ("flow_ms_emit", "f8"),
     ("flow_ms_rank", "f8"), ("flow_ms_apply", "f8"), ("flow_ms_reset", "f8"),
     ("graph_launches", "u8"), ("prep_ms", "f8"), ("walk_commit_gap_ms", "f8"),
-    ("batch_gap_ms", "f8"), ("minpath_walk_ms", "f8"),
+    ("batch_gap_ms", "f8"), ("minpath_walk_ms", "f8"), ("reach_tail_row_bytes", "u8"),
+    ("minpath_tail_row_bytes", "u8"),
 )
 STATS_DTYPE = np.dtype([(n, "<" + t) for n, t in STATS_FIELDS])
 

@@ -127,6 +127,7 @@ struct dyg_session {
   DevEvent* d_events = nullptr;
   DevEvent* h_events_pinned = nullptr;
   BatchCtl* h_ctl = nullptr;
+  BatchCtl* d_ctl = nullptr;  // the single-batch control block (b.ctl is re-pointed per batch)
 
   // Device-resident stream.
   DevEvent* d_stream = nullptr;
@@ -463,7 +464,7 @@ void deliver_decisions(const Pending& p) {
 }
 
 void bind_pending(dyg_session* s, Pending& p) {
-  p.dctl = s->b.ctl;
+  p.dctl = s->d_ctl;
   p.hctl = s->h_ctl;
   p.hdec = &s->h_counts[2];
   p.counter_base = s->counter;
@@ -648,6 +649,8 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   }
   s->stats.reach_steps += c.reach.steps;
   s->stats.reach_row_bytes += c.reach.row_bytes;
+  s->stats.reach_tail_row_bytes += c.reach.tail_bytes;
+  s->stats.minpath_tail_row_bytes += c.minpath.tail_bytes;
   auto tail_ms = [](const WalkCounters& w) {
     return (w.t_end > w.t_drain && w.t_drain != ~0ull) ? (w.t_end - w.t_drain) * 1e-6 : 0.0;
   };
@@ -1559,7 +1562,8 @@ int dyg_session_create(const dyg_csr* g, const dyg_csr* h, const dyg_options* op
       s->b.n_vertices = s->n;
       check(cudaMemset(s->b.fl_depth, 0, sizeof(uint32_t) * s->n), "flow depths");
       check(cudaMemset(s->d_round, 0, sizeof(unsigned long long)), "round counter");
-      dev_alloc(&s->b.ctl, 1, "batch ctl");
+      dev_alloc(&s->d_ctl, 1, "batch ctl");
+      s->b.ctl = s->d_ctl;
       dev_alloc(&s->d_counts, 8, "shard / kind counts");
       check(cudaMallocHost(reinterpret_cast<void**>(&s->h_counts), 8 * sizeof(uint32_t)),
             "pinned counts");
@@ -1610,7 +1614,8 @@ void dyg_session_destroy(dyg_session* s) {
   dev_free(s->b.mscratch.steps);
   dev_free(s->b.mscratch.paths);
   dev_free(s->b.mscratch.rvals);
-  dev_free(s->b.ctl);
+  dev_free(s->d_ctl);
+  s->b.ctl = nullptr;
   dev_free(s->d_locks);
   dev_free(s->d_round);
   dev_free(s->d_work);
@@ -2701,6 +2706,9 @@ int dyg_run_batch(const dyg_csr* g, const dyg_walk_query* queries, size_t n_quer
       dev_alloc(&mo.steps, nm, "out");
       dev_alloc(&mo.resistance, nm, "out");
       dev_alloc(&mo.paths, nm * T1, "out");
+      // Entries past a path's length are never written: zero them so the
+      // whole-buffer read-back below copies defined bytes (initcheck).
+      check(cudaMemset(mo.paths, 0, sizeof(uint32_t) * nm * T1), "out");
       dev_alloc(&sc.acc, nm * sw, "scratch");
       dev_alloc(&sc.term, nm * sw, "scratch");
       dev_alloc(&sc.steps, nm * sw, "scratch");

@@ -169,15 +169,17 @@ __device__ __forceinline__ double u01_of(uint64_t ctr) {
 }
 
 __device__ __forceinline__ void add_counters(WalkCounters* ctr, unsigned long long steps,
-                                             unsigned long long bytes) {
+                                             unsigned long long bytes, unsigned long long tail) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     steps += __shfl_xor_sync(kFull, steps, off);
     bytes += __shfl_xor_sync(kFull, bytes, off);
+    tail += __shfl_xor_sync(kFull, tail, off);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&ctr->steps, steps);
     atomicAdd(&ctr->row_bytes, bytes);
+    atomicAdd(&ctr->tail_bytes, tail);
   }
 }
 
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   const unsigned long long t0 = global_ns();
   uint32_t chunk_base = 0, chunk_pos = 32, chunk_end = 32;
   bool drained = false;
-  unsigned long long my_steps = 0, my_bytes = 0;
+  unsigned long long my_steps = 0, my_bytes = 0, my_tail = 0;
 
   // Give every lane of the warp whose slot is empty the next work item.
   auto refill = [&](Slot& w) {
@@ -427,6 +429,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         const bool ok =
             walk_step(g, stage0 + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
         my_bytes += step_bytes(deg);
+        if (early) my_tail += step_bytes(deg);
         if (!ok) term = kDeadEnd;
       }
     }
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
                   ? sample_inline<C>(r.s, w.prev, u, next, ew)
                   : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next, ew);
           my_bytes += step_bytes(deg);
+          my_tail += step_bytes(deg);
           if (!ok) term = kDeadEnd;
         }
         if (term == 0xFFFFFFFFu) {
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     __syncwarp();
   }
   cp_async_wait<0>();
-  add_counters(ctr, my_steps, my_bytes);
+  add_counters(ctr, my_steps, my_bytes, my_tail);
   if (lane == 0) {
     atomicMin(&ctr->t_start, t0);
     atomicMax(&ctr->t_end, global_ns());

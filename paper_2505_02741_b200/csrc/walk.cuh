@@ -82,6 +82,7 @@ struct MinScratch {
 struct WalkCounters {
   unsigned long long steps;
   unsigned long long row_bytes;
+  unsigned long long tail_bytes;  // row_bytes of steps taken after the warp found the queue drained
   // %globaltimer (ns): first warp start, first warp to find the work queue
   // drained, last warp exit -- the post-drain tail is drain..end.
   unsigned long long t_start;   // min

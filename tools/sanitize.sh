@@ -9,11 +9,14 @@ SEL="tests/test_gpu_replay.py tests/test_gpu_walks.py tests/test_gpu_shard.py te
 for t in $TOOLS; do
   extra=""
   [ "$t" = "memcheck" ] && extra="--leak-check no"
-  timeout ${SAN_TIMEOUT:-1200} compute-sanitizer --tool $t $extra --target-processes all --print-limit 50 \
+  timeout ${SAN_TIMEOUT:-1200} compute-sanitizer --tool $t $extra --target-processes all --print-limit ${SAN_PRINT_LIMIT:-20000} \
     --log-file gpurun_out/san_$t.%p.log \
     python -m pytest -q -m gpu $SEL -k "not c3 and not slow" -p no:cacheprovider \
     > gpurun_out/san_${t}_pytest.log 2>&1
   echo "$t exit $?"
-  grep -h "ERROR SUMMARY" gpurun_out/san_$t.*.log | sort | uniq -c | head
+  python tools/san_summary.py gpurun_out/san_$t.*.log > gpurun_out/san_${t}_summary.txt
+  head -40 gpurun_out/san_${t}_summary.txt
+  # keep the raw logs small enough to travel back
+  for f in gpurun_out/san_$t.*.log; do head -3000 "$f" > "$f.head" && mv "$f.head" "$f"; done
   tail -2 gpurun_out/san_${t}_pytest.log
 done
