@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <string>
 #include <vector>
@@ -164,6 +165,10 @@ struct dyg_session {
   BatchCtl* h_shard_ctls = nullptr;
   uint64_t shard_next_counter = 0;
   uint64_t shard_pend_g = 0, shard_pend_h = 0;
+  // The shard batch's record unpack (enqueued with its commit) and a key of
+  // everything it bakes into kernel arguments.
+  std::function<int(dyg_session*)> shard_unpack;
+  uint64_t shard_unpack_key = 0;
 
   dyg_stats stats{};
   BatchCtl* d_ctls = nullptr;      // batch-range control blocks
@@ -505,9 +510,11 @@ void ensure_pools(dyg_session* s, uint64_t n_ins, uint64_t n_del) {
 }
 
 // validate (:405-407), walk shadow (:416-423), query build (:429-457).
-void phase_prepare(dyg_session* s, Pending& p) {
-  WalkOpts o = walk_opts(s);
-  if (p.shard) o.split_wpq = 0.0;  // shard ranges need contiguous reach slots
+// Buffers sized and the host-side batch binding (s->b) pointed at this
+// batch: everything phase_prepare does besides enqueueing. Called before a
+// capture too (nothing may allocate inside one, and a replayed graph does
+// not re-run the host side).
+void prepare_bind(dyg_session* s, const Pending& p) {
   ensure_batch(s, p.nb, p.n_del);
   ensure_pools(s, p.n_ins, p.n_del);
   BatchDev& b = s->b;
@@ -517,12 +524,19 @@ void phase_prepare(dyg_session* s, Pending& p) {
   b.round_ctr = s->d_round;
   b.abort_flag = s->d_abort;
   b.work = s->d_work;
-  const uint32_t use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
-  const uint32_t fast =
-      (p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass) ? 1u : 0u;
   b.side_top = &b.ctl->side_top;
   b.scratch_edges = &b.ctl->scratch_edges;
   if (p.n_del > 0) ensure_side_pool(s);
+}
+
+void phase_prepare(dyg_session* s, Pending& p) {
+  WalkOpts o = walk_opts(s);
+  if (p.shard) o.split_wpq = 0.0;  // shard ranges need contiguous reach slots
+  prepare_bind(s, p);
+  BatchDev& b = s->b;
+  const uint32_t use_absent_limit = (p.n_ins == 0 && p.n_del > 0) ? 1u : 0u;
+  const uint32_t fast =
+      (p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass) ? 1u : 0u;
   p.launches += launch_ctl_init(
       CtlInitArgs{b.ctl, s->d_epoch, p.nb, use_absent_limit, fast, p.counter_base}, s->stream);
   if (p.n_del > 0 && !o.shadow_lists && ++s->stamp == 0) {  // stamps restart
@@ -859,7 +873,7 @@ CapturedGraph* capture_graph(dyg_session* s, uint64_t key, uint64_t counter, F&&
   cg.base = counter;
   cg.cap_base = counter;
   cg.launches = launches;
-  constexpr size_t kMaxGraphs = 64;  // a whole stream's per-batch graphs
+  constexpr size_t kMaxGraphs = 256;  // a whole stream's per-batch graphs (x3 segments when sharded)
   if (s->graphs.size() >= kMaxGraphs) {  // evict the least recently used
     size_t lru = 0;
     for (size_t i = 1; i < s->graphs.size(); ++i)
@@ -883,6 +897,22 @@ void launch_graph(dyg_session* s, CapturedGraph& g, uint64_t counter) {
   g.last_use = ++s->graph_clock;
   check(cudaGraphLaunch(g.exec, s->stream), "graph launch");
   s->stats.graph_launches += 1;
+}
+
+// Enqueue a device sequence through a captured graph keyed by `key` (its
+// first use captures it), or eagerly when graphs are off. `enqueue` returns
+// the kernels it launched; the return value is that count.
+template <class F>
+int enqueue_captured(dyg_session* s, uint64_t key, uint64_t counter, F&& enqueue) {
+  if (graphs_usable(s)) {
+    CapturedGraph* g = find_graph(s, key);
+    if (g == nullptr) g = capture_graph(s, key, counter, enqueue);
+    if (g != nullptr) {
+      launch_graph(s, *g, counter);
+      return g->launches;
+    }
+  }
+  return enqueue();
 }
 
 void run_deferred(dyg_session* s, const DevEvent* dev_events, const DevEvent* host_events,
@@ -2271,7 +2301,19 @@ void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* p
       p.n_del = n_del;
       p.batch = batch_index;
       p.shard = true;
-      phase_prepare(s, p);
+      // The prepare as a captured graph (the multi-GPU split launches its
+      // three device segments per batch -- prepare, walk, commit -- each
+      // as one graph, like the single-GPU path's one graph per batch).
+      prepare_bind(s, p);
+      uint64_t key = session_fingerprint(s, 3);
+      const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
+                                p.nb, p.n_ins, p.n_del};
+      key = fnv(key, shape, sizeof shape);
+      p.launches += enqueue_captured(s, key, p.counter_base, [&] {
+        Pending q = p;
+        phase_prepare(s, q);
+        return q.launches;
+      });
       // No host round trip: the exchange is sized by upper bounds of the
       // query counts (a reach query per insertion at most, a min-path query
       // per deletion); the walk and the commit read the exact counts on the
@@ -2349,10 +2391,20 @@ int dyg_shard_walk(dyg_session* s, int rank, int world, void* reach_records,
     p.n_ins = s->shard_ins;
     p.n_del = s->shard_del;
     s->b.ctl = p.dctl;
-    p.launches += launch_shard_range(s->b, rank, world, s->d_counts + 4, sl_r, sl_m, s->stream);
-    phase_walk(s, p, false, 0, sl_r, 0, sl_m);
-    p.launches += launch_pack(s->b, s->d_counts + 4, sl_r, sl_m, s->opt.walk.step_cap,
-                              reach_records, minpath_records, s->stream);
+    uint64_t key = session_fingerprint(s, 4);
+    const uint64_t shape[] = {static_cast<uint64_t>(rank), static_cast<uint64_t>(world), sl_r, sl_m,
+                              reinterpret_cast<uint64_t>(reach_records),
+                              reinterpret_cast<uint64_t>(minpath_records),
+                              reinterpret_cast<uint64_t>(p.dctl), p.nb, p.n_ins, p.n_del};
+    key = fnv(key, shape, sizeof shape);
+    p.launches += enqueue_captured(s, key, s->shard_counter, [&] {
+      Pending q = p;
+      q.launches = launch_shard_range(s->b, rank, world, s->d_counts + 4, sl_r, sl_m, s->stream);
+      phase_walk(s, q, false, 0, sl_r, 0, sl_m);
+      q.launches += launch_pack(s->b, s->d_counts + 4, sl_r, sl_m, s->opt.walk.step_cap,
+                                reach_records, minpath_records, s->stream);
+      return q.launches;
+    });
     // No host sync: the records are consumed in stream order (the all-gather
     // is enqueued on the session's stream).
     maybe_sync(s, "shard walk");
@@ -2381,9 +2433,34 @@ Pending shard_commit_pending(dyg_session* s, int world, const void* reach_gather
     p.wall0 = s->shard_wall0;
     p.launches = s->shard_launches;
     s->b.ctl = p.dctl;
-    p.launches += launch_unpack(s->b, s->shard_nq_r, s->shard_nq_m, world, sl_r, sl_m,
-                                s->opt.walk.step_cap, reach_gathered, minpath_gathered, s->stream);
+    s->b.events = const_cast<DevEvent*>(p.dev);
+    s->b.side_top = &p.dctl->side_top;
+    s->b.scratch_edges = &p.dctl->scratch_edges;
+    s->shard_unpack = [=](dyg_session* ss) {
+      return launch_unpack(ss->b, ss->shard_nq_r, ss->shard_nq_m, world, sl_r, sl_m,
+                           ss->opt.walk.step_cap, reach_gathered, minpath_gathered, ss->stream);
+    };
+    const uint64_t shape[] = {static_cast<uint64_t>(world), sl_r, sl_m, s->shard_nq_r, s->shard_nq_m,
+                              reinterpret_cast<uint64_t>(reach_gathered),
+                              reinterpret_cast<uint64_t>(minpath_gathered)};
+    s->shard_unpack_key = fnv(0x9e3779b97f4a7c15ull, shape, sizeof shape);
     return p;
+}
+
+// Unpack + commit of the shard batch as one captured segment (downloading
+// the control block to p.hctl).
+void shard_commit_enqueue(dyg_session* s, Pending& p) {
+  uint64_t key = session_fingerprint(s, 5);
+  const uint64_t shape[] = {s->shard_unpack_key, reinterpret_cast<uint64_t>(p.dev),
+                            reinterpret_cast<uint64_t>(p.dctl), reinterpret_cast<uint64_t>(p.hctl),
+                            reinterpret_cast<uint64_t>(p.hdec), p.nb, p.n_ins, p.n_del};
+  key = fnv(key, shape, sizeof shape);
+  p.launches += enqueue_captured(s, key, p.counter_base, [&] {
+    Pending q = p;
+    q.launches = s->shard_unpack(s);
+    commit_enqueue(s, q, true);
+    return q.launches;
+  });
 }
 }  // namespace
 
@@ -2402,7 +2479,9 @@ int dyg_shard_commit(dyg_session* s, int world, const void* reach_gathered,
       return;
     }
     Pending p = shard_commit_pending(s, world, reach_gathered, minpath_gathered);
-    phase_commit(s, p, out);
+    shard_commit_enqueue(s, p);
+    check(cudaStreamSynchronize(s->stream), "batch");
+    commit_finalize(s, p, out);
   });
 }
 
@@ -2429,7 +2508,7 @@ int dyg_shard_commit_async(dyg_session* s, int world, const void* reach_gathered
     }
     p = shard_commit_pending(s, world, reach_gathered, minpath_gathered);
     p.hctl = s->h_shard_ctls + s->shard_pending.size();
-    commit_enqueue(s, p, true);
+    shard_commit_enqueue(s, p);
     s->shard_pending.push_back(p);
     s->shard_next_counter = p.counter_base + p.nb;
     const uint64_t T1 = static_cast<uint64_t>(s->opt.walk.step_cap) + 1;
