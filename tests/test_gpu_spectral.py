@@ -162,9 +162,10 @@ def test_ordering_reused_for_same_and_nearby_patterns():
     rp, ids, w = (np.asarray(x) for x in h.rows())
     grp, gids, gw = (np.asarray(x) for x in g.rows())
     have = {(u, int(v)) for u in range(len(rp) - 1) for v in ids[rp[u]:rp[u + 1]]}
-    u = next(u for u in range(len(grp) - 1)
-             if any((u, int(v)) not in have for v in gids[grp[u]:grp[u + 1]]))
-    k = next(i for i in range(grp[u], grp[u + 1]) if (u, int(gids[i])) not in have)
+    # (both ends != 0: the grounded pattern drops vertex 0's row and column)
+    u = next(u for u in range(1, len(grp) - 1)
+             if any((u, int(v)) not in have and v != 0 for v in gids[grp[u]:grp[u + 1]]))
+    k = next(i for i in range(grp[u], grp[u + 1]) if (u, int(gids[i])) not in have and gids[i] != 0)
     h.insert_edge(u, int(gids[k]), float(gw[k]))
     e3 = D.condition_number(g, h, o)
     s3 = ordering_cache_stats()
