@@ -3,7 +3,6 @@
 // round scheme.
 #include <cooperative_groups.h>
 
-#include <cub/cub.cuh>
 
 #include <mutex>
 #include <unordered_map>
@@ -1357,7 +1356,7 @@ __global__ void k_flags_del(DevGraph<kCapH> H, DevGraph<kCapG> S,
 // ------------------------------------------------- single-pass batch prepare
 // Validation + query flags + the query scan + the query scatter in ONE
 // launch (decoupled look-back scan over 256-event tiles) for insertion-only
-// and deletion-only batches: the separate k_validate / k_flags_* / cub scan
+// and deletion-only batches: the separate k_validate / k_flags_* / tile scan
 // (2 kernels) / k_scatter chain costs five launches and their gaps per batch.
 // Same results as that chain: a thread checks its own event's shape before
 // touching the graph, and an invalid batch's queries are never committed
@@ -1889,11 +1888,87 @@ int coop_grid_blocks(int device) {
   return sms;
 }
 
+// Query-slot scan of a mixed batch (the packed reach | min-path flags of
+// k_flags_ins / k_flags_del): exclusive sum over 2048-event tiles in three
+// launches -- per-tile totals, one block scanning the totals in place, then
+// every tile scans its own events from its offset. Scratch: one u64 per tile.
+constexpr uint32_t kScanThreads = 256;
+constexpr uint32_t kScanPer = 8;  // events per thread
+constexpr uint32_t kScanTile = kScanThreads * kScanPer;
+
 size_t scan_temp_bytes(uint32_t nb_cap) {
-  size_t temp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<unsigned long long*>(nullptr),
-                                static_cast<unsigned long long*>(nullptr), nb_cap);
-  return temp;
+  return sizeof(unsigned long long) * ((static_cast<size_t>(nb_cap) + kScanTile - 1) / kScanTile + 1);
+}
+
+__device__ __forceinline__ unsigned long long block_exclusive_u64(unsigned long long x,
+                                                                  unsigned long long* total) {
+  __shared__ unsigned long long warp_tot[kScanThreads / 32];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long inc = x;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+    if (lane >= static_cast<uint32_t>(off)) inc += y;
+  }
+  if (lane == 31) warp_tot[w] = inc;
+  __syncthreads();
+  unsigned long long before = 0, all = 0;
+  for (uint32_t i = 0; i < kScanThreads / 32; ++i) {
+    if (i < w) before += warp_tot[i];
+    all += warp_tot[i];
+  }
+  __syncthreads();  // warp_tot is reused by the next call
+  if (total) *total = all;
+  return before + inc - x;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const unsigned long long* __restrict__ in,
+                                                             uint32_t n,
+                                                             unsigned long long* __restrict__ tile_sum) {
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+  unsigned long long x = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < kScanPer; ++j) {
+    const uint64_t i = base + j * kScanThreads + threadIdx.x;  // coalesced
+    if (i < n) x += in[i];
+  }
+  unsigned long long tot = 0;
+  block_exclusive_u64(x, &tot);
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_mid(unsigned long long* __restrict__ tile_sum,
+                                                           uint32_t tiles) {
+  unsigned long long carry = 0;
+  for (uint32_t b0 = 0; b0 < tiles; b0 += kScanThreads) {
+    const uint32_t t = b0 + threadIdx.x;
+    const unsigned long long x = t < tiles ? tile_sum[t] : 0ull;
+    unsigned long long tot = 0;
+    const unsigned long long ex = block_exclusive_u64(x, &tot);
+    if (t < tiles) tile_sum[t] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const unsigned long long* __restrict__ in,
+                                                             uint32_t n,
+                                                             const unsigned long long* __restrict__ tile_sum,
+                                                             unsigned long long* __restrict__ out) {
+  const unsigned long long offset = tile_sum[blockIdx.x];  // exclusive, from k_scan_mid
+  // This thread's kScanPer consecutive events.
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanPer;
+  unsigned long long v[kScanPer], run = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < kScanPer; ++j) {
+    v[j] = base + j < n ? in[base + j] : 0ull;
+    run += v[j];
+  }
+  unsigned long long acc = offset + block_exclusive_u64(run, nullptr);
+#pragma unroll
+  for (uint32_t j = 0; j < kScanPer; ++j) {
+    if (base + j < n) out[base + j] = acc;
+    acc += v[j];
+  }
 }
 
 // Batch control block initialisation on the device (a kernel instead of a
@@ -2047,12 +2122,15 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
     k_flags_del<<<grid_for(nb), 256, 0, st>>>(H, G, b.events, nb, o, b);
     ++l;
   }
-  size_t temp = b.cub_temp_bytes;
-  cuda_check(cub::DeviceScan::ExclusiveSum(b.cub_temp, temp, b.scan_in, b.scan_out, nb, st),
-             "query scan");
+  const uint32_t tiles = (nb + kScanTile - 1) / kScanTile;
+  auto* tile_sum = static_cast<unsigned long long*>(b.scan_temp);
+  k_scan_tiles<<<tiles, kScanThreads, 0, st>>>(b.scan_in, nb, tile_sum);
+  k_scan_mid<<<1, kScanThreads, 0, st>>>(tile_sum, tiles);
+  k_scan_apply<<<tiles, kScanThreads, 0, st>>>(b.scan_in, nb, tile_sum, b.scan_out);
+  cuda_check(cudaGetLastError(), "query scan");
   (void)counter;  // read on the device from the control block (graph replay)
   k_scatter<<<grid_for(nb), 256, 0, st>>>(b.events, nb, o.seed, b);
-  return l + 2;
+  return l + 4;
 }
 
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,

@@ -158,8 +158,8 @@ struct BatchDev {
   ReachQuery* rq_sh;  // multi-GPU split: this rank's query range, moved to the front
   MinQuery* mq_sh;
   uint32_t* save_idx;        // per vertex: index of its saved batch-start G row
-  void* cub_temp;
-  size_t cub_temp_bytes;
+  void* scan_temp;
+  size_t scan_temp_bytes_;
   // Insertion fast path ([0] = G, [1] = H): per-vertex append counts and
   // list heads (zero / kNoSlot between batches), per-record list links.
   uint32_t* fp_cnt[2];

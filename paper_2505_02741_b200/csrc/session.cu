@@ -263,8 +263,8 @@ void free_batch(dyg_session* s) {
   dev_free(b.fl_heavy);
   dev_free(b.fl_wpre);
   dev_free(b.tile_state);
-  cudaFree(b.cub_temp);
-  b.cub_temp = nullptr;
+  cudaFree(b.scan_temp);
+  b.scan_temp = nullptr;
   dev_free(s->d_events);
   if (s->h_events_pinned) cudaFreeHost(s->h_events_pinned);
   s->h_events_pinned = nullptr;
@@ -299,8 +299,8 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&s->d_events, cap, "batch events");
     check(cudaMallocHost(reinterpret_cast<void**>(&s->h_events_pinned), sizeof(DevEvent) * cap),
           "pinned events");
-    b.cub_temp_bytes = scan_temp_bytes(cap);
-    check(cudaMalloc(&b.cub_temp, std::max<size_t>(b.cub_temp_bytes, 16)), "scan temp");
+    b.scan_temp_bytes_ = scan_temp_bytes(cap);
+    check(cudaMalloc(&b.scan_temp, std::max<size_t>(b.scan_temp_bytes_, 16)), "scan temp");
     for (int i = 0; i < 2; ++i) dev_alloc(&b.fp_next[i], 2ull * cap, "append links");
     dev_alloc(&b.fl_base, cap, "flow record ranges");
     dev_alloc(&b.fl_cnt, cap, "flow record ranges");
