@@ -251,8 +251,7 @@ __device__ __forceinline__ bool delete_edge(const DevGraph<C>& g, uint32_t u, ui
 
 // Algorithmic bytes of one walker step at a row of degree d:
 // the header plus d (u32 id, f64 w) pairs, rounded up to 32 B sectors.
-__device__ __forceinline__ uint32_t step_bytes(uint32_t d) {
-  return 32u * ((8u + 12u * d + 31u) / 32u);
-}
+__device__ __forceinline__ uint32_t step_sectors(uint32_t d) { return (8u + 12u * d + 31u) / 32u; }
+__device__ __forceinline__ uint32_t step_bytes(uint32_t d) { return 32u * step_sectors(d); }
 
 }  // namespace dyg
