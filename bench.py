@@ -409,8 +409,13 @@ def run_ours(args):
     nb = stream.batch_count
     batches = [stream.batch(b) for b in range(nb)]
     n_events = int(sum(len(e) for e, _ in batches))
-    sharded = ShardedReplay(st, rank, world) if (world > 1 or force_shard) else None
-    st.upload_stream(stream)  # device-resident events for the device-timed step
+    sharded = (ShardedReplay(st, rank, world, transport=args.transport)
+               if (world > 1 or force_shard) else None)
+    # device-resident events for the device-timed step
+    if sharded is None:
+        st.upload_stream(stream)
+    else:
+        sharded.upload(stream)
 
     def step_device():
         st.restore()
@@ -547,7 +552,8 @@ def run_ours(args):
             "step": (f"restore(G0,H0) + replay of all batches ({kinds['insertion'][2] // args.steps}"
                      f" incremental + {kinds['deletion'][2] // args.steps} decremental)"),
             "K": K_BUDGET, "T": T_CAP, "s": WALKERS, "walk_seed": WALK_SEED,
-            "parallelism": (f"replicated G/H, walks sharded x{world}" if (world > 1 or force_shard)
+            "parallelism": (f"replicated G/H, walks sharded x{world}, {args.transport} exchange"
+                            if (world > 1 or force_shard)
                             else "1 GPU"),
             "l2": (f"inputs larger than L2 (G slabs {g.vertex_count() * 128 / 1e6:.0f} MB + "
                    f"H slabs {g.vertex_count() * 96 / 1e6:.0f} MB > 126 MB)"),
@@ -621,7 +627,10 @@ def main():
                    help="weak: the mesh is widened by the GPU count (cols x N), so the "
                         "events and queries per batch grow with N")
     p.add_argument("--force-shard", action="store_true",
-                   help="one GPU through the multi-GPU (sharded, NCCL) code path")
+                   help="one GPU through the multi-GPU (sharded) code path")
+    p.add_argument("--transport", choices=["peer", "collective"], default="peer",
+                   help="multi-GPU record exchange: device peer memory (CUDA IPC over NVLink, "
+                        "one graph per range) or a torch.distributed all-gather per batch")
     args = p.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

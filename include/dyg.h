@@ -430,6 +430,34 @@ int dyg_shard_commit_async(dyg_session* s, int world, const void* reach_gathered
                            const void* minpath_gathered);
 int dyg_shard_finish(dyg_session* s, dyg_batch_report* out, size_t cap, size_t* n_out);
 
+/* Peer-memory exchange for the split (the B200 path; NCCL not involved):
+ * every rank packs its walk records into its OWN exchange area and
+ * publishes them with a system-scope release of a per-batch epoch; every
+ * rank then reads each peer's records straight from the peer's area (P2P
+ * loads over NVLink through CUDA IPC mappings) once that peer's epoch has
+ * arrived. A batch's prepare, walk, pack, publish, wait, unpack and commit
+ * are all kernels, so a range of uploaded batches is one captured graph
+ * with no host step between them.
+ *   dyg_shard_peer_create: (re)allocates this rank's area for batches of up
+ *     to max_reach insertions / max_minpath deletions split `world` ways;
+ *     returns the area, its size and (ipc_handle non-null) its 64-byte CUDA
+ *     IPC handle for the other ranks.
+ *   dyg_ipc_open / dyg_ipc_close: map / unmap a peer's area on `device`.
+ *   dyg_shard_peer_bind: areas[q] = rank q's area as this device sees it
+ *     (areas[rank] = the own area). A peer that does not publish within
+ *     timeout_s seconds (<= 0: 30 s) fails the batch with DYG_ERR_DEVICE.
+ *   dyg_shard_peer_range_begin / _end: enqueue the uploaded batches
+ *     [first, first + count) (dyg_stream_upload*) / synchronise and report
+ *     them (the first failing batch's error, as dyg_replay_uploaded_range).
+ * Every rank must run the same ranges in the same order. */
+int dyg_shard_peer_create(dyg_session* s, int world, uint64_t max_reach, uint64_t max_minpath,
+                          void** area, size_t* bytes, void* ipc_handle);
+int dyg_ipc_open(const void* ipc_handle, int device, void** ptr);
+int dyg_ipc_close(void* ptr);
+int dyg_shard_peer_bind(dyg_session* s, int rank, int world, void* const* areas, double timeout_s);
+int dyg_shard_peer_range_begin(dyg_session* s, uint32_t first, uint32_t count);
+int dyg_shard_peer_range_end(dyg_session* s, dyg_batch_report* out, size_t cap, size_t* n_out);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -125,6 +125,12 @@ def lib() -> C.CDLL:
         "dyg_session_snapshot": (i32, [vp]),
         "dyg_session_restore": (i32, [vp]),
         "dyg_session_save": (i32, [vp, C.c_char_p]),
+        "dyg_shard_peer_create": (i32, [vp, i32, u64, u64, pvp, C.POINTER(sz), vp]),
+        "dyg_ipc_open": (i32, [vp, i32, pvp]),
+        "dyg_ipc_close": (i32, [vp]),
+        "dyg_shard_peer_bind": (i32, [vp, i32, i32, vp, dbl]),
+        "dyg_shard_peer_range_begin": (i32, [vp, u32, u32]),
+        "dyg_shard_peer_range_end": (i32, [vp, vp, sz, C.POINTER(sz)]),
         "dyg_spectral_ordering_stats": (i32, [C.POINTER(C.c_uint64)] * 3),
         "dyg_session_load": (i32, [C.c_char_p, i32, pvp]),
         "dyg_session_options": (i32, [vp, C.POINTER(Options)]),

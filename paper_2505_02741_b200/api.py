@@ -340,6 +340,18 @@ def _dec_ptr(decisions):
     return ptr(decisions)
 
 
+def ipc_open(handle: bytes, device: int) -> int:
+    """Map a peer rank's exchange area (its 64-byte CUDA IPC handle)."""
+    p = C.c_void_p()
+    buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+    _check(_lib.lib().dyg_ipc_open(buf, device, C.byref(p)))
+    return p.value
+
+
+def ipc_close(p: int) -> None:
+    _check(_lib.lib().dyg_ipc_close(C.c_void_p(p)))
+
+
 class SparsifierState:
     """sparsifier.hpp:71-112 with G and H device-resident on `device`."""
 
@@ -561,6 +573,28 @@ class SparsifierState:
     def shard_commit_async(self, world, reach_ptr, min_ptr) -> None:
         _check(_lib.lib().dyg_shard_commit_async(self._s, world, C.c_void_p(reach_ptr),
                                                  C.c_void_p(min_ptr)))
+
+    # -- peer-memory exchange (dyg_shard_peer_*) ----------------------------
+    def shard_peer_create(self, world: int, max_reach: int, max_minpath: int):
+        """(area pointer, bytes, 64-byte IPC handle) of this rank's exchange area."""
+        area, nbytes = C.c_void_p(), C.c_size_t()
+        handle = (C.c_uint8 * 64)()
+        _check(_lib.lib().dyg_shard_peer_create(self._s, world, max_reach, max_minpath,
+                                                C.byref(area), C.byref(nbytes), handle))
+        return area.value, nbytes.value, bytes(handle)
+
+    def shard_peer_bind(self, rank: int, world: int, areas, timeout_s: float = 30.0) -> None:
+        arr = (C.c_void_p * world)(*areas)
+        _check(_lib.lib().dyg_shard_peer_bind(self._s, rank, world, arr, timeout_s))
+
+    def shard_peer_range_begin(self, first: int, count: int) -> None:
+        _check(_lib.lib().dyg_shard_peer_range_begin(self._s, first, count))
+
+    def shard_peer_range_end(self, count: int):
+        rep = np.zeros(max(count, 1), REPORT_DTYPE)
+        n = C.c_size_t()
+        _check(_lib.lib().dyg_shard_peer_range_end(self._s, ptr(rep), count, C.byref(n)))
+        return [BatchReport.from_record(rep[i]) for i in range(n.value)]
 
     def shard_finish(self, max_reports: int = 256):
         """Reports of the pending asynchronous shard commits, in order."""

@@ -1837,6 +1837,125 @@ __global__ void k_unpack_min(MinOut m, const uint32_t* nq_dev, int world, uint32
   for (uint32_t j = threadIdx.x; j < h->path_len; j += blockDim.x) dst[j] = path[j];
 }
 
+// ---- peer-memory exchange (batch.cuh) -------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint8_t* peer_next_buffer(const PeerX& px) {
+  return px.own + kPeerHeader + ((*px.ep + 1ull) & 1ull) * px.stride;
+}
+
+__global__ void k_pack_reach_peer(ReachOut r, const uint32_t* n_dev, uint32_t slots, PeerX px) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= slots) return;
+  ReachRecord* rec = reinterpret_cast<ReachRecord*>(peer_next_buffer(px));
+  const uint32_t n = *n_dev;
+  ReachRecord x{0, 0, 0ull};
+  if (i < n) {
+    x.reached = r.reached[i];
+    x.steps = r.steps[i];
+  }
+  rec[i] = x;
+}
+
+__global__ void k_pack_min_peer(MinOut m, const uint32_t* n_dev, uint32_t slots, uint32_t T,
+                                PeerX px) {
+  const uint32_t i = blockIdx.x;
+  if (i >= slots) return;
+  const size_t rec_bytes = min_record_bytes(T);
+  uint8_t* base = peer_next_buffer(px) + px.min_off + static_cast<size_t>(i) * rec_bytes;
+  const uint32_t n = *n_dev;
+  MinRecordHead* h = reinterpret_cast<MinRecordHead*>(base);
+  uint32_t* path = reinterpret_cast<uint32_t*>(base + sizeof(MinRecordHead));
+  const bool have = i < n;
+  const uint32_t len = have ? m.path_len[i] : 0;
+  if (threadIdx.x == 0) {
+    h->has_path = have ? m.has_path[i] : 0;
+    h->path_len = len;
+    h->steps = have ? m.steps[i] : 0ull;
+    h->resistance = have ? m.resistance[i] : 0.0;
+  }
+  const uint32_t* src = m.paths + static_cast<uint64_t>(i) * (T + 1ull);
+  for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) path[j] = src[j];
+}
+
+// Publish this rank's records of the batch: epoch += 1, then the release
+// store peers acquire. (Stream order: the pack kernels have completed, their
+// writes sit in this GPU's L2, where peers' P2P loads are served.) A range
+// whose earlier batch failed (abort flag, raised identically on every rank)
+// exchanges nothing, on every rank alike.
+__global__ void k_peer_signal(PeerX px, const unsigned int* abort_flag) {
+  if (*abort_flag) return;
+  __threadfence_system();
+  const unsigned long long e = *px.ep + 1ull;
+  *px.ep = e;
+  st_release_sys(reinterpret_cast<unsigned long long*>(px.own), e);
+}
+
+// Wait until every rank has published this batch's epoch. A peer that does
+// not publish within px.timeout_ns fails the batch (validation slot, code
+// kErrPeer) and raises the abort flag: the host then reports a device error
+// instead of hanging.
+__global__ void k_peer_wait(PeerX px, unsigned int* abort_flag, BatchCtl* ctl) {
+  if (*abort_flag) return;
+  const unsigned long long e = *px.ep;
+  const unsigned long long t0 = global_ns();
+  for (int q = 0; q < px.world; ++q) {
+    const unsigned long long* f = reinterpret_cast<const unsigned long long*>(px.base[q]);
+    while (ld_acquire_sys(f) < e) {
+      if (global_ns() - t0 > px.timeout_ns) {
+        atomicMin(&ctl->val_err, static_cast<unsigned long long>(kErrPeer));
+        atomicExch(abort_flag, 1u);
+        return;
+      }
+      __nanosleep(200);
+    }
+  }
+}
+
+__device__ __forceinline__ const uint8_t* peer_cur_buffer(const PeerX& px, uint32_t rank) {
+  return px.base[rank] + kPeerHeader + (*px.ep & 1ull) * px.stride;
+}
+
+__global__ void k_unpack_reach_peer(ReachOut r, const uint32_t* nq_dev, uint32_t slots, PeerX px) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nq = *nq_dev;
+  if (q >= nq) return;
+  uint32_t rank, idx;
+  locate(q, nq, px.world, &rank, &idx);
+  const ReachRecord x =
+      reinterpret_cast<const ReachRecord*>(peer_cur_buffer(px, rank))[idx];
+  r.reached[q] = x.reached;
+  r.steps[q] = x.steps;
+}
+
+__global__ void k_unpack_min_peer(MinOut m, const uint32_t* nq_dev, uint32_t T, PeerX px) {
+  const uint32_t q = blockIdx.x;
+  const uint32_t nq = *nq_dev;
+  if (q >= nq) return;
+  uint32_t rank, idx;
+  locate(q, nq, px.world, &rank, &idx);
+  const uint8_t* base =
+      peer_cur_buffer(px, rank) + px.min_off + static_cast<size_t>(idx) * min_record_bytes(T);
+  const MinRecordHead* h = reinterpret_cast<const MinRecordHead*>(base);
+  const uint32_t* path = reinterpret_cast<const uint32_t*>(base + sizeof(MinRecordHead));
+  const uint32_t len = h->path_len;
+  if (threadIdx.x == 0) {
+    m.has_path[q] = h->has_path;
+    m.path_len[q] = len;
+    m.steps[q] = h->steps;
+    m.resistance[q] = h->resistance;
+  }
+  uint32_t* dst = m.paths + static_cast<uint64_t>(q) * (T + 1ull);
+  for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) dst[j] = path[j];
+}
+
 // Co-resident grid for a cooperative kernel, cached per kernel (not per
 // kernel type: several cooperative kernels share a signature).
 template <typename K>
@@ -2210,6 +2329,45 @@ int launch_pack(const BatchDev& b, const uint32_t* rng, uint32_t slots_r, uint32
   if (slots_m) {
     k_pack_min<<<slots_m, 128, 0, st>>>(b.mout, rng + 3, slots_m, T, static_cast<uint8_t*>(mrec),
                                         min_record_bytes(T));
+    ++l;
+  }
+  return l;
+}
+
+size_t peer_area_bytes(uint32_t slots_r, uint32_t slots_m, uint32_t T, size_t* stride,
+                       size_t* min_off) {
+  const size_t r = (sizeof(ReachRecord) * static_cast<size_t>(slots_r) + 255) & ~size_t(255);
+  const size_t m = (min_record_bytes(T) * static_cast<size_t>(slots_m) + 255) & ~size_t(255);
+  *min_off = r;
+  *stride = r + m;
+  return kPeerHeader + 2 * (r + m);
+}
+
+int launch_pack_peer(const BatchDev& b, const uint32_t* rng, uint32_t slots_r, uint32_t slots_m,
+                     uint32_t T, const PeerX& px, cudaStream_t st) {
+  int l = 0;
+  if (slots_r) {
+    k_pack_reach_peer<<<grid_for(slots_r), 256, 0, st>>>(b.rout, rng + 1, slots_r, px);
+    ++l;
+  }
+  if (slots_m) {
+    k_pack_min_peer<<<slots_m, 128, 0, st>>>(b.mout, rng + 3, slots_m, T, px);
+    ++l;
+  }
+  k_peer_signal<<<1, 1, 0, st>>>(px, b.abort_flag);
+  return l + 1;
+}
+
+int launch_unpack_peer(const BatchDev& b, uint32_t max_r, uint32_t max_m, uint32_t slots_r,
+                       uint32_t slots_m, uint32_t T, const PeerX& px, cudaStream_t st) {
+  k_peer_wait<<<1, 1, 0, st>>>(px, b.abort_flag, b.ctl);
+  int l = 1;
+  if (max_r && slots_r) {
+    k_unpack_reach_peer<<<grid_for(max_r), 256, 0, st>>>(b.rout, &b.ctl->nq_reach, slots_r, px);
+    ++l;
+  }
+  if (max_m && slots_m) {
+    k_unpack_min_peer<<<max_m, 128, 0, st>>>(b.mout, &b.ctl->nq_min, T, px);
     ++l;
   }
   return l;

@@ -48,6 +48,7 @@ enum EventError : uint32_t {
   kErrAbsent = 4,      // delete_edge: "edge (u, v) does not exist"
   kErrPool = 5,        // overflow pool exhausted (device)
   kErrAborted = 6,     // an earlier batch of the same enqueued range failed
+  kErrPeer = 7,        // a peer never published its walk records (multi-GPU exchange)
 };
 
 struct BatchCtl {
@@ -237,7 +238,7 @@ struct MinRecordHead {
   unsigned long long steps;
   double resistance;
 };
-inline size_t min_record_bytes(uint32_t T) {
+__host__ __device__ inline size_t min_record_bytes(uint32_t T) {
   return (sizeof(MinRecordHead) + 4ull * (T + 1ull) + 7ull) & ~7ull;
 }
 // Pack this rank's queries [lo, hi) into `slots` records (rest zeroed).
@@ -249,5 +250,40 @@ int launch_unpack(const BatchDev& b, uint32_t max_r, uint32_t max_m, int world, 
                   cudaStream_t st);
 // Co-resident blocks for the cooperative round kernels.
 int coop_grid_blocks(int device);
+
+// ---- peer-memory exchange of the multi-GPU split ----------
+// Instead of an NCCL all-gather between two host calls, every rank packs its
+// walk records into its OWN exchange area, publishes them with a
+// system-scope release of its `ready` epoch, and reads every peer's records
+// straight from the peer's area (P2P loads over NVLink, CUDA IPC mappings)
+// once that peer's `ready` reaches the batch's epoch. All of it is kernels,
+// so a whole sharded batch -- prepare, walk, pack, signal, wait, unpack,
+// commit -- is one captured graph with no host step in between.
+// Area layout: [0, 256) the ready epoch (u64 at 0); then two parity
+// buffers of `stride` bytes (reach records, then min-path records at
+// min_off). Batch epoch e uses parity e & 1; a rank writes parity buffer
+// e & 1 again only at epoch e + 2, after it has seen every peer's ready
+// reach e + 1, and a peer publishes e + 1 only after its unpack of e
+// finished (stream order): two buffers suffice.
+constexpr int kMaxPeers = 16;
+constexpr size_t kPeerHeader = 256;
+struct PeerX {
+  uint8_t* own;                    // this rank's area (device memory)
+  const uint8_t* base[kMaxPeers];  // every rank's area as this device sees it
+  unsigned long long* ep;          // this rank's epoch (local device counter)
+  unsigned long long stride;       // bytes per parity buffer
+  unsigned long long min_off;      // min-path records within a parity buffer
+  int world;
+  int rank;
+  unsigned long long timeout_ns;   // a peer that never publishes fails the batch
+};
+size_t peer_area_bytes(uint32_t slots_r, uint32_t slots_m, uint32_t T, size_t* stride,
+                       size_t* min_off);
+// Pack into the own area's next parity buffer, then publish (signal).
+int launch_pack_peer(const BatchDev& b, const uint32_t* rng, uint32_t slots_r, uint32_t slots_m,
+                     uint32_t T, const PeerX& px, cudaStream_t st);
+// Wait for every peer's epoch, then unpack from the peers' areas.
+int launch_unpack_peer(const BatchDev& b, uint32_t max_r, uint32_t max_m, uint32_t slots_r,
+                       uint32_t slots_m, uint32_t T, const PeerX& px, cudaStream_t st);
 
 }  // namespace dyg

@@ -169,6 +169,17 @@ struct dyg_session {
   // everything it bakes into kernel arguments.
   std::function<int(dyg_session*)> shard_unpack;
   uint64_t shard_unpack_key = 0;
+  // Peer-memory exchange (dyg_shard_peer_*, batch.cuh PeerX): this rank's
+  // exchange area and epoch, the bound view of every rank's area, and the
+  // batches of an enqueued peer range awaiting dyg_shard_peer_range_end.
+  uint8_t* px_area = nullptr;
+  size_t px_bytes = 0, px_stride = 0, px_min_off = 0;
+  uint32_t px_slots_r = 0, px_slots_m = 0, px_world = 0;
+  unsigned long long* px_ep = nullptr;
+  PeerX px{};
+  bool px_bound = false;
+  std::vector<Pending> px_pending;
+  uint32_t px_first = 0;
 
   dyg_stats stats{};
   BatchCtl* d_ctls = nullptr;      // batch-range control blocks
@@ -645,6 +656,9 @@ void commit_finalize(dyg_session* s, Pending& p, dyg_batch_report* out) {
   s->stats.d2h_bytes += sizeof c;
   s->stats.kernel_launches += p.launches;
   s->stats.batches += 1;
+  if (c.val_err != ~0ull && (c.val_err & 0xFF) == kErrPeer)
+    fail(DYG_ERR_DEVICE, "multi-GPU peer exchange timed out: a rank did not publish its walk "
+                         "records (batch " + std::to_string(p.batch) + ")");
   if (c.val_err != ~0ull) fail_validation(s, p, c.val_err);
   // Commit-side state is now final for events < limit.
   s->g_edges = c.g_edges;
@@ -1667,6 +1681,8 @@ void dyg_session_destroy(dyg_session* s) {
   if (s->h_shard_ctls) cudaFreeHost(s->h_shard_ctls);
   dev_free(s->d_abort);
   dev_free(s->d_up_kinds);
+  dev_free(s->px_area);
+  dev_free(s->px_ep);
   if (s->h_up_kinds) cudaFreeHost(s->h_up_kinds);
   for (cudaEvent_t e : s->up_ready) cudaEventDestroy(e);
   if (s->ev_up_fence) cudaEventDestroy(s->ev_up_fence);
@@ -1685,6 +1701,8 @@ void dyg_session_destroy(dyg_session* s) {
 static void require_settled(const dyg_session* s) {
   if (s != nullptr && !s->shard_pending.empty())
     fail(DYG_ERR_USAGE, "asynchronous shard commits pending: call dyg_shard_finish first");
+  if (s != nullptr && !s->px_pending.empty())
+    fail(DYG_ERR_USAGE, "a peer-exchange range is pending: call dyg_shard_peer_range_end first");
 }
 
 int dyg_replay_events(dyg_session* s, const dyg_event* events, const uint64_t* positions,
@@ -2534,6 +2552,235 @@ int dyg_shard_finish(dyg_session* s, dyg_batch_report* out, size_t cap, size_t* 
       if (out && i < cap) out[i] = rep;
       if (n_out) *n_out = i + 1;
     }
+  });
+}
+
+// ---- peer-memory exchange of the multi-GPU split (batch.cuh PeerX) --------
+int dyg_shard_peer_create(dyg_session* s, int world, uint64_t max_reach, uint64_t max_minpath,
+                          void** area, size_t* bytes, void* ipc_handle) {
+  return guarded([&] {
+    require_settled(s);
+    if (s == nullptr || area == nullptr || bytes == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    if (world < 1 || world > kMaxPeers)
+      fail(DYG_ERR_USAGE, "peer exchange supports 1.." + std::to_string(kMaxPeers) + " ranks");
+    if (!s->opt.batched) fail(DYG_ERR_USAGE, "the multi-GPU split needs batched (deferred) mode");
+    check(cudaSetDevice(s->device), "set device");
+    check(cudaStreamSynchronize(s->stream), "peer exchange");
+    dev_free(s->px_area);
+    if (s->px_ep == nullptr) dev_alloc(&s->px_ep, 1, "peer epoch");
+    s->px_slots_r = static_cast<uint32_t>((max_reach + world - 1) / world);
+    s->px_slots_m = static_cast<uint32_t>((max_minpath + world - 1) / world);
+    s->px_world = static_cast<uint32_t>(world);
+    s->px_bytes = peer_area_bytes(s->px_slots_r, s->px_slots_m, s->opt.walk.step_cap, &s->px_stride,
+                                  &s->px_min_off);
+    check(cudaMalloc(reinterpret_cast<void**>(&s->px_area), s->px_bytes), "peer exchange area");
+    check(cudaMemset(s->px_area, 0, s->px_bytes), "peer exchange area");
+    check(cudaMemset(s->px_ep, 0, sizeof(unsigned long long)), "peer epoch");
+    s->px_bound = false;
+    *area = s->px_area;
+    *bytes = s->px_bytes;
+    if (ipc_handle != nullptr) {
+      cudaIpcMemHandle_t h;
+      check(cudaIpcGetMemHandle(&h, s->px_area), "IPC handle of the exchange area");
+      std::memcpy(ipc_handle, &h, sizeof h);
+    }
+  });
+}
+
+int dyg_ipc_open(const void* ipc_handle, int device, void** ptr) {
+  return guarded([&] {
+    if (ipc_handle == nullptr || ptr == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    check(cudaSetDevice(device), "set device");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof h);
+    check(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "IPC open");
+  });
+}
+
+int dyg_ipc_close(void* ptr) {
+  return guarded([&] {
+    if (ptr != nullptr) check(cudaIpcCloseMemHandle(ptr), "IPC close");
+  });
+}
+
+int dyg_shard_peer_bind(dyg_session* s, int rank, int world, void* const* areas, double timeout_s) {
+  return guarded([&] {
+    require_settled(s);
+    if (s == nullptr || areas == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    if (s->px_area == nullptr) fail(DYG_ERR_USAGE, "no exchange area: call dyg_shard_peer_create");
+    if (static_cast<uint32_t>(world) != s->px_world || rank < 0 || rank >= world)
+      fail(DYG_ERR_USAGE, "invalid rank / world");
+    if (areas[rank] != s->px_area) fail(DYG_ERR_USAGE, "areas[rank] must be this rank's own area");
+    PeerX px{};
+    px.own = s->px_area;
+    for (int q = 0; q < world; ++q) {
+      if (areas[q] == nullptr) fail(DYG_ERR_USAGE, "null peer area");
+      px.base[q] = static_cast<const uint8_t*>(areas[q]);
+    }
+    px.ep = s->px_ep;
+    px.stride = s->px_stride;
+    px.min_off = s->px_min_off;
+    px.world = world;
+    px.rank = rank;
+    px.timeout_ns = static_cast<unsigned long long>((timeout_s > 0 ? timeout_s : 30.0) * 1e9);
+    s->px = px;
+    s->px_bound = true;
+  });
+}
+
+namespace {
+// The uploaded batches [first, first + count) through the peer exchange:
+// every batch is prepare -> walk of this rank's query range -> pack into
+// the own area + publish -> wait for the peers -> unpack from their areas
+// -> commit, all enqueued (one captured graph for the range) with no host
+// step; dyg_shard_peer_range_end synchronises and reports.
+void peer_range_begin(dyg_session* s, uint32_t first, uint32_t count) {
+  const uint32_t world = s->px_world;
+  const int rank = s->px.rank;
+  uint64_t sum_ins = 0, sum_del = 0;
+  uint32_t max_nb = 0, max_nd = 0;
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t b = first + i;
+    if (b >= s->batch_cnt.size()) continue;
+    sum_ins += s->batch_ins[b];
+    sum_del += s->batch_del[b];
+    max_nb = std::max<uint32_t>(max_nb, static_cast<uint32_t>(s->batch_cnt[b]));
+    max_nd = std::max<uint32_t>(max_nd, static_cast<uint32_t>(s->batch_del[b]));
+    if ((s->batch_ins[b] + world - 1) / world > s->px_slots_r ||
+        (s->batch_del[b] + world - 1) / world > s->px_slots_m)
+      fail(DYG_ERR_USAGE, "batch " + std::to_string(b) +
+                              " exceeds the exchange area (dyg_shard_peer_create maxima)");
+  }
+  ensure_batch(s, std::max<uint32_t>(max_nb, 1), max_nd);
+  ensure_pools(s, sum_ins, sum_del);
+  if (sum_del > 0) ensure_side_pool(s);
+  if (s->ctl_cap < count) {
+    dev_free(s->d_ctls);
+    if (s->h_ctls) cudaFreeHost(s->h_ctls);
+    s->h_ctls = nullptr;
+    dev_alloc(&s->d_ctls, count, "batch control blocks");
+    check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctls), sizeof(BatchCtl) * count),
+          "pinned control blocks");
+    s->ctl_cap = count;
+  }
+  std::vector<Pending> ps(count);
+  const uint64_t counter0 = s->counter;
+  const auto wall0 = std::chrono::steady_clock::now();
+  reset_abort(s);
+  uint64_t counter = counter0;
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t b = first + i;
+    Pending& p = ps[i];
+    p.batch = b;
+    p.wall0 = wall0;
+    p.dctl = s->d_ctls + i;
+    p.hctl = s->h_ctls + i;
+    p.hdec = &s->h_counts[2];
+    p.counter_base = counter;
+    p.shard = true;
+    if (b >= s->batch_cnt.size() || s->batch_cnt[b] == 0) continue;
+    const uint64_t off = s->batch_off[b];
+    p.dev = s->d_stream + off;
+    p.host = uploaded_host(s, off);
+    p.pos = uploaded_pos(s, off);
+    p.pos_base = off;
+    p.nb = static_cast<uint32_t>(s->batch_cnt[b]);
+    p.n_ins = static_cast<uint32_t>(s->batch_ins[b]);
+    p.n_del = static_cast<uint32_t>(s->batch_del[b]);
+    counter += p.nb;
+  }
+  const uint32_t T = s->opt.walk.step_cap;
+  auto enqueue = [&] {
+    int launches = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+      Pending p = ps[i];
+      if (p.nb == 0) continue;
+      const uint32_t sl_r = (p.n_ins + world - 1) / world, sl_m = (p.n_del + world - 1) / world;
+      phase_prepare(s, p);
+      p.launches += launch_shard_range(s->b, rank, static_cast<int>(world), s->d_counts + 4, sl_r,
+                                       sl_m, s->stream);
+      phase_walk(s, p, false, 0, sl_r, 0, sl_m);
+      p.launches += launch_pack_peer(s->b, s->d_counts + 4, sl_r, sl_m, T, s->px, s->stream);
+      p.launches += launch_unpack_peer(s->b, p.n_ins, p.n_del, sl_r, sl_m, T, s->px, s->stream);
+      commit_enqueue(s, p, false);
+      ps[i].launches = p.launches;
+      launches += p.launches;
+    }
+    check(cudaMemcpyAsync(s->h_ctls, s->d_ctls, sizeof(BatchCtl) * count, cudaMemcpyDeviceToHost,
+                          s->stream), "ctl download");
+    return launches;
+  };
+  CapturedGraph* g = nullptr;
+  if (graphs_usable(s)) {
+    uint64_t key = session_fingerprint(s, 6);
+    const uint64_t shape[] = {first, count, s->stream_gen, reinterpret_cast<uint64_t>(s->d_stream),
+                              reinterpret_cast<uint64_t>(s->d_ctls),
+                              reinterpret_cast<uint64_t>(s->h_ctls), world,
+                              static_cast<uint64_t>(rank)};
+    key = fnv(key, shape, sizeof shape);
+    key = fnv(key, &s->px, sizeof s->px);
+    g = find_graph(s, key);
+    if (g == nullptr) g = capture_graph(s, key, counter0, enqueue);
+    else
+      for (uint32_t i = 0; i < count; ++i) ps[i].launches = g->per_batch[i];
+    if (g != nullptr) {
+      if (g->per_batch.empty())
+        for (uint32_t i = 0; i < count; ++i) g->per_batch.push_back(ps[i].launches);
+      launch_graph(s, *g, counter0);
+    }
+  }
+  if (g == nullptr) enqueue();
+  s->px_pending = std::move(ps);
+  s->px_first = first;
+}
+
+void peer_range_end(dyg_session* s, dyg_batch_report* out) {
+  std::vector<Pending> ps;
+  ps.swap(s->px_pending);
+  check(cudaStreamSynchronize(s->stream), "peer range");
+  for (size_t i = 0; i < ps.size(); ++i) {
+    if (ps[i].nb == 0) {
+      empty_report(s, ps[i].batch, &out[i]);
+      continue;
+    }
+    commit_finalize(s, ps[i], &out[i]);  // throws at the first failing batch
+  }
+}
+}  // namespace
+
+int dyg_shard_peer_range_begin(dyg_session* s, uint32_t first, uint32_t count) {
+  return guarded([&] {
+    require_settled(s);
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    if (!s->px_bound) fail(DYG_ERR_USAGE, "no peer exchange bound: call dyg_shard_peer_bind");
+    if (!s->have_stream) fail(DYG_ERR_USAGE, "no stream uploaded");
+    if (count && static_cast<uint64_t>(first) + count > s->stream_batches && s->stream_batches > 0)
+      fail(DYG_ERR_USAGE, "batch index out of range");
+    check(cudaSetDevice(s->device), "set device");
+    settle_upload(s, ~0u);
+    peer_range_begin(s, first, count);
+  });
+}
+
+int dyg_shard_peer_range_end(dyg_session* s, dyg_batch_report* out, size_t cap, size_t* n_out) {
+  return guarded([&] {
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    if (n_out) *n_out = 0;
+    if (s->px_pending.empty()) return;
+    if (out == nullptr || cap < s->px_pending.size()) {
+      // still drain the range (the device work is enqueued)
+      std::vector<dyg_batch_report> tmp(s->px_pending.size());
+      const size_t n = tmp.size();
+      check(cudaSetDevice(s->device), "set device");
+      peer_range_end(s, tmp.data());
+      if (out) std::memcpy(out, tmp.data(), sizeof(dyg_batch_report) * std::min(cap, n));
+      if (n_out) *n_out = n;
+      return;
+    }
+    const size_t n = s->px_pending.size();
+    check(cudaSetDevice(s->device), "set device");
+    peer_range_end(s, out);
+    if (n_out) *n_out = n;
   });
 }
 

@@ -9,14 +9,23 @@ device). For each batch:
      [floor(nq*r/P), floor(nq*(r+1)/P)) and packs one fixed-size record per
      query slot (dyg_shard_walk; reach: 16 B {reached, steps}; min-path:
      24 B header + (T+1) path vertices);
-  3. the records are all-gathered over NCCL (NVLink) -- the batch's single
-     real exchange step;
+  3. the records are exchanged -- the batch's single real exchange step;
   4. every rank applies the identical deterministic commit
      (dyg_shard_commit), so the replicas stay bit-identical.
 
-torch.distributed is plumbing only (process group, the all-gather); the walk
-and commit run in libdyg.so. The exchange helpers take any
-torch.distributed backend, so the protocol is covered on CPU with gloo.
+Two transports for step 3:
+  * "peer" (default for uploaded ranges): each rank's records stay in its
+    own device exchange area; the ranks map each other's areas once (CUDA
+    IPC, handles swapped over torch.distributed) and every rank's kernels
+    read the peers' records over NVLink after a per-batch epoch handshake in
+    device memory (dyg_shard_peer_*). A whole range of batches is then one
+    captured graph per rank with no host step and no collective call.
+  * "collective": an all-gather per batch through torch.distributed (NCCL
+    on NVLink; gloo stages through host memory), between the library's
+    walk and commit calls.
+
+torch.distributed is plumbing only (process group, handle exchange, the
+collective transport); the walk, exchange and commit run in libdyg.so.
 """
 from __future__ import annotations
 
@@ -68,7 +77,8 @@ class ShardedReplay:
     """Drives a SparsifierState replica on this rank's GPU through the
     sharded protocol. `state` must live on torch.cuda.current_device()."""
 
-    def __init__(self, state, rank: int, world: int, group=None):
+    def __init__(self, state, rank: int, world: int, group=None, transport: str = "peer",
+                 peer_timeout_s: float = 30.0):
         import torch
 
         self.state, self.rank, self.world, self.group = state, rank, world, group
@@ -81,6 +91,13 @@ class ShardedReplay:
         import torch.distributed as dist
 
         self._nccl = dist.get_backend(group) == "nccl"
+        if transport not in ("peer", "collective"):
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
+        self.peer_timeout_s = peer_timeout_s
+        self._peer_key = None      # (max_reach, max_minpath) the areas were sized for
+        self._peer_mapped = []     # IPC mappings of the other ranks' areas
+        self._kind_counts = None   # per-batch insertions / deletions of the uploaded stream
         self._bufs = {}  # reused record buffers (grown on demand)
 
     def _buf(self, key, nbytes):
@@ -133,14 +150,71 @@ class ShardedReplay:
         nr, nm = self.state.shard_begin(events, positions, batch_index)
         return self._exchange(nr, nm)
 
+    def upload(self, stream):
+        """dyg_stream_upload of `stream` plus its per-batch kind counts (the
+        peer areas are sized from them)."""
+        self.state.upload_stream(stream)
+        ev = stream.events
+        k = np.asarray(ev["kind"])
+        bi = np.asarray(ev["batch_index"]).astype(np.int64)
+        nb = stream.batch_count
+        self._kind_counts = (np.bincount(bi[k == 0], minlength=nb)[:nb],
+                             np.bincount(bi[k != 0], minlength=nb)[:nb])
+
     def replay_uploaded(self, batch_index: int):
         """Batch `batch_index` of the stream given to state.upload_stream."""
         nr, nm = self.state.shard_begin_uploaded(batch_index)
         return self._exchange(nr, nm)
 
+    def _peer_setup(self, max_reach: int, max_minpath: int):
+        """Size, publish and map the exchange areas (collective over the
+        group: every rank calls it with the same maxima)."""
+        import torch
+        import torch.distributed as dist
+
+        from .api import ipc_close, ipc_open
+
+        key = (max_reach, max_minpath)
+        if self._peer_key is not None and key[0] <= self._peer_key[0] and key[1] <= self._peer_key[1]:
+            return
+        for p in self._peer_mapped:
+            ipc_close(p)
+        self._peer_mapped = []
+        area, _, handle = self.state.shard_peer_create(self.world, max_reach, max_minpath)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle, group=self.group)
+        dev = torch.cuda.current_device()
+        areas = []
+        for q, h in enumerate(handles):
+            if q == self.rank:
+                areas.append(area)
+            else:
+                p = ipc_open(h, dev)
+                self._peer_mapped.append(p)
+                areas.append(p)
+        self.state.shard_peer_bind(self.rank, self.world, areas, self.peer_timeout_s)
+        self._peer_key = key
+
+    def close(self):
+        from .api import ipc_close
+
+        for p in self._peer_mapped:
+            ipc_close(p)
+        self._peer_mapped = []
+
     def replay_uploaded_range(self, first: int, count: int):
         """Batches [first, first + count) of the uploaded stream with no host
-        round trip between them (asynchronous commits); their reports."""
+        round trip between them; their reports. Peer transport: one library
+        call per rank (the range is a captured graph); collective transport:
+        asynchronous commits with a collective per batch."""
+        if self.transport == "peer":
+            if self._kind_counts is None:
+                raise RuntimeError("upload the stream with ShardedReplay.upload(stream) first")
+            ins, dele = self._kind_counts
+            self._peer_setup(int(ins[first:first + count].max(initial=0)),
+                             int(dele[first:first + count].max(initial=0)))
+            self.state.shard_peer_range_begin(first, count)
+            return self.state.shard_peer_range_end(count)
         reports = []
         for i, b in enumerate(range(first, first + count)):
             nr, nm = self.state.shard_begin_uploaded(b)
@@ -154,5 +228,5 @@ class ShardedReplay:
         the events are uploaded once (dyg_stream_upload), then the batches
         chain on the device with asynchronous commits and one host
         synchronisation (replay_uploaded_range); the reports."""
-        self.state.upload_stream(stream)
+        self.upload(stream)
         return self.replay_uploaded_range(0, stream.batch_count)

@@ -4,7 +4,10 @@ ranks on one device, so the records are staged through host memory). Each
 rank runs the DEVICE protocol -- dyg_shard_begin_uploaded, the walk of its
 query range with the device packers (k_pack_*), the all-gather, the device
 unpackers (k_unpack_*) and the replicated commit -- and both replicas must
-end bit-identical to the single-process reference replay."""
+end bit-identical to the single-process reference replay. Both transports:
+"peer" (the exchange areas mapped across the two processes with CUDA IPC,
+the per-batch epoch handshake in device memory; the two contexts time-slice
+the GPU) and "collective" (gloo all-gather through host memory)."""
 import os
 import socket
 
@@ -21,7 +24,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir, cfg):
+def _worker(rank, world, port, out_dir, cfg, transport):
     import sys
 
     sys.path.insert(0, REPO)
@@ -43,7 +46,7 @@ def _worker(rank, world, port, out_dir, cfg):
     st = D.SparsifierState(D.DynamicGraph.from_rows(*g.export()),
                            D.DynamicGraph.from_rows(*h.export()), opts)
     stream = D.UpdateStream(s.events(), s.batch_count)
-    sh = ShardedReplay(st, rank, world)
+    sh = ShardedReplay(st, rank, world, transport=transport, peer_timeout_s=120.0)
     reps = sh.replay_stream(stream)
     torch.cuda.synchronize()
     fields = list(O.REPORT_EXACT)
@@ -53,20 +56,24 @@ def _worker(rank, world, port, out_dir, cfg):
         rp, ids, w = st.rows(which)
         np.savez(os.path.join(out_dir, f"rows_{rank}_{which}.npz"), rp=rp, ids=ids, w=w)
     np.save(os.path.join(out_dir, f"bytes_{rank}.npy"), np.array([sh.bytes_exchanged]))
+    dist.barrier()  # every rank done reading the others' exchange areas
+    sh.close()
     st.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["peer", "collective"])
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
-def test_two_processes_device_protocol_match_reference(tmp_path, oracle, cfg):
+def test_two_processes_device_protocol_match_reference(tmp_path, oracle, cfg, transport):
     import torch.multiprocessing as mp
 
     from oracle import oracle as O
     from tests.parity import same_rows
 
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), cfg), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), cfg, transport), nprocs=world,
+             join=True)
     c = O.CONFIGS[cfg]
     g, h, s = O.build_config(oracle, c)
     ost = oracle.state(g, h, K=c.K, T=c.T, s=c.s, seed=c.walk_seed)

@@ -175,3 +175,45 @@ def test_async_commits_host_events_and_settled_guard(oracle, dyg):
     assert sh.update_counter == ost.update_counter
     assert same_rows(ost.graph().export(), sh.rows(0))
     assert same_rows(ost.sparsifier().export(), sh.rows(1))
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_peer_exchange_world1_equals_reference(oracle, dyg, cfg):
+    """The peer-memory transport (dyg_shard_peer_*) with a world of one rank:
+    prepare, walk, pack into the exchange area, epoch publish / wait, unpack
+    and commit as one captured range. Twice (the second replay reuses the
+    graph; the epoch keeps advancing on the device), both equal to the
+    reference replay; a range larger than the area is refused."""
+    c = O.CONFIGS[cfg]
+    g, h, s = O.build_config(oracle, c)
+    nb = s.batch_count
+    ost = oracle.state(g, h, K=c.K, T=c.T, s=c.s, seed=c.walk_seed)
+    ref = [ost.replay_batch(s, b) for b in range(nb)]
+    opts = dyg.SparsifierOptions(dyg.WalkConfig(c.K, c.T, c.s, c.walk_seed), True, False)
+    st = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
+    ev = s.events()
+    kinds = np.bincount(ev["batch_index"][ev["kind"] == 0].astype(np.int64), minlength=nb)
+    kdel = np.bincount(ev["batch_index"][ev["kind"] != 0].astype(np.int64), minlength=nb)
+    area, nbytes, handle = st.shard_peer_create(1, int(kinds.max()), int(kdel.max()))
+    assert area and nbytes > 0 and len(handle) == 64
+    st.shard_peer_bind(0, 1, [area])
+    st.upload_stream(dyg.UpdateStream(ev, nb))
+    st.snapshot()
+    for rep in range(2):
+        if rep:
+            st.restore()
+        st.shard_peer_range_begin(0, nb)
+        got = st.shard_peer_range_end(nb)
+        assert len(got) == nb
+        for b in range(nb):
+            for f in O.REPORT_EXACT:
+                assert ref[b][f] == getattr(got[b], f), (rep, b, f)
+        assert same_rows(ost.graph().export(), st.rows(0))
+        assert same_rows(ost.sparsifier().export(), st.rows(1))
+    # An area sized below the stream's largest batch refuses the range.
+    area2, _, _ = st.shard_peer_create(1, 1, 1)
+    st.shard_peer_bind(0, 1, [area2])
+    with pytest.raises(dyg.Error) as e:
+        st.shard_peer_range_begin(0, nb)
+    assert e.value.kind == dyg.ErrorKind.Usage and "exceeds the exchange area" in str(e.value)
+    st.close()
