@@ -278,6 +278,19 @@ class UpdateStream:
             self._off, self._off_key = off, key
         return self._off
 
+    def kind_counts(self):
+        """(insertions, deletions) per batch, numpy arrays of batch_count.
+        Cached like batch_offsets()."""
+        key = (self.events.ctypes.data, len(self.events), self.batch_count)
+        if getattr(self, "_kc_key", None) != key:
+            k = np.asarray(self.events["kind"])
+            bi = np.asarray(self.events["batch_index"]).astype(np.int64)
+            nb = self.batch_count
+            ins = np.bincount(bi[k == 0], minlength=nb)[:nb]
+            self._kc = (ins, np.bincount(bi, minlength=nb)[:nb] - ins)
+            self._kc_key = key
+        return self._kc
+
     def batch(self, b: int):
         """(events, positions) of batch b, in stream order. A batch stored
         contiguously (the usual case) is returned as a view of the stream's

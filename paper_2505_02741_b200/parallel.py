@@ -154,12 +154,7 @@ class ShardedReplay:
         """dyg_stream_upload of `stream` plus its per-batch kind counts (the
         peer areas are sized from them)."""
         self.state.upload_stream(stream)
-        ev = stream.events
-        k = np.asarray(ev["kind"])
-        bi = np.asarray(ev["batch_index"]).astype(np.int64)
-        nb = stream.batch_count
-        self._kind_counts = (np.bincount(bi[k == 0], minlength=nb)[:nb],
-                             np.bincount(bi[k != 0], minlength=nb)[:nb])
+        self._kind_counts = stream.kind_counts()
 
     def replay_uploaded(self, batch_index: int):
         """Batch `batch_index` of the stream given to state.upload_stream."""

@@ -85,4 +85,5 @@ def test_two_processes_device_protocol_match_reference(tmp_path, oracle, cfg, tr
         for which, og in ((0, ost.graph()), (1, ost.sparsifier())):
             z = np.load(tmp_path / f"rows_{rank}_{which}.npz")
             assert same_rows(og.export(), (z["rp"], z["ids"], z["w"])), (rank, which)
-        assert int(np.load(tmp_path / f"bytes_{rank}.npy")[0]) > 0
+        if transport == "collective":  # (the peer transport moves no host-visible buffers)
+            assert int(np.load(tmp_path / f"bytes_{rank}.npy")[0]) > 0
