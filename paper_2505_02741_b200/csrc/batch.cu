@@ -1864,25 +1864,30 @@ __global__ void k_pack_reach_peer(ReachOut r, const uint32_t* n_dev, uint32_t sl
   rec[i] = x;
 }
 
+// One warp per record (a record is ~0.4 KB: block-per-record grids of 12 k
+// small blocks cost more in scheduling than in bytes).
 __global__ void k_pack_min_peer(MinOut m, const uint32_t* n_dev, uint32_t slots, uint32_t T,
                                 PeerX px) {
-  const uint32_t i = blockIdx.x;
-  if (i >= slots) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const size_t rec_bytes = min_record_bytes(T);
-  uint8_t* base = peer_next_buffer(px) + px.min_off + static_cast<size_t>(i) * rec_bytes;
+  uint8_t* const buf = peer_next_buffer(px) + px.min_off;
   const uint32_t n = *n_dev;
-  MinRecordHead* h = reinterpret_cast<MinRecordHead*>(base);
-  uint32_t* path = reinterpret_cast<uint32_t*>(base + sizeof(MinRecordHead));
-  const bool have = i < n;
-  const uint32_t len = have ? m.path_len[i] : 0;
-  if (threadIdx.x == 0) {
-    h->has_path = have ? m.has_path[i] : 0;
-    h->path_len = len;
-    h->steps = have ? m.steps[i] : 0ull;
-    h->resistance = have ? m.resistance[i] : 0.0;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < slots; i += nw) {
+    uint8_t* base = buf + static_cast<size_t>(i) * rec_bytes;
+    MinRecordHead* h = reinterpret_cast<MinRecordHead*>(base);
+    uint32_t* path = reinterpret_cast<uint32_t*>(base + sizeof(MinRecordHead));
+    const bool have = i < n;
+    const uint32_t len = have ? m.path_len[i] : 0;
+    if (lane == 0) {
+      h->has_path = have ? m.has_path[i] : 0;
+      h->path_len = len;
+      h->steps = have ? m.steps[i] : 0ull;
+      h->resistance = have ? m.resistance[i] : 0.0;
+    }
+    const uint32_t* src = m.paths + static_cast<uint64_t>(i) * (T + 1ull);
+    for (uint32_t j = lane; j < len; j += 32) path[j] = src[j];
   }
-  const uint32_t* src = m.paths + static_cast<uint64_t>(i) * (T + 1ull);
-  for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) path[j] = src[j];
 }
 
 // Publish this rank's records of the batch: epoch += 1, then the release
@@ -1936,24 +1941,26 @@ __global__ void k_unpack_reach_peer(ReachOut r, const uint32_t* nq_dev, uint32_t
 }
 
 __global__ void k_unpack_min_peer(MinOut m, const uint32_t* nq_dev, uint32_t T, PeerX px) {
-  const uint32_t q = blockIdx.x;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t nq = *nq_dev;
-  if (q >= nq) return;
-  uint32_t rank, idx;
-  locate(q, nq, px.world, &rank, &idx);
-  const uint8_t* base =
-      peer_cur_buffer(px, rank) + px.min_off + static_cast<size_t>(idx) * min_record_bytes(T);
-  const MinRecordHead* h = reinterpret_cast<const MinRecordHead*>(base);
-  const uint32_t* path = reinterpret_cast<const uint32_t*>(base + sizeof(MinRecordHead));
-  const uint32_t len = h->path_len;
-  if (threadIdx.x == 0) {
-    m.has_path[q] = h->has_path;
-    m.path_len[q] = len;
-    m.steps[q] = h->steps;
-    m.resistance[q] = h->resistance;
+  for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += nw) {
+    uint32_t rank, idx;
+    locate(q, nq, px.world, &rank, &idx);
+    const uint8_t* base =
+        peer_cur_buffer(px, rank) + px.min_off + static_cast<size_t>(idx) * min_record_bytes(T);
+    const MinRecordHead* h = reinterpret_cast<const MinRecordHead*>(base);
+    const uint32_t* path = reinterpret_cast<const uint32_t*>(base + sizeof(MinRecordHead));
+    const uint32_t len = h->path_len;
+    if (lane == 0) {
+      m.has_path[q] = h->has_path;
+      m.path_len[q] = len;
+      m.steps[q] = h->steps;
+      m.resistance[q] = h->resistance;
+    }
+    uint32_t* dst = m.paths + static_cast<uint64_t>(q) * (T + 1ull);
+    for (uint32_t j = lane; j < len; j += 32) dst[j] = path[j];
   }
-  uint32_t* dst = m.paths + static_cast<uint64_t>(q) * (T + 1ull);
-  for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) dst[j] = path[j];
 }
 
 // Co-resident grid for a cooperative kernel, cached per kernel (not per
@@ -2351,7 +2358,7 @@ int launch_pack_peer(const BatchDev& b, const uint32_t* rng, uint32_t slots_r, u
     ++l;
   }
   if (slots_m) {
-    k_pack_min_peer<<<slots_m, 128, 0, st>>>(b.mout, rng + 3, slots_m, T, px);
+    k_pack_min_peer<<<(slots_m + 7) / 8, 256, 0, st>>>(b.mout, rng + 3, slots_m, T, px);
     ++l;
   }
   k_peer_signal<<<1, 1, 0, st>>>(px, b.abort_flag);
@@ -2367,7 +2374,7 @@ int launch_unpack_peer(const BatchDev& b, uint32_t max_r, uint32_t max_m, uint32
     ++l;
   }
   if (max_m && slots_m) {
-    k_unpack_min_peer<<<max_m, 128, 0, st>>>(b.mout, &b.ctl->nq_min, T, px);
+    k_unpack_min_peer<<<(max_m + 7) / 8, 256, 0, st>>>(b.mout, &b.ctl->nq_min, T, px);
     ++l;
   }
   return l;
