@@ -31,7 +31,6 @@
 
 #include "graph_store.cuh"
 #include "spectral.cuh"
-#include "host/ordering.hpp"
 
 namespace dyg {
 
@@ -744,24 +743,18 @@ void GroundedChol::build(const HostCsrView& g) {
   if (L.descr_create(&descr_) != 0) sfail(4, "cusparseCreateMatDescr failed");
   // Fill-reducing ordering and the permuted matrix B = A(p, p).
   std::vector<int> perm(m_);
-  // Level-set nested dissection (host/ordering.cpp) by default; METIS
-  // through cuSOLVER with DYG_ORDERING=metis (a measurement switch, read per
-  // call: 8x slower to compute at n = 262 k, somewhat less fill).
-  // (cuSOLVER's host AMD ordering measured 44x slower than METIS here.)
+  // (cuSOLVER's host AMD ordering measured 44x slower than METIS here; a
+  // breadth-first level-set nested dissection was 8x cheaper to compute but
+  // made PCG 5.7x slower at n = 262 k: a sparsifier is nearly a tree, whose
+  // level sets are poor separators.)
   if (ordering_cache_lookup(m_, rp, ci, perm)) {
     lap("cached ordering");
   } else {
-    const char* ord = std::getenv("DYG_ORDERING");
-    if (ord != nullptr && std::strcmp(ord, "metis") == 0) {
-      if (L.metisnd(handle_, static_cast<int>(m_), nnz_, descr_, rp.data(), ci.data(), nullptr,
-                    perm.data()) != 0)
-        sfail(3, "Laplacian factorization failed (ordering)");
-      lap("metis ordering");
-    } else {
-      perm = nested_dissection_order(static_cast<int>(m_), rp.data(), ci.data());
-      lap("nested-dissection ordering");
-    }
+    if (L.metisnd(handle_, static_cast<int>(m_), nnz_, descr_, rp.data(), ci.data(), nullptr,
+                  perm.data()) != 0)
+      sfail(3, "Laplacian factorization failed (ordering)");
     ordering_cache_store(m_, rp, ci, perm);
+    lap("metis ordering");
   }
   size_t pbytes = 0;
   if (L.perm_size(handle_, static_cast<int>(m_), static_cast<int>(m_), nnz_, descr_, rp.data(),
