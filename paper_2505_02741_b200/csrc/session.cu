@@ -562,7 +562,7 @@ void phase_prepare(dyg_session* s, Pending& p) {
 // Walks over query ranges. Full range (single GPU): counts stay on the
 // device (no host sync). Shard range: counts written from the host.
 void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n_r, uint32_t lo_m,
-                uint32_t n_m) {
+                uint32_t n_m, bool fork_g = false) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
@@ -584,6 +584,9 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   // Insertion fast path: G's appends do not depend on the walk (it reads H
   // alone); fork them onto the aux stream so they fill the walk's tail.
   const bool fast = p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass;
+  // A shard walk forks them only when the same Pending reaches the commit
+  // (fork_g: the peer-exchange range enqueues walk and commit together).
+  const bool fork = fast && (full || fork_g);
   // The fork point is recorded before the walk, but the aux kernels are
   // enqueued after it: the walk's blocks claim the SMs first (its start is
   // on the batch's critical path; the appends only need to finish by the
@@ -594,7 +597,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     check(cudaEventRecord(s->ev_join, s->aux_stream), "join");
     p.g_appended = true;
   };
-  if (full && fast) {
+  if (fork) {
     check(cudaEventRecord(s->ev_fork, s->stream), "fork");
   }
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
@@ -607,7 +610,7 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
                                s->d_work, s->stream, /*standalone=*/!full);
     maybe_sync(s, "reach walks");
   }
-  if (full && fast) fork_appends();
+  if (fork) fork_appends();
   if (p.g_appended) check(cudaStreamWaitEvent(s->stream, s->ev_join, 0), "join");
   if (p.n_del > 0 && !o.freeze && max_m > 0) {
     WalkParams Pd = P;
@@ -2699,7 +2702,7 @@ void peer_range_begin(dyg_session* s, uint32_t first, uint32_t count) {
       phase_prepare(s, p);
       p.launches += launch_shard_range(s->b, rank, static_cast<int>(world), s->d_counts + 4, sl_r,
                                        sl_m, s->stream);
-      phase_walk(s, p, false, 0, sl_r, 0, sl_m);
+      phase_walk(s, p, false, 0, sl_r, 0, sl_m, /*fork_g=*/true);
       p.launches += launch_pack_peer(s->b, s->d_counts + 4, sl_r, sl_m, T, s->px, s->stream);
       p.launches += launch_unpack_peer(s->b, p.n_ins, p.n_del, sl_r, sl_m, T, s->px, s->stream);
       commit_enqueue(s, p, false);
