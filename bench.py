@@ -82,7 +82,10 @@ def make_inputs_product(cfg, scale=1):
     g = gen(rows, cols, 1)
     # The device builder, bit-identical to the host one.
     h = D.build_initial_sparsifier_gpu(g, 0.10, 1)
-    s = D.generate_update_stream(g, D.StreamGenOptions(ins, dele, 10, 7, loc))
+    # The stream: insertion sampling on the device for locality 0 (C4 / C5;
+    # bit-identical, checked against the reference arm's inputs below).
+    o = D.StreamGenOptions(ins, dele, 10, 7, loc)
+    s = D.generate_update_stream_gpu(g, o) if loc == 0 else D.generate_update_stream(g, o)
     return g, h, s
 
 

@@ -370,6 +370,19 @@ int dyg_pcg_solve(const dyg_csr* g, const dyg_csr* h, uint32_t factor_cap, const
                   dyg_pcg_result* out, double* energy_trace, size_t energy_cap);
 /* random_rhs(n, seed) (solver.cpp:146-159), on the host. */
 int dyg_random_rhs(uint32_t n, uint64_t seed, double* out);
+
+/* generate_update_stream(G, {insert_fraction, delete_fraction, batches,
+ * seed, locality 0}) (stream.cpp:114-200) with the insertion sampling on
+ * `device`, bit-identical to the reference: attempts are drawn
+ * speculatively in parallel from the counter-based SplitMix64 stream and
+ * accepted up to the first rejected one per round (self-loop, edge of G,
+ * repeated pair); deletions (a partial Fisher-Yates) on the host. Writes the
+ * events in stream order; *n_out is set even when `capacity` is too small
+ * (then DYG_ERR_USAGE: call again with a larger buffer). The locality > 0
+ * mode is the host generator's (dygh_generate_stream). */
+int dyg_generate_stream(const dyg_csr* g, double insert_fraction, double delete_fraction,
+                        uint32_t batches, uint64_t seed, int device, dyg_event* out,
+                        size_t capacity, size_t* n_out, uint32_t* batch_count);
 /* Exact Laplacian solves reuse a fill-reducing ordering for an identical H
  * sparsity pattern, or one differing in at most 5 % of its nonzeros (H
  * between batches); cumulative counts of exact hits, near hits and fresh

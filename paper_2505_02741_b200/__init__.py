@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     build_initial_sparsifier_gpu,
     device_count,
     generate_update_stream,
+    generate_update_stream_gpu,
     load_matrix_market,
     load_update_stream,
     make_grid4,

@@ -317,6 +317,32 @@ def save_update_stream(s: UpdateStream, path: str) -> None:
         L.dygh_stream_free(h)
 
 
+def generate_update_stream_gpu(g: DynamicGraph, options: StreamGenOptions,
+                               device: int = 0) -> UpdateStream:
+    """generate_update_stream with the insertion sampling on the device
+    (dyg_generate_stream); locality > 0 uses the host generator."""
+    if options.locality:
+        return generate_update_stream(g, options)
+    L = _lib.lib()
+    c = g.csr()
+    n, nb = C.c_size_t(), C.c_uint32()
+    n_ins = int(round(options.insert_fraction * g.vertex_count()))
+    cap = n_ins + int(round(options.delete_fraction * g.edge_count())) + 16
+    while True:
+        out = _lib.pinned_empty(cap, EVENT_DTYPE)
+        st = L.dyg_generate_stream(C.byref(c), options.insert_fraction, options.delete_fraction,
+                                   options.batches, options.seed, device, ptr(out), cap,
+                                   C.byref(n), C.byref(nb))
+        if st == 1 and n.value > cap:
+            cap = n.value
+            continue
+        _check(st)
+        break
+    s = UpdateStream(None, nb.value)
+    s.events = out[:n.value]
+    return s
+
+
 def generate_update_stream(g: DynamicGraph, options: StreamGenOptions) -> UpdateStream:
     h = C.c_void_p()
     _hcheck(_lib.lib().dygh_generate_stream(

@@ -17,6 +17,7 @@
 #include "batch.cuh"
 #include "graph_store.cuh"
 #include "spectral.cuh"
+#include "stream_gen.cuh"
 
 using namespace dyg;
 
@@ -2784,6 +2785,31 @@ int dyg_shard_peer_range_end(dyg_session* s, dyg_batch_report* out, size_t cap, 
     check(cudaSetDevice(s->device), "set device");
     peer_range_end(s, out);
     if (n_out) *n_out = n;
+  });
+}
+
+// ---- generate_update_stream with device insertion sampling ---------------
+int dyg_generate_stream(const dyg_csr* g, double insert_fraction, double delete_fraction,
+                        uint32_t batches, uint64_t seed, int device, dyg_event* out,
+                        size_t capacity, size_t* n_out, uint32_t* batch_count) {
+  return guarded([&] {
+    if (n_out == nullptr || batch_count == nullptr) fail(DYG_ERR_USAGE, "null argument");
+    *n_out = 0;
+    *batch_count = 0;
+    check_csr(g, "graph");
+    check(cudaSetDevice(device), "set device");
+    std::vector<dyg_event> ev;
+    uint32_t nb = 0;
+    try {
+      generate_stream_device(*g, insert_fraction, delete_fraction, batches, seed, ev, nb, nullptr);
+    } catch (const GenError& e) {
+      fail(e.code, e.message);
+    }
+    *n_out = ev.size();
+    *batch_count = nb;
+    if (out == nullptr || capacity < ev.size())
+      fail(DYG_ERR_USAGE, "event buffer too small: " + std::to_string(ev.size()) + " events");
+    std::memcpy(out, ev.data(), sizeof(dyg_event) * ev.size());
   });
 }
 
