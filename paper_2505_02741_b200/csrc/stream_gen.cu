@@ -26,6 +26,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "graph_store.cuh"
@@ -196,19 +197,33 @@ void generate_stream_device(const dyg_csr& g, double insert_fraction, double del
   const auto n_ins = static_cast<uint64_t>(std::llround(insert_fraction * static_cast<double>(n)));
   const auto n_del =
       static_cast<uint64_t>(std::llround(delete_fraction * static_cast<double>(m_edges)));
-  // edges(): (u, v) with u < v in row order (graph.cpp:118-127), and the
-  // weight range of G (stream.cpp:129-134).
-  std::vector<std::pair<std::pair<uint32_t, uint32_t>, double>> edges;
-  edges.reserve(m_edges);
+  // edges() -- (u, v) with u < v in row order (graph.cpp:118-127) -- is
+  // not materialised: `upper[u]` counts row u's entries with v > u, so edge p
+  // of the list is found by a binary search over their prefix sums. The
+  // weight range of G (stream.cpp:129-134) in the same pass.
+  std::vector<uint64_t> upper(n + 1ull, 0);
   double wmin = std::numeric_limits<double>::infinity(), wmax = 0.0;
-  for (uint32_t u = 0; u < n; ++u)
+  for (uint32_t u = 0; u < n; ++u) {
+    uint64_t c = 0;
     for (uint64_t i = g.row_ptr[u]; i < g.row_ptr[u + 1]; ++i)
       if (u < g.ids[i]) {
-        edges.push_back({{u, g.ids[i]}, g.w[i]});
+        ++c;
         wmin = std::min(wmin, g.w[i]);
         wmax = std::max(wmax, g.w[i]);
       }
-  if (n_ins > 0 && edges.empty())
+    upper[u + 1] = upper[u] + c;
+  }
+  const uint64_t ne = upper[n];
+  auto edge_at = [&](uint64_t p, uint32_t& eu, uint32_t& ev) {
+    eu = static_cast<uint32_t>(std::upper_bound(upper.begin(), upper.end(), p) - upper.begin() - 1);
+    uint64_t r = p - upper[eu];
+    for (uint64_t i = g.row_ptr[eu];; ++i)
+      if (eu < g.ids[i] && r-- == 0) {
+        ev = g.ids[i];
+        return;
+      }
+  };
+  if (n_ins > 0 && ne == 0)
     throw GenError{2, "cannot derive insertion weights from an edgeless graph"};
   const unsigned long long s0 = mix64(seed + 0x12345678ull);
   events.assign(n_ins, dyg_event{});
@@ -291,20 +306,27 @@ void generate_stream_device(const dyg_csr& g, double insert_fraction, double del
                "stream generator: events");
   }
   // Deletions (stream.cpp:180-196): partial Fisher-Yates over the edge list,
-  // draws continuing after the insertion phase's.
-  if (n_del > edges.size()) throw GenError{2, "deletion fraction exceeds edge count"};
+  // draws continuing after the insertion phase's. Only the positions the
+  // swaps touched differ from the identity: they live in a small map.
+  if (n_del > ne) throw GenError{2, "deletion fraction exceeds edge count"};
   const uint32_t deletion_base = n_ins > 0 ? batches : 0;
   events.reserve(n_ins + n_del);
-  const uint64_t ne = edges.size();
+  std::unordered_map<uint64_t, uint64_t> moved;  // position -> edge index now there
+  moved.reserve(2 * n_del);
+  auto at = [&](uint64_t p) {
+    const auto it = moved.find(p);
+    return it == moved.end() ? p : it->second;
+  };
   for (uint64_t k = 0; k < n_del; ++k) {
     const unsigned long long x = draw(s0, ++j);
     const uint64_t pick =
         k + static_cast<uint64_t>((static_cast<unsigned __int128>(x) * (ne - k)) >> 64);
-    std::swap(edges[k], edges[pick]);
+    const uint64_t ek = at(pick);  // std::swap(edges[k], edges[pick])
+    moved[pick] = at(k);
+    moved[k] = ek;
     dyg_event e{};
     e.kind = 1;
-    e.u = edges[k].first.first;
-    e.v = edges[k].first.second;
+    edge_at(ek, e.u, e.v);
     e.batch_index =
         deletion_base + static_cast<uint32_t>(k * batches / std::max<uint64_t>(n_del, 1));
     events.push_back(e);
