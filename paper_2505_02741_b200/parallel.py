@@ -179,14 +179,31 @@ class ShardedReplay:
         handles = [None] * self.world
         dist.all_gather_object(handles, handle, group=self.group)
         dev = torch.cuda.current_device()
-        areas = []
+        areas, err = [], None
         for q, h in enumerate(handles):
             if q == self.rank:
                 areas.append(area)
-            else:
+                continue
+            try:
                 p = ipc_open(h, dev)
-                self._peer_mapped.append(p)
-                areas.append(p)
+            except Exception as e:  # noqa: BLE001 -- e.g. no P2P / IPC between these GPUs
+                err = e
+                break
+            self._peer_mapped.append(p)
+            areas.append(p)
+        # Every rank must use the same transport: fall back together.
+        ok = torch.tensor([0.0 if err else 1.0],
+                          device=self.device if self._nccl else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if ok.item() < 1.0:
+            import warnings
+            warnings.warn(f"peer-memory exchange unavailable ({err or 'on another rank'}); "
+                          "using the collective transport")
+            for p in self._peer_mapped:
+                ipc_close(p)
+            self._peer_mapped = []
+            self.transport = "collective"
+            return
         self.state.shard_peer_bind(self.rank, self.world, areas, self.peer_timeout_s)
         self._peer_key = key
 
@@ -208,6 +225,7 @@ class ShardedReplay:
             ins, dele = self._kind_counts
             self._peer_setup(int(ins[first:first + count].max(initial=0)),
                              int(dele[first:first + count].max(initial=0)))
+        if self.transport == "peer":
             self.state.shard_peer_range_begin(first, count)
             return self.state.shard_peer_range_end(count)
         reports = []
