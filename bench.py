@@ -555,7 +555,7 @@ def run_ours(args):
             "step": (f"restore(G0,H0) + replay of all batches ({kinds['insertion'][2] // args.steps}"
                      f" incremental + {kinds['deletion'][2] // args.steps} decremental)"),
             "K": K_BUDGET, "T": T_CAP, "s": WALKERS, "walk_seed": WALK_SEED,
-            "parallelism": (f"replicated G/H, walks sharded x{world}, {args.transport} exchange"
+            "parallelism": (f"replicated G/H, walks sharded x{world}, {sharded.transport} exchange"
                             if (world > 1 or force_shard)
                             else "1 GPU"),
             "l2": (f"inputs larger than L2 (G slabs {g.vertex_count() * 128 / 1e6:.0f} MB + "
