@@ -2268,6 +2268,35 @@ int dyg_session_reset_stats(dyg_session* s) {
   });
 }
 
+// Measurement switch DYG_L2_PERSIST_MB=X (read when a stream is bound): an
+// L2 access-policy window over the head of H's slab table with X MB of
+// persisting lines. Measured: no gain --
+// the walks' row accesses are uniform over H, so persisting a part of it
+// only moves hits between regions.
+void apply_l2_window(dyg_session* s) {
+  const char* e = std::getenv("DYG_L2_PERSIST_MB");
+  if (e == nullptr) return;
+  const double mb = std::atof(e);
+  int max_win = 0;
+  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
+  const DevGraph<kCapH> h = s->H.view();
+  const size_t bytes = std::min<size_t>(sizeof(Slab<kCapH>) * static_cast<size_t>(h.n),
+                                        static_cast<size_t>(max_win));
+  const size_t persist = static_cast<size_t>(mb * 1048576.0);
+  if (bytes == 0 || persist == 0) return;
+  check(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist), "persisting L2");
+  cudaStreamAttrValue a{};
+  a.accessPolicyWindow.base_ptr = h.slab;
+  a.accessPolicyWindow.num_bytes = bytes;
+  a.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(persist) / bytes));
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  check(cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &a), "L2 window");
+  if (std::getenv("DYG_GRAPH_DEBUG"))
+    std::fprintf(stderr, "dyg: L2 window %zu MB over H, %zu MB persisting (max window %d MB)\n",
+                 bytes >> 20, persist >> 20, max_win >> 20);
+}
+
 int dyg_set_stream(dyg_session* s, void* cuda_stream) {
   return guarded([&] {
     require_settled(s);
@@ -2276,6 +2305,7 @@ int dyg_set_stream(dyg_session* s, void* cuda_stream) {
     if (s->own_stream) cudaStreamDestroy(s->stream);
     s->stream = static_cast<cudaStream_t>(cuda_stream);
     s->own_stream = false;
+    apply_l2_window(s);
   });
 }
 
