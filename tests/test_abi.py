@@ -108,6 +108,12 @@ def test_null_arguments_are_usage_errors():
     assert L.dyg_session_snapshot(None) == 1
     assert L.dyg_update_counter(None) == 0
     L.dyg_session_destroy(None)  # no-op
+    # round-2 entry points: null / invalid arguments are Usage errors, no device touched
+    assert L.dyg_stream_upload_batches(None, None, 0, None, 0) == 1
+    assert L.dyg_shard_peer_range_begin(None, 0, 0) == 1
+    assert L.dyg_shard_peer_bind(None, 0, 1, None, 1.0) == 1
+    assert L.dyg_session_options(None, None) == 1
+    assert L.dyg_generate_stream(None, 0.1, 0.0, 1, 1, 0, None, 0, None, None) == 1
 
 
 def test_dysparse_adapter_compiles_against_reference_headers(tmp_path):
