@@ -462,7 +462,11 @@ int dyg_shard_finish(dyg_session* s, dyg_batch_report* out, size_t cap, size_t* 
  *   dyg_shard_peer_range_begin / _end: enqueue the uploaded batches
  *     [first, first + count) (dyg_stream_upload*) / synchronise and report
  *     them (the first failing batch's error, as dyg_replay_uploaded_range).
- * Every rank must run the same ranges in the same order. */
+ * Every rank must run the same ranges in the same order. Ranks are
+ * separate processes (one per GPU; several may share a GPU, whose contexts
+ * then time-slice): two sessions of ONE process must not be peers, since a
+ * rank's wait kernel could then hold SM resources another rank's
+ * cooperative commit needs (the exchange would time out). */
 int dyg_shard_peer_create(dyg_session* s, int world, uint64_t max_reach, uint64_t max_minpath,
                           void** area, size_t* bytes, void* ipc_handle);
 int dyg_ipc_open(const void* ipc_handle, int device, void** ptr);
