@@ -385,8 +385,16 @@ def run_ours(args):
         sys.stdout.flush()
         real_stdout = os.dup(1)
         os.dup2(2, 1)
+        # DYG_BENCH_SHARED_GPU=1 (a test switch): every rank on cuda:0 over gloo
+        # -- the N > 1 script path on a one-GPU box (the ranks' contexts
+        # time-slice the GPU, so its numbers are not scaling numbers).
+        shared = os.environ.get("DYG_BENCH_SHARED_GPU") == "1"
+        if shared:
+            local = 0
         torch.cuda.set_device(local)
-        if force_shard:  # the N > 1 code path on one GPU (a world of one rank)
+        if shared:
+            dist.init_process_group("gloo")
+        elif force_shard:  # the N > 1 code path on one GPU (a world of one rank)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
             dist.init_process_group("nccl", rank=0, world_size=1,
@@ -445,7 +453,8 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dev_t = "cuda" if torch.distributed.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev_t)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
