@@ -374,3 +374,38 @@ def test_replay_stream_stops_at_failing_batch(oracle, dyg):
                               dyg.SparsifierOptions(dyg.WalkConfig(10.0, 30, 8, 3), True, False))
     st2.replay(dyg.UpdateStream(ev[:2], 1))
     assert st2.update_counter == 2
+
+
+def test_uploaded_stream_with_empty_batches(oracle, dyg):
+    """A grouped stream with empty batches (batch 1 and the last) through the
+    asynchronous per-batch upload: the uploaded range, the peer-exchange
+    range (world 1) and the per-batch reference replay agree."""
+    c, g, h, s = cfg_inputs(oracle, "C1")
+    ev = s.events().copy()
+    nb0 = s.batch_count
+    ev["batch_index"] = np.where(ev["batch_index"] >= 1, ev["batch_index"] + 1, 0)
+    nb = nb0 + 2  # batch 1 and batch nb - 1 are empty
+    ost = oracle.state(g, h, K=c.K, T=c.T, s=c.s, seed=c.walk_seed)
+    ostream = oracle.stream(ev, nb)
+    ref = [ost.replay_batch(ostream, b) for b in range(nb)]
+    opts = dyg.SparsifierOptions(dyg.WalkConfig(c.K, c.T, c.s, c.walk_seed), True, False)
+    for peer in (False, True):
+        st = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
+        stream = dyg.UpdateStream(ev, nb)
+        st.upload_stream(stream)
+        if peer:
+            ins, dele = stream.kind_counts()
+            area, _, _ = st.shard_peer_create(1, int(ins.max()), int(dele.max()))
+            st.shard_peer_bind(0, 1, [area])
+            st.shard_peer_range_begin(0, nb)
+            got = st.shard_peer_range_end(nb)
+        else:
+            got = st.replay_uploaded_range(0, nb)
+        assert [r.batch_index for r in got] == list(range(nb))
+        for b in range(nb):
+            for f in O.REPORT_EXACT:
+                assert ref[b][f] == getattr(got[b], f), (peer, b, f)
+        assert same_rows(ost.graph().export(), st.rows(0))
+        assert same_rows(ost.sparsifier().export(), st.rows(1))
+        assert st.update_counter == ost.update_counter
+        st.close()
