@@ -5,7 +5,7 @@
 # copied to profiles/ by hand. Usage: gpurun -- bash tools/sanitize.sh [TOOLS...]
 mkdir -p gpurun_out
 TOOLS=${@:-memcheck racecheck synccheck initcheck}
-SEL="tests/test_gpu_replay.py tests/test_gpu_walks.py tests/test_gpu_shard.py tests/test_gpu_engines.py tests/test_gpu_decisions.py"
+SEL="tests/test_gpu_replay.py tests/test_gpu_walks.py tests/test_gpu_shard.py tests/test_gpu_engines.py tests/test_gpu_decisions.py tests/test_gpu_stream_gen.py tests/test_gpu_checkpoint.py"
 for t in $TOOLS; do
   extra=""
   [ "$t" = "memcheck" ] && extra="--leak-check no"
