@@ -1112,6 +1112,9 @@ void run_uploaded_range(dyg_session* s, uint32_t first, uint32_t count, dyg_batc
     if (s->h_ctls) cudaFreeHost(s->h_ctls);
     s->h_ctls = nullptr;
     dev_alloc(&s->d_ctls, count, "batch control blocks");
+    // Empty batches never initialise their block; the whole-range download
+    // then copies defined bytes (initcheck).
+    check(cudaMemset(s->d_ctls, 0, sizeof(BatchCtl) * count), "batch control blocks");
     check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctls), sizeof(BatchCtl) * count),
           "pinned control blocks");
     s->ctl_cap = count;
@@ -1234,6 +1237,7 @@ void run_stream(dyg_session* s, const dyg_event* events, size_t n, const uint64_
     if (s->h_ctls) cudaFreeHost(s->h_ctls);
     s->h_ctls = nullptr;
     dev_alloc(&s->d_ctls, nbatches, "batch control blocks");
+    check(cudaMemset(s->d_ctls, 0, sizeof(BatchCtl) * nbatches), "batch control blocks");
     check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctls), sizeof(BatchCtl) * nbatches),
           "pinned control blocks");
     s->ctl_cap = nbatches;
@@ -2693,6 +2697,9 @@ void peer_range_begin(dyg_session* s, uint32_t first, uint32_t count) {
     if (s->h_ctls) cudaFreeHost(s->h_ctls);
     s->h_ctls = nullptr;
     dev_alloc(&s->d_ctls, count, "batch control blocks");
+    // Empty batches never initialise their block; the whole-range download
+    // then copies defined bytes (initcheck).
+    check(cudaMemset(s->d_ctls, 0, sizeof(BatchCtl) * count), "batch control blocks");
     check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctls), sizeof(BatchCtl) * count),
           "pinned control blocks");
     s->ctl_cap = count;
