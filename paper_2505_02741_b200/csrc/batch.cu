@@ -218,7 +218,6 @@ __device__ void restore_rows(const DevGraph<kCapG>& G, const BatchDev& b, uint32
   for (uint32_t idx = tid; idx < n; idx += nth) {
     const uint32_t row = b.saved_rows[idx];
     const Slab<kCapG> sl = b.side_slab[idx];
-    mark_dirty(G, row);
     G.slab[row] = sl;
     if (sl.ext != kInline) {
       const unsigned long long off = b.side_off[idx];

@@ -116,9 +116,6 @@ struct DevGraph {
   unsigned long long pool_cap;
   unsigned long long* edges;      // |E| (device counter)
   uint32_t n;
-  // Rows changed since the last snapshot (GraphStore::restore_dirty_from):
-  // every row mutator below flags its row (nullptr: not tracked).
-  uint8_t* dirty;
 };
 
 // ---------------------------------------------------------------- rows
@@ -176,14 +173,8 @@ __device__ __forceinline__ double edge_weight(const DevGraph<C>& g, uint32_t u, 
 // push_back with slab -> pool relocation. Returns false when the pool is
 // exhausted (the host keeps enough headroom that this never happens).
 template <int C>
-__device__ __forceinline__ void mark_dirty(const DevGraph<C>& g, uint32_t u) {
-  if (g.dirty) g.dirty[u] = 1;
-}
-
-template <int C>
 __device__ __forceinline__ bool row_push(const DevGraph<C>& g, uint32_t u, uint32_t id,
                                          double w) {
-  mark_dirty(g, u);
   Slab<C>& s = g.slab[u];
   const uint32_t d = s.deg;
   if (s.ext == kInline) {
@@ -221,7 +212,6 @@ __device__ __forceinline__ bool row_push(const DevGraph<C>& g, uint32_t u, uint3
 // graph.cpp:97-105 remove_from: the last entry moves into the hole.
 template <int C>
 __device__ __forceinline__ void row_remove_at(const DevGraph<C>& g, uint32_t u, uint32_t i) {
-  mark_dirty(g, u);
   const RowRef<C> r = row(g, u);
   const uint32_t last = r.deg() - 1;
   r.set(i, r.id(last), r.w(last));
@@ -240,8 +230,6 @@ __device__ __forceinline__ int insert_edge(const DevGraph<C>& g, uint32_t u, uin
     const double nw = __dadd_rn(ru.w(static_cast<uint32_t>(i)), w);
     ru.set_w(static_cast<uint32_t>(i), nw);
     row(g, v).set_w(static_cast<uint32_t>(row_find(g, v, u)), nw);
-    mark_dirty(g, u);
-    mark_dirty(g, v);
     return 1;
   }
   if (!row_push(g, u, v, w)) return -1;

@@ -90,59 +90,7 @@ unsigned grid_for(uint64_t n, unsigned bs = 256) {
   return static_cast<unsigned>((n + bs - 1) / bs);
 }
 
-// Rows flagged since the snapshot get the snapshot's slab, capacity and --
-// when the snapshot's row lived in the pool -- its pool block back; the flags
-// are cleared. Pool blocks of unflagged rows were never written (a block
-// belongs to one row, and only that row's mutators write it; blocks handed
-// out since the snapshot lie above its pool top, which is restored too).
-// Four rows per thread: one 32-bit read of their flags.
-template <int C>
-__global__ void k_restore_dirty(DevGraph<C> cur, DevGraph<C> snap) {
-  const uint32_t n = cur.n;
-  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; 4ull * q < n;
-       q += gridDim.x * blockDim.x) {
-    const uint32_t f = reinterpret_cast<const uint32_t*>(cur.dirty)[q];
-    if (f == 0) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t u = 4 * q + j;
-      if (((f >> (8 * j)) & 0xFFu) == 0 || u >= n) continue;
-      const Slab<C> s = snap.slab[u];
-      cur.slab[u] = s;
-      cur.cap[u] = snap.cap[u];
-      if (s.ext != kInline)
-        for (uint32_t i = 0; i < s.deg; ++i) {
-          cur.pool_id[s.ext + i] = snap.pool_id[s.ext + i];
-          cur.pool_w[s.ext + i] = snap.pool_w[s.ext + i];
-        }
-    }
-    reinterpret_cast<uint32_t*>(cur.dirty)[q] = 0;
-  }
-}
-
 }  // namespace
-
-template <int C>
-void GraphStore<C>::clear_dirty(cudaStream_t st) {
-  cuda_check(cudaMemsetAsync(v_.dirty, 0, std::max<size_t>(v_.n, 4) + 4, st), "row flags");
-  dirty_valid_ = true;
-}
-
-template <int C>
-bool GraphStore<C>::restore_dirty_from(const GraphStore& snap, cudaStream_t st) {
-  if (!dirty_valid_ || !allocated() || v_.n != snap.v_.n || v_.pool_cap < snap.v_.pool_cap)
-    return false;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t words = (static_cast<uint64_t>(v_.n) + 3) / 4;
-  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>(grid_for(words), 8ull * sms));
-  k_restore_dirty<C><<<blocks, 256, 0, st>>>(v_, snap.v_);
-  cuda_check(cudaGetLastError(), "k_restore_dirty");
-  cuda_check(cudaMemcpyAsync(counters_, snap.counters_, 2 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToDevice, st), "restore counters");
-  return true;
-}
 
 template <int C>
 GraphStore<C>::~GraphStore() {
@@ -155,11 +103,9 @@ void GraphStore<C>::release() {
   cudaFree(v_.cap);
   cudaFree(v_.pool_id);
   cudaFree(v_.pool_w);
-  cudaFree(v_.dirty);
   cudaFree(counters_);
   v_ = DevGraph<C>{};
   counters_ = nullptr;
-  dirty_valid_ = false;
 }
 
 template <int C>
@@ -172,11 +118,8 @@ void GraphStore<C>::allocate(uint32_t n, uint64_t pool_cap) {
   cuda_check(cudaMalloc(&v_.pool_id, sizeof(uint32_t) * pool_cap), "alloc pool ids");
   cuda_check(cudaMalloc(&v_.pool_w, sizeof(double) * pool_cap), "alloc pool weights");
   cuda_check(cudaMalloc(&counters_, 2 * sizeof(unsigned long long)), "alloc counters");
-  cuda_check(cudaMalloc(&v_.dirty, std::max<size_t>(n, 4) + 4), "alloc row flags");
-  cuda_check(cudaMemset(v_.dirty, 0, std::max<size_t>(n, 4) + 4), "row flags");
   v_.pool_top = counters_;
   v_.edges = counters_ + 1;
-  dirty_valid_ = false;
 }
 
 template <int C>

@@ -34,12 +34,6 @@ class GraphStore {
   // Row-order export to host buffers (row_ptr[n+1], ids/w[2m]).
   uint64_t export_rows(uint64_t* row_ptr, uint32_t* ids, double* w, uint64_t capacity,
                        cudaStream_t st);
-  // Starts tracking changed rows from here (the state a snapshot copied).
-  void clear_dirty(cudaStream_t st);
-  // Makes *this equal to `snap` again by copying back only the rows changed
-  // since clear_dirty() (slab, capacity, pool block of the snapshot's row)
-  // and the counters; false (nothing done) when tracking was reset since.
-  bool restore_dirty_from(const GraphStore& snap, cudaStream_t st);
   // Guarantees at least `free_entries` unused pool entries (grows the pool,
   // preserving indices). `top` is the last known pool_top.
   void ensure_pool(uint64_t top, uint64_t free_entries, cudaStream_t st);
@@ -56,7 +50,6 @@ class GraphStore {
   void allocate(uint32_t n, uint64_t pool_cap);
   DevGraph<C> v_{};
   unsigned long long* counters_ = nullptr;  // [0] pool_top, [1] edges
-  bool dirty_valid_ = false;                // flags cover every change since clear_dirty
 };
 
 // Initial sparsifier on the device (init_sparsifier.cu): G as a host CSR in

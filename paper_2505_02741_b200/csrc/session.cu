@@ -2084,10 +2084,6 @@ int dyg_session_snapshot(dyg_session* s) {
     check(cudaSetDevice(s->device), "set device");
     s->G_snap.copy_from(s->G, s->stream);
     s->H_snap.copy_from(s->H, s->stream);
-    // From here the live graphs flag every row they change, so a restore
-    // copies back only those (GraphStore::restore_dirty_from).
-    s->G.clear_dirty(s->stream);
-    s->H.clear_dirty(s->stream);
     check(cudaStreamSynchronize(s->stream), "snapshot");
     s->counter_snap = s->counter;
     s->g_edges_snap = s->g_edges;
@@ -2105,16 +2101,8 @@ int dyg_session_restore(dyg_session* s) {
     if (!s->have_snap) fail(DYG_ERR_USAGE, "no snapshot taken");
     s->last_t1 = 0;  // the restore is not a gap between batches of one replay
     check(cudaSetDevice(s->device), "set device");
-    // Rows changed since the snapshot only (~40 % of C5's rows after its
-    // stream); a full copy when the flags no longer cover every change.
-    if (!s->G.restore_dirty_from(s->G_snap, s->stream)) {
-      s->G.copy_from(s->G_snap, s->stream);
-      s->G.clear_dirty(s->stream);
-    }
-    if (!s->H.restore_dirty_from(s->H_snap, s->stream)) {
-      s->H.copy_from(s->H_snap, s->stream);
-      s->H.clear_dirty(s->stream);
-    }
+    s->G.copy_from(s->G_snap, s->stream);
+    s->H.copy_from(s->H_snap, s->stream);
     s->stats.kernel_launches += 2;
     s->counter = s->counter_snap;
     s->g_edges = s->g_edges_snap;
