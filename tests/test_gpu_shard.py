@@ -217,3 +217,47 @@ def test_peer_exchange_world1_equals_reference(oracle, dyg, cfg):
         st.shard_peer_range_begin(0, nb)
     assert e.value.kind == dyg.ErrorKind.Usage and "exceeds the exchange area" in str(e.value)
     st.close()
+
+
+def test_sharded_replay_python_paths_world1(oracle, dyg, tmp_path):
+    """parallel.ShardedReplay's per-batch entry points in one process (a gloo
+    world of one rank): replay_events (host events), replay_uploaded and
+    replay_uploaded_range over the collective transport, and
+    replay_uploaded_range over the peer transport -- all equal to the
+    reference replay."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_02741_b200.parallel import ShardedReplay
+
+    c = O.CONFIGS["C2"]
+    g, h, s = O.build_config(oracle, c)
+    nb = s.batch_count
+    ost = oracle.state(g, h, K=c.K, T=c.T, s=c.s, seed=c.walk_seed)
+    ref = [ost.replay_batch(s, b) for b in range(nb)]
+    opts = dyg.SparsifierOptions(dyg.WalkConfig(c.K, c.T, c.s, c.walk_seed), True, False)
+    dist.init_process_group("gloo", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    try:
+        torch.cuda.set_stream(torch.cuda.Stream())
+        for mode in ("events", "uploaded", "range", "peer"):
+            st = dyg.SparsifierState(to_dyg(dyg, g), to_dyg(dyg, h), opts)
+            sh = ShardedReplay(st, 0, 1, transport="peer" if mode == "peer" else "collective")
+            stream = dyg.UpdateStream(s.events(), nb)
+            if mode == "events":
+                got = [sh.replay_events(*stream.batch(b), b) for b in range(nb)]
+            else:
+                sh.upload(stream)
+                if mode == "uploaded":
+                    got = [sh.replay_uploaded(b) for b in range(nb)]
+                else:
+                    got = sh.replay_uploaded_range(0, nb)
+            for b in range(nb):
+                for f in O.REPORT_EXACT:
+                    assert ref[b][f] == getattr(got[b], f), (mode, b, f)
+            assert same_rows(ost.graph().export(), st.rows(0)), mode
+            assert same_rows(ost.sparsifier().export(), st.rows(1)), mode
+            sh.close()
+            st.close()
+    finally:
+        torch.cuda.set_stream(torch.cuda.default_stream())
+        dist.destroy_process_group()
