@@ -232,6 +232,29 @@ def load_traffic(kernel: str):
         return None
 
 
+def _spin(n: int) -> int:
+    x = 0
+    for i in range(n):
+        x ^= i * 2654435761 & 0xFFFF
+    return x
+
+
+def effective_parallelism(workers: int, n: int = 3_000_000) -> float:
+    """how many of the host's threads really run in parallel
+    (vCPUs can be oversubscribed): the same busy loop on 1 and on `workers`
+    processes, t1 * workers / t_workers."""
+    from concurrent.futures import ProcessPoolExecutor
+    with ProcessPoolExecutor(max_workers=workers) as ex:
+        list(ex.map(_spin, [1000] * workers))  # start the workers
+        t = time.perf_counter()
+        list(ex.map(_spin, [n]))
+        t1 = time.perf_counter() - t
+        t = time.perf_counter()
+        list(ex.map(_spin, [n] * workers))
+        tw = time.perf_counter() - t
+    return t1 * workers / tw
+
+
 def cpu_baseline(cfg: str, product_inputs: dict | None = None, scale: int = 1):
     """The reference CPU implementation on this host: the WHOLE stream of the
     config replayed (deferred mode, SparsifierState::replay_batch per batch)
@@ -276,6 +299,7 @@ def cpu_baseline(cfg: str, product_inputs: dict | None = None, scale: int = 1):
                                    "edge_updates_per_s": v[0] / v[1]}
                                for k, v in split.items() if v[2]},
             "cpu_model": cpu_model, "nproc": os.cpu_count(),
+            "effective_parallelism": round(effective_parallelism(cores), 2),
             "inputs": ref_inputs, "inputs_match_product": product_inputs is not None,
             "sample": (f"{cfg}: all {s.batch_count} batches ({events} events) replayed from the "
                        f"initial state in {wall:.2f} s (setup {setup:.1f} s excluded), "
