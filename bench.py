@@ -273,6 +273,27 @@ def cpu_baseline(cfg: str, product_inputs: dict | None = None, scale: int = 1):
     ref_inputs = inputs_digest(g.export(), h.export(), ev)
     if product_inputs is not None and ref_inputs != product_inputs:
         raise RuntimeError(f"inputs differ: product {product_inputs} reference {ref_inputs}")
+    # the reference's walk-only run_batch time on batch 0's
+    # reach queries (built as replay_batch_deferred does, sparsifier.cpp:
+    # 433-445: w_pq = G.w(u, v) + w -- the generator's insertions are
+    # non-edges -- and a query only when both endpoints have H edges).
+    walk_only = None
+    try:
+        from oracle import oracle as _O
+        hrp = np.asarray(h.export()[0]).astype(np.int64)
+        hdeg = np.diff(hrp)
+        b0 = ev[(ev["batch_index"] == 0) & (ev["kind"] == 0)]
+        keep = (hdeg[b0["u"].astype(np.int64)] > 0) & (hdeg[b0["v"].astype(np.int64)] > 0)
+        q = np.zeros(int(keep.sum()), _O.QUERY_DTYPE)
+        q["kind"], q["p"], q["q"] = 0, b0["u"][keep], b0["v"][keep]
+        q["w_pq"], q["update_id"] = b0["weight"][keep], np.nonzero(keep)[0]
+        t = time.perf_counter()
+        orc.run_batch(h, q, K_BUDGET, T_CAP, WALKERS, WALK_SEED, workers=cores)
+        dt = time.perf_counter() - t
+        walk_only = {"batch": 0, "queries": len(q), "s": round(dt, 3),
+                     "queries_per_s": len(q) / dt}
+    except Exception as e:  # noqa: BLE001 -- a diagnostic only
+        walk_only = {"unavailable": str(e)[:120]}
     st = orc.state(g, h, K=K_BUDGET, T=T_CAP, s=WALKERS, seed=WALK_SEED)
     split = {"insertion": [0, 0.0, 0], "deletion": [0, 0.0, 0]}
     for b in range(s.batch_count):
@@ -300,6 +321,7 @@ def cpu_baseline(cfg: str, product_inputs: dict | None = None, scale: int = 1):
                                for k, v in split.items() if v[2]},
             "cpu_model": cpu_model, "nproc": os.cpu_count(),
             "effective_parallelism": round(effective_parallelism(cores), 2),
+            "walk_only_run_batch": walk_only,
             "inputs": ref_inputs, "inputs_match_product": product_inputs is not None,
             "sample": (f"{cfg}: all {s.batch_count} batches ({events} events) replayed from the "
                        f"initial state in {wall:.2f} s (setup {setup:.1f} s excluded), "
