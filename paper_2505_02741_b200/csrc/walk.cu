@@ -265,6 +265,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   // A drained warp with at most this many live walkers finishes them
   // lane by lane (the thin tail below).
   constexpr uint32_t kTailLanes = kMinPath ? 16u : 32u;
+  // A small min-path batch (fewer walkers than ~4 warps per SM: the memory
+  // system is idle) gains nothing from the cooperative gather: its warps go
+  // lane by lane as soon as the queue is drained.
   extern __shared__ __align__(16) unsigned char walk_smem[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   uint4* stage0 = reinterpret_cast<uint4*>(wbase);
   ChunkSmem& cs = *reinterpret_cast<ChunkSmem*>(wbase + L::kStageBytes);
   const uint32_t total_work = *nq_dev * P.s;
+  const uint32_t tail_lanes = (kMinPath && total_work <= 4u * 32u * 148u) ? 32u : kTailLanes;
   if (threadIdx.x == 0) atomicMin(&ctr->t_start, global_ns());  // block start stamps
   uint32_t chunk_base = 0, chunk_pos = 32, chunk_end = 32;
   bool drained = false;
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     // warp-wide gather, shuffles or shared staging on the dependent chain.
     // (With many live lanes the cooperative gather stays: lane-private row
     // loads cost one L1 wavefront per 16 B chunk.)
-    if (drained && static_cast<uint32_t>(__popc(__ballot_sync(kFull, w.has))) <= kTailLanes)
+    if (drained && static_cast<uint32_t>(__popc(__ballot_sync(kFull, w.has))) <= tail_lanes)
       break;
     // This step's uniform draw (draw k = steps + 1) does not depend on the
     // row: computed while the fetch is in flight. The shared store pins it
