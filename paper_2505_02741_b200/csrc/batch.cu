@@ -1786,7 +1786,7 @@ __global__ void k_pack_min(MinOut m, const uint32_t* n_dev, uint32_t slots, uint
     h->has_path = have ? m.has_path[lo + i] : 0;
     h->path_len = len;
     h->steps = have ? m.steps[lo + i] : 0ull;
-    h->resistance = have ? m.resistance[lo + i] : 0.0;
+    h->resistance = 0.0;  // unused by the commit (K3 skips it in replays)
   }
   const uint32_t* src = m.paths + static_cast<uint64_t>(lo + i) * (T + 1ull);
   for (uint32_t j = threadIdx.x; j < T + 1; j += blockDim.x) path[j] = (j < len) ? src[j] : 0u;
@@ -1831,7 +1831,6 @@ __global__ void k_unpack_min(MinOut m, const uint32_t* nq_dev, int world, uint32
     m.has_path[q] = h->has_path;
     m.path_len[q] = h->path_len;
     m.steps[q] = h->steps;
-    m.resistance[q] = h->resistance;
   }
   uint32_t* dst = m.paths + static_cast<uint64_t>(q) * (T + 1ull);
   for (uint32_t j = threadIdx.x; j < h->path_len; j += blockDim.x) dst[j] = path[j];
@@ -1883,7 +1882,7 @@ __global__ void k_pack_min_peer(MinOut m, const uint32_t* n_dev, uint32_t slots,
       h->has_path = have ? m.has_path[i] : 0;
       h->path_len = len;
       h->steps = have ? m.steps[i] : 0ull;
-      h->resistance = have ? m.resistance[i] : 0.0;
+      h->resistance = 0.0;  // unused by the commit (K3 skips it in replays)
     }
     const uint32_t* src = m.paths + static_cast<uint64_t>(i) * (T + 1ull);
     for (uint32_t j = lane; j < len; j += 32) path[j] = src[j];
@@ -1956,7 +1955,6 @@ __global__ void k_unpack_min_peer(MinOut m, const uint32_t* nq_dev, uint32_t T, 
       m.has_path[q] = h->has_path;
       m.path_len[q] = len;
       m.steps[q] = h->steps;
-      m.resistance[q] = h->resistance;
     }
     uint32_t* dst = m.paths + static_cast<uint64_t>(q) * (T + 1ull);
     for (uint32_t j = lane; j < len; j += 32) dst[j] = path[j];

@@ -617,8 +617,9 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     WalkParams Pd = P;
     Pd.K = std::numeric_limits<double>::infinity();  // sparsifier.cpp:458-459
     const uint64_t T1 = static_cast<uint64_t>(o.T) + 1;
+    // No resistance: the commit uses the recovered path alone (:503-514).
     MinOut mo{b.mout.has_path + lo_m, b.mout.path_len + lo_m, b.mout.steps + lo_m,
-              b.mout.resistance + lo_m, b.mout.paths + lo_m * T1, &b.ctl->t_mp_end};
+              nullptr, b.mout.paths + lo_m * T1, &b.ctl->t_mp_end};
     // k_scatter reset the work counter; a mixed batch's reach walk used it,
     // and a shard range walk may follow another range's walk.
     const bool reset = !full || (p.n_ins > 0 && o.filtering);

@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
     if (lane == 0) {
       out.has_path[qi] = 0;
       out.path_len[qi] = 0;
-      out.resistance[qi] = 0.0;
+      if (out.resistance) out.resistance[qi] = 0.0;
       if (out.t_end) atomicMax(out.t_end, global_ns());
     }
     return;
@@ -600,16 +600,22 @@ __global__ void __launch_bounds__(256) k_minpath_finish(DevGraph<C> g,
   }
   uint32_t* gerased = out.paths + static_cast<uint64_t>(qi) * T1;
   for (uint32_t i = lane; i < elen; i += 32) gerased[i] = erased[i];
-  // resistance = sum of 1/w over the erased path in path order (walk.cpp:140-143)
-  for (uint32_t i = lane; i + 1 < elen; i += 32)
-    rv[i] = __drcp_rn(edge_weight(g, erased[i], erased[i + 1]));
-  __syncwarp();
+  // resistance = sum of 1/w over the erased path in path order
+  // (walk.cpp:140-143) -- for run_batch's results; the replay's commit uses
+  // only the path (sparsifier.cpp:503-514) and passes no resistance array.
+  if (out.resistance) {
+    for (uint32_t i = lane; i + 1 < elen; i += 32)
+      rv[i] = __drcp_rn(edge_weight(g, erased[i], erased[i + 1]));
+    __syncwarp();
+  }
   if (lane == 0) {
-    double r = 0.0;
-    for (uint32_t i = 0; i + 1 < elen; ++i) r = __dadd_rn(r, rv[i]);
+    if (out.resistance) {
+      double r = 0.0;
+      for (uint32_t i = 0; i + 1 < elen; ++i) r = __dadd_rn(r, rv[i]);
+      out.resistance[qi] = r;
+    }
     out.has_path[qi] = 1;
     out.path_len[qi] = elen;
-    out.resistance[qi] = r;
     if (out.t_end) atomicMax(out.t_end, global_ns());
   }
 }
