@@ -291,6 +291,12 @@ int dyg_session_options(const dyg_session* s, dyg_options* out);
 int dyg_session_load(const char* path, int device, dyg_session** out);
 
 int dyg_session_stats(const dyg_session* s, dyg_stats* out);
+/* Per-step walk statistics (dyg_stats reach_steps, minpath_steps,
+ * *_row_bytes, *_tail_row_bytes): counted by an instrumented variant of the
+ * walk kernels, ~6 % slower than the default one; off by default (those
+ * fields then stay 0; the walk durations and drain stamps are always
+ * recorded). The walks themselves -- and every result -- are identical. */
+int dyg_session_set_walk_counters(dyg_session* s, int on);
 int dyg_session_reset_stats(dyg_session* s);
 
 /* build_initial_sparsifier (sparsifier.cpp:105-159) on `device`, bit-identical

@@ -125,6 +125,7 @@ def lib() -> C.CDLL:
         "dyg_session_snapshot": (i32, [vp]),
         "dyg_session_restore": (i32, [vp]),
         "dyg_session_save": (i32, [vp, C.c_char_p]),
+        "dyg_session_set_walk_counters": (i32, [vp, i32]),
         "dyg_generate_stream": (i32, [C.POINTER(Csr), dbl, dbl, u32, u64, i32, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]),
         "dyg_shard_peer_create": (i32, [vp, i32, u64, u64, pvp, C.POINTER(sz), vp]),
         "dyg_ipc_open": (i32, [vp, i32, pvp]),

@@ -121,6 +121,7 @@ struct WalkOpts {
   // w_pq <= split_wpq (the budget lets them walk longest) get the low slots and
   // are walked first, the rest take slots from the top of the buffer; 0 = off.
   double split_wpq;
+  int count;  // instrumented walk kernels (per-step statistics), dyg_session_set_walk_counters
 };
 
 // Device buffers of one batch (sized by the session; grown on demand).

@@ -224,6 +224,7 @@ struct dyg_session {
   bool reach_split = true;         // DYG_REACH_SPLIT=0: reach walks in slot order
   bool keep_shadow = true;         // DYG_KEEP_SHADOW=0: deletion commit restores G
   bool flow_balance = true;        // DYG_FLOW_BALANCE=0: static event ownership
+  bool walk_counters = false;      // dyg_session_set_walk_counters: instrumented walks
   unsigned long long last_t1 = 0;  // end stamp of the previous batch (stats)
   double mean_inv_w = 1.0;         // mean 1/w over G's edges (session creation)
 };
@@ -394,6 +395,7 @@ WalkOpts walk_opts(const dyg_session* s) {
   o.split_wpq = (s->reach_split && o.filtering && o.T > 0)
                     ? o.K / (0.8 * static_cast<double>(o.T) * s->mean_inv_w) : 0.0;
   o.keep_shadow = s->keep_shadow ? 1 : 0;
+  o.count = s->walk_counters ? 1 : 0;
   o.flow_balance = s->flow_balance ? 1 : 0;
   return o;
 }
@@ -567,7 +569,8 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
-  const WalkParams P = make_walk_params(o.K, o.T, o.s, o.seed);
+  WalkParams P = make_walk_params(o.K, o.T, o.s, o.seed);
+  P.count = static_cast<uint32_t>(o.count);
   const uint32_t* cnt_r = &b.ctl->nq_reach;
   const uint32_t* cnt_m = &b.ctl->nq_min;
   uint32_t max_r = p.n_ins, max_m = p.n_del;
@@ -2248,6 +2251,14 @@ int dyg_session_load(const char* path, int device, dyg_session** out) {
     *out = s;
   });
   return rc;
+}
+
+int dyg_session_set_walk_counters(dyg_session* s, int on) {
+  return guarded([&] {
+    require_settled(s);
+    if (s == nullptr) fail(DYG_ERR_USAGE, "null session");
+    s->walk_counters = on != 0;
+  });
 }
 
 int dyg_session_stats(const dyg_session* s, dyg_stats* out) {

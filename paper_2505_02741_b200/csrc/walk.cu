@@ -11,6 +11,10 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "walk.cuh"
 
 namespace dyg {
@@ -256,7 +260,7 @@ __device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row
   cp_async_commit();
 }
 
-template <int C, bool kMinPath, int kWarps, int kMinBlocks>
+template <int C, bool kMinPath, int kWarps, int kMinBlocks, bool kCount>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_walk(DevGraph<C> g, const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
            const uint32_t* __restrict__ nq_dev, WalkParams P, ReachOut rout, MinScratch S,
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   auto row_of = [&](const Slot& w) { return (w.has && w.steps < P.T) ? w.cur : kNoVertex; };
   // A walker ended with `term`: its outputs (walk.cpp:82-98 / :119-134).
   auto finish = [&](Slot& w, uint32_t term) {
-    my_steps += w.steps;
+    if (kCount) my_steps += w.steps;
     if (kMinPath) {
       // The trace's last, partial sector: entries steps-r+1 .. steps.
       const uint32_t r = (w.steps + 1) & 7u;
@@ -435,8 +439,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         uint32_t deg = 0;
         const bool ok =
             walk_step(g, stage0 + lane * Gather<C>::kStride, w.cur, w.prev, u, next, ew, deg);
-        my_sectors += step_sectors(deg);
-        if (early) my_tail += step_sectors(deg);
+        if (kCount) {
+          my_sectors += step_sectors(deg);
+          if (early) my_tail += step_sectors(deg);
+        }
         if (!ok) term = kDeadEnd;
       }
     }
@@ -483,8 +489,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
               r.s.ext == kInline
                   ? sample_inline<C>(r.s, w.prev, u, next, ew)
                   : sample_pool(g.pool_id + r.s.ext, g.pool_w + r.s.ext, deg, w.prev, u, next, ew);
-          my_sectors += step_sectors(deg);
-          my_tail += step_sectors(deg);
+          if (kCount) {
+            my_sectors += step_sectors(deg);
+            my_tail += step_sectors(deg);
+          }
           if (!ok) term = kDeadEnd;
         }
         if (term == 0xFFFFFFFFu) {
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     __syncwarp();
   }
   cp_async_wait<0>();
-  add_counters(ctr, my_steps, my_sectors, my_tail);
+  if (kCount) add_counters(ctr, my_steps, my_sectors, my_tail);
   if (lane == 0) {
     atomicMax(&ctr->t_end, global_ns());
   }
@@ -638,15 +646,19 @@ unsigned persistent_blocks(K kernel, uint64_t work, int threads, size_t smem) {
 // same process needs its own opt-in).
 template <typename K>
 bool smem_opt_in(K kernel, size_t bytes) {
-  constexpr int kMaxDev = 64;
-  static size_t granted[kMaxDev] = {};
+  // Keyed by (kernel, device): instantiations of one template share a type.
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return false;
-  if (granted[dev] >= bytes) return true;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const std::pair<const void*, int> key{reinterpret_cast<const void*>(kernel), dev};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = granted.find(key);
+  if (it != granted.end() && it->second >= bytes) return true;
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(bytes)) != cudaSuccess)
     return false;
-  granted[dev] = bytes;
+  granted[key] = bytes;
   return true;
 }
 
@@ -661,7 +673,8 @@ void launch_walk(const DevGraph<C>& g, const ReachQuery* rq, const MinQuery* mq,
                  MinScratch S, WalkCounters* ctr, unsigned int* work, cudaStream_t st) {
   constexpr int kWarps = 8;
   constexpr int kMinBlocks = kMinPath ? 2 : 4;
-  auto k = k_walk<C, kMinPath, kWarps, kMinBlocks>;
+  auto k = P.count ? k_walk<C, kMinPath, kWarps, kMinBlocks, true>
+                   : k_walk<C, kMinPath, kWarps, kMinBlocks, false>;
   constexpr size_t smem = WalkLayout<C, kWarps>::kBytes;
   smem_opt_in(k, smem);
   k<<<persistent_blocks(k, threads, kWarps * 32, smem), kWarps * 32, smem, st>>>(

@@ -22,6 +22,10 @@ struct WalkParams {
   uint32_t s;        // walkers per query
   uint64_t seed;     // global seed
   uint32_t s_shift;  // log2(s) when s is a power of two, else kNoShift
+  // Per-step statistics (walker steps, algorithmic bytes, tail bytes into
+  // WalkCounters): an instrumented kernel variant, ~6 % slower (registers);
+  // the stamps (start, drain, end) are always taken.
+  uint32_t count;
 };
 
 inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t seed) {
@@ -30,7 +34,7 @@ inline WalkParams make_walk_params(double K, uint32_t T, uint32_t s, uint64_t se
     sh = 0;
     while ((1u << sh) != s) ++sh;
   }
-  return WalkParams{K, T, s, seed, sh};
+  return WalkParams{K, T, s, seed, sh, 0};
 }
 
 // Entries per raw min-path trace: T + 1 rounded up to whole 32 B sectors, so

@@ -223,13 +223,18 @@ def test_uploaded_stream_and_snapshot_restore(oracle, dyg):
     st.restore()
     assert st.update_counter == 0
     st.upload_stream(stream)
+    st.set_walk_counters(True)  # the instrumented walks: same results, per-step stats
+    st.reset_stats()
     b = [st.replay_uploaded(k) for k in range(s.batch_count)]
     for x, y in zip(a, b):
         for f in O.REPORT_EXACT:
             assert getattr(x, f) == getattr(y, f)
     assert same_rows(rows_a[0], st.rows(0)) and same_rows(rows_a[1], st.rows(1))
     stats = st.stats()
-    assert stats["reach_steps"] > 0 and stats["kernel_launches"] > 0
+    assert stats["kernel_launches"] > 0
+    # every walker step is counted once: the reports' total
+    assert stats["reach_steps"] + stats["minpath_steps"] == sum(r.walker_steps for r in b)
+    assert stats["reach_row_bytes"] >= 32 * stats["reach_steps"] > 0
 
 
 def test_session_ctor_checks(dyg):
