@@ -1385,7 +1385,6 @@ __device__ __forceinline__ void scatter_event(const DevEvent& e, uint32_t k, uns
     b.rq[ri] = q;
     b.rout.reached[ri] = 0;  // the reach walk's OR / SUM / MIN start here
     b.rout.steps[ri] = 0;
-    b.rout.best_bits[ri] = 0x7FF0000000000000ull;
     s = ri;
   } else if (f >> 32) {
     MinQuery q;
@@ -1614,7 +1613,6 @@ __global__ void k_scatter(const DevEvent* __restrict__ ev, uint32_t nb, uint64_t
     // steps = SUM, best = MIN).
     b.rout.reached[ri] = 0;
     b.rout.steps[ri] = 0;
-    b.rout.best_bits[ri] = 0x7FF0000000000000ull;
     s = ri;
   } else if (f >> 32) {
     MinQuery q;

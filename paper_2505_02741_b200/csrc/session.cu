@@ -605,7 +605,8 @@ void phase_walk(dyg_session* s, Pending& p, bool full, uint32_t lo_r, uint32_t n
     check(cudaEventRecord(s->ev_fork, s->stream), "fork");
   }
   if (p.n_ins > 0 && o.filtering && max_r > 0) {
-    ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, b.rout.best_bits + lo_r, nullptr, 0};
+    // No best_bits: the commit reads `reached` and `steps` alone.
+    ReachOut ro{b.rout.reached + lo_r, b.rout.steps + lo_r, nullptr, nullptr, 0};
     if (full && o.split_wpq > 0.0 && p.n_del == 0 && o.single_pass) {
       ro.nq_long = &b.ctl->nq_long;
       ro.cap = b.q_cap;

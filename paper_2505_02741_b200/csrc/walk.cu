@@ -368,8 +368,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       atomicAdd(&rout.steps[qi], static_cast<unsigned long long>(w.steps));
       if (term == kReached) {
         atomicOr(&rout.reached[qi], 1u);
-        atomicMin(&rout.best_bits[qi],
-                  static_cast<unsigned long long>(__double_as_longlong(w.acc)));
+        // best_estimate is run_batch's; a replay's commit reads `reached`
+        // alone (sparsifier.cpp:228-233) and passes no best_bits.
+        if (rout.best_bits)
+          atomicMin(&rout.best_bits[qi],
+                    static_cast<unsigned long long>(__double_as_longlong(w.acc)));
       }
     }
     w.has = false;
@@ -521,14 +524,14 @@ __global__ void k_reach_init(ReachOut out, uint32_t n, unsigned int* work) {
   if (i >= n) return;
   out.reached[i] = 0;
   out.steps[i] = 0;
-  out.best_bits[i] = 0x7FF0000000000000ull;
+  if (out.best_bits) out.best_bits[i] = 0x7FF0000000000000ull;
 }
 
 // Reach outputs of queries that found no walker keep +inf in best_bits;
 // the reference leaves best_estimate = 0 when not reached (walk.hpp:31).
 __global__ void k_reach_fix(ReachOut out, const uint32_t* __restrict__ nq_dev) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < *nq_dev && !out.reached[i]) out.best_bits[i] = 0ull;
+  if (out.best_bits && i < *nq_dev && !out.reached[i]) out.best_bits[i] = 0ull;
 }
 
 // K3: one warp per min-path query: winner, loop erasure, resistance. The
