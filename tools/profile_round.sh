@@ -19,8 +19,8 @@ cap() {  # REGEX SKIP NAME
     -o gpurun_out/prof_$3_$TAG -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
   echo "$3 exit $?"
 }
-cap k_walk 6 k1
-cap k_walk 14 k2
+cap k_walk 26 k1   # the 2nd replay (the 1st runs the instrumented kernels)
+cap k_walk 34 k2
 cap k_del_flow 6 flow
 python tools/ncu_summary.py gpurun_out/prof_k1_$TAG.ncu-rep gpurun_out/prof_k2_$TAG.ncu-rep \
   gpurun_out/prof_flow_$TAG.ncu-rep > gpurun_out/ncu_summary_$TAG.txt 2>&1
