@@ -2368,7 +2368,7 @@ void shard_begin_impl(dyg_session* s, const dyg_event* events, const uint64_t* p
       // three device segments per batch -- prepare, walk, commit -- each
       // as one graph, like the single-GPU path's one graph per batch).
       prepare_bind(s, p);
-      uint64_t key = session_fingerprint(s, 3);
+      uint64_t key = session_fingerprint(s, 7);
       const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
                                 p.nb, p.n_ins, p.n_del};
       key = fnv(key, shape, sizeof shape);
@@ -2782,6 +2782,97 @@ void peer_range_begin(dyg_session* s, uint32_t first, uint32_t count) {
   s->px_first = first;
 }
 
+// The same batches while the stream is still being uploaded batch by batch
+// (dyg_stream_upload_batches right before, as replay(stream) does): one
+// graph per batch, each enqueued as soon as its own upload has landed, so
+// the upload overlaps the earlier batches' work (run_stream's pipeline).
+void peer_range_pipelined(dyg_session* s, uint32_t first, uint32_t count) {
+  const uint32_t world = s->px_world;
+  const int rank = s->px.rank;
+  uint32_t max_nb = 1;
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t b = first + i;
+    if (b < s->batch_cnt.size()) max_nb = std::max<uint32_t>(max_nb, static_cast<uint32_t>(s->batch_cnt[b]));
+  }
+  ensure_batch(s, max_nb, 0);
+  if (s->ctl_cap < count) {
+    dev_free(s->d_ctls);
+    if (s->h_ctls) cudaFreeHost(s->h_ctls);
+    s->h_ctls = nullptr;
+    dev_alloc(&s->d_ctls, count, "batch control blocks");
+    check(cudaMemset(s->d_ctls, 0, sizeof(BatchCtl) * count), "batch control blocks");
+    check(cudaMallocHost(reinterpret_cast<void**>(&s->h_ctls), sizeof(BatchCtl) * count),
+          "pinned control blocks");
+    s->ctl_cap = count;
+  }
+  std::vector<Pending> ps(count);
+  const auto wall0 = std::chrono::steady_clock::now();
+  reset_abort(s);
+  uint64_t counter = s->counter, sum_ins = 0, sum_del = 0;
+  const uint32_t T = s->opt.walk.step_cap;
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint32_t b = first + i;
+    Pending& p = ps[i];
+    p.batch = b;
+    p.wall0 = wall0;
+    p.dctl = s->d_ctls + i;
+    p.hctl = s->h_ctls + i;
+    p.hdec = &s->h_counts[2];
+    p.counter_base = counter;
+    p.shard = true;
+    if (b >= s->batch_cnt.size() || s->batch_cnt[b] == 0) continue;
+    settle_upload(s, b);  // this batch's upload and kind counts only
+    const uint64_t off = s->batch_off[b];
+    p.dev = s->d_stream + off;
+    p.host = uploaded_host(s, off);
+    p.pos = uploaded_pos(s, off);
+    p.pos_base = off;
+    p.nb = static_cast<uint32_t>(s->batch_cnt[b]);
+    p.n_ins = static_cast<uint32_t>(s->batch_ins[b]);
+    p.n_del = static_cast<uint32_t>(s->batch_del[b]);
+    const uint32_t sl_r = (p.n_ins + world - 1) / world, sl_m = (p.n_del + world - 1) / world;
+    if (sl_r > s->px_slots_r || sl_m > s->px_slots_m) {
+      check(cudaStreamSynchronize(s->stream), "peer range");  // drain what is enqueued
+      fail(DYG_ERR_USAGE, "batch " + std::to_string(b) +
+                              " exceeds the exchange area (dyg_shard_peer_create maxima)");
+    }
+    sum_ins += p.n_ins;
+    sum_del += p.n_del;
+    ensure_pools(s, sum_ins, sum_del);
+    if (p.n_del > s->nd_cap ||
+        (p.n_del > 0 && (s->b.side_id == nullptr || s->side_cap < s->G.pool_capacity())))
+      check(cudaStreamSynchronize(s->stream), "buffer growth");
+    ensure_batch(s, p.nb, p.n_del);
+    if (p.n_del > 0) ensure_side_pool(s);
+    auto enqueue = [&] {
+      Pending q = p;
+      phase_prepare(s, q);
+      q.launches += launch_shard_range(s->b, rank, static_cast<int>(world), s->d_counts + 4, sl_r,
+                                       sl_m, s->stream);
+      phase_walk(s, q, false, 0, sl_r, 0, sl_m, /*fork_g=*/true);
+      q.launches += launch_pack_peer(s->b, s->d_counts + 4, sl_r, sl_m, T, s->px, s->stream);
+      q.launches += launch_unpack_peer(s->b, q.n_ins, q.n_del, sl_r, sl_m, T, s->px, s->stream);
+      commit_enqueue(s, q, false);
+      return q.launches;
+    };
+    prepare_bind(s, p);
+    uint64_t key = session_fingerprint(s, 8);
+    const uint64_t shape[] = {reinterpret_cast<uint64_t>(p.dev), reinterpret_cast<uint64_t>(p.dctl),
+                              p.nb, p.n_ins, p.n_del, world, static_cast<uint64_t>(rank)};
+    key = fnv(key, shape, sizeof shape);
+    key = fnv(key, &s->px, sizeof s->px);
+    p.launches = enqueue_captured(s, key, p.counter_base, enqueue);
+    counter += p.nb;
+  }
+  check(cudaMemcpyAsync(s->h_ctls, s->d_ctls, sizeof(BatchCtl) * count, cudaMemcpyDeviceToHost,
+                        s->stream), "ctl download");
+  // Every batch has been enqueued: settle the rest of the upload (the host
+  // waits while the GPU works), so later ranges take the one-graph path.
+  settle_upload(s, ~0u);
+  s->px_pending = std::move(ps);
+  s->px_first = first;
+}
+
 void peer_range_end(dyg_session* s, dyg_batch_report* out) {
   std::vector<Pending> ps;
   ps.swap(s->px_pending);
@@ -2805,7 +2896,10 @@ int dyg_shard_peer_range_begin(dyg_session* s, uint32_t first, uint32_t count) {
     if (count && static_cast<uint64_t>(first) + count > s->stream_batches && s->stream_batches > 0)
       fail(DYG_ERR_USAGE, "batch index out of range");
     check(cudaSetDevice(s->device), "set device");
-    settle_upload(s, ~0u);
+    if (s->up_pending) {  // the stream is still landing: pipeline behind it
+      peer_range_pipelined(s, first, count);
+      return;
+    }
     peer_range_begin(s, first, count);
   });
 }
