@@ -4,6 +4,7 @@
 #include <cooperative_groups.h>
 
 
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -983,7 +984,10 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 // Phases: emit records + per-row lists | ranks | apply (spin on done) |
 // reset the per-row heads and counters. A record-buffer overflow skips the
 // apply phase and leaves the batch to the round engine (flow_done = 0).
-__global__ void __launch_bounds__(256, 4) k_del_flow(CommitOp op, uint32_t nev, BatchDev b) {
+#ifndef DYG_FLOW_MINB
+#define DYG_FLOW_MINB 4
+#endif
+__global__ void __launch_bounds__(256, DYG_FLOW_MINB) k_del_flow(CommitOp op, uint32_t nev, BatchDev b) {
   constexpr unsigned kAll = 0xFFFFFFFFu;
   cg::grid_group grid = cg::this_grid();
   const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
@@ -1963,14 +1967,15 @@ __global__ void k_unpack_min_peer(MinOut m, const uint32_t* nq_dev, uint32_t T, 
 // kernel type: several cooperative kernels share a signature).
 template <typename K>
 int coop_blocks_for(K kernel) {
+  // Keyed by (kernel, device), like the walks' shared-memory opt-in.
   static std::mutex mu;
-  static std::unordered_map<const void*, int> cache;
-  std::lock_guard<std::mutex> lock(mu);
-  const void* key = reinterpret_cast<const void*>(kernel);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
+  static std::map<std::pair<const void*, int>, int> cache;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  const std::pair<const void*, int> key{reinterpret_cast<const void*>(kernel), dev};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
   const int blocks = sms * (per_sm > 0 ? per_sm : 1);

@@ -37,10 +37,16 @@ inline unsigned blocks_for(uint64_t threads, unsigned per_block) {
 // The slabs are staged in shared memory (row stride padded to 9 / 5 x 16 B,
 // conflict-free) and each lane reads its own back. Lanes pass kNoVertex when
 // they need no row this iteration.
+#ifndef DYG_H_GATHER_CHUNKS
+#define DYG_H_GATHER_CHUNKS 4
+#endif
+#ifndef DYG_POOL_UNCOND
+#define DYG_POOL_UNCOND 1
+#endif
 template <int C>
 struct Gather {
-  static constexpr int kChunks = C == kCapH ? 4 : 8;   // 16 B chunks fetched
-  static constexpr int kLanesPerRow = kChunks;
+  static constexpr int kChunks = C == kCapH ? DYG_H_GATHER_CHUNKS : 8;  // 16 B chunks fetched
+  static constexpr int kLanesPerRow = kChunks <= 4 ? 4 : 8;
   static constexpr int kRowsPerRound = 32 / kLanesPerRow;
   static constexpr int kRounds = 32 / kRowsPerRound;
   static constexpr int kStride = kChunks + 1;          // uint4 per staged row
@@ -118,8 +124,19 @@ __device__ __forceinline__ bool sample_pool(const uint32_t* __restrict__ ids,
                                             uint32_t prev, double u01, uint32_t& next,
                                             double& ew) {
   double total = 0.0;
+#if DYG_POOL_UNCOND
+  // Both loads of an entry issue together (the weight is not predicated on
+  // the id), so an unrolled group costs one round trip, not two.
+#pragma unroll 8
+  for (uint32_t i = 0; i < deg; ++i) {
+    const uint32_t id = __ldg(ids + i);
+    const double w = __ldg(ws + i);
+    if (id != prev) total = __dadd_rn(total, w);
+  }
+#else
   for (uint32_t i = 0; i < deg; ++i)
     if (__ldg(ids + i) != prev) total = __dadd_rn(total, __ldg(ws + i));
+#endif
   if (total <= 0.0) return false;
   const double target = __dmul_rn(u01, total);
   double cum = 0.0;
@@ -212,7 +229,6 @@ __device__ __forceinline__ void add_counters(WalkCounters* ctr, uint32_t steps32
 // raw trace and (acc, terminal, steps) for K3.
 struct Slot {
   uint32_t cur, prev, tgt, steps, widx, qi;
-  uint32_t tb[8];  // min-path: the last 8 trace entries (a shift register)
   bool has;
   uint64_t rng;
   double acc, wpq;
@@ -226,10 +242,19 @@ struct ChunkSmem {  // per warp: the current 32-item chunk
   double u[32];  // this step's draw, stored before the fetch wait (see k_walk)
 };
 
-template <int C, int kWarps>
+// Min-path walks: the last 8 trace entries of every lane (entry e in row
+// e & 7, lane-minor: conflict-free whatever the lanes' step counts), written
+// out a whole 32 B sector at a time. (A register shift register cost ~40
+// moves per step.)
+struct TraceRing {
+  uint32_t e[8][32];
+};
+
+template <int C, int kWarps, bool kMinPath = false>
 struct WalkLayout {
   static constexpr size_t kStageBytes = sizeof(uint4) * Gather<C>::kWarpWords;
-  static constexpr size_t kWarpBytes = kStageBytes + sizeof(ChunkSmem);
+  static constexpr size_t kWarpBytes =
+      kStageBytes + sizeof(ChunkSmem) + (kMinPath ? sizeof(TraceRing) : 0);
   static constexpr size_t kBytes = kWarps * kWarpBytes;
 };
 
@@ -254,7 +279,8 @@ __device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row
       const uint32_t u = __shfl_sync(kFull, my_row, r);
       const bool live = u != kNoVertex;
       const uint4* src = reinterpret_cast<const uint4*>(g.slab + (live ? u : 0)) + chunk;
-      cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
+      if (Gt::kChunks == Gt::kLanesPerRow || chunk < static_cast<uint32_t>(Gt::kChunks))
+        cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
     }
   }
   cp_async_commit();
@@ -265,7 +291,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_walk(DevGraph<C> g, const ReachQuery* __restrict__ rq, const MinQuery* __restrict__ mq,
            const uint32_t* __restrict__ nq_dev, WalkParams P, ReachOut rout, MinScratch S,
            WalkCounters* ctr, unsigned int* __restrict__ work) {
-  using L = WalkLayout<C, kWarps>;
+  using L = WalkLayout<C, kWarps, kMinPath>;
   // A drained warp with at most this many live walkers finishes them
   // lane by lane (the thin tail below).
   constexpr uint32_t kTailLanes = kMinPath ? 16u : 32u;
@@ -278,6 +304,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
   unsigned char* wbase = walk_smem + warp * L::kWarpBytes;
   uint4* stage0 = reinterpret_cast<uint4*>(wbase);
   ChunkSmem& cs = *reinterpret_cast<ChunkSmem*>(wbase + L::kStageBytes);
+  uint32_t* ring = kMinPath
+                       ? reinterpret_cast<TraceRing*>(wbase + L::kStageBytes + sizeof(ChunkSmem))->e[0] + lane
+                       : nullptr;  // ring[32 * j] = trace entry j (mod 8) of this lane
   const uint32_t total_work = *nq_dev * P.s;
   const uint32_t tail_lanes = (kMinPath && total_work <= 4u * 32u * 148u) ? 32u : kTailLanes;
   if (threadIdx.x == 0) atomicMin(&ctr->t_start, global_ns());  // block start stamps
@@ -343,7 +372,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
         w.steps = 0;
         w.acc = 0.0;
         w.has = true;
-        if (kMinPath) w.tb[7] = w.cur;  // trace entry 0
+        if (kMinPath) ring[0] = w.cur;  // trace entry 0
       }
       chunk_pos += take;
       need = __ballot_sync(kFull, !w.has);
@@ -359,7 +388,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       uint32_t* tr = S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T);
 #pragma unroll
       for (int j = 1; j < 8; ++j)
-        if (static_cast<uint32_t>(j) <= r) tr[w.steps + 1 - j] = w.tb[8 - j];
+        if (static_cast<uint32_t>(j) <= r) tr[w.steps + 1 - j] = ring[32 * (r - j)];
       S.acc[w.widx] = w.acc;
       S.term[w.widx] = term;
       S.steps[w.widx] = w.steps;
@@ -387,14 +416,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     if (kMinPath) {
       // Trace entry `steps`; every 8th entry completes a 32 B sector,
       // written whole.
-#pragma unroll
-      for (int j = 0; j < 7; ++j) w.tb[j] = w.tb[j + 1];
-      w.tb[7] = next;
+      ring[32 * (w.steps & 7u)] = next;
       if ((w.steps & 7u) == 7u) {
         uint4* dst = reinterpret_cast<uint4*>(
             S.paths + static_cast<uint64_t>(w.widx) * trace_stride(P.T) + (w.steps - 7));
-        dst[0] = make_uint4(w.tb[0], w.tb[1], w.tb[2], w.tb[3]);
-        dst[1] = make_uint4(w.tb[4], w.tb[5], w.tb[6], w.tb[7]);
+        dst[0] = make_uint4(ring[0], ring[32], ring[64], ring[96]);
+        dst[1] = make_uint4(ring[128], ring[160], ring[192], ring[224]);
       }
     }
     if (__dmul_rn(w.wpq, w.acc) > P.K) return kBudget;
@@ -678,7 +705,7 @@ void launch_walk(const DevGraph<C>& g, const ReachQuery* rq, const MinQuery* mq,
   constexpr int kMinBlocks = kMinPath ? 2 : 4;
   auto k = P.count ? k_walk<C, kMinPath, kWarps, kMinBlocks, true>
                    : k_walk<C, kMinPath, kWarps, kMinBlocks, false>;
-  constexpr size_t smem = WalkLayout<C, kWarps>::kBytes;
+  constexpr size_t smem = WalkLayout<C, kWarps, kMinPath>::kBytes;
   smem_opt_in(k, smem);
   k<<<persistent_blocks(k, threads, kWarps * 32, smem), kWarps * 32, smem, st>>>(
       g, rq, mq, nq_dev, P, ro, S, ctr, work);
