@@ -981,9 +981,11 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 // predecessor: progress is guaranteed, and the result equals the event-order commit bit for bit
 // (disjoint events commute). No grid barrier per round: the critical path is
 // the longest chain of row-sharing events, not rounds x barriers.
-// Phases: emit records + per-row lists | ranks | apply (spin on done) |
-// reset the per-row heads and counters. A record-buffer overflow skips the
-// apply phase and leaves the batch to the round engine (flow_done = 0).
+// Phases: emit records + per-row lists | apply (each warp first ranks its
+// own events' records, then spins on done) | reset the per-row heads and
+// counters; the last block to finish the reset runs the batch epilogue (no
+// closing grid barrier). A record-buffer overflow skips the apply phase and
+// leaves the batch to the round engine (flow_done = 0).
 #ifndef DYG_FLOW_MINB
 #define DYG_FLOW_MINB 4
 #endif
@@ -1024,8 +1026,9 @@ __global__ void __launch_bounds__(256, DYG_FLOW_MINB) k_del_flow(CommitOp op, ui
   // deletion batch, each several dependent row round trips) then spread ~1
   // per warp instead of clumping Poisson-wise. The accounting-only events
   // are counted in the reset phase. Ranks come from a bitmap and its word
-  // prefix (one block scans it), so batches up to 32 x kMaxWords events.
-  constexpr uint32_t kMaxWords = 4096;
+  // prefix (every block scans it into shared memory), so batches up to 32 x
+  // kMaxWords events; larger ones keep the static deal.
+  constexpr uint32_t kMaxWords = 1024;
   const uint32_t nwords = (lim + 31) / 32;
   const bool balanced = op.o.flow_balance && nwords <= kMaxWords;
   if (tid == 0) ctl->fl_t[0] = global_ns();
@@ -1058,11 +1061,13 @@ __global__ void __launch_bounds__(256, DYG_FLOW_MINB) k_del_flow(CommitOp op, ui
       if (fb) {
         mark[e.u] = 1;
         mark[e.v] = 1;
+        ctl->fl_any_fb = 1;
       }
     }
   }
   grid.sync();
-  if (!op.o.freeze) {
+  // No fallback-capable event: no vertex is marked, nothing can be promoted.
+  if (!op.o.freeze && ctl->fl_any_fb) {
     // Three rotating flags: flag (it + 1) % 3 was last read before the
     // barrier that ended iteration it - 1, so resetting it here is safe.
     for (uint32_t it = 0;; ++it) {
@@ -1134,44 +1139,48 @@ __global__ void __launch_bounds__(256, DYG_FLOW_MINB) k_del_flow(CommitOp op, ui
     }
   }
   grid.sync();
-  if (tid == 0) ctl->fl_t[2] = global_ns();
+  if (tid == 0) ctl->fl_t[2] = ctl->fl_t[3] = global_ns();  // (ranks are part of the apply phase)
   const bool overflow = ctl->fl_overflow != 0;
   Acc acc{};
+  __shared__ uint32_t s_wpre[kMaxWords + 1];  // exclusive popcount prefix of fl_heavy's words
   if (!overflow) {
-    // Phase 2: ranks.
-    const uint32_t total = ctl->fl_top;
-    for (uint32_t p = tid; p < total; p += nth) {
-      const uint32_t x = b.fl_row[p], k = b.fl_ev[p];
-      uint32_t r = 0;
-      for (uint32_t q = head[x]; q != kNoSlot; q = b.fl_next[q]) r += b.fl_ev[q] < k;
-      b.fl_rank[p] = r;
-    }
-    if (balanced && blockIdx.x == 0) {  // exclusive popcount prefix of the heavy bitmap
-      __shared__ uint32_t s_scan[256];
+    if (balanced) {  // every block: the word prefix of the heavy bitmap
+      __shared__ uint32_t s_part[256];
       const uint32_t per = (nwords + blockDim.x - 1) / blockDim.x;
       const uint32_t w0 = threadIdx.x * per;
       uint32_t local = 0;
       for (uint32_t w = w0; w < w0 + per && w < nwords; ++w) local += __popc(b.fl_heavy[w]);
-      s_scan[threadIdx.x] = local;
+      s_part[threadIdx.x] = local;
       __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (uint32_t t = 0; t < blockDim.x; ++t) {
-          const uint32_t c = s_scan[t];
-          s_scan[t] = run;
-          run += c;
+      if (threadIdx.x < 32) {  // exclusive scan of the 256 partials, one warp
+        uint32_t v[8], run = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[i] = s_part[threadIdx.x * 8 + i];
+          run += v[i];
         }
-        b.fl_wpre[nwords] = run;
+        uint32_t inc = run;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t t = __shfl_up_sync(kAll, inc, off);
+          if (lane >= static_cast<uint32_t>(off)) inc += t;
+        }
+        uint32_t ex = inc - run;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          s_part[threadIdx.x * 8 + i] = ex;
+          ex += v[i];
+        }
+        if (threadIdx.x == 31) s_wpre[nwords] = inc;
       }
       __syncthreads();
-      uint32_t run = s_scan[threadIdx.x];
+      uint32_t run = s_part[threadIdx.x];
       for (uint32_t w = w0; w < w0 + per && w < nwords; ++w) {
-        b.fl_wpre[w] = run;
+        s_wpre[w] = run;
         run += __popc(b.fl_heavy[w]);
       }
+      __syncthreads();
     }
-    grid.sync();
-    if (tid == 0) ctl->fl_t[3] = global_ns();
     // Phase 3: apply in dataflow order.
     // Each warp owns events k = wid + j*nw (j = 0, 1, ...) and keeps a
     // window of its 8 lowest unapplied ones, applying whichever is ready
@@ -1179,24 +1188,26 @@ __global__ void __launch_bounds__(256, DYG_FLOW_MINB) k_del_flow(CommitOp op, ui
     // does not hold up the warp's independent later events. The lowest
     // unapplied event overall is always inside its owner's window and ready:
     // no deadlock, and no shared work counter to contend on.
-    const uint32_t nown = balanced ? b.fl_wpre[nwords] : lim;
+    const uint32_t nown = balanced ? s_wpre[nwords] : lim;
     const uint32_t count = wid < nown ? (nown - wid + nw - 1) / nw : 0;
     // The warp's j-th event: rank wid + j * nw among the heavy events
     // (binary search of the word prefix, then the bit within the word).
     auto ev_of = [&](uint32_t j) -> uint32_t {
       const uint32_t h = wid + j * nw;
       if (!balanced) return h;
-      uint32_t lo = 0, hi = nwords;  // fl_wpre[lo] <= h < fl_wpre[hi]
+      uint32_t lo = 0, hi = nwords;  // s_wpre[lo] <= h < s_wpre[hi]
       while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (b.fl_wpre[mid] <= h) lo = mid;
+        if (s_wpre[mid] <= h) lo = mid;
         else hi = mid;
       }
-      return lo * 32 + __fns(b.fl_heavy[lo], 0, static_cast<int>(h - b.fl_wpre[lo]) + 1);
+      return lo * 32 + __fns(b.fl_heavy[lo], 0, static_cast<int>(h - s_wpre[lo]) + 1);
     };
-    // Pull every row this warp's events will touch (G and H slabs) toward L2
-    // now, so the dependent lookups inside apply_warp hit L2 instead of each
-    // paying a DRAM round trip in sequence.
+    // Rank this warp's own events' records (rank = records of earlier events
+    // on the row; only the owner's lanes read them), and pull every row the
+    // events will touch (G and H slabs) toward L2 now, so the dependent
+    // lookups inside apply_warp hit L2 instead of each paying a DRAM round
+    // trip in sequence.
     for (uint32_t j = 0; j < count; ++j) {
       const uint32_t k = ev_of(j);
       const uint32_t base = b.fl_base[k], n = b.fl_cnt[k];
@@ -1204,6 +1215,9 @@ __global__ void __launch_bounds__(256, DYG_FLOW_MINB) k_del_flow(CommitOp op, ui
         const uint32_t x = b.fl_row[base + t];
         asm volatile("prefetch.global.L2 [%0];" ::"l"(op.G.slab + x));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(op.H.slab + x));
+        uint32_t r = 0;
+        for (uint32_t q = head[x]; q != kNoSlot; q = b.fl_next[q]) r += b.fl_ev[q] < k;
+        b.fl_rank[base + t] = r;
       }
     }
     constexpr uint32_t kWin = 8;
@@ -1300,21 +1314,32 @@ __global__ void __launch_bounds__(256, DYG_FLOW_MINB) k_del_flow(CommitOp op, ui
     for (uint32_t w = tid; w < nwords; w += nth) b.fl_heavy[w] = 0;
   if (!overflow) op.flush(acc);
   clear_shadow_lists();
-  grid.sync();
-  if (tid == 0) ctl->fl_t[5] = global_ns();
   if (overflow) {  // record buffer too small: the dependency rounds commit the batch
+    grid.sync();
+    if (tid == 0) ctl->fl_t[5] = global_ns();
     if (keep) {  // they re-apply the deletions: batch-start G first
       restore_rows(op.G, b, tid, nth);
       grid.sync();
     }
     rounds_warp_loop(op, nev, b, grid);
     grid.sync();
+    if (tid == 0) batch_finish(op.G, op.H, b);
+    return;
   }
-  if (tid == 0) {
-    if (!overflow) {
-      ctl->flow_done = 1;
-      ctl->rounds = ctl->rounds + 1;
-    }
+  // The last block past this point runs the epilogue (its counters are the
+  // other blocks' flushed atomics: fence, count, fence).
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&b.ctl->fl_blocks_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    ctl->fl_t[5] = global_ns();
+    ctl->flow_done = 1;
+    ctl->rounds = ctl->rounds + 1;
     batch_finish(op.G, op.H, b);
   }
 }

@@ -78,6 +78,8 @@ struct BatchCtl {
   unsigned int flow_done;    // k_del_flow committed the batch
   unsigned int fl_changed[3];  // fallback-promotion fixpoint (rotating)
   unsigned int fl_depth;     // longest chain of row-sharing events
+  unsigned int fl_blocks_done;  // k_del_flow blocks past the reset (the last one runs the epilogue)
+  unsigned int fl_any_fb;       // some event may run the local fallback (else no promotion fixpoint)
   unsigned long long fl_t[6];  // %globaltimer at the phase boundaries
   unsigned long long counter_base;  // update_counter_ at batch start (:431)
   // %globaltimer stamps (ns) for the phase times in dyg_stats.
@@ -178,7 +180,6 @@ struct BatchDev {
   uint32_t* fl_cnt;
   uint8_t* fl_promo;   // per event: may run the local fallback
   uint32_t* fl_heavy;  // bitmap: events the apply phase must order (0 between batches)
-  uint32_t* fl_wpre;   // exclusive popcount prefix of fl_heavy's words
   uint32_t* fl_depth;  // per vertex, 0 between batches
   uint64_t fl_cap;
 };

@@ -274,7 +274,6 @@ void free_batch(dyg_session* s) {
   dev_free(b.fl_cnt);
   dev_free(b.fl_promo);
   dev_free(b.fl_heavy);
-  dev_free(b.fl_wpre);
   dev_free(b.tile_state);
   cudaFree(b.scan_temp);
   b.scan_temp = nullptr;
@@ -319,7 +318,6 @@ void ensure_batch(dyg_session* s, uint32_t nb, uint32_t nd) {
     dev_alloc(&b.fl_cnt, cap, "flow record ranges");
     dev_alloc(&b.fl_promo, cap, "flow fallback flags");
     dev_alloc(&b.fl_heavy, cap / 32 + 2, "flow heavy bitmap");
-    dev_alloc(&b.fl_wpre, cap / 32 + 3, "flow heavy prefix");
     check(cudaMemset(b.fl_heavy, 0, sizeof(uint32_t) * (cap / 32 + 2)), "flow heavy bitmap");
     b.q_cap = cap;
     dev_alloc(&b.tile_state, 3ull * (cap / 256 + 2), "scan tile states");
