@@ -105,7 +105,11 @@ class ShardedReplay:
 
         b = self._bufs.get(key)
         if b is None or b.numel() < nbytes:
-            b = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+            # Zeroed once: the buffers are sized by host-known upper bounds and
+            # the pack kernels write only the actual records, so the gather
+            # (and gloo's host staging) would otherwise read never-written
+            # bytes (compute-sanitizer initcheck).
+            b = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=self.device)
             self._bufs[key] = b
         return b[:nbytes]
 
