@@ -120,7 +120,7 @@ __device__ __forceinline__ void flush_acc(const Acc& a, BatchCtl* ctl, unsigned 
 // row's records in increasing r, i.e. event order. G's appends do not depend
 // on the walks (which read H alone), so k_fp_check + k_fp_write_g run on a
 // second stream CONCURRENTLY with the reach walk, filling the SMs its tail
-// leaves idle; k_fp_write_h appends the kept records to H after the walk and
+// leaves idle; the commit launch first appends the kept records to H (fp_write_h_pass) and
 // does the per-event accounting. Any violated precondition sets not_simple
 // BEFORE anything is written and the round engine (k_rounds) commits the
 // batch instead. The list heads are left empty for the next batch.
@@ -237,7 +237,7 @@ __global__ void k_fp_write_g(DevGraph<kCapG> G, const DevEvent* __restrict__ ev,
   if (r >= n) return;
   // An invalid batch or a violated precondition: only empty the lists.
   const bool write = !batch_aborted(b.ctl) && !b.ctl->not_simple;
-  // The H pass (k_fp_write_h, after the walk) reads the same lists and
+  // The H pass (fp_write_h_pass, after the walk) reads the same lists and
   // empties them.
   if (!fp_apply(G, ev, b.fp_head[0], b.fp_next[0], r, write, [](uint32_t) { return true; },
                 /*reset=*/false))
@@ -248,13 +248,17 @@ __global__ void k_fp_write_g(DevGraph<kCapG> G, const DevEvent* __restrict__ ev,
 // decision and report counters, one thread per EVENT: its keep decision is
 // read once for both records, and the two rows' list heads, slabs and appends
 // are independent requests in flight together.
-__global__ void k_fp_write_h(DevGraph<kCapH> H, const DevEvent* __restrict__ ev, uint32_t nb,
-                             WalkOpts o, BatchDev b) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+// The H pass over events k0, k0 + kstride, ... (every thread of the block
+// must call it: the block totals end with a barrier).
+__device__ void fp_write_h_pass(const DevGraph<kCapH>& H, const DevEvent* __restrict__ ev,
+                                uint32_t nb, const WalkOpts& o, const BatchDev& b, uint32_t k0,
+                                uint32_t kstride) {
   stamp_commit_start(b.ctl);
-  const bool write = k < nb && !batch_aborted(b.ctl) && !b.ctl->not_simple;
+  unsigned long long kept_acc = 0, pruned_acc = 0, steps_sum = 0, steps_max = 0;
+  for (uint32_t k = k0; k < nb; k += kstride) {
+  const bool write = !batch_aborted(b.ctl) && !b.ctl->not_simple;
   unsigned long long kept_n = 0, pruned_n = 0, steps = 0;
-  if (k < nb) {
+  {
     const DevEvent e = ev[k];
     uint32_t* head = b.fp_head[0];  // the lists k_fp_write_g walked
     const uint32_t* next = b.fp_next[0];
@@ -306,17 +310,22 @@ __global__ void k_fp_write_h(DevGraph<kCapH> H, const DevEvent* __restrict__ ev,
     }
     if (!ok) atomicMin(&b.ctl->commit_err, static_cast<unsigned long long>(kErrPool));
   }
+  kept_acc += kept_n;
+  pruned_acc += pruned_n;
+  steps_sum += steps;
+  steps_max = steps_max > steps ? steps_max : steps;
+  }
   // Block totals, then one atomic per field and block: per-warp atomics on
   // these five addresses serialise in L2 (~18k per C5 batch).
   __shared__ unsigned long long s_red[4][8];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  kept_n = warp_sum(kept_n);
-  pruned_n = warp_sum(pruned_n);
-  const unsigned long long steps_sum = warp_sum(steps);
-  const unsigned long long steps_max = warp_max(steps);
+  kept_acc = warp_sum(kept_acc);
+  pruned_acc = warp_sum(pruned_acc);
+  steps_sum = warp_sum(steps_sum);
+  steps_max = warp_max(steps_max);
   if (lane == 0) {
-    s_red[0][wid] = kept_n;
-    s_red[1][wid] = pruned_n;
+    s_red[0][wid] = kept_acc;
+    s_red[1][wid] = pruned_acc;
     s_red[2][wid] = steps_sum;
     s_red[3][wid] = steps_max;
   }
@@ -349,7 +358,32 @@ __global__ void __launch_bounds__(256) k_rounds(Op op, uint32_t nev, BatchDev b)
   const uint32_t tid = static_cast<uint32_t>(grid.thread_rank());
   const uint32_t nth = static_cast<uint32_t>(grid.size());
   volatile BatchCtl* ctl = b.ctl;
-  if constexpr (Op::kCommit) stamp_commit_start(b.ctl);
+  if constexpr (Op::kCommit) {
+    stamp_commit_start(b.ctl);
+    if (op.fp_h) {
+      // The insertion fast path's H appends (fp_write_h_pass) inside this
+      // launch instead of a kernel of their own. When they commit the batch
+      // (the uniform condition below), the last block past them runs the
+      // epilogue -- no grid barrier; otherwise the rounds follow a barrier.
+      fp_write_h_pass(op.H, op.ev, nev, op.o, b, tid, nth);
+      if (ctl->val_err == ~0ull && ctl->fast && !ctl->not_simple) {
+        __shared__ bool s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          s_last = atomicAdd(&b.ctl->fl_blocks_done, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last && threadIdx.x == 0) {
+          __threadfence();
+          ctl->fl_t[0] = global_ns();  // (timeline only)
+          batch_finish(op.G, op.H, b);
+        }
+        return;
+      }
+      grid.sync();
+    }
+  }
   if (ctl->val_err != ~0ull) {  // uniform: nothing below ran yet
     if constexpr (Op::kCommit) {
       if (tid == 0) batch_finish(op.G, op.H, b);
@@ -566,6 +600,7 @@ struct CommitOp {
   // event k (the batch-start row minus the row's deletions up to k) comes
   // from the saved batch-start rows and the shadow's per-row deletion lists.
   int keep = 0;
+  int fp_h = 0;  // insertion fast path: the H pass runs at the start of the commit launch
   int promo_pre = 0;  // k_prep<del> stored "edge in batch-start H" in fl_promo bit 1
   const uint32_t* save_idx = nullptr;     // vertex -> saved batch-start row
   const Slab<kCapG>* side_slab = nullptr;
@@ -2286,8 +2321,9 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
 }
 
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st) {
+                  uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st, bool fp_h) {
   CommitOp op{G, H, b.events, b.slot, b.rout, b.mout, b.mscratch, b.dec, b.ctl, o};
+  op.fp_h = fp_h && n_del == 0 ? 1 : 0;
   if (n_del == 0) return launch_rounds<false>(op, nb, b, st);
   if (n_del == nb && o.flow) {
     CommitOp op_copy = op;
@@ -2333,13 +2369,6 @@ int launch_fastpath_g(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, 
   k_fp_check<<<grid_for(n), 256, 0, st>>>(b.events, n, b);
   k_fp_write_g<<<grid_for(n), 256, 0, st>>>(G, b.events, n, b);
   return 2;
-}
-
-int launch_fastpath_h(const DevGraph<kCapH>& H, const BatchDev& b, uint32_t nb, const WalkOpts& o,
-                      cudaStream_t st) {
-  if (nb == 0) return 0;
-  k_fp_write_h<<<grid_for(nb), 256, 0, st>>>(H, b.events, nb, o, b);
-  return 1;
 }
 
 int launch_shard_range(const BatchDev& b, int rank, int world, uint32_t* rng, uint32_t max_r,

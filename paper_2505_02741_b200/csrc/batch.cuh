@@ -218,13 +218,14 @@ int launch_queries(const DevGraph<kCapH>& H, DevGraph<kCapG> G, const BatchDev& 
 // the per-event accounting after it; k_rounds only commits if a
 // precondition failed on the device.
 int launch_fastpath_g(const DevGraph<kCapG>& G, const BatchDev& b, uint32_t nb, cudaStream_t st);
-int launch_fastpath_h(const DevGraph<kCapH>& H, const BatchDev& b, uint32_t nb, const WalkOpts& o,
-                      cudaStream_t st);
 // The whole commit in one cooperative launch, epilogue included: insertion
 // batches k_rounds (fast-path appends, or rounds), deletion-only batches
 // k_del_flow (shadow undo + dataflow commit), mixed batches k_rounds_warp.
+// fp_h: an insertion-only fast-path batch -- the launch starts with the H
+// appends (fp_write_h_pass), then the epilogue from its last block.
 int launch_commit(const DevGraph<kCapG>& G, const DevGraph<kCapH>& H, const BatchDev& b,
-                  uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st);
+                  uint32_t nb, uint32_t n_del, const WalkOpts& o, cudaStream_t st,
+                  bool fp_h = false);
 size_t scan_temp_bytes(uint32_t nb_cap);
 
 // Multi-GPU exchange records. Reach: 16 B per query.

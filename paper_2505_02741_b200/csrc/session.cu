@@ -637,11 +637,10 @@ void commit_enqueue(dyg_session* s, Pending& p, bool download = true) {
   const WalkOpts o = walk_opts(s);
   BatchDev& b = s->b;
   b.ctl = p.dctl;
-  if (p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass) {
-    if (!p.g_appended) p.launches += launch_fastpath_g(s->G.view(), b, p.nb, s->stream);
-    p.launches += launch_fastpath_h(s->H.view(), b, p.nb, o, s->stream);
-  }
-  p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream);
+  const bool fp = p.n_del == 0 && p.n_ins > 0 && o.fastpath && o.single_pass;
+  if (fp && !p.g_appended) p.launches += launch_fastpath_g(s->G.view(), b, p.nb, s->stream);
+  // The H appends open the commit launch (fp_h).
+  p.launches += launch_commit(s->G.view(), s->H.view(), b, p.nb, p.n_del, o, s->stream, fp);
   maybe_sync(s, "commit");
   if (download)
     check(cudaMemcpyAsync(p.hctl, b.ctl, sizeof(BatchCtl), cudaMemcpyDeviceToHost, s->stream),

@@ -3,7 +3,7 @@
 # late in the warm-up replay). Usage: gpurun -- bash tools/ncu_commit.sh TAG
 TAG=${1:-x}
 mkdir -p gpurun_out
-for k in "k_prep<0>:k_prep:6" "k_fp_write_h:k_fp_write_h:6" "k_del_flow:k_del_flow:6" "k_prep<1>:k_prep:16"; do
+for k in "k_prep<0>:k_prep:6" "k_del_flow:k_del_flow:6" "k_prep<1>:k_prep:16"; do
   IFS=: read name rx skip <<< "$k"
   tag=$(echo $name | tr -d '<>')
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$rx -s $skip -c 1 \
