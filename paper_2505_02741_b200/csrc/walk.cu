@@ -37,16 +37,10 @@ inline unsigned blocks_for(uint64_t threads, unsigned per_block) {
 // The slabs are staged in shared memory (row stride padded to 9 / 5 x 16 B,
 // conflict-free) and each lane reads its own back. Lanes pass kNoVertex when
 // they need no row this iteration.
-#ifndef DYG_H_GATHER_CHUNKS
-#define DYG_H_GATHER_CHUNKS 4
-#endif
-#ifndef DYG_POOL_UNCOND
-#define DYG_POOL_UNCOND 1
-#endif
 template <int C>
 struct Gather {
-  static constexpr int kChunks = C == kCapH ? DYG_H_GATHER_CHUNKS : 8;  // 16 B chunks fetched
-  static constexpr int kLanesPerRow = kChunks <= 4 ? 4 : 8;
+  static constexpr int kChunks = C == kCapH ? 4 : 8;  // 16 B chunks fetched
+  static constexpr int kLanesPerRow = kChunks;
   static constexpr int kRowsPerRound = 32 / kLanesPerRow;
   static constexpr int kRounds = 32 / kRowsPerRound;
   static constexpr int kStride = kChunks + 1;          // uint4 per staged row
@@ -133,7 +127,6 @@ __device__ __forceinline__ bool sample_pool(const uint32_t* __restrict__ ids,
                                             uint32_t prev, double u01, uint32_t& next,
                                             double& ew) {
   double total = 0.0;
-#if DYG_POOL_UNCOND
   // Both loads of an entry issue together (the weight is not predicated on
   // the id), so an unrolled group costs one round trip, not two.
 #pragma unroll 8
@@ -142,10 +135,6 @@ __device__ __forceinline__ bool sample_pool(const uint32_t* __restrict__ ids,
     const double w = __ldg(ws + i);
     if (id != prev) total = __dadd_rn(total, w);
   }
-#else
-  for (uint32_t i = 0; i < deg; ++i)
-    if (__ldg(ids + i) != prev) total = __dadd_rn(total, __ldg(ws + i));
-#endif
   if (total <= 0.0) return false;
   const double target = __dmul_rn(u01, total);
   double cum = 0.0;
@@ -288,12 +277,10 @@ __device__ __forceinline__ void issue_rows(const DevGraph<C>& g, uint32_t my_row
       const uint32_t u = __shfl_sync(kFull, my_row, r);
       const bool live = u != kNoVertex;
       const uint4* src = reinterpret_cast<const uint4*>(g.slab + (live ? u : 0)) + chunk;
-      if (Gt::kChunks == Gt::kLanesPerRow || chunk < static_cast<uint32_t>(Gt::kChunks)) {
-        if (C == kCapG)
-          cp_async16_cg(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
-        else
-          cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
-      }
+      if (C == kCapG)
+        cp_async16_cg(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
+      else
+        cp_async16(stage + r * Gt::kStride + chunk, src, live ? 16u : 0u);
     }
   }
   cp_async_commit();
